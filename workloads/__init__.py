@@ -1,0 +1,186 @@
+"""Seeded synthetic inputs for the compressed-convolution hot path (W ~ L + S).
+
+This module is shared by the oracle tests, the GPU parity tests and bench.py.
+It holds NO arithmetic of the method: it only draws random numbers, rounds
+them to the storage precision, and builds the CSR index arrays of the sparse
+term from sampled positions.  The method itself (how Y is computed from these
+arrays) lives in `oracle/` (fp64 CPU reference) and in
+`paper_2006_06443_b200/csrc/` (the CUDA path); neither is imported here.
+
+Recipe (SURVEY.md §8(c) readings #7-#11):
+  * one numpy Generator(PCG64(seed)); draw order X, U_in, G, U_out,
+    S positions, S values;
+  * X = ReLU(N(0,1)), NHWC [N, H, W, Cin]                  (BASELINE.json configs)
+  * U_in [Cin, R1] ~ N(0, 1/Cin), G [R1, R2, k, k] ~ N(0, 1/(R1 k^2)),
+    U_out [R2, Cout] ~ N(0, 1/R2)   -- "N(0, v)" read as variance v;
+    SVD pair: U [Cin, R] ~ N(0, 1/Cin), V [R, Cout] ~ N(0, 1/R), core = None;
+  * S: nnz = round(d * Cout*Cin*k*k) positions drawn uniformly without
+    replacement over the OIHW linear index, sorted; values N(0, 0.1)
+    (variance 0.1); CSR by output channel with col = (c*k + y)*k + x;
+  * fp64 draws -> fp32 (RNE); bf16 configs additionally round X and the
+    factors to bf16 (RNE).  S values stay fp32 for both dtypes.
+
+The arrays returned are exactly what both sides consume: the GPU gets the
+fp32/bf16 bits, the oracle gets the same values widened to fp64.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "LayerConfig", "LayerInputs", "CONFIGS", "generate", "bf16_round",
+    "bf16_bits", "resnet50_table2", "RESNET50_COMPRESSED_3X3",
+]
+
+
+@dataclasses.dataclass(frozen=True)
+class LayerConfig:
+    """One compressed conv layer workload (BASELINE.json `configs`)."""
+    name: str
+    batch: int
+    in_h: int
+    in_w: int
+    c_in: int
+    c_out: int
+    k: int
+    stride: int
+    pad: int
+    rank_in: int          # R1 (Tucker-2) or R (SVD pair)
+    rank_out: int         # R2 (Tucker-2) or R (SVD pair)
+    density: float
+    dtype: str            # "f32" | "bf16"
+    svd: bool = False     # 1x1 layer evaluated as an SVD pair (no core)
+    seed: int = 0
+
+    @property
+    def out_h(self) -> int:
+        return (self.in_h + 2 * self.pad - self.k) // self.stride + 1
+
+    @property
+    def out_w(self) -> int:
+        return (self.in_w + 2 * self.pad - self.k) // self.stride + 1
+
+    @property
+    def numel_w(self) -> int:
+        return self.c_out * self.c_in * self.k * self.k
+
+    @property
+    def nnz(self) -> int:
+        # round half to even never triggers for the shipped configs
+        return int(round(self.density * self.numel_w))
+
+    def replace(self, **kw) -> "LayerConfig":
+        return dataclasses.replace(self, **kw)
+
+
+# BASELINE.json configs[0..3] (C1..C4); C2 is listed in both dtypes.
+CONFIGS = {
+    "c1": LayerConfig("c1", 1, 56, 56, 64, 64, 3, 1, 1, 16, 16, 0.01, "f32"),
+    "c2_f32": LayerConfig("c2_f32", 64, 14, 14, 256, 256, 3, 1, 1, 64, 64, 0.02, "f32"),
+    "c2_bf16": LayerConfig("c2_bf16", 64, 14, 14, 256, 256, 3, 1, 1, 64, 64, 0.02, "bf16"),
+    "c3": LayerConfig("c3", 256, 7, 7, 512, 512, 3, 1, 1, 128, 128, 0.05, "bf16"),
+    "c4": LayerConfig("c4", 128, 14, 14, 256, 1024, 1, 1, 0, 64, 64, 0.01, "bf16", svd=True),
+}
+
+
+@dataclasses.dataclass
+class LayerInputs:
+    cfg: LayerConfig
+    x: np.ndarray                 # [N,H,W,Cin] float32 (bf16-representable for bf16)
+    u_in: np.ndarray              # [Cin,R1] float32
+    core: Optional[np.ndarray]    # [R1,R2,k,k] float32 or None (SVD)
+    u_out: np.ndarray             # [R2,Cout] float32
+    row_ptr: np.ndarray           # [Cout+1] int64
+    col_idx: np.ndarray           # [nnz] int32, col = (c*k + y)*k + x
+    values: np.ndarray            # [nnz] float32
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """Round float32 -> bf16 (round-to-nearest-even), returned as float32."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    rounding_bias = ((u >> 16) & 1) + 0x7FFF
+    r = ((u + rounding_bias) >> 16) << 16
+    r = r.astype(np.uint32)
+    nan = np.isnan(a)
+    if nan.any():
+        r[nan] = 0x7FC00000
+    return r.view(np.float32)
+
+
+def bf16_bits(a: np.ndarray) -> np.ndarray:
+    """uint16 bit pattern of bf16-representable float32 values (no rounding)."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return (a.view(np.uint32) >> 16).astype(np.uint16)
+
+
+def _store(a: np.ndarray, dtype: str) -> np.ndarray:
+    a = a.astype(np.float32)
+    return bf16_round(a) if dtype == "bf16" else a
+
+
+def generate(cfg: LayerConfig, batch: Optional[int] = None, seed: Optional[int] = None,
+             empty_rows_skew: bool = False) -> LayerInputs:
+    """Draw the inputs of one layer (draw order fixed, see module doc)."""
+    n = cfg.batch if batch is None else batch
+    rng = np.random.Generator(np.random.PCG64(cfg.seed if seed is None else seed))
+    k = cfg.k
+    x = np.maximum(rng.standard_normal((n, cfg.in_h, cfg.in_w, cfg.c_in)), 0.0)
+    if cfg.svd:
+        u_in = rng.standard_normal((cfg.c_in, cfg.rank_in)) / np.sqrt(cfg.c_in)
+        core = None
+        u_out = rng.standard_normal((cfg.rank_in, cfg.c_out)) / np.sqrt(cfg.rank_in)
+    else:
+        u_in = rng.standard_normal((cfg.c_in, cfg.rank_in)) / np.sqrt(cfg.c_in)
+        core = rng.standard_normal((cfg.rank_in, cfg.rank_out, k, k)) / np.sqrt(cfg.rank_in * k * k)
+        u_out = rng.standard_normal((cfg.rank_out, cfg.c_out)) / np.sqrt(cfg.rank_out)
+    numel = cfg.numel_w
+    nnz = cfg.nnz
+    pos = np.sort(rng.choice(numel, size=nnz, replace=False)) if nnz > 0 else np.zeros(0, np.int64)
+    vals = rng.standard_normal(nnz) * np.sqrt(0.1)
+    row_len = cfg.c_in * k * k
+    rows = pos // row_len
+    cols = pos % row_len
+    row_ptr = np.zeros(cfg.c_out + 1, dtype=np.int64)
+    np.add.at(row_ptr, rows + 1, 1)
+    row_ptr = np.cumsum(row_ptr)
+    return LayerInputs(
+        cfg=cfg,
+        x=_store(x, cfg.dtype),
+        u_in=_store(u_in, cfg.dtype),
+        core=None if core is None else _store(core, cfg.dtype),
+        u_out=_store(u_out, cfg.dtype),
+        row_ptr=row_ptr,
+        col_idx=cols.astype(np.int32),
+        values=vals.astype(np.float32),
+    )
+
+
+def resnet50_table2(path: Optional[str] = None):
+    """Rows of PAPER.md Table 2 (`table:lshapes`) from the
+    committed golden fixture: (index, c_in, in_h, in_w, c_out, k)."""
+    import os
+    if path is None:
+        path = os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "resnet50_table2.csv")
+    rows = []
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#") or line.startswith("index"):
+                continue
+            idx, cin, h, w, cout, cin2, kx, ky = (int(t) for t in line.split(","))
+            assert cin == cin2 and kx == ky
+            rows.append((idx, cin, h, w, cout, kx))
+    return rows
+
+
+# Table-2 indices of the 16 ResNet-50 3x3 convs and their strides (torchvision
+# v1.5 puts the stride on conv2 of the first block of layers 2-4; Table 2's
+# input/output spatial sizes agree: layer 12 56->28, 25 28->14, 44 14->7).
+RESNET50_COMPRESSED_3X3 = {
+    2: 1, 6: 1, 9: 1, 12: 2, 16: 1, 19: 1, 22: 1, 25: 2,
+    29: 1, 32: 1, 35: 1, 38: 1, 41: 1, 44: 2, 48: 1, 51: 1,
+}
