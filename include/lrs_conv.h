@@ -1,0 +1,145 @@
+/*
+ * lrs_conv.h -- C-ABI of the B200 (sm_100a) compressed convolution whose
+ * weight is approximated as W ~ L + S (arXiv 2006.06443, the thesis in
+ * /root/reference/PAPER.md; BASELINE.json north star).
+ *
+ *   Y = conv(X, L) + conv(X, S)
+ *
+ *   L  Tucker-2 chain  T1 = X U_in          (1x1 projection,   PAPER.md:162)
+ *                      T2 = conv(T1, G)     (k x k core,       PAPER.md:165-166, :409)
+ *                      Y_L = T2 U_out       (1x1 expansion,    PAPER.md:168)
+ *      or, for a 1x1 layer, an SVD pair  Y_L = (X U) V          (core == NULL)
+ *   S  direct sparse convolution, CSR by output channel        PAPER.md:171-191 §3.4
+ *   Y  = Y_L + Y_S, written to device memory once.
+ *
+ * Conventions (readings #2, #3, #6):
+ *   - activations are NHWC (the paper's X_{smt}, batched);
+ *   - cross-correlation, zero padding; out_h = (in_h + 2 pad_h - kernel_h)/stride_h + 1;
+ *   - core is indexed [rank_in][rank_out][kernel_h][kernel_w] (the paper's
+ *     (in, out, kx, ky) order), u_in [c_in][rank_in], u_out [rank_out][c_out];
+ *   - CSR row j = output channel j; col = (c * kernel_h + ky) * kernel_w + kx,
+ *     strictly increasing within a row (the OIHW flattening).
+ * No bias: the paper's layer has none.
+ *
+ * No function aborts or prints.  Every function returns an lrs_status;
+ * lrs_conv_last_error() gives the text of the last non-OK status of the
+ * calling thread.  There is no CPU fallback: a missing GPU is LRS_ERR_CUDA.
+ */
+#ifndef LRS_CONV_H_
+#define LRS_CONV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LRS_OK = 0,
+  LRS_ERR_INVALID_ARGUMENT = 1, /* malformed descriptor / pointer / size            */
+  LRS_ERR_UNSUPPORTED = 2,      /* legal but not implemented (see lrs_conv_create) */
+  LRS_ERR_OUT_OF_MEMORY = 3,    /* device or host allocation failed                */
+  LRS_ERR_CUDA = 4              /* CUDA runtime / driver error (launch, no device) */
+} lrs_status;
+
+typedef enum {
+  LRS_DTYPE_F32 = 0,  /* X, Y, factors fp32; chain on tensor cores as 3xTF32 split */
+  LRS_DTYPE_BF16 = 1  /* X, Y, factors bf16; fp32 accumulation everywhere          */
+} lrs_dtype;
+
+typedef struct lrs_conv lrs_conv; /* opaque; immutable after create */
+
+typedef struct lrs_conv_desc {
+  int32_t batch_max;              /* largest n accepted by forward (> 0)            */
+  int32_t in_h, in_w, c_in, c_out;
+  int32_t kernel_h, kernel_w;     /* 1..7                                           */
+  int32_t stride_h, stride_w;     /* >= 1                                           */
+  int32_t pad_h, pad_w;           /* >= 0                                           */
+  int32_t rank_in, rank_out;      /* Tucker-2 (R1, R2); SVD pair: rank_in == rank_out */
+  lrs_dtype dtype;                /* element type of X, Y, u_in, core, u_out        */
+  const void *u_in;               /* host [c_in][rank_in], row-major, dtype         */
+  const void *core;               /* host [rank_in][rank_out][kernel_h][kernel_w]   */
+                                  /* or NULL: SVD pair (requires 1x1, stride 1, pad 0) */
+  const void *u_out;              /* host [rank_out][c_out], row-major, dtype       */
+  int64_t nnz;                    /* >= 0                                           */
+  const int64_t *row_ptr;         /* host [c_out + 1]; 0, non-decreasing, nnz at end */
+  const int32_t *col_idx;         /* host [nnz]; < c_in*kernel_h*kernel_w            */
+  const float *values;            /* host [nnz]; fp32 for both dtypes               */
+} lrs_conv_desc;
+
+/*
+ * Create a layer on CUDA device `device`.  All desc arrays are host memory,
+ * deep-copied and repacked (rank padding, K-major weight tiles, per-tile
+ * sparse code streams); the caller may free them on return.  The handle
+ * owns its device buffers (weights + scratch sized for batch_max).
+ * INVALID_ARGUMENT: any extent <= 0, stride < 1, pad < 0, output extent < 1,
+ *   malformed CSR (row_ptr not monotone / wrong ends, col out of range,
+ *   unsorted or duplicate columns), core == NULL with a non-1x1 / strided /
+ *   padded kernel or rank_in != rank_out, NULL required pointer.
+ * UNSUPPORTED: kernel > 7, rank > 256, c_in or c_out not a multiple of 8
+ *   (bf16) / 4 (fp32) (16-byte TMA rows), output width > 128.
+ * OUT_OF_MEMORY / CUDA: allocation or driver failure (no handle is returned).
+ */
+lrs_status lrs_conv_create(const lrs_conv_desc *desc, int device, lrs_conv **out);
+
+/*
+ * Y = conv(X, L + S) for n images, enqueued on `stream` (a cudaStream_t;
+ * NULL = legacy default stream).  x: device [n][in_h][in_w][c_in], y: device
+ * [n][out_h][out_w][c_out], both dtype, contiguous, 16-byte aligned, on the
+ * handle's device, not aliased.  y is overwritten.  No host sync and no
+ * allocation: the call is CUDA-graph capturable.  The handle's scratch is
+ * shared by all calls, so at most one forward may be in flight per handle.
+ * n == 0 is a no-op.  INVALID_ARGUMENT: n < 0, n > batch_max, NULL or
+ * misaligned pointer.  CUDA: launch failure (asynchronous faults surface at
+ * the caller's next synchronisation).
+ */
+lrs_status lrs_conv_forward(const lrs_conv *h, const void *x, void *y, int32_t n, void *stream);
+
+/*
+ * End-to-end variant with HOST buffers: copies x_host -> device, runs
+ * lrs_conv_forward, copies the result -> y_host, all enqueued on `stream`
+ * (pinned host memory makes the copies asynchronous).  The device staging
+ * buffers are allocated by the first call (so this call is not graph
+ * capturable) and owned by the handle.  The caller synchronises `stream`
+ * before reading y_host.
+ */
+lrs_status lrs_conv_forward_host(lrs_conv *h, const void *x_host, void *y_host, int32_t n,
+                                 void *stream);
+
+/* NULL-safe.  Requires that no forward is in flight on the handle. */
+lrs_status lrs_conv_destroy(lrs_conv *h);
+
+/* Thread-local text of the last non-OK status ("" if none). Never NULL. */
+const char *lrs_conv_last_error(void);
+
+/* Output spatial extent of the layer. */
+lrs_status lrs_conv_output_shape(const lrs_conv *h, int32_t *out_h, int32_t *out_w);
+
+/* Number of kernels one lrs_conv_forward launches (n > 0). */
+int32_t lrs_conv_launches_per_forward(const lrs_conv *h);
+
+/*
+ * Stage timing for measurement (bench.py roofline): when enabled, forward
+ * records a CUDA event pair around every kernel it launches on the caller's
+ * stream.  lrs_conv_stage_times sums, over all forwards since the last
+ * reset, each stage's event-timed duration (ms) into ms[i] and the launch
+ * count into counts[i], for i < min(max_stages, stage count); it
+ * synchronises the recorded events.  Stage names: lrs_conv_stage_name.
+ * Enabling adds an event record per launch; it is off by default.
+ */
+lrs_status lrs_conv_set_timing(lrs_conv *h, int32_t enable);
+lrs_status lrs_conv_stage_times(lrs_conv *h, float *ms, int64_t *counts, int32_t max_stages,
+                                int32_t *n_stages, int32_t reset);
+const char *lrs_conv_stage_name(const lrs_conv *h, int32_t stage);
+
+/*
+ * Test hook: device pointer of an intermediate of the last forward,
+ * which = 0: T1 [n*in_h*in_w][ld] ; 1: T2 [n*out_h*out_w][ld] (NULL for the SVD
+ * pair).  *ld receives the padded row length (elements, dtype).
+ */
+lrs_status lrs_conv_debug_buffer(const lrs_conv *h, int32_t which, const void **ptr, int32_t *ld);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LRS_CONV_H_ */

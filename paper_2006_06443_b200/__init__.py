@@ -1,0 +1,11 @@
+"""B200-native (sm_100a) compressed convolution W ~ L + S (arXiv 2006.06443).
+
+The product is the C-ABI library liblrs_conv.so (include/lrs_conv.h); this
+package is its thin Python binding.  It never imports `oracle/`.
+"""
+from .lrs_conv import (LrsConv, LrsError, lrs_conv_create, lrs_conv_destroy,  # noqa: F401
+                       lrs_conv_forward, lrs_conv_forward_host, lrs_conv_last_error,
+                       load_library, make_desc, EXPORTED, LIB_PATH)
+
+__all__ = ["LrsConv", "LrsError", "lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host",
+           "lrs_conv_destroy", "lrs_conv_last_error", "load_library", "make_desc"]

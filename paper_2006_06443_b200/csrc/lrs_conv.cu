@@ -1,0 +1,722 @@
+// lrs_conv.cu -- host side of the C-ABI declared in include/lrs_conv.h:
+// descriptor validation, weight repacking (rank padding, K-major tiles,
+// tf32 hi/lo split, per-tile sparse code streams), TMA descriptor encoding,
+// kernel launches and stage timing.  See DESIGN.md for the data layout.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lrs_conv.h"
+#include "lrs_kernels.cuh"
+
+using namespace lrs;
+
+namespace {
+
+thread_local std::string g_err;
+
+lrs_status fail(lrs_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define LRS_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(e_ == cudaErrorMemoryAllocation ? LRS_ERR_OUT_OF_MEMORY : LRS_ERR_CUDA, \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);    \
+  } while (0)
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+CUtensorMapSwizzle swz(uint32_t sw) {
+  return sw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                   : (sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+// rank-r tensor map; dims/strides innermost first (strides in bytes, r-1 of them)
+lrs_status encode(CUtensorMap* m, bool f32, int rank, void* ptr, const uint64_t* dims,
+                  const uint64_t* strides, const uint32_t* box, const uint32_t* estr, uint32_t sw) {
+  PFN_encodeTiled fn = get_encode();
+  if (!fn) return fail(LRS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                  rank, ptr, reinterpret_cast<const cuuint64_t*>(dims),
+                  reinterpret_cast<const cuuint64_t*>(strides), box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz(sw), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LRS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return LRS_OK;
+}
+
+inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
+inline uint32_t align1024(uint32_t a) { return (a + 1023u) & ~1023u; }
+inline uint32_t pow2_cols(int n) {
+  uint32_t c = 32;
+  while (c < static_cast<uint32_t>(n)) c <<= 1;
+  return c;
+}
+// widest swizzle (128/64/32 B) that divides a K extent of `bytes`
+uint32_t pick_sw(int bytes) {
+  if (bytes >= 128) return 128;
+  if (bytes >= 64) return 64;
+  return 32;
+}
+
+constexpr int kMaxSmem = 232448;  // 227 KB dynamic shared memory per CTA on sm_100
+
+enum KernelId { K_STORE_BF16, K_STORE_F32, K_SP64_BF16, K_SP128_BF16, K_SP64_F32, K_SP128_F32 };
+
+const void* kernel_ptr(KernelId id) {
+  switch (id) {
+    case K_STORE_BF16: return reinterpret_cast<const void*>(&lrs_gemm_kernel<false, EPI_STORE, 0>);
+    case K_STORE_F32: return reinterpret_cast<const void*>(&lrs_gemm_kernel<true, EPI_STORE, 0>);
+    case K_SP64_BF16: return reinterpret_cast<const void*>(&lrs_gemm_kernel<false, EPI_SPARSE, 64>);
+    case K_SP128_BF16: return reinterpret_cast<const void*>(&lrs_gemm_kernel<false, EPI_SPARSE, 128>);
+    case K_SP64_F32: return reinterpret_cast<const void*>(&lrs_gemm_kernel<true, EPI_SPARSE, 64>);
+    case K_SP128_F32: return reinterpret_cast<const void*>(&lrs_gemm_kernel<true, EPI_SPARSE, 128>);
+  }
+  return nullptr;
+}
+
+struct Stage {
+  const char* name;
+  KernelId kid;
+  GemmParams p;
+  uint32_t smem;
+  int tiles_per_image_or_rows;  // unused helper
+};
+
+struct TimingRing {
+  std::vector<cudaEvent_t> ev;  // pairs
+  int used = 0;
+  double ms = 0.0;
+  long long count = 0;
+};
+
+}  // namespace
+
+struct lrs_conv {
+  lrs_conv_desc d;
+  int device = 0;
+  bool f32 = false, svd = false;
+  int esz = 2;
+  int ho = 0, wo = 0;
+  int r1p = 0, r2p = 0, cout_p = 0, bn = 0;
+  // device buffers
+  void* w_uin = nullptr;   // [R1p (x2)][Cin]
+  void* w_core = nullptr;  // [R2p (x2)][k*k*R1p]
+  void* w_uout = nullptr;  // [Cout_p (x2)][R2p or R1p]
+  void* t1 = nullptr;
+  void* t2 = nullptr;
+  int2* ent = nullptr;
+  int* ent_ptr = nullptr;
+  // stages
+  Stage a1{}, a2{}, a3{};
+  int kc_a1 = 0;
+  uint32_t sw_a1 = 0;
+  // X map cache
+  const void* xmap_ptr = nullptr;
+  int xmap_n = -1;
+  CUtensorMap xmap{};
+  // host-io staging
+  void* hx = nullptr;
+  void* hy = nullptr;
+  // timing
+  bool timing = false;
+  TimingRing ring[3];
+};
+
+namespace {
+
+lrs_status validate(const lrs_conv_desc* d) {
+  if (!d) return fail(LRS_ERR_INVALID_ARGUMENT, "desc is NULL");
+  if (d->batch_max <= 0 || d->in_h <= 0 || d->in_w <= 0 || d->c_in <= 0 || d->c_out <= 0 ||
+      d->kernel_h <= 0 || d->kernel_w <= 0 || d->rank_in <= 0 || d->rank_out <= 0)
+    return fail(LRS_ERR_INVALID_ARGUMENT, "all extents must be > 0");
+  if (d->stride_h < 1 || d->stride_w < 1) return fail(LRS_ERR_INVALID_ARGUMENT, "stride < 1");
+  if (d->pad_h < 0 || d->pad_w < 0) return fail(LRS_ERR_INVALID_ARGUMENT, "pad < 0");
+  if (d->dtype != LRS_DTYPE_F32 && d->dtype != LRS_DTYPE_BF16)
+    return fail(LRS_ERR_INVALID_ARGUMENT, "unknown dtype %d", (int)d->dtype);
+  const int ho = (d->in_h + 2 * d->pad_h - d->kernel_h) / d->stride_h + 1;
+  const int wo = (d->in_w + 2 * d->pad_w - d->kernel_w) / d->stride_w + 1;
+  if (d->in_h + 2 * d->pad_h < d->kernel_h || d->in_w + 2 * d->pad_w < d->kernel_w || ho < 1 || wo < 1)
+    return fail(LRS_ERR_INVALID_ARGUMENT, "output extent < 1");
+  if (!d->u_in || !d->u_out) return fail(LRS_ERR_INVALID_ARGUMENT, "u_in / u_out is NULL");
+  if (!d->core) {
+    if (d->kernel_h != 1 || d->kernel_w != 1 || d->stride_h != 1 || d->stride_w != 1 ||
+        d->pad_h != 0 || d->pad_w != 0)
+      return fail(LRS_ERR_INVALID_ARGUMENT, "core == NULL (SVD pair) needs a 1x1, stride 1, pad 0 layer");
+    if (d->rank_in != d->rank_out)
+      return fail(LRS_ERR_INVALID_ARGUMENT, "core == NULL (SVD pair) needs rank_in == rank_out");
+  }
+  if (d->nnz < 0) return fail(LRS_ERR_INVALID_ARGUMENT, "nnz < 0");
+  if (!d->row_ptr) return fail(LRS_ERR_INVALID_ARGUMENT, "row_ptr is NULL");
+  if (d->nnz > 0 && (!d->col_idx || !d->values))
+    return fail(LRS_ERR_INVALID_ARGUMENT, "col_idx / values is NULL");
+  if (d->row_ptr[0] != 0 || d->row_ptr[d->c_out] != d->nnz)
+    return fail(LRS_ERR_INVALID_ARGUMENT, "row_ptr must start at 0 and end at nnz");
+  const int64_t ncol = static_cast<int64_t>(d->c_in) * d->kernel_h * d->kernel_w;
+  for (int j = 0; j < d->c_out; ++j) {
+    if (d->row_ptr[j + 1] < d->row_ptr[j])
+      return fail(LRS_ERR_INVALID_ARGUMENT, "row_ptr not monotone at row %d", j);
+    for (int64_t e = d->row_ptr[j]; e < d->row_ptr[j + 1]; ++e) {
+      const int32_t c = d->col_idx[e];
+      if (c < 0 || c >= ncol) return fail(LRS_ERR_INVALID_ARGUMENT, "col_idx out of range at %lld", (long long)e);
+      if (e > d->row_ptr[j] && c <= d->col_idx[e - 1])
+        return fail(LRS_ERR_INVALID_ARGUMENT, "columns of row %d not strictly increasing", j);
+    }
+  }
+  // ---- legal but not implemented
+  if (d->kernel_h > 7 || d->kernel_w > 7) return fail(LRS_ERR_UNSUPPORTED, "kernel > 7");
+  if (d->rank_in > 256 || d->rank_out > 256) return fail(LRS_ERR_UNSUPPORTED, "rank > 256");
+  const int vec = d->dtype == LRS_DTYPE_BF16 ? 8 : 4;
+  if (d->c_in % vec || d->c_out % vec)
+    return fail(LRS_ERR_UNSUPPORTED, "c_in and c_out must be multiples of %d", vec);
+  if (wo > 128) return fail(LRS_ERR_UNSUPPORTED, "output width > 128");
+  if (wo * d->stride_w > 256 || d->stride_h * std::min(ho, 128) > 256)
+    return fail(LRS_ERR_UNSUPPORTED, "TMA box too wide");
+  return LRS_OK;
+}
+
+// host value of element i of a dtype array
+inline float host_val(const void* a, size_t i, bool f32) {
+  if (f32) return static_cast<const float*>(a)[i];
+  uint32_t b = static_cast<uint32_t>(static_cast<const uint16_t*>(a)[i]) << 16;
+  float f;
+  memcpy(&f, &b, 4);
+  return f;
+}
+
+// pack `rows` x `k` fp32 matrix into the device dtype; fp32 -> [hi rows ; lo rows]
+std::vector<uint8_t> pack_matrix(const std::vector<float>& m, int rows, int k, bool f32) {
+  std::vector<uint8_t> out;
+  if (f32) {
+    out.resize(static_cast<size_t>(2) * rows * k * 4);
+    float* o = reinterpret_cast<float*>(out.data());
+    for (size_t i = 0; i < static_cast<size_t>(rows) * k; ++i) {
+      uint32_t b;
+      memcpy(&b, &m[i], 4);
+      b &= 0xFFFFE000u;
+      float hi;
+      memcpy(&hi, &b, 4);
+      o[i] = hi;
+      o[static_cast<size_t>(rows) * k + i] = m[i] - hi;
+    }
+  } else {
+    out.resize(static_cast<size_t>(rows) * k * 2);
+    uint16_t* o = reinterpret_cast<uint16_t*>(out.data());
+    for (size_t i = 0; i < static_cast<size_t>(rows) * k; ++i) {
+      uint32_t b;
+      memcpy(&b, &m[i], 4);  // values are bf16-exact (copied from bf16 input)
+      o[i] = static_cast<uint16_t>(b >> 16);
+    }
+  }
+  return out;
+}
+
+lrs_status upload(void** dst, const std::vector<uint8_t>& h) {
+  LRS_CUDA(cudaMalloc(dst, std::max<size_t>(h.size(), 16)));
+  if (!h.empty()) LRS_CUDA(cudaMemcpy(*dst, h.data(), h.size(), cudaMemcpyHostToDevice));
+  return LRS_OK;
+}
+
+// Fill the common GEMM stage fields; returns smem bytes (0 if it does not fit)
+uint32_t plan_stage(GemmParams& p, bool f32, int k_bytes_total, uint32_t sw, int bn, int b_lo_row,
+                    uint32_t a_box_bytes, uint32_t sparse_bytes) {
+  const int esz = f32 ? 4 : 2;
+  p.sw_bytes = sw;
+  p.kc = static_cast<int>(sw) / esz;
+  p.num_k_iters = (k_bytes_total + static_cast<int>(sw) - 1) / static_cast<int>(sw);
+  p.bn = bn;
+  p.b_lo_row = b_lo_row;
+  p.a_box_bytes = a_box_bytes;
+  p.a_stage_stride = align1024(kTileM * sw);
+  p.b_box_bytes = static_cast<uint32_t>(bn) * sw;
+  p.b_stage_stride = align1024(p.b_box_bytes) * (f32 ? 2u : 1u);
+  p.tmem_cols = pow2_cols(bn);
+  int S = std::min(4, p.num_k_iters);
+  for (; S >= 1; --S) {
+    uint32_t off = S * p.a_stage_stride * (f32 ? 2u : 1u) + S * p.b_stage_stride;
+    off = (off + 15u) & ~15u;
+    const uint32_t sparse_off = off;
+    off += sparse_bytes;
+    off = (off + 15u) & ~15u;
+    const uint32_t bar_off = off;
+    off += 8u * (3u * S + 1u) + 16u;
+    const uint32_t total = off + 1024u;
+    if (total <= static_cast<uint32_t>(kMaxSmem)) {
+      p.n_stages = S;
+      p.smem_sparse_off = sparse_off;
+      p.smem_bar_off = bar_off;
+      return total;
+    }
+  }
+  return 0;
+}
+
+lrs_status launch(lrs_conv* h, int si, Stage& st, dim3 grid, cudaStream_t stream) {
+  TimingRing& r = h->ring[si];
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->timing) {
+    if (r.used + 2 > static_cast<int>(r.ev.size())) {
+      const size_t old = r.ev.size();
+      r.ev.resize(old + 512);
+      for (size_t i = old; i < r.ev.size(); ++i) LRS_CUDA(cudaEventCreate(&r.ev[i]));
+    }
+    e0 = r.ev[r.used];
+    e1 = r.ev[r.used + 1];
+    r.used += 2;
+    LRS_CUDA(cudaEventRecord(e0, stream));
+  }
+  void* args[] = {&st.p};
+  LRS_CUDA(cudaLaunchKernel(kernel_ptr(st.kid), grid, dim3(kThreads), args, st.smem, stream));
+  if (h->timing) LRS_CUDA(cudaEventRecord(e1, stream));
+  return LRS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lrs_conv_last_error(void) { return g_err.c_str(); }
+
+lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
+  if (!out) return fail(LRS_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  lrs_status st = validate(d);
+  if (st != LRS_OK) return st;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(LRS_ERR_CUDA, "no CUDA device available (there is no CPU fallback)");
+  if (device < 0 || device >= ndev) return fail(LRS_ERR_INVALID_ARGUMENT, "device %d out of range", device);
+  int prev = 0;
+  LRS_CUDA(cudaGetDevice(&prev));
+  LRS_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  LRS_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    cudaSetDevice(prev);
+    return fail(LRS_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a only",
+                device, prop.major, prop.minor);
+  }
+
+  lrs_conv* h = new lrs_conv();
+  h->d = *d;
+  h->d.u_in = h->d.core = h->d.u_out = nullptr;
+  h->d.row_ptr = nullptr;
+  h->d.col_idx = nullptr;
+  h->d.values = nullptr;
+  h->device = device;
+  h->f32 = d->dtype == LRS_DTYPE_F32;
+  h->svd = d->core == nullptr;
+  h->esz = h->f32 ? 4 : 2;
+  const bool f32 = h->f32;
+  const int esz = h->esz;
+  const int cin = d->c_in, cout = d->c_out, kh = d->kernel_h, kw = d->kernel_w;
+  const int H = d->in_h, W = d->in_w;
+  h->ho = (H + 2 * d->pad_h - kh) / d->stride_h + 1;
+  h->wo = (W + 2 * d->pad_w - kw) / d->stride_w + 1;
+  const int ho = h->ho, wo = h->wo;
+  const int r1 = d->rank_in, r2 = h->svd ? d->rank_in : d->rank_out;
+  h->r1p = round_up(r1, 16);
+  h->r2p = h->svd ? h->r1p : round_up(r2, 16);
+  h->bn = cout <= 64 ? 64 : 128;
+  h->cout_p = round_up(cout, h->bn);
+  const int r1p = h->r1p, r2p = h->r2p, bn = h->bn, cout_p = h->cout_p;
+  const long long pin_max = static_cast<long long>(d->batch_max) * H * W;
+  const long long p_max = static_cast<long long>(d->batch_max) * ho * wo;
+
+  auto cleanup_fail = [&](lrs_status s) {
+    lrs_conv_destroy(h);
+    cudaSetDevice(prev);
+    return s;
+  };
+
+  // ---------------------------------------------------------------- weights
+  {
+    std::vector<float> m(static_cast<size_t>(r1p) * cin, 0.f);  // U_in^T [R1p][Cin]
+    for (int c = 0; c < cin; ++c)
+      for (int a = 0; a < r1; ++a) m[static_cast<size_t>(a) * cin + c] = host_val(d->u_in, (size_t)c * r1 + a, f32);
+    if ((st = upload(&h->w_uin, pack_matrix(m, r1p, cin, f32))) != LRS_OK) return cleanup_fail(st);
+  }
+  if (!h->svd) {
+    const int kk = kh * kw;
+    std::vector<float> m(static_cast<size_t>(r2p) * kk * r1p, 0.f);  // G^T [R2p][tap*R1p + a]
+    for (int a = 0; a < r1; ++a)
+      for (int b = 0; b < r2; ++b)
+        for (int t = 0; t < kk; ++t)
+          m[static_cast<size_t>(b) * kk * r1p + static_cast<size_t>(t) * r1p + a] =
+              host_val(d->core, ((size_t)a * r2 + b) * kk + t, f32);
+    if ((st = upload(&h->w_core, pack_matrix(m, r2p, kk * r1p, f32))) != LRS_OK) return cleanup_fail(st);
+  }
+  {
+    std::vector<float> m(static_cast<size_t>(cout_p) * r2p, 0.f);  // U_out^T [Cout_p][R2p]
+    for (int b = 0; b < r2; ++b)
+      for (int j = 0; j < cout; ++j) m[static_cast<size_t>(j) * r2p + b] = host_val(d->u_out, (size_t)b * cout + j, f32);
+    if ((st = upload(&h->w_uout, pack_matrix(m, cout_p, r2p, f32))) != LRS_OK) return cleanup_fail(st);
+  }
+  // ---------------------------------------------------------------- scratch
+  if (cudaMalloc(&h->t1, static_cast<size_t>(pin_max) * r1p * esz) != cudaSuccess)
+    return cleanup_fail(fail(LRS_ERR_OUT_OF_MEMORY, "T1 scratch allocation failed"));
+  if (!h->svd && cudaMalloc(&h->t2, static_cast<size_t>(p_max) * r2p * esz) != cudaSuccess)
+    return cleanup_fail(fail(LRS_ERR_OUT_OF_MEMORY, "T2 scratch allocation failed"));
+
+  // ---------------------------------------------------------------- a1: T1 = X U_in
+  {
+    GemmParams& p = h->a1.p;
+    memset(&p, 0, sizeof(p));
+    const uint32_t sw = pick_sw(cin * esz);
+    h->sw_a1 = sw;
+    h->kc_a1 = static_cast<int>(sw) / esz;
+    h->a1.smem = plan_stage(p, f32, cin * esz, sw, r1p, r1p, kTileM * sw, 0);
+    if (!h->a1.smem) return cleanup_fail(fail(LRS_ERR_UNSUPPORTED, "a1 does not fit in shared memory"));
+    p.amode = AMODE_2D;
+    p.out = h->t1;
+    p.out_ld = r1p;
+    uint64_t dims[2] = {static_cast<uint64_t>(cin), static_cast<uint64_t>(r1p) * (f32 ? 2 : 1)};
+    uint64_t strides[1] = {static_cast<uint64_t>(cin) * esz};
+    uint32_t box[2] = {static_cast<uint32_t>(p.kc), static_cast<uint32_t>(r1p)};
+    uint32_t estr[2] = {1, 1};
+    if ((st = encode(&p.tmB, f32, 2, h->w_uin, dims, strides, box, estr, sw)) != LRS_OK) return cleanup_fail(st);
+    h->a1.name = "a1_proj";
+    h->a1.kid = f32 ? K_STORE_F32 : K_STORE_BF16;
+  }
+  ConvGeom g{};
+  g.h = H; g.w = W; g.ho = ho; g.wo = wo; g.kh = kh; g.kw = kw;
+  g.sh = d->stride_h; g.sw = d->stride_w; g.ph = d->pad_h; g.pw = d->pad_w;
+  // ---------------------------------------------------------------- a2: T2 = conv(T1, G)
+  if (!h->svd) {
+    GemmParams& p = h->a2.p;
+    memset(&p, 0, sizeof(p));
+    const uint32_t sw = pick_sw(r1p * esz);
+    if (ho * wo <= kTileM) {
+      g.th = ho;
+      g.nb = kTileM / (ho * wo);
+    } else {
+      g.nb = 1;
+      const int thmax = kTileM / wo;
+      const int ntiles = (ho + thmax - 1) / thmax;
+      g.th = (ho + ntiles - 1) / ntiles;
+    }
+    g.tiles_h = (ho + g.th - 1) / g.th;
+    const uint32_t a_box = static_cast<uint32_t>(g.nb * g.th * wo) * sw;
+    const int kbytes = kh * kw * r1p * esz;
+    h->a2.smem = plan_stage(p, f32, kbytes, sw, r2p, r2p, a_box, 0);
+    if (!h->a2.smem) return cleanup_fail(fail(LRS_ERR_UNSUPPORTED, "a2 does not fit in shared memory"));
+    p.chunks_per_tap = (r1p * esz) / static_cast<int>(sw);
+    p.amode = AMODE_CONV;
+    p.out = h->t2;
+    p.out_ld = r2p;
+    {
+      uint64_t dims[4] = {static_cast<uint64_t>(r1p), static_cast<uint64_t>(W), static_cast<uint64_t>(H),
+                          static_cast<uint64_t>(d->batch_max)};
+      uint64_t strides[3] = {static_cast<uint64_t>(r1p) * esz, static_cast<uint64_t>(W) * r1p * esz,
+                             static_cast<uint64_t>(H) * W * r1p * esz};
+      uint32_t box[4] = {static_cast<uint32_t>(p.kc), static_cast<uint32_t>(wo * g.sw),
+                         static_cast<uint32_t>(g.th * g.sh), static_cast<uint32_t>(g.nb)};
+      uint32_t estr[4] = {1, static_cast<uint32_t>(g.sw), static_cast<uint32_t>(g.sh), 1};
+      if ((st = encode(&p.tmA, f32, 4, h->t1, dims, strides, box, estr, sw)) != LRS_OK) return cleanup_fail(st);
+    }
+    {
+      uint64_t dims[2] = {static_cast<uint64_t>(kh * kw * r1p), static_cast<uint64_t>(r2p) * (f32 ? 2 : 1)};
+      uint64_t strides[1] = {static_cast<uint64_t>(kh * kw * r1p) * esz};
+      uint32_t box[2] = {static_cast<uint32_t>(p.kc), static_cast<uint32_t>(r2p)};
+      uint32_t estr[2] = {1, 1};
+      if ((st = encode(&p.tmB, f32, 2, h->w_core, dims, strides, box, estr, sw)) != LRS_OK) return cleanup_fail(st);
+    }
+    h->a2.name = "a2_core";
+    h->a2.kid = f32 ? K_STORE_F32 : K_STORE_BF16;
+  }
+  // ---------------------------------------------------------------- a3+a4+a5
+  {
+    GemmParams& p = h->a3.p;
+    memset(&p, 0, sizeof(p));
+    const int kdim = r2p;  // K of the expansion (R2, or R for the SVD pair)
+    const uint32_t sw = pick_sw(kdim * esz);
+    // sparse window geometry: max padded rows over all tiles of batch_max images
+    const int wp = (wo - 1) * g.sw + kw;
+    int rows_max = 1;
+    {
+      const long long howo = static_cast<long long>(ho) * wo;
+      for (long long m0 = 0; m0 < p_max; m0 += kTileM) {
+        const long long m_last = std::min(m0 + kTileM - 1, p_max - 1);
+        const long long n_first = m0 / howo, n_last = m_last / howo;
+        const int nt = static_cast<int>(n_last - n_first + 1);
+        const int lo0 = static_cast<int>((m0 - n_first * howo) / wo);
+        const int hi0 = nt == 1 ? static_cast<int>((m_last - n_first * howo) / wo) : ho - 1;
+        const int rows0 = (hi0 - lo0) * g.sh + kh;
+        const int rows_full = (ho - 1) * g.sh + kh;
+        const int hi_last = static_cast<int>((m_last - n_last * howo) / wo);
+        const int rows_last = hi_last * g.sh + kh;
+        const int tot = nt == 1 ? rows0 : rows0 + (nt - 2) * rows_full + rows_last;
+        rows_max = std::max(rows_max, tot);
+      }
+    }
+    int wstride = rows_max * wp;
+    if (wstride % 2 == 0) wstride += 1;
+    const int vec = f32 ? 4 : 8;
+    const int budget = 64 * 1024;
+    int cc = (budget / (wstride * esz)) / vec * vec;
+    cc = std::min(cc, round_up(cin, vec));
+    if (cc < vec) return cleanup_fail(fail(LRS_ERR_UNSUPPORTED, "sparse window does not fit in shared memory"));
+    const int n_cc = (cin + cc - 1) / cc;
+    const uint32_t sparse_bytes = std::max<uint32_t>(static_cast<uint32_t>(cc) * wstride * esz,
+                                                     static_cast<uint32_t>(kTileM) * (bn + 1) * 4);
+    h->a3.smem = plan_stage(p, f32, kdim * esz, sw, bn, cout_p, kTileM * sw, sparse_bytes);
+    if (!h->a3.smem) return cleanup_fail(fail(LRS_ERR_UNSUPPORTED, "a3 does not fit in shared memory"));
+    p.amode = AMODE_2D;
+    p.sp.cin = cin;
+    p.sp.cc = cc;
+    p.sp.n_cc = n_cc;
+    p.sp.wstride = wstride;
+    p.sp.wp = wp;
+    p.sp.cout = cout;
+    {
+      void* src = h->svd ? h->t1 : h->t2;
+      uint64_t dims[2] = {static_cast<uint64_t>(kdim), static_cast<uint64_t>(p_max)};
+      uint64_t strides[1] = {static_cast<uint64_t>(kdim) * esz};
+      uint32_t box[2] = {static_cast<uint32_t>(p.kc), static_cast<uint32_t>(kTileM)};
+      uint32_t estr[2] = {1, 1};
+      if ((st = encode(&p.tmA, f32, 2, src, dims, strides, box, estr, sw)) != LRS_OK) return cleanup_fail(st);
+    }
+    {
+      uint64_t dims[2] = {static_cast<uint64_t>(kdim), static_cast<uint64_t>(cout_p) * (f32 ? 2 : 1)};
+      uint64_t strides[1] = {static_cast<uint64_t>(kdim) * esz};
+      uint32_t box[2] = {static_cast<uint32_t>(p.kc), static_cast<uint32_t>(bn)};
+      uint32_t estr[2] = {1, 1};
+      if ((st = encode(&p.tmB, f32, 2, h->w_uout, dims, strides, box, estr, sw)) != LRS_OK) return cleanup_fail(st);
+    }
+    // per (Cout chunk, channel chunk, output channel) code streams
+    const int n_chunks = cout_p / bn;
+    std::vector<int> ptr(static_cast<size_t>(n_chunks) * n_cc * bn + 1, 0);
+    std::vector<int2> ent;
+    ent.reserve(static_cast<size_t>(d->nnz));
+    const int kk = kh * kw;
+    for (int nc = 0; nc < n_chunks; ++nc)
+      for (int c = 0; c < n_cc; ++c)
+        for (int jl = 0; jl < bn; ++jl) {
+          const int j = nc * bn + jl;
+          ptr[(static_cast<size_t>(nc) * n_cc + c) * bn + jl] = static_cast<int>(ent.size());
+          if (j >= cout) continue;
+          for (int64_t e = d->row_ptr[j]; e < d->row_ptr[j + 1]; ++e) {
+            const int col = d->col_idx[e];
+            const int ch = col / kk, tap = col % kk;
+            if (ch / cc != c) continue;
+            const int ty = tap / kw, tx = tap % kw;
+            int2 v;
+            float val = d->values[e];
+            memcpy(&v.x, &val, 4);
+            v.y = (ch - c * cc) * wstride + ty * wp + tx;
+            ent.push_back(v);
+          }
+        }
+    ptr.back() = static_cast<int>(ent.size());
+    std::vector<uint8_t> pe(ptr.size() * 4), ee(std::max<size_t>(ent.size(), 1) * 8, 0);
+    memcpy(pe.data(), ptr.data(), pe.size());
+    if (!ent.empty()) memcpy(ee.data(), ent.data(), ent.size() * 8);
+    void* pp = nullptr;
+    void* pee = nullptr;
+    if ((st = upload(&pp, pe)) != LRS_OK) return cleanup_fail(st);
+    h->ent_ptr = static_cast<int*>(pp);
+    if ((st = upload(&pee, ee)) != LRS_OK) return cleanup_fail(st);
+    h->ent = static_cast<int2*>(pee);
+    p.sp.ent = h->ent;
+    p.sp.ent_ptr = h->ent_ptr;
+    h->a3.name = "a345_expand_sparse";
+    h->a3.kid = f32 ? (bn == 64 ? K_SP64_F32 : K_SP128_F32) : (bn == 64 ? K_SP64_BF16 : K_SP128_BF16);
+  }
+  h->a1.p.g = g;
+  h->a2.p.g = g;
+  h->a3.p.g = g;
+  for (int k = 0; k < 6; ++k) {
+    cudaError_t e = cudaFuncSetAttribute(kernel_ptr(static_cast<KernelId>(k)),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+    if (e != cudaSuccess)
+      return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
+  }
+  cudaSetDevice(prev);
+  *out = h;
+  return LRS_OK;
+}
+
+lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t n, void* stream_) {
+  lrs_conv* h = const_cast<lrs_conv*>(hc);
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (n < 0 || n > h->d.batch_max) return fail(LRS_ERR_INVALID_ARGUMENT, "n=%d outside [0, %d]", n, h->d.batch_max);
+  if (n == 0) return LRS_OK;
+  if (!x || !y) return fail(LRS_ERR_INVALID_ARGUMENT, "x / y is NULL");
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(y) & 15))
+    return fail(LRS_ERR_INVALID_ARGUMENT, "x / y must be 16-byte aligned");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  int prev = 0;
+  LRS_CUDA(cudaGetDevice(&prev));
+  if (prev != h->device) LRS_CUDA(cudaSetDevice(h->device));
+  const bool f32 = h->f32;
+  const int esz = h->esz;
+  const lrs_conv_desc& d = h->d;
+  lrs_status st = LRS_OK;
+  if (h->xmap_ptr != x || h->xmap_n != n) {
+    uint64_t dims[2] = {static_cast<uint64_t>(d.c_in), static_cast<uint64_t>(n) * d.in_h * d.in_w};
+    uint64_t strides[1] = {static_cast<uint64_t>(d.c_in) * esz};
+    uint32_t box[2] = {static_cast<uint32_t>(h->kc_a1), static_cast<uint32_t>(kTileM)};
+    uint32_t estr[2] = {1, 1};
+    if ((st = encode(&h->xmap, f32, 2, const_cast<void*>(x), dims, strides, box, estr, h->sw_a1)) != LRS_OK)
+      return st;
+    h->xmap_ptr = x;
+    h->xmap_n = n;
+  }
+  const long long pin = static_cast<long long>(n) * d.in_h * d.in_w;
+  const long long P = static_cast<long long>(n) * h->ho * h->wo;
+  // a1
+  h->a1.p.tmA = h->xmap;
+  h->a1.p.m_total = static_cast<int>(pin);
+  h->a1.p.g.n = n;
+  if ((st = launch(h, 0, h->a1, dim3(static_cast<unsigned>((pin + kTileM - 1) / kTileM)), stream)) != LRS_OK)
+    return st;
+  // a2
+  if (!h->svd) {
+    h->a2.p.g.n = n;
+    const int tiles = ((n + h->a2.p.g.nb - 1) / h->a2.p.g.nb) * h->a2.p.g.tiles_h;
+    if ((st = launch(h, 1, h->a2, dim3(tiles), stream)) != LRS_OK) return st;
+  }
+  // a3 + a4 + a5
+  h->a3.p.m_total = static_cast<int>(P);
+  h->a3.p.g.n = n;
+  h->a3.p.sp.x = x;
+  h->a3.p.sp.y = y;
+  if ((st = launch(h, 2, h->a3,
+                   dim3(static_cast<unsigned>((P + kTileM - 1) / kTileM), h->cout_p / h->bn), stream)) != LRS_OK)
+    return st;
+  if (prev != h->device) cudaSetDevice(prev);
+  return LRS_OK;
+}
+
+lrs_status lrs_conv_forward_host(lrs_conv* h, const void* x_host, void* y_host, int32_t n, void* stream_) {
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (n < 0 || n > h->d.batch_max) return fail(LRS_ERR_INVALID_ARGUMENT, "n=%d outside [0, %d]", n, h->d.batch_max);
+  if (n == 0) return LRS_OK;
+  if (!x_host || !y_host) return fail(LRS_ERR_INVALID_ARGUMENT, "x_host / y_host is NULL");
+  int prev = 0;
+  LRS_CUDA(cudaGetDevice(&prev));
+  if (prev != h->device) LRS_CUDA(cudaSetDevice(h->device));
+  const size_t xb = static_cast<size_t>(h->d.batch_max) * h->d.in_h * h->d.in_w * h->d.c_in * h->esz;
+  const size_t yb = static_cast<size_t>(h->d.batch_max) * h->ho * h->wo * h->d.c_out * h->esz;
+  if (!h->hx) LRS_CUDA(cudaMalloc(&h->hx, xb));
+  if (!h->hy) LRS_CUDA(cudaMalloc(&h->hy, yb));
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const size_t xn = static_cast<size_t>(n) * h->d.in_h * h->d.in_w * h->d.c_in * h->esz;
+  const size_t yn = static_cast<size_t>(n) * h->ho * h->wo * h->d.c_out * h->esz;
+  LRS_CUDA(cudaMemcpyAsync(h->hx, x_host, xn, cudaMemcpyHostToDevice, stream));
+  lrs_status st = lrs_conv_forward(h, h->hx, h->hy, n, stream_);
+  if (st != LRS_OK) return st;
+  LRS_CUDA(cudaMemcpyAsync(y_host, h->hy, yn, cudaMemcpyDeviceToHost, stream));
+  if (prev != h->device) cudaSetDevice(prev);
+  return LRS_OK;
+}
+
+lrs_status lrs_conv_destroy(lrs_conv* h) {
+  if (!h) return LRS_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->device);
+  void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  for (auto& r : h->ring)
+    for (auto e : r.ev) cudaEventDestroy(e);
+  cudaSetDevice(prev);
+  delete h;
+  return LRS_OK;
+}
+
+lrs_status lrs_conv_output_shape(const lrs_conv* h, int32_t* out_h, int32_t* out_w) {
+  if (!h || !out_h || !out_w) return fail(LRS_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out_h = h->ho;
+  *out_w = h->wo;
+  return LRS_OK;
+}
+
+int32_t lrs_conv_launches_per_forward(const lrs_conv* h) { return h ? (h->svd ? 2 : 3) : 0; }
+
+lrs_status lrs_conv_set_timing(lrs_conv* h, int32_t enable) {
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  h->timing = enable != 0;
+  return LRS_OK;
+}
+
+lrs_status lrs_conv_stage_times(lrs_conv* h, float* ms, int64_t* counts, int32_t max_stages,
+                                int32_t* n_stages, int32_t reset) {
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  for (int s = 0; s < 3; ++s) {
+    TimingRing& r = h->ring[s];
+    for (int i = 0; i + 1 < r.used; i += 2) {
+      LRS_CUDA(cudaEventSynchronize(r.ev[i + 1]));
+      float t = 0.f;
+      LRS_CUDA(cudaEventElapsedTime(&t, r.ev[i], r.ev[i + 1]));
+      r.ms += t;
+      r.count += 1;
+    }
+    r.used = 0;
+  }
+  if (n_stages) *n_stages = 3;
+  for (int s = 0; s < 3 && s < max_stages; ++s) {
+    if (ms) ms[s] = static_cast<float>(h->ring[s].ms);
+    if (counts) counts[s] = h->ring[s].count;
+  }
+  if (reset)
+    for (auto& r : h->ring) {
+      r.ms = 0.0;
+      r.count = 0;
+    }
+  return LRS_OK;
+}
+
+const char* lrs_conv_stage_name(const lrs_conv* h, int32_t stage) {
+  (void)h;
+  static const char* names[] = {"a1_proj", "a2_core", "a345_expand_sparse"};
+  return (stage >= 0 && stage < 3) ? names[stage] : "";
+}
+
+lrs_status lrs_conv_debug_buffer(const lrs_conv* h, int32_t which, const void** ptr, int32_t* ld) {
+  if (!h || !ptr || !ld) return fail(LRS_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (which == 0) {
+    *ptr = h->t1;
+    *ld = h->r1p;
+  } else if (which == 1) {
+    *ptr = h->t2;
+    *ld = h->r2p;
+  } else {
+    return fail(LRS_ERR_INVALID_ARGUMENT, "which must be 0 or 1");
+  }
+  return LRS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,250 @@
+"""Thin ctypes binding of the C-ABI in include/lrs_conv.h.
+
+Argument marshalling only: every step of the compressed convolution runs in
+the CUDA kernels of liblrs_conv.so.  PyTorch is used for device memory and
+streams.  There is no CPU fallback: if the shared library is missing or the
+device is not an sm_100 GPU, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "liblrs_conv.so")
+
+LRS_OK, LRS_ERR_INVALID_ARGUMENT, LRS_ERR_UNSUPPORTED, LRS_ERR_OUT_OF_MEMORY, LRS_ERR_CUDA = range(5)
+LRS_DTYPE_F32, LRS_DTYPE_BF16 = 0, 1
+STATUS_NAMES = {0: "LRS_OK", 1: "LRS_ERR_INVALID_ARGUMENT", 2: "LRS_ERR_UNSUPPORTED",
+                3: "LRS_ERR_OUT_OF_MEMORY", 4: "LRS_ERR_CUDA"}
+
+#: every symbol include/lrs_conv.h declares
+EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
+            "lrs_conv_last_error", "lrs_conv_output_shape", "lrs_conv_launches_per_forward",
+            "lrs_conv_set_timing", "lrs_conv_stage_times", "lrs_conv_stage_name",
+            "lrs_conv_debug_buffer")
+
+
+class LrsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class lrs_conv_desc(ctypes.Structure):
+    _fields_ = [
+        ("batch_max", ctypes.c_int32), ("in_h", ctypes.c_int32), ("in_w", ctypes.c_int32),
+        ("c_in", ctypes.c_int32), ("c_out", ctypes.c_int32),
+        ("kernel_h", ctypes.c_int32), ("kernel_w", ctypes.c_int32),
+        ("stride_h", ctypes.c_int32), ("stride_w", ctypes.c_int32),
+        ("pad_h", ctypes.c_int32), ("pad_w", ctypes.c_int32),
+        ("rank_in", ctypes.c_int32), ("rank_out", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("u_in", ctypes.c_void_p), ("core", ctypes.c_void_p), ("u_out", ctypes.c_void_p),
+        ("nnz", ctypes.c_int64),
+        ("row_ptr", ctypes.POINTER(ctypes.c_int64)),
+        ("col_idx", ctypes.POINTER(ctypes.c_int32)),
+        ("values", ctypes.POINTER(ctypes.c_float)),
+    ]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load liblrs_conv.so (raises if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run `python -m paper_2006_06443_b200._build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    lib.lrs_conv_create.argtypes = [ctypes.POINTER(lrs_conv_desc), ctypes.c_int, ctypes.POINTER(P)]
+    lib.lrs_conv_forward.argtypes = [P, P, P, ctypes.c_int32, P]
+    lib.lrs_conv_forward_host.argtypes = [P, P, P, ctypes.c_int32, P]
+    lib.lrs_conv_destroy.argtypes = [P]
+    lib.lrs_conv_last_error.restype = ctypes.c_char_p
+    lib.lrs_conv_output_shape.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+    lib.lrs_conv_launches_per_forward.argtypes = [P]
+    lib.lrs_conv_launches_per_forward.restype = ctypes.c_int32
+    lib.lrs_conv_set_timing.argtypes = [P, ctypes.c_int32]
+    lib.lrs_conv_stage_times.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64),
+                                         ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]
+    lib.lrs_conv_stage_name.argtypes = [P, ctypes.c_int32]
+    lib.lrs_conv_stage_name.restype = ctypes.c_char_p
+    lib.lrs_conv_debug_buffer.argtypes = [P, ctypes.c_int32, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_int32)]
+    for name in ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
+                 "lrs_conv_output_shape", "lrs_conv_set_timing", "lrs_conv_stage_times",
+                 "lrs_conv_debug_buffer"):
+        getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(st: int):
+    if st != LRS_OK:
+        raise LrsError(st, load_library().lrs_conv_last_error().decode())
+
+
+# ---------------------------------------------------------------- C-ABI names
+def lrs_conv_create(desc: lrs_conv_desc, device: int = 0) -> int:
+    h = ctypes.c_void_p()
+    _check(load_library().lrs_conv_create(ctypes.byref(desc), device, ctypes.byref(h)))
+    return h.value
+
+
+def lrs_conv_forward(handle: int, x_ptr: int, y_ptr: int, n: int, stream: int = 0) -> None:
+    _check(load_library().lrs_conv_forward(handle, x_ptr, y_ptr, n, stream))
+
+
+def lrs_conv_forward_host(handle: int, x_ptr: int, y_ptr: int, n: int, stream: int = 0) -> None:
+    _check(load_library().lrs_conv_forward_host(handle, x_ptr, y_ptr, n, stream))
+
+
+def lrs_conv_destroy(handle: int) -> None:
+    _check(load_library().lrs_conv_destroy(handle))
+
+
+def lrs_conv_last_error() -> str:
+    return load_library().lrs_conv_last_error().decode()
+
+
+def make_desc(batch_max: int, in_h: int, in_w: int, c_in: int, c_out: int, kernel: int,
+              stride: int, pad: int, rank_in: int, rank_out: int, dtype: str,
+              u_in: np.ndarray, core: Optional[np.ndarray], u_out: np.ndarray,
+              row_ptr: np.ndarray, col_idx: np.ndarray, values: np.ndarray):
+    """Build an lrs_conv_desc from host arrays.  Factor arrays are float32
+    holding dtype-representable values; for bf16 their bf16 bits are passed.
+    Returns (desc, keepalive) -- keep `keepalive` until lrs_conv_create returns."""
+    def as_dtype(a):
+        a = np.ascontiguousarray(a, np.float32)
+        if dtype == "bf16":
+            return np.ascontiguousarray((a.view(np.uint32) >> 16).astype(np.uint16))
+        return a
+    keep = []
+
+    def ptr(a):
+        keep.append(a)
+        return a.ctypes.data_as(ctypes.c_void_p)
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx, np.int32)
+    va = np.ascontiguousarray(values, np.float32)
+    keep += [rp, ci, va]
+    d = lrs_conv_desc(
+        batch_max=batch_max, in_h=in_h, in_w=in_w, c_in=c_in, c_out=c_out,
+        kernel_h=kernel, kernel_w=kernel, stride_h=stride, stride_w=stride, pad_h=pad, pad_w=pad,
+        rank_in=rank_in, rank_out=rank_out,
+        dtype=LRS_DTYPE_BF16 if dtype == "bf16" else LRS_DTYPE_F32,
+        u_in=ptr(as_dtype(u_in)), core=None if core is None else ptr(as_dtype(core)),
+        u_out=ptr(as_dtype(u_out)), nnz=len(va),
+        row_ptr=rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+        col_idx=ci.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+        values=va.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+    return d, keep
+
+
+class LrsConv:
+    """One compressed conv layer on one device: `LrsConv(...)(x) -> y`
+    with x, y NHWC torch tensors (contiguous, or channels_last NCHW views)."""
+
+    def __init__(self, batch_max, in_h, in_w, c_in, c_out, kernel, stride, pad, rank_in, rank_out,
+                 dtype, u_in, core, u_out, row_ptr, col_idx, values, device: int = 0):
+        import torch
+        self.torch = torch
+        self.dtype = dtype
+        self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.device = device
+        self.c_out = c_out
+        desc, keep = make_desc(batch_max, in_h, in_w, c_in, c_out, kernel, stride, pad, rank_in,
+                               rank_out, dtype, u_in, core, u_out, row_ptr, col_idx, values)
+        self.handle = lrs_conv_create(desc, device)
+        del keep
+        oh, ow = ctypes.c_int32(), ctypes.c_int32()
+        _check(load_library().lrs_conv_output_shape(self.handle, ctypes.byref(oh), ctypes.byref(ow)))
+        self.out_h, self.out_w = oh.value, ow.value
+        self.batch_max, self.in_h, self.in_w, self.c_in = batch_max, in_h, in_w, c_in
+
+    @classmethod
+    def from_inputs(cls, inp, batch_max: Optional[int] = None, device: int = 0) -> "LrsConv":
+        c = inp.cfg
+        return cls(batch_max or inp.x.shape[0], c.in_h, c.in_w, c.c_in, c.c_out, c.k, c.stride, c.pad,
+                   c.rank_in, c.rank_out, c.dtype, inp.u_in, inp.core, inp.u_out, inp.row_ptr,
+                   inp.col_idx, inp.values, device)
+
+    @property
+    def launches_per_forward(self) -> int:
+        return load_library().lrs_conv_launches_per_forward(self.handle)
+
+    def forward_into(self, x, y, stream=None) -> None:
+        torch = self.torch
+        n = x.shape[0]
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        lrs_conv_forward(self.handle, x.data_ptr(), y.data_ptr(), n, s.cuda_stream)
+
+    def __call__(self, x):
+        torch = self.torch
+        assert x.dtype == self.tdtype and x.is_cuda
+        assert x.shape[1:] == (self.in_h, self.in_w, self.c_in) and x.is_contiguous()
+        y = torch.empty((x.shape[0], self.out_h, self.out_w, self.c_out), dtype=self.tdtype, device=x.device)
+        self.forward_into(x, y)
+        return y
+
+    def forward_host(self, x_host, y_host, stream=None) -> None:
+        """x_host / y_host: pinned CPU tensors; enqueued on `stream`."""
+        torch = self.torch
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        lrs_conv_forward_host(self.handle, x_host.data_ptr(), y_host.data_ptr(), x_host.shape[0], s.cuda_stream)
+
+    def set_timing(self, on: bool) -> None:
+        _check(load_library().lrs_conv_set_timing(self.handle, 1 if on else 0))
+
+    def stage_times(self, reset: bool = True):
+        """{stage name: (total ms, launches)} of event-timed kernels since the last reset."""
+        ms = (ctypes.c_float * 8)()
+        cnt = (ctypes.c_int64 * 8)()
+        ns = ctypes.c_int32()
+        lib = load_library()
+        _check(lib.lrs_conv_stage_times(self.handle, ms, cnt, 8, ctypes.byref(ns), 1 if reset else 0))
+        return {lib.lrs_conv_stage_name(self.handle, i).decode(): (ms[i], cnt[i]) for i in range(ns.value)}
+
+    def debug_buffer(self, which: int, rows: int):
+        """Intermediate T1 (which=0) / T2 (which=1) of the last forward as a torch tensor view copy."""
+        torch = self.torch
+        p = ctypes.c_void_p()
+        ld = ctypes.c_int32()
+        _check(load_library().lrs_conv_debug_buffer(self.handle, which, ctypes.byref(p), ctypes.byref(ld)))
+        esz = 2 if self.dtype == "bf16" else 4
+        nbytes = rows * ld.value * esz
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        torch.cuda.synchronize(self.device)
+        cudart_memcpy(buf.data_ptr(), p.value, nbytes)
+        return buf.view(self.tdtype).view(rows, ld.value)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            lrs_conv_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def cudart_memcpy(dst: int, src: int, nbytes: int) -> None:
+    """device->device copy through torch (used only by the debug hook)."""
+    import torch
+    s = torch.cuda.current_stream()
+    _cudart = ctypes.CDLL("libcudart.so.12") if not hasattr(cudart_memcpy, "_lib") else cudart_memcpy._lib
+    cudart_memcpy._lib = _cudart
+    _cudart.cudaMemcpyAsync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+    r = _cudart.cudaMemcpyAsync(dst, src, nbytes, 3, s.cuda_stream)
+    if r != 0:
+        raise RuntimeError(f"cudaMemcpyAsync failed {r}")
+    torch.cuda.synchronize()

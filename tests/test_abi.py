@@ -1,0 +1,128 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/lrs_conv.h declares, and create() rejects malformed or
+unsupported descriptors with the documented status (validation runs before
+any device call), while a well-formed descriptor on a GPU-less host fails
+loudly with LRS_ERR_CUDA (no CPU fallback)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2006_06443_b200 as P
+from paper_2006_06443_b200 import lrs_conv as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "lrs_conv.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:lrs_status|const char \*|int32_t)\s*\**\s*(lrs_conv_\w+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = P.load_library()
+    names = header_functions()
+    assert len(names) >= 10
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(B.EXPORTED)
+
+
+def base_desc_args(**over):
+    rng = np.random.default_rng(0)
+    a = dict(batch_max=2, in_h=8, in_w=8, c_in=16, c_out=16, kernel=3, stride=1, pad=1,
+             rank_in=4, rank_out=4, dtype="bf16",
+             u_in=rng.standard_normal((16, 4)).astype(np.float32),
+             core=rng.standard_normal((4, 4, 3, 3)).astype(np.float32),
+             u_out=rng.standard_normal((4, 16)).astype(np.float32),
+             row_ptr=np.r_[0, np.full(16, 1).cumsum()].astype(np.int64),
+             col_idx=np.arange(16, dtype=np.int32) * 9 + 4, values=np.ones(16, np.float32))
+    a.update(over)
+    return a
+
+
+def create_status(**over):
+    a = base_desc_args(**over)
+    d, keep = B.make_desc(**a)
+    for k, v in over.pop("_patch", {}).items() if "_patch" in over else []:
+        setattr(d, k, v)
+    lib = P.load_library()
+    h = ctypes.c_void_p()
+    st = lib.lrs_conv_create(ctypes.byref(d), 0, ctypes.byref(h))
+    if st == 0:
+        lib.lrs_conv_destroy(h)
+    return st, lib.lrs_conv_last_error().decode()
+
+
+def patched_status(**fields):
+    d, keep = B.make_desc(**base_desc_args())
+    for k, v in fields.items():
+        setattr(d, k, v)
+    lib = P.load_library()
+    h = ctypes.c_void_p()
+    st = lib.lrs_conv_create(ctypes.byref(d), 0, ctypes.byref(h))
+    return st, lib.lrs_conv_last_error().decode()
+
+
+@pytest.mark.parametrize("fields", [
+    dict(batch_max=0), dict(in_h=0), dict(c_out=-1), dict(rank_in=0),
+    dict(stride_h=0), dict(pad_w=-1), dict(kernel_h=20),  # output extent < 1
+    dict(dtype=7), dict(nnz=-1),
+])
+def test_invalid_descriptors(fields):
+    st, msg = patched_status(**fields)
+    assert st == B.LRS_ERR_INVALID_ARGUMENT, (st, msg)
+    assert msg
+
+
+def test_invalid_csr():
+    rp = np.r_[0, np.full(16, 1).cumsum()].astype(np.int64)
+    st, _ = create_status(row_ptr=rp[::-1].copy())
+    assert st == B.LRS_ERR_INVALID_ARGUMENT
+    st, _ = create_status(col_idx=np.full(16, 16 * 9, np.int32))  # col out of range
+    assert st == B.LRS_ERR_INVALID_ARGUMENT
+    rp2 = np.zeros(17, np.int64)
+    rp2[1:] = 16
+    st, msg = create_status(row_ptr=rp2, col_idx=np.r_[np.arange(15, dtype=np.int32), 3])  # unsorted/dup
+    assert st == B.LRS_ERR_INVALID_ARGUMENT and "increasing" in msg
+
+
+def test_svd_pair_requires_1x1():
+    st, msg = create_status(core=None)
+    assert st == B.LRS_ERR_INVALID_ARGUMENT and "SVD" in msg
+    st, msg = create_status(core=None, kernel=1, pad=0, rank_out=5,
+                            col_idx=np.arange(16, dtype=np.int32))
+    assert st == B.LRS_ERR_INVALID_ARGUMENT and "rank_in == rank_out" in msg
+
+
+@pytest.mark.parametrize("over,needle", [
+    (dict(c_in=12, u_in=np.zeros((12, 4), np.float32), col_idx=np.arange(16, dtype=np.int32)), "multiples"),
+    (dict(rank_in=300, u_in=np.zeros((16, 300), np.float32), core=np.zeros((300, 4, 3, 3), np.float32)), "rank"),
+])
+def test_unsupported_descriptors(over, needle):
+    st, msg = create_status(**over)
+    assert st == B.LRS_ERR_UNSUPPORTED and needle in msg
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    st, msg = create_status()
+    assert st == B.LRS_ERR_CUDA and "no CUDA device" in msg
+
+
+def test_product_package_does_not_import_oracle():
+    """The CUDA path and the oracle share no code (only workloads/ feeds both)."""
+    pkg = os.path.join(ROOT, "paper_2006_06443_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "from oracle" not in src and "import oracle" not in src, f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith(".py"):
+            src = open(os.path.join(ROOT, "oracle", f)).read()
+            assert "import paper_2006_06443_b200" not in src and "from paper_2006_06443_b200" not in src, f
