@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 compressed convolution W ~ L + S (arXiv 2006.06443).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_bf16] [--impl lrs|reference]
+(N > 1: launched by torchrun, one process per GPU; RANK/WORLD_SIZE from env.)
+
+A step = one forward of the whole hot path (a1 projection, a2 core, a3
+expansion + a4 sparse + a5 sum/store) over one batch of the workload
+(default BASELINE.json configs[1] = C2, ResNet-50 layer3 3x3 256->256 at
+14x14, batch 64, bf16).  Weak scaling: every rank runs its own batch (its
+own seeded images, same weights); there is no collective on the data path.
+
+Timing: W untimed warm-up steps, then EXACTLY K steps replayed from a CUDA
+graph, bracketed by barrier + cuda.synchronize; CUDA events on the launching
+stream; max over ranks.  Inputs rotate over enough X/Y buffer sets to cover
+2.1x the L2, so every step reads X from HBM.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+CONFIG_TEXT = {
+    "c1": "C1: 3x3 conv 64->64 @56x56, stride 1, pad 1, batch 1, Tucker-2 (16,16), S 1% (369 nnz), fp32",
+    "c2_f32": "C2: ResNet-50 layer3 3x3 conv 256->256 @14x14, batch 64, Tucker-2 (64,64), S 2%, fp32",
+    "c2_bf16": "C2: ResNet-50 layer3 3x3 conv 256->256 @14x14, batch 64, Tucker-2 (64,64), S 2%, bf16",
+    "c3": "C3: ResNet-50 layer4 3x3 conv 512->512 @7x7, batch 256, Tucker-2 (128,128), S 5%, bf16",
+    "c4": "C4: ResNet-50 1x1 expansion 256->1024 @14x14, batch 128, SVD rank 64, S 1%, bf16",
+}
+METRIC = "compressed-conv images/s and % of roofline at 1/2/4/8 B200 vs CPU oracle"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c2_bf16", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--impl", default="lrs", choices=["lrs", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def cpu_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        return max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        return 1
+
+
+def oracle_rate(cfg, inp, seconds: float, sample_images: int):
+    """Time the fp64 oracle (forward_factored, as it stands) on a bounded
+    sample of the workload: repeated calls on `sample_images` images."""
+    from oracle import lrs_oracle as O
+    x = inp.x[:sample_images].astype(np.float64)
+    calls, t0 = 0, time.perf_counter()
+    while True:
+        O.forward_factored(x, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx, inp.values,
+                           cfg.stride, cfg.pad)
+        calls += 1
+        el = time.perf_counter() - t0
+        if el >= seconds and calls >= 2:
+            break
+    return calls * sample_images / el, calls, el
+
+
+class ClockSampler:
+    """NVML SM clock / throttle-reason sampling during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop_ev.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the oracle (fp64 numpy, as it stands) on host cores."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    sample = max(1, min(cfg.batch, 8))
+    inp = workloads.generate(cfg, batch=sample)
+    from oracle import lrs_oracle as O
+    x = inp.x.astype(np.float64)
+
+    def step():
+        O.forward_factored(x, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx, inp.values,
+                           cfg.stride, cfg.pad)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    value = args.steps * sample / el
+    line = {"metric": METRIC, "value": value, "unit": "images/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, workloads/)",
+            "config": {"workload": CONFIG_TEXT[args.config], "images_per_step": sample},
+            "cpu_baseline": {"value": value, "unit": "images/s", "cores": cpu_threads(), "kind": "oracle",
+                             "sample": f"{sample} images of {args.config} per step (fp64 numpy oracle, "
+                                       "forward_factored)"},
+            "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = workloads.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    from paper_2006_06443_b200 import LrsConv
+    from paper_2006_06443_b200 import roofline as RL
+
+    # ---- inputs: same weights everywhere, rank-specific images (weak scaling)
+    inp = workloads.generate(cfg)
+    if rank > 0:
+        inp.x = workloads.generate(cfg, seed=1000 + rank).x
+    n = cfg.batch
+    layer = LrsConv.from_inputs(inp, batch_max=n, device=local)
+    tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    esz = 2 if cfg.dtype == "bf16" else 4
+    x_bytes = n * cfg.in_h * cfg.in_w * cfg.c_in * esz
+    y_bytes = n * cfg.out_h * cfg.out_w * cfg.c_out * esz
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    n_sets = max(2, math.ceil(2.1 * l2 / (x_bytes + y_bytes)))
+    x0 = torch.from_numpy(inp.x).to(tdt).to(dev)
+    xs = [x0] + [x0.clone() for _ in range(n_sets - 1)]
+    ys = [torch.empty((n, cfg.out_h, cfg.out_w, cfg.c_out), dtype=tdt, device=dev) for _ in range(n_sets)]
+    stream = torch.cuda.Stream(device=dev)
+
+    def capture(count: int):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(count):
+                    layer.forward_into(xs[i % n_sets], ys[i % n_sets], stream=stream)
+        return g
+
+    with torch.cuda.stream(stream):
+        for i in range(n_sets):  # eager warm-up (also JIT-loads the module)
+            layer.forward_into(xs[i], ys[i], stream=stream)
+    torch.cuda.synchronize(dev)
+    K, W = args.steps, args.warmup
+    g_full = capture(n_sets)
+    rem = K % n_sets
+    g_rem = capture(rem) if rem else None
+
+    def run_steps(k_full, with_rem):
+        for _ in range(k_full):
+            g_full.replay()
+        if with_rem and g_rem is not None:
+            g_rem.replay()
+
+    # ---- warm-up
+    for _ in range(max(1, math.ceil(W / n_sets))):
+        g_full.replay()
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # ---- timed region: exactly K forwards
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+    barrier()
+    with sampler:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            run_steps(K // n_sets, True)
+            ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / K
+    value = world * n * K / (ms_max / 1e3)
+
+    # ---- per-kernel durations: same graphs with an event pair around every launch
+    layer.set_timing(True)
+    with torch.cuda.stream(stream):
+        for i in range(n_sets):
+            layer.forward_into(xs[i], ys[i], stream=stream)
+    torch.cuda.synchronize(dev)
+    layer.stage_times(reset=True)
+    g_t = capture(n_sets)  # event pairs are recorded by the replays below
+    g_t.replay()
+    torch.cuda.synchronize(dev)
+    g_t.replay()
+    torch.cuda.synchronize(dev)
+    stages = layer.stage_times(reset=True)
+    layer.set_timing(False)
+
+    # ---- end to end through the C-ABI with host buffers (H2D + forward + D2H per step)
+    e2e = None
+    if not args.no_e2e:
+        xh = x0.cpu().pin_memory()
+        yh = torch.empty(ys[0].shape, dtype=tdt).pin_memory()
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                layer.forward_host(xh, yh, stream=stream)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ke = max(3, min(K, 50))
+        barrier()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(ke):
+                layer.forward_host(xh, yh, stream=stream)
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * n * ke / (float(te.item()) / 1e3), "unit": "images/s",
+               "h2d_bytes_per_step": x_bytes, "d2h_bytes_per_step": y_bytes, "steps": ke,
+               "api": "lrs_conv_forward_host (pinned host buffers)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel + layer roofs
+    peaks = RL.measured_peaks()
+    work = RL.layer_work(cfg, n, inp.col_idx)
+    roofs = RL.layer_roofs(work, peaks, cfg.dtype)
+    avg = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in stages.items()}
+    dom = max(avg, key=lambda k: avg[k])
+    t_dom = avg[dom] / 1e3
+    fma_peak = RL.fp32_fma_tflops(peaks["sm_max_mhz"])
+    if dom == "a345_expand_sparse":
+        wk = work[dom]
+        achieved = wk["flops_sparse"] / t_dom / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s",
+                "frac": achieved / fma_peak, "traffic": None, "kernel": dom,
+                "work": "sparse in-bounds MACs x 2 per launch (FP32 FMA pipe)",
+                "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz"}
+    else:
+        wk = work[dom]
+        tc = peaks["bf16_tflops"] * (1.0 if cfg.dtype == "bf16" else 0.5 / 3.0)
+        if wk["bytes"] / (peaks["hbm_gbs"] * 1e9) >= wk["flops"] / (tc * 1e12):
+            achieved = wk["bytes"] / t_dom / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dom}
+        else:
+            achieved = wk["flops"] / t_dom / 1e12
+            roof = {"bound": "tensor", "achieved": achieved, "peak": tc, "unit": "TFLOP/s",
+                    "frac": achieved / tc, "traffic": None, "kernel": dom}
+    roof["peak_kind"] = peaks["source"]
+    roof["stage_us"] = {k: round(v * 1e3, 3) for k, v in avg.items()}
+    step_s = ms_per_step / 1e3
+    layer_roof = {"literal_roof_us": roofs["t_literal_s"] * 1e6, "three_roof_us": roofs["t_three_roof_s"] * 1e6,
+                  "frac_literal": roofs["t_literal_s"] / step_s, "frac_three_roof": roofs["t_three_roof_s"] / step_s,
+                  "t_hbm_us": roofs["t_hbm_s"] * 1e6, "t_chain_tc_us": roofs["t_chain_tc_s"] * 1e6,
+                  "t_sparse_fma_us": roofs["t_sparse_fma_s"] * 1e6}
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        sample = max(1, min(n, 8))
+        rate, calls, el = oracle_rate(cfg, inp, args.cpu_seconds, sample)
+        cpu = {"value": rate, "unit": "images/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": f"{calls} oracle forwards x {sample} images of {args.config} ({el:.1f} s, fp64 numpy "
+                         "forward_factored; BLAS threads = cores, sparse scatter single-threaded)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": cfg.dtype, "data": "synthetic (seeded ReLU(N(0,1)) images, N(0,1/fan_in) factors, uniform S)",
+        "config": {"workload": CONFIG_TEXT[args.config], "config_id": args.config, "global_batch": n * world,
+                   "per_gpu_batch": n, "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
+                   "l2": f"{n_sets} rotating X/Y buffer sets = {n_sets * (x_bytes + y_bytes) / 2**20:.0f} MiB "
+                         f"(2.1x L2 {l2 / 2**20:.0f} MiB)",
+                   "timing": "CUDA graph replay, CUDA events, max over ranks"},
+        "clocks": sampler.summary(),
+        "e2e": e2e,
+        "gpu_launches": layer.launches_per_forward * K,
+        "roofline": roof,
+        "roofline_layer": layer_roof,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

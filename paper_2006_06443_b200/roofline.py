@@ -1,0 +1,99 @@
+"""Algorithmic work of the compressed convolution, for roofline fractions.
+
+Host-side measurement arithmetic only (no kernels).  Definitions follow
+SURVEY.md §8(d) / DESIGN.md "Roofline": bytes count what the method itself
+must move (X read once, Y written once, weights + CSR once, intermediates
+T1/T2 written and read once), FLOPs count 2 per multiply-add; the sparse term
+counts only in-bounds taps.
+"""
+from __future__ import annotations
+
+import json
+import os
+from typing import Dict, Optional
+
+import numpy as np
+
+#: B200 FP32 CUDA-core pipe: 148 SMs x 128 FMA/clk (B200_PROFILING.md table: 148 SMs;
+#: Blackwell SM = 4 partitions x 32 FP32 lanes); 2 FLOP per FMA.
+FP32_FMA_PER_CLK_PER_SM = 128
+NUM_SMS = 148
+
+
+def measured_peaks(path: Optional[str] = None) -> Dict[str, float]:
+    """MEASURED_PEAKS.json (driver-written) or the profiling guide's fallback."""
+    if path is None:
+        path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)), "source": "measured"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0, "source": "fallback"}
+
+
+def fp32_fma_tflops(sm_mhz: float) -> float:
+    return NUM_SMS * FP32_FMA_PER_CLK_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+
+
+def out_size(n: int, k: int, s: int, p: int) -> int:
+    return (n + 2 * p - k) // s + 1
+
+
+def sparse_macs(n: int, h: int, w: int, k: int, s: int, p: int, col_idx: np.ndarray) -> int:
+    """In-bounds sparse multiply-adds: n * sum_e V(y_e) V(x_e) with
+    V(t) = #{o in [0, Ho): 0 <= o*s + t - p < H}."""
+    ho, wo = out_size(h, k, s, p), out_size(w, k, s, p)
+    vh = np.array([sum(1 for o in range(ho) if 0 <= o * s + t - p < h) for t in range(k)], np.int64)
+    vw = np.array([sum(1 for o in range(wo) if 0 <= o * s + t - p < w) for t in range(k)], np.int64)
+    tap = np.asarray(col_idx, np.int64) % (k * k)
+    return int(n * (vh[tap // k] * vw[tap % k]).sum())
+
+
+def layer_work(cfg, n: int, col_idx: np.ndarray) -> Dict[str, Dict[str, float]]:
+    """Per-stage algorithmic bytes and FLOPs for n images of layer `cfg`
+    (a workloads.LayerConfig)."""
+    esz = 2 if cfg.dtype == "bf16" else 4
+    ho, wo = cfg.out_h, cfg.out_w
+    p_in = n * cfg.in_h * cfg.in_w
+    p = n * ho * wo
+    r1 = cfg.rank_in
+    r2 = cfg.rank_in if cfg.svd else cfg.rank_out
+    nnz = len(col_idx)
+    x_b = p_in * cfg.c_in * esz
+    y_b = p * cfg.c_out * esz
+    t1_b = p_in * r1 * esz
+    t2_b = 0 if cfg.svd else p * r2 * esz
+    macs_s = sparse_macs(n, cfg.in_h, cfg.in_w, cfg.k, cfg.stride, cfg.pad, col_idx)
+    st = {
+        "a1_proj": {"bytes": x_b + t1_b + cfg.c_in * r1 * esz, "flops": 2.0 * p_in * cfg.c_in * r1},
+        "a345_expand_sparse": {
+            "bytes": (t2_b if not cfg.svd else t1_b) + y_b + r2 * cfg.c_out * esz + nnz * 8 + (cfg.c_out + 1) * 4,
+            "flops_tc": 2.0 * p * r2 * cfg.c_out, "flops_sparse": 2.0 * macs_s, "sparse_macs": macs_s},
+    }
+    st["a345_expand_sparse"]["flops"] = st["a345_expand_sparse"]["flops_tc"] + st["a345_expand_sparse"]["flops_sparse"]
+    if not cfg.svd:
+        st["a2_core"] = {"bytes": t1_b + t2_b + r1 * r2 * cfg.k * cfg.k * esz,
+                         "flops": 2.0 * p * r1 * r2 * cfg.k * cfg.k}
+    layer_bytes = x_b + y_b + esz * (cfg.c_in * r1 + (0 if cfg.svd else r1 * r2 * cfg.k ** 2) + r2 * cfg.c_out) \
+        + nnz * 8 + (cfg.c_out + 1) * 4
+    chain = 2.0 * (p_in * cfg.c_in * r1 + (0 if cfg.svd else p * r1 * r2 * cfg.k ** 2) + p * r2 * cfg.c_out)
+    st["layer"] = {"bytes": layer_bytes, "flops_chain": chain, "flops_sparse": 2.0 * macs_s,
+                   "sparse_macs": macs_s, "flops": chain + 2.0 * macs_s}
+    return st
+
+
+def layer_roofs(work: Dict[str, Dict[str, float]], peaks: Dict[str, float], dtype: str) -> Dict[str, float]:
+    """Literal roof (BASELINE: max(bytes/BW, all FLOPs/tensor peak)) and the
+    three-roof (sparse MACs on the FP32 pipe), in seconds."""
+    lay = work["layer"]
+    tc = peaks["bf16_tflops"] * 1e12 * (1.0 if dtype == "bf16" else 0.5 / 3.0)  # fp32: 3xTF32 at TF32 = bf16/2
+    bw = peaks["hbm_gbs"] * 1e9
+    fma = fp32_fma_tflops(peaks["sm_max_mhz"]) * 1e12
+    t_lit = max(lay["bytes"] / bw, lay["flops"] / tc)
+    t_three = max(lay["bytes"] / bw, lay["flops_chain"] / tc, lay["flops_sparse"] / fma)
+    return {"t_literal_s": t_lit, "t_three_roof_s": t_three, "t_hbm_s": lay["bytes"] / bw,
+            "t_chain_tc_s": lay["flops_chain"] / tc, "t_sparse_fma_s": lay["flops_sparse"] / fma}
