@@ -139,6 +139,26 @@ const char *lrs_conv_stage_name(const lrs_conv *h, int32_t stage);
  */
 lrs_status lrs_conv_debug_buffer(const lrs_conv *h, int32_t which, const void **ptr, int32_t *ld);
 
+/*
+ * Which engine evaluates the sparse term S of this layer (returns -1 for NULL):
+ *   0  SIMT CSR gather fused into the epilogue of the expansion GEMM
+ *      (fp32 layers and shapes the tensor-core path does not cover);
+ *   1  2:4 sparse tensor cores (tcgen05.mma.sp): every group of 4 consecutive
+ *      input channels of a (output channel, tap) is split exactly into a main
+ *      2:4 block and, where the group holds 3-4 nonzeros, a residual 2:4 block;
+ *      fused with the expansion GEMM (bf16 layers with c_in % 64 == 0).
+ * For engine 1, *main_blocks / *residual_blocks (may be NULL) receive the
+ * number of 128-row compressed blocks of each kind.
+ */
+int32_t lrs_conv_sparse_engine(const lrs_conv *h, int32_t *main_blocks, int32_t *residual_blocks);
+
+/*
+ * Debug hook: when dev_buf (device, >= 1005 uint64) is non-NULL, CTA 0 of the
+ * fused tensor-core kernel stores %globaltimer stamps of its pipeline events
+ * there (NULL disables).  Not for production use.
+ */
+lrs_status lrs_conv_debug_trace(lrs_conv *h, void *dev_buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,7 @@
 
 #include "../../include/lrs_conv.h"
 #include "lrs_kernels.cuh"
+#include "lrs_wconv.cuh"
 
 using namespace lrs;
 
@@ -62,18 +63,23 @@ CUtensorMapSwizzle swz(uint32_t sw) {
                    : (sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
-// rank-r tensor map; dims/strides innermost first (strides in bytes, r-1 of them)
-lrs_status encode(CUtensorMap* m, bool f32, int rank, void* ptr, const uint64_t* dims,
-                  const uint64_t* strides, const uint32_t* box, const uint32_t* estr, uint32_t sw) {
+// rank-r tensor map; dims/strides innermost first (strides in bytes, r-1 of them);
+// sw = 0 means no swizzle
+lrs_status encode_t(CUtensorMap* m, CUtensorMapDataType dt, int rank, void* ptr, const uint64_t* dims,
+                    const uint64_t* strides, const uint32_t* box, const uint32_t* estr, uint32_t sw) {
   PFN_encodeTiled fn = get_encode();
   if (!fn) return fail(LRS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
-                  rank, ptr, reinterpret_cast<const cuuint64_t*>(dims),
-                  reinterpret_cast<const cuuint64_t*>(strides), box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz(sw), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = fn(m, dt, rank, ptr, reinterpret_cast<const cuuint64_t*>(dims),
+                  reinterpret_cast<const cuuint64_t*>(strides), box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  sw == 0 ? CU_TENSOR_MAP_SWIZZLE_NONE : swz(sw), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(LRS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  if (r != CUDA_SUCCESS) return fail(LRS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d, rank %d)", (int)r, rank);
   return LRS_OK;
+}
+lrs_status encode(CUtensorMap* m, bool f32, int rank, void* ptr, const uint64_t* dims,
+                  const uint64_t* strides, const uint32_t* box, const uint32_t* estr, uint32_t sw) {
+  return encode_t(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, ptr, dims,
+                  strides, box, estr, sw);
 }
 
 inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
@@ -152,6 +158,16 @@ struct lrs_conv {
   // timing
   bool timing = false;
   TimingRing ring[3];
+  // fused a3+a4+a5 on the tensor cores (lrs_wconv.cuh), bf16 layers
+  bool use_w = false;
+  WconvParams wp{};
+  uint32_t w_smem = 0;
+  void* w_as = nullptr;   // compressed 2:4 blocks of S
+  void* w_e = nullptr;    // their metadata
+  int* w_res = nullptr;   // residual block table
+  const void* wx_ptr = nullptr;
+  int wx_n = -1;
+  int w_main_blocks = 0, w_res_blocks = 0;
 };
 
 namespace {
@@ -302,6 +318,278 @@ lrs_status launch(lrs_conv* h, int si, Stage& st, dim3 grid, cudaStream_t stream
   return LRS_OK;
 }
 
+
+inline uint16_t bf16_bits_rne(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+// Fused a3+a4+a5 on the tensor cores (lrs_wconv.cuh): choose the tile geometry,
+// split S into exact 2:4 main + residual blocks with their TMEM metadata, and
+// encode the static tensor maps.  Leaves h->use_w false if the layer does not fit.
+lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
+  const int cin = d->c_in, cout = d->c_out, kh = d->kernel_h, kw = d->kernel_w;
+  const int ho = h->ho, wo = h->wo;
+  const int taps = kh * kw;
+  const int n_ck = cin / 64;
+  const int n_mt = (cout + 127) / 128;
+  const int rp = h->r2p;  // K of the dense part: R2, or R of the SVD pair
+  const int t_kc = rp < 64 ? rp : 64;
+  if (rp % t_kc) return LRS_OK;
+  const int n_tk = rp / t_kc;
+  const uint32_t sw_t = static_cast<uint32_t>(t_kc) * 2u;
+  const bool s1 = g.sh == 1 && g.sw == 1;
+  struct Unit { int col, n, xpos, tpos, r0, wo0, pitch, nw, rows; };
+  // MMA units covering a tile of th output rows x tc output columns (see lrs_wconv.cuh);
+  // wcw = window width, tbw = T window row pitch
+  auto make_units = [&](int th, int tc, int wcw, int tbw, std::vector<Unit>& us) -> int {
+    us.clear();
+    int col = 0;
+    if (s1 && wcw <= 32) {
+      const int rpu = std::max(1, 32 / wcw);
+      for (int r0 = 0; r0 < th; r0 += rpu) {
+        const int rows = std::min(rpu, th - r0);
+        const int npos = (rows - 1) * wcw + tc;
+        Unit u{col, round_up(8 * npos, 16), r0 * wcw, r0 * tbw, r0, 0, wcw, tc, rows};
+        us.push_back(u);
+        col += u.n;
+      }
+    } else {
+      const int nsplit = (tc + 31) / 32;
+      const int wsplit = (tc + nsplit - 1) / nsplit;
+      for (int r = 0; r < th; ++r)
+        for (int q = 0; q < nsplit; ++q) {
+          const int wo0 = q * wsplit, nw = std::min(wsplit, tc - wo0);
+          Unit u{col, round_up(8 * nw, 16), r * g.sh * wcw + wo0 * g.sw, r * tbw + wo0, r, wo0, nw, nw, 1};
+          us.push_back(u);
+          col += u.n;
+        }
+    }
+    return col;
+  };
+  std::vector<Unit> units, best_units;
+  int best_th = 0, best_ns = 0, best_tc = 0, best_wc = 0, best_tbw = 0;
+  long long best_cost = 1LL << 60;
+  uint32_t best_stride = 0, best_xw = 0, best_tw = 0, best_total = 0, best_acc = 0;
+  for (int cb = 1; cb <= 16 && !best_th; ++cb) {  // column bands: as few as fit
+    const int tc = (wo + cb - 1) / cb;
+    if (cb > 1 && (wo + tc - 1) / tc != cb) continue;
+    const int wcw = (tc - 1) * g.sw + kw;
+    const int tbw = s1 ? wcw : tc;
+    if (wcw > 256) continue;
+    for (int th = std::min(ho, 64); th >= 1; --th) {
+      const int acc = make_units(th, tc, wcw, tbw, units);
+      if (static_cast<int>(units.size()) > kWMaxUnits) continue;
+      const int wr = (th - 1) * g.sh + kh;
+      if (wr > 256) continue;
+      for (int ns = 4; ns >= 2; --ns) {
+        if (acc + 4 * ns > 512) continue;
+        const uint32_t xw = static_cast<uint32_t>(wr) * wcw * 1024u;
+        const uint32_t tw = static_cast<uint32_t>(th) * tbw * 8u * sw_t;
+        // slack: positions read past the end of a window by the last (padded) MMA rows
+        long long last_x = 0, last_t = 0;
+        for (const Unit& u : units) {
+          last_x = std::max<long long>(last_x, u.xpos + static_cast<long long>(kh - 1) * wcw + (kw - 1) +
+                                                   static_cast<long long>(u.n / 8 - 1) * g.sw);
+          last_t = std::max<long long>(last_t, u.tpos + u.n / 8 - 1);
+        }
+        const long long slack_x = std::max(0LL, last_x + 1 - static_cast<long long>(wr) * wcw) * 1024;
+        const long long slack_t = std::max(0LL, last_t + 1 - static_cast<long long>(th) * tbw) * 8 * sw_t;
+        const uint32_t stride =
+            align1024(static_cast<uint32_t>(std::max<long long>(xw + slack_x, tw + slack_t)));
+        const uint32_t total = 2 * stride + ns * (kASlotBytes + kESlotBytes) + 256 + 1024;
+        if (total > static_cast<uint32_t>(kMaxSmem)) continue;
+        // cost: MMA columns issued over the whole layer (waste of row bands and padding positions)
+        const long long cost = static_cast<long long>((ho + th - 1) / th) * acc * cb;
+        if (cost < best_cost) {
+          best_cost = cost;
+          best_th = th;
+          best_ns = ns;
+          best_tc = tc;
+          best_wc = wcw;
+          best_tbw = tbw;
+          best_stride = stride;
+          best_xw = xw;
+          best_tw = tw;
+          best_total = total;
+          best_acc = static_cast<uint32_t>(acc);
+          best_units = units;
+        }
+        break;
+      }
+    }
+  }
+  if (!best_th) return LRS_OK;
+  const int th = best_th;
+  const int wc = best_wc, tbox_w = best_tbw, tcols = best_tc;
+
+  // ---- S -> exact 2:4 main + residual blocks (bf16 values, RNE), TMEM metadata
+  const int nblk_main = n_mt * n_ck * taps;
+  std::vector<uint16_t> as(static_cast<size_t>(nblk_main) * 128 * 32, 0);
+  std::vector<uint32_t> ee(static_cast<size_t>(nblk_main) * 128 * 4, 0x44444444u);
+  std::vector<int> res_tab(nblk_main, -1);
+  int nres = 0;
+  std::vector<float> dense(static_cast<size_t>(n_ck) * taps * 64);
+  auto put = [&](int blk, int m, int grp, int i0, int i1, float v0, float v1) {
+    as[(static_cast<size_t>(blk) * 128 + m) * 32 + 2 * grp] = bf16_bits_rne(v0);
+    as[(static_cast<size_t>(blk) * 128 + m) * 32 + 2 * grp + 1] = bf16_bits_rne(v1);
+    const int st = grp / 8, gs = grp % 8;
+    const int lane = m % 8 + 8 * (gs / 4) + 16 * (m / 16);
+    const int nib = (gs % 4) + 4 * ((m / 8) % 2);
+    uint32_t& w = ee[(static_cast<size_t>(blk) * 128 + lane) * 4 + st];
+    w = (w & ~(0xFu << (4 * nib))) | (static_cast<uint32_t>(i0 | (i1 << 2)) << (4 * nib));
+  };
+  auto put_list = [&](int blk, int m, int grp, const int* idx, const float* val, int cnt) {
+    if (cnt == 0) return;  // block pre-filled with zeros and the (0,1) pattern
+    if (cnt == 1) {
+      if (idx[0] < 3) put(blk, m, grp, idx[0], idx[0] + 1, val[0], 0.f);
+      else put(blk, m, grp, 2, 3, 0.f, val[0]);
+    } else {
+      put(blk, m, grp, idx[0], idx[1], val[0], val[1]);
+    }
+  };
+  for (int j = 0; j < cout; ++j) {
+    const int64_t e0 = d->row_ptr[j], e1 = d->row_ptr[j + 1];
+    if (e0 == e1) continue;
+    std::fill(dense.begin(), dense.end(), 0.f);
+    for (int64_t e = e0; e < e1; ++e) {
+      const int col = d->col_idx[e];
+      const int ch = col / taps, t = col % taps;
+      dense[(static_cast<size_t>(ch / 64) * taps + t) * 64 + ch % 64] = d->values[e];
+    }
+    const int mt = j / 128, m = j % 128;
+    for (int c = 0; c < n_ck; ++c)
+      for (int t = 0; t < taps; ++t) {
+        const float* b = &dense[(static_cast<size_t>(c) * taps + t) * 64];
+        const int key = (mt * n_ck + c) * taps + t;
+        for (int grp = 0; grp < 16; ++grp) {
+          int idx[4];
+          float val[4];
+          int cnt = 0;
+          for (int i = 0; i < 4; ++i)
+            if (b[4 * grp + i] != 0.f) {
+              idx[cnt] = i;
+              val[cnt] = b[4 * grp + i];
+              ++cnt;
+            }
+          put_list(key, m, grp, idx, val, std::min(cnt, 2));
+          if (cnt > 2) {
+            if (res_tab[key] < 0) {
+              res_tab[key] = nblk_main + nres++;
+              as.resize(as.size() + 128 * 32, 0);
+              ee.resize(ee.size() + 128 * 4, 0x44444444u);
+            }
+            put_list(res_tab[key], m, grp, idx + 2, val + 2, cnt - 2);
+          }
+        }
+      }
+  }
+  h->w_main_blocks = nblk_main;
+  h->w_res_blocks = nres;
+  const int nblk = nblk_main + nres;
+  lrs_status st;
+  {
+    std::vector<uint8_t> b(as.size() * 2);
+    memcpy(b.data(), as.data(), b.size());
+    if ((st = upload(&h->w_as, b)) != LRS_OK) return st;
+    std::vector<uint8_t> e(ee.size() * 4);
+    memcpy(e.data(), ee.data(), e.size());
+    if ((st = upload(&h->w_e, e)) != LRS_OK) return st;
+    std::vector<uint8_t> r(res_tab.size() * 4);
+    memcpy(r.data(), res_tab.data(), r.size());
+    void* rp_ = nullptr;
+    if ((st = upload(&rp_, r)) != LRS_OK) return st;
+    h->w_res = static_cast<int*>(rp_);
+  }
+  WconvParams& w = h->wp;
+  memset(&w, 0, sizeof(w));
+  {
+    uint64_t dims[2] = {32, static_cast<uint64_t>(nblk) * 128};
+    uint64_t strides[1] = {64};
+    uint32_t box[2] = {32, 128};
+    uint32_t estr[2] = {1, 1};
+    if ((st = encode_t(&w.tmAs, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, h->w_as, dims, strides, box, estr, 64)) != LRS_OK)
+      return st;
+  }
+  {
+    uint64_t dims[2] = {4, static_cast<uint64_t>(nblk) * 128};
+    uint64_t strides[1] = {16};
+    uint32_t box[2] = {4, 128};
+    uint32_t estr[2] = {1, 1};
+    if ((st = encode_t(&w.tmE, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, h->w_e, dims, strides, box, estr, 0)) != LRS_OK)
+      return st;
+  }
+  {
+    uint64_t dims[2] = {static_cast<uint64_t>(rp), static_cast<uint64_t>(n_mt) * 128};
+    uint64_t strides[1] = {static_cast<uint64_t>(rp) * 2};
+    uint32_t box[2] = {static_cast<uint32_t>(t_kc), 128};
+    uint32_t estr[2] = {1, 1};
+    if ((st = encode_t(&w.tmAd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, h->w_uout, dims, strides, box, estr, sw_t)) !=
+        LRS_OK)
+      return st;
+  }
+  {
+    void* src = h->svd ? h->t1 : h->t2;
+    const uint64_t bm = static_cast<uint64_t>(d->batch_max);
+    uint64_t dims[4] = {static_cast<uint64_t>(rp), bm, static_cast<uint64_t>(wo), static_cast<uint64_t>(ho)};
+    uint64_t strides[3] = {static_cast<uint64_t>(ho) * wo * rp * 2, static_cast<uint64_t>(rp) * 2,
+                           static_cast<uint64_t>(wo) * rp * 2};
+    uint32_t box[4] = {static_cast<uint32_t>(t_kc), 8, static_cast<uint32_t>(tbox_w), static_cast<uint32_t>(th)};
+    uint32_t estr[4] = {1, 1, 1, 1};
+    if ((st = encode_t(&w.tmT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, src, dims, strides, box, estr, sw_t)) != LRS_OK)
+      return st;
+  }
+  w.res_block = h->w_res;
+  w.ho = ho;
+  w.wo = wo;
+  w.cout = cout;
+  w.kh = kh;
+  w.kw = kw;
+  w.sh = g.sh;
+  w.sw = g.sw;
+  w.ph = g.ph;
+  w.pw = g.pw;
+  w.th = th;
+  w.bands = (ho + th - 1) / th;
+  w.tcols = tcols;
+  w.cbands = (wo + tcols - 1) / tcols;
+  w.n_mt = n_mt;
+  w.n_units = static_cast<int>(best_units.size());
+  for (int i = 0; i < w.n_units; ++i) {
+    const Unit& u = best_units[i];
+    w.u_col[i] = u.col;
+    w.u_n[i] = u.n;
+    w.u_xpos[i] = u.xpos;
+    w.u_tpos[i] = u.tpos;
+    w.u_r0[i] = u.r0;
+    w.u_wo0[i] = u.wo0;
+    w.u_pitch[i] = u.pitch;
+    w.u_nw[i] = u.nw;
+    w.u_rows[i] = u.rows;
+  }
+  w.tbox_w = tbox_w;
+  w.n_ck = n_ck;
+  w.n_tk = n_tk;
+  w.t_kc = t_kc;
+  w.sw_t = sw_t;
+  w.wr = (th - 1) * g.sh + kh;
+  w.wc = wc;
+  w.x_win_bytes = best_xw;
+  w.t_win_bytes = best_tw;
+  w.win_stride = best_stride;
+  w.ns = best_ns;
+  const uint32_t acc = best_acc;
+  w.e_col0 = acc;
+  w.tmem_cols = pow2_cols(static_cast<int>(acc) + 4 * best_ns);
+  w.off_a = 2 * best_stride;
+  w.off_e = w.off_a + best_ns * kASlotBytes;
+  w.off_bar = w.off_e + best_ns * kESlotBytes;
+  h->w_smem = best_total;
+  h->use_w = true;
+  return LRS_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -346,10 +634,14 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   h->wo = (W + 2 * d->pad_w - kw) / d->stride_w + 1;
   const int ho = h->ho, wo = h->wo;
   const int r1 = d->rank_in, r2 = h->svd ? d->rank_in : d->rank_out;
-  h->r1p = round_up(r1, 16);
-  h->r2p = h->svd ? h->r1p : round_up(r2, 16);
+  // ranks padded to the MMA granularity; a rank consumed as the K of a TMEM-window
+  // operand (T2, or T1 of the SVD pair) is padded to 16, 32 or a multiple of 64
+  auto t_round = [](int r) { return r <= 16 ? 16 : (r <= 32 ? 32 : round_up(r, 64)); };
+  const bool bf16_w = !f32 && cin % 64 == 0;
+  h->r1p = (bf16_w && h->svd) ? t_round(r1) : round_up(r1, 16);
+  h->r2p = h->svd ? h->r1p : (bf16_w ? t_round(r2) : round_up(r2, 16));
   h->bn = cout <= 64 ? 64 : 128;
-  h->cout_p = round_up(cout, h->bn);
+  h->cout_p = bf16_w ? round_up(cout, 128) : round_up(cout, h->bn);
   const int r1p = h->r1p, r2p = h->r2p, bn = h->bn, cout_p = h->cout_p;
   const long long pin_max = static_cast<long long>(d->batch_max) * H * W;
   const long long p_max = static_cast<long long>(d->batch_max) * ho * wo;
@@ -456,7 +748,10 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     h->a2.kid = f32 ? K_STORE_F32 : K_STORE_BF16;
   }
   // ---------------------------------------------------------------- a3+a4+a5
-  {
+  if (bf16_w) {
+    if ((st = build_wconv(h, d, g)) != LRS_OK) return cleanup_fail(st);
+  }
+  if (!h->use_w) {
     GemmParams& p = h->a3.p;
     memset(&p, 0, sizeof(p));
     const int kdim = r2p;  // K of the expansion (R2, or R for the SVD pair)
@@ -562,6 +857,12 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     if (e != cudaSuccess)
       return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
+  {
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&lrs_wconv_kernel),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+    if (e != cudaSuccess)
+      return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
+  }
   cudaSetDevice(prev);
   *out = h;
   return LRS_OK;
@@ -608,6 +909,44 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
     if ((st = launch(h, 1, h->a2, dim3(tiles), stream)) != LRS_OK) return st;
   }
   // a3 + a4 + a5
+  if (h->use_w) {
+    WconvParams& w = h->wp;
+    if (h->wx_ptr != x || h->wx_n != n) {
+      uint64_t dims[4] = {static_cast<uint64_t>(d.c_in), static_cast<uint64_t>(n), static_cast<uint64_t>(d.in_w),
+                          static_cast<uint64_t>(d.in_h)};
+      uint64_t strides[3] = {static_cast<uint64_t>(d.in_h) * d.in_w * d.c_in * 2, static_cast<uint64_t>(d.c_in) * 2,
+                             static_cast<uint64_t>(d.in_w) * d.c_in * 2};
+      uint32_t box[4] = {64, 8, static_cast<uint32_t>(w.wc), static_cast<uint32_t>(w.wr)};
+      uint32_t estr[4] = {1, 1, 1, 1};
+      if ((st = encode_t(&w.tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box,
+                         estr, 128)) != LRS_OK)
+        return st;
+      h->wx_ptr = x;
+      h->wx_n = n;
+    }
+    w.n = n;
+    w.y = y;
+    const unsigned grid = static_cast<unsigned>(((n + 7) / 8) * w.bands * w.cbands * w.n_mt);
+    TimingRing& r = h->ring[2];
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->timing) {
+      if (r.used + 2 > static_cast<int>(r.ev.size())) {
+        const size_t old = r.ev.size();
+        r.ev.resize(old + 512);
+        for (size_t i = old; i < r.ev.size(); ++i) LRS_CUDA(cudaEventCreate(&r.ev[i]));
+      }
+      e0 = r.ev[r.used];
+      e1 = r.ev[r.used + 1];
+      r.used += 2;
+      LRS_CUDA(cudaEventRecord(e0, stream));
+    }
+    void* args[] = {&w};
+    LRS_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(&lrs_wconv_kernel), dim3(grid), dim3(kWThreads), args,
+                              h->w_smem, stream));
+    if (h->timing) LRS_CUDA(cudaEventRecord(e1, stream));
+    if (prev != h->device) cudaSetDevice(prev);
+    return LRS_OK;
+  }
   h->a3.p.m_total = static_cast<int>(P);
   h->a3.p.g.n = n;
   h->a3.p.sp.x = x;
@@ -647,7 +986,8 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
-  void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy};
+  void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
+                  h->w_as, h->w_e, h->w_res};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto& r : h->ring)
@@ -703,6 +1043,19 @@ const char* lrs_conv_stage_name(const lrs_conv* h, int32_t stage) {
   (void)h;
   static const char* names[] = {"a1_proj", "a2_core", "a345_expand_sparse"};
   return (stage >= 0 && stage < 3) ? names[stage] : "";
+}
+
+int32_t lrs_conv_sparse_engine(const lrs_conv* h, int32_t* main_blocks, int32_t* residual_blocks) {
+  if (!h) return -1;
+  if (main_blocks) *main_blocks = h->use_w ? h->w_main_blocks : 0;
+  if (residual_blocks) *residual_blocks = h->use_w ? h->w_res_blocks : 0;
+  return h->use_w ? 1 : 0;
+}
+
+lrs_status lrs_conv_debug_trace(lrs_conv* h, void* dev_buf) {
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  h->wp.trace = static_cast<unsigned long long*>(dev_buf);
+  return LRS_OK;
 }
 
 lrs_status lrs_conv_debug_buffer(const lrs_conv* h, int32_t which, const void** ptr, int32_t* ld) {

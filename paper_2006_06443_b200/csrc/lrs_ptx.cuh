@@ -149,10 +149,58 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sw_bytes)
   d |= layout << 61;
   return d;
 }
+// Same, with an explicit stride between 8-row core-matrix groups (SBO, bytes):
+// used for the windowed B operand, whose 8-row groups are output positions.
+__device__ __forceinline__ uint64_t umma_desc_sbo(uint32_t saddr, uint32_t sw_bytes, uint32_t sbo) {
+  const uint64_t layout = sw_bytes == 128 ? 2ull : (sw_bytes == 64 ? 4ull : 6ull);
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  d |= layout << 61;
+  return d;
+}
+// No-swizzle descriptor of a [128 rows][16 B] row-major block (tcgen05.cp source).
+__device__ __forceinline__ uint64_t umma_desc_rows16(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(128u >> 4) << 16;
+  d |= static_cast<uint64_t>(128u >> 4) << 32;
+  d |= 1ull << 46;
+  return d;
+}
+// 2:4 sparse MMA (A sparse along K, compressed in smem; metadata in TMEM at e_tmem).
+// Measured layout (tools/sp_mma_probe3/4, profiles/r01_sp_mma_probe*): logical
+// K step s (32 elements) of row m, group gs = 0..7 of the step -> TMEM column s,
+// lane m%8 + 8*(gs/4) + 16*(m/16), nibble (gs%4) + 4*((m/8)%2), nibble = i0 | i1 << 2;
+// the instruction addresses column (s & ~1) with sparsity selector s & 1 (idesc bits 0-1).
+__device__ __forceinline__ void mma_sp_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate, uint32_t e_tmem) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%5], %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(e_tmem)
+      : "memory");
+}
+// smem [128 lanes][16 B] -> TMEM 4 columns x 128 lanes
+__device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
 // Instruction descriptor: f32 accumulate, K-major A and B, M = 128.
 // ab_fmt: 1 = bf16 (kind::f16), 2 = tf32 (kind::tf32).
 __host__ __device__ __forceinline__ uint32_t umma_idesc(uint32_t ab_fmt, uint32_t n, uint32_t m) {
   return (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
+
+// one lane of the (fully active) warp returns true
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n}"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {

@@ -1,0 +1,323 @@
+// lrs_wconv.cuh -- the fused a3 + a4 + a5 kernel on the sm_100a tensor cores:
+//
+//   Y[n, ho, wo, j] = sum_b T2[n, ho, wo, b] U_out[b, j]                          (a3)
+//                   + sum_{c, y, x} S[j, c, y, x] X[n, ho*s + y - p, wo*s + x - p, c]  (a4)
+//
+// computed transposed, D[j, (ho, wo, n)] in TMEM (M = 128 output channels per
+// CTA, TMEM lane = channel), and written to Y once (a5).
+//
+// * The sparse term S runs on the 2:4 sparse tensor-core MMA
+//   (tcgen05.mma.sp, kind::f16): at create time every group of 4 consecutive
+//   input channels of a (row j, tap) is split into a "main" 2:4 block (its
+//   first two nonzeros) and, only where a group holds 3-4 nonzeros, a
+//   "residual" 2:4 block; both are exact, so S = S_main + S_res bit for bit.
+// * The activation operand B is a shared-memory WINDOW of X per 64-channel
+//   chunk, loaded by one TMA box {64 ch, 8 images, window cols, window rows}
+//   straight from NHWC X (out-of-bounds = zero padding).  Its 8-row core
+//   matrices are the 8 images of one spatial position, so the im2col operand
+//   of every kernel tap (y, x) is the same window at a different start
+//   address -- the window is loaded once and reused by all k*k taps.
+//   Stride s is the descriptor's SBO (s KB between output positions).
+// * The dense part (a3) uses the same machinery with a window of T2 (or T1
+//   for the SVD pair) at the output positions and U_out^T as A.
+//
+// Tile: 8 images x th output rows x all output columns x 128 channels.
+// The tile's outputs are covered by up to kWMaxUnits MMA "units", each one
+// N range (<= 256 columns = 8 images x <= 32 positions) with its accumulator
+// side by side in TMEM.  At stride 1 a unit spans several output rows: its
+// positions run along the window rows with the window width as pitch, so one
+// MMA covers rows * window_width positions (the window's padding columns are
+// computed and discarded) -- few, wide MMAs, because every MMA re-reads its A
+// block from shared memory and has a fixed issue cost.  At stride 2 a unit
+// is (part of) one output row.
+//
+// Warps: 0 = TMA producer, 1 = TMEM allocator + MMA issuer, 2..5 = epilogue
+// (warp w drains TMEM lanes 32*(w%4) ..).
+#pragma once
+#include "lrs_ptx.cuh"
+
+namespace lrs {
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr int kWThreads = 192;
+constexpr int kWMaxSlots = 6;
+constexpr int kWMaxUnits = 8;
+constexpr uint32_t kASlotBytes = 16384;  // dense A box 128 x 128 B, or sparse 128 x 64 B
+constexpr uint32_t kESlotBytes = 2048;   // metadata 128 lanes x 16 B
+
+struct WconvParams {
+  CUtensorMap tmX;   // X   4-D (C, N, W, H) bf16, box {64, 8, wc, wr}, SW128
+  CUtensorMap tmT;   // T   4-D (R, N, Wo, Ho) bf16, box {t_kc, 8, wo, th}, swizzle sw_t
+  CUtensorMap tmAd;  // U_out^T [n_mt*128][R_p] bf16, box {t_kc, 128}, swizzle sw_t
+  CUtensorMap tmAs;  // compressed S blocks [blocks*128][32] bf16, box {32, 128}, SW64
+  CUtensorMap tmE;   // metadata blocks [blocks*128][4] u32, box {4, 128}
+  const int* res_block;  // [n_mt][n_ck][taps] residual block index or -1
+  void* y;
+  int n, ho, wo, cout;
+  int kh, kw, sh, sw, ph, pw;
+  int th, bands, n_mt;
+  int tcols, cbands;       // output columns per tile, column bands
+  int n_units;
+  int u_col[kWMaxUnits];   // first TMEM column
+  int u_n[kWMaxUnits];     // MMA N (multiple of 16)
+  int u_xpos[kWMaxUnits];  // X window position of the unit's first output at tap (0, 0)
+  int u_tpos[kWMaxUnits];  // T window position of the unit's first output
+  int u_r0[kWMaxUnits];    // first output row (tile-relative)
+  int u_wo0[kWMaxUnits];   // first output column
+  int u_pitch[kWMaxUnits]; // columns/8 per output row inside the unit
+  int u_nw[kWMaxUnits];    // real output columns per row
+  int u_rows[kWMaxUnits];  // output rows covered
+  int tbox_w;              // width of the T window box (its row pitch)
+  unsigned long long* trace;  // optional: per-event globaltimer stamps of CTA 0 (debug)
+  int n_ck, n_tk, t_kc;
+  uint32_t sw_t;        // bytes per T window row (t_kc * 2) = its swizzle width
+  int wr, wc;
+  uint32_t x_win_bytes, t_win_bytes, win_stride;
+  int ns;
+  uint32_t e_col0, tmem_cols;
+  uint32_t off_a, off_e, off_bar;
+};
+
+__global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_constant__ WconvParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  uint64_t* win_full = bars;
+  uint64_t* win_empty = bars + 2;
+  uint64_t* a_full = bars + 4;
+  uint64_t* a_empty = bars + 4 + kWMaxSlots;
+  uint64_t* acc_full = bars + 4 + 2 * kWMaxSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 + 2 * kWMaxSlots);
+
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[1004] = gtimer();
+  int bid = blockIdx.x;
+  const int mt = bid % p.n_mt;
+  bid /= p.n_mt;
+  const int cband = bid % p.cbands;
+  bid /= p.cbands;
+  const int band = bid % p.bands;
+  const int grp = bid / p.bands;
+  const int n0 = grp * 8, ho0 = band * p.th, j0 = mt * 128, wo0t = cband * p.tcols;
+  const int taps = p.kh * p.kw;
+  const int nwin = p.n_tk + p.n_ck;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&win_full[i], 1);
+      mbar_init(&win_empty[i], 1);
+    }
+    for (int i = 0; i < p.ns; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&p.tmX);
+    tma_prefetch_desc(&p.tmT);
+    tma_prefetch_desc(&p.tmAd);
+    tma_prefetch_desc(&p.tmAs);
+    tma_prefetch_desc(&p.tmE);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[1003] = gtimer();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      int it = 0;
+      for (int w = 0; w < nwin; ++w) {
+        const int buf = w & 1;
+        if (w >= 2) mbar_wait(&win_empty[buf], ((w >> 1) - 1) & 1);
+        uint8_t* wdst = smem + buf * p.win_stride;
+        if (w < p.n_tk) {
+          mbar_arrive_expect_tx(&win_full[buf], p.t_win_bytes);
+          tma_load_4d(wdst, &p.tmT, &win_full[buf], w * p.t_kc, n0, wo0t, ho0);
+          const int slot = it % p.ns;
+          if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
+          mbar_arrive_expect_tx(&a_full[slot], 128u * p.sw_t);
+          tma_load_2d(smem + p.off_a + slot * kASlotBytes, &p.tmAd, &a_full[slot], w * p.t_kc, j0);
+          ++it;
+        } else {
+          const int c = w - p.n_tk;
+          mbar_arrive_expect_tx(&win_full[buf], p.x_win_bytes);
+          tma_load_4d(wdst, &p.tmX, &win_full[buf], c * 64, n0, wo0t * p.sw - p.pw, ho0 * p.sh - p.ph);
+          const int* rb = p.res_block + (mt * p.n_ck + c) * taps;
+          int rblk[9];
+#pragma unroll
+          for (int t = 0; t < 9; ++t) rblk[t] = t < taps ? __ldg(rb + t) : -1;
+          for (int t = 0; t < taps; ++t) {
+            for (int part = 0; part < 2; ++part) {
+              const int key = (mt * p.n_ck + c) * taps + t;
+              int blk = key;
+              if (part == 1) {
+                blk = -1;
+#pragma unroll
+                for (int q = 0; q < 9; ++q)
+                  if (q == t) blk = rblk[q];
+                if (taps > 9) blk = __ldg(rb + t);
+              }
+              if (blk < 0) continue;
+              const int slot = it % p.ns;
+              if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
+              mbar_arrive_expect_tx(&a_full[slot], 8192u + kESlotBytes);
+              tma_load_2d(smem + p.off_a + slot * kASlotBytes, &p.tmAs, &a_full[slot], 0, blk * 128);
+              tma_load_2d(smem + p.off_e + slot * kESlotBytes, &p.tmE, &a_full[slot], 0, blk * 128);
+              ++it;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    {
+      // ------------------------------------------------------------ MMA issuer
+      // The whole warp walks the loop (so the per-unit values stay warp-uniform
+      // and live in uniform registers); one elected lane issues each tcgen05 op.
+      // Descriptors are linear in the start address (14-bit field of addr>>4),
+      // so every per-unit descriptor is precomputed once and the inner loop
+      // only adds byte offsets >> 4: the single-thread issue loop stays short.
+      const uint32_t win0 = smem_u32(smem);
+      const uint32_t t_pos = 8u * p.sw_t;  // bytes per output position in a T window
+      const uint32_t x_sbo = 1024u * static_cast<uint32_t>(p.sw);
+      const int nu = p.n_units;
+      uint32_t dcol[kWMaxUnits], idu[kWMaxUnits];
+      uint64_t bxd[kWMaxUnits], btd[kWMaxUnits];
+#pragma unroll
+      for (int u = 0; u < kWMaxUnits; ++u) {
+        if (u < nu) {
+          dcol[u] = tmem + static_cast<uint32_t>(p.u_col[u]);
+          idu[u] = umma_idesc(1u, static_cast<uint32_t>(p.u_n[u]), 128u);
+          bxd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_xpos[u]) * 1024u, 128, x_sbo);
+          btd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_tpos[u]) * t_pos, p.sw_t, t_pos);
+        }
+      }
+      const uint64_t ad_dense = umma_desc(smem_u32(smem + p.off_a), p.sw_t);
+      const uint64_t ad_sp = umma_desc(smem_u32(smem + p.off_a), 64);
+      const uint64_t ed0 = umma_desc_rows16(smem_u32(smem + p.off_e));
+      const uint32_t slot_a16 = kASlotBytes >> 4, slot_e16 = kESlotBytes >> 4;
+      const uint32_t win16 = p.win_stride >> 4;
+      const int ksteps = static_cast<int>(p.sw_t / 32);
+      int it = 0, slot = 0;
+      uint32_t ph = 0;
+      for (int w = 0; w < nwin; ++w) {
+        const int buf = w & 1;
+        mbar_wait(&win_full[buf], (w >> 1) & 1);
+        tc_fence_after();
+        const uint32_t boff = buf ? win16 : 0u;
+        if (w < p.n_tk) {
+          mbar_wait(&a_full[slot], ph);
+          tc_fence_after();
+          const uint64_t ab = ad_dense + slot * slot_a16;
+#pragma unroll
+          if (elect_one()) {
+#pragma unroll
+            for (int u = 0; u < kWMaxUnits; ++u) {
+              if (u < nu) {
+                for (int k = 0; k < ksteps; ++k)
+                  mma_bf16(dcol[u], ab + 2 * k, btd[u] + boff + 2 * k, idu[u], (w > 0 || k > 0) ? 1u : 0u);
+              }
+            }
+            mma_commit(&a_empty[slot]);
+          }
+          __syncwarp();
+          ++it;
+          if (++slot == p.ns) { slot = 0; ph ^= 1u; }
+        } else {
+          const int c = w - p.n_tk;
+          const int* rb = p.res_block + (mt * p.n_ck + c) * taps;
+          uint32_t resmask = 0;
+          for (int t = 0; t < taps; ++t) resmask |= (__ldg(rb + t) >= 0 ? 1u : 0u) << t;
+          for (int t = 0; t < taps; ++t) {
+            const int ty = t / p.kw, tx = t - ty * p.kw;
+            const uint32_t tap16 = static_cast<uint32_t>(ty * p.wc + tx) * 64u;  // (pos * 1024) >> 4
+            const int nparts = 1 + static_cast<int>((resmask >> t) & 1u);
+            for (int part = 0; part < nparts; ++part) {
+              const unsigned long long tw0 = p.trace ? gtimer() : 0ull;
+              mbar_wait(&a_full[slot], ph);
+              tc_fence_after();
+              if (p.trace && blockIdx.x == 0 && it < 500 && lane == 0) {
+                p.trace[2 * it] = tw0;
+                p.trace[2 * it + 1] = gtimer();
+              }
+              const uint32_t et = tmem + p.e_col0 + 4u * slot;
+              const uint64_t ab = ad_sp + slot * slot_a16;
+              if (elect_one()) {
+                tmem_cp_128x128b(et, ed0 + slot * slot_e16);
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+#pragma unroll
+                  for (int u = 0; u < kWMaxUnits; ++u) {
+                    if (u < nu)
+                      mma_sp_bf16(dcol[u], ab + 2 * s2, bxd[u] + boff + tap16 + 4 * s2,
+                                  idu[u] | (1u << 2) | static_cast<uint32_t>(s2), 1u, et);
+                  }
+                }
+                mma_commit(&a_empty[slot]);
+              }
+              __syncwarp();
+              ++it;
+              if (++slot == p.ns) { slot = 0; ph ^= 1u; }
+            }
+          }
+        }
+        if (elect_one()) mma_commit(&win_empty[buf]);
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit(acc_full);
+      __syncwarp();
+      if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[1000] = gtimer();
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue
+    const int q4 = warp & 3;
+    const int j = j0 + q4 * 32 + lane;
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    if (p.trace && blockIdx.x == 0 && threadIdx.x == 64) p.trace[1001] = gtimer();
+    __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(p.y);
+    for (int u = 0; u < p.n_units; ++u) {
+      const int pitch = p.u_pitch[u], nw = p.u_nw[u];
+      for (int cb = 0; cb < p.u_n[u] / 16; ++cb) {
+        float v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + static_cast<uint32_t>(p.u_col[u] + cb * 16), v);
+        if (j >= p.cout) continue;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const int qv = cb * 2 + half;  // virtual position inside the unit
+          const int rr = qv / pitch, cc = qv - rr * pitch;
+          const int ho = ho0 + p.u_r0[u] + rr, wo = wo0t + p.u_wo0[u] + cc;
+          if (cc >= nw || rr >= p.u_rows[u] || ho >= p.ho || wo >= p.wo) continue;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int n = n0 + i;
+            if (n < p.n)
+              y[((static_cast<long long>(n) * p.ho + ho) * p.wo + wo) * p.cout + j] = __float2bfloat16_rn(v[half * 8 + i]);
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[1002] = gtimer();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem, p.tmem_cols);
+  }
+}
+
+}  // namespace lrs

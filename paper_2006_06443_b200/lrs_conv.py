@@ -25,7 +25,7 @@ STATUS_NAMES = {0: "LRS_OK", 1: "LRS_ERR_INVALID_ARGUMENT", 2: "LRS_ERR_UNSUPPOR
 EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
             "lrs_conv_last_error", "lrs_conv_output_shape", "lrs_conv_launches_per_forward",
             "lrs_conv_set_timing", "lrs_conv_stage_times", "lrs_conv_stage_name",
-            "lrs_conv_debug_buffer")
+            "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine")
 
 
 class LrsError(RuntimeError):
@@ -78,9 +78,12 @@ def load_library(path: str = LIB_PATH):
     lib.lrs_conv_stage_name.argtypes = [P, ctypes.c_int32]
     lib.lrs_conv_stage_name.restype = ctypes.c_char_p
     lib.lrs_conv_debug_buffer.argtypes = [P, ctypes.c_int32, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_int32)]
-    for name in ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
+    lib.lrs_conv_debug_trace.argtypes = [P, P]
+    lib.lrs_conv_sparse_engine.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+    lib.lrs_conv_sparse_engine.restype = ctypes.c_int32
+    for name in ("lrs_conv_debug_trace", "lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
                  "lrs_conv_output_shape", "lrs_conv_set_timing", "lrs_conv_stage_times",
-                 "lrs_conv_debug_buffer"):
+                 "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -179,6 +182,14 @@ class LrsConv:
     @property
     def launches_per_forward(self) -> int:
         return load_library().lrs_conv_launches_per_forward(self.handle)
+
+    @property
+    def sparse_engine(self):
+        """(engine, main_blocks, residual_blocks): engine 1 = 2:4 sparse tensor
+        cores, 0 = SIMT CSR epilogue (see include/lrs_conv.h)."""
+        m, r = ctypes.c_int32(), ctypes.c_int32()
+        e = load_library().lrs_conv_sparse_engine(self.handle, ctypes.byref(m), ctypes.byref(r))
+        return int(e), int(m.value), int(r.value)
 
     def forward_into(self, x, y, stream=None) -> None:
         torch = self.torch

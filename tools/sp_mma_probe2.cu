@@ -22,14 +22,6 @@ using namespace lrs;
 constexpr int M = 128, N = 64, KL = 64, KC = KL / 2;  // logical / stored K
 constexpr int ECOLS = 16;                              // metadata columns written per lane
 
-__device__ __forceinline__ void mma_sp_bf16(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc,
-                                            uint32_t e) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%5], %3, p;\n}" ::"r"(d),
-      "l"(ad), "l"(bd), "r"(idesc), "r"(acc), "r"(e)
-      : "memory");
-}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),

@@ -1,4 +1,4 @@
-// sp_mma_probe4.cu -- verify (tcgen05.cp E path)  the TMEM metadata layout of the sm_100a 2:4
+// sp_mma_probe5.cu -- sparse MMA with A in TMEM (tcgen05.mma.sp [a_tmem])  the TMEM metadata layout of the sm_100a 2:4
 // sparse tensor-core MMA (tcgen05.mma.sp.cta_group::1.kind::f16, bf16 in, fp32
 // accumulate, M = 128, N = 64, K = 64 logical = 2 MMAs of K = 32).
 // Metadata words are written straight into TMEM with tcgen05.st (each thread
@@ -22,6 +22,21 @@ using namespace lrs;
 constexpr int M = 128, N = 64, KL = 128, KC = KL / 2;  // logical / stored K
 constexpr int ECOLS = 16;                              // metadata columns written per lane
 
+__device__ __forceinline__ void mma_sp_ts(uint32_t d, uint32_t a_tmem, uint64_t bd, uint32_t idesc, uint32_t acc,
+                                          uint32_t e) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%5], %3, p;\n}" ::"r"(d),
+      "r"(a_tmem), "l"(bd), "r"(idesc), "r"(acc), "r"(e)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ts_dense(uint32_t d, uint32_t a_tmem, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+      "r"(a_tmem), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
@@ -95,7 +110,9 @@ __global__ void probe(const __nv_bfloat16* ac, const __nv_bfloat16* b, const uin
                              ((N >> 3) << 17) | ((M >> 4) << 24);
       const uint64_t ad = umma_desc(smem_u32(sa) + (s / 2) * 8192 + (s % 2) * 32, 64);
       const uint64_t bd = umma_desc(smem_u32(sb) + (s / 2) * 8192 + (s % 2) * 64, 128);
-      mma_sp_bf16(tm, ad, bd, idesc, s > 0 ? 1u : 0u, tm_e + e_addr0 * (s / 2));
+      if (e_addr1 == 6 || e_addr1 == 7) mma_sp_ts(tm, tm + 72 + 8 * s, bd, idesc, s > 0 ? 1u : 0u, tm_e + 2 * (s / 2));
+      else mma_sp_bf16(tm, ad, bd, idesc, s > 0 ? 1u : 0u, tm_e + e_addr0 * (s / 2));
+      (void)ad;
     }
     mma_commit(&bar);
   }

@@ -17,8 +17,10 @@ Recipe (SURVEY.md §8(c) readings #7-#11):
   * S: nnz = round(d * Cout*Cin*k*k) positions drawn uniformly without
     replacement over the OIHW linear index, sorted; values N(0, 0.1)
     (variance 0.1); CSR by output channel with col = (c*k + y)*k + x;
-  * fp64 draws -> fp32 (RNE); bf16 configs additionally round X and the
-    factors to bf16 (RNE).  S values stay fp32 for both dtypes.
+  * fp64 draws -> fp32 (RNE); bf16 configs additionally round X, the
+    factors and the S values to bf16 (RNE) -- "bf16 with fp32 accumulate"
+    (BASELINE.json configs 2-5) read as every operand in bf16, DESIGN.md
+    reading #12.  The fp32 configs keep fp32 S values.
 
 The arrays returned are exactly what both sides consume: the GPU gets the
 fp32/bf16 bits, the oracle gets the same values widened to fp64.
@@ -155,7 +157,7 @@ def generate(cfg: LayerConfig, batch: Optional[int] = None, seed: Optional[int] 
         u_out=_store(u_out, cfg.dtype),
         row_ptr=row_ptr,
         col_idx=cols.astype(np.int32),
-        values=vals.astype(np.float32),
+        values=_store(vals, cfg.dtype),
     )
 
 
