@@ -132,6 +132,7 @@ struct TimingRing {
 struct lrs_conv {
   lrs_conv_desc d;
   int device = 0;
+  int sms = 148;
   bool f32 = false, svd = false;
   int esz = 2;
   int ho = 0, wo = 0;
@@ -167,6 +168,8 @@ struct lrs_conv {
   int* w_res = nullptr;   // residual block table
   const void* wx_ptr = nullptr;
   int wx_n = -1;
+  const void* wy_ptr = nullptr;
+  int wy_n = -1;
   int w_main_blocks = 0, w_res_blocks = 0;
 };
 
@@ -401,8 +404,16 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
             align1024(static_cast<uint32_t>(std::max<long long>(xw + slack_x, tw + slack_t)));
         const uint32_t total = 2 * stride + ns * (kASlotBytes + kESlotBytes) + 256 + 1024;
         if (total > static_cast<uint32_t>(kMaxSmem)) continue;
-        // cost: MMA columns issued over the whole layer (waste of row bands and padding positions)
-        const long long cost = static_cast<long long>((ho + th - 1) / th) * acc * cb;
+        if (8u * th * tc * 256u > 2 * stride) continue;  // epilogue staging tile reuses the windows
+        // cost model (cycles, measured with tools/mma_rate2 and tools/wtrace on B200): a
+        // sparse MMA costs max(~100 issue, (A 4 KB + B N*64 B) / 128 B/clk smem), an item
+        // (one tap of a 64-channel chunk: 2 MMA steps per unit) adds ~200; CTAs run in
+        // waves of one per SM.
+        long long item = 200;
+        for (const Unit& u : units) item += 2 * std::max<long long>(100, (4096 + 64LL * u.n) / 128);
+        const long long ctas = static_cast<long long>((d->batch_max + 7) / 8) * ((ho + th - 1) / th) * cb * n_mt;
+        const long long waves = (ctas + h->sms - 1) / h->sms;
+        const long long cost = waves * item;
         if (cost < best_cost) {
           best_cost = cost;
           best_th = th;
@@ -582,7 +593,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   w.ns = best_ns;
   const uint32_t acc = best_acc;
   w.e_col0 = acc;
-  w.tmem_cols = pow2_cols(static_cast<int>(acc) + 4 * best_ns);
+  w.tmem_cols = 512;  // whole TMEM: base address 0 (lrs_wconv_kernel relies on it)
   w.off_a = 2 * best_stride;
   w.off_e = w.off_a + best_ns * kASlotBytes;
   w.off_bar = w.off_e + best_ns * kESlotBytes;
@@ -623,6 +634,7 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   h->d.col_idx = nullptr;
   h->d.values = nullptr;
   h->device = device;
+  h->sms = prop.multiProcessorCount;
   h->f32 = d->dtype == LRS_DTYPE_F32;
   h->svd = d->core == nullptr;
   h->esz = h->f32 ? 4 : 2;
@@ -923,6 +935,18 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
         return st;
       h->wx_ptr = x;
       h->wx_n = n;
+    }
+    if (h->wy_ptr != y || h->wy_n != n) {
+      uint64_t dims[4] = {static_cast<uint64_t>(d.c_out), static_cast<uint64_t>(h->wo), static_cast<uint64_t>(h->ho),
+                          static_cast<uint64_t>(n)};
+      uint64_t strides[3] = {static_cast<uint64_t>(d.c_out) * 2, static_cast<uint64_t>(h->wo) * d.c_out * 2,
+                             static_cast<uint64_t>(h->ho) * h->wo * d.c_out * 2};
+      uint32_t box[4] = {128, static_cast<uint32_t>(w.tcols), static_cast<uint32_t>(w.th), 8};
+      uint32_t estr[4] = {1, 1, 1, 1};
+      if ((st = encode_t(&w.tmY, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, y, dims, strides, box, estr, 0)) != LRS_OK)
+        return st;
+      h->wy_ptr = y;
+      h->wy_n = n;
     }
     w.n = n;
     w.y = y;

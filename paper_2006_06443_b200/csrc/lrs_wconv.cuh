@@ -31,8 +31,8 @@
 // block from shared memory and has a fixed issue cost.  At stride 2 a unit
 // is (part of) one output row.
 //
-// Warps: 0 = TMA producer, 1 = TMEM allocator + MMA issuer, 2..5 = epilogue
-// (warp w drains TMEM lanes 32*(w%4) ..).
+// Warps: 0 = TMA producer, 1 = TMEM allocator + MMA issuer, 2..9 = epilogue
+// (warp w drains TMEM lanes 32*(w%4) .., the two warps of a quarter split the columns).
 #pragma once
 #include "lrs_ptx.cuh"
 
@@ -44,7 +44,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-constexpr int kWThreads = 192;
+constexpr int kWThreads = 320;  // warps 0 producer, 1 MMA, 2..9 epilogue (2 per TMEM lane quarter)
 constexpr int kWMaxSlots = 6;
 constexpr int kWMaxUnits = 8;
 constexpr uint32_t kASlotBytes = 16384;  // dense A box 128 x 128 B, or sparse 128 x 64 B
@@ -56,6 +56,7 @@ struct WconvParams {
   CUtensorMap tmAd;  // U_out^T [n_mt*128][R_p] bf16, box {t_kc, 128}, swizzle sw_t
   CUtensorMap tmAs;  // compressed S blocks [blocks*128][32] bf16, box {32, 128}, SW64
   CUtensorMap tmE;   // metadata blocks [blocks*128][4] u32, box {4, 128}
+  CUtensorMap tmY;   // Y   4-D (Cout, Wo, Ho, N) bf16, box {128, tcols, th, 8}, no swizzle (TMA store)
   const int* res_block;  // [n_mt][n_ck][taps] residual block index or -1
   void* y;
   int n, ho, wo, cout;
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 + 2 * kWMaxSlots);
 
   if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[1004] = gtimer();
+  if (p.trace && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
   int bid = blockIdx.x;
   const int mt = bid % p.n_mt;
   bid /= p.n_mt;
@@ -130,7 +132,14 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // The CTA owns the whole TMEM of its SM (tmem_cols = 512, one CTA per SM), so
+  // the allocation starts at lane 0 / column 0.  Using the literal 0 keeps every
+  // TMEM address compile-time uniform (uniform registers in the MMA loop).
+  if (threadIdx.x == 32 && *tmem_slot != 0u) {
+    printf("lrs_wconv: unexpected TMEM base %u\n", *tmem_slot);
+    __trap();
+  }
+  constexpr uint32_t tmem = 0u;
   if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[1003] = gtimer();
 
   if (warp == 0) {
@@ -282,37 +291,66 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   } else {
     // -------------------------------------------------------------- epilogue
     const int q4 = warp & 3;
-    const int j = j0 + q4 * 32 + lane;
-    mbar_wait(acc_full, 0);
+    mbar_wait_sleep(acc_full, 0);
     tc_fence_after();
     if (p.trace && blockIdx.x == 0 && threadIdx.x == 64) p.trace[1001] = gtimer();
-    __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(p.y);
+    if (p.trace && threadIdx.x == 64 && blockIdx.x < 2048) p.trace[8200 + blockIdx.x] = gtimer();
+    // TMEM -> bf16 staging tile [8 images][th][tcols][128 ch] in the (now idle) window
+    // buffers, then one TMA tensor store (clips rows/cols/images/channels out of range).
+    // Columns go in chunks of 32 (4 virtual positions x 8 images); the two warps of a
+    // lane quarter take alternate chunks.
+    const uint32_t stage = smem_u32(smem);
+    const uint32_t img_stride = static_cast<uint32_t>(p.th * p.tcols) * 256u;  // bytes per image plane
+    const int jl = q4 * 32 + lane;
+    const int ehalf = (warp - 2) >> 2;
     for (int u = 0; u < p.n_units; ++u) {
-      const int pitch = p.u_pitch[u], nw = p.u_nw[u];
-      for (int cb = 0; cb < p.u_n[u] / 16; ++cb) {
-        float v[16];
-        tmem_ld16(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + static_cast<uint32_t>(p.u_col[u] + cb * 16), v);
-        if (j >= p.cout) continue;
+      const int pitch = p.u_pitch[u], nw = p.u_nw[u], un = p.u_n[u], rows = p.u_rows[u];
+      const int r0 = p.u_r0[u], w0 = p.u_wo0[u], ucol = p.u_col[u];
+      int rr = 0, cc = ehalf * 4;  // virtual position (row, col) of this warp's first chunk
+      while (cc >= pitch) { cc -= pitch; ++rr; }
+      for (int c0 = ehalf * 32; c0 < un; c0 += 64) {
+        uint32_t v[32];
+        tmem_ld32_nowait(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + static_cast<uint32_t>(ucol + c0), v);
+        tmem_ld_wait();
+        int r = rr, c = cc;
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          const int qv = cb * 2 + half;  // virtual position inside the unit
-          const int rr = qv / pitch, cc = qv - rr * pitch;
-          const int ho = ho0 + p.u_r0[u] + rr, wo = wo0t + p.u_wo0[u] + cc;
-          if (cc >= nw || rr >= p.u_rows[u] || ho >= p.ho || wo >= p.wo) continue;
+        for (int qq = 0; qq < 4; ++qq) {
+          if (c0 + qq * 8 < un && c < nw && r < rows) {
+            const uint32_t a0 = stage + (static_cast<uint32_t>((r0 + r) * p.tcols + w0 + c) * 128u + jl) * 2u;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int n = n0 + i;
-            if (n < p.n)
-              y[((static_cast<long long>(n) * p.ho + ho) * p.wo + wo) * p.cout + j] = __float2bfloat16_rn(v[half * 8 + i]);
+            for (int i = 0; i < 8; ++i) {
+              const __nv_bfloat16 b = __float2bfloat16_rn(__uint_as_float(v[qq * 8 + i]));
+              sts_u16(a0 + i * img_stride, *reinterpret_cast<const uint16_t*>(&b));
+            }
           }
+          if (++c == pitch) { c = 0; ++r; }
         }
+        // advance 8 virtual positions (this warp's next chunk)
+        cc += 8;
+        while (cc >= pitch) { cc -= pitch; ++rr; }
       }
+    }
+    if (p.trace && blockIdx.x == 0 && threadIdx.x == 64) p.trace[1005] = gtimer();
+    fence_proxy_async_smem();
+    named_bar_sync(1, 256);
+    if (threadIdx.x == 64) {
+      if (p.trace && blockIdx.x == 0) p.trace[1006] = gtimer();
+      tma_store_4d(&p.tmY, smem, j0, wo0t, ho0, n0);
+      bulk_commit();
+      bulk_wait_read0();
+      if (p.trace && blockIdx.x == 0) p.trace[1007] = gtimer();
     }
   }
 
   tc_fence_before();
   __syncthreads();
   if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[1002] = gtimer();
+  if (p.trace && threadIdx.x == 0 && blockIdx.x < 2048) {
+    p.trace[2000 + 3 * blockIdx.x + 2] = gtimer();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    p.trace[2000 + 3 * blockIdx.x + 1] = smid;
+  }
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
