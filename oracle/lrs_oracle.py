@@ -80,7 +80,7 @@ def reconstruct_tucker2(u_in: np.ndarray, core: Optional[np.ndarray], u_out: np.
     if core is None:
         return (u_in @ u_out)[:, :, None, None]
     core = np.asarray(core, np.float64)
-    return np.einsum("ca,abyx,bj->cjyx", u_in, core, u_out)
+    return np.einsum("ca,abyx,bj->cjyx", u_in, core, u_out, optimize=True)
 
 
 def reconstruct_cp(a: np.ndarray, b: np.ndarray, c: np.ndarray, d: np.ndarray) -> np.ndarray:

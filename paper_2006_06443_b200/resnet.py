@@ -1,0 +1,86 @@
+"""C5: ResNet-50 with every 3x3 conv replaced by a compressed W ~ L + S layer
+(BASELINE.json configs[4]; §5.5, :343-387, the network-integration
+experiment, with the thesis' CP term read as Tucker-2 -- DESIGN.md reading #1).
+
+The 16 compressed layers run through the C-ABI library (liblrs_conv.so) via
+`CompressedConv2d`; every other layer (stem, 1x1 convs, BN in eval mode,
+ReLU, residual adds, pooling, FC) stays dense in torch/cuDNN (DESIGN.md
+reading #16 -- those layers are not the hot path).  Activations are bf16
+`channels_last`, whose storage is the NHWC layout the ABI takes, so the
+library reads and writes torch's tensors in place.  Weights are torchvision's
+random init under `torch.manual_seed(seed)`; the compressed factors come from
+`workloads.resnet50_compressed_layers` (seeded, synthetic).
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from .lrs_conv import LrsConv
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class CompressedConv2d:
+    """A drop-in for a torch 3x3 conv module: y = conv(x, L + S) on the GPU
+    library.  Holds one LrsConv handle sized for `batch_max` images."""
+
+    def __init__(self, inp, batch_max: int, device: int = 0):
+        torch = _torch()
+        self.cfg = inp.cfg
+        self.layer = LrsConv.from_inputs(inp, batch_max=batch_max, device=device)
+        self.device = device
+        self.stream = None  # None: torch's current stream at call time
+
+    def __call__(self, x):
+        torch = self.layer.torch
+        if not x.is_contiguous(memory_format=torch.channels_last):
+            x = x.contiguous(memory_format=torch.channels_last)
+        n = x.shape[0]
+        y = torch.empty((n, self.cfg.c_out, self.layer.out_h, self.layer.out_w), dtype=x.dtype, device=x.device,
+                        memory_format=torch.channels_last)
+        self.layer.forward_into(x, y, stream=self.stream)
+        return y
+
+    def close(self):
+        self.layer.close()
+
+
+def _module(conv: CompressedConv2d):
+    """nn.Module shim so the library layer can sit inside torchvision's graph."""
+    torch = _torch()
+
+    class LrsConvModule(torch.nn.Module):
+        def __init__(self, c):
+            super().__init__()
+            self.c = c
+
+        def forward(self, x):
+            return self.c(x)
+
+    return LrsConvModule(conv)
+
+
+def build_compressed_resnet50(batch_max: int, device: int = 0, seed: int = 0, density: float = 0.02,
+                              layers: Optional[List] = None):
+    """torchvision resnet50 (random init under manual_seed(seed), eval mode,
+    bf16, channels_last) on cuda:device with its 16 3x3 convs compressed.
+    Returns (model, {table index: CompressedConv2d})."""
+    torch = _torch()
+    import torchvision
+    import workloads
+    torch.manual_seed(seed)
+    model = torchvision.models.resnet50(weights=None).eval()
+    model = model.to(device=f"cuda:{device}", dtype=torch.bfloat16).to(memory_format=torch.channels_last)
+    comp: Dict[int, CompressedConv2d] = {}
+    for idx, name, cfg in (layers or workloads.resnet50_compressed_layers(batch=batch_max, density=density)):
+        inp = workloads.generate_weights(cfg)
+        conv = CompressedConv2d(inp, batch_max=batch_max, device=device)
+        comp[idx] = conv
+        parent = model.get_submodule(name.rsplit(".", 1)[0])
+        setattr(parent, name.rsplit(".", 1)[1], _module(conv))
+    return model, comp

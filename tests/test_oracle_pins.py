@@ -293,3 +293,22 @@ def test_workload_generator_contract():
     r = np.random.default_rng(0).standard_normal(10000).astype(np.float32) * 7
     ref = torch.from_numpy(r).to(torch.bfloat16).to(torch.float32).numpy()
     assert np.array_equal(workloads.bf16_round(r), ref)
+
+
+def test_c5_reference_network_pinned_to_dense_conv2d():
+    """C5 oracle (§5.5): the ResNet-50 whose 16 3x3 convs are
+    evaluated by forward_factored (and its other convs by conv_direct) equals
+    the same network with each conv2 weight set to the dense W = L + S and
+    every conv run by torch's own fp64 conv2d (an independent library route;
+    strides of layer{2,3,4}.0.conv2 included).  32x32 images keep torch's fp64
+    CPU convs fast; both routes are size-agnostic."""
+    import workloads
+    from oracle import resnet_oracle as R
+    img = workloads.resnet50_images(1, seed=3)[:, :, :32, :32].copy()
+    a = R.reference_logits(img)
+    b = R.reference_logits(img, dense_conv2=True, torch_convs=True)
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-10
+    layers = workloads.resnet50_compressed_layers()
+    assert len(layers) == 16
+    assert sum(c.stride == 2 for _, _, c in layers) == 3
+    assert {n for _, n, c in layers if c.stride == 2} == {"layer2.0.conv2", "layer3.0.conv2", "layer4.0.conv2"}

@@ -34,7 +34,8 @@ import numpy as np
 
 __all__ = [
     "LayerConfig", "LayerInputs", "CONFIGS", "generate", "bf16_round",
-    "bf16_bits", "resnet50_table2", "RESNET50_COMPRESSED_3X3",
+    "bf16_bits", "resnet50_table2", "RESNET50_COMPRESSED_3X3", "generate_weights",
+    "resnet50_compressed_layers", "RESNET50_CONV2_MODULES", "resnet50_images",
 ]
 
 
@@ -161,6 +162,31 @@ def generate(cfg: LayerConfig, batch: Optional[int] = None, seed: Optional[int] 
     )
 
 
+def generate_weights(cfg: LayerConfig, seed: Optional[int] = None) -> LayerInputs:
+    """Factors and S of one layer WITHOUT an input X (C5 network layers, whose
+    input is the previous layer's output).  Same recipe as `generate`, draw
+    order U_in, G, U_out, S positions, S values from PCG64(seed)."""
+    rng = np.random.Generator(np.random.PCG64(cfg.seed if seed is None else seed))
+    k = cfg.k
+    u_in = rng.standard_normal((cfg.c_in, cfg.rank_in)) / np.sqrt(cfg.c_in)
+    if cfg.svd:
+        core = None
+        u_out = rng.standard_normal((cfg.rank_in, cfg.c_out)) / np.sqrt(cfg.rank_in)
+    else:
+        core = rng.standard_normal((cfg.rank_in, cfg.rank_out, k, k)) / np.sqrt(cfg.rank_in * k * k)
+        u_out = rng.standard_normal((cfg.rank_out, cfg.c_out)) / np.sqrt(cfg.rank_out)
+    nnz = cfg.nnz
+    pos = np.sort(rng.choice(cfg.numel_w, size=nnz, replace=False)) if nnz > 0 else np.zeros(0, np.int64)
+    vals = rng.standard_normal(nnz) * np.sqrt(0.1)
+    row_len = cfg.c_in * k * k
+    rows, cols = pos // row_len, pos % row_len
+    row_ptr = np.zeros(cfg.c_out + 1, dtype=np.int64)
+    np.add.at(row_ptr, rows + 1, 1)
+    return LayerInputs(cfg=cfg, x=None, u_in=_store(u_in, cfg.dtype),
+                       core=None if core is None else _store(core, cfg.dtype), u_out=_store(u_out, cfg.dtype),
+                       row_ptr=np.cumsum(row_ptr), col_idx=cols.astype(np.int32), values=_store(vals, cfg.dtype))
+
+
 def resnet50_table2(path: Optional[str] = None):
     """Rows of PAPER.md Table 2 (`table:lshapes`) from the
     committed golden fixture: (index, c_in, in_h, in_w, c_out, k)."""
@@ -186,3 +212,37 @@ RESNET50_COMPRESSED_3X3 = {
     2: 1, 6: 1, 9: 1, 12: 2, 16: 1, 19: 1, 22: 1, 25: 2,
     29: 1, 32: 1, 35: 1, 38: 1, 41: 1, 44: 2, 48: 1, 51: 1,
 }
+
+
+# torchvision resnet50 module of each compressed 3x3 conv (Table-2 index -> name)
+RESNET50_CONV2_MODULES = {
+    2: "layer1.0.conv2", 6: "layer1.1.conv2", 9: "layer1.2.conv2",
+    12: "layer2.0.conv2", 16: "layer2.1.conv2", 19: "layer2.2.conv2", 22: "layer2.3.conv2",
+    25: "layer3.0.conv2", 29: "layer3.1.conv2", 32: "layer3.2.conv2", 35: "layer3.3.conv2",
+    38: "layer3.4.conv2", 41: "layer3.5.conv2",
+    44: "layer4.0.conv2", 48: "layer4.1.conv2", 51: "layer4.2.conv2",
+}
+
+
+def resnet50_compressed_layers(batch: int = 256, density: float = 0.02, dtype: str = "bf16"):
+    """C5 (BASELINE.json configs[4]): every ResNet-50 3x3 conv replaced by a
+    Tucker-2 term with ranks Cin/4, Cout/4 plus a `density` sparse S.  Shapes
+    are PAPER.md Table 2 rows (tests/golden/resnet50_table2.csv); strides
+    RESNET50_COMPRESSED_3X3; seed 1000 + Table-2 index (reading #11).
+    Returns [(table index, torchvision module name, LayerConfig)]."""
+    rows = {r[0]: r for r in resnet50_table2()}
+    out = []
+    for idx, stride in RESNET50_COMPRESSED_3X3.items():
+        _, cin, h, w, cout, k = rows[idx]
+        assert k == 3
+        cfg = LayerConfig(f"c5_l{idx}", batch, h, w, cin, cout, 3, stride, 1, cin // 4, cout // 4, density, dtype,
+                          seed=1000 + idx)
+        out.append((idx, RESNET50_CONV2_MODULES[idx], cfg))
+    return out
+
+
+def resnet50_images(n: int, seed: int = 0) -> np.ndarray:
+    """C5 input: N(0,1) images [n, 3, 224, 224] (NCHW) standing in for
+    normalised ImageNet pixels; float32 holding bf16 values."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return bf16_round(rng.standard_normal((n, 3, 224, 224)).astype(np.float32))
