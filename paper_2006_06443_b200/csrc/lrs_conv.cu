@@ -373,7 +373,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     return col;
   };
   std::vector<Unit> units, best_units;
-  int best_th = 0, best_ns = 0, best_tc = 0, best_wc = 0, best_tbw = 0;
+  int best_th = 0, best_ns = 0, best_tc = 0, best_wc = 0, best_tbw = 0, best_nwb = 2;
   long long best_cost = 1LL << 60;
   uint32_t best_stride = 0, best_xw = 0, best_tw = 0, best_total = 0, best_acc = 0;
   for (int cb = 1; cb <= 16 && !best_th; ++cb) {  // column bands: as few as fit
@@ -402,9 +402,11 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         const long long slack_t = std::max(0LL, last_t + 1 - static_cast<long long>(th) * tbw) * 8 * sw_t;
         const uint32_t stride =
             align1024(static_cast<uint32_t>(std::max<long long>(xw + slack_x, tw + slack_t)));
-        const uint32_t total = 2 * stride + ns * (kASlotBytes + kESlotBytes) + 256 + 1024;
-        if (total > static_cast<uint32_t>(kMaxSmem)) continue;
-        if (8u * th * tc * 256u > 2 * stride) continue;  // epilogue staging tile reuses the windows
+        const uint32_t fixed = ns * (kASlotBytes + kESlotBytes) + 8 * kEpiScratch + 512 + 1024;
+        if (2 * stride + fixed > static_cast<uint32_t>(kMaxSmem)) continue;
+        int nwb = 2;
+        while (nwb < kWMaxWin && (nwb + 1) * stride + fixed <= static_cast<uint32_t>(kMaxSmem)) ++nwb;
+        const uint32_t total = nwb * stride + fixed;
         // cost model (cycles, measured with tools/mma_rate2 and tools/wtrace on B200): a
         // sparse MMA costs max(~100 issue, (A 4 KB + B N*64 B) / 128 B/clk smem), an item
         // (one tap of a 64-channel chunk: 2 MMA steps per unit) adds ~200; CTAs run in
@@ -425,6 +427,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
           best_xw = xw;
           best_tw = tw;
           best_total = total;
+          best_nwb = nwb;
           best_acc = static_cast<uint32_t>(acc);
           best_units = units;
         }
@@ -592,11 +595,15 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   w.win_stride = best_stride;
   w.ns = best_ns;
   const uint32_t acc = best_acc;
-  w.e_col0 = acc;
+  w.acc_cols = acc;
+  w.nacc = (2 * acc + 4 * best_ns <= 512) ? 2 : 1;  // double-buffered accumulators: epilogue overlaps MMAs
+  w.e_col0 = w.nacc * acc;
   w.tmem_cols = 512;  // whole TMEM: base address 0 (lrs_wconv_kernel relies on it)
-  w.off_a = 2 * best_stride;
+  w.nwb = best_nwb;
+  w.off_a = best_nwb * best_stride;
   w.off_e = w.off_a + best_ns * kASlotBytes;
-  w.off_bar = w.off_e + best_ns * kESlotBytes;
+  w.off_epi = w.off_e + best_ns * kESlotBytes;
+  w.off_bar = w.off_epi + 8 * kEpiScratch;
   h->w_smem = best_total;
   h->use_w = true;
   return LRS_OK;
@@ -936,21 +943,10 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
       h->wx_ptr = x;
       h->wx_n = n;
     }
-    if (h->wy_ptr != y || h->wy_n != n) {
-      uint64_t dims[4] = {static_cast<uint64_t>(d.c_out), static_cast<uint64_t>(h->wo), static_cast<uint64_t>(h->ho),
-                          static_cast<uint64_t>(n)};
-      uint64_t strides[3] = {static_cast<uint64_t>(d.c_out) * 2, static_cast<uint64_t>(h->wo) * d.c_out * 2,
-                             static_cast<uint64_t>(h->ho) * h->wo * d.c_out * 2};
-      uint32_t box[4] = {128, static_cast<uint32_t>(w.tcols), static_cast<uint32_t>(w.th), 8};
-      uint32_t estr[4] = {1, 1, 1, 1};
-      if ((st = encode_t(&w.tmY, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, y, dims, strides, box, estr, 0)) != LRS_OK)
-        return st;
-      h->wy_ptr = y;
-      h->wy_n = n;
-    }
     w.n = n;
     w.y = y;
-    const unsigned grid = static_cast<unsigned>(((n + 7) / 8) * w.bands * w.cbands * w.n_mt);
+    w.n_tiles = ((n + 7) / 8) * w.bands * w.cbands * w.n_mt;
+    const unsigned grid = static_cast<unsigned>(std::min(w.n_tiles, h->sms));
     TimingRing& r = h->ring[2];
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {

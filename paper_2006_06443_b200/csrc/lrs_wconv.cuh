@@ -4,7 +4,7 @@
 //                   + sum_{c, y, x} S[j, c, y, x] X[n, ho*s + y - p, wo*s + x - p, c]  (a4)
 //
 // computed transposed, D[j, (ho, wo, n)] in TMEM (M = 128 output channels per
-// CTA, TMEM lane = channel), and written to Y once (a5).
+// tile, TMEM lane = channel), and written to Y once (a5).
 //
 // * The sparse term S runs on the 2:4 sparse tensor-core MMA
 //   (tcgen05.mma.sp, kind::f16): at create time every group of 4 consecutive
@@ -21,7 +21,7 @@
 // * The dense part (a3) uses the same machinery with a window of T2 (or T1
 //   for the SVD pair) at the output positions and U_out^T as A.
 //
-// Tile: 8 images x th output rows x all output columns x 128 channels.
+// Tile: 8 images x th output rows x tcols output columns x 128 channels.
 // The tile's outputs are covered by up to kWMaxUnits MMA "units", each one
 // N range (<= 256 columns = 8 images x <= 32 positions) with its accumulator
 // side by side in TMEM.  At stride 1 a unit spans several output rows: its
@@ -31,8 +31,14 @@
 // block from shared memory and has a fixed issue cost.  At stride 2 a unit
 // is (part of) one output row.
 //
+// Persistent: gridDim.x <= #SMs CTAs walk the tiles; the producer and the MMA
+// issuer stream windows/items across tile boundaries, and when two tiles'
+// accumulators fit in TMEM the epilogue of tile k overlaps the MMAs of k+1.
+//
 // Warps: 0 = TMA producer, 1 = TMEM allocator + MMA issuer, 2..9 = epilogue
-// (warp w drains TMEM lanes 32*(w%4) .., the two warps of a quarter split the columns).
+// (warp w drains TMEM lanes 32*(w%4) .., the two warps of a quarter split the
+// columns; each transposes 32 columns x 32 channels through a private 2 KB
+// shared-memory tile so every lane stores 16 contiguous bytes of Y).
 #pragma once
 #include "lrs_ptx.cuh"
 
@@ -46,43 +52,72 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 constexpr int kWThreads = 320;  // warps 0 producer, 1 MMA, 2..9 epilogue (2 per TMEM lane quarter)
 constexpr int kWMaxSlots = 6;
+constexpr int kWMaxWin = 4;  // window buffers in the ring
 constexpr int kWMaxUnits = 8;
 constexpr uint32_t kASlotBytes = 16384;  // dense A box 128 x 128 B, or sparse 128 x 64 B
 constexpr uint32_t kESlotBytes = 2048;   // metadata 128 lanes x 16 B
+constexpr uint32_t kEpiScratch = 2048;   // per epilogue warp: 32 columns x 32 channels bf16
 
 struct WconvParams {
   CUtensorMap tmX;   // X   4-D (C, N, W, H) bf16, box {64, 8, wc, wr}, SW128
-  CUtensorMap tmT;   // T   4-D (R, N, Wo, Ho) bf16, box {t_kc, 8, wo, th}, swizzle sw_t
+  CUtensorMap tmT;   // T   4-D (R, N, Wo, Ho) bf16, box {t_kc, 8, tbox_w, th}, swizzle sw_t
   CUtensorMap tmAd;  // U_out^T [n_mt*128][R_p] bf16, box {t_kc, 128}, swizzle sw_t
   CUtensorMap tmAs;  // compressed S blocks [blocks*128][32] bf16, box {32, 128}, SW64
   CUtensorMap tmE;   // metadata blocks [blocks*128][4] u32, box {4, 128}
-  CUtensorMap tmY;   // Y   4-D (Cout, Wo, Ho, N) bf16, box {128, tcols, th, 8}, no swizzle (TMA store)
   const int* res_block;  // [n_mt][n_ck][taps] residual block index or -1
   void* y;
   int n, ho, wo, cout;
   int kh, kw, sh, sw, ph, pw;
   int th, bands, n_mt;
   int tcols, cbands;       // output columns per tile, column bands
+  int n_tiles;             // groups * bands * cbands * n_mt (for this forward's n)
   int n_units;
-  int u_col[kWMaxUnits];   // first TMEM column
+  int u_col[kWMaxUnits];   // first TMEM column (within one accumulator buffer)
   int u_n[kWMaxUnits];     // MMA N (multiple of 16)
   int u_xpos[kWMaxUnits];  // X window position of the unit's first output at tap (0, 0)
   int u_tpos[kWMaxUnits];  // T window position of the unit's first output
   int u_r0[kWMaxUnits];    // first output row (tile-relative)
-  int u_wo0[kWMaxUnits];   // first output column
+  int u_wo0[kWMaxUnits];   // first output column (tile-relative)
   int u_pitch[kWMaxUnits]; // columns/8 per output row inside the unit
   int u_nw[kWMaxUnits];    // real output columns per row
   int u_rows[kWMaxUnits];  // output rows covered
   int tbox_w;              // width of the T window box (its row pitch)
-  unsigned long long* trace;  // optional: per-event globaltimer stamps of CTA 0 (debug)
+  unsigned long long* trace;  // optional: globaltimer stamps (debug, lrs_conv_debug_trace)
   int n_ck, n_tk, t_kc;
   uint32_t sw_t;        // bytes per T window row (t_kc * 2) = its swizzle width
   int wr, wc;
   uint32_t x_win_bytes, t_win_bytes, win_stride;
   int ns;
+  int nwb;              // window buffers (2..kWMaxWin)
+  int nacc;             // accumulator buffers in TMEM (1 or 2)
+  uint32_t acc_cols;    // TMEM columns of one accumulator buffer
   uint32_t e_col0, tmem_cols;
-  uint32_t off_a, off_e, off_bar;
+  uint32_t off_a, off_e, off_epi, off_bar;
 };
+
+struct TileCoord {
+  int mt, n0, ho0, wo0, j0;
+};
+__device__ __forceinline__ TileCoord tile_coord(const WconvParams& p, int tile) {
+  TileCoord c;
+  c.mt = tile % p.n_mt;
+  tile /= p.n_mt;
+  const int cband = tile % p.cbands;
+  tile /= p.cbands;
+  const int band = tile % p.bands;
+  const int grp = tile / p.bands;
+  c.n0 = grp * 8;
+  c.ho0 = band * p.th;
+  c.wo0 = cband * p.tcols;
+  c.j0 = c.mt * 128;
+  return c;
+}
+
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
 
 __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_constant__ WconvParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -92,35 +127,30 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   const int lane = threadIdx.x & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   uint64_t* win_full = bars;
-  uint64_t* win_empty = bars + 2;
-  uint64_t* a_full = bars + 4;
-  uint64_t* a_empty = bars + 4 + kWMaxSlots;
-  uint64_t* acc_full = bars + 4 + 2 * kWMaxSlots;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 + 2 * kWMaxSlots);
+  uint64_t* win_empty = bars + kWMaxWin;
+  uint64_t* a_full = bars + 2 * kWMaxWin;
+  uint64_t* a_empty = a_full + kWMaxSlots;
+  uint64_t* acc_full = a_empty + kWMaxSlots;  // [2]
+  uint64_t* acc_empty = acc_full + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
-  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[1004] = gtimer();
   if (p.trace && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
-  int bid = blockIdx.x;
-  const int mt = bid % p.n_mt;
-  bid /= p.n_mt;
-  const int cband = bid % p.cbands;
-  bid /= p.cbands;
-  const int band = bid % p.bands;
-  const int grp = bid / p.bands;
-  const int n0 = grp * 8, ho0 = band * p.th, j0 = mt * 128, wo0t = cband * p.tcols;
   const int taps = p.kh * p.kw;
   const int nwin = p.n_tk + p.n_ck;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < p.nwb; ++i) {
       mbar_init(&win_full[i], 1);
       mbar_init(&win_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 8);  // one arrival per epilogue warp
     }
     for (int i = 0; i < p.ns; ++i) {
       mbar_init(&a_full[i], 1);
       mbar_init(&a_empty[i], 1);
     }
-    mbar_init(acc_full, 1);
     fence_mbar_init();
     tma_prefetch_desc(&p.tmX);
     tma_prefetch_desc(&p.tmT);
@@ -140,126 +170,117 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     __trap();
   }
   constexpr uint32_t tmem = 0u;
-  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[1003] = gtimer();
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
-      int it = 0;
-      for (int w = 0; w < nwin; ++w) {
-        const int buf = w & 1;
-        if (w >= 2) mbar_wait(&win_empty[buf], ((w >> 1) - 1) & 1);
-        uint8_t* wdst = smem + buf * p.win_stride;
-        if (w < p.n_tk) {
-          mbar_arrive_expect_tx(&win_full[buf], p.t_win_bytes);
-          tma_load_4d(wdst, &p.tmT, &win_full[buf], w * p.t_kc, n0, wo0t, ho0);
-          const int slot = it % p.ns;
-          if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
-          mbar_arrive_expect_tx(&a_full[slot], 128u * p.sw_t);
-          tma_load_2d(smem + p.off_a + slot * kASlotBytes, &p.tmAd, &a_full[slot], w * p.t_kc, j0);
-          ++it;
-        } else {
-          const int c = w - p.n_tk;
-          mbar_arrive_expect_tx(&win_full[buf], p.x_win_bytes);
-          tma_load_4d(wdst, &p.tmX, &win_full[buf], c * 64, n0, wo0t * p.sw - p.pw, ho0 * p.sh - p.ph);
-          const int* rb = p.res_block + (mt * p.n_ck + c) * taps;
-          int rblk[9];
-#pragma unroll
-          for (int t = 0; t < 9; ++t) rblk[t] = t < taps ? __ldg(rb + t) : -1;
-          for (int t = 0; t < taps; ++t) {
-            for (int part = 0; part < 2; ++part) {
-              const int key = (mt * p.n_ck + c) * taps + t;
-              int blk = key;
-              if (part == 1) {
-                blk = -1;
-#pragma unroll
-                for (int q = 0; q < 9; ++q)
-                  if (q == t) blk = rblk[q];
-                if (taps > 9) blk = __ldg(rb + t);
+      int it = 0, wg = 0, buf = 0;
+      uint32_t wph = 0;
+      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        const TileCoord tc = tile_coord(p, tile);
+        for (int w = 0; w < nwin; ++w, ++wg) {
+          if (wg >= p.nwb) mbar_wait(&win_empty[buf], wph ^ 1u);
+          uint8_t* wdst = smem + buf * p.win_stride;
+          if (w < p.n_tk) {
+            mbar_arrive_expect_tx(&win_full[buf], p.t_win_bytes);
+            tma_load_4d(wdst, &p.tmT, &win_full[buf], w * p.t_kc, tc.n0, tc.wo0, tc.ho0);
+            const int slot = it % p.ns;
+            if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
+            mbar_arrive_expect_tx(&a_full[slot], 128u * p.sw_t);
+            tma_load_2d(smem + p.off_a + slot * kASlotBytes, &p.tmAd, &a_full[slot], w * p.t_kc, tc.j0);
+            ++it;
+          } else {
+            const int c = w - p.n_tk;
+            mbar_arrive_expect_tx(&win_full[buf], p.x_win_bytes);
+            tma_load_4d(wdst, &p.tmX, &win_full[buf], c * 64, tc.n0, tc.wo0 * p.sw - p.pw, tc.ho0 * p.sh - p.ph);
+            const int key0 = (tc.mt * p.n_ck + c) * taps;
+            for (int t = 0; t < taps; ++t) {
+              const int rblk = __ldg(p.res_block + key0 + t);
+              for (int part = 0; part < 2; ++part) {
+                const int blk = part == 0 ? key0 + t : rblk;
+                if (blk < 0) continue;
+                const int slot = it % p.ns;
+                if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
+                mbar_arrive_expect_tx(&a_full[slot], 8192u + kESlotBytes);
+                tma_load_2d(smem + p.off_a + slot * kASlotBytes, &p.tmAs, &a_full[slot], 0, blk * 128);
+                tma_load_2d(smem + p.off_e + slot * kESlotBytes, &p.tmE, &a_full[slot], 0, blk * 128);
+                ++it;
               }
-              if (blk < 0) continue;
-              const int slot = it % p.ns;
-              if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
-              mbar_arrive_expect_tx(&a_full[slot], 8192u + kESlotBytes);
-              tma_load_2d(smem + p.off_a + slot * kASlotBytes, &p.tmAs, &a_full[slot], 0, blk * 128);
-              tma_load_2d(smem + p.off_e + slot * kESlotBytes, &p.tmE, &a_full[slot], 0, blk * 128);
-              ++it;
             }
           }
+          if (++buf == p.nwb) { buf = 0; wph ^= 1u; }
         }
       }
     }
   } else if (warp == 1) {
-    {
-      // ------------------------------------------------------------ MMA issuer
-      // The whole warp walks the loop (so the per-unit values stay warp-uniform
-      // and live in uniform registers); one elected lane issues each tcgen05 op.
-      // Descriptors are linear in the start address (14-bit field of addr>>4),
-      // so every per-unit descriptor is precomputed once and the inner loop
-      // only adds byte offsets >> 4: the single-thread issue loop stays short.
-      const uint32_t win0 = smem_u32(smem);
-      const uint32_t t_pos = 8u * p.sw_t;  // bytes per output position in a T window
-      const uint32_t x_sbo = 1024u * static_cast<uint32_t>(p.sw);
-      const int nu = p.n_units;
-      uint32_t dcol[kWMaxUnits], idu[kWMaxUnits];
-      uint64_t bxd[kWMaxUnits], btd[kWMaxUnits];
+    // -------------------------------------------------------------- MMA issuer
+    // The whole warp walks the loop (so the per-unit values stay warp-uniform
+    // and live in uniform registers); one elected lane issues each tcgen05 op.
+    // Descriptors are linear in the start address (14-bit field of addr>>4),
+    // so every per-unit descriptor is precomputed once and the inner loop
+    // only adds byte offsets >> 4: the single-thread issue loop stays short.
+    const uint32_t win0 = smem_u32(smem);
+    const uint32_t t_pos = 8u * p.sw_t;  // bytes per output position in a T window
+    const uint32_t x_sbo = 1024u * static_cast<uint32_t>(p.sw);
+    const int nu = p.n_units;
+    uint32_t dcol[kWMaxUnits], idu[kWMaxUnits];
+    uint64_t bxd[kWMaxUnits], btd[kWMaxUnits];
 #pragma unroll
-      for (int u = 0; u < kWMaxUnits; ++u) {
-        if (u < nu) {
-          dcol[u] = tmem + static_cast<uint32_t>(p.u_col[u]);
-          idu[u] = umma_idesc(1u, static_cast<uint32_t>(p.u_n[u]), 128u);
-          bxd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_xpos[u]) * 1024u, 128, x_sbo);
-          btd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_tpos[u]) * t_pos, p.sw_t, t_pos);
-        }
+    for (int u = 0; u < kWMaxUnits; ++u) {
+      if (u < nu) {
+        dcol[u] = tmem + static_cast<uint32_t>(p.u_col[u]);
+        idu[u] = umma_idesc(1u, static_cast<uint32_t>(p.u_n[u]), 128u);
+        bxd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_xpos[u]) * 1024u, 128, x_sbo);
+        btd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_tpos[u]) * t_pos, p.sw_t, t_pos);
       }
-      const uint64_t ad_dense = umma_desc(smem_u32(smem + p.off_a), p.sw_t);
-      const uint64_t ad_sp = umma_desc(smem_u32(smem + p.off_a), 64);
-      const uint64_t ed0 = umma_desc_rows16(smem_u32(smem + p.off_e));
-      const uint32_t slot_a16 = kASlotBytes >> 4, slot_e16 = kESlotBytes >> 4;
-      const uint32_t win16 = p.win_stride >> 4;
-      const int ksteps = static_cast<int>(p.sw_t / 32);
-      int it = 0, slot = 0;
-      uint32_t ph = 0;
-      for (int w = 0; w < nwin; ++w) {
-        const int buf = w & 1;
-        mbar_wait(&win_full[buf], (w >> 1) & 1);
+    }
+    const uint64_t ad_dense = umma_desc(smem_u32(smem + p.off_a), p.sw_t);
+    const uint64_t ad_sp = umma_desc(smem_u32(smem + p.off_a), 64);
+    const uint64_t ed0 = umma_desc_rows16(smem_u32(smem + p.off_e));
+    const uint32_t slot_a16 = kASlotBytes >> 4, slot_e16 = kESlotBytes >> 4;
+    const uint32_t win16 = p.win_stride >> 4;
+    const int ksteps = static_cast<int>(p.sw_t / 32);
+    int slot = 0, k = 0, buf = 0;
+    uint32_t ph = 0, wph = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++k) {
+      const TileCoord tc = tile_coord(p, tile);
+      const int b = p.nacc == 2 ? (k & 1) : 0;
+      const int use = p.nacc == 2 ? (k >> 1) : k;  // previous uses of accumulator b
+      if (use > 0) {
+        mbar_wait(&acc_empty[b], (use - 1) & 1);
         tc_fence_after();
-        const uint32_t boff = buf ? win16 : 0u;
+      }
+      const uint32_t acc0 = static_cast<uint32_t>(b) * p.acc_cols;
+      for (int w = 0; w < nwin; ++w) {
+        mbar_wait(&win_full[buf], wph);
+        tc_fence_after();
+        const uint32_t boff = static_cast<uint32_t>(buf) * win16;
         if (w < p.n_tk) {
           mbar_wait(&a_full[slot], ph);
           tc_fence_after();
           const uint64_t ab = ad_dense + slot * slot_a16;
-#pragma unroll
           if (elect_one()) {
 #pragma unroll
             for (int u = 0; u < kWMaxUnits; ++u) {
               if (u < nu) {
-                for (int k = 0; k < ksteps; ++k)
-                  mma_bf16(dcol[u], ab + 2 * k, btd[u] + boff + 2 * k, idu[u], (w > 0 || k > 0) ? 1u : 0u);
+                for (int kk = 0; kk < ksteps; ++kk)
+                  mma_bf16(dcol[u] + acc0, ab + 2 * kk, btd[u] + boff + 2 * kk, idu[u], (w > 0 || kk > 0) ? 1u : 0u);
               }
             }
             mma_commit(&a_empty[slot]);
           }
           __syncwarp();
-          ++it;
           if (++slot == p.ns) { slot = 0; ph ^= 1u; }
         } else {
           const int c = w - p.n_tk;
-          const int* rb = p.res_block + (mt * p.n_ck + c) * taps;
-          uint32_t resmask = 0;
-          for (int t = 0; t < taps; ++t) resmask |= (__ldg(rb + t) >= 0 ? 1u : 0u) << t;
+          const int* rb = p.res_block + (tc.mt * p.n_ck + c) * taps;
           for (int t = 0; t < taps; ++t) {
             const int ty = t / p.kw, tx = t - ty * p.kw;
             const uint32_t tap16 = static_cast<uint32_t>(ty * p.wc + tx) * 64u;  // (pos * 1024) >> 4
-            const int nparts = 1 + static_cast<int>((resmask >> t) & 1u);
+            const int nparts = 1 + (__ldg(rb + t) >= 0 ? 1 : 0);
             for (int part = 0; part < nparts; ++part) {
-              const unsigned long long tw0 = p.trace ? gtimer() : 0ull;
               mbar_wait(&a_full[slot], ph);
               tc_fence_after();
-              if (p.trace && blockIdx.x == 0 && it < 500 && lane == 0) {
-                p.trace[2 * it] = tw0;
-                p.trace[2 * it + 1] = gtimer();
-              }
               const uint32_t et = tmem + p.e_col0 + 4u * slot;
               const uint64_t ab = ad_sp + slot * slot_a16;
               if (elect_one()) {
@@ -269,88 +290,84 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
 #pragma unroll
                   for (int u = 0; u < kWMaxUnits; ++u) {
                     if (u < nu)
-                      mma_sp_bf16(dcol[u], ab + 2 * s2, bxd[u] + boff + tap16 + 4 * s2,
+                      mma_sp_bf16(dcol[u] + acc0, ab + 2 * s2, bxd[u] + boff + tap16 + 4 * s2,
                                   idu[u] | (1u << 2) | static_cast<uint32_t>(s2), 1u, et);
                   }
                 }
                 mma_commit(&a_empty[slot]);
               }
               __syncwarp();
-              ++it;
               if (++slot == p.ns) { slot = 0; ph ^= 1u; }
             }
           }
         }
         if (elect_one()) mma_commit(&win_empty[buf]);
         __syncwarp();
+        if (++buf == p.nwb) { buf = 0; wph ^= 1u; }
       }
-      if (elect_one()) mma_commit(acc_full);
+      if (elect_one()) mma_commit(&acc_full[b]);
       __syncwarp();
-      if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[1000] = gtimer();
     }
   } else {
     // -------------------------------------------------------------- epilogue
-    const int q4 = warp & 3;
-    mbar_wait_sleep(acc_full, 0);
-    tc_fence_after();
-    if (p.trace && blockIdx.x == 0 && threadIdx.x == 64) p.trace[1001] = gtimer();
-    if (p.trace && threadIdx.x == 64 && blockIdx.x < 2048) p.trace[8200 + blockIdx.x] = gtimer();
-    // TMEM -> bf16 staging tile [8 images][th][tcols][128 ch] in the (now idle) window
-    // buffers, then one TMA tensor store (clips rows/cols/images/channels out of range).
-    // Columns go in chunks of 32 (4 virtual positions x 8 images); the two warps of a
-    // lane quarter take alternate chunks.
-    const uint32_t stage = smem_u32(smem);
-    const uint32_t img_stride = static_cast<uint32_t>(p.th * p.tcols) * 256u;  // bytes per image plane
-    const int jl = q4 * 32 + lane;
-    const int ehalf = (warp - 2) >> 2;
-    for (int u = 0; u < p.n_units; ++u) {
-      const int pitch = p.u_pitch[u], nw = p.u_nw[u], un = p.u_n[u], rows = p.u_rows[u];
-      const int r0 = p.u_r0[u], w0 = p.u_wo0[u], ucol = p.u_col[u];
-      int rr = 0, cc = ehalf * 4;  // virtual position (row, col) of this warp's first chunk
-      while (cc >= pitch) { cc -= pitch; ++rr; }
-      for (int c0 = ehalf * 32; c0 < un; c0 += 64) {
-        uint32_t v[32];
-        tmem_ld32_nowait(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + static_cast<uint32_t>(ucol + c0), v);
-        tmem_ld_wait();
-        int r = rr, c = cc;
+    const int q4 = warp & 3;            // TMEM lane quarter
+    const int ehalf = (warp - 2) >> 2;  // which half of the columns
+    const uint32_t scr = smem_u32(smem + p.off_epi) + static_cast<uint32_t>(warp - 2) * kEpiScratch;
+    __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(p.y);
+    int k = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++k) {
+      const TileCoord tc = tile_coord(p, tile);
+      const int b = p.nacc == 2 ? (k & 1) : 0;
+      const int use = p.nacc == 2 ? (k >> 1) : k;
+      mbar_wait_sleep(&acc_full[b], use & 1);
+      tc_fence_after();
+      const uint32_t acc0 = static_cast<uint32_t>(b) * p.acc_cols;
+      const int jw = tc.j0 + q4 * 32;  // first channel of this warp
+      for (int u = 0; u < p.n_units; ++u) {
+        const int pitch = p.u_pitch[u], nw = p.u_nw[u], un = p.u_n[u], rows = p.u_rows[u];
+        const int r0 = p.u_r0[u], w0 = p.u_wo0[u], ucol = p.u_col[u];
+        for (int c0 = ehalf * 32; c0 < un; c0 += 64) {
+          uint32_t v[32];
+          tmem_ld32_nowait(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + acc0 + static_cast<uint32_t>(ucol + c0),
+                           v);
+          tmem_ld_wait();
+          // lane = channel jw + lane holds 32 columns; transpose through the scratch
+          // tile [32 columns][32 channels] so each lane then owns 8 channels of a column
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          if (c0 + qq * 8 < un && c < nw && r < rows) {
-            const uint32_t a0 = stage + (static_cast<uint32_t>((r0 + r) * p.tcols + w0 + c) * 128u + jl) * 2u;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const __nv_bfloat16 b = __float2bfloat16_rn(__uint_as_float(v[qq * 8 + i]));
-              sts_u16(a0 + i * img_stride, *reinterpret_cast<const uint16_t*>(&b));
-            }
+          for (int cc2 = 0; cc2 < 32; ++cc2) {
+            const __nv_bfloat16 hb = __float2bfloat16_rn(__uint_as_float(v[cc2]));
+            sts_u16(scr + static_cast<uint32_t>(cc2 * 64 + lane * 2), *reinterpret_cast<const uint16_t*>(&hb));
           }
-          if (++c == pitch) { c = 0; ++r; }
+          __syncwarp();
+          // lane l, pass q: column col = q*8 + l/4, channels 8*(l%4) .. +7
+          const int part = lane & 3;
+          const int jch = jw + part * 8;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int col = q * 8 + (lane >> 2);
+            const int cidx = c0 + col;
+            const uint4 val = lds_v4(scr + static_cast<uint32_t>(col * 64 + part * 16));
+            if (cidx >= un) continue;
+            const int qv = cidx >> 3, img = cidx & 7;
+            const int rr = qv / pitch, cc = qv - rr * pitch;
+            const int n = tc.n0 + img, ho = tc.ho0 + r0 + rr, wo = tc.wo0 + w0 + cc;
+            if (cc < nw && rr < rows && n < p.n && ho < p.ho && wo < p.wo && jch < p.cout)
+              *reinterpret_cast<uint4*>(y + ((static_cast<long long>(n) * p.ho + ho) * p.wo + wo) * p.cout + jch) =
+                  val;
+          }
+          __syncwarp();
         }
-        // advance 8 virtual positions (this warp's next chunk)
-        cc += 8;
-        while (cc >= pitch) { cc -= pitch; ++rr; }
       }
-    }
-    if (p.trace && blockIdx.x == 0 && threadIdx.x == 64) p.trace[1005] = gtimer();
-    fence_proxy_async_smem();
-    named_bar_sync(1, 256);
-    if (threadIdx.x == 64) {
-      if (p.trace && blockIdx.x == 0) p.trace[1006] = gtimer();
-      tma_store_4d(&p.tmY, smem, j0, wo0t, ho0, n0);
-      bulk_commit();
-      bulk_wait_read0();
-      if (p.trace && blockIdx.x == 0) p.trace[1007] = gtimer();
+      // this warp's TMEM reads of buffer b are complete (wait::ld above)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[1002] = gtimer();
-  if (p.trace && threadIdx.x == 0 && blockIdx.x < 2048) {
-    p.trace[2000 + 3 * blockIdx.x + 2] = gtimer();
-    unsigned smid;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    p.trace[2000 + 3 * blockIdx.x + 1] = smid;
-  }
+  if (p.trace && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x + 2] = gtimer();
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
