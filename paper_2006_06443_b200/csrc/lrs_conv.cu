@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -402,7 +403,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         const long long slack_t = std::max(0LL, last_t + 1 - static_cast<long long>(th) * tbw) * 8 * sw_t;
         const uint32_t stride =
             align1024(static_cast<uint32_t>(std::max<long long>(xw + slack_x, tw + slack_t)));
-        const uint32_t fixed = ns * (kASlotBytes + kESlotBytes) + 8 * kEpiScratch + 512 + 1024;
+        const uint32_t fixed = ns * (kASlotBytes + kESlotBytes) + 8 * kEpiScratch + 1024 + 1024;
         if (2 * stride + fixed > static_cast<uint32_t>(kMaxSmem)) continue;
         int nwb = 2;
         while (nwb < kWMaxWin && (nwb + 1) * stride + fixed <= static_cast<uint32_t>(kMaxSmem)) ++nwb;
@@ -1075,6 +1076,7 @@ int32_t lrs_conv_sparse_engine(const lrs_conv* h, int32_t* main_blocks, int32_t*
 lrs_status lrs_conv_debug_trace(lrs_conv* h, void* dev_buf) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
   h->wp.trace = static_cast<unsigned long long*>(dev_buf);
+  if (const char* e = getenv("LRS_WCONV_DBG")) h->wp.dbg = atoi(e);
   return LRS_OK;
 }
 

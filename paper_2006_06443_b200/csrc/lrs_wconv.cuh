@@ -83,6 +83,7 @@ struct WconvParams {
   int u_rows[kWMaxUnits];  // output rows covered
   int tbox_w;              // width of the T window box (its row pitch)
   unsigned long long* trace;  // optional: globaltimer stamps (debug, lrs_conv_debug_trace)
+  int dbg;                 // debug experiment bits (0 in production)
   int n_ck, n_tk, t_kc;
   uint32_t sw_t;        // bytes per T window row (t_kc * 2) = its swizzle width
   int wr, wc;
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   uint64_t* acc_full = a_empty + kWMaxSlots;  // [2]
   uint64_t* acc_empty = acc_full + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const uint32_t slot_info = smem_u32(tmem_slot + 4);  // [kWMaxSlots] u32, written by the producer
 
   if (p.trace && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
   const int taps = p.kh * p.kw;
@@ -196,14 +198,22 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             const int key0 = (tc.mt * p.n_ck + c) * taps;
             for (int t = 0; t < taps; ++t) {
               const int rblk = __ldg(p.res_block + key0 + t);
+              const int ty = t / p.kw, tx = t - ty * p.kw;
+              const uint32_t tap16 = static_cast<uint32_t>(ty * p.wc + tx) * 64u;  // (pos * 1024) >> 4
               for (int part = 0; part < 2; ++part) {
                 const int blk = part == 0 ? key0 + t : rblk;
                 if (blk < 0) continue;
+                const bool last = t == taps - 1 && (part == 1 || rblk < 0);
                 const int slot = it % p.ns;
                 if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
-                mbar_arrive_expect_tx(&a_full[slot], 8192u + kESlotBytes);
-                tma_load_2d(smem + p.off_a + slot * kASlotBytes, &p.tmAs, &a_full[slot], 0, blk * 128);
-                tma_load_2d(smem + p.off_e + slot * kESlotBytes, &p.tmE, &a_full[slot], 0, blk * 128);
+                st_shared_u32(slot_info + 4u * slot, tap16 | (last ? 0x80000000u : 0u));
+                if (p.dbg & 2) {
+                  mbar_arrive(&a_full[slot]);
+                } else {
+                  mbar_arrive_expect_tx(&a_full[slot], 8192u + kESlotBytes);
+                  tma_load_2d(smem + p.off_a + slot * kASlotBytes, &p.tmAs, &a_full[slot], 0, blk * 128);
+                  tma_load_2d(smem + p.off_e + slot * kESlotBytes, &p.tmE, &a_full[slot], 0, blk * 128);
+                }
                 ++it;
               }
             }
@@ -251,9 +261,12 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         tc_fence_after();
       }
       const uint32_t acc0 = static_cast<uint32_t>(b) * p.acc_cols;
+      if (p.trace && blockIdx.x == 0 && lane == 0 && k < 16) p.trace[100 + 4 * k] = gtimer();
       for (int w = 0; w < nwin; ++w) {
+        if (p.trace && blockIdx.x == 0 && lane == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w] = gtimer();
         mbar_wait(&win_full[buf], wph);
         tc_fence_after();
+        if (p.trace && blockIdx.x == 0 && lane == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w + 1] = gtimer();
         const uint32_t boff = static_cast<uint32_t>(buf) * win16;
         if (w < p.n_tk) {
           mbar_wait(&a_full[slot], ph);
@@ -272,33 +285,31 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           __syncwarp();
           if (++slot == p.ns) { slot = 0; ph ^= 1u; }
         } else {
-          const int c = w - p.n_tk;
-          const int* rb = p.res_block + (tc.mt * p.n_ck + c) * taps;
-          for (int t = 0; t < taps; ++t) {
-            const int ty = t / p.kw, tx = t - ty * p.kw;
-            const uint32_t tap16 = static_cast<uint32_t>(ty * p.wc + tx) * 64u;  // (pos * 1024) >> 4
-            const int nparts = 1 + (__ldg(rb + t) >= 0 ? 1 : 0);
-            for (int part = 0; part < nparts; ++part) {
-              mbar_wait(&a_full[slot], ph);
-              tc_fence_after();
-              const uint32_t et = tmem + p.e_col0 + 4u * slot;
-              const uint64_t ab = ad_sp + slot * slot_a16;
-              if (elect_one()) {
-                tmem_cp_128x128b(et, ed0 + slot * slot_e16);
+          // sparse items of this window: the producer tags each slot with the
+          // tap's window offset and whether it is the window's last item
+          while (true) {
+            mbar_wait(&a_full[slot], ph);
+            tc_fence_after();
+            const uint32_t info = ld_shared_u32(slot_info + 4u * slot);
+            const uint32_t tap16 = info & 0x7FFFFFFFu;
+            const uint32_t et = tmem + p.e_col0 + 4u * slot;
+            const uint64_t ab = ad_sp + slot * slot_a16;
+            if (elect_one()) {
+              if (!(p.dbg & 1)) tmem_cp_128x128b(et, ed0 + slot * slot_e16);
 #pragma unroll
-                for (int s2 = 0; s2 < 2; ++s2) {
+              for (int s2 = 0; s2 < 2 && !(p.dbg & 1); ++s2) {
 #pragma unroll
-                  for (int u = 0; u < kWMaxUnits; ++u) {
-                    if (u < nu)
-                      mma_sp_bf16(dcol[u] + acc0, ab + 2 * s2, bxd[u] + boff + tap16 + 4 * s2,
-                                  idu[u] | (1u << 2) | static_cast<uint32_t>(s2), 1u, et);
-                  }
+                for (int u = 0; u < kWMaxUnits; ++u) {
+                  if (u < nu)
+                    mma_sp_bf16(dcol[u] + acc0, ab + 2 * s2, bxd[u] + boff + tap16 + 4 * s2,
+                                idu[u] | (1u << 2) | static_cast<uint32_t>(s2), 1u, et);
                 }
-                mma_commit(&a_empty[slot]);
               }
-              __syncwarp();
-              if (++slot == p.ns) { slot = 0; ph ^= 1u; }
+              mma_commit(&a_empty[slot]);
             }
+            __syncwarp();
+            if (++slot == p.ns) { slot = 0; ph ^= 1u; }
+            if (info >> 31) break;
           }
         }
         if (elect_one()) mma_commit(&win_empty[buf]);
@@ -307,6 +318,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       }
       if (elect_one()) mma_commit(&acc_full[b]);
       __syncwarp();
+      if (p.trace && blockIdx.x == 0 && lane == 0 && k < 16) p.trace[100 + 4 * k + 1] = gtimer();
     }
   } else {
     // -------------------------------------------------------------- epilogue
@@ -321,6 +333,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       const int use = p.nacc == 2 ? (k >> 1) : k;
       mbar_wait_sleep(&acc_full[b], use & 1);
       tc_fence_after();
+      if (p.trace && blockIdx.x == 0 && threadIdx.x == 64 && k < 16) p.trace[100 + 4 * k + 2] = gtimer();
       const uint32_t acc0 = static_cast<uint32_t>(b) * p.acc_cols;
       const int jw = tc.j0 + q4 * 32;  // first channel of this warp
       for (int u = 0; u < p.n_units; ++u) {
@@ -362,6 +375,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
+      if (p.trace && blockIdx.x == 0 && threadIdx.x == 64 && k < 16) p.trace[100 + 4 * k + 3] = gtimer();
     }
   }
 

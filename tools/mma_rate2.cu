@@ -7,15 +7,15 @@
 #include "../paper_2006_06443_b200/csrc/lrs_ptx.cuh"
 using namespace lrs;
 
-__global__ void k(int n, int nmma, int use_cp, int move_b, int items, unsigned long long* out) {
+__global__ void k(int n, int nmma, int use_cp, int move_b, int items, unsigned long long* out, int samed, int dowait) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar, bar2;
+  __shared__ uint64_t bar, bar2, bar3;
   __shared__ uint32_t slot;
   for (int i = threadIdx.x; i < 180 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
   for (int i = threadIdx.x; i < 2048 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem + 176 * 1024)[i] = 0x44444444u;
   fence_proxy_async_smem();
-  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, 1); fence_mbar_init(); }
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, 1); mbar_init(&bar3, 1); mbar_arrive(&bar3); fence_mbar_init(); }
   if (threadIdx.x < 32) tmem_alloc(&slot, 512);
   tc_fence_before(); __syncthreads(); tc_fence_after();
   const uint32_t tm = slot;
@@ -26,11 +26,12 @@ __global__ void k(int n, int nmma, int use_cp, int move_b, int items, unsigned l
     const uint32_t idesc = umma_idesc(1u, n, 128u) | (1u << 2);
     const long long t0 = clock64();
     for (int i = 0; i < items; ++i) {
+      if (dowait) { mbar_wait(&bar3, 0); tc_fence_after(); }
       const uint32_t tapoff = move_b ? static_cast<uint32_t>((i % 9) / 3 * 9 + (i % 3)) * 64u : 0u;
       if (elect_one()) {
         if (use_cp) tmem_cp_128x128b(tm + 480 + 4 * (i % 3), ed);
         for (int m = 0; m < nmma; ++m)
-          mma_sp_bf16(tm + (m % 2) * 256 % 480, ad + 2 * (m & 1), bd + tapoff + 4 * (m & 1), idesc | (m & 1), 1u,
+          mma_sp_bf16(samed ? tm : (tm + (m % 2) * 256 % 480), ad + 2 * (m & 1), bd + tapoff + 4 * (m & 1), idesc | (m & 1), 1u,
                       tm + 480 + 4 * (i % 3));
         mma_commit(&bar2);
       }
@@ -51,11 +52,9 @@ int main() {
   cudaMalloc(&d, 4096 * 8);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   const int items = 2000;
-  struct C { int n, nmma, cp, mv; } cs[] = {{256, 2, 1, 1}, {256, 2, 0, 1}, {256, 2, 1, 0}, {256, 2, 0, 0},
-                                           {256, 4, 1, 1}, {256, 8, 1, 1}, {208, 6, 1, 1}, {64, 6, 1, 1},
-                                           {128, 2, 1, 1}};
+  struct C { int n, nmma, cp, mv, same, wt; } cs[] = {{224, 2, 1, 1, 1, 0}, {224, 2, 1, 1, 1, 1}, {224, 2, 0, 1, 1, 1}};
   for (auto c : cs) {
-    k<<<148, 128, 200 * 1024>>>(c.n, c.nmma, c.cp, c.mv, items, d);
+    k<<<148, 128, 200 * 1024>>>(c.n, c.nmma, c.cp, c.mv, items, d, c.same, c.wt);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
     unsigned long long h[148];
@@ -63,7 +62,7 @@ int main() {
     double avg = 0;
     for (int i = 0; i < 148; ++i) avg += h[i];
     avg /= 148;
-    printf("N=%3d mma/item=%d cp=%d moveB=%d: %7.1f cycles/item, %6.1f cycles/MMA, %5.0f logical MAC/clk/SM\n", c.n,
+    printf("wait=%d sameD=%d ", c.wt, c.same); printf("N=%3d mma/item=%d cp=%d moveB=%d: %7.1f cycles/item, %6.1f cycles/MMA, %5.0f logical MAC/clk/SM\n", c.n,
            c.nmma, c.cp, c.mv, avg / items, avg / items / c.nmma, 128.0 * c.n * 32 * c.nmma / (avg / items));
   }
   return 0;

@@ -22,3 +22,9 @@ st = np.array([t[2000 + 3 * b] for b in range(nb)]); en = np.array([t[2000 + 3 *
 base = st.min()
 print(f"{name} n={x.shape[0]}: {nb} CTAs; start spread {st.max()-base} ns; end max {en.max()-base} ns; "
       f"CTA dur min {(en-st).min()} med {np.median(en-st):.0f} max {(en-st).max()}")
+t0 = t[2000]
+for k in range(16):
+    if t[100 + 4 * k] == 0: break
+    a, b, c, d = (t[100 + 4 * k + i] - t0 for i in range(4))
+    ws = [(t[200 + 16 * k + 2 * w] - t0, t[200 + 16 * k + 2 * w + 1] - t0) for w in range(8) if t[200 + 16 * k + 2 * w]]
+    print(f"tile {k}: mma start {a} end {b} | epi woke {c} done {d} | windows (wait, got): {ws}")
