@@ -207,8 +207,10 @@ def main_c5(args):
     dev = torch.device(f"cuda:{local}")
     from paper_2006_06443_b200 import roofline as RL
     from paper_2006_06443_b200.resnet import build_compressed_resnet50
+    from paper_2006_06443_b200.dist import shard_range
     gb = 256
-    per = gb // world
+    s0, s1 = shard_range(gb, rank, world)
+    per = s1 - s0
     model, comp = build_compressed_resnet50(batch_max=per, device=local)
     img = workloads.resnet50_images(per, seed=rank)
     x = torch.from_numpy(img).to(torch.bfloat16).to(dev).contiguous(memory_format=torch.channels_last)
