@@ -64,7 +64,8 @@ typedef struct lrs_conv_desc {
   int64_t nnz;                    /* >= 0                                           */
   const int64_t *row_ptr;         /* host [c_out + 1]; 0, non-decreasing, nnz at end */
   const int32_t *col_idx;         /* host [nnz]; < c_in*kernel_h*kernel_w            */
-  const float *values;            /* host [nnz]; fp32 for both dtypes               */
+  const float *values;            /* host [nnz]; fp32; bf16 layers round them to bf16 (RNE)
+                                     at create (reading #12)               */
 } lrs_conv_desc;
 
 /*
@@ -78,6 +79,10 @@ typedef struct lrs_conv_desc {
  *   padded kernel or rank_in != rank_out, NULL required pointer.
  * UNSUPPORTED: kernel > 7, rank > 256, c_in or c_out not a multiple of 8
  *   (bf16) / 4 (fp32) (16-byte TMA rows), output width > 128.
+ * bf16 layers with c_in % 64 == 0 run the fused expansion + sparse term on
+ * the 2:4 sparse tensor cores (lrs_conv_sparse_engine() == 1); S is split at
+ * create into exact 2:4 main and residual blocks (PAPER.md:171-191 evaluated
+ * exactly).
  * OUT_OF_MEMORY / CUDA: allocation or driver failure (no handle is returned).
  */
 lrs_status lrs_conv_create(const lrs_conv_desc *desc, int device, lrs_conv **out);
