@@ -389,7 +389,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       const int wr = (th - 1) * g.sh + kh;
       if (wr > 256) continue;
       for (int ns = 4; ns >= 2; --ns) {
-        if (acc + 4 * ns > 512) continue;
+        if (acc + 8 * ns > 512) continue;
         const uint32_t xw = static_cast<uint32_t>(wr) * wcw * 1024u;
         const uint32_t tw = static_cast<uint32_t>(th) * tbw * 8u * sw_t;
         // slack: positions read past the end of a window by the last (padded) MMA rows
@@ -597,7 +597,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   w.ns = best_ns;
   const uint32_t acc = best_acc;
   w.acc_cols = acc;
-  w.nacc = (2 * acc + 4 * best_ns <= 512) ? 2 : 1;  // double-buffered accumulators: epilogue overlaps MMAs
+  w.nacc = (2 * acc + 8 * best_ns <= 512) ? 2 : 1;  // double-buffered accumulators: epilogue overlaps MMAs
   w.e_col0 = w.nacc * acc;
   w.tmem_cols = 512;  // whole TMEM: base address 0 (lrs_wconv_kernel relies on it)
   w.nwb = best_nwb;

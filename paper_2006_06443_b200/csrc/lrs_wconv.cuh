@@ -55,7 +55,7 @@ constexpr int kWMaxSlots = 6;
 constexpr int kWMaxWin = 4;  // window buffers in the ring
 constexpr int kWMaxUnits = 8;
 constexpr uint32_t kASlotBytes = 16384;  // dense A box 128 x 128 B, or sparse 128 x 64 B
-constexpr uint32_t kESlotBytes = 2048;   // metadata 128 lanes x 16 B
+constexpr uint32_t kESlotBytes = 4096;   // metadata of 2 sparse blocks: 2 x (128 lanes x 16 B)
 constexpr uint32_t kEpiScratch = 2048;   // per epilogue warp: 32 columns x 32 channels bf16
 
 struct WconvParams {
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   uint64_t* acc_full = a_empty + kWMaxSlots;  // [2]
   uint64_t* acc_empty = acc_full + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  const uint32_t slot_info = smem_u32(tmem_slot + 4);  // [kWMaxSlots] u32, written by the producer
+  const uint32_t slot_info = smem_u32(tmem_slot + 4);  // [kWMaxSlots][2] u32, written by the producer
 
   if (p.trace && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
   const int taps = p.kh * p.kw;
@@ -195,26 +195,49 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             const int c = w - p.n_tk;
             mbar_arrive_expect_tx(&win_full[buf], p.x_win_bytes);
             tma_load_4d(wdst, &p.tmX, &win_full[buf], c * 64, tc.n0, tc.wo0 * p.sw - p.pw, tc.ho0 * p.sh - p.ph);
+            // sparse blocks of this window in (tap, main/residual) order, packed two per
+            // slot (one item): fewer producer <-> MMA hand-offs per window
             const int key0 = (tc.mt * p.n_ck + c) * taps;
-            for (int t = 0; t < taps; ++t) {
-              const int rblk = __ldg(p.res_block + key0 + t);
+            int pend_blk = -1;
+            uint32_t pend_tap = 0;
+            for (int t = 0; t <= taps; ++t) {
+              const int rblk = t < taps ? __ldg(p.res_block + key0 + t) : -1;
               const int ty = t / p.kw, tx = t - ty * p.kw;
               const uint32_t tap16 = static_cast<uint32_t>(ty * p.wc + tx) * 64u;  // (pos * 1024) >> 4
               for (int part = 0; part < 2; ++part) {
-                const int blk = part == 0 ? key0 + t : rblk;
-                if (blk < 0) continue;
-                const bool last = t == taps - 1 && (part == 1 || rblk < 0);
+                int blk = -1;
+                if (t < taps) blk = part == 0 ? key0 + t : rblk;
+                if (blk < 0 && !(t == taps && part == 0)) continue;
+                // blk >= 0: a block to place; t == taps: flush a pending half-filled item
+                if (blk >= 0 && pend_blk < 0) {
+                  pend_blk = blk;
+                  pend_tap = tap16;
+                  continue;
+                }
+                if (pend_blk < 0) continue;
+                const int nb = blk >= 0 ? 2 : 1;
+                const bool last = (t == taps - 1 && (part == 1 || rblk < 0)) || t == taps;
                 const int slot = it % p.ns;
                 if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
-                st_shared_u32(slot_info + 4u * slot, tap16 | (last ? 0x80000000u : 0u));
+                st_shared_u32(slot_info + 8u * slot, pend_tap | (static_cast<uint32_t>(nb) << 29) |
+                                                       (last ? 0x80000000u : 0u));
+                st_shared_u32(slot_info + 8u * slot + 4u, nb == 2 ? tap16 : 0u);
                 if (p.dbg & 2) {
                   mbar_arrive(&a_full[slot]);
                 } else {
-                  mbar_arrive_expect_tx(&a_full[slot], 8192u + kESlotBytes);
-                  tma_load_2d(smem + p.off_a + slot * kASlotBytes, &p.tmAs, &a_full[slot], 0, blk * 128);
-                  tma_load_2d(smem + p.off_e + slot * kESlotBytes, &p.tmE, &a_full[slot], 0, blk * 128);
+                  mbar_arrive_expect_tx(&a_full[slot], static_cast<uint32_t>(nb) * (8192u + 2048u));
+                  uint8_t* ad = smem + p.off_a + slot * kASlotBytes;
+                  uint8_t* ed = smem + p.off_e + slot * kESlotBytes;
+                  tma_load_2d(ad, &p.tmAs, &a_full[slot], 0, pend_blk * 128);
+                  tma_load_2d(ed, &p.tmE, &a_full[slot], 0, pend_blk * 128);
+                  if (nb == 2) {
+                    tma_load_2d(ad + 8192, &p.tmAs, &a_full[slot], 0, blk * 128);
+                    tma_load_2d(ed + 2048, &p.tmE, &a_full[slot], 0, blk * 128);
+                  }
                 }
                 ++it;
+                pend_blk = -1;
+                if (t == taps) break;
               }
             }
           }
@@ -290,26 +313,32 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           while (true) {
             mbar_wait(&a_full[slot], ph);
             tc_fence_after();
-            const uint32_t info = ld_shared_u32(slot_info + 4u * slot);
-            const uint32_t tap16 = info & 0x7FFFFFFFu;
-            const uint32_t et = tmem + p.e_col0 + 4u * slot;
+            const uint32_t info0 = ld_shared_u32(slot_info + 8u * slot);
+            const uint32_t info1 = ld_shared_u32(slot_info + 8u * slot + 4u);
+            const int nb = static_cast<int>((info0 >> 29) & 3u);
+            const uint32_t et = tmem + p.e_col0 + 8u * slot;
             const uint64_t ab = ad_sp + slot * slot_a16;
             if (elect_one()) {
-              if (!(p.dbg & 1)) tmem_cp_128x128b(et, ed0 + slot * slot_e16);
+              for (int bi = 0; bi < nb; ++bi) {
+                const uint32_t tap16 = (bi == 0 ? info0 : info1) & 0x1FFFFFFFu;
+                const uint32_t ebi = et + 4u * static_cast<uint32_t>(bi);
+                if (!(p.dbg & 1)) tmem_cp_128x128b(ebi, ed0 + slot * slot_e16 + static_cast<uint32_t>(bi) * 128u);
 #pragma unroll
-              for (int s2 = 0; s2 < 2 && !(p.dbg & 1); ++s2) {
+                for (int s2 = 0; s2 < 2 && !(p.dbg & 1); ++s2) {
 #pragma unroll
-                for (int u = 0; u < kWMaxUnits; ++u) {
-                  if (u < nu)
-                    mma_sp_bf16(dcol[u] + acc0, ab + 2 * s2, bxd[u] + boff + tap16 + 4 * s2,
-                                idu[u] | (1u << 2) | static_cast<uint32_t>(s2), 1u, et);
+                  for (int u = 0; u < kWMaxUnits; ++u) {
+                    if (u < nu)
+                      mma_sp_bf16(dcol[u] + acc0, ab + static_cast<uint32_t>(bi) * 512u + 2 * s2,
+                                  bxd[u] + boff + tap16 + 4 * s2, idu[u] | (1u << 2) | static_cast<uint32_t>(s2), 1u,
+                                  ebi);
+                  }
                 }
               }
               mma_commit(&a_empty[slot]);
             }
             __syncwarp();
             if (++slot == p.ns) { slot = 0; ph ^= 1u; }
-            if (info >> 31) break;
+            if (info0 >> 31) break;
           }
         }
         if (elect_one()) mma_commit(&win_empty[buf]);
