@@ -302,6 +302,26 @@ uint32_t plan_stage(GemmParams& p, bool f32, int k_bytes_total, uint32_t sw, int
   return 0;
 }
 
+// Every kernel is launched with programmatic stream serialization (PDL): it may
+// start while the previous kernel in the stream drains; the kernels call
+// griddepcontrol.wait after their prologue (barrier init, TMEM alloc,
+// descriptor prefetch) and before touching memory.  Captured into CUDA graphs
+// as programmatic edges.
+cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void* param, size_t smem, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {param};
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 lrs_status launch(lrs_conv* h, int si, Stage& st, dim3 grid, cudaStream_t stream) {
   TimingRing& r = h->ring[si];
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -316,8 +336,7 @@ lrs_status launch(lrs_conv* h, int si, Stage& st, dim3 grid, cudaStream_t stream
     r.used += 2;
     LRS_CUDA(cudaEventRecord(e0, stream));
   }
-  void* args[] = {&st.p};
-  LRS_CUDA(cudaLaunchKernel(kernel_ptr(st.kid), grid, dim3(kThreads), args, st.smem, stream));
+  LRS_CUDA(launch_pdl(kernel_ptr(st.kid), grid, dim3(kThreads), &st.p, st.smem, stream));
   if (h->timing) LRS_CUDA(cudaEventRecord(e1, stream));
   return LRS_OK;
 }
@@ -345,18 +364,20 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   const int n_tk = rp / t_kc;
   const uint32_t sw_t = static_cast<uint32_t>(t_kc) * 2u;
   const bool s1 = g.sh == 1 && g.sw == 1;
-  struct Unit { int col, n, xpos, tpos, r0, wo0, pitch, nw, rows; };
+  struct Unit { int col, n, xpos, tpos, r0, wo0, pitch, nw, rows, q0; };
   // MMA units covering a tile of th output rows x tc output columns (see lrs_wconv.cuh);
   // wcw = window width, tbw = T window row pitch
   auto make_units = [&](int th, int tc, int wcw, int tbw, std::vector<Unit>& us) -> int {
     us.clear();
     int col = 0;
-    if (s1 && wcw <= 32) {
-      const int rpu = std::max(1, 32 / wcw);
-      for (int r0 = 0; r0 < th; r0 += rpu) {
-        const int rows = std::min(rpu, th - r0);
-        const int npos = (rows - 1) * wcw + tc;
-        Unit u{col, round_up(8 * npos, 16), r0 * wcw, r0 * tbw, r0, 0, wcw, tc, rows};
+    if (s1) {
+      // stride 1: the tile's outputs are positions q = r * wcw + c of the window
+      // (c >= tc are the window's padding columns, computed and discarded); a unit
+      // is a run of <= 32 consecutive positions, whatever rows it spans
+      const int npos = (th - 1) * wcw + tc;
+      for (int q0 = 0; q0 < npos; q0 += 32) {
+        const int np = std::min(32, npos - q0);
+        Unit u{col, round_up(8 * np, 16), q0, q0, 0, 0, wcw, tc, th, q0};
         us.push_back(u);
         col += u.n;
       }
@@ -366,7 +387,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       for (int r = 0; r < th; ++r)
         for (int q = 0; q < nsplit; ++q) {
           const int wo0 = q * wsplit, nw = std::min(wsplit, tc - wo0);
-          Unit u{col, round_up(8 * nw, 16), r * g.sh * wcw + wo0 * g.sw, r * tbw + wo0, r, wo0, nw, nw, 1};
+          Unit u{col, round_up(8 * nw, 16), r * g.sh * wcw + wo0 * g.sw, r * tbw + wo0, r, wo0, nw, nw, 1, 0};
           us.push_back(u);
           col += u.n;
         }
@@ -583,6 +604,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     w.u_pitch[i] = u.pitch;
     w.u_nw[i] = u.nw;
     w.u_rows[i] = u.rows;
+    w.u_q0[i] = u.q0;
   }
   w.tbox_w = tbox_w;
   w.n_ck = n_ck;
@@ -961,9 +983,8 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
       r.used += 2;
       LRS_CUDA(cudaEventRecord(e0, stream));
     }
-    void* args[] = {&w};
-    LRS_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(&lrs_wconv_kernel), dim3(grid), dim3(kWThreads), args,
-                              h->w_smem, stream));
+    LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_wconv_kernel), dim3(grid), dim3(kWThreads), &w,
+                        h->w_smem, stream));
     if (h->timing) LRS_CUDA(cudaEventRecord(e1, stream));
     if (prev != h->device) cudaSetDevice(prev);
     return LRS_OK;

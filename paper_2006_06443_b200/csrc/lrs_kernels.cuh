@@ -194,6 +194,10 @@ __global__ void __launch_bounds__(kThreads, 1) lrs_gemm_kernel(const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: the prologue above overlapped the previous kernel's tail; from here on
+  // we read its outputs (and overwrite buffers it may read)
+  pdl_launch_dependents();
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {

@@ -247,6 +247,13 @@ __device__ __forceinline__ void sts_u16(uint32_t saddr, uint16_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(saddr), "h"(v) : "memory");
 }
 
+// Programmatic dependent launch: let the next kernel in the stream start its
+// prologue now / wait until the previous kernel's memory is visible.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // one lane of the (fully active) warp returns true
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;

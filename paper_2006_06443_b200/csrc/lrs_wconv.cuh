@@ -81,6 +81,7 @@ struct WconvParams {
   int u_pitch[kWMaxUnits]; // columns/8 per output row inside the unit
   int u_nw[kWMaxUnits];    // real output columns per row
   int u_rows[kWMaxUnits];  // output rows covered
+  int u_q0[kWMaxUnits];    // first virtual position of the unit (pitch-major: row = q / pitch)
   int tbox_w;              // width of the T window box (its row pitch)
   unsigned long long* trace;  // optional: globaltimer stamps (debug, lrs_conv_debug_trace)
   int dbg;                 // debug experiment bits (0 in production)
@@ -172,6 +173,9 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     __trap();
   }
   constexpr uint32_t tmem = 0u;
+  // PDL: the prologue above overlapped the previous kernel's tail
+  pdl_launch_dependents();
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -367,7 +371,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       const int jw = tc.j0 + q4 * 32;  // first channel of this warp
       for (int u = 0; u < p.n_units; ++u) {
         const int pitch = p.u_pitch[u], nw = p.u_nw[u], un = p.u_n[u], rows = p.u_rows[u];
-        const int r0 = p.u_r0[u], w0 = p.u_wo0[u], ucol = p.u_col[u];
+        const int r0 = p.u_r0[u], w0 = p.u_wo0[u], ucol = p.u_col[u], q0 = p.u_q0[u];
         for (int c0 = ehalf * 32; c0 < un; c0 += 64) {
           uint32_t v[32];
           tmem_ld32_nowait(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + acc0 + static_cast<uint32_t>(ucol + c0),
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             const int cidx = c0 + col;
             const uint4 val = lds_v4(scr + static_cast<uint32_t>(col * 64 + part * 16));
             if (cidx >= un) continue;
-            const int qv = cidx >> 3, img = cidx & 7;
+            const int qv = q0 + (cidx >> 3), img = cidx & 7;
             const int rr = qv / pitch, cc = qv - rr * pitch;
             const int n = tc.n0 + img, ho = tc.ho0 + r0 + rr, wo = tc.wo0 + w0 + cc;
             if (cc < nw && rr < rows && n < p.n && ho < p.ho && wo < p.wo && jch < p.cout)
