@@ -395,7 +395,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     return col;
   };
   std::vector<Unit> units, best_units;
-  int best_th = 0, best_ns = 0, best_tc = 0, best_wc = 0, best_tbw = 0, best_nwb = 2;
+  int best_th = 0, best_ns = 0, best_tc = 0, best_wc = 0, best_tbw = 0, best_nwb = 2, best_bpi = 2;
   long long best_cost = 1LL << 60;
   uint32_t best_stride = 0, best_xw = 0, best_tw = 0, best_total = 0, best_acc = 0;
   for (int cb = 1; cb <= 16 && !best_th; ++cb) {  // column bands: as few as fit
@@ -409,8 +409,16 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       if (static_cast<int>(units.size()) > kWMaxUnits) continue;
       const int wr = (th - 1) * g.sh + kh;
       if (wr > 256) continue;
-      for (int ns = 4; ns >= 2; --ns) {
-        if (acc + 8 * ns > 512) continue;
+      const int ns_max = getenv("LRS_WCONV_NS") ? atoi(getenv("LRS_WCONV_NS")) : kWMaxSlots;
+      const int bpi_max = getenv("LRS_WCONV_BPI") ? atoi(getenv("LRS_WCONV_BPI")) : kWMaxBpi;
+      // (blocks per item, slots): prefer big items, then more slots
+      const int cand[][2] = {{4, 3}, {4, 2}, {2, 4}, {2, 3}, {2, 2}};
+      for (const auto& cnd : cand) {
+        const int bpi = cnd[0], ns = cnd[1];
+        if (bpi > bpi_max || ns > ns_max) continue;
+        const uint32_t a_slot = static_cast<uint32_t>(bpi) * kSpBlockBytes;  // >= 16 KB dense box
+        const uint32_t e_slot = static_cast<uint32_t>(bpi) * kEBlockBytes;
+        if (acc + 4 * bpi * ns > 512) continue;
         const uint32_t xw = static_cast<uint32_t>(wr) * wcw * 1024u;
         const uint32_t tw = static_cast<uint32_t>(th) * tbw * 8u * sw_t;
         // slack: positions read past the end of a window by the last (padded) MMA rows
@@ -424,7 +432,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         const long long slack_t = std::max(0LL, last_t + 1 - static_cast<long long>(th) * tbw) * 8 * sw_t;
         const uint32_t stride =
             align1024(static_cast<uint32_t>(std::max<long long>(xw + slack_x, tw + slack_t)));
-        const uint32_t fixed = ns * (kASlotBytes + kESlotBytes) + 8 * kEpiScratch + 1024 + 1024;
+        const uint32_t fixed = ns * (a_slot + e_slot) + 8 * kEpiScratch + 1024 + 1024;
         if (2 * stride + fixed > static_cast<uint32_t>(kMaxSmem)) continue;
         int nwb = 2;
         while (nwb < kWMaxWin && (nwb + 1) * stride + fixed <= static_cast<uint32_t>(kMaxSmem)) ++nwb;
@@ -433,10 +441,12 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         // sparse MMA costs max(~100 issue, (A 4 KB + B N*64 B) / 128 B/clk smem), an item
         // (one tap of a 64-channel chunk: 2 MMA steps per unit) adds ~200; CTAs run in
         // waves of one per SM.
-        long long item = 200;
+        long long item = 450 / bpi;  // per-block share of the item's hand-off + commit
         for (const Unit& u : units) item += 2 * std::max<long long>(100, (4096 + 64LL * u.n) / 128);
         const long long ctas = static_cast<long long>((d->batch_max + 7) / 8) * ((ho + th - 1) / th) * cb * n_mt;
         const long long waves = (ctas + h->sms - 1) / h->sms;
+        // waves x per-block cost: favours few, large tiles (per-tile fixed costs -- window
+        // halos, prologue, epilogue -- are not modelled; small tiles measured slower)
         const long long cost = waves * item;
         if (cost < best_cost) {
           best_cost = cost;
@@ -450,6 +460,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
           best_tw = tw;
           best_total = total;
           best_nwb = nwb;
+          best_bpi = bpi;
           best_acc = static_cast<uint32_t>(acc);
           best_units = units;
         }
@@ -619,16 +630,23 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   w.ns = best_ns;
   const uint32_t acc = best_acc;
   w.acc_cols = acc;
-  w.nacc = (2 * acc + 8 * best_ns <= 512) ? 2 : 1;  // double-buffered accumulators: epilogue overlaps MMAs
+  w.bpi = best_bpi;
+  w.a_slot = static_cast<uint32_t>(best_bpi) * kSpBlockBytes;
+  w.e_slot = static_cast<uint32_t>(best_bpi) * kEBlockBytes;
+  // double-buffered accumulators (epilogue overlaps MMAs) when two fit next to the metadata columns
+  w.nacc = (2 * acc + 4 * best_bpi * best_ns <= 512) ? 2 : 1;
   w.e_col0 = w.nacc * acc;
   w.tmem_cols = 512;  // whole TMEM: base address 0 (lrs_wconv_kernel relies on it)
   w.nwb = best_nwb;
   w.off_a = best_nwb * best_stride;
-  w.off_e = w.off_a + best_ns * kASlotBytes;
-  w.off_epi = w.off_e + best_ns * kESlotBytes;
+  w.off_e = w.off_a + best_ns * w.a_slot;
+  w.off_epi = w.off_e + best_ns * w.e_slot;
   w.off_bar = w.off_epi + 8 * kEpiScratch;
   h->w_smem = best_total;
   h->use_w = true;
+  if (getenv("LRS_VERBOSE"))
+    fprintf(stderr, "lrs_wconv plan: th %d tcols %d units %d acc %u nacc %d ns %d bpi %d nwb %d win %u B smem %u B tiles/img-group %d\n",
+            th, tcols, w.n_units, acc, w.nacc, w.ns, w.bpi, w.nwb, best_stride, best_total, w.bands * w.cbands * w.n_mt);
   return LRS_OK;
 }
 }  // namespace
@@ -958,6 +976,7 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
                           static_cast<uint64_t>(d.in_h)};
       uint64_t strides[3] = {static_cast<uint64_t>(d.in_h) * d.in_w * d.c_in * 2, static_cast<uint64_t>(d.c_in) * 2,
                              static_cast<uint64_t>(d.in_w) * d.c_in * 2};
+      if (w.dbg & 32) strides[0] = 128;  // timing experiment: contiguous 1 KB per position (wrong data)
       uint32_t box[4] = {64, 8, static_cast<uint32_t>(w.wc), static_cast<uint32_t>(w.wr)};
       uint32_t estr[4] = {1, 1, 1, 1};
       if ((st = encode_t(&w.tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box,

@@ -54,8 +54,9 @@ constexpr int kWThreads = 320;  // warps 0 producer, 1 MMA, 2..9 epilogue (2 per
 constexpr int kWMaxSlots = 6;
 constexpr int kWMaxWin = 4;  // window buffers in the ring
 constexpr int kWMaxUnits = 8;
-constexpr uint32_t kASlotBytes = 16384;  // dense A box 128 x 128 B, or sparse 128 x 64 B
-constexpr uint32_t kESlotBytes = 4096;   // metadata of 2 sparse blocks: 2 x (128 lanes x 16 B)
+constexpr int kWMaxBpi = 4;              // sparse blocks per pipeline item
+constexpr uint32_t kSpBlockBytes = 8192;  // one compressed 2:4 block: 128 rows x 64 B
+constexpr uint32_t kEBlockBytes = 2048;   // its metadata: 128 lanes x 16 B
 constexpr uint32_t kEpiScratch = 2048;   // per epilogue warp: 32 columns x 32 channels bf16
 
 struct WconvParams {
@@ -90,6 +91,8 @@ struct WconvParams {
   int wr, wc;
   uint32_t x_win_bytes, t_win_bytes, win_stride;
   int ns;
+  int bpi;              // sparse blocks per item (2..kWMaxBpi); A slot = bpi * 8 KB, E slot = bpi * 2 KB
+  uint32_t a_slot, e_slot;
   int nwb;              // window buffers (2..kWMaxWin)
   int nacc;             // accumulator buffers in TMEM (1 or 2)
   uint32_t acc_cols;    // TMEM columns of one accumulator buffer
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   uint64_t* acc_full = a_empty + kWMaxSlots;  // [2]
   uint64_t* acc_empty = acc_full + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  const uint32_t slot_info = smem_u32(tmem_slot + 4);  // [kWMaxSlots][2] u32, written by the producer
+  const uint32_t slot_info = smem_u32(tmem_slot + 4);  // [kWMaxSlots][kWMaxBpi] u32, written by the producer
 
   if (p.trace && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
   const int taps = p.kh * p.kw;
@@ -187,61 +190,68 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         for (int w = 0; w < nwin; ++w, ++wg) {
           if (wg >= p.nwb) mbar_wait(&win_empty[buf], wph ^ 1u);
           uint8_t* wdst = smem + buf * p.win_stride;
-          if (w < p.n_tk) {
+          if (p.dbg & 64) {
+            mbar_arrive(&win_full[buf]);
+          } else if (w < p.n_tk) {
             mbar_arrive_expect_tx(&win_full[buf], p.t_win_bytes);
             tma_load_4d(wdst, &p.tmT, &win_full[buf], w * p.t_kc, tc.n0, tc.wo0, tc.ho0);
+          }
+          if (w < p.n_tk) {
             const int slot = it % p.ns;
             if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
             mbar_arrive_expect_tx(&a_full[slot], 128u * p.sw_t);
-            tma_load_2d(smem + p.off_a + slot * kASlotBytes, &p.tmAd, &a_full[slot], w * p.t_kc, tc.j0);
+            tma_load_2d(smem + p.off_a + slot * p.a_slot, &p.tmAd, &a_full[slot], w * p.t_kc, tc.j0);
             ++it;
           } else {
             const int c = w - p.n_tk;
-            mbar_arrive_expect_tx(&win_full[buf], p.x_win_bytes);
-            tma_load_4d(wdst, &p.tmX, &win_full[buf], c * 64, tc.n0, tc.wo0 * p.sw - p.pw, tc.ho0 * p.sh - p.ph);
-            // sparse blocks of this window in (tap, main/residual) order, packed two per
-            // slot (one item): fewer producer <-> MMA hand-offs per window
+            if (!(p.dbg & 64)) {
+              mbar_arrive_expect_tx(&win_full[buf], p.x_win_bytes);
+              tma_load_4d(wdst, &p.tmX, &win_full[buf], c * 64, tc.n0, tc.wo0 * p.sw - p.pw, tc.ho0 * p.sh - p.ph);
+            }
+            // sparse blocks of this window in (tap, main/residual) order, packed bpi per
+            // slot (one item): every item costs an mbarrier hand-off and a tcgen05.commit
+            // (~450 cycles, tools/mma_rate2.cu), so items are made as large as smem allows
             const int key0 = (tc.mt * p.n_ck + c) * taps;
-            int pend_blk = -1;
-            uint32_t pend_tap = 0;
-            for (int t = 0; t <= taps; ++t) {
-              const int rblk = t < taps ? __ldg(p.res_block + key0 + t) : -1;
+            int pb[kWMaxBpi];
+            uint32_t pt[kWMaxBpi];
+            int np = 0;
+            for (int t = 0; t < taps; ++t) {
+              const int rblk = __ldg(p.res_block + key0 + t);
               const int ty = t / p.kw, tx = t - ty * p.kw;
               const uint32_t tap16 = static_cast<uint32_t>(ty * p.wc + tx) * 64u;  // (pos * 1024) >> 4
               for (int part = 0; part < 2; ++part) {
-                int blk = -1;
-                if (t < taps) blk = part == 0 ? key0 + t : rblk;
-                if (blk < 0 && !(t == taps && part == 0)) continue;
-                // blk >= 0: a block to place; t == taps: flush a pending half-filled item
-                if (blk >= 0 && pend_blk < 0) {
-                  pend_blk = blk;
-                  pend_tap = tap16;
-                  continue;
-                }
-                if (pend_blk < 0) continue;
-                const int nb = blk >= 0 ? 2 : 1;
-                const bool last = (t == taps - 1 && (part == 1 || rblk < 0)) || t == taps;
+                const int blk = part == 0 ? key0 + t : rblk;
+                if (blk < 0) continue;
+#pragma unroll
+                for (int q = 0; q < kWMaxBpi; ++q)
+                  if (q == np) { pb[q] = blk; pt[q] = tap16; }
+                ++np;
+                const bool last = t == taps - 1 && (part == 1 || rblk < 0);
+                if (np < p.bpi && !last) continue;
                 const int slot = it % p.ns;
                 if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
-                st_shared_u32(slot_info + 8u * slot, pend_tap | (static_cast<uint32_t>(nb) << 29) |
-                                                       (last ? 0x80000000u : 0u));
-                st_shared_u32(slot_info + 8u * slot + 4u, nb == 2 ? tap16 : 0u);
+#pragma unroll
+                for (int q = 0; q < kWMaxBpi; ++q)
+                  if (q < np)
+                    st_shared_u32(slot_info + 4u * (kWMaxBpi * slot + q),
+                                  pt[q] | (q == 0 ? (static_cast<uint32_t>(np) << 28) | (last ? 0x80000000u : 0u)
+                                                  : 0u));
                 if (p.dbg & 2) {
                   mbar_arrive(&a_full[slot]);
                 } else {
-                  mbar_arrive_expect_tx(&a_full[slot], static_cast<uint32_t>(nb) * (8192u + 2048u));
-                  uint8_t* ad = smem + p.off_a + slot * kASlotBytes;
-                  uint8_t* ed = smem + p.off_e + slot * kESlotBytes;
-                  tma_load_2d(ad, &p.tmAs, &a_full[slot], 0, pend_blk * 128);
-                  tma_load_2d(ed, &p.tmE, &a_full[slot], 0, pend_blk * 128);
-                  if (nb == 2) {
-                    tma_load_2d(ad + 8192, &p.tmAs, &a_full[slot], 0, blk * 128);
-                    tma_load_2d(ed + 2048, &p.tmE, &a_full[slot], 0, blk * 128);
+                  mbar_arrive_expect_tx(&a_full[slot], static_cast<uint32_t>(np) * (kSpBlockBytes + kEBlockBytes));
+                  uint8_t* ad = smem + p.off_a + slot * p.a_slot;
+                  uint8_t* ed = smem + p.off_e + slot * p.e_slot;
+#pragma unroll
+                  for (int q = 0; q < kWMaxBpi; ++q) {
+                    if (q < np) {
+                      tma_load_2d(ad + q * kSpBlockBytes, &p.tmAs, &a_full[slot], 0, pb[q] * 128);
+                      tma_load_2d(ed + q * kEBlockBytes, &p.tmE, &a_full[slot], 0, pb[q] * 128);
+                    }
                   }
                 }
                 ++it;
-                pend_blk = -1;
-                if (t == taps) break;
+                np = 0;
               }
             }
           }
@@ -274,7 +284,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const uint64_t ad_dense = umma_desc(smem_u32(smem + p.off_a), p.sw_t);
     const uint64_t ad_sp = umma_desc(smem_u32(smem + p.off_a), 64);
     const uint64_t ed0 = umma_desc_rows16(smem_u32(smem + p.off_e));
-    const uint32_t slot_a16 = kASlotBytes >> 4, slot_e16 = kESlotBytes >> 4;
+    const uint32_t slot_a16 = p.a_slot >> 4, slot_e16 = p.e_slot >> 4;
     const uint32_t win16 = p.win_stride >> 4;
     const int ksteps = static_cast<int>(p.sw_t / 32);
     int slot = 0, k = 0, buf = 0;
@@ -317,22 +327,23 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           while (true) {
             mbar_wait(&a_full[slot], ph);
             tc_fence_after();
-            const uint32_t info0 = ld_shared_u32(slot_info + 8u * slot);
-            const uint32_t info1 = ld_shared_u32(slot_info + 8u * slot + 4u);
-            const int nb = static_cast<int>((info0 >> 29) & 3u);
-            const uint32_t et = tmem + p.e_col0 + 8u * slot;
+            const uint32_t info0 = ld_shared_u32(slot_info + 4u * kWMaxBpi * slot);
+            const int nb = static_cast<int>((info0 >> 28) & 7u);
+            const uint32_t et = tmem + p.e_col0 + 4u * static_cast<uint32_t>(p.bpi) * slot;
             const uint64_t ab = ad_sp + slot * slot_a16;
             if (elect_one()) {
               for (int bi = 0; bi < nb; ++bi) {
-                const uint32_t tap16 = (bi == 0 ? info0 : info1) & 0x1FFFFFFFu;
+                const uint32_t tap16 =
+                    (bi == 0 ? info0 : ld_shared_u32(slot_info + 4u * (kWMaxBpi * slot + bi))) & 0x0FFFFFFFu;
                 const uint32_t ebi = et + 4u * static_cast<uint32_t>(bi);
-                if (!(p.dbg & 1)) tmem_cp_128x128b(ebi, ed0 + slot * slot_e16 + static_cast<uint32_t>(bi) * 128u);
+                if (!(p.dbg & 5))
+                  tmem_cp_128x128b(ebi, ed0 + slot * slot_e16 + static_cast<uint32_t>(bi) * (kEBlockBytes >> 4));
 #pragma unroll
-                for (int s2 = 0; s2 < 2 && !(p.dbg & 1); ++s2) {
+                for (int s2 = 0; s2 < ((p.dbg & 8) ? 1 : 2) && !(p.dbg & 1); ++s2) {
 #pragma unroll
                   for (int u = 0; u < kWMaxUnits; ++u) {
                     if (u < nu)
-                      mma_sp_bf16(dcol[u] + acc0, ab + static_cast<uint32_t>(bi) * 512u + 2 * s2,
+                      mma_sp_bf16(dcol[u] + acc0, ab + static_cast<uint32_t>(bi) * (kSpBlockBytes >> 4) + 2 * s2,
                                   bxd[u] + boff + tap16 + 4 * s2, idu[u] | (1u << 2) | static_cast<uint32_t>(s2), 1u,
                                   ebi);
                   }
@@ -366,6 +377,12 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       const int use = p.nacc == 2 ? (k >> 1) : k;
       mbar_wait_sleep(&acc_full[b], use & 1);
       tc_fence_after();
+      if (p.dbg & 16) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[b]);
+        continue;
+      }
       if (p.trace && blockIdx.x == 0 && threadIdx.x == 64 && k < 16) p.trace[100 + 4 * k + 2] = gtimer();
       const uint32_t acc0 = static_cast<uint32_t>(b) * p.acc_cols;
       const int jw = tc.j0 + q4 * 32;  // first channel of this warp

@@ -52,7 +52,8 @@ int main() {
   cudaMalloc(&d, 4096 * 8);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   const int items = 2000;
-  struct C { int n, nmma, cp, mv, same, wt; } cs[] = {{224, 2, 1, 1, 1, 0}, {224, 2, 1, 1, 1, 1}, {224, 2, 0, 1, 1, 1}};
+  struct C { int n, nmma, cp, mv, same, wt; } cs[] = {{224, 0, 0, 1, 1, 0}, {224, 0, 1, 1, 1, 0}, {224, 0, 0, 1, 1, 1},
+                                                       {224, 2, 1, 1, 1, 0}};
   for (auto c : cs) {
     k<<<148, 128, 200 * 1024>>>(c.n, c.nmma, c.cp, c.mv, items, d, c.same, c.wt);
     cudaError_t e = cudaDeviceSynchronize();
@@ -63,7 +64,7 @@ int main() {
     for (int i = 0; i < 148; ++i) avg += h[i];
     avg /= 148;
     printf("wait=%d sameD=%d ", c.wt, c.same); printf("N=%3d mma/item=%d cp=%d moveB=%d: %7.1f cycles/item, %6.1f cycles/MMA, %5.0f logical MAC/clk/SM\n", c.n,
-           c.nmma, c.cp, c.mv, avg / items, avg / items / c.nmma, 128.0 * c.n * 32 * c.nmma / (avg / items));
+           c.nmma, c.cp, c.mv, avg / items, avg / items / (c.nmma ? c.nmma : 1), 128.0 * c.n * 32 * c.nmma / (avg / items));
   }
   return 0;
 }
