@@ -445,9 +445,12 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         for (const Unit& u : units) item += 2 * std::max<long long>(100, (4096 + 64LL * u.n) / 128);
         const long long ctas = static_cast<long long>((d->batch_max + 7) / 8) * ((ho + th - 1) / th) * cb * n_mt;
         const long long waves = (ctas + h->sms - 1) / h->sms;
-        // waves x per-block cost: favours few, large tiles (per-tile fixed costs -- window
-        // halos, prologue, epilogue -- are not modelled; small tiles measured slower)
-        const long long cost = waves * item;
+        // waves x per-tile cost: the tile's blocks x per-block cost, plus the epilogue
+        // (~30 cycles per accumulator column, measured with tools/wtrace) unless two
+        // accumulators fit in TMEM and it overlaps the next tile's MMAs
+        const long long tile_mma = static_cast<long long>(n_tk + n_ck * taps) * item;
+        const bool dbl = 2 * acc + 4 * bpi * ns <= 512;
+        const long long cost = waves * (tile_mma + (dbl ? 0LL : 30LL * acc));
         if (cost < best_cost) {
           best_cost = cost;
           best_th = th;
