@@ -97,7 +97,7 @@ struct WconvParams {
   int nacc;             // accumulator buffers in TMEM (1 or 2)
   uint32_t acc_cols;    // TMEM columns of one accumulator buffer
   uint32_t e_col0, tmem_cols;
-  uint32_t off_a, off_e, off_epi, off_bar;
+  uint32_t off_a, off_e, off_epi, off_res, off_bar;
 };
 
 struct TileCoord {
@@ -181,12 +181,19 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   pdl_wait();
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ TMA producer
-      int it = 0, wg = 0, buf = 0;
-      uint32_t wph = 0;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-        const TileCoord tc = tile_coord(p, tile);
+    // ---------------------------------------------------------------- TMA producer
+    // The warp stages the tile's residual-block table in shared memory (global
+    // loads on the issue path cost an L2 round trip each); lane 0 issues.
+    int* res_s = reinterpret_cast<int*>(smem + p.off_res);
+    const int nres = p.n_ck * taps;
+    int it = 0, wg = 0, buf = 0;
+    uint32_t wph = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+      const TileCoord tc = tile_coord(p, tile);
+      __syncwarp();
+      for (int i = lane; i < nres; i += 32) res_s[i] = __ldg(p.res_block + tc.mt * nres + i);
+      __syncwarp();
+      if (lane == 0) {
         for (int w = 0; w < nwin; ++w, ++wg) {
           if (wg >= p.nwb) mbar_wait(&win_empty[buf], wph ^ 1u);
           uint8_t* wdst = smem + buf * p.win_stride;
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             uint32_t pt[kWMaxBpi];
             int np = 0;
             for (int t = 0; t < taps; ++t) {
-              const int rblk = __ldg(p.res_block + key0 + t);
+              const int rblk = res_s[key0 - tc.mt * nres + t];
               const int ty = t / p.kw, tx = t - ty * p.kw;
               const uint32_t tap16 = static_cast<uint32_t>(ty * p.wc + tx) * 64u;  // (pos * 1024) >> 4
               for (int part = 0; part < 2; ++part) {
