@@ -480,10 +480,14 @@ def main():
     if dom == "a345_expand_sparse":
         wk = work[dom]
         achieved = wk["flops_sparse"] / t_dom / 1e12
+        eng = layer.sparse_engine[0]
         roof = {"bound": "alu", "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s",
                 "frac": achieved / fma_peak, "traffic": None, "kernel": dom,
-                "work": "sparse in-bounds MACs x 2 per launch (FP32 FMA pipe)",
-                "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz"}
+                "work": "sparse in-bounds MACs x 2 per launch (the sparse term's algorithmic work)",
+                "engine": ("2:4 sparse tensor cores (tcgen05.mma.sp), fused with the expansion GEMM" if eng == 1
+                           else "SIMT CSR gather fused into the expansion GEMM epilogue"),
+                "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (the sparse term's "
+                               "CUDA-core roof, SURVEY §8d three-roof)"}
     else:
         wk = work[dom]
         tc = peaks["bf16_tflops"] * (1.0 if cfg.dtype == "bf16" else 0.5 / 3.0)

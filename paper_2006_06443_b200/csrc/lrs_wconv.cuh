@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       const TileCoord tc = tile_coord(p, tile);
       const int b = p.nacc == 2 ? (k & 1) : 0;
       const int use = p.nacc == 2 ? (k >> 1) : k;
-      mbar_wait_sleep(&acc_full[b], use & 1);
+      if (p.dbg & 128) mbar_wait(&acc_full[b], use & 1); else mbar_wait_sleep(&acc_full[b], use & 1);
       tc_fence_after();
       if (p.dbg & 16) {
         tc_fence_before();
