@@ -236,7 +236,12 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                 const bool last = t == taps - 1 && (part == 1 || rblk < 0);
                 if (np < p.bpi && !last) continue;
                 const int slot = it % p.ns;
+                const unsigned long long pw0 = (p.trace && blockIdx.x == 0 && it < 64) ? gtimer() : 0ull;
                 if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
+                if (p.trace && blockIdx.x == 0 && it < 64) {
+                  p.trace[3000 + 3 * it] = pw0;
+                  p.trace[3000 + 3 * it + 1] = gtimer();
+                }
 #pragma unroll
                 for (int q = 0; q < kWMaxBpi; ++q)
                   if (q < np)
@@ -257,6 +262,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                     }
                   }
                 }
+                if (p.trace && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it + 2] = gtimer();
                 ++it;
                 np = 0;
               }
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const uint32_t slot_a16 = p.a_slot >> 4, slot_e16 = p.e_slot >> 4;
     const uint32_t win16 = p.win_stride >> 4;
     const int ksteps = static_cast<int>(p.sw_t / 32);
-    int slot = 0, k = 0, buf = 0;
+    int slot = 0, k = 0, buf = 0, itm = 0;
     uint32_t ph = 0, wph = 0;
     for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++k) {
       const TileCoord tc = tile_coord(p, tile);
@@ -332,8 +338,13 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           // sparse items of this window: the producer tags each slot with the
           // tap's window offset and whether it is the window's last item
           while (true) {
+            const unsigned long long mw0 = (p.trace && blockIdx.x == 0 && itm < 64) ? gtimer() : 0ull;
             mbar_wait(&a_full[slot], ph);
             tc_fence_after();
+            if (p.trace && blockIdx.x == 0 && itm < 64 && lane == 0) {
+              p.trace[3300 + 3 * itm] = mw0;
+              p.trace[3300 + 3 * itm + 1] = gtimer();
+            }
             const uint32_t info0 = ld_shared_u32(slot_info + 4u * kWMaxBpi * slot);
             const int nb = static_cast<int>((info0 >> 28) & 7u);
             const uint32_t et = tmem + p.e_col0 + 4u * static_cast<uint32_t>(p.bpi) * slot;
@@ -359,6 +370,8 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
               mma_commit(&a_empty[slot]);
             }
             __syncwarp();
+            if (p.trace && blockIdx.x == 0 && itm < 64 && lane == 0) p.trace[3300 + 3 * itm + 2] = gtimer();
+            ++itm;
             if (++slot == p.ns) { slot = 0; ph ^= 1u; }
             if (info0 >> 31) break;
           }

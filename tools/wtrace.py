@@ -28,3 +28,7 @@ for k in range(16):
     a, b, c, d = (t[100 + 4 * k + i] - t0 for i in range(4))
     ws = [(t[200 + 16 * k + 2 * w] - t0, t[200 + 16 * k + 2 * w + 1] - t0) for w in range(8) if t[200 + 16 * k + 2 * w]]
     print(f"tile {k}: mma start {a} end {b} | epi woke {c} done {d} | windows (wait, got): {ws}")
+pi = [(t[3000 + 3 * i] - t0, t[3000 + 3 * i + 1] - t0, t[3000 + 3 * i + 2] - t0) for i in range(64) if t[3000 + 3 * i]]
+mi = [(t[3300 + 3 * i] - t0, t[3300 + 3 * i + 1] - t0, t[3300 + 3 * i + 2] - t0) for i in range(64) if t[3300 + 3 * i]]
+print("producer items (wait a_empty, got, issued):", pi[:14])
+print("mma items (wait a_full, got, committed):", mi[:14])
