@@ -97,7 +97,7 @@ struct WconvParams {
   int nacc;             // accumulator buffers in TMEM (1 or 2)
   uint32_t acc_cols;    // TMEM columns of one accumulator buffer
   uint32_t e_col0, tmem_cols;
-  uint32_t off_a, off_e, off_epi, off_res, off_bar;
+  uint32_t off_a, off_e, off_epi, off_bar;
 };
 
 struct TileCoord {
@@ -181,19 +181,12 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   pdl_wait();
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- TMA producer
-    // The warp stages the tile's residual-block table in shared memory (global
-    // loads on the issue path cost an L2 round trip each); lane 0 issues.
-    int* res_s = reinterpret_cast<int*>(smem + p.off_res);
-    const int nres = p.n_ck * taps;
-    int it = 0, wg = 0, buf = 0;
-    uint32_t wph = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-      const TileCoord tc = tile_coord(p, tile);
-      __syncwarp();
-      for (int i = lane; i < nres; i += 32) res_s[i] = __ldg(p.res_block + tc.mt * nres + i);
-      __syncwarp();
-      if (lane == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      int it = 0, wg = 0, buf = 0;
+      uint32_t wph = 0;
+      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        const TileCoord tc = tile_coord(p, tile);
         for (int w = 0; w < nwin; ++w, ++wg) {
           if (wg >= p.nwb) mbar_wait(&win_empty[buf], wph ^ 1u);
           uint8_t* wdst = smem + buf * p.win_stride;
@@ -223,7 +216,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             uint32_t pt[kWMaxBpi];
             int np = 0;
             for (int t = 0; t < taps; ++t) {
-              const int rblk = res_s[key0 - tc.mt * nres + t];
+              const int rblk = __ldg(p.res_block + key0 + t);
               const int ty = t / p.kw, tx = t - ty * p.kw;
               const uint32_t tap16 = static_cast<uint32_t>(ty * p.wc + tx) * 64u;  // (pos * 1024) >> 4
               for (int part = 0; part < 2; ++part) {
@@ -236,12 +229,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                 const bool last = t == taps - 1 && (part == 1 || rblk < 0);
                 if (np < p.bpi && !last) continue;
                 const int slot = it % p.ns;
-                const unsigned long long pw0 = (p.trace && blockIdx.x == 0 && it < 64) ? gtimer() : 0ull;
                 if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
-                if (p.trace && blockIdx.x == 0 && it < 64) {
-                  p.trace[3000 + 3 * it] = pw0;
-                  p.trace[3000 + 3 * it + 1] = gtimer();
-                }
 #pragma unroll
                 for (int q = 0; q < kWMaxBpi; ++q)
                   if (q < np)
@@ -262,7 +250,6 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                     }
                   }
                 }
-                if (p.trace && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it + 2] = gtimer();
                 ++it;
                 np = 0;
               }
@@ -300,7 +287,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const uint32_t slot_a16 = p.a_slot >> 4, slot_e16 = p.e_slot >> 4;
     const uint32_t win16 = p.win_stride >> 4;
     const int ksteps = static_cast<int>(p.sw_t / 32);
-    int slot = 0, k = 0, buf = 0, itm = 0;
+    int slot = 0, k = 0, buf = 0;
     uint32_t ph = 0, wph = 0;
     for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++k) {
       const TileCoord tc = tile_coord(p, tile);
@@ -338,13 +325,8 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           // sparse items of this window: the producer tags each slot with the
           // tap's window offset and whether it is the window's last item
           while (true) {
-            const unsigned long long mw0 = (p.trace && blockIdx.x == 0 && itm < 64) ? gtimer() : 0ull;
             mbar_wait(&a_full[slot], ph);
             tc_fence_after();
-            if (p.trace && blockIdx.x == 0 && itm < 64 && lane == 0) {
-              p.trace[3300 + 3 * itm] = mw0;
-              p.trace[3300 + 3 * itm + 1] = gtimer();
-            }
             const uint32_t info0 = ld_shared_u32(slot_info + 4u * kWMaxBpi * slot);
             const int nb = static_cast<int>((info0 >> 28) & 7u);
             const uint32_t et = tmem + p.e_col0 + 4u * static_cast<uint32_t>(p.bpi) * slot;
@@ -370,8 +352,6 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
               mma_commit(&a_empty[slot]);
             }
             __syncwarp();
-            if (p.trace && blockIdx.x == 0 && itm < 64 && lane == 0) p.trace[3300 + 3 * itm + 2] = gtimer();
-            ++itm;
             if (++slot == p.ns) { slot = 0; ph ^= 1u; }
             if (info0 >> 31) break;
           }
@@ -395,7 +375,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       const TileCoord tc = tile_coord(p, tile);
       const int b = p.nacc == 2 ? (k & 1) : 0;
       const int use = p.nacc == 2 ? (k >> 1) : k;
-      if (p.dbg & 128) mbar_wait(&acc_full[b], use & 1); else mbar_wait_sleep(&acc_full[b], use & 1);
+      mbar_wait_sleep(&acc_full[b], use & 1);
       tc_fence_after();
       if (p.dbg & 16) {
         tc_fence_before();
