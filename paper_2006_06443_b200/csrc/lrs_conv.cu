@@ -113,6 +113,20 @@ const void* kernel_ptr(KernelId id) {
   return nullptr;
 }
 
+// fused TC kernel instantiation for an exact MMA unit count
+const void* wconv_kernel_ptr(int nu) {
+  switch (nu) {
+    case 1: return reinterpret_cast<const void*>(&lrs_wconv_kernel<1>);
+    case 2: return reinterpret_cast<const void*>(&lrs_wconv_kernel<2>);
+    case 3: return reinterpret_cast<const void*>(&lrs_wconv_kernel<3>);
+    case 4: return reinterpret_cast<const void*>(&lrs_wconv_kernel<4>);
+    case 5: return reinterpret_cast<const void*>(&lrs_wconv_kernel<5>);
+    case 6: return reinterpret_cast<const void*>(&lrs_wconv_kernel<6>);
+    case 7: return reinterpret_cast<const void*>(&lrs_wconv_kernel<7>);
+    default: return reinterpret_cast<const void*>(&lrs_wconv_kernel<8>);
+  }
+}
+
 struct Stage {
   const char* name;
   KernelId kid;
@@ -920,9 +934,8 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     if (e != cudaSuccess)
       return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
-  {
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&lrs_wconv_kernel),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  for (int u = 1; u <= kWMaxUnits; ++u) {
+    cudaError_t e = cudaFuncSetAttribute(wconv_kernel_ptr(u), cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     if (e != cudaSuccess)
       return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
@@ -1005,7 +1018,7 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
       r.used += 2;
       LRS_CUDA(cudaEventRecord(e0, stream));
     }
-    LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_wconv_kernel), dim3(grid), dim3(kWThreads), &w,
+    LRS_CUDA(launch_pdl(wconv_kernel_ptr(w.n_units), dim3(grid), dim3(kWThreads), &w,
                         h->w_smem, stream));
     if (h->timing) LRS_CUDA(cudaEventRecord(e1, stream));
     if (prev != h->device) cudaSetDevice(prev);
