@@ -42,7 +42,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
+    extra = ["-DLRS_WCONV_DEBUG"] if os.environ.get("LRS_WCONV_DEBUG") else []  # tools/wtrace.py experiments
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", tmp, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = r.stdout + r.stderr
     with open(os.path.join(PKG, "build.log"), "w") as f:

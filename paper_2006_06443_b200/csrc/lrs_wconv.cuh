@@ -42,6 +42,17 @@
 #pragma once
 #include "lrs_ptx.cuh"
 
+// Debug experiments (LRS_WCONV_DEBUG builds only): timeline stamps into
+// p.trace and the p.dbg bits that skip parts of the pipeline; compiled out of
+// production builds so the issue loops carry no extra branches.
+#ifdef LRS_WCONV_DEBUG
+#define WDBG(p, bits) ((p).dbg & (bits))
+#define WTRACE(p) ((p).trace != nullptr)
+#else
+#define WDBG(p, bits) 0
+#define WTRACE(p) false
+#endif
+
 namespace lrs {
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -144,7 +155,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const uint32_t slot_info = smem_u32(tmem_slot + 4);  // [kWMaxSlots][kWMaxBpi] u32, written by the producer
 
-  if (p.trace && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
+  if (WTRACE(p) && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
   const int taps = p.kh * p.kw;
   const int nwin = p.n_tk + p.n_ck;
 
@@ -194,7 +205,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         for (int w = 0; w < nwin; ++w, ++wg) {
           if (wg >= p.nwb) mbar_wait(&win_empty[buf], wph ^ 1u);
           uint8_t* wdst = smem + buf * p.win_stride;
-          if (p.dbg & 64) {
+          if (WDBG(p, 64)) {
             mbar_arrive(&win_full[buf]);
           } else if (w < p.n_tk) {
             mbar_arrive_expect_tx(&win_full[buf], p.t_win_bytes);
@@ -208,7 +219,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             ++it;
           } else {
             const int c = w - p.n_tk;
-            if (!(p.dbg & 64)) {
+            if (!(WDBG(p, 64))) {
               mbar_arrive_expect_tx(&win_full[buf], p.x_win_bytes);
               tma_load_4d(wdst, &p.tmX, &win_full[buf], c * 64, tc.n0, tc.wo0 * p.sw - p.pw, tc.ho0 * p.sh - p.ph);
             }
@@ -240,7 +251,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                     st_shared_u32(slot_info + 4u * (kWMaxBpi * slot + q),
                                   pt[q] | (q == 0 ? (static_cast<uint32_t>(np) << 28) | (last ? 0x80000000u : 0u)
                                                   : 0u));
-                if (p.dbg & 2) {
+                if (WDBG(p, 2)) {
                   mbar_arrive(&a_full[slot]);
                 } else {
                   mbar_arrive_expect_tx(&a_full[slot], static_cast<uint32_t>(np) * (kSpBlockBytes + kEBlockBytes));
@@ -301,12 +312,12 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         tc_fence_after();
       }
       const uint32_t acc0 = static_cast<uint32_t>(b) * p.acc_cols;
-      if (p.trace && blockIdx.x == 0 && lane == 0 && k < 16) p.trace[100 + 4 * k] = gtimer();
+      if (WTRACE(p) && blockIdx.x == 0 && lane == 0 && k < 16) p.trace[100 + 4 * k] = gtimer();
       for (int w = 0; w < nwin; ++w) {
-        if (p.trace && blockIdx.x == 0 && lane == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w] = gtimer();
+        if (WTRACE(p) && blockIdx.x == 0 && lane == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w] = gtimer();
         mbar_wait(&win_full[buf], wph);
         tc_fence_after();
-        if (p.trace && blockIdx.x == 0 && lane == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w + 1] = gtimer();
+        if (WTRACE(p) && blockIdx.x == 0 && lane == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w + 1] = gtimer();
         const uint32_t boff = static_cast<uint32_t>(buf) * win16;
         if (w < p.n_tk) {
           mbar_wait(&a_full[slot], ph);
@@ -339,10 +350,10 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                 const uint32_t tap16 =
                     (bi == 0 ? info0 : ld_shared_u32(slot_info + 4u * (kWMaxBpi * slot + bi))) & 0x0FFFFFFFu;
                 const uint32_t ebi = et + 4u * static_cast<uint32_t>(bi);
-                if (!(p.dbg & 5))
+                if (!(WDBG(p, 5)))
                   tmem_cp_128x128b(ebi, ed0 + slot * slot_e16 + static_cast<uint32_t>(bi) * (kEBlockBytes >> 4));
 #pragma unroll
-                for (int s2 = 0; s2 < ((p.dbg & 8) ? 1 : 2) && !(p.dbg & 1); ++s2) {
+                for (int s2 = 0; s2 < (WDBG(p, 8) ? 1 : 2) && !(WDBG(p, 1)); ++s2) {
 #pragma unroll
                   for (int u = 0; u < NU; ++u) {
                       mma_sp_bf16(dcol[u] + acc0, ab + static_cast<uint32_t>(bi) * (kSpBlockBytes >> 4) + 2 * s2,
@@ -364,7 +375,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       }
       if (elect_one()) mma_commit(&acc_full[b]);
       __syncwarp();
-      if (p.trace && blockIdx.x == 0 && lane == 0 && k < 16) p.trace[100 + 4 * k + 1] = gtimer();
+      if (WTRACE(p) && blockIdx.x == 0 && lane == 0 && k < 16) p.trace[100 + 4 * k + 1] = gtimer();
     }
   } else {
     // -------------------------------------------------------------- epilogue
@@ -379,13 +390,13 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       const int use = p.nacc == 2 ? (k >> 1) : k;
       mbar_wait_sleep(&acc_full[b], use & 1);
       tc_fence_after();
-      if (p.dbg & 16) {
+      if (WDBG(p, 16)) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[b]);
         continue;
       }
-      if (p.trace && blockIdx.x == 0 && threadIdx.x == 64 && k < 16) p.trace[100 + 4 * k + 2] = gtimer();
+      if (WTRACE(p) && blockIdx.x == 0 && threadIdx.x == 64 && k < 16) p.trace[100 + 4 * k + 2] = gtimer();
       const uint32_t acc0 = static_cast<uint32_t>(b) * p.acc_cols;
       const int jw = tc.j0 + q4 * 32;  // first channel of this warp
       for (int u = 0; u < p.n_units; ++u) {
@@ -427,13 +438,13 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
-      if (p.trace && blockIdx.x == 0 && threadIdx.x == 64 && k < 16) p.trace[100 + 4 * k + 3] = gtimer();
+      if (WTRACE(p) && blockIdx.x == 0 && threadIdx.x == 64 && k < 16) p.trace[100 + 4 * k + 3] = gtimer();
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (p.trace && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x + 2] = gtimer();
+  if (WTRACE(p) && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x + 2] = gtimer();
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
