@@ -114,17 +114,20 @@ const void* kernel_ptr(KernelId id) {
 }
 
 // fused TC kernel instantiation for an exact MMA unit count
-const void* wconv_kernel_ptr(int nu) {
+const void* wconv_kernel_ptr(int nu, int bpi) {
+#define LRS_WK(U) (bpi == 4 ? reinterpret_cast<const void*>(&lrs_wconv_kernel<U, 4>) \
+                            : reinterpret_cast<const void*>(&lrs_wconv_kernel<U, 2>))
   switch (nu) {
-    case 1: return reinterpret_cast<const void*>(&lrs_wconv_kernel<1>);
-    case 2: return reinterpret_cast<const void*>(&lrs_wconv_kernel<2>);
-    case 3: return reinterpret_cast<const void*>(&lrs_wconv_kernel<3>);
-    case 4: return reinterpret_cast<const void*>(&lrs_wconv_kernel<4>);
-    case 5: return reinterpret_cast<const void*>(&lrs_wconv_kernel<5>);
-    case 6: return reinterpret_cast<const void*>(&lrs_wconv_kernel<6>);
-    case 7: return reinterpret_cast<const void*>(&lrs_wconv_kernel<7>);
-    default: return reinterpret_cast<const void*>(&lrs_wconv_kernel<8>);
+    case 1: return LRS_WK(1);
+    case 2: return LRS_WK(2);
+    case 3: return LRS_WK(3);
+    case 4: return LRS_WK(4);
+    case 5: return LRS_WK(5);
+    case 6: return LRS_WK(6);
+    case 7: return LRS_WK(7);
+    default: return LRS_WK(8);
   }
+#undef LRS_WK
 }
 
 struct Stage {
@@ -934,11 +937,13 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     if (e != cudaSuccess)
       return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
-  for (int u = 1; u <= kWMaxUnits; ++u) {
-    cudaError_t e = cudaFuncSetAttribute(wconv_kernel_ptr(u), cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-    if (e != cudaSuccess)
-      return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
-  }
+  for (int u = 1; u <= kWMaxUnits; ++u)
+    for (int b = 2; b <= 4; b += 2) {
+      cudaError_t e =
+          cudaFuncSetAttribute(wconv_kernel_ptr(u, b), cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+      if (e != cudaSuccess)
+        return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
+    }
   cudaSetDevice(prev);
   *out = h;
   return LRS_OK;
@@ -1018,7 +1023,7 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
       r.used += 2;
       LRS_CUDA(cudaEventRecord(e0, stream));
     }
-    LRS_CUDA(launch_pdl(wconv_kernel_ptr(w.n_units), dim3(grid), dim3(kWThreads), &w,
+    LRS_CUDA(launch_pdl(wconv_kernel_ptr(w.n_units, w.bpi), dim3(grid), dim3(kWThreads), &w,
                         h->w_smem, stream));
     if (h->timing) LRS_CUDA(cudaEventRecord(e1, stream));
     if (prev != h->device) cudaSetDevice(prev);

@@ -241,6 +241,14 @@ __device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t sdesc)
   asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
 
+// smem [2 blocks][128 lanes][16 B] (blocks 2 KB apart) -> TMEM 8 columns x 128 lanes:
+// K-major no-swizzle canonical layout with LBO = 2048 B (next 16-B K chunk = next block)
+// and SBO = 128 B (next 8 lanes)
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc_rows16) {
+  const uint64_t d = (sdesc_rows16 & ~(static_cast<uint64_t>(0x3FFFu) << 16)) | (static_cast<uint64_t>(2048u >> 4) << 16);
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(d) : "memory");
+}
+
 // Instruction descriptor: f32 accumulate, K-major A and B, M = 128.
 // ab_fmt: 1 = bf16 (kind::f16), 2 = tf32 (kind::tf32).
 __host__ __device__ __forceinline__ uint32_t umma_idesc(uint32_t ab_fmt, uint32_t n, uint32_t m) {

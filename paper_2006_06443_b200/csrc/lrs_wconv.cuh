@@ -138,7 +138,7 @@ __device__ __forceinline__ uint4 lds_v4(uint32_t a) {
 // NU = the layer's exact unit count (1..kWMaxUnits): the MMA issue loops are fully
 // unrolled without predicates -- a generic 8-unit loop measured 17-39 % slower
 // (instruction fetch of the issuing warp dominates small MMAs).
-template <int NU>
+template <int NU, int BPI>
 __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_constant__ WconvParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -343,22 +343,31 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             tc_fence_after();
             const uint32_t info0 = ld_shared_u32(slot_info + 4u * kWMaxBpi * slot);
             const int nb = static_cast<int>((info0 >> 28) & 7u);
+            uint32_t tapv[BPI];
+#pragma unroll
+            for (int q = 0; q < BPI; ++q)
+              tapv[q] = (q == 0 ? info0 : ld_shared_u32(slot_info + 4u * (kWMaxBpi * slot + q))) & 0x0FFFFFFFu;
             const uint32_t et = tmem + p.e_col0 + 4u * static_cast<uint32_t>(p.bpi) * slot;
             const uint64_t ab = ad_sp + slot * slot_a16;
             if (elect_one()) {
-              for (int bi = 0; bi < nb; ++bi) {
-                const uint32_t tap16 =
-                    (bi == 0 ? info0 : ld_shared_u32(slot_info + 4u * (kWMaxBpi * slot + bi))) & 0x0FFFFFFFu;
-                const uint32_t ebi = et + 4u * static_cast<uint32_t>(bi);
-                if (!(WDBG(p, 5)))
-                  tmem_cp_128x128b(ebi, ed0 + slot * slot_e16 + static_cast<uint32_t>(bi) * (kEBlockBytes >> 4));
+              // metadata of block pairs in one tcgen05.cp.128x256b (blocks 2 KB apart = LBO)
 #pragma unroll
-                for (int s2 = 0; s2 < (WDBG(p, 8) ? 1 : 2) && !(WDBG(p, 1)); ++s2) {
+              for (int bp = 0; bp < BPI; bp += 2)
+                if (bp < nb && !WDBG(p, 5))
+                  tmem_cp_128x256b(et + 4u * static_cast<uint32_t>(bp),
+                                   ed0 + slot * slot_e16 + static_cast<uint32_t>(bp) * (kEBlockBytes >> 4));
 #pragma unroll
-                  for (int u = 0; u < NU; ++u) {
+              for (int bi = 0; bi < BPI; ++bi) {
+                if (bi < nb) {
+                  const uint32_t ebi = et + 4u * static_cast<uint32_t>(bi);
+#pragma unroll
+                  for (int s2 = 0; s2 < (WDBG(p, 8) ? 1 : 2) && !(WDBG(p, 1)); ++s2) {
+#pragma unroll
+                    for (int u = 0; u < NU; ++u) {
                       mma_sp_bf16(dcol[u] + acc0, ab + static_cast<uint32_t>(bi) * (kSpBlockBytes >> 4) + 2 * s2,
-                                  bxd[u] + boff + tap16 + 4 * s2, idu[u] | (1u << 2) | static_cast<uint32_t>(s2), 1u,
-                                  ebi);
+                                  bxd[u] + boff + tapv[bi] + 4 * s2, idu[u] | (1u << 2) | static_cast<uint32_t>(s2),
+                                  1u, ebi);
+                    }
                   }
                 }
               }
