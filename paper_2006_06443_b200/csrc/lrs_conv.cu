@@ -378,6 +378,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   const int rp = h->r2p;  // K of the dense part: R2, or R of the SVD pair
   const int t_kc = rp < 64 ? rp : 64;
   if (rp % t_kc) return LRS_OK;
+  if (n_ck * kh * kw > 1024) return LRS_OK;  // residual table staged in shared memory
   const int n_tk = rp / t_kc;
   const uint32_t sw_t = static_cast<uint32_t>(t_kc) * 2u;
   const bool s1 = g.sh == 1 && g.sw == 1;
@@ -449,7 +450,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         const long long slack_t = std::max(0LL, last_t + 1 - static_cast<long long>(th) * tbw) * 8 * sw_t;
         const uint32_t stride =
             align1024(static_cast<uint32_t>(std::max<long long>(xw + slack_x, tw + slack_t)));
-        const uint32_t fixed = ns * (a_slot + e_slot) + 8 * kEpiScratch + 1024 + 1024;
+        const uint32_t res_bytes = (static_cast<uint32_t>(n_ck * taps) * 4u + 127u) & ~127u;
+        const uint32_t fixed = ns * (a_slot + e_slot) + 8 * kEpiScratch + res_bytes + 1024 + 1024;
         if (2 * stride + fixed > static_cast<uint32_t>(kMaxSmem)) continue;
         int nwb = 2;
         while (nwb < kWMaxWin && (nwb + 1) * stride + fixed <= static_cast<uint32_t>(kMaxSmem)) ++nwb;
@@ -661,7 +663,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   w.off_a = best_nwb * best_stride;
   w.off_e = w.off_a + best_ns * w.a_slot;
   w.off_epi = w.off_e + best_ns * w.e_slot;
-  w.off_bar = w.off_epi + 8 * kEpiScratch;
+  w.off_res = w.off_epi + 8 * kEpiScratch;  // residual-block table of the tile's M-tile
+  w.off_bar = w.off_res + ((static_cast<uint32_t>(n_ck * taps) * 4u + 127u) & ~127u);
   h->w_smem = best_total;
   h->use_w = true;
   if (getenv("LRS_VERBOSE"))

@@ -108,7 +108,7 @@ struct WconvParams {
   int nacc;             // accumulator buffers in TMEM (1 or 2)
   uint32_t acc_cols;    // TMEM columns of one accumulator buffer
   uint32_t e_col0, tmem_cols;
-  uint32_t off_a, off_e, off_epi, off_bar;
+  uint32_t off_a, off_e, off_epi, off_res, off_bar;
 };
 
 struct TileCoord {
@@ -200,11 +200,22 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       // ------------------------------------------------------------ TMA producer
       int it = 0, wg = 0, buf = 0;
       uint32_t wph = 0;
+      // the tile's residual-block table, staged in shared memory by independent
+      // (pipelined) loads at the tile start: a global load per tap on the issue
+      // path measured ~250 ns each (tools/wtrace.py producer stamps)
+      int* res_s = reinterpret_cast<int*>(smem + p.off_res);
+      const int nres = p.n_ck * taps;
+      int cur_mt = -1;
       for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
         const TileCoord tc = tile_coord(p, tile);
+        if (tc.mt != cur_mt) {
+          for (int i = 0; i < nres; ++i) res_s[i] = __ldg(p.res_block + tc.mt * nres + i);
+          cur_mt = tc.mt;
+        }
         for (int w = 0; w < nwin; ++w, ++wg) {
           if (wg >= p.nwb) mbar_wait(&win_empty[buf], wph ^ 1u);
           uint8_t* wdst = smem + buf * p.win_stride;
+          if (WTRACE(p) && blockIdx.x == 0 && wg < 16) p.trace[3600 + wg] = gtimer();
           if (WDBG(p, 64)) {
             mbar_arrive(&win_full[buf]);
           } else if (w < p.n_tk) {
@@ -231,7 +242,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             uint32_t pt[kWMaxBpi];
             int np = 0;
             for (int t = 0; t < taps; ++t) {
-              const int rblk = __ldg(p.res_block + key0 + t);
+              const int rblk = WDBG(p, 256) ? -1 : res_s[key0 - tc.mt * nres + t];
               const int ty = t / p.kw, tx = t - ty * p.kw;
               const uint32_t tap16 = static_cast<uint32_t>(ty * p.wc + tx) * 64u;  // (pos * 1024) >> 4
               for (int part = 0; part < 2; ++part) {
@@ -244,7 +255,9 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                 const bool last = t == taps - 1 && (part == 1 || rblk < 0);
                 if (np < p.bpi && !last) continue;
                 const int slot = it % p.ns;
+                if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it] = gtimer();
                 if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
+                if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it + 1] = gtimer();
 #pragma unroll
                 for (int q = 0; q < kWMaxBpi; ++q)
                   if (q < np)
@@ -265,6 +278,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                     }
                   }
                 }
+                if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it + 2] = gtimer();
                 ++it;
                 np = 0;
               }
@@ -371,7 +385,8 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                   }
                 }
               }
-              mma_commit(&a_empty[slot]);
+              if (WDBG(p, 512)) mbar_arrive(&a_empty[slot]);
+              else mma_commit(&a_empty[slot]);
             }
             __syncwarp();
             if (++slot == p.ns) { slot = 0; ph ^= 1u; }

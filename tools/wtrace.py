@@ -32,3 +32,7 @@ pi = [(t[3000 + 3 * i] - t0, t[3000 + 3 * i + 1] - t0, t[3000 + 3 * i + 2] - t0)
 mi = [(t[3300 + 3 * i] - t0, t[3300 + 3 * i + 1] - t0, t[3300 + 3 * i + 2] - t0) for i in range(64) if t[3300 + 3 * i]]
 print("producer items (wait a_empty, got, issued):", pi[:14])
 print("mma items (wait a_full, got, committed):", mi[:14])
+wi = [t[3600 + i] - t0 for i in range(16) if t[3600 + i]]
+print("producer window issue times:", wi)
+pi = [(t[3000 + 3 * i] - t0, t[3000 + 3 * i + 1] - t0, t[3000 + 3 * i + 2] - t0) for i in range(64) if t[3000 + 3 * i]]
+print("producer items (start, got slot, issued):", pi[:12])
