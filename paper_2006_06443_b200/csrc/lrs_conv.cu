@@ -181,7 +181,8 @@ struct lrs_conv {
   bool use_w = false;
   WconvParams wp{};
   uint32_t w_smem = 0;
-  void* w_as = nullptr;   // compressed 2:4 blocks of S
+  void* w_as = nullptr;   // compressed 2:4 blocks of S (SW64 shared-memory images)
+  void* w_dense_img = nullptr;  // U_out^T blocks (shared-memory images)
   void* w_e = nullptr;    // their metadata
   int* w_res = nullptr;   // residual block table
   const void* wx_ptr = nullptr;
@@ -559,9 +560,18 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   h->w_res_blocks = nres;
   const int nblk = nblk_main + nres;
   lrs_status st;
+  // shared-memory images of the A operands (swizzle applied here, 1-D bulk copies in the kernel)
+  auto swz_off = [](int r, int byte, int sw) {  // K-major, rows of sw bytes, 8-row atoms
+    return (r / 8) * (8 * sw) + (r % 8) * sw + ((((byte / 16) ^ ((r % 8) / (128 / sw))) % (sw / 16)) * 16) +
+           byte % 16;
+  };
   {
-    std::vector<uint8_t> b(as.size() * 2);
-    memcpy(b.data(), as.data(), b.size());
+    std::vector<uint8_t> b(static_cast<size_t>(nblk) * kSpBlockBytes, 0);
+    for (int blk = 0; blk < nblk; ++blk)
+      for (int m = 0; m < 128; ++m)
+        for (int k = 0; k < 32; ++k)
+          memcpy(&b[static_cast<size_t>(blk) * kSpBlockBytes + swz_off(m, 2 * k, 64)],
+                 &as[(static_cast<size_t>(blk) * 128 + m) * 32 + k], 2);
     if ((st = upload(&h->w_as, b)) != LRS_OK) return st;
     std::vector<uint8_t> e(ee.size() * 4);
     memcpy(e.data(), ee.data(), e.size());
@@ -571,34 +581,28 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     void* rp_ = nullptr;
     if ((st = upload(&rp_, r)) != LRS_OK) return st;
     h->w_res = static_cast<int*>(rp_);
+    // dense A: U_out^T rows (output channels) x R chunks, the layer's bf16 values
+    const int r2 = h->svd ? d->rank_in : d->rank_out;
+    std::vector<uint8_t> dn(static_cast<size_t>(n_mt) * n_tk * 128 * sw_t, 0);
+    for (int mt = 0; mt < n_mt; ++mt)
+      for (int kc = 0; kc < n_tk; ++kc)
+        for (int m = 0; m < 128; ++m) {
+          const int j = mt * 128 + m;
+          if (j >= cout) continue;
+          for (int e2 = 0; e2 < t_kc; ++e2) {
+            const int bb = kc * t_kc + e2;
+            if (bb >= r2) continue;
+            const uint16_t bits = static_cast<const uint16_t*>(d->u_out)[static_cast<size_t>(bb) * cout + j];
+            memcpy(&dn[(static_cast<size_t>(mt) * n_tk + kc) * 128 * sw_t + swz_off(m, 2 * e2, sw_t)], &bits, 2);
+          }
+        }
+    if ((st = upload(&h->w_dense_img, dn)) != LRS_OK) return st;
   }
   WconvParams& w = h->wp;
   memset(&w, 0, sizeof(w));
-  {
-    uint64_t dims[2] = {32, static_cast<uint64_t>(nblk) * 128};
-    uint64_t strides[1] = {64};
-    uint32_t box[2] = {32, 128};
-    uint32_t estr[2] = {1, 1};
-    if ((st = encode_t(&w.tmAs, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, h->w_as, dims, strides, box, estr, 64)) != LRS_OK)
-      return st;
-  }
-  {
-    uint64_t dims[2] = {4, static_cast<uint64_t>(nblk) * 128};
-    uint64_t strides[1] = {16};
-    uint32_t box[2] = {4, 128};
-    uint32_t estr[2] = {1, 1};
-    if ((st = encode_t(&w.tmE, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, h->w_e, dims, strides, box, estr, 0)) != LRS_OK)
-      return st;
-  }
-  {
-    uint64_t dims[2] = {static_cast<uint64_t>(rp), static_cast<uint64_t>(n_mt) * 128};
-    uint64_t strides[1] = {static_cast<uint64_t>(rp) * 2};
-    uint32_t box[2] = {static_cast<uint32_t>(t_kc), 128};
-    uint32_t estr[2] = {1, 1};
-    if ((st = encode_t(&w.tmAd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, h->w_uout, dims, strides, box, estr, sw_t)) !=
-        LRS_OK)
-      return st;
-  }
+  w.img_sp = static_cast<const uint8_t*>(h->w_as);
+  w.img_e = static_cast<const uint8_t*>(h->w_e);
+  w.img_dense = static_cast<const uint8_t*>(h->w_dense_img);
   {
     void* src = h->svd ? h->t1 : h->t2;
     const uint64_t bm = static_cast<uint64_t>(d->batch_max);
@@ -1072,7 +1076,7 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
-                  h->w_as, h->w_e, h->w_res};
+                  h->w_as, h->w_e, h->w_res, h->w_dense_img};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto& r : h->ring)

@@ -73,9 +73,12 @@ constexpr uint32_t kEpiScratch = 2048;   // per epilogue warp: 32 columns x 32 c
 struct WconvParams {
   CUtensorMap tmX;   // X   4-D (C, N, W, H) bf16, box {64, 8, wc, wr}, SW128
   CUtensorMap tmT;   // T   4-D (R, N, Wo, Ho) bf16, box {t_kc, 8, tbox_w, th}, swizzle sw_t
-  CUtensorMap tmAd;  // U_out^T [n_mt*128][R_p] bf16, box {t_kc, 128}, swizzle sw_t
-  CUtensorMap tmAs;  // compressed S blocks [blocks*128][32] bf16, box {32, 128}, SW64
-  CUtensorMap tmE;   // metadata blocks [blocks*128][4] u32, box {4, 128}
+  // A operands as ready-made shared-memory images (host-swizzled), fetched with one
+  // 1-D bulk copy each: a 2-D TMA box of 128 short rows costs 128 TMA requests and
+  // the TMA request rate measured as the producer's bottleneck (tools/wtrace.py)
+  const uint8_t* img_sp;     // compressed 2:4 blocks, SW64 image, 8 KB each
+  const uint8_t* img_e;      // their metadata, [128 lanes][16 B], 2 KB each
+  const uint8_t* img_dense;  // U_out^T (or V^T) blocks [n_mt][n_tk], 128 rows x sw_t B, swizzle sw_t
   const int* res_block;  // [n_mt][n_ck][taps] residual block index or -1
   void* y;
   int n, ho, wo, cout;
@@ -175,9 +178,6 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     fence_mbar_init();
     tma_prefetch_desc(&p.tmX);
     tma_prefetch_desc(&p.tmT);
-    tma_prefetch_desc(&p.tmAd);
-    tma_prefetch_desc(&p.tmAs);
-    tma_prefetch_desc(&p.tmE);
   }
   if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
   tc_fence_before();
@@ -226,7 +226,9 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             const int slot = it % p.ns;
             if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
             mbar_arrive_expect_tx(&a_full[slot], 128u * p.sw_t);
-            tma_load_2d(smem + p.off_a + slot * p.a_slot, &p.tmAd, &a_full[slot], w * p.t_kc, tc.j0);
+            bulk_load(smem + p.off_a + slot * p.a_slot,
+                      p.img_dense + (static_cast<size_t>(tc.mt) * p.n_tk + w) * (128u * p.sw_t), 128u * p.sw_t,
+                      &a_full[slot]);
             ++it;
           } else {
             const int c = w - p.n_tk;
@@ -273,8 +275,10 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
 #pragma unroll
                   for (int q = 0; q < kWMaxBpi; ++q) {
                     if (q < np) {
-                      tma_load_2d(ad + q * kSpBlockBytes, &p.tmAs, &a_full[slot], 0, pb[q] * 128);
-                      tma_load_2d(ed + q * kEBlockBytes, &p.tmE, &a_full[slot], 0, pb[q] * 128);
+                      bulk_load(ad + q * kSpBlockBytes, p.img_sp + static_cast<size_t>(pb[q]) * kSpBlockBytes,
+                                kSpBlockBytes, &a_full[slot]);
+                      bulk_load(ed + q * kEBlockBytes, p.img_e + static_cast<size_t>(pb[q]) * kEBlockBytes,
+                                kEBlockBytes, &a_full[slot]);
                     }
                   }
                 }
