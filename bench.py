@@ -477,15 +477,16 @@ def main():
     dom = max(avg, key=lambda k: avg[k])
     t_dom = avg[dom] / 1e3
     fma_peak = RL.fp32_fma_tflops(peaks["sm_max_mhz"])
-    if dom == "a345_expand_sparse":
+    if dom in ("a345_expand_sparse", "a4_sparse_add"):
         wk = work[dom]
         achieved = wk["flops_sparse"] / t_dom / 1e12
         eng = layer.sparse_engine[0]
         roof = {"bound": "alu", "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s",
                 "frac": achieved / fma_peak, "traffic": None, "kernel": dom,
                 "work": "sparse in-bounds MACs x 2 per launch (the sparse term's algorithmic work)",
-                "engine": ("2:4 sparse tensor cores (tcgen05.mma.sp), fused with the expansion GEMM" if eng == 1
-                           else "SIMT CSR gather fused into the expansion GEMM epilogue"),
+                "engine": {1: "2:4 sparse tensor cores (tcgen05.mma.sp), fused with the expansion GEMM",
+                           2: "SIMT CSR gather over 4-image shared-memory windows, added into Y after a3"}.get(
+                               eng, "SIMT CSR gather fused into the expansion GEMM epilogue"),
                 "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (the sparse term's "
                                "CUDA-core roof, SURVEY §8d three-roof)"}
     else:

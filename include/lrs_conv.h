@@ -151,11 +151,24 @@ lrs_status lrs_conv_debug_buffer(const lrs_conv *h, int32_t which, const void **
  *   1  2:4 sparse tensor cores (tcgen05.mma.sp): every group of 4 consecutive
  *      input channels of a (output channel, tap) is split exactly into a main
  *      2:4 block and, where the group holds 3-4 nonzeros, a residual 2:4 block;
- *      fused with the expansion GEMM (bf16 layers with c_in % 64 == 0).
+ *      fused with the expansion GEMM (bf16 layers with c_in % 64 == 0);
+ *   2  fp32 layers with out_w <= 64: the expansion GEMM stores Y_L, then a
+ *      SIMT CSR gather over shared-memory windows of 4 images adds Y_S into Y
+ *      (one extra read-modify-write of Y; set LRS_F32_FUSED=1 at create to
+ *      select engine 0 instead).
  * For engine 1, *main_blocks / *residual_blocks (may be NULL) receive the
  * number of 128-row compressed blocks of each kind.
  */
 int32_t lrs_conv_sparse_engine(const lrs_conv *h, int32_t *main_blocks, int32_t *residual_blocks);
+
+/*
+ * 1 if the projection a1 and the core convolution a2 of this layer run as one
+ * kernel (bf16 Tucker-2 layers with stride 1 and c_in % 64 == 0: T1 is computed
+ * on each tile's input window and kept in shared memory, never written to HBM;
+ * PAPER.md:162-166), 0 if they run as two kernels with T1 in HBM, -1 for NULL.
+ * With the fused kernel lrs_conv_debug_buffer(h, 0, ...) returns stale data.
+ */
+int32_t lrs_conv_core_fused(const lrs_conv *h);
 
 /*
  * Debug hook: when dev_buf (device, >= 1005 uint64) is non-NULL, CTA 0 of the

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblrs_conv.so")
 SOURCES = [os.path.join(CSRC, "lrs_conv.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("lrs_kernels.cuh", "lrs_ptx.cuh")] + [
+DEPS = SOURCES + sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")) + [
     os.path.join(ROOT, "include", "lrs_conv.h")]
 
 NVCC_FLAGS = [

@@ -16,6 +16,8 @@
 
 #include "../../include/lrs_conv.h"
 #include "lrs_kernels.cuh"
+#include "lrs_core.cuh"
+#include "lrs_spadd.cuh"
 #include "lrs_wconv.cuh"
 
 using namespace lrs;
@@ -176,7 +178,8 @@ struct lrs_conv {
   void* hy = nullptr;
   // timing
   bool timing = false;
-  TimingRing ring[3];
+  int skip = 0;  // timing experiments only (LRS_SKIP at create): 1 a1, 2 a2, 4 a3/fused, 8 a4 split
+  TimingRing ring[4];
   // fused a3+a4+a5 on the tensor cores (lrs_wconv.cuh), bf16 layers
   bool use_w = false;
   WconvParams wp{};
@@ -190,6 +193,18 @@ struct lrs_conv {
   const void* wy_ptr = nullptr;
   int wy_n = -1;
   int w_main_blocks = 0, w_res_blocks = 0;
+  // fp32 layers: a3 GEMM stores Y_L, then the SIMT gather kernel adds Y_S (lrs_spadd.cuh)
+  bool use_spadd = false;
+  SpaddParams spp{};
+  uint32_t sp_smem = 0;
+  int2* sp_ent = nullptr;
+  int* sp_ptr = nullptr;
+  // bf16 Tucker-2 stride-1 layers: a1 + a2 in one kernel (lrs_core.cuh), T1 stays on chip
+  bool use_core = false;
+  CoreParams cp{};
+  uint32_t core_smem = 0;
+  const void* cx_ptr = nullptr;
+  int cx_n = -1;
 };
 
 namespace {
@@ -340,22 +355,28 @@ cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void* param, size_
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-lrs_status launch(lrs_conv* h, int si, Stage& st, dim3 grid, cudaStream_t stream) {
+// event pair around one launch of stage `si` when timing is on
+lrs_status time_begin(lrs_conv* h, int si, cudaStream_t stream, cudaEvent_t* e1) {
+  *e1 = nullptr;
+  if (!h->timing) return LRS_OK;
   TimingRing& r = h->ring[si];
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (h->timing) {
-    if (r.used + 2 > static_cast<int>(r.ev.size())) {
-      const size_t old = r.ev.size();
-      r.ev.resize(old + 512);
-      for (size_t i = old; i < r.ev.size(); ++i) LRS_CUDA(cudaEventCreate(&r.ev[i]));
-    }
-    e0 = r.ev[r.used];
-    e1 = r.ev[r.used + 1];
-    r.used += 2;
-    LRS_CUDA(cudaEventRecord(e0, stream));
+  if (r.used + 2 > static_cast<int>(r.ev.size())) {
+    const size_t old = r.ev.size();
+    r.ev.resize(old + 512);
+    for (size_t i = old; i < r.ev.size(); ++i) LRS_CUDA(cudaEventCreate(&r.ev[i]));
   }
+  *e1 = r.ev[r.used + 1];
+  LRS_CUDA(cudaEventRecord(r.ev[r.used], stream));
+  r.used += 2;
+  return LRS_OK;
+}
+
+lrs_status launch(lrs_conv* h, int si, Stage& st, dim3 grid, cudaStream_t stream) {
+  cudaEvent_t e1 = nullptr;
+  lrs_status s = time_begin(h, si, stream, &e1);
+  if (s != LRS_OK) return s;
   LRS_CUDA(launch_pdl(kernel_ptr(st.kid), grid, dim3(kThreads), &st.p, st.smem, stream));
-  if (h->timing) LRS_CUDA(cudaEventRecord(e1, stream));
+  if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
   return LRS_OK;
 }
 
@@ -365,6 +386,196 @@ inline uint16_t bf16_bits_rne(float f) {
   memcpy(&u, &f, 4);
   u += 0x7FFFu + ((u >> 16) & 1u);
   return static_cast<uint16_t>(u >> 16);
+}
+
+// a1 + a2 fused (lrs_core.cuh): pick the band height th and the images per tile ipt
+// (tile = ipt images x th output rows) minimising waves x bytes a tile moves into
+// shared memory (its X windows + the U_in and G chunks it streams), within TMEM
+// (max(T1, T2) columns <= 512) and shared memory (>= 2 slots + the T1 window).
+lrs_status build_core(lrs_conv* h, const lrs_conv_desc* d) {
+  const int cin = d->c_in, kh = d->kernel_h, kw = d->kernel_w;
+  const int ho = h->ho, wo = h->wo, r1p = h->r1p, r2p = h->r2p;
+  if (h->f32 || h->svd || d->stride_h != 1 || d->stride_w != 1 || cin % 64 != 0 || getenv("LRS_NO_CORE"))
+    return LRS_OK;
+  const int wc = wo + kw - 1;
+  if (wc > 256 || r1p > 256 || r2p > 256) return LRS_OK;
+  const int g_kc = r1p % 64 == 0 ? 64 : (r1p % 32 == 0 ? 32 : 16);
+  const int taps = kh * kw;
+  CoreParams& c = h->cp;
+  memset(&c, 0, sizeof(c));
+  double best = 1e30;
+  int best_th = 0, best_ipt = 0;
+  const int ipt_env = getenv("LRS_CORE_IPT") ? atoi(getenv("LRS_CORE_IPT")) : 0;
+  for (int ipt = 1; ipt <= 8; ++ipt) {
+    if (ipt_env && ipt != ipt_env) continue;
+    for (int th = 1; th <= ho; ++th) {
+      const int wr = th + kh - 1;
+      if (wr > 256) break;
+      const int p1 = wr * wc, nb1 = (ipt * p1 + 127) / 128;
+      const int nb2 = ((ipt - 1) * p1 + (th - 1) * wc + wo + 127) / 128;
+      const uint32_t acc = static_cast<uint32_t>(std::max(nb1 * r1p, nb2 * r2p));
+      if (acc > 512) continue;
+      const uint32_t t1_rows = static_cast<uint32_t>(std::max(nb1 * 128, nb2 * 128 + (kh - 1) * wc + kw - 1));
+      const uint32_t t1_bytes = align1024(t1_rows * static_cast<uint32_t>(r1p) * 2u);
+      const uint32_t x_region = static_cast<uint32_t>(nb1) * 16384u;
+      const uint32_t b_bytes = align1024(std::max<uint32_t>(static_cast<uint32_t>(r1p) * 128u,
+                                                            static_cast<uint32_t>(r2p * g_kc * 2)));
+      const uint32_t slot = x_region + b_bytes;
+      const uint32_t fixed = t1_bytes + 1024u + 1024u;  // barriers + alignment slack
+      if (fixed + 2 * slot > static_cast<uint32_t>(kMaxSmem)) continue;
+      const int bands = (ho + th - 1) / th;
+      const long long tiles = static_cast<long long>((d->batch_max + ipt - 1) / ipt) * bands;
+      const double bytes = static_cast<double>(ipt) * p1 * cin * 2 + static_cast<double>(cin) * r1p * 2 +
+                           static_cast<double>(taps) * r1p * r2p * 2 + 8192.0;
+      const double cost = static_cast<double>((tiles + h->sms - 1) / h->sms) * bytes;
+      if (cost < best * 0.999) {
+        best = cost;
+        best_th = th;
+        best_ipt = ipt;
+      }
+    }
+  }
+  if (!best_th) return LRS_OK;
+  const int th = best_th, ipt = best_ipt, wr = th + kh - 1;
+  const int bands = (ho + th - 1) / th;
+  c.n = d->batch_max; c.ho = ho; c.wo = wo; c.kh = kh; c.kw = kw; c.ph = d->pad_h; c.pw = d->pad_w;
+  c.th = th; c.bands = bands; c.ipt = ipt; c.wr = wr; c.wc = wc; c.p1 = wr * wc;
+  c.nb1 = (ipt * c.p1 + 127) / 128;
+  c.nb2 = ((ipt - 1) * c.p1 + (th - 1) * wc + wo + 127) / 128;
+  c.n_ck = cin / 64;
+  c.r1p = r1p; c.r2p = r2p; c.g_kc = g_kc; c.n_gk = r1p / g_kc; c.sw_g = static_cast<uint32_t>(g_kc * 2);
+  c.x_bytes = static_cast<uint32_t>(ipt * wr * wc) * 128u;
+  c.x_region = static_cast<uint32_t>(c.nb1) * 16384u;
+  c.u_bytes = static_cast<uint32_t>(r1p) * 128u;
+  c.g_bytes = static_cast<uint32_t>(r2p * g_kc * 2);
+  c.slot_bytes = c.x_region + align1024(std::max(c.u_bytes, c.g_bytes));
+  c.t1_rows = static_cast<uint32_t>(std::max(c.nb1 * 128, c.nb2 * 128 + (kh - 1) * wc + kw - 1));
+  const uint32_t t1_bytes = align1024(c.t1_rows * static_cast<uint32_t>(r1p) * 2u);
+  c.ns = std::min<int>(kCMaxSlots, static_cast<int>((kMaxSmem - t1_bytes - 2048u) / c.slot_bytes));
+  c.off_t1 = static_cast<uint32_t>(c.ns) * c.slot_bytes;
+  c.off_bar = c.off_t1 + t1_bytes;
+  c.acc_cols = static_cast<uint32_t>(std::max(c.nb1 * r1p, c.nb2 * r2p));
+  c.nacc = 2 * c.acc_cols <= 512 ? 2 : 1;
+  uint32_t tc = 32;
+  while (tc < c.nacc * c.acc_cols) tc <<= 1;
+  c.tmem_cols = tc;
+  h->core_smem = c.off_bar + 1024u + 1024u;
+  lrs_status st;
+  {
+    uint64_t dims[2] = {static_cast<uint64_t>(cin), static_cast<uint64_t>(r1p)};
+    uint64_t strides[1] = {static_cast<uint64_t>(cin) * 2};
+    uint32_t box[2] = {64, static_cast<uint32_t>(r1p)};
+    uint32_t estr[2] = {1, 1};
+    if ((st = encode_t(&c.tmU, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, h->w_uin, dims, strides, box, estr, 128)) != LRS_OK)
+      return st;
+  }
+  {
+    uint64_t dims[2] = {static_cast<uint64_t>(kh * kw * r1p), static_cast<uint64_t>(r2p)};
+    uint64_t strides[1] = {static_cast<uint64_t>(kh * kw * r1p) * 2};
+    uint32_t box[2] = {static_cast<uint32_t>(g_kc), static_cast<uint32_t>(r2p)};
+    uint32_t estr[2] = {1, 1};
+    if ((st = encode_t(&c.tmG, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, h->w_core, dims, strides, box, estr, c.sw_g)) !=
+        LRS_OK)
+      return st;
+  }
+  h->use_core = true;
+  if (getenv("LRS_VERBOSE"))
+    fprintf(stderr, "[lrs] core: th=%d ipt=%d bands=%d wr=%d wc=%d nb1=%d nb2=%d acc=%u nacc=%d ns=%d t1_rows=%u smem=%u\n",
+            th, ipt, bands, wr, wc, c.nb1, c.nb2, c.acc_cols, c.nacc, c.ns, c.t1_rows, h->core_smem);
+  return LRS_OK;
+}
+
+// fp32 sparse term (lrs_spadd.cuh): tile = 4 images x th output rows x 64 output
+// channels, X window of cc input channels in shared memory; nonzeros regrouped per
+// (64-channel chunk, input-channel chunk, output channel) as (value, window offset).
+// Leaves h->use_spadd false if the layer does not suit the kernel.
+lrs_status build_spadd(lrs_conv* h, const lrs_conv_desc* d) {
+  const int cin = d->c_in, cout = d->c_out, kh = d->kernel_h, kw = d->kernel_w;
+  const int ho = h->ho, wo = h->wo, sh = d->stride_h, sw = d->stride_w;
+  if (cin % 4 != 0 || wo > 32 * kSpKP) return LRS_OK;
+  SpaddParams& q = h->spp;
+  memset(&q, 0, sizeof(q));
+  const int npos_max = 32 * kSpKP;
+  int th = std::max(1, std::min(ho, npos_max / wo));
+  const int bands = (ho + th - 1) / th;
+  th = (ho + bands - 1) / bands;
+  const int wr = (th - 1) * sh + kh, wc = (wo - 1) * sw + kw;
+  // row pitch with sh*pitch == sw*wo (mod 8): lane q then reads vector sw*q (mod 8), so the
+  // 8 lanes of an LDS.128 phase hit distinct banks across row wraps (stride 1)
+  int pitch = wc;
+  if (th > 1)
+    for (int t = wc; t < wc + 8; ++t)
+      if ((sh * t - sw * wo) % 8 == 0) {
+        pitch = t;
+        break;
+      }
+  const int plane = wr * pitch;
+  const int n_nc = (cout + 63) / 64;
+  const int kk = kh * kw;
+  // channel chunk: window + staged nonzeros within ~110 KB so two CTAs share an SM
+  const uint32_t budget = 110 * 1024;
+  int cc = std::min(round_up(cin, 4), static_cast<int>((96 * 1024) / (plane * 16)) / 4 * 4);
+  if (cc < 4) return LRS_OK;
+  std::vector<int> ptr;
+  std::vector<int2> ent;
+  int n_cc = 0, max_ent = 0;
+  for (;;) {
+    n_cc = (cin + cc - 1) / cc;
+    ptr.assign(static_cast<size_t>(n_nc) * n_cc * 64 + 1, 0);
+    ent.clear();
+    max_ent = 0;
+    for (int nc = 0; nc < n_nc; ++nc)
+      for (int c = 0; c < n_cc; ++c) {
+        const size_t first = ent.size();
+        for (int jl = 0; jl < 64; ++jl) {
+          const int j = nc * 64 + jl;
+          ptr[(static_cast<size_t>(nc) * n_cc + c) * 64 + jl] = static_cast<int>(ent.size());
+          if (j >= cout) continue;
+          for (int64_t e = d->row_ptr[j]; e < d->row_ptr[j + 1]; ++e) {
+            const int col = d->col_idx[e];
+            const int ch = col / kk, tap = col % kk;
+            if (ch / cc != c) continue;
+            const int ty = tap / kw, tx = tap % kw;
+            int2 v;
+            const float val = d->values[e];
+            memcpy(&v.x, &val, 4);
+            v.y = (((ch - c * cc) * wr + ty) * pitch + tx) * 16;
+            ent.push_back(v);
+          }
+        }
+        max_ent = std::max(max_ent, static_cast<int>(ent.size() - first));
+      }
+    ptr.back() = static_cast<int>(ent.size());
+    const uint32_t need = static_cast<uint32_t>(cc) * plane * 16 + static_cast<uint32_t>(max_ent) * 8;
+    if (need <= budget) break;
+    if (cc <= 4) return LRS_OK;
+    cc = std::max(4, cc / 2 / 4 * 4);
+  }
+  q.h = d->in_h; q.w = d->in_w; q.cin = cin; q.ho = ho; q.wo = wo; q.cout = cout;
+  q.kh = kh; q.kw = kw; q.sh = sh; q.sw = sw; q.ph = d->pad_h; q.pw = d->pad_w;
+  q.th = th; q.bands = bands; q.n_nc = n_nc; q.cc = cc; q.n_cc = n_cc; q.wr = wr; q.wc = wc;
+  q.pitch = pitch;
+  q.max_ent = max_ent;
+  if (const char* e = getenv("LRS_SPADD_DBG")) q.dbg = atoi(e);
+  q.win_bytes = static_cast<uint32_t>(cc) * plane * 16;
+  h->sp_smem = q.win_bytes + static_cast<uint32_t>(std::max(max_ent, 1)) * 8;
+  std::vector<uint8_t> pe(ptr.size() * 4), ee(std::max<size_t>(ent.size(), 1) * 8, 0);
+  memcpy(pe.data(), ptr.data(), pe.size());
+  if (!ent.empty()) memcpy(ee.data(), ent.data(), ent.size() * 8);
+  lrs_status st;
+  void* pp = nullptr;
+  void* pee = nullptr;
+  if ((st = upload(&pp, pe)) != LRS_OK) return st;
+  h->sp_ptr = static_cast<int*>(pp);
+  if ((st = upload(&pee, ee)) != LRS_OK) return st;
+  h->sp_ent = static_cast<int2*>(pee);
+  q.ent = h->sp_ent;
+  q.ent_ptr = h->sp_ptr;
+  h->use_spadd = true;
+  if (getenv("LRS_VERBOSE"))
+    fprintf(stderr, "[lrs] spadd: th=%d bands=%d wr=%d wc=%d pitch=%d cc=%d n_cc=%d n_nc=%d max_ent=%d smem=%u\n", th, bands,
+            wr, wc, pitch, cc, n_cc, n_nc, max_ent, h->sp_smem);
+  return LRS_OK;
 }
 
 // Fused a3+a4+a5 on the tensor cores (lrs_wconv.cuh): choose the tile geometry,
@@ -710,6 +921,7 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   h->d.values = nullptr;
   h->device = device;
   h->sms = prop.multiProcessorCount;
+  if (const char* e = getenv("LRS_SKIP")) h->skip = atoi(e);
   h->f32 = d->dtype == LRS_DTYPE_F32;
   h->svd = d->core == nullptr;
   h->esz = h->f32 ? 4 : 2;
@@ -795,7 +1007,8 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   if (!h->svd) {
     GemmParams& p = h->a2.p;
     memset(&p, 0, sizeof(p));
-    const uint32_t sw = pick_sw(r1p * esz);
+    // K chunks must not straddle taps: the swizzle width has to divide R1p * esz
+    const uint32_t sw = (r1p * esz) % 128 == 0 ? 128u : ((r1p * esz) % 64 == 0 ? 64u : 32u);
     if (ho * wo <= kTileM) {
       g.th = ho;
       g.nb = kTileM / (ho * wo);
@@ -834,11 +1047,43 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     h->a2.name = "a2_core";
     h->a2.kid = f32 ? K_STORE_F32 : K_STORE_BF16;
   }
+  if ((st = build_core(h, d)) != LRS_OK) return cleanup_fail(st);
   // ---------------------------------------------------------------- a3+a4+a5
   if (bf16_w) {
     if ((st = build_wconv(h, d, g)) != LRS_OK) return cleanup_fail(st);
   }
-  if (!h->use_w) {
+  if (!h->use_w && f32 && !getenv("LRS_F32_FUSED")) {
+    if ((st = build_spadd(h, d)) != LRS_OK) return cleanup_fail(st);
+  }
+  if (h->use_spadd) {
+    // a3 alone: Y = T2 U_out (Y_L); lrs_spadd_kernel then adds Y_S in place
+    GemmParams& p = h->a3.p;
+    memset(&p, 0, sizeof(p));
+    const int kdim = r2p;
+    const uint32_t sw = pick_sw(kdim * esz);
+    h->a3.smem = plan_stage(p, f32, kdim * esz, sw, bn, cout_p, kTileM * sw, 0);
+    if (!h->a3.smem) return cleanup_fail(fail(LRS_ERR_UNSUPPORTED, "a3 does not fit in shared memory"));
+    p.amode = AMODE_2D;
+    p.out_ld = cout;
+    p.out_cols = cout;
+    {
+      void* src = h->svd ? h->t1 : h->t2;
+      uint64_t dims[2] = {static_cast<uint64_t>(kdim), static_cast<uint64_t>(p_max)};
+      uint64_t strides[1] = {static_cast<uint64_t>(kdim) * esz};
+      uint32_t box[2] = {static_cast<uint32_t>(p.kc), static_cast<uint32_t>(kTileM)};
+      uint32_t estr[2] = {1, 1};
+      if ((st = encode(&p.tmA, f32, 2, src, dims, strides, box, estr, sw)) != LRS_OK) return cleanup_fail(st);
+    }
+    {
+      uint64_t dims[2] = {static_cast<uint64_t>(kdim), static_cast<uint64_t>(cout_p) * (f32 ? 2 : 1)};
+      uint64_t strides[1] = {static_cast<uint64_t>(kdim) * esz};
+      uint32_t box[2] = {static_cast<uint32_t>(p.kc), static_cast<uint32_t>(bn)};
+      uint32_t estr[2] = {1, 1};
+      if ((st = encode(&p.tmB, f32, 2, h->w_uout, dims, strides, box, estr, sw)) != LRS_OK) return cleanup_fail(st);
+    }
+    h->a3.name = "a3_expand";
+    h->a3.kid = K_STORE_F32;
+  } else if (!h->use_w) {
     GemmParams& p = h->a3.p;
     memset(&p, 0, sizeof(p));
     const int kdim = r2p;  // K of the expansion (R2, or R for the SVD pair)
@@ -944,6 +1189,15 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     if (e != cudaSuccess)
       return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
+  for (const void* fn : {reinterpret_cast<const void*>(&lrs_core_kernel)}) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+    if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
+  }
+  {
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&lrs_spadd_kernel),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+    if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
+  }
   for (int u = 1; u <= kWMaxUnits; ++u)
     for (int b = 2; b <= 4; b += 2) {
       cudaError_t e =
@@ -984,19 +1238,46 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
   }
   const long long pin = static_cast<long long>(n) * d.in_h * d.in_w;
   const long long P = static_cast<long long>(n) * h->ho * h->wo;
+  if (h->use_core && !(h->skip & 1)) {
+    CoreParams& c = h->cp;
+    if (h->cx_ptr != x || h->cx_n != n) {
+      uint64_t dims[4] = {static_cast<uint64_t>(d.c_in), static_cast<uint64_t>(d.in_w), static_cast<uint64_t>(d.in_h),
+                          static_cast<uint64_t>(n)};
+      uint64_t strides[3] = {static_cast<uint64_t>(d.c_in) * 2, static_cast<uint64_t>(d.in_w) * d.c_in * 2,
+                             static_cast<uint64_t>(d.in_h) * d.in_w * d.c_in * 2};
+      uint32_t box[4] = {64, static_cast<uint32_t>(c.wc), static_cast<uint32_t>(c.wr), static_cast<uint32_t>(c.ipt)};
+      uint32_t estr[4] = {1, 1, 1, 1};
+      if ((st = encode_t(&c.tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box, estr,
+                         128)) != LRS_OK)
+        return st;
+      h->cx_ptr = x;
+      h->cx_n = n;
+    }
+    c.n = n;
+    c.t2 = static_cast<__nv_bfloat16*>(h->t2);
+    c.n_tiles = ((n + c.ipt - 1) / c.ipt) * c.bands;
+    const unsigned grid = static_cast<unsigned>(std::min(c.n_tiles, h->sms));
+    cudaEvent_t e1 = nullptr;
+    if ((st = time_begin(h, 0, stream, &e1)) != LRS_OK) return st;
+    LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_core_kernel), dim3(grid), dim3(kCThreads), &c,
+                        h->core_smem, stream));
+    if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
+  }
   // a1
   h->a1.p.tmA = h->xmap;
   h->a1.p.m_total = static_cast<int>(pin);
   h->a1.p.g.n = n;
-  if ((st = launch(h, 0, h->a1, dim3(static_cast<unsigned>((pin + kTileM - 1) / kTileM)), stream)) != LRS_OK)
+  if (!h->use_core && !(h->skip & 1) &&
+      (st = launch(h, 0, h->a1, dim3(static_cast<unsigned>((pin + kTileM - 1) / kTileM)), stream)) != LRS_OK)
     return st;
   // a2
-  if (!h->svd) {
+  if (!h->svd && !h->use_core && !(h->skip & 2)) {
     h->a2.p.g.n = n;
     const int tiles = ((n + h->a2.p.g.nb - 1) / h->a2.p.g.nb) * h->a2.p.g.tiles_h;
     if ((st = launch(h, 1, h->a2, dim3(tiles), stream)) != LRS_OK) return st;
   }
   // a3 + a4 + a5
+  if (h->use_w && (h->skip & 4)) return LRS_OK;
   if (h->use_w) {
     WconvParams& w = h->wp;
     if (h->wx_ptr != x || h->wx_n != n) {
@@ -1017,22 +1298,11 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
     w.y = y;
     w.n_tiles = ((n + 7) / 8) * w.bands * w.cbands * w.n_mt;
     const unsigned grid = static_cast<unsigned>(std::min(w.n_tiles, h->sms));
-    TimingRing& r = h->ring[2];
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->timing) {
-      if (r.used + 2 > static_cast<int>(r.ev.size())) {
-        const size_t old = r.ev.size();
-        r.ev.resize(old + 512);
-        for (size_t i = old; i < r.ev.size(); ++i) LRS_CUDA(cudaEventCreate(&r.ev[i]));
-      }
-      e0 = r.ev[r.used];
-      e1 = r.ev[r.used + 1];
-      r.used += 2;
-      LRS_CUDA(cudaEventRecord(e0, stream));
-    }
+    cudaEvent_t e1 = nullptr;
+    if ((st = time_begin(h, 2, stream, &e1)) != LRS_OK) return st;
     LRS_CUDA(launch_pdl(wconv_kernel_ptr(w.n_units, w.bpi), dim3(grid), dim3(kWThreads), &w,
                         h->w_smem, stream));
-    if (h->timing) LRS_CUDA(cudaEventRecord(e1, stream));
+    if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
     if (prev != h->device) cudaSetDevice(prev);
     return LRS_OK;
   }
@@ -1040,9 +1310,23 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
   h->a3.p.g.n = n;
   h->a3.p.sp.x = x;
   h->a3.p.sp.y = y;
-  if ((st = launch(h, 2, h->a3,
+  if (h->use_spadd) h->a3.p.out = y;
+  if (!(h->skip & 4) &&
+      (st = launch(h, 2, h->a3,
                    dim3(static_cast<unsigned>((P + kTileM - 1) / kTileM), h->cout_p / h->bn), stream)) != LRS_OK)
     return st;
+  if (h->use_spadd && !(h->skip & 8)) {
+    SpaddParams& q = h->spp;
+    q.x = static_cast<const float*>(x);
+    q.y = static_cast<float*>(y);
+    q.n = n;
+    const unsigned grid = static_cast<unsigned>(((n + 3) / 4) * q.bands * q.n_nc);
+    cudaEvent_t e1 = nullptr;
+    if ((st = time_begin(h, 3, stream, &e1)) != LRS_OK) return st;
+    LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_spadd_kernel), dim3(grid), dim3(kSpThreads), &q,
+                        h->sp_smem, stream));
+    if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
+  }
   if (prev != h->device) cudaSetDevice(prev);
   return LRS_OK;
 }
@@ -1076,7 +1360,7 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
-                  h->w_as, h->w_e, h->w_res, h->w_dense_img};
+                  h->w_as, h->w_e, h->w_res, h->w_dense_img, h->sp_ent, h->sp_ptr};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto& r : h->ring)
@@ -1093,7 +1377,9 @@ lrs_status lrs_conv_output_shape(const lrs_conv* h, int32_t* out_h, int32_t* out
   return LRS_OK;
 }
 
-int32_t lrs_conv_launches_per_forward(const lrs_conv* h) { return h ? (h->svd ? 2 : 3) : 0; }
+int32_t lrs_conv_launches_per_forward(const lrs_conv* h) {
+  return h ? (h->svd ? 2 : 3) + (h->use_spadd ? 1 : 0) - (h->use_core ? 1 : 0) : 0;
+}
 
 lrs_status lrs_conv_set_timing(lrs_conv* h, int32_t enable) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
@@ -1104,7 +1390,7 @@ lrs_status lrs_conv_set_timing(lrs_conv* h, int32_t enable) {
 lrs_status lrs_conv_stage_times(lrs_conv* h, float* ms, int64_t* counts, int32_t max_stages,
                                 int32_t* n_stages, int32_t reset) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
-  for (int s = 0; s < 3; ++s) {
+  for (int s = 0; s < 4; ++s) {
     TimingRing& r = h->ring[s];
     for (int i = 0; i + 1 < r.used; i += 2) {
       LRS_CUDA(cudaEventSynchronize(r.ev[i + 1]));
@@ -1115,8 +1401,8 @@ lrs_status lrs_conv_stage_times(lrs_conv* h, float* ms, int64_t* counts, int32_t
     }
     r.used = 0;
   }
-  if (n_stages) *n_stages = 3;
-  for (int s = 0; s < 3 && s < max_stages; ++s) {
+  if (n_stages) *n_stages = 4;
+  for (int s = 0; s < 4 && s < max_stages; ++s) {
     if (ms) ms[s] = static_cast<float>(h->ring[s].ms);
     if (counts) counts[s] = h->ring[s].count;
   }
@@ -1129,17 +1415,20 @@ lrs_status lrs_conv_stage_times(lrs_conv* h, float* ms, int64_t* counts, int32_t
 }
 
 const char* lrs_conv_stage_name(const lrs_conv* h, int32_t stage) {
-  (void)h;
-  static const char* names[] = {"a1_proj", "a2_core", "a345_expand_sparse"};
-  return (stage >= 0 && stage < 3) ? names[stage] : "";
+  static const char* names[] = {"a1_proj", "a2_core", "a345_expand_sparse", "a4_sparse_add"};
+  if (stage == 0 && h && h->use_core) return "a12_proj_core";
+  if (stage == 2 && h && h->use_spadd) return "a3_expand";
+  return (stage >= 0 && stage < 4) ? names[stage] : "";
 }
 
 int32_t lrs_conv_sparse_engine(const lrs_conv* h, int32_t* main_blocks, int32_t* residual_blocks) {
   if (!h) return -1;
   if (main_blocks) *main_blocks = h->use_w ? h->w_main_blocks : 0;
   if (residual_blocks) *residual_blocks = h->use_w ? h->w_res_blocks : 0;
-  return h->use_w ? 1 : 0;
+  return h->use_w ? 1 : (h->use_spadd ? 2 : 0);
 }
+
+int32_t lrs_conv_core_fused(const lrs_conv* h) { return h ? (h->use_core ? 1 : 0) : -1; }
 
 lrs_status lrs_conv_debug_trace(lrs_conv* h, void* dev_buf) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");

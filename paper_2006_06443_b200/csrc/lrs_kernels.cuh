@@ -71,6 +71,7 @@ struct GemmParams {
   ConvGeom g;
   void* out;              // EPI_STORE destination rows
   int out_ld;             // elements per destination row
+  int out_cols;           // EPI_STORE: valid destination columns (0: all); N chunk c writes columns c*bn..
   uint32_t smem_sparse_off;
   uint32_t smem_bar_off;
   SparseParams sp;
@@ -302,12 +303,18 @@ __global__ void __launch_bounds__(kThreads, 1) lrs_gemm_kernel(const __grid_cons
       } else {
         if (m0 + m < p.m_total) row = m0 + m;
       }
-      T* out = reinterpret_cast<T*>(p.out);
+      T* out = reinterpret_cast<T*>(p.out) + nchunk * p.bn;
       const int nblk = p.bn / 16;
+      const int cols = p.out_cols ? p.out_cols - nchunk * p.bn : p.bn;
       for (int cb = (e >> 2); cb < nblk; cb += 2) {
         float v[16];
         tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + cb * 16, v);
-        if (row >= 0) store16<F32>(out + row * p.out_ld + cb * 16, v);
+        if (row < 0 || cb * 16 >= cols) continue;
+        if (cb * 16 + 16 <= cols) {
+          store16<F32>(out + row * p.out_ld + cb * 16, v);
+        } else {
+          for (int i = 0; cb * 16 + i < cols; ++i) out[row * p.out_ld + cb * 16 + i] = static_cast<T>(v[i]);
+        }
       }
     } else {
       // ------------------------------------------- a4 sparse term + a5 sum and store

@@ -230,6 +230,17 @@ __device__ __forceinline__ uint64_t umma_desc_rows16(uint32_t saddr) {
   d |= 1ull << 46;
   return d;
 }
+// K-major SWIZZLE_NONE operand: core matrices of 8 rows x 16 B (rows 16 B apart);
+// LBO = bytes between core matrices along K, SBO = along M/N.  Any 16-B aligned
+// start address is legal, so a row offset is just an address offset.
+__device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  return d;
+}
 // 2:4 sparse MMA (A sparse along K, compressed in smem; metadata in TMEM at e_tmem).
 // Measured layout (tools/sp_mma_probe3/4, profiles/r01_sp_mma_probe*): logical
 // K step s (32 elements) of row m, group gs = 0..7 of the step -> TMEM column s,

@@ -25,7 +25,7 @@ STATUS_NAMES = {0: "LRS_OK", 1: "LRS_ERR_INVALID_ARGUMENT", 2: "LRS_ERR_UNSUPPOR
 EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
             "lrs_conv_last_error", "lrs_conv_output_shape", "lrs_conv_launches_per_forward",
             "lrs_conv_set_timing", "lrs_conv_stage_times", "lrs_conv_stage_name",
-            "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine")
+            "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine", "lrs_conv_core_fused")
 
 
 class LrsError(RuntimeError):
@@ -81,6 +81,8 @@ def load_library(path: str = LIB_PATH):
     lib.lrs_conv_debug_trace.argtypes = [P, P]
     lib.lrs_conv_sparse_engine.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
     lib.lrs_conv_sparse_engine.restype = ctypes.c_int32
+    lib.lrs_conv_core_fused.argtypes = [P]
+    lib.lrs_conv_core_fused.restype = ctypes.c_int32
     for name in ("lrs_conv_debug_trace", "lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
                  "lrs_conv_output_shape", "lrs_conv_set_timing", "lrs_conv_stage_times",
                  "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine"):
@@ -190,6 +192,11 @@ class LrsConv:
         m, r = ctypes.c_int32(), ctypes.c_int32()
         e = load_library().lrs_conv_sparse_engine(self.handle, ctypes.byref(m), ctypes.byref(r))
         return int(e), int(m.value), int(r.value)
+
+    @property
+    def core_fused(self) -> bool:
+        """True if a1 + a2 run as one kernel with T1 kept on chip (include/lrs_conv.h)."""
+        return load_library().lrs_conv_core_fused(self.handle) == 1
 
     def forward_into(self, x, y, stream=None) -> None:
         torch = self.torch

@@ -75,7 +75,15 @@ def layer_work(cfg, n: int, col_idx: np.ndarray) -> Dict[str, Dict[str, float]]:
             "flops_tc": 2.0 * p * r2 * cfg.c_out, "flops_sparse": 2.0 * macs_s, "sparse_macs": macs_s},
     }
     st["a345_expand_sparse"]["flops"] = st["a345_expand_sparse"]["flops_tc"] + st["a345_expand_sparse"]["flops_sparse"]
+    # fp32 split engine: a3 GEMM stores Y_L, a4 gathers X and adds Y_S into Y (read + write)
+    st["a3_expand"] = {"bytes": (t2_b if not cfg.svd else t1_b) + y_b + r2 * cfg.c_out * esz,
+                       "flops": 2.0 * p * r2 * cfg.c_out}
+    st["a4_sparse_add"] = {"bytes": x_b + 2 * y_b + nnz * 8 + (cfg.c_out + 1) * 4,
+                           "flops": 2.0 * macs_s, "flops_sparse": 2.0 * macs_s, "sparse_macs": macs_s}
     if not cfg.svd:
+        # a1 + a2 fused (T1 stays on chip): X in, T2 out, U_in and G read once
+        st["a12_proj_core"] = {"bytes": x_b + t2_b + cfg.c_in * r1 * esz + r1 * r2 * cfg.k * cfg.k * esz,
+                               "flops": 2.0 * p_in * cfg.c_in * r1 + 2.0 * p * r1 * r2 * cfg.k * cfg.k}
         st["a2_core"] = {"bytes": t1_b + t2_b + r1 * r2 * cfg.k * cfg.k * esz,
                          "flops": 2.0 * p * r1 * r2 * cfg.k * cfg.k}
     layer_bytes = x_b + y_b + esz * (cfg.c_in * r1 + (0 if cfg.svd else r1 * r2 * cfg.k ** 2) + r2 * cfg.c_out) \

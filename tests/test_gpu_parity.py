@@ -77,6 +77,8 @@ GEOMS = [  # (n, h, w, cin, cout, k, s, p, r1, r2, density, dtype, svd)
     (5, 6, 6, 64, 64, 1, 1, 0, 32, 32, 0.02, "bf16", True),      # SVD, tiles spanning images
     (2, 12, 12, 16, 16, 5, 1, 2, 16, 16, 0.05, "bf16", False),   # 5x5
     (300, 7, 7, 16, 16, 3, 1, 1, 16, 16, 0.05, "bf16", False),   # many images per tile
+    (2, 14, 14, 64, 64, 3, 2, 1, 48, 32, 0.03, "bf16", False),   # stride 2 (two kernels), R1 = 48: K chunks per tap
+    (2, 10, 10, 16, 32, 3, 1, 1, 40, 24, 0.03, "f32", False),    # fp32, R1 = 40 -> 48 (192 B per tap)
 ]
 
 

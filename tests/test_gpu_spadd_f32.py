@@ -1,0 +1,117 @@
+"""GPU parity of the fp32 sparse engine (lrs_spadd.cuh): a3 stores Y_L = T2 U_out,
+then a SIMT CSR gather over 4-image shared-memory windows adds the sparse term
+(eq. for the sparse convolution; a5 sum as a read-modify-write).
+Compared with the fp64 oracle at the fp32 tolerance of the BASELINE.json north
+star (relL2 <= 1e-5, max-abs <= 1e-4).  Each geometry pins one mechanism of the
+tiling: ragged image groups (n % 4), Cout not a multiple of 64 or of 8, stride 2,
+5x5 taps, input-channel chunking (n_cc > 1), wide rows (two positions per lane),
+and the fall-back to the fused epilogue engine (Wo > 64).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from oracle import lrs_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def run(inp, env=None):
+    from paper_2006_06443_b200 import LrsConv
+    old = {k: os.environ.get(k) for k in (env or {})}
+    os.environ.update(env or {})
+    try:
+        layer = LrsConv.from_inputs(inp)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    y = layer(torch.from_numpy(inp.x).float().cuda())
+    torch.cuda.synchronize()
+    return layer, y.cpu().numpy().astype(np.float64)
+
+
+def oracle(inp):
+    c = inp.cfg
+    return O.forward_factored(inp.x.astype(np.float64), inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx,
+                              inp.values, c.stride, c.pad)
+
+
+def check(y, ref):
+    err = np.linalg.norm(y - ref) / np.linalg.norm(ref)
+    mx = np.abs(y - ref).max()
+    assert err <= 1e-5 and mx <= 1e-4, (err, mx)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2_f32"])
+def test_fp32_configs_use_the_simt_engine(name):
+    inp = workloads.generate(workloads.CONFIGS[name], batch=1)
+    layer, _ = run(inp)
+    assert layer.sparse_engine[0] == 2
+    assert layer.launches_per_forward == 4
+
+
+GEOMS = [  # (n, h, w, cin, cout, k, s, p, r1, r2, density, svd, engine)
+    (6, 14, 14, 64, 200, 3, 1, 1, 16, 32, 0.03, False, 2),    # 6 images: one full + one half group; Cout 200
+    (5, 9, 9, 32, 68, 3, 1, 1, 16, 16, 0.05, False, 2),       # Cout 68: partial 8-channel warp
+    (3, 28, 28, 32, 64, 3, 2, 1, 8, 8, 0.04, False, 2),       # stride 2
+    (4, 12, 12, 16, 48, 5, 1, 2, 16, 16, 0.05, False, 2),     # 5x5 taps
+    (2, 30, 30, 256, 64, 3, 1, 1, 16, 16, 0.02, False, 2),    # wide plane: input-channel chunks (n_cc > 1)
+    (3, 40, 40, 16, 32, 3, 1, 1, 16, 16, 0.05, False, 2),     # Wo = 40: second position per lane
+    (2, 64, 64, 8, 16, 3, 1, 1, 8, 8, 0.05, False, 2),        # Wo = 64: the widest the engine takes
+    (7, 10, 10, 64, 128, 1, 1, 0, 32, 32, 0.03, True, 2),     # SVD pair (1x1)
+    (3, 8, 8, 32, 32, 3, 1, 0, 16, 16, 0.40, False, 2),       # dense-ish S, pad 0
+    (2, 70, 70, 8, 16, 3, 1, 1, 8, 8, 0.05, False, 0),        # Wo = 70 > 64: fused epilogue engine
+]
+
+
+@pytest.mark.parametrize("geom", GEOMS)
+def test_fp32_geometries_vs_oracle(geom):
+    n, h, w, cin, cout, k, s, p, r1, r2, dens, svd, eng = geom
+    cfg = workloads.LayerConfig("t", n, h, w, cin, cout, k, s, p, r1, r1 if svd else r2, dens, "f32", svd, seed=13)
+    inp = workloads.generate(cfg)
+    layer, y = run(inp)
+    assert layer.sparse_engine[0] == eng
+    check(y, oracle(inp))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2_f32"])
+def test_fused_and_split_engines_agree_with_oracle(name):
+    """LRS_F32_FUSED selects the fused SIMT epilogue (engine 0) instead; both
+    must meet the fp32 bar on the same inputs."""
+    inp = workloads.generate(workloads.CONFIGS[name], batch=5 if name == "c2_f32" else 1)
+    ref = oracle(inp)
+    la, ya = run(inp)
+    lb, yb = run(inp, {"LRS_F32_FUSED": "1"})
+    assert la.sparse_engine[0] == 2 and lb.sparse_engine[0] == 0
+    check(ya, ref)
+    check(yb, ref)
+
+
+def test_sparse_only_is_exact_sum_order_independent_for_one_entry_per_row():
+    """U_out = 0 and one nonzero per output channel: each output is a single
+    product v * x (exactly rounded once), so the engine must be bitwise."""
+    n, h, w, cin, cout, k = 5, 11, 11, 16, 24, 3
+    rng = np.random.default_rng(9)
+    x = np.maximum(rng.standard_normal((n, h, w, cin)), 0).astype(np.float32)
+    cols = rng.integers(0, cin * k * k, cout).astype(np.int32)
+    vals = rng.standard_normal(cout).astype(np.float32)
+    rp = np.arange(cout + 1, dtype=np.int64)
+    cfg = workloads.LayerConfig("t", n, h, w, cin, cout, k, 1, 1, 8, 8, 0.0, "f32")
+    inp = workloads.LayerInputs(cfg, x, np.ones((cin, 8), np.float32), np.ones((8, 8, k, k), np.float32),
+                                np.zeros((8, cout), np.float32), rp, cols, vals)
+    layer, y = run(inp)
+    assert layer.sparse_engine[0] == 2
+    xp = np.zeros((n, h + 2, w + 2, cin), np.float32)
+    xp[:, 1:-1, 1:-1] = x
+    ref = np.zeros((n, h, w, cout), np.float32)
+    for j in range(cout):
+        c, t = divmod(int(cols[j]), k * k)
+        ty, tx = divmod(t, k)
+        ref[..., j] = vals[j] * xp[:, ty:ty + h, tx:tx + w, c]
+    assert np.array_equal(y.astype(np.float32), ref)
