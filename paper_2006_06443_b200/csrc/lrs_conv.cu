@@ -350,7 +350,8 @@ cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void* param, size_
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool no_pdl = getenv("LRS_NO_PDL") != nullptr;  // timing experiments
+  cfg.numAttrs = no_pdl ? 0 : 1;
   void* args[] = {param};
   return cudaLaunchKernelExC(&cfg, fn, args);
 }

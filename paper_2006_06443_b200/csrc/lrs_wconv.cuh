@@ -55,11 +55,6 @@
 
 namespace lrs {
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 constexpr int kWThreads = 320;  // warps 0 producer, 1 MMA, 2..9 epilogue (2 per TMEM lane quarter)
 constexpr int kWMaxSlots = 6;
