@@ -38,6 +38,10 @@ CONFIG_TEXT = {
     "c2_bf16": "C2: ResNet-50 layer3 3x3 conv 256->256 @14x14, batch 64, Tucker-2 (64,64), S 2%, bf16",
     "c3": "C3: ResNet-50 layer4 3x3 conv 512->512 @7x7, batch 256, Tucker-2 (128,128), S 5%, bf16",
     "c4": "C4: ResNet-50 1x1 expansion 256->1024 @14x14, batch 128, SVD rank 64, S 1%, bf16",
+    "c1_cp": "C1 shape with the paper's CP form of L (SURVEY 8f f1): 3x3 conv 64->64 @56x56, batch 1, "
+             "CP rank 16 (1x1, 3x1 + 1x3 depthwise, 1x1), S 1%, fp32",
+    "c2_cp": "C2 shape with the paper's CP form of L (SURVEY 8f f1): 3x3 conv 256->256 @14x14, batch 64, "
+             "CP rank 64 (1x1, 3x1 + 1x3 depthwise, 1x1), S 2%, bf16",
     "c5": "C5: full ResNet-50 forward, global batch 256 (224x224x3 N(0,1) images), random-init weights, "
           "16 3x3 convs -> Tucker-2 (Cin/4, Cout/4) + 2% S via the C-ABI, other layers dense cuDNN, bf16",
 }
@@ -49,7 +53,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c2_bf16", choices=sorted(workloads.CONFIGS) + ["c5"])
+    ap.add_argument("--config", default="c2_bf16", choices=sorted(workloads.CONFIGS) + sorted(workloads.CP_CONFIGS) + ["c5"])
     ap.add_argument("--impl", default="lrs", choices=["lrs", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -79,8 +83,11 @@ def oracle_rate(cfg, inp, seconds: float, sample_images: int):
     x = inp.x[:sample_images].astype(np.float64)
     calls, t0 = 0, time.perf_counter()
     while True:
-        O.forward_factored(x, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx, inp.values,
-                           cfg.stride, cfg.pad)
+        if isinstance(inp, workloads.CpInputs):
+            O.forward_cp(x, inp.a, inp.b, inp.c, inp.d, inp.row_ptr, inp.col_idx, inp.values, cfg.stride, cfg.pad)
+        else:
+            O.forward_factored(x, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx, inp.values,
+                               cfg.stride, cfg.pad)
         calls += 1
         el = time.perf_counter() - t0
         if el >= seconds and calls >= 2:
@@ -143,13 +150,17 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     sample = max(1, min(cfg.batch, 8))
-    inp = workloads.generate(cfg, batch=sample)
+    is_cp = args.config in workloads.CP_CONFIGS
+    inp = (workloads.generate_cp if is_cp else workloads.generate)(cfg, batch=sample)
     from oracle import lrs_oracle as O
     x = inp.x.astype(np.float64)
 
     def step():
-        O.forward_factored(x, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx, inp.values,
-                           cfg.stride, cfg.pad)
+        if is_cp:
+            O.forward_cp(x, inp.a, inp.b, inp.c, inp.d, inp.row_ptr, inp.col_idx, inp.values, cfg.stride, cfg.pad)
+        else:
+            O.forward_factored(x, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx, inp.values,
+                               cfg.stride, cfg.pad)
     for _ in range(args.warmup):
         step()
     t0 = time.perf_counter()
@@ -164,7 +175,7 @@ def run_reference(args, cfg):
             "config": {"workload": CONFIG_TEXT[args.config], "images_per_step": sample},
             "cpu_baseline": {"value": value, "unit": "images/s", "cores": cpu_threads(), "kind": "oracle",
                              "sample": f"{sample} images of {args.config} per step (fp64 numpy oracle, "
-                                       "forward_factored)"},
+                                       f"{'forward_cp' if is_cp else 'forward_factored'})"},
             "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -282,12 +293,13 @@ def main_c5(args):
     torch.cuda.synchronize(dev)
     peaks = RL.measured_peaks()
     fma = RL.fp32_fma_tflops(peaks["sm_max_mhz"])
-    tot = {"a1_proj": 0.0, "a2_core": 0.0, "a345_expand_sparse": 0.0}
+    tot = {}
     sparse_flops = 0.0
     for idx, c in comp.items():
         st = c.layer.stage_times(reset=True)
         for k, v in st.items():
-            tot[k] += v[0] / max(v[1], 1)
+            if v[1]:
+                tot[k] = tot.get(k, 0.0) + v[0] / v[1]
         sparse_flops += RL.layer_work(c.cfg, per, workloads.generate_weights(c.cfg).col_idx)["layer"]["flops_sparse"]
         c.layer.set_timing(False)
     t_a345 = tot["a345_expand_sparse"] / 1e3
@@ -341,7 +353,8 @@ def main():
         else:
             main_c5(args)
         return
-    cfg = workloads.CONFIGS[args.config]
+    is_cp = args.config in workloads.CP_CONFIGS
+    cfg = workloads.CP_CONFIGS[args.config] if is_cp else workloads.CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
         return
@@ -356,11 +369,16 @@ def main():
     from paper_2006_06443_b200 import roofline as RL
 
     # ---- inputs: same weights everywhere, rank-specific images (weak scaling)
-    inp = workloads.generate(cfg)
+    gen = workloads.generate_cp if is_cp else workloads.generate
+    inp = gen(cfg)
     if rank > 0:
-        inp.x = workloads.generate(cfg, seed=1000 + rank).x
+        inp.x = gen(cfg, seed=1000 + rank).x
     n = cfg.batch
-    layer = LrsConv.from_inputs(inp, batch_max=n, device=local)
+    if is_cp:
+        layer = LrsConv.from_cp(n, cfg.in_h, cfg.in_w, cfg.k, cfg.stride, cfg.pad, cfg.dtype, inp.a, inp.b, inp.c,
+                                inp.d, inp.row_ptr, inp.col_idx, inp.values, device=local)
+    else:
+        layer = LrsConv.from_inputs(inp, batch_max=n, device=local)
     tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
     esz = 2 if cfg.dtype == "bf16" else 4
     x_bytes = n * cfg.in_h * cfg.in_w * cfg.c_in * esz
@@ -471,7 +489,7 @@ def main():
 
     # ---- roofline of the dominant kernel + layer roofs
     peaks = RL.measured_peaks()
-    work = RL.layer_work(cfg, n, inp.col_idx)
+    work = RL.layer_work(cfg, n, inp.col_idx, cp=is_cp)
     roofs = RL.layer_roofs(work, peaks, cfg.dtype)
     avg = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in stages.items()}
     dom = max(avg, key=lambda k: avg[k])

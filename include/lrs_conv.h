@@ -8,6 +8,9 @@
  *   L  Tucker-2 chain  T1 = X U_in          (1x1 projection,   PAPER.md:162)
  *                      T2 = conv(T1, G)     (k x k core,       PAPER.md:165-166, :409)
  *                      Y_L = T2 U_out       (1x1 expansion,    PAPER.md:168)
+ *      or the paper's CP chain (core_kind = LRS_CORE_CP):
+ *                      T1 = X A, T2 = depthwise k x 1 (B) then 1 x k (C) over
+ *                      the R rank channels, Y_L = T2 D^T
  *      or, for a 1x1 layer, an SVD pair  Y_L = (X U) V          (core == NULL)
  *   S  direct sparse convolution, CSR by output channel        PAPER.md:171-191 §3.4
  *   Y  = Y_L + Y_S, written to device memory once.
@@ -47,6 +50,14 @@ typedef enum {
   LRS_DTYPE_BF16 = 1  /* X, Y, factors bf16; fp32 accumulation everywhere          */
 } lrs_dtype;
 
+typedef enum {
+  LRS_CORE_TUCKER2 = 0, /* core = dense G [rank_in][rank_out][kernel_h][kernel_w]        */
+  LRS_CORE_CP = 1       /* core = B [kernel_h][R] then C [kernel_w][R], R = rank_in = rank_out:
+                           L[c,j,y,x] = sum_r u_in[c,r] B[y,r] C[x,r] u_out[r,j]
+                           (A = u_in, D^T = u_out); stages 2-3 run as the
+                           paper's two depthwise convolutions         */
+} lrs_core_kind;
+
 typedef struct lrs_conv lrs_conv; /* opaque; immutable after create */
 
 typedef struct lrs_conv_desc {
@@ -66,6 +77,8 @@ typedef struct lrs_conv_desc {
   const int32_t *col_idx;         /* host [nnz]; < c_in*kernel_h*kernel_w            */
   const float *values;            /* host [nnz]; fp32; bf16 layers round them to bf16 (RNE)
                                      at create (reading #12)               */
+  lrs_core_kind core_kind;        /* LRS_CORE_TUCKER2 (0, the zero-initialised default)
+                                     or LRS_CORE_CP; ignored when core == NULL        */
 } lrs_conv_desc;
 
 /*
@@ -160,6 +173,23 @@ lrs_status lrs_conv_debug_buffer(const lrs_conv *h, int32_t which, const void **
  * number of 128-row compressed blocks of each kind.
  */
 int32_t lrs_conv_sparse_engine(const lrs_conv *h, int32_t *main_blocks, int32_t *residual_blocks);
+
+/*
+ * The paper's sparse storage (§3.4) -> the CSR this
+ * ABI takes.  Per input channel i (a "slice"), entries slice_ptr[i] .. slice_ptr[i+1]-1
+ * of packed[] / values[] (host arrays) hold one nonzero each:
+ *   packed = j * (kernel_h * kernel_w) + ky * kernel_w + kx    (output channel j, tap ky, kx)
+ * as uint16 (packed_bytes = 2; requires c_out * kernel_h * kernel_w <= 65536, the
+ * paper's "one int16 number") or uint32 (packed_bytes = 4).  Slices may hold any
+ * number of entries in any order.  Writes row_ptr [c_out + 1], and col_idx / values_out
+ * [slice_ptr[c_in]] sorted by (row, col) with col = (i * kernel_h + ky) * kernel_w + kx.
+ * Host-only (no device needed).  INVALID_ARGUMENT: bad extents, packed_bytes not 2/4,
+ * slice_ptr not starting at 0 / not monotone, an index decoding to j >= c_out, a
+ * duplicate (j, col), or uint16 packing where c_out * taps > 65536.
+ */
+lrs_status lrs_sparse_from_slices(int32_t c_in, int32_t c_out, int32_t kernel_h, int32_t kernel_w,
+                                  const int64_t *slice_ptr, const void *packed, int32_t packed_bytes,
+                                  const float *values, int64_t *row_ptr, int32_t *col_idx, float *values_out);
 
 /*
  * 1 if the projection a1 and the core convolution a2 of this layer run as one

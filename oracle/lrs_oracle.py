@@ -27,7 +27,7 @@ import numpy as np
 __all__ = [
     "out_size", "conv_direct", "reconstruct_tucker2", "reconstruct_cp",
     "densify_sparse", "forward_dense", "conv_1x1", "sparse_conv_scatter",
-    "forward_factored", "cp_conv", "brute_force_conv", "param_counts", "cp_param_count",
+    "forward_factored", "cp_conv", "forward_cp", "brute_force_conv", "param_counts", "cp_param_count",
     "pack_sparse_slices", "unpack_sparse_slices", "sparse_mac_count",
 ]
 
@@ -213,6 +213,24 @@ def cp_conv(x, a, b, c, d, pad: Optional[int] = None) -> np.ndarray:
     for t in range(kk):
         yc += ypad[:, :, t:t + yc.shape[2]] * c[t]
     return yc @ d.T
+
+
+def forward_cp(x, a, b, c, d, row_ptr, col_idx, values, stride: int = 1, pad: int = 0) -> np.ndarray:
+    """A layer whose L is in the paper's CP form plus the sparse
+    term: Y = conv(X, L) + conv(X, S).  At stride 1 with centred
+    padding L runs as the paper's four stages (cp_conv); the
+    paper has no strided form (reading #4), so other strides/paddings evaluate
+    conv(X, L) on the reconstructed kernel (reconstruct_cp + conv_direct) --
+    the plain definition the four stages equal.  The sparse term is
+    sparse_conv_scatter (PAPER.md:189)."""
+    x = np.asarray(x, np.float64)
+    k = np.asarray(b).shape[0]
+    if stride == 1 and pad == k // 2:
+        y_l = cp_conv(x, a, b, c, d, pad)
+    else:
+        y_l = conv_direct(x, reconstruct_cp(a, b, c, d), stride, pad)
+    d = np.asarray(d)
+    return y_l + sparse_conv_scatter(x, d.shape[0], k, row_ptr, col_idx, values, stride, pad)
 
 
 def brute_force_conv(x, w, stride=1, pad=0) -> np.ndarray:

@@ -17,6 +17,7 @@
 #include "../../include/lrs_conv.h"
 #include "lrs_kernels.cuh"
 #include "lrs_core.cuh"
+#include "lrs_cpdw.cuh"
 #include "lrs_spadd.cuh"
 #include "lrs_wconv.cuh"
 
@@ -199,6 +200,11 @@ struct lrs_conv {
   uint32_t sp_smem = 0;
   int2* sp_ent = nullptr;
   int* sp_ptr = nullptr;
+  // CP core (the paper's form): stages 2-3 as two depthwise convs
+  bool cp_core = false;
+  float* w_cpb = nullptr;  // [kh][R1p] vertical taps
+  float* w_cpc = nullptr;  // [kw][R1p] horizontal taps
+  CpDwParams cpp{};
   // bf16 Tucker-2 stride-1 layers: a1 + a2 in one kernel (lrs_core.cuh), T1 stays on chip
   bool use_core = false;
   CoreParams cp{};
@@ -223,6 +229,10 @@ lrs_status validate(const lrs_conv_desc* d) {
   if (d->in_h + 2 * d->pad_h < d->kernel_h || d->in_w + 2 * d->pad_w < d->kernel_w || ho < 1 || wo < 1)
     return fail(LRS_ERR_INVALID_ARGUMENT, "output extent < 1");
   if (!d->u_in || !d->u_out) return fail(LRS_ERR_INVALID_ARGUMENT, "u_in / u_out is NULL");
+  if (d->core_kind != LRS_CORE_TUCKER2 && d->core_kind != LRS_CORE_CP)
+    return fail(LRS_ERR_INVALID_ARGUMENT, "unknown core_kind %d", (int)d->core_kind);
+  if (d->core_kind == LRS_CORE_CP && (!d->core || d->rank_in != d->rank_out))
+    return fail(LRS_ERR_INVALID_ARGUMENT, "a CP core needs core != NULL and rank_in == rank_out");
   if (!d->core) {
     if (d->kernel_h != 1 || d->kernel_w != 1 || d->stride_h != 1 || d->stride_w != 1 ||
         d->pad_h != 0 || d->pad_w != 0)
@@ -396,7 +406,7 @@ inline uint16_t bf16_bits_rne(float f) {
 lrs_status build_core(lrs_conv* h, const lrs_conv_desc* d) {
   const int cin = d->c_in, kh = d->kernel_h, kw = d->kernel_w;
   const int ho = h->ho, wo = h->wo, r1p = h->r1p, r2p = h->r2p;
-  if (h->f32 || h->svd || d->stride_h != 1 || d->stride_w != 1 || cin % 64 != 0 || getenv("LRS_NO_CORE"))
+  if (h->f32 || h->svd || h->cp_core || d->stride_h != 1 || d->stride_w != 1 || cin % 64 != 0 || getenv("LRS_NO_CORE"))
     return LRS_OK;
   const int wc = wo + kw - 1;
   if (wc > 256 || r1p > 256 || r2p > 256) return LRS_OK;
@@ -925,6 +935,7 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   if (const char* e = getenv("LRS_SKIP")) h->skip = atoi(e);
   h->f32 = d->dtype == LRS_DTYPE_F32;
   h->svd = d->core == nullptr;
+  h->cp_core = d->core_kind == LRS_CORE_CP;
   h->esz = h->f32 ? 4 : 2;
   const bool f32 = h->f32;
   const int esz = h->esz;
@@ -940,6 +951,7 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   const bool bf16_w = !f32 && cin % 64 == 0;
   h->r1p = (bf16_w && h->svd) ? t_round(r1) : round_up(r1, 16);
   h->r2p = h->svd ? h->r1p : (bf16_w ? t_round(r2) : round_up(r2, 16));
+  if (h->cp_core) h->r1p = h->r2p = std::max(h->r1p, h->r2p);  // T1 and T2 share one row pitch
   h->bn = cout <= 64 ? 64 : 128;
   h->cout_p = bf16_w ? round_up(cout, 128) : round_up(cout, h->bn);
   const int r1p = h->r1p, r2p = h->r2p, bn = h->bn, cout_p = h->cout_p;
@@ -959,7 +971,24 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
       for (int a = 0; a < r1; ++a) m[static_cast<size_t>(a) * cin + c] = host_val(d->u_in, (size_t)c * r1 + a, f32);
     if ((st = upload(&h->w_uin, pack_matrix(m, r1p, cin, f32))) != LRS_OK) return cleanup_fail(st);
   }
-  if (!h->svd) {
+  if (h->cp_core) {
+    // CP factors: core = B [kernel_h][R] followed by C [kernel_w][R] (dtype), kept fp32 [k][R1p]
+    std::vector<float> b(static_cast<size_t>(kh) * r1p, 0.f), c(static_cast<size_t>(kw) * r1p, 0.f);
+    for (int y = 0; y < kh; ++y)
+      for (int a = 0; a < r1; ++a) b[static_cast<size_t>(y) * r1p + a] = host_val(d->core, (size_t)y * r1 + a, f32);
+    for (int x = 0; x < kw; ++x)
+      for (int a = 0; a < r1; ++a)
+        c[static_cast<size_t>(x) * r1p + a] = host_val(d->core, (size_t)(kh + x) * r1 + a, f32);
+    std::vector<uint8_t> bb(b.size() * 4), cb(c.size() * 4);
+    memcpy(bb.data(), b.data(), bb.size());
+    memcpy(cb.data(), c.data(), cb.size());
+    void* pb = nullptr;
+    void* pc = nullptr;
+    if ((st = upload(&pb, bb)) != LRS_OK) return cleanup_fail(st);
+    h->w_cpb = static_cast<float*>(pb);
+    if ((st = upload(&pc, cb)) != LRS_OK) return cleanup_fail(st);
+    h->w_cpc = static_cast<float*>(pc);
+  } else if (!h->svd) {
     const int kk = kh * kw;
     std::vector<float> m(static_cast<size_t>(r2p) * kk * r1p, 0.f);  // G^T [R2p][tap*R1p + a]
     for (int a = 0; a < r1; ++a)
@@ -1005,7 +1034,15 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   g.h = H; g.w = W; g.ho = ho; g.wo = wo; g.kh = kh; g.kw = kw;
   g.sh = d->stride_h; g.sw = d->stride_w; g.ph = d->pad_h; g.pw = d->pad_w;
   // ---------------------------------------------------------------- a2: T2 = conv(T1, G)
-  if (!h->svd) {
+  if (h->cp_core) {
+    CpDwParams& q = h->cpp;
+    q.t1 = h->t1;
+    q.t2 = h->t2;
+    q.b = h->w_cpb;
+    q.c = h->w_cpc;
+    q.h = H; q.w = W; q.ho = ho; q.wo = wo; q.ld = r1p;
+    q.kh = kh; q.kw = kw; q.sh = d->stride_h; q.sw = d->stride_w; q.ph = d->pad_h; q.pw = d->pad_w;
+  } else if (!h->svd) {
     GemmParams& p = h->a2.p;
     memset(&p, 0, sizeof(p));
     // K chunks must not straddle taps: the swizzle width has to divide R1p * esz
@@ -1272,7 +1309,18 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
       (st = launch(h, 0, h->a1, dim3(static_cast<unsigned>((pin + kTileM - 1) / kTileM)), stream)) != LRS_OK)
     return st;
   // a2
-  if (!h->svd && !h->use_core && !(h->skip & 2)) {
+  if (h->cp_core && !(h->skip & 2)) {
+    CpDwParams& q = h->cpp;
+    q.n = n;
+    const long long items = static_cast<long long>(n) * h->ho * h->wo * (q.ld / (f32 ? 4 : 8));
+    const unsigned grid = static_cast<unsigned>(std::min<long long>((items + kCpThreads - 1) / kCpThreads, 16LL * h->sms));
+    cudaEvent_t e1 = nullptr;
+    if ((st = time_begin(h, 1, stream, &e1)) != LRS_OK) return st;
+    LRS_CUDA(launch_pdl(f32 ? reinterpret_cast<const void*>(&lrs_cp_dw_kernel<true>)
+                            : reinterpret_cast<const void*>(&lrs_cp_dw_kernel<false>),
+                        dim3(grid), dim3(kCpThreads), &q, 0, stream));
+    if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
+  } else if (!h->svd && !h->use_core && !(h->skip & 2)) {
     h->a2.p.g.n = n;
     const int tiles = ((n + h->a2.p.g.nb - 1) / h->a2.p.g.nb) * h->a2.p.g.tiles_h;
     if ((st = launch(h, 1, h->a2, dim3(tiles), stream)) != LRS_OK) return st;
@@ -1361,7 +1409,7 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
-                  h->w_as, h->w_e, h->w_res, h->w_dense_img, h->sp_ent, h->sp_ptr};
+                  h->w_as, h->w_e, h->w_res, h->w_dense_img, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto& r : h->ring)
@@ -1418,6 +1466,7 @@ lrs_status lrs_conv_stage_times(lrs_conv* h, float* ms, int64_t* counts, int32_t
 const char* lrs_conv_stage_name(const lrs_conv* h, int32_t stage) {
   static const char* names[] = {"a1_proj", "a2_core", "a345_expand_sparse", "a4_sparse_add"};
   if (stage == 0 && h && h->use_core) return "a12_proj_core";
+  if (stage == 1 && h && h->cp_core) return "a2_cp_depthwise";
   if (stage == 2 && h && h->use_spadd) return "a3_expand";
   return (stage >= 0 && stage < 4) ? names[stage] : "";
 }
@@ -1430,6 +1479,59 @@ int32_t lrs_conv_sparse_engine(const lrs_conv* h, int32_t* main_blocks, int32_t*
 }
 
 int32_t lrs_conv_core_fused(const lrs_conv* h) { return h ? (h->use_core ? 1 : 0) : -1; }
+
+lrs_status lrs_sparse_from_slices(int32_t c_in, int32_t c_out, int32_t kernel_h, int32_t kernel_w,
+                                  const int64_t* slice_ptr, const void* packed, int32_t packed_bytes,
+                                  const float* values, int64_t* row_ptr, int32_t* col_idx, float* values_out) {
+  if (c_in <= 0 || c_out <= 0 || kernel_h <= 0 || kernel_w <= 0)
+    return fail(LRS_ERR_INVALID_ARGUMENT, "all extents must be > 0");
+  if (packed_bytes != 2 && packed_bytes != 4) return fail(LRS_ERR_INVALID_ARGUMENT, "packed_bytes must be 2 or 4");
+  if (!slice_ptr || !row_ptr) return fail(LRS_ERR_INVALID_ARGUMENT, "slice_ptr / row_ptr is NULL");
+  if (slice_ptr[0] != 0) return fail(LRS_ERR_INVALID_ARGUMENT, "slice_ptr[0] != 0");
+  for (int i = 0; i < c_in; ++i)
+    if (slice_ptr[i + 1] < slice_ptr[i]) return fail(LRS_ERR_INVALID_ARGUMENT, "slice_ptr not monotone at %d", i);
+  const int64_t nnz = slice_ptr[c_in];
+  if (nnz > 0 && (!packed || !values || !col_idx || !values_out))
+    return fail(LRS_ERR_INVALID_ARGUMENT, "NULL entry array");
+  const int64_t taps = static_cast<int64_t>(kernel_h) * kernel_w;
+  if (packed_bytes == 2 && static_cast<int64_t>(c_out) * taps > 65536)
+    return fail(LRS_ERR_INVALID_ARGUMENT, "c_out * kernel taps > 65536 needs 4-byte packed indices");
+  // decode: packed = j * taps + tap (tap = ky * kernel_w + kx), slice i = input channel
+  std::vector<int64_t> cnt(static_cast<size_t>(c_out) + 1, 0);
+  std::vector<std::pair<int32_t, int32_t>> jc(static_cast<size_t>(nnz));  // (row j, col)
+  for (int i = 0; i < c_in; ++i)
+    for (int64_t e = slice_ptr[i]; e < slice_ptr[i + 1]; ++e) {
+      const int64_t pk = packed_bytes == 2 ? static_cast<const uint16_t*>(packed)[e]
+                                           : static_cast<const uint32_t*>(packed)[e];
+      const int64_t j = pk / taps, tap = pk % taps;
+      if (j >= c_out) return fail(LRS_ERR_INVALID_ARGUMENT, "packed index %lld decodes to row %lld >= c_out",
+                                  (long long)pk, (long long)j);
+      jc[static_cast<size_t>(e)] = {static_cast<int32_t>(j), static_cast<int32_t>(i * taps + tap)};
+      ++cnt[static_cast<size_t>(j) + 1];
+    }
+  for (int j = 0; j < c_out; ++j) cnt[j + 1] += cnt[j];
+  for (int j = 0; j <= c_out; ++j) row_ptr[j] = cnt[j];
+  std::vector<int64_t> fillp(cnt.begin(), cnt.end() - 1);
+  std::vector<std::pair<int32_t, float>> tmp(static_cast<size_t>(nnz));
+  for (int64_t e = 0; e < nnz; ++e) {
+    const int32_t j = jc[static_cast<size_t>(e)].first;
+    tmp[static_cast<size_t>(fillp[j]++)] = {jc[static_cast<size_t>(e)].second, values[e]};
+  }
+  for (int j = 0; j < c_out; ++j) {
+    auto b = tmp.begin() + cnt[j], en = tmp.begin() + cnt[j + 1];
+    std::sort(b, en, [](const std::pair<int32_t, float>& u, const std::pair<int32_t, float>& v) {
+      return u.first < v.first;
+    });
+    for (auto it = b; it != en; ++it) {
+      if (it != b && it->first == (it - 1)->first)
+        return fail(LRS_ERR_INVALID_ARGUMENT, "duplicate entry (row %d, col %d)", j, it->first);
+      const int64_t e = it - tmp.begin();
+      col_idx[e] = it->first;
+      values_out[e] = it->second;
+    }
+  }
+  return LRS_OK;
+}
 
 lrs_status lrs_conv_debug_trace(lrs_conv* h, void* dev_buf) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");

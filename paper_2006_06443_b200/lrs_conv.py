@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_PKG, "liblrs_conv.so")
 
 LRS_OK, LRS_ERR_INVALID_ARGUMENT, LRS_ERR_UNSUPPORTED, LRS_ERR_OUT_OF_MEMORY, LRS_ERR_CUDA = range(5)
 LRS_DTYPE_F32, LRS_DTYPE_BF16 = 0, 1
+LRS_CORE_TUCKER2, LRS_CORE_CP = 0, 1
 STATUS_NAMES = {0: "LRS_OK", 1: "LRS_ERR_INVALID_ARGUMENT", 2: "LRS_ERR_UNSUPPORTED",
                 3: "LRS_ERR_OUT_OF_MEMORY", 4: "LRS_ERR_CUDA"}
 
@@ -25,7 +26,8 @@ STATUS_NAMES = {0: "LRS_OK", 1: "LRS_ERR_INVALID_ARGUMENT", 2: "LRS_ERR_UNSUPPOR
 EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
             "lrs_conv_last_error", "lrs_conv_output_shape", "lrs_conv_launches_per_forward",
             "lrs_conv_set_timing", "lrs_conv_stage_times", "lrs_conv_stage_name",
-            "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine", "lrs_conv_core_fused")
+            "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine", "lrs_conv_core_fused",
+            "lrs_sparse_from_slices")
 
 
 class LrsError(RuntimeError):
@@ -48,6 +50,7 @@ class lrs_conv_desc(ctypes.Structure):
         ("row_ptr", ctypes.POINTER(ctypes.c_int64)),
         ("col_idx", ctypes.POINTER(ctypes.c_int32)),
         ("values", ctypes.POINTER(ctypes.c_float)),
+        ("core_kind", ctypes.c_int32),
     ]
 
 
@@ -83,6 +86,11 @@ def load_library(path: str = LIB_PATH):
     lib.lrs_conv_sparse_engine.restype = ctypes.c_int32
     lib.lrs_conv_core_fused.argtypes = [P]
     lib.lrs_conv_core_fused.restype = ctypes.c_int32
+    lib.lrs_sparse_from_slices.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.POINTER(ctypes.c_int64), P, ctypes.c_int32,
+                                           ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64),
+                                           ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_float)]
+    lib.lrs_sparse_from_slices.restype = ctypes.c_int
     for name in ("lrs_conv_debug_trace", "lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
                  "lrs_conv_output_shape", "lrs_conv_set_timing", "lrs_conv_stage_times",
                  "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine"):
@@ -122,7 +130,7 @@ def lrs_conv_last_error() -> str:
 def make_desc(batch_max: int, in_h: int, in_w: int, c_in: int, c_out: int, kernel: int,
               stride: int, pad: int, rank_in: int, rank_out: int, dtype: str,
               u_in: np.ndarray, core: Optional[np.ndarray], u_out: np.ndarray,
-              row_ptr: np.ndarray, col_idx: np.ndarray, values: np.ndarray):
+              row_ptr: np.ndarray, col_idx: np.ndarray, values: np.ndarray, core_kind: int = LRS_CORE_TUCKER2):
     """Build an lrs_conv_desc from host arrays.  Factor arrays are float32
     holding dtype-representable values; for bf16 their bf16 bits are passed.
     Returns (desc, keepalive) -- keep `keepalive` until lrs_conv_create returns."""
@@ -149,8 +157,36 @@ def make_desc(batch_max: int, in_h: int, in_w: int, c_in: int, c_out: int, kerne
         u_out=ptr(as_dtype(u_out)), nnz=len(va),
         row_ptr=rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
         col_idx=ci.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-        values=va.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+        values=va.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), core_kind=core_kind)
     return d, keep
+
+
+def sparse_from_slices(c_in: int, c_out: int, kernel_h: int, kernel_w: int, vals, packed):
+    """The paper's per-input-channel (values, packed index) slices -> CSR, through
+    the C-ABI's host converter lrs_sparse_from_slices (include/lrs_conv.h).
+    vals/packed: lists of c_in arrays (packed uint16 or uint32).  Returns
+    (row_ptr int64 [c_out+1], col_idx int32 [nnz], values float32 [nnz])."""
+    lib = load_library()
+    lens = [len(v) for v in vals]
+    sp = np.zeros(c_in + 1, np.int64)
+    sp[1:] = np.cumsum(lens)
+    nnz = int(sp[-1])
+    width = 4 if any(np.asarray(p).dtype.itemsize == 4 for p in packed) else 2
+    pk = np.ascontiguousarray(np.concatenate([np.asarray(p) for p in packed]) if nnz else np.zeros(1),
+                              np.uint32 if width == 4 else np.uint16)
+    va = np.ascontiguousarray(np.concatenate([np.asarray(v, np.float32) for v in vals]) if nnz else np.zeros(1),
+                              np.float32)
+    rp = np.zeros(c_out + 1, np.int64)
+    ci = np.zeros(max(nnz, 1), np.int32)
+    vo = np.zeros(max(nnz, 1), np.float32)
+    _check(lib.lrs_sparse_from_slices(c_in, c_out, kernel_h, kernel_w,
+                                      sp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                      pk.ctypes.data_as(ctypes.c_void_p), width,
+                                      va.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                      rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                      ci.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                      vo.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+    return rp, ci[:nnz], vo[:nnz]
 
 
 class LrsConv:
@@ -158,7 +194,8 @@ class LrsConv:
     with x, y NHWC torch tensors (contiguous, or channels_last NCHW views)."""
 
     def __init__(self, batch_max, in_h, in_w, c_in, c_out, kernel, stride, pad, rank_in, rank_out,
-                 dtype, u_in, core, u_out, row_ptr, col_idx, values, device: int = 0):
+                 dtype, u_in, core, u_out, row_ptr, col_idx, values, device: int = 0,
+                 core_kind: int = LRS_CORE_TUCKER2):
         import torch
         self.torch = torch
         self.dtype = dtype
@@ -166,7 +203,7 @@ class LrsConv:
         self.device = device
         self.c_out = c_out
         desc, keep = make_desc(batch_max, in_h, in_w, c_in, c_out, kernel, stride, pad, rank_in,
-                               rank_out, dtype, u_in, core, u_out, row_ptr, col_idx, values)
+                               rank_out, dtype, u_in, core, u_out, row_ptr, col_idx, values, core_kind)
         self.handle = lrs_conv_create(desc, device)
         del keep
         oh, ow = ctypes.c_int32(), ctypes.c_int32()
@@ -180,6 +217,17 @@ class LrsConv:
         return cls(batch_max or inp.x.shape[0], c.in_h, c.in_w, c.c_in, c.c_out, c.k, c.stride, c.pad,
                    c.rank_in, c.rank_out, c.dtype, inp.u_in, inp.core, inp.u_out, inp.row_ptr,
                    inp.col_idx, inp.values, device)
+
+    @classmethod
+    def from_cp(cls, batch_max: int, in_h: int, in_w: int, kernel: int, stride: int, pad: int, dtype: str,
+                a, b, c, d, row_ptr, col_idx, values, device: int = 0) -> "LrsConv":
+        """The paper's CP form L = A_ir B_kr C_pr D_jr: a [c_in][R],
+        b [k][R] (taps along H), c [k][R] (taps along W), d [c_out][R]."""
+        a, b, c, d = (np.asarray(t, np.float32) for t in (a, b, c, d))
+        r = a.shape[1]
+        core = np.concatenate([b, c], axis=0)  # [2k][R]: B then C
+        return cls(batch_max, in_h, in_w, a.shape[0], d.shape[0], kernel, stride, pad, r, r, dtype,
+                   a, core, np.ascontiguousarray(d.T), row_ptr, col_idx, values, device, core_kind=LRS_CORE_CP)
 
     @property
     def launches_per_forward(self) -> int:

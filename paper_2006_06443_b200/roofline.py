@@ -53,9 +53,10 @@ def sparse_macs(n: int, h: int, w: int, k: int, s: int, p: int, col_idx: np.ndar
     return int(n * (vh[tap // k] * vw[tap % k]).sum())
 
 
-def layer_work(cfg, n: int, col_idx: np.ndarray) -> Dict[str, Dict[str, float]]:
+def layer_work(cfg, n: int, col_idx: np.ndarray, cp: bool = False) -> Dict[str, Dict[str, float]]:
     """Per-stage algorithmic bytes and FLOPs for n images of layer `cfg`
-    (a workloads.LayerConfig)."""
+    (a workloads.LayerConfig).  cp: L in the paper's CP form (rank R = rank_in),
+    whose stages 2-3 are two depthwise convs of k MACs per output and channel."""
     esz = 2 if cfg.dtype == "bf16" else 4
     ho, wo = cfg.out_h, cfg.out_w
     p_in = n * cfg.in_h * cfg.in_w
@@ -86,9 +87,12 @@ def layer_work(cfg, n: int, col_idx: np.ndarray) -> Dict[str, Dict[str, float]]:
                                "flops": 2.0 * p_in * cfg.c_in * r1 + 2.0 * p * r1 * r2 * cfg.k * cfg.k}
         st["a2_core"] = {"bytes": t1_b + t2_b + r1 * r2 * cfg.k * cfg.k * esz,
                          "flops": 2.0 * p * r1 * r2 * cfg.k * cfg.k}
-    layer_bytes = x_b + y_b + esz * (cfg.c_in * r1 + (0 if cfg.svd else r1 * r2 * cfg.k ** 2) + r2 * cfg.c_out) \
-        + nnz * 8 + (cfg.c_out + 1) * 4
-    chain = 2.0 * (p_in * cfg.c_in * r1 + (0 if cfg.svd else p * r1 * r2 * cfg.k ** 2) + p * r2 * cfg.c_out)
+    core_w = (2 * cfg.k * r1) if cp else (0 if cfg.svd else r1 * r2 * cfg.k ** 2)
+    core_macs = (2 * p * r1 * cfg.k) if cp else (0 if cfg.svd else p * r1 * r2 * cfg.k ** 2)
+    if cp:
+        st["a2_cp_depthwise"] = {"bytes": t1_b + t2_b + core_w * 4, "flops": 2.0 * core_macs}
+    layer_bytes = x_b + y_b + esz * (cfg.c_in * r1 + core_w + r2 * cfg.c_out) + nnz * 8 + (cfg.c_out + 1) * 4
+    chain = 2.0 * (p_in * cfg.c_in * r1 + core_macs + p * r2 * cfg.c_out)
     st["layer"] = {"bytes": layer_bytes, "flops_chain": chain, "flops_sparse": 2.0 * macs_s,
                    "sparse_macs": macs_s, "flops": chain + 2.0 * macs_s}
     return st

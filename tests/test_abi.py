@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_functions():
     src = open(os.path.join(ROOT, "include", "lrs_conv.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:lrs_status|const char \*|int32_t)\s*\**\s*(lrs_conv_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:lrs_status|const char \*|int32_t)\s*\**\s*(lrs_(?:conv|sparse)_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_header_symbol():
@@ -69,7 +69,7 @@ def patched_status(**fields):
 @pytest.mark.parametrize("fields", [
     dict(batch_max=0), dict(in_h=0), dict(c_out=-1), dict(rank_in=0),
     dict(stride_h=0), dict(pad_w=-1), dict(kernel_h=20),  # output extent < 1
-    dict(dtype=7), dict(nnz=-1),
+    dict(dtype=7), dict(nnz=-1), dict(core_kind=5),
 ])
 def test_invalid_descriptors(fields):
     st, msg = patched_status(**fields)
@@ -126,3 +126,11 @@ def test_product_package_does_not_import_oracle():
         if f.endswith(".py"):
             src = open(os.path.join(ROOT, "oracle", f)).read()
             assert "import paper_2006_06443_b200" not in src and "from paper_2006_06443_b200" not in src, f
+
+
+def test_cp_core_requires_core_and_equal_ranks():
+    """LRS_CORE_CP (include/lrs_conv.h): R = rank_in = rank_out and a core array."""
+    st, msg = patched_status(core_kind=1, rank_out=3)
+    assert st == B.LRS_ERR_INVALID_ARGUMENT and "CP" in msg
+    st, msg = patched_status(core_kind=1, core=None)
+    assert st == B.LRS_ERR_INVALID_ARGUMENT and "CP" in msg

@@ -312,3 +312,30 @@ def test_c5_reference_network_pinned_to_dense_conv2d():
     assert len(layers) == 16
     assert sum(c.stride == 2 for _, _, c in layers) == 3
     assert {n for _, n, c in layers if c.stride == 2} == {"layer2.0.conv2", "layer3.0.conv2", "layer4.0.conv2"}
+
+
+@pytest.mark.parametrize("stride,pad", [(1, 1), (2, 1), (1, 0)])
+def test_forward_cp_against_brute_force(stride, pad):
+    """O.forward_cp (the CP layer the GPU CP path is compared with) against the
+    independent quintuple loop on the densified kernel, tiny input: the CP
+    kernel L = A_ir B_kr C_pr D_jr written out with loops here,
+    plus the sparse entries placed by hand."""
+    rng = np.random.default_rng(21)
+    i_ch, j_ch, k, r = 3, 4, 3, 2
+    a, b, c, d = (rng.standard_normal(s) for s in ((i_ch, r), (k, r), (k, r), (j_ch, r)))
+    x = rng.standard_normal((1, 5, 6, i_ch))
+    w = np.zeros((i_ch, j_ch, k, k))
+    for ii in range(i_ch):
+        for jj in range(j_ch):
+            for y in range(k):
+                for xx in range(k):
+                    w[ii, jj, y, xx] = sum(a[ii, q] * b[y, q] * c[xx, q] * d[jj, q] for q in range(r))
+    row_ptr = np.array([0, 1, 1, 3, 3], np.int64)
+    col_idx = np.array([4, 0, 26], np.int32)        # (c*k + y)*k + x
+    values = np.array([0.5, -1.0, 2.0])
+    w[0, 0, 1, 1] += 0.5
+    w[0, 2, 0, 0] += -1.0
+    w[2, 2, 2, 2] += 2.0
+    ref = O.brute_force_conv(x, w, stride, pad)
+    got = O.forward_cp(x, a, b, c, d, row_ptr, col_idx, values, stride, pad)
+    assert rel_l2(got, ref) < 1e-13

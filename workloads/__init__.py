@@ -36,6 +36,7 @@ __all__ = [
     "LayerConfig", "LayerInputs", "CONFIGS", "generate", "bf16_round",
     "bf16_bits", "resnet50_table2", "RESNET50_COMPRESSED_3X3", "generate_weights",
     "resnet50_compressed_layers", "RESNET50_CONV2_MODULES", "resnet50_images",
+    "CpInputs", "generate_cp", "CP_CONFIGS",
 ]
 
 
@@ -185,6 +186,52 @@ def generate_weights(cfg: LayerConfig, seed: Optional[int] = None) -> LayerInput
     return LayerInputs(cfg=cfg, x=None, u_in=_store(u_in, cfg.dtype),
                        core=None if core is None else _store(core, cfg.dtype), u_out=_store(u_out, cfg.dtype),
                        row_ptr=np.cumsum(row_ptr), col_idx=cols.astype(np.int32), values=_store(vals, cfg.dtype))
+
+
+# the paper's own CP form of L at the C1 / C2 shapes,
+# rank R = the configs' Tucker ranks (rank_in == rank_out).
+CP_CONFIGS = {
+    "c1_cp": LayerConfig("c1_cp", 1, 56, 56, 64, 64, 3, 1, 1, 16, 16, 0.01, "f32"),
+    "c2_cp": LayerConfig("c2_cp", 64, 14, 14, 256, 256, 3, 1, 1, 64, 64, 0.02, "bf16"),
+}
+
+
+@dataclasses.dataclass
+class CpInputs:
+    """Inputs of a layer whose L is CP: L_{ijkp} = A_ir B_kr C_pr D_jr."""
+    cfg: LayerConfig
+    x: np.ndarray                 # [N,H,W,Cin]
+    a: np.ndarray                 # [Cin,R]
+    b: np.ndarray                 # [k,R]   taps along H
+    c: np.ndarray                 # [k,R]   taps along W
+    d: np.ndarray                 # [Cout,R]
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+
+def generate_cp(cfg: LayerConfig, batch: Optional[int] = None, seed: Optional[int] = None) -> CpInputs:
+    """Same recipe as `generate` with the CP factors in place of (U_in, G, U_out):
+    draw order X, A ~ N(0, 1/Cin), B ~ N(0, 1/k), C ~ N(0, 1/k), D ~ N(0, 1/R),
+    S positions, S values (fan-in variances, reading #8)."""
+    n = cfg.batch if batch is None else batch
+    rng = np.random.Generator(np.random.PCG64(cfg.seed if seed is None else seed))
+    k, r = cfg.k, cfg.rank_in
+    x = np.maximum(rng.standard_normal((n, cfg.in_h, cfg.in_w, cfg.c_in)), 0.0)
+    a = rng.standard_normal((cfg.c_in, r)) / np.sqrt(cfg.c_in)
+    b = rng.standard_normal((k, r)) / np.sqrt(k)
+    c = rng.standard_normal((k, r)) / np.sqrt(k)
+    d = rng.standard_normal((cfg.c_out, r)) / np.sqrt(r)
+    nnz = cfg.nnz
+    pos = np.sort(rng.choice(cfg.numel_w, size=nnz, replace=False)) if nnz > 0 else np.zeros(0, np.int64)
+    vals = rng.standard_normal(nnz) * np.sqrt(0.1)
+    row_len = cfg.c_in * k * k
+    rows, cols = pos // row_len, pos % row_len
+    row_ptr = np.zeros(cfg.c_out + 1, dtype=np.int64)
+    np.add.at(row_ptr, rows + 1, 1)
+    st = lambda t: _store(t, cfg.dtype)  # noqa: E731
+    return CpInputs(cfg=cfg, x=st(x), a=st(a), b=st(b), c=st(c), d=st(d), row_ptr=np.cumsum(row_ptr),
+                    col_idx=cols.astype(np.int32), values=st(vals))
 
 
 def resnet50_table2(path: Optional[str] = None):
