@@ -165,10 +165,10 @@ lrs_status lrs_conv_debug_buffer(const lrs_conv *h, int32_t which, const void **
  *      input channels of a (output channel, tap) is split exactly into a main
  *      2:4 block and, where the group holds 3-4 nonzeros, a residual 2:4 block;
  *      fused with the expansion GEMM (bf16 layers with c_in % 64 == 0);
- *   2  fp32 layers with out_w <= 64: the expansion GEMM stores Y_L, then a
- *      SIMT CSR gather over shared-memory windows of 4 images adds Y_S into Y
- *      (one extra read-modify-write of Y; set LRS_F32_FUSED=1 at create to
- *      select engine 0 instead).
+ *   2  fp32 layers with out_w <= 64: one SIMT kernel computes the expansion
+ *      (register-blocked fp32 GEMM over a shared-memory tile of T2) and the
+ *      sparse term (CSR gather over shared-memory windows of 4 images) and
+ *      writes Y once (set LRS_F32_FUSED=1 at create to select engine 0).
  * For engine 1, *main_blocks / *residual_blocks (may be NULL) receive the
  * number of 128-row compressed blocks of each kind.
  */

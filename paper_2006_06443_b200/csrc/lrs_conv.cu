@@ -200,6 +200,7 @@ struct lrs_conv {
   uint32_t sp_smem = 0;
   int2* sp_ent = nullptr;
   int* sp_ptr = nullptr;
+  float* sp_uo = nullptr;  // U_out fp32 [R2p][Cout] for the SIMT expansion
   // CP core (the paper's form): stages 2-3 as two depthwise convs
   bool cp_core = false;
   float* w_cpb = nullptr;  // [kh][R1p] vertical taps
@@ -557,7 +558,8 @@ lrs_status build_spadd(lrs_conv* h, const lrs_conv_desc* d) {
         max_ent = std::max(max_ent, static_cast<int>(ent.size() - first));
       }
     ptr.back() = static_cast<int>(ent.size());
-    const uint32_t need = static_cast<uint32_t>(cc) * plane * 16 + static_cast<uint32_t>(max_ent) * 8;
+    const uint32_t need = std::max(static_cast<uint32_t>(cc) * plane * 16, kSpDenseBytes) +
+                          static_cast<uint32_t>(max_ent) * 8;
     if (need <= budget) break;
     if (cc <= 4) return LRS_OK;
     cc = std::max(4, cc / 2 / 4 * 4);
@@ -568,8 +570,9 @@ lrs_status build_spadd(lrs_conv* h, const lrs_conv_desc* d) {
   q.pitch = pitch;
   q.max_ent = max_ent;
   if (const char* e = getenv("LRS_SPADD_DBG")) q.dbg = atoi(e);
-  q.win_bytes = static_cast<uint32_t>(cc) * plane * 16;
+  q.win_bytes = std::max(static_cast<uint32_t>(cc) * plane * 16, kSpDenseBytes);
   h->sp_smem = q.win_bytes + static_cast<uint32_t>(std::max(max_ent, 1)) * 8;
+  if (h->sp_smem > 113 * 1024u) return LRS_OK;  // keep two CTAs per SM
   std::vector<uint8_t> pe(ptr.size() * 4), ee(std::max<size_t>(ent.size(), 1) * 8, 0);
   memcpy(pe.data(), ptr.data(), pe.size());
   if (!ent.empty()) memcpy(ee.data(), ent.data(), ent.size() * 8);
@@ -645,7 +648,9 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     const int wcw = (tc - 1) * g.sw + kw;
     const int tbw = s1 ? wcw : tc;
     if (wcw > 256) continue;
+    const int th_env = getenv("LRS_WCONV_TH") ? atoi(getenv("LRS_WCONV_TH")) : 0;  // planner experiments
     for (int th = std::min(ho, 64); th >= 1; --th) {
+      if (th_env && th != th_env) continue;
       const int acc = make_units(th, tc, wcw, tbw, units);
       if (static_cast<int>(units.size()) > kWMaxUnits) continue;
       const int wr = (th - 1) * g.sh + kh;
@@ -1094,33 +1099,20 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     if ((st = build_spadd(h, d)) != LRS_OK) return cleanup_fail(st);
   }
   if (h->use_spadd) {
-    // a3 alone: Y = T2 U_out (Y_L); lrs_spadd_kernel then adds Y_S in place
-    GemmParams& p = h->a3.p;
-    memset(&p, 0, sizeof(p));
-    const int kdim = r2p;
-    const uint32_t sw = pick_sw(kdim * esz);
-    h->a3.smem = plan_stage(p, f32, kdim * esz, sw, bn, cout_p, kTileM * sw, 0);
-    if (!h->a3.smem) return cleanup_fail(fail(LRS_ERR_UNSUPPORTED, "a3 does not fit in shared memory"));
-    p.amode = AMODE_2D;
-    p.out_ld = cout;
-    p.out_cols = cout;
-    {
-      void* src = h->svd ? h->t1 : h->t2;
-      uint64_t dims[2] = {static_cast<uint64_t>(kdim), static_cast<uint64_t>(p_max)};
-      uint64_t strides[1] = {static_cast<uint64_t>(kdim) * esz};
-      uint32_t box[2] = {static_cast<uint32_t>(p.kc), static_cast<uint32_t>(kTileM)};
-      uint32_t estr[2] = {1, 1};
-      if ((st = encode(&p.tmA, f32, 2, src, dims, strides, box, estr, sw)) != LRS_OK) return cleanup_fail(st);
-    }
-    {
-      uint64_t dims[2] = {static_cast<uint64_t>(kdim), static_cast<uint64_t>(cout_p) * (f32 ? 2 : 1)};
-      uint64_t strides[1] = {static_cast<uint64_t>(kdim) * esz};
-      uint32_t box[2] = {static_cast<uint32_t>(p.kc), static_cast<uint32_t>(bn)};
-      uint32_t estr[2] = {1, 1};
-      if ((st = encode(&p.tmB, f32, 2, h->w_uout, dims, strides, box, estr, sw)) != LRS_OK) return cleanup_fail(st);
-    }
-    h->a3.name = "a3_expand";
-    h->a3.kid = K_STORE_F32;
+    // a3 + a4 + a5 in lrs_spadd_kernel: U_out as plain fp32 [R2p][Cout] (zero rows past R2)
+    std::vector<float> m(static_cast<size_t>(r2p) * cout, 0.f);
+    for (int b = 0; b < r2; ++b)
+      for (int j = 0; j < cout; ++j) m[static_cast<size_t>(b) * cout + j] = host_val(d->u_out, (size_t)b * cout + j, f32);
+    std::vector<uint8_t> mb(m.size() * 4);
+    memcpy(mb.data(), m.data(), mb.size());
+    void* pu = nullptr;
+    if ((st = upload(&pu, mb)) != LRS_OK) return cleanup_fail(st);
+    h->sp_uo = static_cast<float*>(pu);
+    SpaddParams& q = h->spp;
+    q.t = static_cast<const float*>(h->svd ? h->t1 : h->t2);
+    q.t_ld = r2p;
+    q.r = r2p;
+    q.uo = h->sp_uo;
   } else if (!h->use_w) {
     GemmParams& p = h->a3.p;
     memset(&p, 0, sizeof(p));
@@ -1359,19 +1351,18 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
   h->a3.p.g.n = n;
   h->a3.p.sp.x = x;
   h->a3.p.sp.y = y;
-  if (h->use_spadd) h->a3.p.out = y;
-  if (!(h->skip & 4) &&
+  if (!h->use_spadd && !(h->skip & 4) &&
       (st = launch(h, 2, h->a3,
                    dim3(static_cast<unsigned>((P + kTileM - 1) / kTileM), h->cout_p / h->bn), stream)) != LRS_OK)
     return st;
-  if (h->use_spadd && !(h->skip & 8)) {
+  if (h->use_spadd && !(h->skip & 4)) {
     SpaddParams& q = h->spp;
     q.x = static_cast<const float*>(x);
     q.y = static_cast<float*>(y);
     q.n = n;
     const unsigned grid = static_cast<unsigned>(((n + 3) / 4) * q.bands * q.n_nc);
     cudaEvent_t e1 = nullptr;
-    if ((st = time_begin(h, 3, stream, &e1)) != LRS_OK) return st;
+    if ((st = time_begin(h, 2, stream, &e1)) != LRS_OK) return st;
     LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_spadd_kernel), dim3(grid), dim3(kSpThreads), &q,
                         h->sp_smem, stream));
     if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
@@ -1409,7 +1400,8 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
-                  h->w_as, h->w_e, h->w_res, h->w_dense_img, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc};
+                  h->w_as, h->w_e, h->w_res, h->w_dense_img, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc,
+                  h->sp_uo};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto& r : h->ring)
@@ -1427,7 +1419,7 @@ lrs_status lrs_conv_output_shape(const lrs_conv* h, int32_t* out_h, int32_t* out
 }
 
 int32_t lrs_conv_launches_per_forward(const lrs_conv* h) {
-  return h ? (h->svd ? 2 : 3) + (h->use_spadd ? 1 : 0) - (h->use_core ? 1 : 0) : 0;
+  return h ? (h->svd ? 2 : 3) - (h->use_core ? 1 : 0) : 0;
 }
 
 lrs_status lrs_conv_set_timing(lrs_conv* h, int32_t enable) {
@@ -1467,7 +1459,6 @@ const char* lrs_conv_stage_name(const lrs_conv* h, int32_t stage) {
   static const char* names[] = {"a1_proj", "a2_core", "a345_expand_sparse", "a4_sparse_add"};
   if (stage == 0 && h && h->use_core) return "a12_proj_core";
   if (stage == 1 && h && h->cp_core) return "a2_cp_depthwise";
-  if (stage == 2 && h && h->use_spadd) return "a3_expand";
   return (stage >= 0 && stage < 4) ? names[stage] : "";
 }
 

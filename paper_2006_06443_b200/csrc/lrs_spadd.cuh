@@ -1,9 +1,11 @@
-// lrs_spadd.cuh -- the sparse term a4 for fp32 layers on the CUDA cores:
+// lrs_spadd.cuh -- a3 + a4 + a5 for fp32 layers on the CUDA cores:
 //
-//   Y[n, ho, wo, j] += sum_{e in row j} v_e X[n, ho*s + y_e - p, wo*s + x_e - p, c_e]
+//   Y[n, ho, wo, j] = sum_b T2[n, ho, wo, b] U_out[b, j]                                 (a3)
+//                   + sum_{e in row j} v_e X[n, ho*s + y_e - p, wo*s + x_e - p, c_e]   (a4)
 //
-// added into Y after the expansion GEMM (a3) has written Y_L there (a5: one
-// read-modify-write of Y).  Direct CSR gather over a shared-memory window of X
+// accumulated in fp32 registers and written to Y once (a5).  The expansion is a
+// register-blocked SIMT GEMM over a shared-memory tile of T2 (exact fp32, no tf32
+// split); the sparse term is a direct CSR gather over a shared-memory window of X
 // whose innermost dimension is 4 IMAGES: one 16-byte shared load then feeds 4
 // FMAs that share the nonzero's value -- the layout the round-1 microbenchmark
 // (tools/ubench_sparse.cu) measured fastest for fp32 activations.  The window
@@ -23,7 +25,9 @@
 namespace lrs {
 
 constexpr int kSpThreads = 256;
-constexpr int kSpKP = 2;  // output positions per lane
+constexpr int kSpKP = 2;   // output positions per lane
+constexpr int kSpRc = 32;  // ranks per staged chunk of the expansion
+constexpr uint32_t kSpDenseBytes = kSpRc * 32 * kSpKP * 16 + kSpRc * 64 * 4;  // T2 tile + U_out tile
 
 struct SpaddParams {
   const float* x;
@@ -37,14 +41,17 @@ struct SpaddParams {
   const int2* ent;      // (fp32 value bits, window byte offset)
   const int* ent_ptr;   // [(nc * n_cc + c) * 64 + jl] first entry; [+64] end of the chunk
   int max_ent;          // max entries of one (nc, c) chunk (smem staging)
-  uint32_t win_bytes;
+  uint32_t win_bytes;    // the shared region: max(X window, kSpDenseBytes)
+  const float* t;        // T2 (or T1 of the SVD pair) [n][ho][wo][t_ld]
+  const float* uo;       // U_out [r][cout] fp32 (rows >= R2 zero)
+  int t_ld, r;           // row pitch of T, ranks to sum (multiple of 4)
   int dbg;              // timing experiments (LRS_SPADD_DBG): 1 skip staging, 2 skip gather, 4 skip Y update
 };
 
 __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_constant__ SpaddParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
   float4* win = reinterpret_cast<float4*>(sm);
-  int2* ents = reinterpret_cast<int2*>(sm + p.win_bytes);
+  int2* ents0 = reinterpret_cast<int2*>(sm + p.win_bytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int bid = blockIdx.x;
   const int nc = bid % p.n_nc;
@@ -55,7 +62,7 @@ __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_c
   const int rows = min(p.th, p.ho - ho0);
   const int npos = rows * p.wo;
   const int jw = nc * 64 + warp * 8;  // first output channel of this warp
-  // PDL: Y is written by the expansion GEMM launched just before (and X by
+  // PDL: T2 is written by the core kernel launched just before (and X by
   // whatever ran before the chain); wait for both before touching either
   pdl_launch_dependents();
   pdl_wait();
@@ -78,8 +85,59 @@ __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_c
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[k][jj][i] = 0.f;
 
+  // ---- a3: acc = T2 tile . U_out, rank chunks of kSpRc staged as [rank][position][4 images]
+  {
+    float4* tt = win;
+    const float4* us4 = reinterpret_cast<const float4*>(sm + kSpRc * 32 * kSpKP * 16);
+    for (int b0 = 0; b0 < p.r; b0 += kSpRc) {
+      const int rcn = min(kSpRc, p.r - b0);
+      for (int wi = threadIdx.x; wi < npos * (rcn / 4); wi += kSpThreads) {
+        const int b4 = wi / npos, q = wi - b4 * npos;
+        const int ho = ho0 + q / p.wo, wo = q - (q / p.wo) * p.wo;
+        float4 v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (n0 + i < p.n)
+            v[i] = __ldg(reinterpret_cast<const float4*>(
+                p.t + ((static_cast<long long>(n0 + i) * p.ho + ho) * p.wo + wo) * p.t_ld + b0 + 4 * b4));
+        }
+        float4* dst = tt + (4 * b4) * (32 * kSpKP) + q;
+        dst[0] = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
+        dst[32 * kSpKP] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
+        dst[64 * kSpKP] = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
+        dst[96 * kSpKP] = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+      }
+      float4* usw = reinterpret_cast<float4*>(sm + kSpRc * 32 * kSpKP * 16);
+      for (int wi = threadIdx.x; wi < rcn * 16; wi += kSpThreads) {
+        const int bl = wi >> 4, j = nc * 64 + 4 * (wi & 15);
+        usw[wi] = j < p.cout ? __ldg(reinterpret_cast<const float4*>(p.uo + static_cast<long long>(b0 + bl) * p.cout + j))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int bl = 0; bl < rcn; ++bl) {
+        const float4 ua = us4[bl * 16 + warp * 2], ub = us4[bl * 16 + warp * 2 + 1];
+        const float u[8] = {ua.x, ua.y, ua.z, ua.w, ub.x, ub.y, ub.z, ub.w};
+#pragma unroll
+        for (int k = 0; k < kSpKP; ++k) {
+          const float4 tv = tt[bl * (32 * kSpKP) + lane + 32 * k];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            acc[k][jj][0] = fmaf(u[jj], tv.x, acc[k][jj][0]);
+            acc[k][jj][1] = fmaf(u[jj], tv.y, acc[k][jj][1]);
+            acc[k][jj][2] = fmaf(u[jj], tv.z, acc[k][jj][2]);
+            acc[k][jj][3] = fmaf(u[jj], tv.w, acc[k][jj][3]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+
   const int plane = p.wr * p.pitch;  // vectors per channel
   const int items = p.wr * p.wc * (p.cc / 4);
+  int2* ents = ents0;
   for (int c = 0; c < p.n_cc; ++c) {
     const int c0 = c * p.cc;
     // this warp's CSR row bounds of the chunk (lanes 0..8), loaded ahead of the staging
@@ -153,7 +211,7 @@ __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_c
     }
     __syncthreads();
   }
-  // ---- Y += Y_S: each lane owns 8 consecutive channels of its positions (2 x 16 B per image)
+  // ---- Y = Y_L + Y_S, written once: each lane owns 8 consecutive channels of its positions
   if (jw >= p.cout || (p.dbg & 4)) return;
 #pragma unroll
   for (int k = 0; k < kSpKP; ++k) {
@@ -165,15 +223,12 @@ __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_c
       if (n0 + i >= p.n) continue;
       float* yp = p.y + ((static_cast<long long>(n0 + i) * p.ho + ho) * p.wo + wo) * p.cout + jw;
       if (jw + 8 <= p.cout) {
-        float4 a = *reinterpret_cast<float4*>(yp), b = *reinterpret_cast<float4*>(yp + 4);
-        a.x += acc[k][0][i]; a.y += acc[k][1][i]; a.z += acc[k][2][i]; a.w += acc[k][3][i];
-        b.x += acc[k][4][i]; b.y += acc[k][5][i]; b.z += acc[k][6][i]; b.w += acc[k][7][i];
-        *reinterpret_cast<float4*>(yp) = a;
-        *reinterpret_cast<float4*>(yp + 4) = b;
+        *reinterpret_cast<float4*>(yp) = make_float4(acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
+        *reinterpret_cast<float4*>(yp + 4) = make_float4(acc[k][4][i], acc[k][5][i], acc[k][6][i], acc[k][7][i]);
       } else {
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj)
-          if (jw + jj < p.cout) yp[jj] += acc[k][jj][i];
+          if (jw + jj < p.cout) yp[jj] = acc[k][jj][i];
       }
     }
   }

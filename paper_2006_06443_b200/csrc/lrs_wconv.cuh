@@ -411,7 +411,11 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       const TileCoord tc = tile_coord(p, tile);
       const int b = p.nacc == 2 ? (k & 1) : 0;
       const int use = p.nacc == 2 ? (k >> 1) : k;
-      mbar_wait_sleep(&acc_full[b], use & 1);
+      // one thread polls the accumulator barrier, the other epilogue threads block in a
+      // named barrier: eight warps spinning on an mbarrier slowed the producer's and the
+      // MMA issuer's own barrier traffic (tools/wtrace.py: ~300 ns per hand-off)
+      if (threadIdx.x == 64) mbar_wait_sleep(&acc_full[b], use & 1);
+      named_bar_sync(2, kWThreads - 64);
       tc_fence_after();
       if (WDBG(p, 16)) {
         tc_fence_before();

@@ -1,6 +1,7 @@
-"""GPU parity of the fp32 sparse engine (lrs_spadd.cuh): a3 stores Y_L = T2 U_out,
-then a SIMT CSR gather over 4-image shared-memory windows adds the sparse term
-(eq. for the sparse convolution; a5 sum as a read-modify-write).
+"""GPU parity of the fp32 expansion + sparse engine (lrs_spadd.cuh): one SIMT kernel
+computes Y_L = T2 U_out from a shared-memory tile of T2 and adds the sparse term by
+a CSR gather over 4-image shared-memory windows of X,
+writing Y once (a5).
 Compared with the fp64 oracle at the fp32 tolerance of the BASELINE.json north
 star (relL2 <= 1e-5, max-abs <= 1e-4).  Each geometry pins one mechanism of the
 tiling: ragged image groups (n % 4), Cout not a multiple of 64 or of 8, stride 2,
@@ -53,7 +54,7 @@ def test_fp32_configs_use_the_simt_engine(name):
     inp = workloads.generate(workloads.CONFIGS[name], batch=1)
     layer, _ = run(inp)
     assert layer.sparse_engine[0] == 2
-    assert layer.launches_per_forward == 4
+    assert layer.launches_per_forward == 3  # a1, a2, expansion + sparse
 
 
 GEOMS = [  # (n, h, w, cin, cout, k, s, p, r1, r2, density, svd, engine)
