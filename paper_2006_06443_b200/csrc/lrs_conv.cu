@@ -19,6 +19,7 @@
 #include "lrs_core.cuh"
 #include "lrs_cpdw.cuh"
 #include "lrs_spadd.cuh"
+#include "lrs_tiny.cuh"
 #include "lrs_wconv.cuh"
 
 using namespace lrs;
@@ -201,6 +202,11 @@ struct lrs_conv {
   int2* sp_ent = nullptr;
   int* sp_ptr = nullptr;
   float* sp_uo = nullptr;  // U_out fp32 [R2p][Cout] for the SIMT expansion
+  // small fp32 layers: the whole layer in one SIMT kernel (lrs_tiny.cuh)
+  bool use_tiny = false;
+  TinyParams tp{};
+  uint32_t tiny_smem = 0;
+  void* tiny_buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   // CP core (the paper's form): stages 2-3 as two depthwise convs
   bool cp_core = false;
   float* w_cpb = nullptr;  // [kh][R1p] vertical taps
@@ -398,6 +404,84 @@ inline uint16_t bf16_bits_rne(float f) {
   memcpy(&u, &f, 4);
   u += 0x7FFFu + ((u >> 16) & 1u);
   return static_cast<uint16_t>(u >> 16);
+}
+
+// Small fp32 Tucker-2 layers: the four stages in one SIMT kernel when the weights and one
+// output row's window fit in shared memory and the grid (images x row bands) is small --
+// the regime where the chain's three dependent launches are pure latency (C1).
+lrs_status build_tiny(lrs_conv* h, const lrs_conv_desc* d) {
+  if (!h->f32 || h->svd || h->cp_core || getenv("LRS_NO_TINY")) return LRS_OK;
+  const int cin = d->c_in, cout = d->c_out, kh = d->kernel_h, kw = d->kernel_w;
+  const int ho = h->ho, wo = h->wo, sh = d->stride_h, sw = d->stride_w;
+  const int r1 = d->rank_in, r2 = d->rank_out;
+  const int r1p = round_up(r1, 4), r2p = round_up(r2, 4), taps = kh * kw;
+  const int wc = (wo - 1) * sw + kw;
+  auto a16 = [](uint32_t b) { return (b + 15u) & ~15u; };
+  int th = 1;
+  for (; th <= ho; ++th)  // fewest rows per CTA that keep the grid within two waves
+    if (static_cast<long long>(d->batch_max) * ((ho + th - 1) / th) <= 2LL * h->sms) break;
+  if (th > ho) return LRS_OK;
+  const int wr = (th - 1) * sh + kh;
+  TinyParams& q = h->tp;
+  memset(&q, 0, sizeof(q));
+  const uint32_t xs = a16(static_cast<uint32_t>(cin) * wr * wc * 4);
+  const uint32_t t1 = a16(static_cast<uint32_t>(wr) * wc * r1p * 4);
+  const uint32_t t2 = a16(static_cast<uint32_t>(th) * wo * r2p * 4);
+  const uint32_t us = a16(static_cast<uint32_t>(cin) * r1p * 4);
+  const uint32_t gs = a16(static_cast<uint32_t>(taps) * r1p * r2p * 4);
+  const uint32_t uo = a16(static_cast<uint32_t>(r2p) * cout * 4);
+  const uint32_t rpb = a16(static_cast<uint32_t>(cout + 1) * 4);
+  const uint32_t eb = a16(static_cast<uint32_t>(std::max<int64_t>(d->nnz, 1)) * 4);
+  const uint32_t total = xs + t1 + t2 + us + gs + uo + rpb + 2 * eb;
+  if (total > static_cast<uint32_t>(kMaxSmem) - 1024u || cin % 4 || cout % 4) return LRS_OK;
+  q.off_t1 = xs; q.off_t2 = xs + t1; q.off_u = xs + t1 + t2; q.off_g = q.off_u + us; q.off_uo = q.off_g + gs;
+  q.off_rp = q.off_uo + uo; q.off_ec = q.off_rp + rpb; q.off_ev = q.off_ec + eb;
+  q.nnz = static_cast<int>(d->nnz);
+  const bool f32 = true;
+  std::vector<float> u(static_cast<size_t>(cin) * r1p, 0.f), g(static_cast<size_t>(taps) * r1p * r2p, 0.f),
+      o(static_cast<size_t>(r2p) * cout, 0.f);
+  for (int c = 0; c < cin; ++c)
+    for (int a = 0; a < r1; ++a) u[static_cast<size_t>(c) * r1p + a] = host_val(d->u_in, (size_t)c * r1 + a, f32);
+  for (int a = 0; a < r1; ++a)
+    for (int b = 0; b < r2; ++b)
+      for (int t = 0; t < taps; ++t)
+        g[(static_cast<size_t>(t) * r1p + a) * r2p + b] = host_val(d->core, ((size_t)a * r2 + b) * taps + t, f32);
+  for (int b = 0; b < r2; ++b)
+    for (int j = 0; j < cout; ++j) o[static_cast<size_t>(b) * cout + j] = host_val(d->u_out, (size_t)b * cout + j, f32);
+  std::vector<int> rp(static_cast<size_t>(cout) + 1), ec(static_cast<size_t>(std::max<int64_t>(d->nnz, 1)), 0);
+  std::vector<float> ev(ec.size(), 0.f);
+  for (int j = 0; j <= cout; ++j) rp[j] = static_cast<int>(d->row_ptr[j]);
+  for (int64_t e = 0; e < d->nnz; ++e) {
+    const int col = d->col_idx[e], c = col / taps, t = col % taps;
+    ec[e] = c | ((t / kw) << 16) | ((t % kw) << 24);
+    ev[e] = d->values[e];
+  }
+  auto up = [&](void** dst, const void* src, size_t bytes) {
+    std::vector<uint8_t> b(bytes);
+    memcpy(b.data(), src, bytes);
+    return upload(dst, b);
+  };
+  lrs_status st;
+  if ((st = up(&h->tiny_buf[0], u.data(), u.size() * 4)) != LRS_OK) return st;
+  if ((st = up(&h->tiny_buf[1], g.data(), g.size() * 4)) != LRS_OK) return st;
+  if ((st = up(&h->tiny_buf[2], o.data(), o.size() * 4)) != LRS_OK) return st;
+  if ((st = up(&h->tiny_buf[3], rp.data(), rp.size() * 4)) != LRS_OK) return st;
+  if ((st = up(&h->tiny_buf[4], ec.data(), ec.size() * 4)) != LRS_OK) return st;
+  if ((st = up(&h->tiny_buf[5], ev.data(), ev.size() * 4)) != LRS_OK) return st;
+  q.uin = static_cast<const float*>(h->tiny_buf[0]);
+  q.g = static_cast<const float*>(h->tiny_buf[1]);
+  q.uo = static_cast<const float*>(h->tiny_buf[2]);
+  q.rp = static_cast<const int*>(h->tiny_buf[3]);
+  q.ent_c = static_cast<const int*>(h->tiny_buf[4]);
+  q.ent_v = static_cast<const float*>(h->tiny_buf[5]);
+  q.h = d->in_h; q.w = d->in_w; q.cin = cin; q.ho = ho; q.wo = wo; q.cout = cout;
+  q.kh = kh; q.kw = kw; q.sh = sh; q.sw = sw; q.ph = d->pad_h; q.pw = d->pad_w;
+  q.r1p = r1p; q.r2p = r2p; q.th = th; q.bands = (ho + th - 1) / th; q.wr = wr; q.wc = wc;
+  h->tiny_smem = total;
+  h->use_tiny = true;
+  if (getenv("LRS_VERBOSE"))
+    fprintf(stderr, "[lrs] tiny: th=%d bands=%d wr=%d wc=%d smem=%u\n", th, q.bands, wr, wc, total);
+  return LRS_OK;
 }
 
 // a1 + a2 fused (lrs_core.cuh): pick the band height th and the images per tile ipt
@@ -1091,6 +1175,7 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     h->a2.kid = f32 ? K_STORE_F32 : K_STORE_BF16;
   }
   if ((st = build_core(h, d)) != LRS_OK) return cleanup_fail(st);
+  if ((st = build_tiny(h, d)) != LRS_OK) return cleanup_fail(st);
   // ---------------------------------------------------------------- a3+a4+a5
   if (bf16_w) {
     if ((st = build_wconv(h, d, g)) != LRS_OK) return cleanup_fail(st);
@@ -1219,7 +1304,7 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     if (e != cudaSuccess)
       return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
-  for (const void* fn : {reinterpret_cast<const void*>(&lrs_core_kernel)}) {
+  for (const void* fn : {reinterpret_cast<const void*>(&lrs_core_kernel), reinterpret_cast<const void*>(&lrs_tiny_kernel)}) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
@@ -1268,6 +1353,19 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
   }
   const long long pin = static_cast<long long>(n) * d.in_h * d.in_w;
   const long long P = static_cast<long long>(n) * h->ho * h->wo;
+  if (h->use_tiny) {
+    TinyParams& q = h->tp;
+    q.x = static_cast<const float*>(x);
+    q.y = static_cast<float*>(y);
+    q.n = n;
+    cudaEvent_t e1 = nullptr;
+    if ((st = time_begin(h, 2, stream, &e1)) != LRS_OK) return st;
+    LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_tiny_kernel), dim3(static_cast<unsigned>(n * q.bands)),
+                        dim3(kTyThreads), &q, h->tiny_smem, stream));
+    if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
+    if (prev != h->device) cudaSetDevice(prev);
+    return LRS_OK;
+  }
   if (h->use_core && !(h->skip & 1)) {
     CoreParams& c = h->cp;
     if (h->cx_ptr != x || h->cx_n != n) {
@@ -1404,6 +1502,8 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
                   h->sp_uo};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  for (void* b : h->tiny_buf)
+    if (b) cudaFree(b);
   for (auto& r : h->ring)
     for (auto e : r.ev) cudaEventDestroy(e);
   cudaSetDevice(prev);
@@ -1419,6 +1519,7 @@ lrs_status lrs_conv_output_shape(const lrs_conv* h, int32_t* out_h, int32_t* out
 }
 
 int32_t lrs_conv_launches_per_forward(const lrs_conv* h) {
+  if (h && h->use_tiny) return 1;
   return h ? (h->svd ? 2 : 3) - (h->use_core ? 1 : 0) : 0;
 }
 
@@ -1466,7 +1567,7 @@ int32_t lrs_conv_sparse_engine(const lrs_conv* h, int32_t* main_blocks, int32_t*
   if (!h) return -1;
   if (main_blocks) *main_blocks = h->use_w ? h->w_main_blocks : 0;
   if (residual_blocks) *residual_blocks = h->use_w ? h->w_res_blocks : 0;
-  return h->use_w ? 1 : (h->use_spadd ? 2 : 0);
+  return h->use_w ? 1 : (h->use_tiny ? 3 : (h->use_spadd ? 2 : 0));
 }
 
 int32_t lrs_conv_core_fused(const lrs_conv* h) { return h ? (h->use_core ? 1 : 0) : -1; }
