@@ -65,16 +65,40 @@ def _module(conv: CompressedConv2d):
     return LrsConvModule(conv)
 
 
+def fold_dense_batchnorms(model):
+    """Fold every eval-mode BatchNorm that follows a DENSE conv (stem, bottleneck conv1 /
+    conv3, downsample) into that conv's weight and bias -- the standard inference
+    transform, y = conv(x, W * g / s) + (b - m * g / s), done in fp32 before the bf16
+    cast.  The BatchNorm after each compressed 3x3 conv (bn2) stays a separate op:
+    the library layer has no bias (reading #15)."""
+    torch = _torch()
+    from torch.nn.utils.fusion import fuse_conv_bn_eval
+    model.conv1 = fuse_conv_bn_eval(model.conv1, model.bn1)
+    model.bn1 = torch.nn.Identity()
+    for layer in (model.layer1, model.layer2, model.layer3, model.layer4):
+        for blk in layer:
+            blk.conv1 = fuse_conv_bn_eval(blk.conv1, blk.bn1)
+            blk.bn1 = torch.nn.Identity()
+            blk.conv3 = fuse_conv_bn_eval(blk.conv3, blk.bn3)
+            blk.bn3 = torch.nn.Identity()
+            if blk.downsample is not None:
+                blk.downsample = torch.nn.Sequential(fuse_conv_bn_eval(blk.downsample[0], blk.downsample[1]))
+    return model
+
+
 def build_compressed_resnet50(batch_max: int, device: int = 0, seed: int = 0, density: float = 0.02,
-                              layers: Optional[List] = None):
+                              layers: Optional[List] = None, fold_bn: bool = True):
     """torchvision resnet50 (random init under manual_seed(seed), eval mode,
     bf16, channels_last) on cuda:device with its 16 3x3 convs compressed.
-    Returns (model, {table index: CompressedConv2d})."""
+    fold_bn: fold the BatchNorms of the dense convs into them (fp32, before the
+    bf16 cast).  Returns (model, {table index: CompressedConv2d})."""
     torch = _torch()
     import torchvision
     import workloads
     torch.manual_seed(seed)
     model = torchvision.models.resnet50(weights=None).eval()
+    if fold_bn:
+        model = fold_dense_batchnorms(model)
     model = model.to(device=f"cuda:{device}", dtype=torch.bfloat16).to(memory_format=torch.channels_last)
     comp: Dict[int, CompressedConv2d] = {}
     for idx, name, cfg in (layers or workloads.resnet50_compressed_layers(batch=batch_max, density=density)):

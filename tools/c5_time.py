@@ -21,10 +21,15 @@ def tg(m):
     return e0.elapsed_time(e1) / 10
 t = tg(model)
 print(f"compressed resnet50 n={n}: {t:.3f} ms/forward, {n/t*1e3:.0f} img/s")
-torch.manual_seed(0)
-dense = torchvision.models.resnet50(weights=None).eval().cuda().to(torch.bfloat16).to(memory_format=torch.channels_last)
-t2 = tg(dense)
-print(f"dense cuDNN resnet50 n={n}: {t2:.3f} ms/forward, {n/t2*1e3:.0f} img/s")
+from paper_2006_06443_b200.resnet import fold_dense_batchnorms
+for fold in (False, True):
+    torch.manual_seed(0)
+    dense = torchvision.models.resnet50(weights=None).eval()
+    if fold:
+        dense = fold_dense_batchnorms(dense)
+    dense = dense.cuda().to(torch.bfloat16).to(memory_format=torch.channels_last)
+    t2 = tg(dense)
+    print(f"dense cuDNN resnet50 (dense BNs folded: {fold}) n={n}: {t2:.3f} ms/forward, {n/t2*1e3:.0f} img/s")
 # per compressed layer time
 for idx, c in comp.items():
     c.layer.set_timing(True); c.layer.stage_times(reset=True)
