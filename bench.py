@@ -519,6 +519,18 @@ def main():
             roof = {"bound": "tensor", "achieved": achieved, "peak": tc, "unit": "TFLOP/s",
                     "frac": achieved / tc, "traffic": None, "kernel": dom}
     roof["peak_kind"] = peaks["source"]
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    # (tools/ncu_traffic.py -> profiles/ncu_traffic.json); per launch, cold cache
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(args.config)
+        if tr:
+            roof["traffic"] = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+            roof["traffic_detail"] = {"kernel": tr["kernel"], "dram_read_bytes": tr["dram_read_bytes"],
+                                      "dram_write_bytes": tr["dram_write_bytes"], "source": tr["source"],
+                                      "note": "Y's write-back mostly lands in L2 after the kernel ends"}
+    except (OSError, ValueError, KeyError):
+        pass
     roof["stage_us"] = {k: round(v * 1e3, 3) for k, v in avg.items()}
     step_s = ms_per_step / 1e3
     layer_roof = {"literal_roof_us": roofs["t_literal_s"] * 1e6, "three_roof_us": roofs["t_three_roof_s"] * 1e6,
