@@ -762,7 +762,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         const long long slack_t = std::max(0LL, last_t + 1 - static_cast<long long>(th) * tbw) * 8 * sw_t;
         const uint32_t stride =
             align1024(static_cast<uint32_t>(std::max<long long>(xw + slack_x, tw + slack_t)));
-        const uint32_t res_bytes = (static_cast<uint32_t>(n_ck * taps) * 4u + 127u) & ~127u;
+        // the M-tile's block stream: chunk starts + a tap offset per (main or residual) block
+        const uint32_t res_bytes = (static_cast<uint32_t>(n_ck + 1 + 2 * n_ck * taps) * 4u + 127u) & ~127u;
         const uint32_t fixed = ns * (a_slot + e_slot) + 8 * kEpiScratch + res_bytes + 1024 + 1024;
         if (2 * stride + fixed > static_cast<uint32_t>(kMaxSmem)) continue;
         int nwb = 2;
@@ -870,6 +871,27 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   h->w_main_blocks = nblk_main;
   h->w_res_blocks = nres;
   const int nblk = nblk_main + nres;
+  // stream order: per (M-tile, chunk), per tap its main block then its residual block, so
+  // the kernel fetches each item (consecutive blocks of a window) with one bulk copy
+  std::vector<int> order, stream_off(static_cast<size_t>(n_mt) * n_ck + 1, 0);
+  std::vector<uint32_t> blk_tap;
+  order.reserve(nblk);
+  blk_tap.reserve(nblk);
+  for (int mt = 0; mt < n_mt; ++mt)
+    for (int c = 0; c < n_ck; ++c) {
+      stream_off[static_cast<size_t>(mt) * n_ck + c] = static_cast<int>(order.size());
+      for (int t = 0; t < taps; ++t) {
+        const int key = (mt * n_ck + c) * taps + t;
+        const uint32_t tap16 = static_cast<uint32_t>((t / kw) * wc + (t % kw)) * 64u;  // (pos * 1024) >> 4
+        order.push_back(key);
+        blk_tap.push_back(tap16);
+        if (res_tab[key] >= 0) {
+          order.push_back(res_tab[key]);
+          blk_tap.push_back(tap16);
+        }
+      }
+    }
+  stream_off.back() = static_cast<int>(order.size());
   lrs_status st;
   // shared-memory images of the A operands (swizzle applied here, 1-D bulk copies in the kernel)
   auto swz_off = [](int r, int byte, int sw) {  // K-major, rows of sw bytes, 8-row atoms
@@ -878,17 +900,21 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   };
   {
     std::vector<uint8_t> b(static_cast<size_t>(nblk) * kSpBlockBytes, 0);
-    for (int blk = 0; blk < nblk; ++blk)
+    std::vector<uint8_t> e(static_cast<size_t>(nblk) * kEBlockBytes);
+    for (int pos = 0; pos < nblk; ++pos) {
+      const int blk = order[pos];
       for (int m = 0; m < 128; ++m)
         for (int k = 0; k < 32; ++k)
-          memcpy(&b[static_cast<size_t>(blk) * kSpBlockBytes + swz_off(m, 2 * k, 64)],
+          memcpy(&b[static_cast<size_t>(pos) * kSpBlockBytes + swz_off(m, 2 * k, 64)],
                  &as[(static_cast<size_t>(blk) * 128 + m) * 32 + k], 2);
+      memcpy(&e[static_cast<size_t>(pos) * kEBlockBytes], &ee[static_cast<size_t>(blk) * 128 * 4], kEBlockBytes);
+    }
     if ((st = upload(&h->w_as, b)) != LRS_OK) return st;
-    std::vector<uint8_t> e(ee.size() * 4);
-    memcpy(e.data(), ee.data(), e.size());
     if ((st = upload(&h->w_e, e)) != LRS_OK) return st;
-    std::vector<uint8_t> r(res_tab.size() * 4);
-    memcpy(r.data(), res_tab.data(), r.size());
+    // stream tables: [n_mt * n_ck + 1] chunk starts, then [nblk] tap offsets, one buffer
+    std::vector<uint8_t> r((stream_off.size() + blk_tap.size()) * 4);
+    memcpy(r.data(), stream_off.data(), stream_off.size() * 4);
+    memcpy(r.data() + stream_off.size() * 4, blk_tap.data(), blk_tap.size() * 4);
     void* rp_ = nullptr;
     if ((st = upload(&rp_, r)) != LRS_OK) return st;
     h->w_res = static_cast<int*>(rp_);
@@ -925,7 +951,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     if ((st = encode_t(&w.tmT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, src, dims, strides, box, estr, sw_t)) != LRS_OK)
       return st;
   }
-  w.res_block = h->w_res;
+  w.stream_off = h->w_res;
+  w.blk_tap = reinterpret_cast<const uint32_t*>(h->w_res + stream_off.size());
   w.ho = ho;
   w.wo = wo;
   w.cout = cout;
@@ -978,8 +1005,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   w.off_a = best_nwb * best_stride;
   w.off_e = w.off_a + best_ns * w.a_slot;
   w.off_epi = w.off_e + best_ns * w.e_slot;
-  w.off_res = w.off_epi + 8 * kEpiScratch;  // residual-block table of the tile's M-tile
-  w.off_bar = w.off_res + ((static_cast<uint32_t>(n_ck * taps) * 4u + 127u) & ~127u);
+  w.off_res = w.off_epi + 8 * kEpiScratch;  // block stream of the tile's M-tile
+  w.off_bar = w.off_res + ((static_cast<uint32_t>(n_ck + 1 + 2 * n_ck * taps) * 4u + 127u) & ~127u);
   h->w_smem = best_total;
   h->use_w = true;
   if (getenv("LRS_VERBOSE"))

@@ -74,7 +74,11 @@ struct WconvParams {
   const uint8_t* img_sp;     // compressed 2:4 blocks, SW64 image, 8 KB each
   const uint8_t* img_e;      // their metadata, [128 lanes][16 B], 2 KB each
   const uint8_t* img_dense;  // U_out^T (or V^T) blocks [n_mt][n_tk], 128 rows x sw_t B, swizzle sw_t
-  const int* res_block;  // [n_mt][n_ck][taps] residual block index or -1
+  // 2:4 blocks are stored in STREAM order -- per (M-tile, chunk): for each tap its main block,
+  // then its residual block if it has one -- so every item (bpi consecutive blocks of a
+  // window) is ONE bulk copy of A and one of E (2 requests instead of 2 per block)
+  const int* stream_off;     // [n_mt * n_ck + 1] first block of each (M-tile, chunk)
+  const uint32_t* blk_tap;   // [blocks] tap offset of each block: window position * 1024 >> 4
   void* y;
   int n, ho, wo, cout;
   int kh, kw, sh, sw, ph, pw;
@@ -195,16 +199,19 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       // ------------------------------------------------------------ TMA producer
       int it = 0, wg = 0, buf = 0;
       uint32_t wph = 0;
-      // the tile's residual-block table, staged in shared memory by independent
-      // (pipelined) loads at the tile start: a global load per tap on the issue
-      // path measured ~250 ns each (tools/wtrace.py producer stamps)
-      int* res_s = reinterpret_cast<int*>(smem + p.off_res);
-      const int nres = p.n_ck * taps;
-      int cur_mt = -1;
+      // the M-tile's block stream (chunk starts + per-block tap offsets), staged in shared
+      // memory by independent (pipelined) loads when the M-tile changes: a global load on
+      // the issue path measured ~250 ns each (tools/wtrace.py producer stamps)
+      int* so_s = reinterpret_cast<int*>(smem + p.off_res);   // [n_ck + 1], relative to mt0
+      uint32_t* tap_s = reinterpret_cast<uint32_t*>(so_s + p.n_ck + 1);
+      int cur_mt = -1, mt0 = 0;
       for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
         const TileCoord tc = tile_coord(p, tile);
         if (tc.mt != cur_mt) {
-          for (int i = 0; i < nres; ++i) res_s[i] = __ldg(p.res_block + tc.mt * nres + i);
+          mt0 = __ldg(p.stream_off + tc.mt * p.n_ck);
+          for (int i = 0; i <= p.n_ck; ++i) so_s[i] = __ldg(p.stream_off + tc.mt * p.n_ck + i) - mt0;
+          const int len = so_s[p.n_ck];
+          for (int i = 0; i < len; ++i) tap_s[i] = __ldg(p.blk_tap + mt0 + i);
           cur_mt = tc.mt;
         }
         for (int w = 0; w < nwin; ++w, ++wg) {
@@ -231,56 +238,34 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
               mbar_arrive_expect_tx(&win_full[buf], p.x_win_bytes);
               tma_load_4d(wdst, &p.tmX, &win_full[buf], c * 64, tc.n0, tc.wo0 * p.sw - p.pw, tc.ho0 * p.sh - p.ph);
             }
-            // sparse blocks of this window in (tap, main/residual) order, packed bpi per
-            // slot (one item): every item costs an mbarrier hand-off and a tcgen05.commit
-            // (~450 cycles, tools/mma_rate2.cu), so items are made as large as smem allows
-            const int key0 = (tc.mt * p.n_ck + c) * taps;
-            int pb[kWMaxBpi];
-            uint32_t pt[kWMaxBpi];
-            int np = 0;
-            for (int t = 0; t < taps; ++t) {
-              const int rblk = WDBG(p, 256) ? -1 : res_s[key0 - tc.mt * nres + t];
-              const int ty = t / p.kw, tx = t - ty * p.kw;
-              const uint32_t tap16 = static_cast<uint32_t>(ty * p.wc + tx) * 64u;  // (pos * 1024) >> 4
-              for (int part = 0; part < 2; ++part) {
-                const int blk = part == 0 ? key0 + t : rblk;
-                if (blk < 0) continue;
+            // this window's blocks in stream order, bpi per item: every item costs an
+            // mbarrier hand-off and a tcgen05.commit (~450 cycles, tools/mma_rate2.cu), so
+            // items are as large as smem allows; each is one bulk copy of A and one of E
+            const int sb = so_s[c], se = so_s[c + 1];
+            for (int b = sb; b < se; b += p.bpi) {
+              const int np = min(p.bpi, se - b);
+              const bool last = b + np >= se;
+              const int slot = it % p.ns;
+              if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it] = gtimer();
+              if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
+              if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it + 1] = gtimer();
 #pragma unroll
-                for (int q = 0; q < kWMaxBpi; ++q)
-                  if (q == np) { pb[q] = blk; pt[q] = tap16; }
-                ++np;
-                const bool last = t == taps - 1 && (part == 1 || rblk < 0);
-                if (np < p.bpi && !last) continue;
-                const int slot = it % p.ns;
-                if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it] = gtimer();
-                if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
-                if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it + 1] = gtimer();
-#pragma unroll
-                for (int q = 0; q < kWMaxBpi; ++q)
-                  if (q < np)
-                    st_shared_u32(slot_info + 4u * (kWMaxBpi * slot + q),
-                                  pt[q] | (q == 0 ? (static_cast<uint32_t>(np) << 28) | (last ? 0x80000000u : 0u)
-                                                  : 0u));
-                if (WDBG(p, 2)) {
-                  mbar_arrive(&a_full[slot]);
-                } else {
-                  mbar_arrive_expect_tx(&a_full[slot], static_cast<uint32_t>(np) * (kSpBlockBytes + kEBlockBytes));
-                  uint8_t* ad = smem + p.off_a + slot * p.a_slot;
-                  uint8_t* ed = smem + p.off_e + slot * p.e_slot;
-#pragma unroll
-                  for (int q = 0; q < kWMaxBpi; ++q) {
-                    if (q < np) {
-                      bulk_load(ad + q * kSpBlockBytes, p.img_sp + static_cast<size_t>(pb[q]) * kSpBlockBytes,
-                                kSpBlockBytes, &a_full[slot]);
-                      bulk_load(ed + q * kEBlockBytes, p.img_e + static_cast<size_t>(pb[q]) * kEBlockBytes,
-                                kEBlockBytes, &a_full[slot]);
-                    }
-                  }
-                }
-                if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it + 2] = gtimer();
-                ++it;
-                np = 0;
+              for (int q = 0; q < kWMaxBpi; ++q)
+                if (q < np)
+                  st_shared_u32(slot_info + 4u * (kWMaxBpi * slot + q),
+                                tap_s[b + q] | (q == 0 ? (static_cast<uint32_t>(np) << 28) | (last ? 0x80000000u : 0u)
+                                                       : 0u));
+              if (WDBG(p, 2)) {
+                mbar_arrive(&a_full[slot]);
+              } else {
+                mbar_arrive_expect_tx(&a_full[slot], static_cast<uint32_t>(np) * (kSpBlockBytes + kEBlockBytes));
+                bulk_load(smem + p.off_a + slot * p.a_slot, p.img_sp + static_cast<size_t>(mt0 + b) * kSpBlockBytes,
+                          static_cast<uint32_t>(np) * kSpBlockBytes, &a_full[slot]);
+                bulk_load(smem + p.off_e + slot * p.e_slot, p.img_e + static_cast<size_t>(mt0 + b) * kEBlockBytes,
+                          static_cast<uint32_t>(np) * kEBlockBytes, &a_full[slot]);
               }
+              if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it + 2] = gtimer();
+              ++it;
             }
           }
           if (++buf == p.nwb) { buf = 0; wph ^= 1u; }
