@@ -99,8 +99,8 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_launch_dependents();
-  pdl_wait();
+  pdl_wait();  // the previous kernel's output is visible from here on
+  pdl_launch_dependents();  // only after the wait: every kernel before us is then complete
 
   if (warp == 0) {
     if (lane == 0) {

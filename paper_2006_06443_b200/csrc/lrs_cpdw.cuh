@@ -38,8 +38,8 @@ struct CpDwParams {
 template <bool F32>
 __global__ void __launch_bounds__(kCpThreads) lrs_cp_dw_kernel(const __grid_constant__ CpDwParams p) {
   constexpr int V = F32 ? 4 : 8;  // channels per 16-byte vector
-  pdl_launch_dependents();
   pdl_wait();  // T1 comes from the projection kernel launched just before
+  pdl_launch_dependents();  // only after the wait: every kernel before us is then complete
   const int nvec = p.ld / V;
   const long long total = static_cast<long long>(p.n) * p.ho * p.wo * nvec;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;

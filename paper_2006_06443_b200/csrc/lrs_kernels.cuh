@@ -197,8 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1) lrs_gemm_kernel(const __grid_cons
   const uint32_t tmem = *tmem_slot;
   // PDL: the prologue above overlapped the previous kernel's tail; from here on
   // we read its outputs (and overwrite buffers it may read)
-  pdl_launch_dependents();
-  pdl_wait();
+  pdl_wait();  // the previous kernel's output is visible from here on
+  pdl_launch_dependents();  // only after the wait: every kernel before us is then complete
 
   if (warp == 0) {
     if (lane == 0) {

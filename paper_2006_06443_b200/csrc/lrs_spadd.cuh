@@ -64,8 +64,8 @@ __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_c
   const int jw = nc * 64 + warp * 8;  // first output channel of this warp
   // PDL: T2 is written by the core kernel launched just before (and X by
   // whatever ran before the chain); wait for both before touching either
-  pdl_launch_dependents();
-  pdl_wait();
+  pdl_wait();  // the previous kernel's output is visible from here on
+  pdl_launch_dependents();  // only after the wait: every kernel before us is then complete
 
   // window-relative base (in 16-byte vectors) of each of this lane's positions
   int base[kSpKP];

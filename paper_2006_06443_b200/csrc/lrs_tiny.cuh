@@ -65,8 +65,8 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
     ecs[i] = __ldg(p.ent_c + i);
     evs[i] = __ldg(p.ent_v + i);
   }
-  pdl_launch_dependents();
-  pdl_wait();
+  pdl_wait();  // the previous kernel's output is visible from here on
+  pdl_launch_dependents();  // only after the wait: every kernel before us is then complete
   // ---- X window [c][row][col] (zero padding), 4 channels per load, 4 loads in flight
   {
     const int nit = wrc * (p.cin / 4);

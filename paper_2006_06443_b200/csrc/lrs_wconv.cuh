@@ -190,9 +190,11 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     __trap();
   }
   constexpr uint32_t tmem = 0u;
-  // PDL: the prologue above overlapped the previous kernel's tail
-  pdl_launch_dependents();
-  pdl_wait();
+  // PDL: every kernel of this library triggers its dependents only after its own
+  // griddepcontrol.wait, so when this grid starts everything before the previous kernel
+  // is complete: X, the weights and Y may be touched at once.  Only T2 (T1 for the SVD
+  // pair) comes from the previous kernel -- each tile runs its sparse windows first and
+  // the producer waits just before the first T window, overlapping the previous kernel.
 
   if (warp == 0) {
     if (lane == 0) {
@@ -205,6 +207,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       int* so_s = reinterpret_cast<int*>(smem + p.off_res);   // [n_ck + 1], relative to mt0
       uint32_t* tap_s = reinterpret_cast<uint32_t*>(so_s + p.n_ck + 1);
       int cur_mt = -1, mt0 = 0;
+      bool waited = false;
       for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
         const TileCoord tc = tile_coord(p, tile);
         if (tc.mt != cur_mt) {
@@ -218,22 +221,28 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           if (wg >= p.nwb) mbar_wait(&win_empty[buf], wph ^ 1u);
           uint8_t* wdst = smem + buf * p.win_stride;
           if (WTRACE(p) && blockIdx.x == 0 && wg < 16) p.trace[3600 + wg] = gtimer();
+          const int tk = w - p.n_ck;  // >= 0: dense (T) window, after the tile's sparse ones
+          if (tk >= 0 && !waited) {
+            pdl_wait();
+            pdl_launch_dependents();
+            waited = true;
+          }
           if (WDBG(p, 64)) {
             mbar_arrive(&win_full[buf]);
-          } else if (w < p.n_tk) {
+          } else if (tk >= 0) {
             mbar_arrive_expect_tx(&win_full[buf], p.t_win_bytes);
-            tma_load_4d(wdst, &p.tmT, &win_full[buf], w * p.t_kc, tc.n0, tc.wo0, tc.ho0);
+            tma_load_4d(wdst, &p.tmT, &win_full[buf], tk * p.t_kc, tc.n0, tc.wo0, tc.ho0);
           }
-          if (w < p.n_tk) {
+          if (tk >= 0) {
             const int slot = it % p.ns;
             if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
             mbar_arrive_expect_tx(&a_full[slot], 128u * p.sw_t);
             bulk_load(smem + p.off_a + slot * p.a_slot,
-                      p.img_dense + (static_cast<size_t>(tc.mt) * p.n_tk + w) * (128u * p.sw_t), 128u * p.sw_t,
+                      p.img_dense + (static_cast<size_t>(tc.mt) * p.n_tk + tk) * (128u * p.sw_t), 128u * p.sw_t,
                       &a_full[slot]);
             ++it;
           } else {
-            const int c = w - p.n_tk;
+            const int c = w;
             if (!(WDBG(p, 64))) {
               mbar_arrive_expect_tx(&win_full[buf], p.x_win_bytes);
               tma_load_4d(wdst, &p.tmX, &win_full[buf], c * 64, tc.n0, tc.wo0 * p.sw - p.pw, tc.ho0 * p.sh - p.ph);
@@ -317,7 +326,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         tc_fence_after();
         if (WTRACE(p) && blockIdx.x == 0 && lane == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w + 1] = gtimer();
         const uint32_t boff = static_cast<uint32_t>(buf) * win16;
-        if (w < p.n_tk) {
+        if (w >= p.n_ck) {  // dense window: the accumulator already holds the sparse term
           mbar_wait(&a_full[slot], ph);
           tc_fence_after();
           const uint64_t ab = ad_dense + slot * slot_a16;
@@ -326,7 +335,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             for (int u = 0; u < NU; ++u) {
               {
                 for (int kk = 0; kk < ksteps; ++kk)
-                  mma_bf16(dcol[u] + acc0, ab + 2 * kk, btd[u] + boff + 2 * kk, idu[u], (w > 0 || kk > 0) ? 1u : 0u);
+                  mma_bf16(dcol[u] + acc0, ab + 2 * kk, btd[u] + boff + 2 * kk, idu[u], 1u);
               }
             }
             mma_commit(&a_empty[slot]);
@@ -335,7 +344,9 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           if (++slot == p.ns) { slot = 0; ph ^= 1u; }
         } else {
           // sparse items of this window: the producer tags each slot with the
-          // tap's window offset and whether it is the window's last item
+          // tap's window offset and whether it is the window's last item; the tile's
+          // very first MMA step of each unit starts the accumulator (accumulate = 0)
+          bool first = w == 0;
           while (true) {
             mbar_wait(&a_full[slot], ph);
             tc_fence_after();
@@ -364,7 +375,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                     for (int u = 0; u < NU; ++u) {
                       mma_sp_bf16(dcol[u] + acc0, ab + static_cast<uint32_t>(bi) * (kSpBlockBytes >> 4) + 2 * s2,
                                   bxd[u] + boff + tapv[bi] + 4 * s2, idu[u] | (1u << 2) | static_cast<uint32_t>(s2),
-                                  1u, ebi);
+                                  (first && bi == 0 && s2 == 0) ? 0u : 1u, ebi);
                     }
                   }
                 }
@@ -373,6 +384,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
               else mma_commit(&a_empty[slot]);
             }
             __syncwarp();
+            first = false;
             if (++slot == p.ns) { slot = 0; ph ^= 1u; }
             if (info0 >> 31) break;
           }
