@@ -58,7 +58,7 @@ namespace lrs {
 
 constexpr int kWThreads = 320;  // warps 0 producer, 1 MMA, 2..9 epilogue (2 per TMEM lane quarter)
 constexpr int kWMaxSlots = 6;
-constexpr int kWMaxWin = 4;  // window buffers in the ring
+constexpr int kWMaxWin = 8;  // window buffers in the ring
 constexpr int kWMaxUnits = 8;
 constexpr int kWMaxBpi = 4;              // sparse blocks per pipeline item
 constexpr uint32_t kSpBlockBytes = 8192;  // one compressed 2:4 block: 128 rows x 64 B
@@ -208,8 +208,21 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       uint32_t* tap_s = reinterpret_cast<uint32_t*>(so_s + p.n_ck + 1);
       int cur_mt = -1, mt0 = 0;
       bool waited = false;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+      // CTAs own contiguous tile ranges, M-tile fastest: consecutive tiles of a CTA share
+      // their windows; with one ring buffer per window (nwb == nwin) a window still resident
+      // from the previous tile is reused instead of re-loaded
+      const bool contig = p.nwb == nwin;
+      const int t_begin = contig ? static_cast<int>(static_cast<long long>(blockIdx.x) * p.n_tiles / gridDim.x)
+                                 : static_cast<int>(blockIdx.x);
+      const int t_end = contig ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * p.n_tiles / gridDim.x)
+                               : p.n_tiles;
+      const int t_step = contig ? 1 : static_cast<int>(gridDim.x);
+      int prev_win = -1;
+      for (int tile = t_begin; tile < t_end; tile += t_step) {
         const TileCoord tc = tile_coord(p, tile);
+        const int win_key = tile / p.n_mt;
+        const bool reuse = p.nwb == nwin && win_key == prev_win;
+        prev_win = win_key;
         if (tc.mt != cur_mt) {
           mt0 = __ldg(p.stream_off + tc.mt * p.n_ck);
           for (int i = 0; i <= p.n_ck; ++i) so_s[i] = __ldg(p.stream_off + tc.mt * p.n_ck + i) - mt0;
@@ -227,8 +240,8 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             pdl_launch_dependents();
             waited = true;
           }
-          if (WDBG(p, 64)) {
-            mbar_arrive(&win_full[buf]);
+          if (WDBG(p, 64) || reuse) {
+            mbar_arrive(&win_full[buf]);  // window already resident (or timing experiment)
           } else if (tk >= 0) {
             mbar_arrive_expect_tx(&win_full[buf], p.t_win_bytes);
             tma_load_4d(wdst, &p.tmT, &win_full[buf], tk * p.t_kc, tc.n0, tc.wo0, tc.ho0);
@@ -243,7 +256,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             ++it;
           } else {
             const int c = w;
-            if (!(WDBG(p, 64))) {
+            if (!(WDBG(p, 64)) && !reuse) {
               mbar_arrive_expect_tx(&win_full[buf], p.x_win_bytes);
               tma_load_4d(wdst, &p.tmX, &win_full[buf], c * 64, tc.n0, tc.wo0 * p.sw - p.pw, tc.ho0 * p.sh - p.ph);
             }
@@ -310,7 +323,13 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const int ksteps = static_cast<int>(p.sw_t / 32);
     int slot = 0, k = 0, buf = 0;
     uint32_t ph = 0, wph = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++k) {
+    const bool contig = p.nwb == nwin;  // must match the producer's tile order
+    const int t_begin = contig ? static_cast<int>(static_cast<long long>(blockIdx.x) * p.n_tiles / gridDim.x)
+                               : static_cast<int>(blockIdx.x);
+    const int t_end = contig ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * p.n_tiles / gridDim.x)
+                             : p.n_tiles;
+    const int t_step = contig ? 1 : static_cast<int>(gridDim.x);
+    for (int tile = t_begin; tile < t_end; tile += t_step, ++k) {
       const TileCoord tc = tile_coord(p, tile);
       const int b = p.nacc == 2 ? (k & 1) : 0;
       const int use = p.nacc == 2 ? (k >> 1) : k;  // previous uses of accumulator b
@@ -404,7 +423,13 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const uint32_t scr = smem_u32(smem + p.off_epi) + static_cast<uint32_t>(warp - 2) * kEpiScratch;
     __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(p.y);
     int k = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++k) {
+    const bool contig = p.nwb == nwin;  // must match the producer's tile order
+    const int t_begin = contig ? static_cast<int>(static_cast<long long>(blockIdx.x) * p.n_tiles / gridDim.x)
+                               : static_cast<int>(blockIdx.x);
+    const int t_end = contig ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * p.n_tiles / gridDim.x)
+                             : p.n_tiles;
+    const int t_step = contig ? 1 : static_cast<int>(gridDim.x);
+    for (int tile = t_begin; tile < t_end; tile += t_step, ++k) {
       const TileCoord tc = tile_coord(p, tile);
       const int b = p.nacc == 2 ? (k & 1) : 0;
       const int use = p.nacc == 2 ? (k >> 1) : k;
