@@ -726,6 +726,15 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   int best_th = 0, best_ns = 0, best_tc = 0, best_wc = 0, best_tbw = 0, best_nwb = 2, best_bpi = 2;
   long long best_cost = 1LL << 60;
   uint32_t best_stride = 0, best_xw = 0, best_tw = 0, best_total = 0, best_acc = 0;
+  // chunks per X window: several 64-channel boxes in one window buffer share one
+  // pipeline hand-off (the per-window round trip dominated C4's timeline); the largest
+  // that fits wins
+  int best_cpw = 1;
+  const int cpw_env = getenv("LRS_WCONV_CPW") ? atoi(getenv("LRS_WCONV_CPW")) : 0;
+  // ("largest that fits" shrank the tiles and lost badly at C2/C3, so only 1x1 layers --
+  // no halo, small windows -- take cpw > 1; C4: 49.0 -> 47.0 us)
+  for (int cpw = 8; cpw >= 1 && !best_th; cpw /= 2) {
+  if (n_ck % cpw || (cpw_env ? cpw != cpw_env : (taps > 1 && cpw != 1))) continue;
   for (int cb = 1; cb <= 16 && !best_th; ++cb) {  // column bands: as few as fit
     const int tc = (wo + cb - 1) / cb;
     if (cb > 1 && (wo + tc - 1) / tc != cb) continue;
@@ -757,7 +766,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         const uint32_t a_slot = static_cast<uint32_t>(bpi) * kSpBlockBytes;  // >= 16 KB dense box
         const uint32_t e_slot = static_cast<uint32_t>(bpi) * kEBlockBytes;
         if (acc + 4 * bpi * ns > 512) continue;
-        const uint32_t xw = static_cast<uint32_t>(wr) * wcw * 1024u;
+        const uint32_t xw = static_cast<uint32_t>(wr) * wcw * 1024u;  // one chunk's box
         const uint32_t tw = static_cast<uint32_t>(th) * tbw * 8u * sw_t;
         // slack: positions read past the end of a window by the last (padded) MMA rows
         long long last_x = 0, last_t = 0;
@@ -766,7 +775,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
                                                    static_cast<long long>(u.n / 8 - 1) * g.sw);
           last_t = std::max<long long>(last_t, u.tpos + u.n / 8 - 1);
         }
-        const long long slack_x = std::max(0LL, last_x + 1 - static_cast<long long>(wr) * wcw) * 1024;
+        const long long slack_x = std::max(0LL, last_x + 1 - static_cast<long long>(wr) * wcw) * 1024 +
+                                  static_cast<long long>(cpw - 1) * xw;  // the window's other boxes
         const long long slack_t = std::max(0LL, last_t + 1 - static_cast<long long>(th) * tbw) * 8 * sw_t;
         const uint32_t stride =
             align1024(static_cast<uint32_t>(std::max<long long>(xw + slack_x, tw + slack_t)));
@@ -812,6 +822,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
           best_bpi = bpi;
           best_acc = static_cast<uint32_t>(acc);
           best_units = units;
+          best_cpw = cpw;
         }
         found = true;
         break;
@@ -820,7 +831,9 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       }  // pass
     }
   }
+  }  // cpw
   if (!best_th) return LRS_OK;
+  const int cpw = best_cpw;
   const int th = best_th;
   const int wc = best_wc, tbox_w = best_tbw, tcols = best_tc;
 
@@ -899,7 +912,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       stream_off[static_cast<size_t>(mt) * n_ck + c] = static_cast<int>(order.size());
       for (int t = 0; t < taps; ++t) {
         const int key = (mt * n_ck + c) * taps + t;
-        const uint32_t tap16 = static_cast<uint32_t>((t / kw) * wc + (t % kw)) * 64u;  // (pos * 1024) >> 4
+        const uint32_t tap16 = static_cast<uint32_t>((t / kw) * wc + (t % kw)) * 64u +  // (pos * 1024) >> 4
+                               static_cast<uint32_t>(c % cpw) * (best_xw >> 4);          // the chunk's box
         order.push_back(key);
         blk_tap.push_back(tap16);
         if (res_tab[key] >= 0) {
@@ -1000,6 +1014,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   }
   w.tbox_w = tbox_w;
   w.n_ck = n_ck;
+  w.cpw = cpw;
+  w.n_xw = n_ck / cpw;
   w.n_tk = n_tk;
   w.t_kc = t_kc;
   w.sw_t = sw_t;
@@ -1027,8 +1043,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   h->w_smem = best_total;
   h->use_w = true;
   if (getenv("LRS_VERBOSE"))
-    fprintf(stderr, "lrs_wconv plan: th %d tcols %d units %d acc %u nacc %d ns %d bpi %d nwb %d win %u B smem %u B tiles/img-group %d\n",
-            th, tcols, w.n_units, acc, w.nacc, w.ns, w.bpi, w.nwb, best_stride, best_total, w.bands * w.cbands * w.n_mt);
+    fprintf(stderr, "lrs_wconv plan: th %d tcols %d units %d acc %u nacc %d ns %d bpi %d nwb %d cpw %d win %u B smem %u B tiles/img-group %d\n",
+            th, tcols, w.n_units, acc, w.nacc, w.ns, w.bpi, w.nwb, cpw, best_stride, best_total, w.bands * w.cbands * w.n_mt);
   return LRS_OK;
 }
 }  // namespace

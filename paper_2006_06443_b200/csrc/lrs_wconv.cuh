@@ -100,6 +100,7 @@ struct WconvParams {
   unsigned long long* trace;  // optional: globaltimer stamps (debug, lrs_conv_debug_trace)
   int dbg;                 // debug experiment bits (0 in production)
   int n_ck, n_tk, t_kc;
+  int cpw, n_xw;        // 64-channel chunks per X window (boxes x_win_bytes apart), X windows per tile
   uint32_t sw_t;        // bytes per T window row (t_kc * 2) = its swizzle width
   int wr, wc;
   uint32_t x_win_bytes, t_win_bytes, win_stride;
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
 
   if (WTRACE(p) && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
   const int taps = p.kh * p.kw;
-  const int nwin = p.n_tk + p.n_ck;
+  const int nwin = p.n_tk + p.n_xw;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.nwb; ++i) {
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           if (wg >= p.nwb) mbar_wait(&win_empty[buf], wph ^ 1u);
           uint8_t* wdst = smem + buf * p.win_stride;
           if (WTRACE(p) && blockIdx.x == 0 && wg < 16) p.trace[3600 + wg] = gtimer();
-          const int tk = w - p.n_ck;  // >= 0: dense (T) window, after the tile's sparse ones
+          const int tk = w - p.n_xw;  // >= 0: dense (T) window, after the tile's sparse ones
           if (tk >= 0 && !waited) {
             pdl_wait();
             pdl_launch_dependents();
@@ -255,15 +256,17 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                       &a_full[slot]);
             ++it;
           } else {
-            const int c = w;
+            const int c = w * p.cpw;  // first chunk of this window
             if (!(WDBG(p, 64)) && !reuse) {
-              mbar_arrive_expect_tx(&win_full[buf], p.x_win_bytes);
-              tma_load_4d(wdst, &p.tmX, &win_full[buf], c * 64, tc.n0, tc.wo0 * p.sw - p.pw, tc.ho0 * p.sh - p.ph);
+              mbar_arrive_expect_tx(&win_full[buf], static_cast<uint32_t>(p.cpw) * p.x_win_bytes);
+              for (int q = 0; q < p.cpw; ++q)
+                tma_load_4d(wdst + q * p.x_win_bytes, &p.tmX, &win_full[buf], (c + q) * 64, tc.n0,
+                            tc.wo0 * p.sw - p.pw, tc.ho0 * p.sh - p.ph);
             }
             // this window's blocks in stream order, bpi per item: every item costs an
             // mbarrier hand-off and a tcgen05.commit (~450 cycles, tools/mma_rate2.cu), so
             // items are as large as smem allows; each is one bulk copy of A and one of E
-            const int sb = so_s[c], se = so_s[c + 1];
+            const int sb = so_s[c], se = so_s[c + p.cpw];
             for (int b = sb; b < se; b += p.bpi) {
               const int np = min(p.bpi, se - b);
               const bool last = b + np >= se;
@@ -345,7 +348,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         tc_fence_after();
         if (WTRACE(p) && blockIdx.x == 0 && lane == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w + 1] = gtimer();
         const uint32_t boff = static_cast<uint32_t>(buf) * win16;
-        if (w >= p.n_ck) {  // dense window: the accumulator already holds the sparse term
+        if (w >= p.n_xw) {  // dense window: the accumulator already holds the sparse term
           mbar_wait(&a_full[slot], ph);
           tc_fence_after();
           const uint64_t ab = ad_dense + slot * slot_a16;
