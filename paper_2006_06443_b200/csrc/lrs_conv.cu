@@ -1015,7 +1015,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   w.tbox_w = tbox_w;
   w.n_ck = n_ck;
   w.cpw = cpw;
-  w.n_xw = n_ck / cpw;
+  w.n_xw = d->nnz > 0 ? n_ck / cpw : 0;  // an empty S needs no X windows at all (LR-only layers)
   w.n_tk = n_tk;
   w.t_kc = t_kc;
   w.sw_t = sw_t;

@@ -357,7 +357,8 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             for (int u = 0; u < NU; ++u) {
               {
                 for (int kk = 0; kk < ksteps; ++kk)
-                  mma_bf16(dcol[u] + acc0, ab + 2 * kk, btd[u] + boff + 2 * kk, idu[u], 1u);
+                  mma_bf16(dcol[u] + acc0, ab + 2 * kk, btd[u] + boff + 2 * kk, idu[u],
+                           (p.n_xw > 0 || w > 0 || kk > 0) ? 1u : 0u);  // S empty: dense starts the sum
               }
             }
             mma_commit(&a_empty[slot]);

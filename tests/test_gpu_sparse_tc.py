@@ -59,6 +59,8 @@ GEOMS = [  # (n, h, w, cin, cout, k, s, p, r1, r2, density, svd)  -- all bf16, c
     (8, 10, 10, 64, 128, 3, 1, 0, 32, 32, 0.02, False),     # pad 0
     (4, 28, 28, 128, 128, 3, 2, 1, 32, 32, 0.02, False),    # stride 2, 28 -> 14
     (3, 7, 7, 128, 128, 3, 1, 1, 32, 32, 0.30, False),      # dense-ish S: most groups need a residual block
+    (4, 14, 14, 64, 128, 3, 1, 1, 32, 32, 0.0, False),      # empty S: no X windows, the dense MMAs start the sum
+    (3, 9, 9, 128, 192, 1, 1, 0, 16, 16, 0.0, True),        # empty S, SVD pair
 ]
 
 
