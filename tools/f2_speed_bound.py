@@ -140,8 +140,10 @@ def main():
            "paper_cpu_x1": {"1.5": 1.08, "2": 1.2, "3": 1.39, "5": 1.66, "10": 2.03, "20": 2.33},
            "note": "network speedup = sum of cuDNN dense conv times / sum of compressed-layer times over the "
                    "52 layers (stem excluded); paper_cpu_x1 = PAPER.md:250-266 (i3-8130U CPU), context only"}
-    with open(os.path.join(ROOT, "profiles", "r01_f2_speed_bound.json"), "w") as f:
-        json.dump(out, f, indent=1)
+    for d in ("profiles", "gpurun_out"):  # gpurun_out/ travels back from the GPU box
+        if os.path.isdir(os.path.join(ROOT, d)):
+            with open(os.path.join(ROOT, d, "r01_f2_speed_bound.json"), "w") as f:
+                json.dump(out, f, indent=1)
     print("\nnetwork-level speedup of the low-rank layers vs cuDNN dense (paper CPU x1 for context):")
     print("compression | " + " | ".join(f"x{s} input" for s in SCALES) + " | paper CPU x1")
     for c in COMPRESSIONS:
