@@ -735,7 +735,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   // no halo, small windows -- take cpw > 1; C4: 49.0 -> 47.0 us)
   for (int cpw = 8; cpw >= 1 && !best_th; cpw /= 2) {
   if (n_ck % cpw || (cpw_env ? cpw != cpw_env : (taps > 1 && cpw != 1))) continue;
-  for (int cb = 1; cb <= 16 && !best_th; ++cb) {  // column bands: as few as fit
+  const int cb_env = getenv("LRS_WCONV_CB") ? atoi(getenv("LRS_WCONV_CB")) : 0;  // planner experiments
+  for (int cb = cb_env ? cb_env : 1; cb <= 16 && !best_th; ++cb) {  // column bands: as few as fit
     const int tc = (wo + cb - 1) / cb;
     if (cb > 1 && (wo + tc - 1) / tc != cb) continue;
     const int wcw = (tc - 1) * g.sw + kw;

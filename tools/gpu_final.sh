@@ -18,3 +18,5 @@ for c in c2_f32:spadd c1:tiny c2_bf16:core_kernel c4:wconv c3:wconv; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o gpurun_out/prof_${k}_$cfg -f python tools/gpu_debug.py $cfg > gpurun_out/ncu_${k}_$cfg.log 2>&1; echo "ncu $k $cfg rc=$?" >> gpurun_out/rcf.txt
 done
 cat gpurun_out/rcf.txt
+timeout 1500 python tools/f2_speed_bound.py > gpurun_out/f2.log 2>&1; echo "f2 rc=$?" >> gpurun_out/rcf.txt
+cat gpurun_out/rcf.txt
