@@ -115,11 +115,14 @@ lrs_status lrs_conv_forward(const lrs_conv *h, const void *x, void *y, int32_t n
 
 /*
  * End-to-end variant with HOST buffers: copies x_host -> device, runs
- * lrs_conv_forward, copies the result -> y_host, all enqueued on `stream`
- * (pinned host memory makes the copies asynchronous).  The device staging
- * buffers are allocated by the first call (so this call is not graph
- * capturable) and owned by the handle.  The caller synchronises `stream`
- * before reading y_host.
+ * lrs_conv_forward, copies the result -> y_host.  The batch is pipelined in up
+ * to 4 chunks of >= 8 images on two handle-owned copy streams (chunk i+1 in,
+ * chunk i computed, chunk i-1 out); the copies start after the caller's prior
+ * work on `stream`, and `stream` is made to wait for the last copy out, so the
+ * call behaves as if everything ran on `stream` (pinned host memory makes the
+ * copies asynchronous).  The device staging buffers, streams and events are
+ * created by the first call (so this call is not graph capturable) and owned
+ * by the handle.  The caller synchronises `stream` before reading y_host.
  */
 lrs_status lrs_conv_forward_host(lrs_conv *h, const void *x_host, void *y_host, int32_t n,
                                  void *stream);

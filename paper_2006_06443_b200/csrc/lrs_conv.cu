@@ -175,9 +175,11 @@ struct lrs_conv {
   const void* xmap_ptr = nullptr;
   int xmap_n = -1;
   CUtensorMap xmap{};
-  // host-io staging
+  // host-io staging (lrs_conv_forward_host): device buffers, copy streams, chunk events
   void* hx = nullptr;
   void* hy = nullptr;
+  cudaStream_t hs_in = nullptr, hs_out = nullptr;
+  cudaEvent_t hev[18] = {};  // [0..7] H2D done, [8..15] forward done, [16] start, [17] D2H done
   // timing
   bool timing = false;
   int skip = 0;  // timing experiments only (LRS_SKIP at create): 1 a1, 2 a2, 4 a3/fused, 8 a4 split
@@ -1538,17 +1540,44 @@ lrs_status lrs_conv_forward_host(lrs_conv* h, const void* x_host, void* y_host, 
   int prev = 0;
   LRS_CUDA(cudaGetDevice(&prev));
   if (prev != h->device) LRS_CUDA(cudaSetDevice(h->device));
-  const size_t xb = static_cast<size_t>(h->d.batch_max) * h->d.in_h * h->d.in_w * h->d.c_in * h->esz;
-  const size_t yb = static_cast<size_t>(h->d.batch_max) * h->ho * h->wo * h->d.c_out * h->esz;
-  if (!h->hx) LRS_CUDA(cudaMalloc(&h->hx, xb));
-  if (!h->hy) LRS_CUDA(cudaMalloc(&h->hy, yb));
+  const size_t xi = static_cast<size_t>(h->d.in_h) * h->d.in_w * h->d.c_in * h->esz;  // bytes per image
+  const size_t yi = static_cast<size_t>(h->ho) * h->wo * h->d.c_out * h->esz;
+  if (!h->hx) LRS_CUDA(cudaMalloc(&h->hx, xi * h->d.batch_max));
+  if (!h->hy) LRS_CUDA(cudaMalloc(&h->hy, yi * h->d.batch_max));
+  if (!h->hs_in) {
+    LRS_CUDA(cudaStreamCreateWithFlags(&h->hs_in, cudaStreamNonBlocking));
+    LRS_CUDA(cudaStreamCreateWithFlags(&h->hs_out, cudaStreamNonBlocking));
+    for (auto& e : h->hev) LRS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  const size_t xn = static_cast<size_t>(n) * h->d.in_h * h->d.in_w * h->d.c_in * h->esz;
-  const size_t yn = static_cast<size_t>(n) * h->ho * h->wo * h->d.c_out * h->esz;
-  LRS_CUDA(cudaMemcpyAsync(h->hx, x_host, xn, cudaMemcpyHostToDevice, stream));
-  lrs_status st = lrs_conv_forward(h, h->hx, h->hy, n, stream_);
-  if (st != LRS_OK) return st;
-  LRS_CUDA(cudaMemcpyAsync(y_host, h->hy, yn, cudaMemcpyDeviceToHost, stream));
+  // Pipeline in chunks of >= 8 images (the fused kernel's image groups): the copy of
+  // chunk i+1 in, the forward of chunk i and the copy of chunk i-1 out overlap (the copy
+  // engines run both directions concurrently).  Every stream starts after the caller's
+  // prior work on `stream`, and `stream` ends after the last copy out, so the call keeps
+  // single-stream semantics.
+  const int nch = std::max(1, std::min(4, n / 8));
+  const uint8_t* xs = static_cast<const uint8_t*>(x_host);
+  uint8_t* ys = static_cast<uint8_t*>(y_host);
+  uint8_t* dx = static_cast<uint8_t*>(h->hx);
+  uint8_t* dy = static_cast<uint8_t*>(h->hy);
+  LRS_CUDA(cudaEventRecord(h->hev[16], stream));
+  LRS_CUDA(cudaStreamWaitEvent(h->hs_in, h->hev[16], 0));
+  LRS_CUDA(cudaStreamWaitEvent(h->hs_out, h->hev[16], 0));
+  for (int i = 0; i < nch; ++i) {
+    const int i0 = static_cast<int>(static_cast<long long>(n) * i / nch) / 8 * 8;
+    const int i1 = i + 1 == nch ? n : static_cast<int>(static_cast<long long>(n) * (i + 1) / nch) / 8 * 8;
+    if (i1 <= i0) continue;
+    LRS_CUDA(cudaMemcpyAsync(dx + i0 * xi, xs + i0 * xi, (i1 - i0) * xi, cudaMemcpyHostToDevice, h->hs_in));
+    LRS_CUDA(cudaEventRecord(h->hev[i], h->hs_in));
+    LRS_CUDA(cudaStreamWaitEvent(stream, h->hev[i], 0));
+    lrs_status st = lrs_conv_forward(h, dx + i0 * xi, dy + i0 * yi, i1 - i0, stream_);
+    if (st != LRS_OK) return st;
+    LRS_CUDA(cudaEventRecord(h->hev[8 + i], stream));
+    LRS_CUDA(cudaStreamWaitEvent(h->hs_out, h->hev[8 + i], 0));
+    LRS_CUDA(cudaMemcpyAsync(ys + i0 * yi, dy + i0 * yi, (i1 - i0) * yi, cudaMemcpyDeviceToHost, h->hs_out));
+  }
+  LRS_CUDA(cudaEventRecord(h->hev[17], h->hs_out));
+  LRS_CUDA(cudaStreamWaitEvent(stream, h->hev[17], 0));
   if (prev != h->device) cudaSetDevice(prev);
   return LRS_OK;
 }
@@ -1565,6 +1594,13 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
     if (b) cudaFree(b);
   for (void* b : h->tiny_buf)
     if (b) cudaFree(b);
+  if (h->hs_in) {
+    cudaStreamSynchronize(h->hs_in);
+    cudaStreamSynchronize(h->hs_out);
+    cudaStreamDestroy(h->hs_in);
+    cudaStreamDestroy(h->hs_out);
+    for (auto e : h->hev) cudaEventDestroy(e);
+  }
   for (auto& r : h->ring)
     for (auto e : r.ev) cudaEventDestroy(e);
   cudaSetDevice(prev);

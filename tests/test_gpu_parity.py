@@ -193,3 +193,20 @@ def test_host_io_and_graph_capture():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(y2, y)
+
+
+@pytest.mark.parametrize("name,batch", [("c2_bf16", 64), ("c2_bf16", 37), ("c2_f32", 20), ("c3", 24)])
+def test_host_io_pipelined_chunks_bitwise(name, batch):
+    """lrs_conv_forward_host splits the batch into up to 4 chunks of >= 8 images
+    (copy in / compute / copy out overlapped on two handle streams); the result is
+    bitwise the device forward's, on a non-default caller stream, twice in a row."""
+    inp = workloads.generate(workloads.CONFIGS[name], batch=batch)
+    layer, x, y = run(inp)
+    xh = x.cpu().pin_memory()
+    s = torch.cuda.Stream()
+    for _ in range(2):
+        yh = torch.full(y.shape, -7.0, dtype=y.dtype).pin_memory()
+        with torch.cuda.stream(s):
+            layer.forward_host(xh, yh, stream=s)
+        s.synchronize()
+        assert torch.equal(yh, y.cpu())
