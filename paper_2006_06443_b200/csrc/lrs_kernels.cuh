@@ -256,17 +256,20 @@ __global__ void __launch_bounds__(kThreads, 1) lrs_gemm_kernel(const __grid_cons
       }
       mma_commit(tmem_full);
     }
-  } else if (warp < 4) {
+  } else {
     if constexpr (F32) {
       // ------------------------------------------------------------ tf32 hi/lo split
+      // warps 2..11: the epilogue warps join the split (they are idle until the
+      // accumulator is complete) -- with 2 warps the split was the mainloop's bottleneck
       const int t = threadIdx.x - 64;
+      constexpr int nt = kThreads - 64;
       const int n16 = static_cast<int>((kTileM * p.sw_bytes) / 16);
       for (int it = 0; it < p.num_k_iters; ++it) {
         const int s = it % S;
         mbar_wait(&full[s], (it / S) & 1);
         uint4* a = reinterpret_cast<uint4*>(a_region + s * p.a_stage_stride);
         uint4* alo = reinterpret_cast<uint4*>(alo_region + s * p.a_stage_stride);
-        for (int i = t; i < n16; i += 64) {
+        for (int i = t; i < n16; i += nt) {
           uint4 v = a[i];
           uint4 hi, lo;
           hi.x = v.x & 0xFFFFE000u; hi.y = v.y & 0xFFFFE000u;
@@ -279,11 +282,12 @@ __global__ void __launch_bounds__(kThreads, 1) lrs_gemm_kernel(const __grid_cons
           alo[i] = lo;
         }
         fence_proxy_async_smem();
-        named_bar_sync(1, 64);
+        named_bar_sync(1, nt);
         if (t == 0) mbar_arrive(&ready[s]);
       }
     }
-  } else {
+  }
+  if (warp >= 4) {
     const int e = warp - 4;      // 0..7
     const int q = warp & 3;      // TMEM lane quarter this warp may access
     if constexpr (EPI == EPI_STORE) {
