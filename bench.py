@@ -495,29 +495,40 @@ def main():
     dom = max(avg, key=lambda k: avg[k])
     t_dom = avg[dom] / 1e3
     fma_peak = RL.fp32_fma_tflops(peaks["sm_max_mhz"])
+    tc_peak = peaks["bf16_tflops"] * (1.0 if cfg.dtype == "bf16" else 0.5 / 3.0)  # fp32: 3xTF32 at TF32 = bf16/2
+    eng = layer.sparse_engine[0]
+    wk = work[dom]
+    # the dominant kernel's algorithmic work per pipe: HBM bytes, FP32-pipe flops (the
+    # sparse term -- SURVEY §8d three-roof -- plus whatever the kernel computes on the
+    # CUDA cores), tensor-pipe flops; its roofline bound is the pipe with the largest
+    # roof time, frac = that roof time / the measured kernel time
     if dom in ("a345_expand_sparse", "a4_sparse_add"):
-        wk = work[dom]
-        achieved = wk["flops_sparse"] / t_dom / 1e12
-        eng = layer.sparse_engine[0]
-        roof = {"bound": "alu", "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s",
-                "frac": achieved / fma_peak, "traffic": None, "kernel": dom,
-                "work": "sparse in-bounds MACs x 2 per launch (the sparse term's algorithmic work)",
-                "engine": {1: "2:4 sparse tensor cores (tcgen05.mma.sp), fused with the expansion GEMM",
-                           2: "SIMT CSR gather over 4-image shared-memory windows, added into Y after a3"}.get(
-                               eng, "SIMT CSR gather fused into the expansion GEMM epilogue"),
-                "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (the sparse term's "
-                               "CUDA-core roof, SURVEY §8d three-roof)"}
+        if eng == 3:  # the one-kernel fp32 path: the whole layer on the CUDA cores
+            lay = work["layer"]
+            b_alg, f_fma, f_tc = lay["bytes"], lay["flops_chain"] + lay["flops_sparse"], 0.0
+        elif eng == 2:  # expansion + sparse term on the CUDA cores
+            b_alg, f_fma, f_tc = wk["bytes"], wk["flops_sparse"] + wk["flops_tc"], 0.0
+        else:  # tensor-core expansion (+ 2:4 tensor-core or SIMT sparse term)
+            b_alg, f_fma, f_tc = wk["bytes"], wk["flops_sparse"], wk["flops_tc"]
     else:
-        wk = work[dom]
-        tc = peaks["bf16_tflops"] * (1.0 if cfg.dtype == "bf16" else 0.5 / 3.0)
-        if wk["bytes"] / (peaks["hbm_gbs"] * 1e9) >= wk["flops"] / (tc * 1e12):
-            achieved = wk["bytes"] / t_dom / 1e9
-            roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dom}
-        else:
-            achieved = wk["flops"] / t_dom / 1e12
-            roof = {"bound": "tensor", "achieved": achieved, "peak": tc, "unit": "TFLOP/s",
-                    "frac": achieved / tc, "traffic": None, "kernel": dom}
+        b_alg, f_fma, f_tc = wk["bytes"], 0.0, wk["flops"]
+    roofs_k = {"hbm": (b_alg / (peaks["hbm_gbs"] * 1e9), b_alg / t_dom / 1e9, peaks["hbm_gbs"], "GB/s"),
+               "alu": (f_fma / (fma_peak * 1e12), f_fma / t_dom / 1e12, fma_peak, "TFLOP/s"),
+               "tensor": (f_tc / (tc_peak * 1e12), f_tc / t_dom / 1e12, tc_peak, "TFLOP/s")}
+    bound = max(roofs_k, key=lambda k: roofs_k[k][0])
+    t_roof, achieved, peak, unit = roofs_k[bound]
+    roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+            "traffic": None, "kernel": dom,
+            "work": {"bytes": b_alg, "fp32_pipe_flops": f_fma, "tensor_flops": f_tc,
+                     "roof_us": {k: v[0] * 1e6 for k, v in roofs_k.items()}, "kernel_us": t_dom * 1e6},
+            "engine": {0: "SIMT CSR gather fused into the expansion GEMM epilogue",
+                       1: "2:4 sparse tensor cores (tcgen05.mma.sp), fused with the expansion GEMM",
+                       2: "SIMT expansion + CSR gather over 4-image shared-memory windows, Y written once",
+                       3: "the whole fp32 layer in one SIMT kernel"}.get(eng, "?"),
+            "peak_source": {"hbm": "MEASURED_PEAKS.json hbm_gbs",
+                            "alu": "derived: 148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (SURVEY §8d three-roof)",
+                            "tensor": "MEASURED_PEAKS.json bf16_tflops" + (" x 1/6 (3xTF32)" if cfg.dtype != "bf16"
+                                                                          else "")}[bound]}
     roof["peak_kind"] = peaks["source"]
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
     # (tools/ncu_traffic.py -> profiles/ncu_traffic.json); per launch, cold cache

@@ -72,7 +72,8 @@ def layer_work(cfg, n: int, col_idx: np.ndarray, cp: bool = False) -> Dict[str, 
     st = {
         "a1_proj": {"bytes": x_b + t1_b + cfg.c_in * r1 * esz, "flops": 2.0 * p_in * cfg.c_in * r1},
         "a345_expand_sparse": {
-            "bytes": (t2_b if not cfg.svd else t1_b) + y_b + r2 * cfg.c_out * esz + nnz * 8 + (cfg.c_out + 1) * 4,
+            # the fused kernel reads X (sparse term), T2 (T1 for the SVD pair), the weights, writes Y
+            "bytes": x_b + (t2_b if not cfg.svd else t1_b) + y_b + r2 * cfg.c_out * esz + nnz * 8 + (cfg.c_out + 1) * 4,
             "flops_tc": 2.0 * p * r2 * cfg.c_out, "flops_sparse": 2.0 * macs_s, "sparse_macs": macs_s},
     }
     st["a345_expand_sparse"]["flops"] = st["a345_expand_sparse"]["flops_tc"] + st["a345_expand_sparse"]["flops_sparse"]
