@@ -79,6 +79,12 @@ typedef struct lrs_conv_desc {
                                      at create (reading #12)               */
   lrs_core_kind core_kind;        /* LRS_CORE_TUCKER2 (0, the zero-initialised default)
                                      or LRS_CORE_CP; ignored when core == NULL        */
+  /* Optional fused output epilogue (e.g. an inference BatchNorm + ReLU
+     that follows the layer in a network): Y[..., j] = act(s_j * conv_j + b_j), applied
+     in fp32 to the accumulator before the single store of Y.  All zero = identity.   */
+  const float *out_scale;         /* host [c_out] or NULL (s = 1)                    */
+  const float *out_bias;          /* host [c_out] or NULL (b = 0)                    */
+  int32_t out_relu;               /* 1: act = max(., 0); 0: act = identity           */
 } lrs_conv_desc;
 
 /*

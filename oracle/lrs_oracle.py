@@ -28,6 +28,7 @@ __all__ = [
     "out_size", "conv_direct", "reconstruct_tucker2", "reconstruct_cp",
     "densify_sparse", "forward_dense", "conv_1x1", "sparse_conv_scatter",
     "forward_factored", "cp_conv", "forward_cp", "brute_force_conv", "param_counts", "cp_param_count",
+    "output_epilogue",
     "pack_sparse_slices", "unpack_sparse_slices", "sparse_mac_count",
 ]
 
@@ -231,6 +232,18 @@ def forward_cp(x, a, b, c, d, row_ptr, col_idx, values, stride: int = 1, pad: in
         y_l = conv_direct(x, reconstruct_cp(a, b, c, d), stride, pad)
     d = np.asarray(d)
     return y_l + sparse_conv_scatter(x, d.shape[0], k, row_ptr, col_idx, values, stride, pad)
+
+
+def output_epilogue(y, scale=None, bias=None, relu: bool = False) -> np.ndarray:
+    """The library's optional fused output epilogue (include/lrs_conv.h; SURVEY §8(f) f3 --
+    an inference BatchNorm y*s + b with its scale/shift per output channel, and a ReLU,
+    as in ResNet's conv2 -> bn2 -> relu):  act(y[..., j] * scale[j] + bias[j])."""
+    y = np.asarray(y, np.float64)
+    if scale is not None:
+        y = y * np.asarray(scale, np.float64)
+    if bias is not None:
+        y = y + np.asarray(bias, np.float64)
+    return np.maximum(y, 0.0) if relu else y
 
 
 def brute_force_conv(x, w, stride=1, pad=0) -> np.ndarray:

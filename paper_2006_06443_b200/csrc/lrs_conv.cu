@@ -209,6 +209,7 @@ struct lrs_conv {
   TinyParams tp{};
   uint32_t tiny_smem = 0;
   void* tiny_buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  float2* epi = nullptr;  // fused output epilogue: (scale, bias) per output channel
   // CP core (the paper's form): stages 2-3 as two depthwise convs
   bool cp_core = false;
   float* w_cpb = nullptr;  // [kh][R1p] vertical taps
@@ -1361,6 +1362,28 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   h->a1.p.g = g;
   h->a2.p.g = g;
   h->a3.p.g = g;
+  // ---------------------------------------------------------------- fused output epilogue
+  if (d->out_scale || d->out_bias) {
+    std::vector<float> sb(static_cast<size_t>(cout) * 2);
+    for (int j = 0; j < cout; ++j) {
+      sb[2 * j] = d->out_scale ? d->out_scale[j] : 1.f;
+      sb[2 * j + 1] = d->out_bias ? d->out_bias[j] : 0.f;
+    }
+    std::vector<uint8_t> b(sb.size() * 4);
+    memcpy(b.data(), sb.data(), b.size());
+    void* pe = nullptr;
+    if ((st = upload(&pe, b)) != LRS_OK) return cleanup_fail(st);
+    h->epi = static_cast<float2*>(pe);
+  }
+  const int relu = d->out_relu ? 1 : 0;
+  h->wp.epi = h->epi;
+  h->wp.relu = relu;
+  h->spp.epi = h->epi;
+  h->spp.relu = relu;
+  h->tp.epi = h->epi;
+  h->tp.relu = relu;
+  h->a3.p.sp.epi = h->epi;
+  h->a3.p.sp.relu = relu;
   for (int k = 0; k < 6; ++k) {
     cudaError_t e = cudaFuncSetAttribute(kernel_ptr(static_cast<KernelId>(k)),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
@@ -1589,7 +1612,7 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
                   h->w_as, h->w_e, h->w_res, h->w_dense_img, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc,
-                  h->sp_uo};
+                  h->sp_uo, h->epi};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (void* b : h->tiny_buf)

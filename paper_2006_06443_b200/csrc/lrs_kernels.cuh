@@ -49,6 +49,8 @@ struct SparseParams {
   int wp;                 // window width in padded columns = (wo-1)*sw + kw
   void* y;                // NHWC Y (device)
   int cout;
+  const float2* epi;      // per output channel (scale, bias) of the fused output epilogue, or NULL
+  int relu;
 };
 
 struct GemmParams {
@@ -423,7 +425,9 @@ __global__ void __launch_bounds__(kThreads, 1) lrs_gemm_kernel(const __grid_cons
         if (m >= P) continue;
         float out[JW];
 #pragma unroll
-        for (int jj = 0; jj < JW; ++jj) out[jj] = yl[ml * LD + e * JW + jj] + acc[i][jj];
+        for (int jj = 0; jj < JW; ++jj)
+          out[jj] = out_epi(yl[ml * LD + e * JW + jj] + acc[i][jj],
+                            out_epi_load(sp.epi, min(jbase + jj, sp.cout - 1)), sp.relu);
         T* dst = yg + static_cast<long long>(m) * sp.cout + jbase;
 #pragma unroll
         for (int b = 0; b < JW / 8; ++b) {

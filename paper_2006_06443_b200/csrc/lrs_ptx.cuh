@@ -317,6 +317,16 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Optional fused output epilogue (include/lrs_conv.h out_scale / out_bias / out_relu):
+// y = act(s * acc + b) on the fp32 accumulator before the single store of Y.
+__device__ __forceinline__ float2 out_epi_load(const float2* epi, int j) {
+  return epi ? __ldg(epi + j) : make_float2(1.f, 0.f);
+}
+__device__ __forceinline__ float out_epi(float v, float2 sb, int relu) {
+  v = fmaf(v, sb.x, sb.y);
+  return relu ? fmaxf(v, 0.f) : v;
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -46,6 +46,8 @@ struct SpaddParams {
   const float* uo;       // U_out [r][cout] fp32 (rows >= R2 zero)
   int t_ld, r;           // row pitch of T, ranks to sum (multiple of 4)
   int dbg;              // timing experiments (LRS_SPADD_DBG): 1 skip staging, 2 skip gather, 4 skip Y update
+  const float2* epi;    // per output channel (scale, bias) of the fused output epilogue, or NULL
+  int relu;
 };
 
 __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_constant__ SpaddParams p) {
@@ -213,6 +215,16 @@ __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_c
   }
   // ---- Y = Y_L + Y_S, written once: each lane owns 8 consecutive channels of its positions
   if (jw >= p.cout || (p.dbg & 4)) return;
+  if (p.epi != nullptr || p.relu) {
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const float2 sb = out_epi_load(p.epi, min(jw + jj, p.cout - 1));
+#pragma unroll
+      for (int k = 0; k < kSpKP; ++k)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[k][jj][i] = out_epi(acc[k][jj][i], sb, p.relu);
+    }
+  }
 #pragma unroll
   for (int k = 0; k < kSpKP; ++k) {
     if (!valid[k]) continue;

@@ -36,6 +36,8 @@ struct TinyParams {
   int r1p, r2p, th, bands, wr, wc;
   int nnz;
   uint32_t off_t1, off_t2, off_u, off_g, off_uo, off_rp, off_ec, off_ev;  // shared-memory carve-up (bytes)
+  const float2* epi;  // per output channel (scale, bias) of the fused output epilogue, or NULL
+  int relu;
 };
 
 __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_constant__ TinyParams p) {
@@ -184,7 +186,8 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
       for (int k = 0; k < 8; ++k) {
         if (pp0 + k < pb) {
           const int q = pp0 + k, hl = q / p.wo, wl = q - hl * p.wo;
-          p.y[((static_cast<long long>(n) * p.ho + ho0 + hl) * p.wo + wl) * p.cout + j] = acc[k];
+          p.y[((static_cast<long long>(n) * p.ho + ho0 + hl) * p.wo + wl) * p.cout + j] =
+              out_epi(acc[k], out_epi_load(p.epi, j), p.relu);
         }
       }
     }

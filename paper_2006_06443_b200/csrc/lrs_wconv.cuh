@@ -112,6 +112,8 @@ struct WconvParams {
   uint32_t acc_cols;    // TMEM columns of one accumulator buffer
   uint32_t e_col0, tmem_cols;
   uint32_t off_a, off_e, off_epi, off_res, off_bar;
+  const float2* epi;    // per output channel (scale, bias) of the fused output epilogue, or NULL
+  int relu;
 };
 
 struct TileCoord {
@@ -462,6 +464,11 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           tmem_ld_wait();
           // lane = channel jw + lane holds 32 columns; transpose through the scratch
           // tile [32 columns][32 channels] so each lane then owns 8 channels of a column
+          if (p.epi != nullptr || p.relu) {  // fused output epilogue (uniform branch)
+            const float2 sb = out_epi_load(p.epi, min(jw + lane, p.cout - 1));
+#pragma unroll
+            for (int cc2 = 0; cc2 < 32; ++cc2) v[cc2] = __float_as_uint(out_epi(__uint_as_float(v[cc2]), sb, p.relu));
+          }
 #pragma unroll
           for (int cc2 = 0; cc2 < 32; ++cc2) {
             const __nv_bfloat16 hb = __float2bfloat16_rn(__uint_as_float(v[cc2]));

@@ -51,6 +51,9 @@ class lrs_conv_desc(ctypes.Structure):
         ("col_idx", ctypes.POINTER(ctypes.c_int32)),
         ("values", ctypes.POINTER(ctypes.c_float)),
         ("core_kind", ctypes.c_int32),
+        ("out_scale", ctypes.POINTER(ctypes.c_float)),
+        ("out_bias", ctypes.POINTER(ctypes.c_float)),
+        ("out_relu", ctypes.c_int32),
     ]
 
 
@@ -130,7 +133,8 @@ def lrs_conv_last_error() -> str:
 def make_desc(batch_max: int, in_h: int, in_w: int, c_in: int, c_out: int, kernel: int,
               stride: int, pad: int, rank_in: int, rank_out: int, dtype: str,
               u_in: np.ndarray, core: Optional[np.ndarray], u_out: np.ndarray,
-              row_ptr: np.ndarray, col_idx: np.ndarray, values: np.ndarray, core_kind: int = LRS_CORE_TUCKER2):
+              row_ptr: np.ndarray, col_idx: np.ndarray, values: np.ndarray, core_kind: int = LRS_CORE_TUCKER2,
+              out_scale: Optional[np.ndarray] = None, out_bias: Optional[np.ndarray] = None, out_relu: bool = False):
     """Build an lrs_conv_desc from host arrays.  Factor arrays are float32
     holding dtype-representable values; for bf16 their bf16 bits are passed.
     Returns (desc, keepalive) -- keep `keepalive` until lrs_conv_create returns."""
@@ -157,7 +161,12 @@ def make_desc(batch_max: int, in_h: int, in_w: int, c_in: int, c_out: int, kerne
         u_out=ptr(as_dtype(u_out)), nnz=len(va),
         row_ptr=rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
         col_idx=ci.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-        values=va.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), core_kind=core_kind)
+        values=va.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), core_kind=core_kind, out_relu=1 if out_relu else 0)
+    for name, arr in (("out_scale", out_scale), ("out_bias", out_bias)):
+        if arr is not None:
+            a = np.ascontiguousarray(arr, np.float32)
+            keep.append(a)
+            setattr(d, name, a.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
     return d, keep
 
 
@@ -195,7 +204,7 @@ class LrsConv:
 
     def __init__(self, batch_max, in_h, in_w, c_in, c_out, kernel, stride, pad, rank_in, rank_out,
                  dtype, u_in, core, u_out, row_ptr, col_idx, values, device: int = 0,
-                 core_kind: int = LRS_CORE_TUCKER2):
+                 core_kind: int = LRS_CORE_TUCKER2, out_scale=None, out_bias=None, out_relu: bool = False):
         import torch
         self.torch = torch
         self.dtype = dtype
@@ -203,7 +212,8 @@ class LrsConv:
         self.device = device
         self.c_out = c_out
         desc, keep = make_desc(batch_max, in_h, in_w, c_in, c_out, kernel, stride, pad, rank_in,
-                               rank_out, dtype, u_in, core, u_out, row_ptr, col_idx, values, core_kind)
+                               rank_out, dtype, u_in, core, u_out, row_ptr, col_idx, values, core_kind,
+                               out_scale, out_bias, out_relu)
         self.handle = lrs_conv_create(desc, device)
         del keep
         oh, ow = ctypes.c_int32(), ctypes.c_int32()
@@ -212,11 +222,12 @@ class LrsConv:
         self.batch_max, self.in_h, self.in_w, self.c_in = batch_max, in_h, in_w, c_in
 
     @classmethod
-    def from_inputs(cls, inp, batch_max: Optional[int] = None, device: int = 0) -> "LrsConv":
+    def from_inputs(cls, inp, batch_max: Optional[int] = None, device: int = 0, out_scale=None, out_bias=None,
+                    out_relu: bool = False) -> "LrsConv":
         c = inp.cfg
-        return cls(batch_max or inp.x.shape[0], c.in_h, c.in_w, c.c_in, c.c_out, c.k, c.stride, c.pad,
-                   c.rank_in, c.rank_out, c.dtype, inp.u_in, inp.core, inp.u_out, inp.row_ptr,
-                   inp.col_idx, inp.values, device)
+        return cls(batch_max or (inp.x.shape[0] if inp.x is not None else c.batch), c.in_h, c.in_w, c.c_in, c.c_out,
+                   c.k, c.stride, c.pad, c.rank_in, c.rank_out, c.dtype, inp.u_in, inp.core, inp.u_out, inp.row_ptr,
+                   inp.col_idx, inp.values, device, out_scale=out_scale, out_bias=out_bias, out_relu=out_relu)
 
     @classmethod
     def from_cp(cls, batch_max: int, in_h: int, in_w: int, kernel: int, stride: int, pad: int, dtype: str,

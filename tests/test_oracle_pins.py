@@ -339,3 +339,13 @@ def test_forward_cp_against_brute_force(stride, pad):
     ref = O.brute_force_conv(x, w, stride, pad)
     got = O.forward_cp(x, a, b, c, d, row_ptr, col_idx, values, stride, pad)
     assert rel_l2(got, ref) < 1e-13
+
+
+def test_output_epilogue_hand_values():
+    """The fused output epilogue (BatchNorm-style affine + ReLU per output channel) on
+    a hand-computed case: channel 0 -> 2*y - 1, channel 1 -> -y + 0.5, then ReLU."""
+    y = np.array([[[[1.0, 1.0], [0.25, -2.0]]]])
+    got = O.output_epilogue(y, [2.0, -1.0], [-1.0, 0.5], relu=True)
+    assert np.array_equal(got, np.array([[[[1.0, 0.0], [0.0, 2.5]]]]))
+    assert np.array_equal(O.output_epilogue(y), y)
+    assert np.array_equal(O.output_epilogue(y, bias=[1.0, 0.0]), y + np.array([1.0, 0.0]))
