@@ -29,10 +29,11 @@ class CompressedConv2d:
     """A drop-in for a torch 3x3 conv module: y = conv(x, L + S) on the GPU
     library.  Holds one LrsConv handle sized for `batch_max` images."""
 
-    def __init__(self, inp, batch_max: int, device: int = 0):
+    def __init__(self, inp, batch_max: int, device: int = 0, out_scale=None, out_bias=None, out_relu: bool = False):
         torch = _torch()
         self.cfg = inp.cfg
-        self.layer = LrsConv.from_inputs(inp, batch_max=batch_max, device=device)
+        self.layer = LrsConv.from_inputs(inp, batch_max=batch_max, device=device, out_scale=out_scale,
+                                         out_bias=out_bias, out_relu=out_relu)
         self.device = device
         self.stream = None  # None: torch's current stream at call time
 
@@ -86,25 +87,55 @@ def fold_dense_batchnorms(model):
     return model
 
 
+def _bottleneck_forward_fused(self, x):
+    """torchvision Bottleneck.forward with bn2 + relu fused into the compressed conv2
+    (the library's output epilogue), everything else unchanged."""
+    identity = x
+    out = self.relu(self.bn1(self.conv1(x)))
+    out = self.conv2(out)  # conv + bn2 + relu in one library launch chain
+    out = self.bn3(self.conv3(out))
+    if self.downsample is not None:
+        identity = self.downsample(x)
+    out += identity
+    return self.relu(out)
+
+
 def build_compressed_resnet50(batch_max: int, device: int = 0, seed: int = 0, density: float = 0.02,
                               layers: Optional[List] = None, fold_bn: bool = True):
     """torchvision resnet50 (random init under manual_seed(seed), eval mode,
     bf16, channels_last) on cuda:device with its 16 3x3 convs compressed.
     fold_bn: fold the BatchNorms of the dense convs into them (fp32, before the
-    bf16 cast).  Returns (model, {table index: CompressedConv2d})."""
+    bf16 cast), and the BatchNorm + ReLU after each compressed conv into the
+    library's fused output epilogue.  Returns (model, {table index:
+    CompressedConv2d})."""
     torch = _torch()
+    import types
     import torchvision
     import workloads
     torch.manual_seed(seed)
     model = torchvision.models.resnet50(weights=None).eval()
     if fold_bn:
         model = fold_dense_batchnorms(model)
+    # bn2's inference affine from its fp32 parameters (before the bf16 cast)
+    bn2 = {}
+    for idx, name, cfg in (layers or workloads.resnet50_compressed_layers(batch=batch_max, density=density)):
+        bn = model.get_submodule(name.rsplit(".", 1)[0] + ".bn2")
+        scale = (bn.weight / torch.sqrt(bn.running_var + bn.eps)).detach().float()
+        bias = (bn.bias - bn.running_mean * scale).detach().float()
+        bn2[idx] = (scale.numpy(), bias.numpy())
     model = model.to(device=f"cuda:{device}", dtype=torch.bfloat16).to(memory_format=torch.channels_last)
     comp: Dict[int, CompressedConv2d] = {}
     for idx, name, cfg in (layers or workloads.resnet50_compressed_layers(batch=batch_max, density=density)):
         inp = workloads.generate_weights(cfg)
-        conv = CompressedConv2d(inp, batch_max=batch_max, device=device)
+        parent_name = name.rsplit(".", 1)[0]
+        parent = model.get_submodule(parent_name)
+        if fold_bn:
+            conv = CompressedConv2d(inp, batch_max=batch_max, device=device, out_scale=bn2[idx][0],
+                                    out_bias=bn2[idx][1], out_relu=True)
+            parent.bn2 = torch.nn.Identity()
+            parent.forward = types.MethodType(_bottleneck_forward_fused, parent)
+        else:
+            conv = CompressedConv2d(inp, batch_max=batch_max, device=device)
         comp[idx] = conv
-        parent = model.get_submodule(name.rsplit(".", 1)[0])
         setattr(parent, name.rsplit(".", 1)[1], _module(conv))
     return model, comp
