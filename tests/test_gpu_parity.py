@@ -210,3 +210,21 @@ def test_host_io_pipelined_chunks_bitwise(name, batch):
             layer.forward_host(xh, yh, stream=s)
         s.synchronize()
         assert torch.equal(yh, y.cpu())
+
+
+EDGE = [  # (n, h, w, cin, cout, k, s, p, r1, r2, density, dtype)  -- the ABI's limits
+    (2, 16, 16, 64, 64, 7, 1, 3, 32, 32, 0.02, "bf16"),     # largest kernel (7x7)
+    (2, 9, 9, 64, 64, 7, 2, 3, 16, 16, 0.03, "f32"),        # 7x7, stride 2, fp32
+    (3, 7, 7, 256, 256, 3, 1, 1, 256, 256, 0.02, "bf16"),   # largest ranks (256)
+    (2, 5, 128, 64, 64, 3, 1, 1, 16, 16, 0.02, "bf16"),     # widest output row (128)
+    (1, 4, 4, 8, 8, 3, 1, 1, 4, 4, 0.5, "bf16"),            # smallest channels (8), dense-ish S
+]
+
+
+@pytest.mark.parametrize("geom", EDGE)
+def test_edge_geometries_vs_oracle(geom):
+    n, h, w, cin, cout, k, s, p, r1, r2, dens, dtype = geom
+    cfg = workloads.LayerConfig("t", n, h, w, cin, cout, k, s, p, r1, r2, dens, dtype, seed=31)
+    inp = workloads.generate(cfg)
+    _, _, y = run(inp)
+    check(y, oracle(inp), dtype)
