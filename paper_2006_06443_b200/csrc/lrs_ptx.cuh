@@ -209,6 +209,25 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// 16 lanes x 256 bits, repeated twice along the columns (16 columns): thread t gets
+// lane t/4 (regs 0-1: columns 2(t%4), +1; regs 4-5: columns 8 + 2(t%4), +1) and lane
+// t/4 + 8 (regs 2-3, 6-7) -- the m8n8 fragment layout stmatrix consumes
+__device__ __forceinline__ void tmem_ld_16x256b_x2(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+// four 8x8 b16 matrices stored transposed (thread 8i + j gives the address of row j of matrix i)
+__device__ __forceinline__ void stmatrix_x4_trans(uint32_t saddr, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+  asm volatile("stmatrix.sync.aligned.x4.trans.m8n8.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a0),
+               "r"(a1), "r"(a2), "r"(a3)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&b);
+}
+
 // UMMA shared-memory matrix descriptor, K-major, swizzle width sw_bytes
 // (128/64/32): rows of sw_bytes, 8-row atoms at SBO = 8*sw_bytes.
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sw_bytes) {

@@ -458,21 +458,48 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         const int pitch = p.u_pitch[u], nw = p.u_nw[u], un = p.u_n[u], rows = p.u_rows[u];
         const int r0 = p.u_r0[u], w0 = p.u_wo0[u], ucol = p.u_col[u], q0 = p.u_q0[u];
         for (int c0 = ehalf * 32; c0 < un; c0 += 64) {
-          uint32_t v[32];
-          tmem_ld32_nowait(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + acc0 + static_cast<uint32_t>(ucol + c0),
-                           v);
-          tmem_ld_wait();
-          // lane = channel jw + lane holds 32 columns; transpose through the scratch
-          // tile [32 columns][32 channels] so each lane then owns 8 channels of a column
-          if (p.epi != nullptr || p.relu) {  // fused output epilogue (uniform branch)
-            const float2 sb = out_epi_load(p.epi, min(jw + lane, p.cout - 1));
+          // 32 columns x this warp's 32 channels -> the scratch tile [32 columns][32 channels]
+          // bf16: per 16 lanes x 16 columns one tcgen05.ld.16x256b (already in the m8n8
+          // fragment layout) and one transposing stmatrix (each stored row = 8 channels of
+          // one column) -- instead of 32 two-byte shared stores per lane
+          {
+            const int t1 = lane >> 2, mi = lane >> 3, mj = lane & 7;
+            const bool epi = p.epi != nullptr || p.relu;
 #pragma unroll
-            for (int cc2 = 0; cc2 < 32; ++cc2) v[cc2] = __float_as_uint(out_epi(__uint_as_float(v[cc2]), sb, p.relu));
-          }
+            for (int h = 0; h < 2; ++h) {
+              float2 sba = make_float2(1.f, 0.f), sbb = make_float2(1.f, 0.f);
+              if (epi) {
+                sba = out_epi_load(p.epi, min(jw + 16 * h + t1, p.cout - 1));
+                sbb = out_epi_load(p.epi, min(jw + 16 * h + t1 + 8, p.cout - 1));
+              }
 #pragma unroll
-          for (int cc2 = 0; cc2 < 32; ++cc2) {
-            const __nv_bfloat16 hb = __float2bfloat16_rn(__uint_as_float(v[cc2]));
-            sts_u16(scr + static_cast<uint32_t>(cc2 * 64 + lane * 2), *reinterpret_cast<const uint16_t*>(&hb));
+              for (int cb = 0; cb < 2; ++cb) {
+                uint32_t r[8];
+                tmem_ld_16x256b_x2(tmem + (static_cast<uint32_t>(q4 * 32 + 16 * h) << 16) + acc0 +
+                                       static_cast<uint32_t>(ucol + c0 + 16 * cb),
+                                   r);
+                tmem_ld_wait();
+                float f[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[i]);
+                if (epi) {
+                  f[0] = out_epi(f[0], sba, p.relu);
+                  f[1] = out_epi(f[1], sba, p.relu);
+                  f[4] = out_epi(f[4], sba, p.relu);
+                  f[5] = out_epi(f[5], sba, p.relu);
+                  f[2] = out_epi(f[2], sbb, p.relu);
+                  f[3] = out_epi(f[3], sbb, p.relu);
+                  f[6] = out_epi(f[6], sbb, p.relu);
+                  f[7] = out_epi(f[7], sbb, p.relu);
+                }
+                // scratch row (column col, 8-channel part) at col*64 + (part ^ ((col >> 1) & 3))*16:
+                // the 8 rows of one stmatrix phase land in 8 distinct 16-byte bank groups
+                const int scol = cb * 16 + (mi >> 1) * 8 + mj, spart = 2 * h + (mi & 1);
+                const uint32_t addr = scr + static_cast<uint32_t>(scol * 64 + ((spart ^ ((scol >> 1) & 3)) * 16));
+                stmatrix_x4_trans(addr, pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                  pack_bf16x2(f[6], f[7]));
+              }
+            }
           }
           __syncwarp();
           // lane l, pass q: column col = q*8 + l/4, channels 8*(l%4) .. +7
@@ -482,7 +509,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           for (int q = 0; q < 4; ++q) {
             const int col = q * 8 + (lane >> 2);
             const int cidx = c0 + col;
-            const uint4 val = lds_v4(scr + static_cast<uint32_t>(col * 64 + part * 16));
+            const uint4 val = lds_v4(scr + static_cast<uint32_t>(col * 64 + ((part ^ ((col >> 1) & 3)) * 16)));
             if (cidx >= un) continue;
             const int qv = q0 + (cidx >> 3), img = cidx & 7;
             const int rr = qv / pitch, cc = qv - rr * pitch;
