@@ -504,10 +504,12 @@ lrs_status build_core(lrs_conv* h, const lrs_conv_desc* d) {
   memset(&c, 0, sizeof(c));
   double best = 1e30;
   int best_th = 0, best_ipt = 0;
-  const int ipt_env = getenv("LRS_CORE_IPT") ? atoi(getenv("LRS_CORE_IPT")) : 0;
+  const int ipt_env = getenv("LRS_CORE_IPT") ? atoi(getenv("LRS_CORE_IPT")) : 0;  // planner experiments
+  const int th_env = getenv("LRS_CORE_TH") ? atoi(getenv("LRS_CORE_TH")) : 0;
   for (int ipt = 1; ipt <= 8; ++ipt) {
     if (ipt_env && ipt != ipt_env) continue;
     for (int th = 1; th <= ho; ++th) {
+      if (th_env && th != th_env) continue;
       const int wr = th + kh - 1;
       if (wr > 256) break;
       const int p1 = wr * wc, nb1 = (ipt * p1 + 127) / 128;
@@ -1748,6 +1750,7 @@ lrs_status lrs_sparse_from_slices(int32_t c_in, int32_t c_out, int32_t kernel_h,
 lrs_status lrs_conv_debug_trace(lrs_conv* h, void* dev_buf) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
   h->wp.trace = static_cast<unsigned long long*>(dev_buf);
+  h->cp.trace = static_cast<unsigned long long*>(dev_buf);  // core kernel: indices 8190..13095
   if (const char* e = getenv("LRS_WCONV_DBG")) h->wp.dbg = atoi(e);
   return LRS_OK;
 }

@@ -58,7 +58,19 @@ struct CoreParams {
   int nacc;
   uint32_t tmem_cols;
   uint32_t off_t1, off_bar;
+  unsigned long long* trace;  // optional globaltimer stamps (LRS_WCONV_DEBUG builds, tools/ctrace.py)
 };
+
+#ifdef LRS_WCONV_DEBUG
+#define CTRACE(p, cond, idx) \
+  do {                       \
+    if ((p).trace && (cond)) (p).trace[idx] = gtimer(); \
+  } while (0)
+#else
+#define CTRACE(p, cond, idx) \
+  do {                       \
+  } while (0)
+#endif
 
 __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_constant__ CoreParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -99,8 +111,10 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  CTRACE(p, threadIdx.x == 0 && blockIdx.x < 2048, 9000 + 2 * blockIdx.x);
   pdl_wait();  // the previous kernel's output is visible from here on
   pdl_launch_dependents();  // only after the wait: every kernel before us is then complete
+  CTRACE(p, threadIdx.x == 0 && blockIdx.x == 0, 8190);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -111,6 +125,8 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         for (int c = 0; c < p.n_ck; ++c, ++it) {
           const int s = it % p.ns;
           if (it >= p.ns) mbar_wait(&empty[s], ((it / p.ns) - 1) & 1);
+          CTRACE(p, blockIdx.x == 0 && c == 0 && (tile - blockIdx.x) / gridDim.x < 4,
+                 8200 + 10 * ((tile - blockIdx.x) / gridDim.x) + 1);
           uint8_t* dst = smem + s * p.slot_bytes;
           mbar_arrive_expect_tx(&full[s], p.x_bytes + p.u_bytes);
           tma_load_4d(dst, &p.tmX, &full[s], c * 64, -p.pw, ho0 - p.ph, g * p.ipt);
@@ -148,6 +164,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         const int s = it % p.ns;
         mbar_wait(&full[s], (it / p.ns) & 1);
         tc_fence_after();
+        CTRACE(p, blockIdx.x == 0 && lane == 0 && k < 4 && c == 0, 8200 + 10 * k + 2);
         const uint32_t xa = base + s * p.slot_bytes;
         if (elect_one()) {
           for (int b1 = 0; b1 < p.nb1; ++b1)
@@ -160,9 +177,11 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         }
         __syncwarp();
       }
+      CTRACE(p, blockIdx.x == 0 && lane == 0 && k < 4, 8200 + 10 * k + 3);
       // ---- wait for the bf16 T1 window in shared memory
       mbar_wait(t1s_full, k & 1);
       tc_fence_after();
+      CTRACE(p, blockIdx.x == 0 && lane == 0 && k < 4, 8200 + 10 * k + 6);
       // ---- a2: T2 = sum over taps of (window shifted by y*wc + x) . G[tap]
       for (int t = 0; t < taps; ++t) {
         const int ty = t / p.kw, tx = t - ty * p.kw;
@@ -191,6 +210,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         mma_commit(t1w_empty);
       }
       __syncwarp();
+      CTRACE(p, blockIdx.x == 0 && lane == 0 && k < 4, 8200 + 10 * k + 7);
     }
   } else {
     // -------------------------------------------------------------- epilogue
@@ -208,6 +228,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       mbar_wait_sleep(&t1_full[b], use & 1);
       if (k > 0) mbar_wait(t1w_empty, (k - 1) & 1);
       tc_fence_after();
+      CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 4);
       for (int b1 = 0; b1 < p.nb1; ++b1) {
         const uint32_t row = static_cast<uint32_t>(b1 * 128 + q4 * 32 + lane);
         for (int c0 = ehalf * 16; c0 < p.r1p; c0 += 32) {
@@ -233,9 +254,11 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(t1s_full);
+      CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 5);
       // ---- T2 (fp32 TMEM) -> bf16 rows of global T2
       mbar_wait_sleep(&t2_full[b], use & 1);
       tc_fence_after();
+      CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 8);
       for (int b2 = 0; b2 < p.nb2; ++b2) {
         const int q = b2 * 128 + q4 * 32 + lane;
         const int img = q / p.p1, rem = q - img * p.p1;
@@ -263,8 +286,10 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
+      CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 9);
     }
   }
+  CTRACE(p, threadIdx.x == 64 && blockIdx.x < 2048, 9000 + 2 * blockIdx.x + 1);
 
   tc_fence_before();
   __syncthreads();

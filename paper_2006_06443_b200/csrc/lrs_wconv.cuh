@@ -161,7 +161,6 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   const uint32_t slot_info = smem_u32(tmem_slot + 4);  // [kWMaxSlots][kWMaxBpi] u32, written by the producer
 
   if (WTRACE(p) && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
-  const int taps = p.kh * p.kw;
   const int nwin = p.n_tk + p.n_xw;
 
   if (threadIdx.x == 0) {
