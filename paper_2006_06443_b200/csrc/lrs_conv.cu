@@ -12,6 +12,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/lrs_conv.h"
@@ -219,6 +220,7 @@ struct lrs_conv {
   bool use_core = false;
   CoreParams cp{};
   uint32_t core_smem = 0;
+  int core_grid = 0;  // CTAs of the core kernel (persistent over its tiles)
   const void* cx_ptr = nullptr;
   int cx_n = -1;
 };
@@ -487,80 +489,143 @@ lrs_status build_tiny(lrs_conv* h, const lrs_conv_desc* d) {
   return LRS_OK;
 }
 
-// a1 + a2 fused (lrs_core.cuh): pick the band height th and the images per tile ipt
-// (tile = ipt images x th output rows) minimising waves x bytes a tile moves into
-// shared memory (its X windows + the U_in and G chunks it streams), within TMEM
-// (max(T1, T2) columns <= 512) and shared memory (>= 2 slots + the T1 window).
-lrs_status build_core(lrs_conv* h, const lrs_conv_desc* d) {
-  const int cin = d->c_in, kh = d->kernel_h, kw = d->kernel_w;
-  const int ho = h->ho, wo = h->wo, r1p = h->r1p, r2p = h->r2p;
-  if (h->f32 || h->svd || h->cp_core || d->stride_h != 1 || d->stride_w != 1 || cin % 64 != 0 || getenv("LRS_NO_CORE"))
-    return LRS_OK;
-  const int wc = wo + kw - 1;
-  if (wc > 256 || r1p > 256 || r2p > 256) return LRS_OK;
-  const int g_kc = r1p % 64 == 0 ? 64 : (r1p % 32 == 0 ? 32 : 16);
-  const int taps = kh * kw;
-  CoreParams& c = h->cp;
-  memset(&c, 0, sizeof(c));
-  double best = 1e30;
-  int best_th = 0, best_ipt = 0;
+// a1 + a2 fused (lrs_core.cuh).  A plan is (ipt images per tile, th output rows per
+// tile, grid): tile = ipt images x th rows, within TMEM (max(T1, T2) columns <= 512) and
+// shared memory (X ring >= 2 slots, G ring >= 2 slots, the T1 window).  The model cost
+// is waves x bytes a tile moves into shared memory (its X windows + the U_in and G
+// chunks it streams); autotune_core then times the best few plans on the device.
+struct CoreGeom {
+  int cin, kh, kw, ho, wo, wc, r1p, r2p, g_kc, taps, n_g;
+  uint32_t u_bytes, g_bytes, g_slot, avail;
+};
+
+static CoreGeom core_geom(const lrs_conv* h, const lrs_conv_desc* d) {
+  CoreGeom G;
+  G.cin = d->c_in; G.kh = d->kernel_h; G.kw = d->kernel_w; G.ho = h->ho; G.wo = h->wo;
+  G.wc = h->wo + G.kw - 1; G.r1p = h->r1p; G.r2p = h->r2p;
+  G.g_kc = G.r1p % 64 == 0 ? 64 : (G.r1p % 32 == 0 ? 32 : 16);
+  G.taps = G.kh * G.kw;
+  G.n_g = G.taps * (G.r1p / G.g_kc);
+  G.u_bytes = static_cast<uint32_t>(G.r1p) * 128u;
+  G.g_bytes = static_cast<uint32_t>(G.r2p * G.g_kc * 2);
+  G.g_slot = align1024(G.g_bytes);
+  G.avail = static_cast<uint32_t>(kMaxSmem) - 1024u - 2048u;  // alignment slack, barriers
+  return G;
+}
+
+// Shared-memory layout of one (ipt, th): X ring (ns_x slots), G ring (ns_g), T1 window.
+static bool core_layout(const CoreGeom& G, int ipt, int th, CoreParams& q) {
+  const int wr = th + G.kh - 1, p1 = wr * G.wc;
+  if (wr > 256) return false;
+  q.nb1 = (ipt * p1 + 127) / 128;
+  q.nb2 = ((ipt - 1) * p1 + (th - 1) * G.wc + G.wo + 127) / 128;
+  q.acc_cols = static_cast<uint32_t>(std::max(q.nb1 * G.r1p, q.nb2 * G.r2p));
+  if (q.acc_cols > 512) return false;
+  q.t1_rows = static_cast<uint32_t>((q.nb2 * 128 + (G.kh - 1) * G.wc + G.kw - 1 + 7) & ~7);
+  const uint32_t t1_bytes = align1024(q.t1_rows * static_cast<uint32_t>(G.r1p) * 2u);
+  q.x_bytes = static_cast<uint32_t>(ipt * wr * G.wc) * 128u;
+  q.u_off = align1024(q.x_bytes);
+  q.x_slot = q.u_off + G.u_bytes;
+  // the last M block of the last X slot reads up to nb1 * 16 KB from the slot start
+  const uint32_t x_tail =
+      static_cast<uint32_t>(q.nb1) * 16384u > q.x_slot ? static_cast<uint32_t>(q.nb1) * 16384u - q.x_slot : 0u;
+  if (t1_bytes + x_tail + 2 * q.x_slot + 2 * G.g_slot > G.avail) return false;
+  const uint32_t left = G.avail - t1_bytes - x_tail;
+  const int n_ck = G.cin / 64;
+  // all X chunks of a tile if possible, then as much of G as fits (all of it: resident)
+  q.ns_x = std::min(kCMaxX, std::max(2, n_ck));
+  while (q.ns_x > 2 && q.ns_x * q.x_slot + 2 * G.g_slot > left) --q.ns_x;
+  q.ns_g = static_cast<int>(std::min<uint32_t>(static_cast<uint32_t>(std::min(kCMaxG, G.n_g)),
+                                               (left - q.ns_x * q.x_slot) / G.g_slot));
+  if (q.ns_g < G.n_g) {  // prefer a resident G over a full X ring when one X slot less makes room
+    const int ns_x2 = std::max(2, q.ns_x - 1);
+    if (G.n_g <= kCMaxG && static_cast<uint32_t>(ns_x2) * q.x_slot + G.n_g * G.g_slot <= left) {
+      q.ns_x = ns_x2;
+      q.ns_g = G.n_g;
+    }
+  }
+  q.g_res = q.ns_g == G.n_g ? 1 : 0;
+  q.off_g = static_cast<uint32_t>(q.ns_x) * q.x_slot + x_tail;
+  q.off_t1 = q.off_g + static_cast<uint32_t>(q.ns_g) * G.g_slot;
+  q.off_bar = q.off_t1 + t1_bytes;
+  return true;
+}
+
+// Feasible (model cost, ipt, th) for a grid of `grid` CTAs, cheapest first.
+static std::vector<std::tuple<double, int, int>> core_candidates(const lrs_conv* h, const lrs_conv_desc* d,
+                                                                 int grid) {
+  const CoreGeom G = core_geom(h, d);
+  std::vector<std::tuple<double, int, int>> v;
   const int ipt_env = getenv("LRS_CORE_IPT") ? atoi(getenv("LRS_CORE_IPT")) : 0;  // planner experiments
   const int th_env = getenv("LRS_CORE_TH") ? atoi(getenv("LRS_CORE_TH")) : 0;
   for (int ipt = 1; ipt <= 8; ++ipt) {
     if (ipt_env && ipt != ipt_env) continue;
-    for (int th = 1; th <= ho; ++th) {
+    for (int th = 1; th <= G.ho; ++th) {
       if (th_env && th != th_env) continue;
-      const int wr = th + kh - 1;
-      if (wr > 256) break;
-      const int p1 = wr * wc, nb1 = (ipt * p1 + 127) / 128;
-      const int nb2 = ((ipt - 1) * p1 + (th - 1) * wc + wo + 127) / 128;
-      const uint32_t acc = static_cast<uint32_t>(std::max(nb1 * r1p, nb2 * r2p));
-      if (acc > 512) continue;
-      const uint32_t t1_rows = static_cast<uint32_t>(std::max(nb1 * 128, nb2 * 128 + (kh - 1) * wc + kw - 1));
-      const uint32_t t1_bytes = align1024(t1_rows * static_cast<uint32_t>(r1p) * 2u);
-      const uint32_t x_region = static_cast<uint32_t>(nb1) * 16384u;
-      const uint32_t b_bytes = align1024(std::max<uint32_t>(static_cast<uint32_t>(r1p) * 128u,
-                                                            static_cast<uint32_t>(r2p * g_kc * 2)));
-      const uint32_t slot = x_region + b_bytes;
-      const uint32_t fixed = t1_bytes + 1024u + 1024u;  // barriers + alignment slack
-      if (fixed + 2 * slot > static_cast<uint32_t>(kMaxSmem)) continue;
-      const int bands = (ho + th - 1) / th;
+      CoreParams q;
+      memset(&q, 0, sizeof(q));
+      if (!core_layout(G, ipt, th, q)) continue;
+      const int p1 = (th + G.kh - 1) * G.wc;
+      const int bands = (G.ho + th - 1) / th;
       const long long tiles = static_cast<long long>((d->batch_max + ipt - 1) / ipt) * bands;
-      const double bytes = static_cast<double>(ipt) * p1 * cin * 2 + static_cast<double>(cin) * r1p * 2 +
-                           static_cast<double>(taps) * r1p * r2p * 2 + 8192.0;
-      const double cost = static_cast<double>((tiles + h->sms - 1) / h->sms) * bytes;
-      if (cost < best * 0.999) {
-        best = cost;
-        best_th = th;
-        best_ipt = ipt;
-      }
+      const double bytes = static_cast<double>(ipt) * p1 * G.cin * 2 + static_cast<double>(G.cin) * G.r1p * 2 +
+                           static_cast<double>(G.taps) * G.r1p * G.r2p * 2 + 8192.0;
+      v.emplace_back(static_cast<double>((tiles + grid - 1) / grid) * bytes, ipt, th);
     }
   }
-  if (!best_th) return LRS_OK;
-  const int th = best_th, ipt = best_ipt, wr = th + kh - 1;
-  const int bands = (ho + th - 1) / th;
-  c.n = d->batch_max; c.ho = ho; c.wo = wo; c.kh = kh; c.kw = kw; c.ph = d->pad_h; c.pw = d->pad_w;
-  c.th = th; c.bands = bands; c.ipt = ipt; c.wr = wr; c.wc = wc; c.p1 = wr * wc;
-  c.nb1 = (ipt * c.p1 + 127) / 128;
-  c.nb2 = ((ipt - 1) * c.p1 + (th - 1) * wc + wo + 127) / 128;
-  c.n_ck = cin / 64;
-  c.r1p = r1p; c.r2p = r2p; c.g_kc = g_kc; c.n_gk = r1p / g_kc; c.sw_g = static_cast<uint32_t>(g_kc * 2);
-  c.x_bytes = static_cast<uint32_t>(ipt * wr * wc) * 128u;
-  c.x_region = static_cast<uint32_t>(c.nb1) * 16384u;
-  c.u_bytes = static_cast<uint32_t>(r1p) * 128u;
-  c.g_bytes = static_cast<uint32_t>(r2p * g_kc * 2);
-  c.slot_bytes = c.x_region + align1024(std::max(c.u_bytes, c.g_bytes));
-  c.t1_rows = static_cast<uint32_t>(std::max(c.nb1 * 128, c.nb2 * 128 + (kh - 1) * wc + kw - 1));
-  const uint32_t t1_bytes = align1024(c.t1_rows * static_cast<uint32_t>(r1p) * 2u);
-  c.ns = std::min<int>(kCMaxSlots, static_cast<int>((kMaxSmem - t1_bytes - 2048u) / c.slot_bytes));
-  c.off_t1 = static_cast<uint32_t>(c.ns) * c.slot_bytes;
-  c.off_bar = c.off_t1 + t1_bytes;
-  c.acc_cols = static_cast<uint32_t>(std::max(c.nb1 * r1p, c.nb2 * r2p));
+  std::stable_sort(v.begin(), v.end(),
+                   [](const auto& a, const auto& b) { return std::get<0>(a) < std::get<0>(b) * 0.999; });
+  return v;
+}
+
+// Fill h->cp for one plan (the tensor maps of U_in and G are plan-independent and kept).
+static void apply_core_plan(lrs_conv* h, const lrs_conv_desc* d, int ipt, int th, int grid) {
+  const CoreGeom G = core_geom(h, d);
+  CoreParams& c = h->cp;
+  const CUtensorMap tmU = c.tmU, tmG = c.tmG;
+  unsigned long long* trace = c.trace;
+  memset(&c, 0, sizeof(c));
+  c.tmU = tmU;
+  c.tmG = tmG;
+  c.trace = trace;
+  core_layout(G, ipt, th, c);
+  c.n = d->batch_max; c.ho = G.ho; c.wo = G.wo; c.kh = G.kh; c.kw = G.kw; c.ph = d->pad_h; c.pw = d->pad_w;
+  c.th = th; c.bands = (G.ho + th - 1) / th; c.ipt = ipt; c.wr = th + G.kh - 1; c.wc = G.wc; c.p1 = c.wr * G.wc;
+  c.n_ck = G.cin / 64;
+  c.r1p = G.r1p; c.r2p = G.r2p; c.g_kc = G.g_kc; c.n_gk = G.r1p / G.g_kc; c.sw_g = static_cast<uint32_t>(G.g_kc * 2);
+  c.u_bytes = G.u_bytes;
+  c.g_bytes = G.g_bytes;
+  c.g_slot = G.g_slot;
+  c.t1_sw128 = (G.r1p % 64 == 0 && !getenv("LRS_CORE_T1_NOSWZ")) ? 1 : 0;
   c.nacc = 2 * c.acc_cols <= 512 ? 2 : 1;
   uint32_t tc = 32;
   while (tc < c.nacc * c.acc_cols) tc <<= 1;
   c.tmem_cols = tc;
-  h->core_smem = c.off_bar + 1024u + 1024u;
+  h->core_smem = c.off_bar + 2048u + 1024u;
+  h->core_grid = std::max(1, std::min(h->sms, grid));
+  h->cx_ptr = nullptr;  // the X tensor map's box depends on the plan
+  if (getenv("LRS_VERBOSE"))
+    fprintf(stderr,
+            "[lrs] core: th=%d ipt=%d bands=%d wr=%d wc=%d nb1=%d nb2=%d acc=%u nacc=%d ns_x=%d ns_g=%d g_res=%d "
+            "t1_sw128=%d t1_rows=%u smem=%u grid<=%d\n",
+            th, ipt, c.bands, c.wr, G.wc, c.nb1, c.nb2, c.acc_cols, c.nacc, c.ns_x, c.ns_g, c.g_res, c.t1_sw128,
+            c.t1_rows, h->core_smem, h->core_grid);
+}
+
+lrs_status build_core(lrs_conv* h, const lrs_conv_desc* d) {
+  const int cin = d->c_in, kh = d->kernel_h, kw = d->kernel_w;
+  const int r1p = h->r1p, r2p = h->r2p;
+  if (h->f32 || h->svd || h->cp_core || d->stride_h != 1 || d->stride_w != 1 || cin % 64 != 0 || getenv("LRS_NO_CORE"))
+    return LRS_OK;
+  const int wc = h->wo + kw - 1;
+  if (wc > 256 || r1p > 256 || r2p > 256) return LRS_OK;
+  int grid = h->sms;
+  if (const char* e = getenv("LRS_CORE_GRID")) grid = std::max(1, std::min(h->sms, atoi(e)));
+  const auto cand = core_candidates(h, d, grid);
+  if (cand.empty()) return LRS_OK;
+  const CoreGeom G = core_geom(h, d);
+  CoreParams& c = h->cp;
+  memset(&c, 0, sizeof(c));
   lrs_status st;
   {
     uint64_t dims[2] = {static_cast<uint64_t>(cin), static_cast<uint64_t>(r1p)};
@@ -573,16 +638,14 @@ lrs_status build_core(lrs_conv* h, const lrs_conv_desc* d) {
   {
     uint64_t dims[2] = {static_cast<uint64_t>(kh * kw * r1p), static_cast<uint64_t>(r2p)};
     uint64_t strides[1] = {static_cast<uint64_t>(kh * kw * r1p) * 2};
-    uint32_t box[2] = {static_cast<uint32_t>(g_kc), static_cast<uint32_t>(r2p)};
+    uint32_t box[2] = {static_cast<uint32_t>(G.g_kc), static_cast<uint32_t>(r2p)};
     uint32_t estr[2] = {1, 1};
-    if ((st = encode_t(&c.tmG, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, h->w_core, dims, strides, box, estr, c.sw_g)) !=
-        LRS_OK)
+    if ((st = encode_t(&c.tmG, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, h->w_core, dims, strides, box, estr,
+                       static_cast<uint32_t>(G.g_kc * 2))) != LRS_OK)
       return st;
   }
+  apply_core_plan(h, d, std::get<1>(cand[0]), std::get<2>(cand[0]), grid);
   h->use_core = true;
-  if (getenv("LRS_VERBOSE"))
-    fprintf(stderr, "[lrs] core: th=%d ipt=%d bands=%d wr=%d wc=%d nb1=%d nb2=%d acc=%u nacc=%d ns=%d t1_rows=%u smem=%u\n",
-            th, ipt, bands, wr, wc, c.nb1, c.nb2, c.acc_cols, c.nacc, c.ns, c.t1_rows, h->core_smem);
   return LRS_OK;
 }
 
@@ -1059,6 +1122,84 @@ extern "C" {
 
 const char* lrs_conv_last_error(void) { return g_err.c_str(); }
 
+// Time the best few core plans on the device (after every kernel is built): for the
+// full grid and, when the expansion + sparse kernel leaves SMs free, for a grid of
+// exactly those SMs -- the two kernels of consecutive forwards are then co-resident and
+// overlap under PDL (C2: the core on 36 SMs while the fused kernel's sparse windows run
+// on the other 112).  Each plan runs back-to-back forwards on zero-filled scratch
+// buffers of batch_max images; the fastest stays.  LRS_NO_AUTOTUNE=1 keeps the model's
+// choice; any LRS_CORE_* override disables the tuning.
+static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d) {
+  if (!h->use_core || getenv("LRS_NO_AUTOTUNE") || getenv("LRS_CORE_IPT") || getenv("LRS_CORE_TH") ||
+      getenv("LRS_CORE_GRID") || h->skip)
+    return LRS_OK;
+  const int n = d->batch_max;
+  std::vector<std::tuple<int, int, int>> plans;  // (ipt, th, grid)
+  std::vector<int> grids{h->sms};
+  if (h->use_w) {
+    const WconvParams& w = h->wp;
+    const long long wt = static_cast<long long>((n + 7) / 8) * w.bands * w.cbands * w.n_mt;
+    const int free_sms = h->sms - static_cast<int>(std::min<long long>(wt, h->sms));
+    if (free_sms >= 16) grids.push_back(free_sms);
+  }
+  for (int g : grids) {
+    const auto cand = core_candidates(h, d, g);
+    for (size_t i = 0; i < cand.size() && i < 4; ++i) plans.emplace_back(std::get<1>(cand[i]), std::get<2>(cand[i]), g);
+  }
+  if (plans.size() <= 1) return LRS_OK;
+  const size_t xb = static_cast<size_t>(n) * d->in_h * d->in_w * d->c_in * 2;
+  const size_t yb = static_cast<size_t>(n) * h->ho * h->wo * d->c_out * 2;
+  void *xs = nullptr, *ys = nullptr;
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  lrs_status st = LRS_OK;
+  const CoreParams keep = h->cp;
+  const uint32_t keep_smem = h->core_smem;
+  const int keep_grid = h->core_grid;
+  float best = 1e30f;
+  int bi = -1;
+  if (cudaMalloc(&xs, xb) != cudaSuccess || cudaMalloc(&ys, yb) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess || cudaEventCreate(&e0) != cudaSuccess ||
+      cudaEventCreate(&e1) != cudaSuccess || cudaMemsetAsync(xs, 0, xb, s) != cudaSuccess) {
+    st = fail(LRS_ERR_CUDA, "autotune: scratch allocation failed");
+  }
+  for (size_t i = 0; st == LRS_OK && i < plans.size(); ++i) {
+    apply_core_plan(h, d, std::get<0>(plans[i]), std::get<1>(plans[i]), std::get<2>(plans[i]));
+    for (int r = 0; r < 3 && st == LRS_OK; ++r) st = lrs_conv_forward(h, xs, ys, n, s);
+    if (st != LRS_OK) break;
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < 10 && st == LRS_OK; ++r) st = lrs_conv_forward(h, xs, ys, n, s);
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) != cudaSuccess) st = fail(LRS_ERR_CUDA, "autotune: %s", cudaGetErrorString(cudaGetLastError()));
+    float ms = 0.f;
+    if (st == LRS_OK) cudaEventElapsedTime(&ms, e0, e1);
+    if (getenv("LRS_VERBOSE"))
+      fprintf(stderr, "[lrs] autotune core ipt=%d th=%d grid=%d: %.2f us/forward\n", std::get<0>(plans[i]),
+              std::get<1>(plans[i]), std::get<2>(plans[i]), ms * 100.f);
+    if (st == LRS_OK && ms < best) {
+      best = ms;
+      bi = static_cast<int>(i);
+    }
+  }
+  if (st == LRS_OK && bi >= 0) {
+    apply_core_plan(h, d, std::get<0>(plans[bi]), std::get<1>(plans[bi]), std::get<2>(plans[bi]));
+  } else {
+    h->cp = keep;
+    h->core_smem = keep_smem;
+    h->core_grid = keep_grid;
+    h->cx_ptr = nullptr;
+  }
+  h->wx_ptr = nullptr;  // tensor maps cached for the scratch X
+  h->xmap_ptr = nullptr;
+  if (s) cudaStreamSynchronize(s);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (s) cudaStreamDestroy(s);
+  if (xs) cudaFree(xs);
+  if (ys) cudaFree(ys);
+  return st;
+}
+
 lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   if (!out) return fail(LRS_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
@@ -1392,7 +1533,8 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     if (e != cudaSuccess)
       return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
-  for (const void* fn : {reinterpret_cast<const void*>(&lrs_core_kernel), reinterpret_cast<const void*>(&lrs_tiny_kernel)}) {
+  for (const void* fn : {reinterpret_cast<const void*>(&lrs_core_kernel<4>), reinterpret_cast<const void*>(&lrs_core_kernel<2>),
+                         reinterpret_cast<const void*>(&lrs_core_kernel<1>), reinterpret_cast<const void*>(&lrs_tiny_kernel)}) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
@@ -1408,6 +1550,7 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
       if (e != cudaSuccess)
         return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
     }
+  if ((st = autotune_core(h, d)) != LRS_OK) return cleanup_fail(st);
   cudaSetDevice(prev);
   *out = h;
   return LRS_OK;
@@ -1472,11 +1615,13 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
     c.n = n;
     c.t2 = static_cast<__nv_bfloat16*>(h->t2);
     c.n_tiles = ((n + c.ipt - 1) / c.ipt) * c.bands;
-    const unsigned grid = static_cast<unsigned>(std::min(c.n_tiles, h->sms));
+    const unsigned grid = static_cast<unsigned>(std::min(c.n_tiles, h->core_grid));
     cudaEvent_t e1 = nullptr;
     if ((st = time_begin(h, 0, stream, &e1)) != LRS_OK) return st;
-    LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_core_kernel), dim3(grid), dim3(kCThreads), &c,
-                        h->core_smem, stream));
+    const void* kfn = c.g_kc == 64 ? reinterpret_cast<const void*>(&lrs_core_kernel<4>)
+                      : c.g_kc == 32 ? reinterpret_cast<const void*>(&lrs_core_kernel<2>)
+                                     : reinterpret_cast<const void*>(&lrs_core_kernel<1>);
+    LRS_CUDA(launch_pdl(kfn, dim3(grid), dim3(kCThreads), &c, h->core_smem, stream));
     if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
   }
   // a1

@@ -22,6 +22,19 @@
 // ipt images.  A T2 MMA row m reads T1 rows m + tap offset, so M blocks run across
 // the image boundaries; rows whose window position is no output are discarded.
 //
+// T1 window layout: when R1p is a multiple of 64 it is K-major SWIZZLE_128B (64-rank
+// chunks of 128-B rows).  The hardware applies the swizzle to absolute shared-memory
+// address bits, so a start row that is not a multiple of the 8-row atom is a legal
+// operand (tools/mma_baseoff.cu: exact at every row offset with base offset 0), and
+// an N = 64 MMA then costs 48 instead of 88 cycles (SWIZZLE_NONE, the fallback for
+// other ranks; profiles/r01_mma_layout_swizzle_none.log, r01_mma_baseoff.log).
+//
+// Shared memory: an X ring (one slot = a 64-channel X box + its U_in chunk; the last
+// M block of a box reads past its end into the next slot -- garbage rows whose T1 and
+// T2 rows are discarded), a G ring of separate small slots (when all k*k*R1p/g_kc
+// chunks fit, G is loaded once per CTA, before the PDL wait: weights do not depend on
+// the previous kernel), and the T1 window.
+//
 // Persistent CTAs walk the tiles.  Warps: 0 TMA producer, 1 MMA issuer,
 // 2..9 epilogue (T1 restage, T2 store); TMEM holds T1 and T2 of a tile, double
 // buffered when it fits so the T2 epilogue of tile k overlaps tile k+1.  T2 reuses
@@ -32,10 +45,11 @@
 namespace lrs {
 
 constexpr int kCThreads = 320;
-constexpr int kCMaxSlots = 8;
+constexpr int kCMaxX = 8;   // X ring slots
+constexpr int kCMaxG = 32;  // G ring slots
 
 struct CoreParams {
-  CUtensorMap tmX;  // X 4-D (C, W, H, N) bf16, box {64, wc, wr, 1}, SW128
+  CUtensorMap tmX;  // X 4-D (C, W, H, N) bf16, box {64, wc, wr, ipt}, SW128
   CUtensorMap tmU;  // U_in^T [R1p][Cin] bf16, box {64, R1p}, SW128
   CUtensorMap tmG;  // G^T [R2p][taps * R1p] bf16, box {g_kc, R2p}, swizzle sw_g
   __nv_bfloat16* t2;  // [n * ho * wo][R2p]
@@ -49,15 +63,17 @@ struct CoreParams {
   int g_kc, n_gk;        // G K chunk (elements) and chunks per tap
   uint32_t sw_g;
   uint32_t x_bytes;      // one X box (ipt * wr * wc * 128 B)
-  uint32_t x_region;     // X part of a slot (nb1 * 16 KB)
+  uint32_t u_off;        // U_in chunk offset inside an X slot (x_bytes rounded up to 1 KB)
   uint32_t u_bytes, g_bytes;
-  uint32_t slot_bytes;
-  int ns;
-  uint32_t t1_rows;      // rows of the T1 window (LBO = t1_rows * 16 B)
+  uint32_t x_slot, g_slot;  // ring slot strides
+  int ns_x, ns_g;
+  int g_res;             // 1: every G chunk has its own slot, loaded once per CTA
+  int t1_sw128;          // 1: T1 window K-major SW128 (R1p % 64 == 0), 0: SWIZZLE_NONE
+  uint32_t t1_rows;      // rows of the T1 window (multiple of 8)
   uint32_t acc_cols;     // TMEM columns per buffer: max(nb1 * R1p, nb2 * R2p)
   int nacc;
   uint32_t tmem_cols;
-  uint32_t off_t1, off_bar;
+  uint32_t off_g, off_t1, off_bar;
   unsigned long long* trace;  // optional globaltimer stamps (LRS_WCONV_DEBUG builds, tools/ctrace.py)
 };
 
@@ -72,6 +88,14 @@ struct CoreParams {
   } while (0)
 #endif
 
+// Byte offset of the 16-byte piece holding ranks [kel, kel + 8) of T1 window row `row`.
+__device__ __forceinline__ uint32_t t1_piece(const CoreParams& p, uint32_t row, uint32_t kel) {
+  return p.t1_sw128 ? (kel >> 6) * p.t1_rows * 128u + row * 128u + ((((kel & 63u) >> 3) ^ (row & 7u)) << 4)
+                    : ((kel >> 3) * p.t1_rows + row) * 16u;
+}
+
+// GS = K steps of 16 per G chunk (g_kc / 16: 4, 2 or 1)
+template <int GS>
 __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_constant__ CoreParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -79,20 +103,26 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
-  uint64_t* full = bars;                        // [ns]
-  uint64_t* empty = bars + kCMaxSlots;          // [ns]
-  uint64_t* t1_full = bars + 2 * kCMaxSlots;    // [2] MMA -> epilogue: T1 accumulated
+  uint64_t* full_x = bars;                      // [ns_x]
+  uint64_t* empty_x = full_x + kCMaxX;          // [ns_x]
+  uint64_t* full_g = empty_x + kCMaxX;          // [ns_g]
+  uint64_t* empty_g = full_g + kCMaxG;          // [ns_g]
+  uint64_t* t1_full = empty_g + kCMaxG;         // [2] MMA -> epilogue: T1 accumulated
   uint64_t* t2_full = t1_full + 2;              // [2] MMA -> epilogue: T2 accumulated
   uint64_t* acc_empty = t2_full + 2;            // [2] epilogue -> MMA (8 arrivals)
   uint64_t* t1s_full = acc_empty + 2;           // epilogue -> MMA: T1 window restaged (8 arrivals)
   uint64_t* t1w_empty = t1s_full + 1;           // MMA -> epilogue: core MMAs done reading the window
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t1w_empty + 1);
-  const int taps = p.kh * p.kw;
+  const int n_g = p.kh * p.kw * p.n_gk;         // G chunks per tile
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < p.ns; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+    for (int i = 0; i < p.ns_x; ++i) {
+      mbar_init(&full_x[i], 1);
+      mbar_init(&empty_x[i], 1);
+    }
+    for (int i = 0; i < p.ns_g; ++i) {
+      mbar_init(&full_g[i], 1);
+      mbar_init(&empty_g[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&t1_full[i], 1);
@@ -112,6 +142,14 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   CTRACE(p, threadIdx.x == 0 && blockIdx.x < 2048, 9000 + 2 * blockIdx.x);
+  // a resident G is requested before the PDL wait (weights do not depend on the previous kernel)
+  if (threadIdx.x == 0 && p.g_res) {
+    for (int j = 0; j < n_g; ++j) {
+      const int t = j / p.n_gk, gk = j - t * p.n_gk;
+      mbar_arrive_expect_tx(&full_g[j], p.g_bytes);
+      tma_load_2d(smem + p.off_g + j * p.g_slot, &p.tmG, &full_g[j], t * p.r1p + gk * p.g_kc, 0);
+    }
+  }
   pdl_wait();  // the previous kernel's output is visible from here on
   pdl_launch_dependents();  // only after the wait: every kernel before us is then complete
   CTRACE(p, threadIdx.x == 0 && blockIdx.x == 0, 8190);
@@ -119,37 +157,49 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
-      int it = 0;
+      int ix = 0, ig = 0;
       for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
         const int g = tile / p.bands, ho0 = (tile - g * p.bands) * p.th;
-        for (int c = 0; c < p.n_ck; ++c, ++it) {
-          const int s = it % p.ns;
-          if (it >= p.ns) mbar_wait(&empty[s], ((it / p.ns) - 1) & 1);
+        for (int c = 0; c < p.n_ck; ++c, ++ix) {
+          const int s = ix % p.ns_x;
+          if (ix >= p.ns_x) mbar_wait(&empty_x[s], ((ix / p.ns_x) - 1) & 1);
           CTRACE(p, blockIdx.x == 0 && c == 0 && (tile - blockIdx.x) / gridDim.x < 4,
                  8200 + 10 * ((tile - blockIdx.x) / gridDim.x) + 1);
-          uint8_t* dst = smem + s * p.slot_bytes;
-          mbar_arrive_expect_tx(&full[s], p.x_bytes + p.u_bytes);
-          tma_load_4d(dst, &p.tmX, &full[s], c * 64, -p.pw, ho0 - p.ph, g * p.ipt);
-          tma_load_2d(dst + p.x_region, &p.tmU, &full[s], c * 64, 0);
+          uint8_t* dst = smem + s * p.x_slot;
+          mbar_arrive_expect_tx(&full_x[s], p.x_bytes + p.u_bytes);
+          tma_load_4d(dst, &p.tmX, &full_x[s], c * 64, -p.pw, ho0 - p.ph, g * p.ipt);
+          tma_load_2d(dst + p.u_off, &p.tmU, &full_x[s], c * 64, 0);
         }
-        for (int t = 0; t < taps; ++t)
-          for (int gk = 0; gk < p.n_gk; ++gk, ++it) {
-            const int s = it % p.ns;
-            if (it >= p.ns) mbar_wait(&empty[s], ((it / p.ns) - 1) & 1);
-            mbar_arrive_expect_tx(&full[s], p.g_bytes);
-            tma_load_2d(smem + s * p.slot_bytes + p.x_region, &p.tmG, &full[s], t * p.r1p + gk * p.g_kc, 0);
+        if (!p.g_res)
+          for (int j = 0; j < n_g; ++j, ++ig) {
+            const int s = ig % p.ns_g;
+            if (ig >= p.ns_g) mbar_wait(&empty_g[s], ((ig / p.ns_g) - 1) & 1);
+            const int t = j / p.n_gk, gk = j - t * p.n_gk;
+            mbar_arrive_expect_tx(&full_g[s], p.g_bytes);
+            tma_load_2d(smem + p.off_g + s * p.g_slot, &p.tmG, &full_g[s], t * p.r1p + gk * p.g_kc, 0);
           }
       }
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
+    // Descriptors are linear in the shared-memory address (start >> 4 in the low 14
+    // bits), so every operand is a base descriptor plus a precomputed offset: the issue
+    // loop is adds and MMAs (address arithmetic per MMA made it issue-bound).
     const uint32_t idesc1 = umma_idesc(1u, static_cast<uint32_t>(p.r1p), 128u);
     const uint32_t idesc2 = umma_idesc(1u, static_cast<uint32_t>(p.r2p), 128u);
     const uint32_t base = smem_u32(smem);
     const uint32_t t1w = smem_u32(smem + p.off_t1);
     const uint32_t lbo = p.t1_rows * 16u;
-    const int gsteps = p.g_kc / 16;
-    int it = 0, k = 0;
+    const uint64_t xd0 = umma_desc(base, 128);
+    const uint64_t ud0 = umma_desc(base + p.u_off, 128);
+    const uint64_t gd0 = umma_desc(base + p.off_g, p.sw_g);
+    const uint64_t t1d0 = p.t1_sw128 ? umma_desc(t1w, 128) : umma_desc_noswz(t1w, lbo, 128u);
+    // T1 window: descriptor units (16 B) per window row, per G chunk of g_kc ranks, per K step of 16
+    const uint32_t a_rs = p.t1_sw128 ? 8u : 1u;
+    const uint32_t a_gs = p.t1_sw128 ? p.t1_rows * 8u : static_cast<uint32_t>(p.g_kc / 8) * (lbo >> 4);
+    const uint32_t a_ks = p.t1_sw128 ? 2u : 2u * (lbo >> 4);
+    const uint32_t x16 = p.x_slot >> 4, g16 = p.g_slot >> 4;
+    int ix = 0, ig = 0, k = 0;
     for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++k) {
       const int b = p.nacc == 2 ? (k & 1) : 0;
       const int use = p.nacc == 2 ? (k >> 1) : k;
@@ -160,19 +210,21 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * p.acc_cols;
       const uint32_t t2c = acc0;  // T2 overwrites T1's columns (restaged already)
       // ---- a1: T1 (window rows) = X window . U_in, K = Cin in 64-channel chunks
-      for (int c = 0; c < p.n_ck; ++c, ++it) {
-        const int s = it % p.ns;
-        mbar_wait(&full[s], (it / p.ns) & 1);
+      for (int c = 0; c < p.n_ck; ++c, ++ix) {
+        const int s = ix % p.ns_x;
+        mbar_wait(&full_x[s], (ix / p.ns_x) & 1);
         tc_fence_after();
         CTRACE(p, blockIdx.x == 0 && lane == 0 && k < 4 && c == 0, 8200 + 10 * k + 2);
-        const uint32_t xa = base + s * p.slot_bytes;
+        const uint64_t xd = xd0 + static_cast<uint32_t>(s) * x16;
+        const uint64_t ud = ud0 + static_cast<uint32_t>(s) * x16;
         if (elect_one()) {
-          for (int b1 = 0; b1 < p.nb1; ++b1)
+          for (int b1 = 0; b1 < p.nb1; ++b1) {
+            const uint32_t d = acc0 + static_cast<uint32_t>(b1 * p.r1p);
+            const uint64_t xb = xd + static_cast<uint32_t>(b1) * 1024u;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_bf16(acc0 + static_cast<uint32_t>(b1 * p.r1p), umma_desc(xa + b1 * 16384u + kk * 32u, 128),
-                       umma_desc(xa + p.x_region + kk * 32u, 128), idesc1, (c > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&empty[s]);
+            for (int kk = 0; kk < 4; ++kk) mma_bf16(d, xb + 2 * kk, ud + 2 * kk, idesc1, (c > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty_x[s]);
           if (c == p.n_ck - 1) mma_commit(&t1_full[b]);
         }
         __syncwarp();
@@ -182,27 +234,72 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       mbar_wait(t1s_full, k & 1);
       tc_fence_after();
       CTRACE(p, blockIdx.x == 0 && lane == 0 && k < 4, 8200 + 10 * k + 6);
-      // ---- a2: T2 = sum over taps of (window shifted by y*wc + x) . G[tap]
-      for (int t = 0; t < taps; ++t) {
-        const int ty = t / p.kw, tx = t - ty * p.kw;
-        const uint32_t tap_off = static_cast<uint32_t>(ty * p.wc + tx) * 16u;
-        for (int gk = 0; gk < p.n_gk; ++gk, ++it) {
-          const int s = it % p.ns;
-          mbar_wait(&full[s], (it / p.ns) & 1);
-          tc_fence_after();
-          const uint32_t ga = base + s * p.slot_bytes + p.x_region;
-          if (elect_one()) {
-            for (int b2 = 0; b2 < p.nb2; ++b2)
-              for (int kk = 0; kk < gsteps; ++kk) {
-                const uint32_t kslice = static_cast<uint32_t>((gk * p.g_kc) / 8 + 2 * kk);
-                mma_bf16(t2c + static_cast<uint32_t>(b2 * p.r2p),
-                         umma_desc_noswz(t1w + static_cast<uint32_t>(b2 * 128) * 16u + tap_off + kslice * lbo, lbo,
-                                         128u),
-                         umma_desc(ga + kk * 32u, p.sw_g), idesc2, (t > 0 || gk > 0 || kk > 0) ? 1u : 0u);
+      // ---- a2: T2 = sum over taps of (window shifted by y*wc + x rows) . G[tap]
+      // Operand descriptors advance by running offsets: next G chunk of the tap (+a_gs),
+      // next tap column (+a_rs), next tap row (+(wc - kw) rows more).
+      const uint32_t a_tap = a_rs - static_cast<uint32_t>(p.n_gk - 1) * a_gs;
+      const uint32_t a_row = static_cast<uint32_t>(p.wc - p.kw) * a_rs;
+      const uint32_t a_b2 = 128u * a_rs;
+      if (p.g_res) {
+        // resident G: one wait per chunk for the CTA's first tile, then one issue block
+        if (k == 0)
+          for (int j = 0; j < n_g; ++j) mbar_wait(&full_g[j], 0);
+        tc_fence_after();
+        if (elect_one()) {
+          uint64_t bj = gd0;
+          uint32_t aj = 0;  // window offset in 16-B units (uint32 wrap-around of the steps cancels)
+          int gk = 0, tx = 0;
+          for (int j = 0; j < n_g; ++j) {
+            uint64_t ab = t1d0 + aj;
+            uint32_t d = t2c;
+            for (int b2 = 0; b2 < p.nb2; ++b2, ab += a_b2, d += static_cast<uint32_t>(p.r2p)) {
+#pragma unroll
+              for (int kk = 0; kk < GS; ++kk)
+                mma_bf16(d, ab + kk * a_ks, bj + 2 * kk, idesc2, (j > 0 || kk > 0) ? 1u : 0u);
+            }
+            bj += g16;
+            if (++gk == p.n_gk) {
+              gk = 0;
+              aj += a_tap;
+              if (++tx == p.kw) {
+                tx = 0;
+                aj += a_row;
               }
-            mma_commit(&empty[s]);
+            } else {
+              aj += a_gs;
+            }
+          }
+        }
+        __syncwarp();
+      } else {
+        uint32_t aj = 0;
+        int gk = 0, tx = 0;
+        for (int j = 0; j < n_g; ++j, ++ig) {
+          const int s = ig % p.ns_g;
+          mbar_wait(&full_g[s], static_cast<uint32_t>((ig / p.ns_g) & 1));
+          tc_fence_after();
+          const uint64_t bj = gd0 + static_cast<uint32_t>(s) * g16;
+          if (elect_one()) {
+            uint64_t ab = t1d0 + aj;
+            uint32_t d = t2c;
+            for (int b2 = 0; b2 < p.nb2; ++b2, ab += a_b2, d += static_cast<uint32_t>(p.r2p)) {
+#pragma unroll
+              for (int kk = 0; kk < GS; ++kk)
+                mma_bf16(d, ab + kk * a_ks, bj + 2 * kk, idesc2, (j > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(&empty_g[s]);
           }
           __syncwarp();
+          if (++gk == p.n_gk) {
+            gk = 0;
+            aj += a_tap;
+            if (++tx == p.kw) {
+              tx = 0;
+              aj += a_row;
+            }
+          } else {
+            aj += a_gs;
+          }
         }
       }
       if (elect_one()) {
@@ -224,7 +321,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       const int b = p.nacc == 2 ? (k & 1) : 0;
       const int use = p.nacc == 2 ? (k >> 1) : k;
       const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * p.acc_cols + (static_cast<uint32_t>(q4 * 32) << 16);
-      // ---- restage T1 (fp32 TMEM) as bf16 into the SWIZZLE_NONE window
+      // ---- restage T1 (fp32 TMEM) as bf16 into the window (rows >= t1_rows are never read)
       mbar_wait_sleep(&t1_full[b], use & 1);
       if (k > 0) mbar_wait(t1w_empty, (k - 1) & 1);
       tc_fence_after();
@@ -233,7 +330,8 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         const uint32_t row = static_cast<uint32_t>(b1 * 128 + q4 * 32 + lane);
         for (int c0 = ehalf * 16; c0 < p.r1p; c0 += 32) {
           float v[16];
-          tmem_ld16(acc0 + static_cast<uint32_t>(b1 * p.r1p + c0), v);
+          tmem_ld16(acc0 + static_cast<uint32_t>(b1 * p.r1p + c0), v);  // warp-collective: all lanes
+          if (row >= p.t1_rows) continue;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             uint4 u;
@@ -243,8 +341,8 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
               __nv_bfloat162 bb = __floats2bfloat162_rn(v[8 * h + 2 * i], v[8 * h + 2 * i + 1]);
               w[i] = *reinterpret_cast<uint32_t*>(&bb);
             }
-            const uint32_t kslice = static_cast<uint32_t>(c0 / 8 + h);
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(t1w + (kslice * p.t1_rows + row) * 16u),
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             t1w + t1_piece(p, row, static_cast<uint32_t>(c0 + 8 * h))),
                          "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
                          : "memory");
           }

@@ -84,3 +84,33 @@ def test_stride_two_keeps_two_kernels():
     layer = make(inp)
     assert not layer.core_fused
     assert rel(fwd(layer, inp), oracle(inp)) <= 2e-2
+
+
+PLAN_GEOMS = {  # ragged batches at the C2 / C3 layer shapes
+    "c2": (9, 14, 14, 256, 256, 3, 1, 64, 64, 0.02),
+    "c3": (10, 7, 7, 512, 512, 3, 1, 128, 128, 0.05),
+}
+PLANS = [  # planner overrides (read at create): tile shape, persistent grid, T1 window layout
+    ("c2", {"LRS_CORE_IPT": "2", "LRS_CORE_TH": "7"}),
+    ("c2", {"LRS_CORE_IPT": "1", "LRS_CORE_TH": "7", "LRS_CORE_GRID": "5"}),   # several tiles per CTA
+    ("c2", {"LRS_CORE_IPT": "4", "LRS_CORE_TH": "2", "LRS_CORE_GRID": "3"}),
+    ("c2", {"LRS_CORE_T1_NOSWZ": "1"}),                                     # SWIZZLE_NONE T1 window
+    ("c3", {"LRS_CORE_GRID": "7"}),
+    ("c3", {"LRS_CORE_IPT": "2", "LRS_CORE_TH": "3", "LRS_CORE_GRID": "4"}),
+    ("c3", {"LRS_CORE_IPT": "1", "LRS_CORE_TH": "7", "LRS_CORE_T1_NOSWZ": "1"}),
+]
+
+
+@pytest.mark.parametrize("geom,env", PLANS)
+def test_core_plans_bitwise_equal_to_two_kernel_path(geom, env):
+    """Every tile shape / grid / window layout the planner can pick computes the same
+    bits as the two-kernel path (same bf16 T1, same products, same order)."""
+    n, h, w, cin, cout, k, p, r1, r2, dens = PLAN_GEOMS[geom]
+    cfg = workloads.LayerConfig("t", n, h, w, cin, cout, k, 1, p, r1, r2, dens, "bf16", seed=8)
+    inp = workloads.generate(cfg)
+    fused = make(inp, env)
+    split = make(inp, {"LRS_NO_CORE": "1"})
+    assert fused.core_fused
+    yf, ys = fwd(fused, inp), fwd(split, inp)
+    assert np.array_equal(yf, ys)
+    assert rel(yf, oracle(inp)) <= 2e-2

@@ -4,7 +4,7 @@ and the step is timed graph-replayed over rotating X/Y sets (L2 defeated), once 
 the whole layer and once with the expansion + sparse kernel skipped (LRS_SKIP=4), which
 leaves the core kernel alone.  Timing experiment only.
 
-usage: python tools/core_sweep.py [config] [ipt,th ipt,th ...]
+usage: python tools/core_sweep.py [config] [ipt,th[,grid] ...]
 """
 import math
 import os
@@ -69,15 +69,18 @@ def main():
         [(i, t) for i in (1, 2, 4, 8) for t in range(1, cfg.out_h + 1)]
     print(f"{name}: default full {step_us(inp, {}):.2f} us, core only {step_us(inp, {'LRS_SKIP': 4}):.2f} us",
           flush=True)
-    for ipt, th in combos:
+    for combo in combos:
+        ipt, th = combo[0], combo[1]
         env = {"LRS_CORE_IPT": ipt, "LRS_CORE_TH": th}
+        if len(combo) > 2:
+            env["LRS_CORE_GRID"] = combo[2]
         try:
             full = step_us(inp, env)
             core = step_us(inp, dict(env, LRS_SKIP=4))
         except LrsError as e:
-            print(f"ipt={ipt} th={th}: {e}")
+            print(f"{combo}: {e}")
             continue
-        print(f"ipt={ipt} th={th}: full {full:.2f} us  core-only {core:.2f} us", flush=True)
+        print(f"ipt,th,grid={combo}: full {full:.2f} us  core-only {core:.2f} us", flush=True)
 
 
 if __name__ == "__main__":
