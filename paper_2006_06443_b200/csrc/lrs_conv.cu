@@ -1037,6 +1037,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   }
   WconvParams& w = h->wp;
   memset(&w, 0, sizeof(w));
+  if (const char* e = getenv("LRS_WCONV_DBG")) w.dbg = atoi(e);  // experiment bits (LRS_WCONV_DEBUG builds only)
   w.img_sp = static_cast<const uint8_t*>(h->w_as);
   w.img_e = static_cast<const uint8_t*>(h->w_e);
   w.img_dense = static_cast<const uint8_t*>(h->w_dense_img);

@@ -182,6 +182,10 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
+    // ONE elected thread runs the whole loop (its mbarrier waits included): an elect +
+    // reconvergence per item costs ~240 cycles of issue (tools/mma_seq.cu: 108 vs 48
+    // cycles per N = 64 MMA), more than the MMAs it feeds.
+    if (elect_one()) {
     // Descriptors are linear in the shared-memory address (start >> 4 in the low 14
     // bits), so every operand is a base descriptor plus a precomputed offset: the issue
     // loop is adds and MMAs (address arithmetic per MMA made it issue-bound).
@@ -214,10 +218,10 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         const int s = ix % p.ns_x;
         mbar_wait(&full_x[s], (ix / p.ns_x) & 1);
         tc_fence_after();
-        CTRACE(p, blockIdx.x == 0 && lane == 0 && k < 4 && c == 0, 8200 + 10 * k + 2);
+        CTRACE(p, blockIdx.x == 0 && k < 4 && c == 0, 8200 + 10 * k + 2);
         const uint64_t xd = xd0 + static_cast<uint32_t>(s) * x16;
         const uint64_t ud = ud0 + static_cast<uint32_t>(s) * x16;
-        if (elect_one()) {
+        {
           for (int b1 = 0; b1 < p.nb1; ++b1) {
             const uint32_t d = acc0 + static_cast<uint32_t>(b1 * p.r1p);
             const uint64_t xb = xd + static_cast<uint32_t>(b1) * 1024u;
@@ -227,13 +231,12 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
           mma_commit(&empty_x[s]);
           if (c == p.n_ck - 1) mma_commit(&t1_full[b]);
         }
-        __syncwarp();
       }
-      CTRACE(p, blockIdx.x == 0 && lane == 0 && k < 4, 8200 + 10 * k + 3);
+      CTRACE(p, blockIdx.x == 0 && k < 4, 8200 + 10 * k + 3);
       // ---- wait for the bf16 T1 window in shared memory
       mbar_wait(t1s_full, k & 1);
       tc_fence_after();
-      CTRACE(p, blockIdx.x == 0 && lane == 0 && k < 4, 8200 + 10 * k + 6);
+      CTRACE(p, blockIdx.x == 0 && k < 4, 8200 + 10 * k + 6);
       // ---- a2: T2 = sum over taps of (window shifted by y*wc + x rows) . G[tap]
       // Operand descriptors advance by running offsets: next G chunk of the tap (+a_gs),
       // next tap column (+a_rs), next tap row (+(wc - kw) rows more).
@@ -245,7 +248,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         if (k == 0)
           for (int j = 0; j < n_g; ++j) mbar_wait(&full_g[j], 0);
         tc_fence_after();
-        if (elect_one()) {
+        {
           uint64_t bj = gd0;
           uint32_t aj = 0;  // window offset in 16-B units (uint32 wrap-around of the steps cancels)
           int gk = 0, tx = 0;
@@ -270,7 +273,6 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
             }
           }
         }
-        __syncwarp();
       } else {
         uint32_t aj = 0;
         int gk = 0, tx = 0;
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
           mbar_wait(&full_g[s], static_cast<uint32_t>((ig / p.ns_g) & 1));
           tc_fence_after();
           const uint64_t bj = gd0 + static_cast<uint32_t>(s) * g16;
-          if (elect_one()) {
+          {
             uint64_t ab = t1d0 + aj;
             uint32_t d = t2c;
             for (int b2 = 0; b2 < p.nb2; ++b2, ab += a_b2, d += static_cast<uint32_t>(p.r2p)) {
@@ -289,7 +291,6 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
             }
             mma_commit(&empty_g[s]);
           }
-          __syncwarp();
           if (++gk == p.n_gk) {
             gk = 0;
             aj += a_tap;
@@ -302,13 +303,14 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
           }
         }
       }
-      if (elect_one()) {
+      {
         mma_commit(&t2_full[b]);
         mma_commit(t1w_empty);
       }
-      __syncwarp();
-      CTRACE(p, blockIdx.x == 0 && lane == 0 && k < 4, 8200 + 10 * k + 7);
+      CTRACE(p, blockIdx.x == 0 && k < 4, 8200 + 10 * k + 7);
     }
+    }
+    __syncwarp();
   } else {
     // -------------------------------------------------------------- epilogue
     const int q4 = warp & 3;            // TMEM lane quarter

@@ -300,8 +300,9 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
-    // The whole warp walks the loop (so the per-unit values stay warp-uniform
-    // and live in uniform registers); one elected lane issues each tcgen05 op.
+    // ONE elected thread runs the whole loop, its mbarrier waits included: an elect +
+    // warp reconvergence around every item cost ~240 cycles of issue each
+    // (tools/mma_seq.cu: 108 vs 48 cycles per N = 64 MMA), more than the MMAs it feeds.
     // Descriptors are linear in the start address (14-bit field of addr>>4),
     // so every per-unit descriptor is precomputed once and the inner loop
     // only adds byte offsets >> 4: the single-thread issue loop stays short.
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const int ksteps = static_cast<int>(p.sw_t / 32);
     int slot = 0, k = 0, buf = 0;
     uint32_t ph = 0, wph = 0;
+    if (elect_one()) {
     const bool contig = p.nwb == nwin;  // must match the producer's tile order
     const int t_begin = contig ? static_cast<int>(static_cast<long long>(blockIdx.x) * p.n_tiles / gridDim.x)
                                : static_cast<int>(blockIdx.x);
@@ -342,18 +344,18 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         tc_fence_after();
       }
       const uint32_t acc0 = static_cast<uint32_t>(b) * p.acc_cols;
-      if (WTRACE(p) && blockIdx.x == 0 && lane == 0 && k < 16) p.trace[100 + 4 * k] = gtimer();
+      if (WTRACE(p) && blockIdx.x == 0 && k < 16) p.trace[100 + 4 * k] = gtimer();
       for (int w = 0; w < nwin; ++w) {
-        if (WTRACE(p) && blockIdx.x == 0 && lane == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w] = gtimer();
+        if (WTRACE(p) && blockIdx.x == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w] = gtimer();
         mbar_wait(&win_full[buf], wph);
         tc_fence_after();
-        if (WTRACE(p) && blockIdx.x == 0 && lane == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w + 1] = gtimer();
+        if (WTRACE(p) && blockIdx.x == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w + 1] = gtimer();
         const uint32_t boff = static_cast<uint32_t>(buf) * win16;
         if (w >= p.n_xw) {  // dense window: the accumulator already holds the sparse term
           mbar_wait(&a_full[slot], ph);
           tc_fence_after();
           const uint64_t ab = ad_dense + slot * slot_a16;
-          if (elect_one()) {
+          {
 #pragma unroll
             for (int u = 0; u < NU; ++u) {
               {
@@ -364,7 +366,6 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             }
             mma_commit(&a_empty[slot]);
           }
-          __syncwarp();
           if (++slot == p.ns) { slot = 0; ph ^= 1u; }
         } else {
           // sparse items of this window: the producer tags each slot with the
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
               tapv[q] = (q == 0 ? info0 : ld_shared_u32(slot_info + 4u * (kWMaxBpi * slot + q))) & 0x0FFFFFFFu;
             const uint32_t et = tmem + p.e_col0 + 4u * static_cast<uint32_t>(p.bpi) * slot;
             const uint64_t ab = ad_sp + slot * slot_a16;
-            if (elect_one()) {
+            {
               // metadata of block pairs in one tcgen05.cp.128x256b (blocks 2 KB apart = LBO)
 #pragma unroll
               for (int bp = 0; bp < BPI; bp += 2)
@@ -407,20 +408,19 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
               if (WDBG(p, 512)) mbar_arrive(&a_empty[slot]);
               else mma_commit(&a_empty[slot]);
             }
-            __syncwarp();
             first = false;
             if (++slot == p.ns) { slot = 0; ph ^= 1u; }
             if (info0 >> 31) break;
           }
         }
-        if (elect_one()) mma_commit(&win_empty[buf]);
-        __syncwarp();
+        mma_commit(&win_empty[buf]);
         if (++buf == p.nwb) { buf = 0; wph ^= 1u; }
       }
-      if (elect_one()) mma_commit(&acc_full[b]);
-      __syncwarp();
-      if (WTRACE(p) && blockIdx.x == 0 && lane == 0 && k < 16) p.trace[100 + 4 * k + 1] = gtimer();
+      mma_commit(&acc_full[b]);
+      if (WTRACE(p) && blockIdx.x == 0 && k < 16) p.trace[100 + 4 * k + 1] = gtimer();
     }
+    }
+    __syncwarp();
   } else {
     // -------------------------------------------------------------- epilogue
     const int q4 = warp & 3;            // TMEM lane quarter
@@ -453,6 +453,11 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       if (WTRACE(p) && blockIdx.x == 0 && threadIdx.x == 64 && k < 16) p.trace[100 + 4 * k + 2] = gtimer();
       const uint32_t acc0 = static_cast<uint32_t>(b) * p.acc_cols;
       const int jw = tc.j0 + q4 * 32;  // first channel of this warp
+      // store side of the transpose: lane = (image lane/4, 8-channel part lane%4)
+      const int part = lane & 3, img8 = lane >> 2;
+      const int jch = jw + part * 8;
+      const bool lane_ok = tc.n0 + img8 < p.n && jch < p.cout;
+      __nv_bfloat16* ybase = y + (static_cast<long long>(lane_ok ? tc.n0 + img8 : 0) * p.ho * p.wo) * p.cout + jch;
       for (int u = 0; u < p.n_units; ++u) {
         const int pitch = p.u_pitch[u], nw = p.u_nw[u], un = p.u_n[u], rows = p.u_rows[u];
         const int r0 = p.u_r0[u], w0 = p.u_wo0[u], ucol = p.u_col[u], q0 = p.u_q0[u];
@@ -464,32 +469,41 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           {
             const int t1 = lane >> 2, mi = lane >> 3, mj = lane & 7;
             const bool epi = p.epi != nullptr || p.relu;
+            // all four TMEM loads in flight before one wait (each wait is a TMEM round trip)
+            uint32_t r[2][2][8];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              float2 sba = make_float2(1.f, 0.f), sbb = make_float2(1.f, 0.f);
-              if (epi) {
-                sba = out_epi_load(p.epi, min(jw + 16 * h + t1, p.cout - 1));
-                sbb = out_epi_load(p.epi, min(jw + 16 * h + t1 + 8, p.cout - 1));
-              }
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-              for (int cb = 0; cb < 2; ++cb) {
-                uint32_t r[8];
+              for (int cb = 0; cb < 2; ++cb)
                 tmem_ld_16x256b_x2(tmem + (static_cast<uint32_t>(q4 * 32 + 16 * h) << 16) + acc0 +
                                        static_cast<uint32_t>(ucol + c0 + 16 * cb),
-                                   r);
-                tmem_ld_wait();
+                                   r[h][cb]);
+            float2 sb[2][2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              sb[h][0] = sb[h][1] = make_float2(1.f, 0.f);
+              if (epi) {
+                sb[h][0] = out_epi_load(p.epi, min(jw + 16 * h + t1, p.cout - 1));
+                sb[h][1] = out_epi_load(p.epi, min(jw + 16 * h + t1 + 8, p.cout - 1));
+              }
+            }
+            tmem_ld_wait();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+              for (int cb = 0; cb < 2; ++cb) {
                 float f[8];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[i]);
+                for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[h][cb][i]);
                 if (epi) {
-                  f[0] = out_epi(f[0], sba, p.relu);
-                  f[1] = out_epi(f[1], sba, p.relu);
-                  f[4] = out_epi(f[4], sba, p.relu);
-                  f[5] = out_epi(f[5], sba, p.relu);
-                  f[2] = out_epi(f[2], sbb, p.relu);
-                  f[3] = out_epi(f[3], sbb, p.relu);
-                  f[6] = out_epi(f[6], sbb, p.relu);
-                  f[7] = out_epi(f[7], sbb, p.relu);
+                  f[0] = out_epi(f[0], sb[h][0], p.relu);
+                  f[1] = out_epi(f[1], sb[h][0], p.relu);
+                  f[4] = out_epi(f[4], sb[h][0], p.relu);
+                  f[5] = out_epi(f[5], sb[h][0], p.relu);
+                  f[2] = out_epi(f[2], sb[h][1], p.relu);
+                  f[3] = out_epi(f[3], sb[h][1], p.relu);
+                  f[6] = out_epi(f[6], sb[h][1], p.relu);
+                  f[7] = out_epi(f[7], sb[h][1], p.relu);
                 }
                 // scratch row (column col, 8-channel part) at col*64 + (part ^ ((col >> 1) & 3))*16:
                 // the 8 rows of one stmatrix phase land in 8 distinct 16-byte bank groups
@@ -501,21 +515,23 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             }
           }
           __syncwarp();
-          // lane l, pass q: column col = q*8 + l/4, channels 8*(l%4) .. +7
-          const int part = lane & 3;
-          const int jch = jw + part * 8;
+          // lane l, pass q: column col = q*8 + l/4 = output position q0 + c0/8 + q (warp-uniform,
+          // stepped without divisions) of image l/4, channels 8*(l%4) .. +7
+          {
+            const int qv0 = q0 + (c0 >> 3);
+            int rr = qv0 / pitch, cc = qv0 - rr * pitch;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int col = q * 8 + (lane >> 2);
-            const int cidx = c0 + col;
-            const uint4 val = lds_v4(scr + static_cast<uint32_t>(col * 64 + ((part ^ ((col >> 1) & 3)) * 16)));
-            if (cidx >= un) continue;
-            const int qv = q0 + (cidx >> 3), img = cidx & 7;
-            const int rr = qv / pitch, cc = qv - rr * pitch;
-            const int n = tc.n0 + img, ho = tc.ho0 + r0 + rr, wo = tc.wo0 + w0 + cc;
-            if (cc < nw && rr < rows && n < p.n && ho < p.ho && wo < p.wo && jch < p.cout)
-              *reinterpret_cast<uint4*>(y + ((static_cast<long long>(n) * p.ho + ho) * p.wo + wo) * p.cout + jch) =
-                  val;
+            for (int q = 0; q < 4; ++q) {
+              const int col = q * 8 + img8;
+              const uint4 val = lds_v4(scr + static_cast<uint32_t>(col * 64 + ((part ^ ((col >> 1) & 3)) * 16)));
+              const int ho = tc.ho0 + r0 + rr, wo = tc.wo0 + w0 + cc;
+              if (lane_ok && c0 + col < un && cc < nw && rr < rows && ho < p.ho && wo < p.wo)
+                *reinterpret_cast<uint4*>(ybase + (static_cast<long long>(ho) * p.wo + wo) * p.cout) = val;
+              if (++cc == pitch) {
+                cc = 0;
+                ++rr;
+              }
+            }
           }
           __syncwarp();
         }

@@ -4,7 +4,7 @@ and the step is timed graph-replayed over rotating X/Y sets (L2 defeated), once 
 the whole layer and once with the expansion + sparse kernel skipped (LRS_SKIP=4), which
 leaves the core kernel alone.  Timing experiment only.
 
-usage: python tools/core_sweep.py [config] [ipt,th[,grid] ...]
+usage: python tools/core_sweep.py [config] [ipt,th[,grid[,wconv_th]] ...]  (grid 0 = all SMs)
 """
 import math
 import os
@@ -72,8 +72,10 @@ def main():
     for combo in combos:
         ipt, th = combo[0], combo[1]
         env = {"LRS_CORE_IPT": ipt, "LRS_CORE_TH": th}
-        if len(combo) > 2:
+        if len(combo) > 2 and combo[2]:
             env["LRS_CORE_GRID"] = combo[2]
+        if len(combo) > 3:
+            env["LRS_WCONV_TH"] = combo[3]
         try:
             full = step_us(inp, env)
             core = step_us(inp, dict(env, LRS_SKIP=4))
