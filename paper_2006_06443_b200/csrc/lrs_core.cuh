@@ -323,30 +323,41 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       const int b = p.nacc == 2 ? (k & 1) : 0;
       const int use = p.nacc == 2 ? (k >> 1) : k;
       const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * p.acc_cols + (static_cast<uint32_t>(q4 * 32) << 16);
-      // ---- restage T1 (fp32 TMEM) as bf16 into the window (rows >= t1_rows are never read)
-      mbar_wait_sleep(&t1_full[b], use & 1);
-      if (k > 0) mbar_wait(t1w_empty, (k - 1) & 1);
+      // ---- restage T1 (fp32 TMEM) as bf16 into the window (rows >= t1_rows are never read).
+      // One thread polls (no sleep: this hand-off is on the tile's critical path), the other
+      // epilogue threads block in a named barrier; TMEM loads are issued in groups of up
+      // to four before one wait.
+      if (threadIdx.x == 64) {
+        mbar_wait(&t1_full[b], use & 1);
+        if (k > 0) mbar_wait(t1w_empty, (k - 1) & 1);
+      }
+      named_bar_sync(1, kCThreads - 64);
       tc_fence_after();
       CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 4);
       for (int b1 = 0; b1 < p.nb1; ++b1) {
         const uint32_t row = static_cast<uint32_t>(b1 * 128 + q4 * 32 + lane);
-        for (int c0 = ehalf * 16; c0 < p.r1p; c0 += 32) {
-          float v[16];
-          tmem_ld16(acc0 + static_cast<uint32_t>(b1 * p.r1p + c0), v);  // warp-collective: all lanes
+        for (int cg = ehalf * 16; cg < p.r1p; cg += 128) {
+          uint32_t v[4][16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (cg + 32 * i < p.r1p) tmem_ld16_nowait(acc0 + static_cast<uint32_t>(b1 * p.r1p + cg + 32 * i), v[i]);
+          tmem_ld_wait();
           if (row >= p.t1_rows) continue;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint4 u;
-            uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+          for (int i = 0; i < 4; ++i) {
+            if (cg + 32 * i >= p.r1p) break;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              __nv_bfloat162 bb = __floats2bfloat162_rn(v[8 * h + 2 * i], v[8 * h + 2 * i + 1]);
-              w[i] = *reinterpret_cast<uint32_t*>(&bb);
+            for (int h = 0; h < 2; ++h) {
+              uint4 u;
+              uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                w[e] = pack_bf16x2(__uint_as_float(v[i][8 * h + 2 * e]), __uint_as_float(v[i][8 * h + 2 * e + 1]));
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                               t1w + t1_piece(p, row, static_cast<uint32_t>(cg + 32 * i + 8 * h))),
+                           "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
+                           : "memory");
             }
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
-                             t1w + t1_piece(p, row, static_cast<uint32_t>(c0 + 8 * h))),
-                         "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
-                         : "memory");
           }
         }
       }
@@ -356,7 +367,8 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       if (lane == 0) mbar_arrive(t1s_full);
       CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 5);
       // ---- T2 (fp32 TMEM) -> bf16 rows of global T2
-      mbar_wait_sleep(&t2_full[b], use & 1);
+      if (threadIdx.x == 64) mbar_wait(&t2_full[b], use & 1);
+      named_bar_sync(1, kCThreads - 64);
       tc_fence_after();
       CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 8);
       for (int b2 = 0; b2 < p.nb2; ++b2) {
@@ -367,19 +379,22 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         const bool ok = wl < p.wo && hl < rows && img < p.ipt && n < p.n;
         __nv_bfloat16* dst =
             p.t2 + ((static_cast<long long>(ok ? n : 0) * p.ho + ho0 + (ok ? hl : 0)) * p.wo + (ok ? wl : 0)) * p.r2p;
-        for (int c0 = ehalf * 16; c0 < p.r2p; c0 += 32) {
-          float v[16];
-          tmem_ld16(acc0 + static_cast<uint32_t>(b2 * p.r2p + c0), v);
-          if (ok) {
+        for (int cg = ehalf * 16; cg < p.r2p; cg += 128) {
+          uint32_t v[4][16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (cg + 32 * i < p.r2p) tmem_ld16_nowait(acc0 + static_cast<uint32_t>(b2 * p.r2p + cg + 32 * i), v[i]);
+          tmem_ld_wait();
+          if (!ok) continue;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (cg + 32 * i >= p.r2p) break;
             uint4 u[2];
             uint32_t* w = reinterpret_cast<uint32_t*>(u);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              __nv_bfloat162 bb = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-              w[i] = *reinterpret_cast<uint32_t*>(&bb);
-            }
-            reinterpret_cast<uint4*>(dst + c0)[0] = u[0];
-            reinterpret_cast<uint4*>(dst + c0)[1] = u[1];
+            for (int e = 0; e < 8; ++e) w[e] = pack_bf16x2(__uint_as_float(v[i][2 * e]), __uint_as_float(v[i][2 * e + 1]));
+            reinterpret_cast<uint4*>(dst + cg + 32 * i)[0] = u[0];
+            reinterpret_cast<uint4*>(dst + cg + 32 * i)[1] = u[1];
           }
         }
       }
