@@ -420,25 +420,63 @@ lrs_status build_tiny(lrs_conv* h, const lrs_conv_desc* d) {
   const int ho = h->ho, wo = h->wo, sh = d->stride_h, sw = d->stride_w;
   const int r1 = d->rank_in, r2 = d->rank_out;
   const int r1p = round_up(r1, 4), r2p = round_up(r2, 4), taps = kh * kw;
-  const int wc = (wo - 1) * sw + kw;
   auto a16 = [](uint32_t b) { return (b + 15u) & ~15u; };
-  int th = 1;
-  for (; th <= ho; ++th)  // fewest rows per CTA that keep the grid within two waves
-    if (static_cast<long long>(d->batch_max) * ((ho + th - 1) / th) <= 2LL * h->sms) break;
-  if (th > ho) return LRS_OK;
-  const int wr = (th - 1) * sh + kh;
-  TinyParams& q = h->tp;
-  memset(&q, 0, sizeof(q));
-  const uint32_t xs = a16(static_cast<uint32_t>(cin) * wr * wc * 4);
-  const uint32_t t1 = a16(static_cast<uint32_t>(wr) * wc * r1p * 4);
-  const uint32_t t2 = a16(static_cast<uint32_t>(th) * wo * r2p * 4);
+  {  // small layers only: some row band height keeps whole-width CTAs within two waves
+    int th0 = 1;
+    while (th0 <= ho && static_cast<long long>(d->batch_max) * ((ho + th0 - 1) / th0) > 2LL * h->sms) ++th0;
+    if (th0 > ho) return LRS_OK;
+  }
+  // CTA = image x th output rows x tc output columns.  Pick the tile minimising waves x
+  // per-CTA FMAs (the halo is recomputed: a1 runs on the (th + k - 1) x (tc + k - 1)
+  // window); a CTA's stages are serial, so at batch 1 (C1) small tiles spread the layer
+  // over more SMs.
   const uint32_t us = a16(static_cast<uint32_t>(cin) * r1p * 4);
   const uint32_t gs = a16(static_cast<uint32_t>(taps) * r1p * r2p * 4);
   const uint32_t uo = a16(static_cast<uint32_t>(r2p) * cout * 4);
   const uint32_t rpb = a16(static_cast<uint32_t>(cout + 1) * 4);
   const uint32_t eb = a16(static_cast<uint32_t>(std::max<int64_t>(d->nnz, 1)) * 4);
-  const uint32_t total = xs + t1 + t2 + us + gs + uo + rpb + 2 * eb;
-  if (total > static_cast<uint32_t>(kMaxSmem) - 1024u || cin % 4 || cout % 4) return LRS_OK;
+  const uint32_t fixed_b = us + gs + uo + rpb + 2 * eb;
+  auto tile_bytes = [&](int th_, int tc_, uint32_t* xs_, uint32_t* t1_, uint32_t* t2_) {
+    const int wr_ = (th_ - 1) * sh + kh, wc_ = (tc_ - 1) * sw + kw;
+    *xs_ = a16(static_cast<uint32_t>(cin) * wr_ * wc_ * 4);
+    *t1_ = a16(static_cast<uint32_t>(wr_) * wc_ * r1p * 4);
+    *t2_ = a16(static_cast<uint32_t>(th_) * tc_ * r2p * 4);
+    return *xs_ + *t1_ + *t2_ + fixed_b;
+  };
+  const int cb_env = getenv("LRS_TINY_CB") ? atoi(getenv("LRS_TINY_CB")) : 0;  // planner experiments
+  double best = 1e300;
+  int th = 0, tcb = 0;
+  for (int th_ = 1; th_ <= ho; ++th_) {
+    for (int cb = 1; cb <= wo; ++cb) {
+      if (cb_env && cb != cb_env) continue;
+      const int tc_ = (wo + cb - 1) / cb;
+      if ((wo + tc_ - 1) / tc_ != cb) continue;
+      uint32_t xs_, t1_, t2_;
+      const uint32_t tot = tile_bytes(th_, tc_, &xs_, &t1_, &t2_);
+      if (tot > static_cast<uint32_t>(kMaxSmem) - 1024u) continue;
+      const long long ctas = static_cast<long long>(d->batch_max) * ((ho + th_ - 1) / th_) * cb;
+      const int per_sm = 1;  // 512 threads x ~96 registers: one CTA per SM
+      if (ctas > 2LL * h->sms * per_sm) continue;  // at most two waves
+      const long long waves = (ctas + static_cast<long long>(h->sms) * per_sm - 1) / (static_cast<long long>(h->sms) * per_sm);
+      const int wr_ = (th_ - 1) * sh + kh, wc_ = (tc_ - 1) * sw + kw;
+      const double fma = static_cast<double>(wr_) * wc_ * r1p * cin + static_cast<double>(th_) * tc_ * taps * r1p * r2p +
+                         static_cast<double>(th_) * tc_ * (static_cast<double>(r2p) * cout + static_cast<double>(d->nnz));
+      const double cost = static_cast<double>(waves) * (fma / kTyThreads + 1500.0);  // + per-CTA load latency
+      if (cost < best * 0.999) {
+        best = cost;
+        th = th_;
+        tcb = tc_;
+      }
+    }
+  }
+  if (!th) return LRS_OK;
+  const int wr = (th - 1) * sh + kh;
+  const int wc = (tcb - 1) * sw + kw;
+  TinyParams& q = h->tp;
+  memset(&q, 0, sizeof(q));
+  uint32_t xs, t1, t2;
+  const uint32_t total = tile_bytes(th, tcb, &xs, &t1, &t2);
+  if (cin % 4 || cout % 4) return LRS_OK;
   q.off_t1 = xs; q.off_t2 = xs + t1; q.off_u = xs + t1 + t2; q.off_g = q.off_u + us; q.off_uo = q.off_g + gs;
   q.off_rp = q.off_uo + uo; q.off_ec = q.off_rp + rpb; q.off_ev = q.off_ec + eb;
   q.nnz = static_cast<int>(d->nnz);
@@ -482,10 +520,12 @@ lrs_status build_tiny(lrs_conv* h, const lrs_conv_desc* d) {
   q.h = d->in_h; q.w = d->in_w; q.cin = cin; q.ho = ho; q.wo = wo; q.cout = cout;
   q.kh = kh; q.kw = kw; q.sh = sh; q.sw = sw; q.ph = d->pad_h; q.pw = d->pad_w;
   q.r1p = r1p; q.r2p = r2p; q.th = th; q.bands = (ho + th - 1) / th; q.wr = wr; q.wc = wc;
+  q.tc = tcb; q.cbands = (wo + tcb - 1) / tcb;
   h->tiny_smem = total;
   h->use_tiny = true;
   if (getenv("LRS_VERBOSE"))
-    fprintf(stderr, "[lrs] tiny: th=%d bands=%d wr=%d wc=%d smem=%u\n", th, q.bands, wr, wc, total);
+    fprintf(stderr, "[lrs] tiny: th=%d bands=%d tc=%d cbands=%d wr=%d wc=%d smem=%u\n", th, q.bands, tcb, q.cbands, wr,
+            wc, total);
   return LRS_OK;
 }
 
@@ -824,7 +864,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       // smem (window reuse across the CTA's consecutive M-tiles)
       const int cand[][2] = {{4, 3}, {4, 2}, {2, 4}, {2, 3}, {2, 2}};
       // (opt-in: measured slower on C4, 49.4 vs 45.7 us -- the window loads are not its bottleneck)
-      int want_all = (n_mt > 1 && n_tk + n_ck <= kWMaxWin && getenv("LRS_WCONV_REUSE")) ? 1 : 0;
+      int want_all = (n_mt > 1 && n_tk + (d->nnz > 0 ? n_ck / cpw : 0) <= kWMaxWin && getenv("LRS_WCONV_REUSE")) ? 1 : 0;
       for (int pass = 0; pass < 2; ++pass) {
       const bool need_all = pass == 0 && want_all;
       if (pass == 1 && !want_all) break;
@@ -857,7 +897,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         while (nwb < 4 && (nwb + 1) * stride + fixed <= static_cast<uint32_t>(kMaxSmem)) ++nwb;
         // one buffer per window of a tile when they all fit: windows are then reused by
         // the CTA's next tile of the same images / band (the next M-tile)
-        const int nwin_t = n_tk + n_ck;
+        const int nwin_t = n_tk + (d->nnz > 0 ? n_ck / cpw : 0);  // the kernel's windows per tile
         const bool all_fit = static_cast<uint32_t>(nwin_t) * stride + fixed <= static_cast<uint32_t>(kMaxSmem);
         if (need_all && !all_fit) continue;
         if (need_all) nwb = nwin_t;
@@ -1592,7 +1632,7 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
     q.n = n;
     cudaEvent_t e1 = nullptr;
     if ((st = time_begin(h, 2, stream, &e1)) != LRS_OK) return st;
-    LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_tiny_kernel), dim3(static_cast<unsigned>(n * q.bands)),
+    LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_tiny_kernel), dim3(static_cast<unsigned>(n * q.bands * q.cbands)),
                         dim3(kTyThreads), &q, h->tiny_smem, stream));
     if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
     if (prev != h->device) cudaSetDevice(prev);

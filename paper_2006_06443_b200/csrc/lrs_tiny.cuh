@@ -8,7 +8,7 @@
 //
 // written to Y once (a5).  At batch 1 the tensor-core chain is three dependent launches
 // of a few CTAs each (~35 us of latency for ~14 M MAC); here a CTA owns one image x th
-// output rows x all columns x all output channels and runs the four stages back to back
+// output rows x tc output columns x all output channels and runs the four stages back to back
 // out of shared memory with exact fp32 FMAs (the north star's fp32 bar, no tf32 split).
 // T1 is recomputed on the window's halo rows (a1 is the cheapest stage at small ranks).
 #pragma once
@@ -34,6 +34,7 @@ struct TinyParams {
   int n, h, w, cin, ho, wo, cout;
   int kh, kw, sh, sw, ph, pw;
   int r1p, r2p, th, bands, wr, wc;
+  int tc, cbands;  // output columns per CTA and column bands (CTA = image x row band x column band)
   int nnz;
   uint32_t off_t1, off_t2, off_u, off_g, off_uo, off_rp, off_ec, off_ev;  // shared-memory carve-up (bytes)
   const float2* epi;  // per output channel (scale, bias) of the fused output epilogue, or NULL
@@ -44,15 +45,18 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
   extern __shared__ __align__(16) uint8_t sm[];
   float* xs = reinterpret_cast<float*>(sm);              // [cin][wr][wc]
   float* t1 = reinterpret_cast<float*>(sm + p.off_t1);   // [wr*wc][r1p]
-  float* t2 = reinterpret_cast<float*>(sm + p.off_t2);   // [th*wo][r2p]
+  float* t2 = reinterpret_cast<float*>(sm + p.off_t2);   // [th*tc][r2p]
   float* us = reinterpret_cast<float*>(sm + p.off_u);    // [cin][r1p]
   float* gs = reinterpret_cast<float*>(sm + p.off_g);    // [taps][r1p][r2p]
   float* uos = reinterpret_cast<float*>(sm + p.off_uo);  // [r2p][cout]
   int* rps = reinterpret_cast<int*>(sm + p.off_rp);      // CSR of S in shared memory
   int* ecs = reinterpret_cast<int*>(sm + p.off_ec);
   float* evs = reinterpret_cast<float*>(sm + p.off_ev);
-  const int n = blockIdx.x / p.bands, ho0 = (blockIdx.x - n * p.bands) * p.th;
+  const int cbi = blockIdx.x % p.cbands, rb = blockIdx.x / p.cbands;
+  const int n = rb / p.bands, ho0 = (rb - n * p.bands) * p.th;
+  const int wo0 = cbi * p.tc;
   const int rows = min(p.th, p.ho - ho0);
+  const int cols = min(p.tc, p.wo - wo0);
   const int taps = p.kh * p.kw;
   const int wrc = p.wr * p.wc;
   // weights first: they do not depend on the previous kernel
@@ -81,7 +85,7 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
         if (i < nit) {
           const int c4 = i / wrc, q = i - c4 * wrc;
           const int r = q / p.wc, col = q - r * p.wc;
-          const int hi = ho0 * p.sh - p.ph + r, wi = col - p.pw;
+          const int hi = ho0 * p.sh - p.ph + r, wi = wo0 * p.sw + col - p.pw;
           if (hi >= 0 && hi < p.h && wi >= 0 && wi < p.w)
             v[u] = __ldg(reinterpret_cast<const float4*>(p.x + ((static_cast<long long>(n) * p.h + hi) * p.w + wi) * p.cin) +
                          c4);
@@ -128,12 +132,12 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
   }
   __syncthreads();
   // ---- a2: T2 at the tile's output positions, 4 ranks per item
-  const int npos = rows * p.wo;
+  const int npos = rows * cols;
   {
     const int bg = p.r2p / 4;
     for (int it = threadIdx.x; it < npos * bg; it += kTyThreads) {
       const int pp = it / bg, b0 = 4 * (it - pp * bg);
-      const int hl = pp / p.wo, wl = pp - hl * p.wo;
+      const int hl = pp / cols, wl = pp - hl * cols;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int t = 0; t < taps; ++t) {
         const int ty = t / p.kw, tx = t - ty * p.kw;
@@ -165,7 +169,7 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         acc[k] = 0.f;
-        const int q = min(pp0 + k, pb - 1), hl = q / p.wo, wl = q - hl * p.wo;
+        const int q = min(pp0 + k, pb - 1), hl = q / cols, wl = q - hl * cols;
         qoff[k] = hl * p.sh * p.wc + wl * p.sw;
       }
       for (int b = 0; b < p.r2p; ++b) {
@@ -185,8 +189,8 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (pp0 + k < pb) {
-          const int q = pp0 + k, hl = q / p.wo, wl = q - hl * p.wo;
-          p.y[((static_cast<long long>(n) * p.ho + ho0 + hl) * p.wo + wl) * p.cout + j] =
+          const int q = pp0 + k, hl = q / cols, wl = q - hl * cols;
+          p.y[((static_cast<long long>(n) * p.ho + ho0 + hl) * p.wo + wo0 + wl) * p.cout + j] =
               out_epi(acc[k], out_epi_load(p.epi, j), p.relu);
         }
       }

@@ -76,3 +76,19 @@ def test_tiny_single_nonzero_is_bitwise():
     ref = np.zeros((n, h, w, cout), np.float32)
     ref[..., j] = v * xp[:, ty:ty + h, tx:tx + w, c]
     assert np.array_equal(y.astype(np.float32), ref)
+
+
+@pytest.mark.parametrize("geom,cb", [
+    ((1, 56, 56, 64, 64, 3, 1, 1, 16, 16, 0.01), 3),   # C1 shape, 3 column bands of 19/19/18
+    ((3, 10, 9, 24, 32, 3, 1, 0, 12, 16, 0.03), 2),    # pad 0, 7 output columns -> bands of 4 + 3
+    ((1, 28, 28, 32, 64, 3, 2, 1, 16, 8, 0.02), 4),    # stride 2, 14 output columns -> 4 bands
+])
+def test_tiny_column_bands_vs_oracle(geom, cb, monkeypatch):
+    """CTA = image x row band x column band (the window's halo columns recomputed)."""
+    monkeypatch.setenv("LRS_TINY_CB", str(cb))
+    n, h, w, cin, cout, k, s, p, r1, r2, dens = geom
+    cfg = workloads.LayerConfig("t", n, h, w, cin, cout, k, s, p, r1, r2, dens, "f32", seed=23)
+    inp = workloads.generate(cfg)
+    layer, y = run(inp)
+    assert layer.sparse_engine[0] == 3
+    check(y, oracle(inp))
