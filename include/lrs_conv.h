@@ -178,10 +178,12 @@ lrs_status lrs_conv_debug_buffer(const lrs_conv *h, int32_t which, const void **
  *      (register-blocked fp32 GEMM over a shared-memory tile of T2) and the
  *      sparse term (CSR gather over shared-memory windows of 4 images) and
  *      writes Y once (set LRS_F32_FUSED=1 at create to select engine 0);
- *   3  small fp32 Tucker-2 layers (weights + one output row band fit in shared
- *      memory, grid <= 2 waves, e.g. batch 1): the whole layer -- projection,
- *      core, expansion and sparse term -- in ONE SIMT kernel (LRS_NO_TINY=1 at
- *      create disables it).
+ *   3  small fp32 Tucker-2 or CP layers (weights + one tile's window fit in
+ *      shared memory, grid <= 2 waves, e.g. batch 1): the whole layer --
+ *      projection, core (dense k x k, or the CP form's two depthwise stages in
+ *      the paper's order), expansion and sparse term -- in ONE SIMT kernel, a
+ *      CTA per image x row band x column band (LRS_NO_TINY=1 at create
+ *      disables it).
  * For engine 1, *main_blocks / *residual_blocks (may be NULL) receive the
  * number of 128-row compressed blocks of each kind.
  */

@@ -415,7 +415,7 @@ inline uint16_t bf16_bits_rne(float f) {
 // output row's window fit in shared memory and the grid (images x row bands) is small --
 // the regime where the chain's three dependent launches are pure latency (C1).
 lrs_status build_tiny(lrs_conv* h, const lrs_conv_desc* d) {
-  if (!h->f32 || h->svd || h->cp_core || getenv("LRS_NO_TINY")) return LRS_OK;
+  if (!h->f32 || h->svd || getenv("LRS_NO_TINY")) return LRS_OK;
   const int cin = d->c_in, cout = d->c_out, kh = d->kernel_h, kw = d->kernel_w;
   const int ho = h->ho, wo = h->wo, sh = d->stride_h, sw = d->stride_w;
   const int r1 = d->rank_in, r2 = d->rank_out;
@@ -431,7 +431,8 @@ lrs_status build_tiny(lrs_conv* h, const lrs_conv_desc* d) {
   // window); a CTA's stages are serial, so at batch 1 (C1) small tiles spread the layer
   // over more SMs.
   const uint32_t us = a16(static_cast<uint32_t>(cin) * r1p * 4);
-  const uint32_t gs = a16(static_cast<uint32_t>(taps) * r1p * r2p * 4);
+  const bool cp = h->cp_core;
+  const uint32_t gs = a16(static_cast<uint32_t>(cp ? (kh + kw) * r1p : taps * r1p * r2p) * 4);
   const uint32_t uo = a16(static_cast<uint32_t>(r2p) * cout * 4);
   const uint32_t rpb = a16(static_cast<uint32_t>(cout + 1) * 4);
   const uint32_t eb = a16(static_cast<uint32_t>(std::max<int64_t>(d->nnz, 1)) * 4);
@@ -459,7 +460,8 @@ lrs_status build_tiny(lrs_conv* h, const lrs_conv_desc* d) {
       if (ctas > 2LL * h->sms * per_sm) continue;  // at most two waves
       const long long waves = (ctas + static_cast<long long>(h->sms) * per_sm - 1) / (static_cast<long long>(h->sms) * per_sm);
       const int wr_ = (th_ - 1) * sh + kh, wc_ = (tc_ - 1) * sw + kw;
-      const double fma = static_cast<double>(wr_) * wc_ * r1p * cin + static_cast<double>(th_) * tc_ * taps * r1p * r2p +
+      const double fma = static_cast<double>(wr_) * wc_ * r1p * cin +
+                         static_cast<double>(th_) * tc_ * (cp ? kw * (kh + 1) * r1p : taps * r1p * r2p) +
                          static_cast<double>(th_) * tc_ * (static_cast<double>(r2p) * cout + static_cast<double>(d->nnz));
       const double cost = static_cast<double>(waves) * (fma / kTyThreads + 1500.0);  // + per-CTA load latency
       if (cost < best * 0.999) {
@@ -481,14 +483,19 @@ lrs_status build_tiny(lrs_conv* h, const lrs_conv_desc* d) {
   q.off_rp = q.off_uo + uo; q.off_ec = q.off_rp + rpb; q.off_ev = q.off_ec + eb;
   q.nnz = static_cast<int>(d->nnz);
   const bool f32 = true;
-  std::vector<float> u(static_cast<size_t>(cin) * r1p, 0.f), g(static_cast<size_t>(taps) * r1p * r2p, 0.f),
-      o(static_cast<size_t>(r2p) * cout, 0.f);
+  std::vector<float> u(static_cast<size_t>(cin) * r1p, 0.f),
+      g(static_cast<size_t>(cp ? (kh + kw) * r1p : taps * r1p * r2p), 0.f), o(static_cast<size_t>(r2p) * cout, 0.f);
   for (int c = 0; c < cin; ++c)
     for (int a = 0; a < r1; ++a) u[static_cast<size_t>(c) * r1p + a] = host_val(d->u_in, (size_t)c * r1 + a, f32);
-  for (int a = 0; a < r1; ++a)
-    for (int b = 0; b < r2; ++b)
-      for (int t = 0; t < taps; ++t)
-        g[(static_cast<size_t>(t) * r1p + a) * r2p + b] = host_val(d->core, ((size_t)a * r2 + b) * taps + t, f32);
+  if (cp) {  // core = B [kh][R] then C [kw][R] (include/lrs_conv.h LRS_CORE_CP)
+    for (int y = 0; y < kh + kw; ++y)
+      for (int a = 0; a < r1; ++a) g[static_cast<size_t>(y) * r1p + a] = host_val(d->core, (size_t)y * r1 + a, f32);
+  } else {
+    for (int a = 0; a < r1; ++a)
+      for (int b = 0; b < r2; ++b)
+        for (int t = 0; t < taps; ++t)
+          g[(static_cast<size_t>(t) * r1p + a) * r2p + b] = host_val(d->core, ((size_t)a * r2 + b) * taps + t, f32);
+  }
   for (int b = 0; b < r2; ++b)
     for (int j = 0; j < cout; ++j) o[static_cast<size_t>(b) * cout + j] = host_val(d->u_out, (size_t)b * cout + j, f32);
   std::vector<int> rp(static_cast<size_t>(cout) + 1), ec(static_cast<size_t>(std::max<int64_t>(d->nnz, 1)), 0);
@@ -521,6 +528,7 @@ lrs_status build_tiny(lrs_conv* h, const lrs_conv_desc* d) {
   q.kh = kh; q.kw = kw; q.sh = sh; q.sw = sw; q.ph = d->pad_h; q.pw = d->pad_w;
   q.r1p = r1p; q.r2p = r2p; q.th = th; q.bands = (ho + th - 1) / th; q.wr = wr; q.wc = wc;
   q.tc = tcb; q.cbands = (wo + tcb - 1) / tcb;
+  q.cp = cp ? 1 : 0;
   h->tiny_smem = total;
   h->use_tiny = true;
   if (getenv("LRS_VERBOSE"))

@@ -35,6 +35,7 @@ struct TinyParams {
   int kh, kw, sh, sw, ph, pw;
   int r1p, r2p, th, bands, wr, wc;
   int tc, cbands;  // output columns per CTA and column bands (CTA = image x row band x column band)
+  int cp;          // 1: CP core: g holds B [kh][r1p] then C [kw][r1p], r2p == r1p
   int nnz;
   uint32_t off_t1, off_t2, off_u, off_g, off_uo, off_rp, off_ec, off_ev;  // shared-memory carve-up (bytes)
   const float2* epi;  // per output channel (scale, bias) of the fused output epilogue, or NULL
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
   float* t1 = reinterpret_cast<float*>(sm + p.off_t1);   // [wr*wc][r1p]
   float* t2 = reinterpret_cast<float*>(sm + p.off_t2);   // [th*tc][r2p]
   float* us = reinterpret_cast<float*>(sm + p.off_u);    // [cin][r1p]
-  float* gs = reinterpret_cast<float*>(sm + p.off_g);    // [taps][r1p][r2p]
+  float* gs = reinterpret_cast<float*>(sm + p.off_g);    // [taps][r1p][r2p], or CP: B [kh][r1p], C [kw][r1p]
   float* uos = reinterpret_cast<float*>(sm + p.off_uo);  // [r2p][cout]
   int* rps = reinterpret_cast<int*>(sm + p.off_rp);      // CSR of S in shared memory
   int* ecs = reinterpret_cast<int*>(sm + p.off_ec);
@@ -62,7 +63,8 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
   // weights first: they do not depend on the previous kernel
   for (int i = threadIdx.x; i < p.cin * p.r1p / 4; i += kTyThreads)
     reinterpret_cast<float4*>(us)[i] = __ldg(reinterpret_cast<const float4*>(p.uin) + i);
-  for (int i = threadIdx.x; i < taps * p.r1p * p.r2p / 4; i += kTyThreads)
+  const int gn = p.cp ? (p.kh + p.kw) * p.r1p : taps * p.r1p * p.r2p;
+  for (int i = threadIdx.x; i < gn / 4; i += kTyThreads)
     reinterpret_cast<float4*>(gs)[i] = __ldg(reinterpret_cast<const float4*>(p.g) + i);
   for (int i = threadIdx.x; i < p.r2p * p.cout / 4; i += kTyThreads)
     reinterpret_cast<float4*>(uos)[i] = __ldg(reinterpret_cast<const float4*>(p.uo) + i);
@@ -133,7 +135,33 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
   __syncthreads();
   // ---- a2: T2 at the tile's output positions, 4 ranks per item
   const int npos = rows * cols;
-  {
+  if (p.cp) {
+    // CP: the paper's two depthwise stages per rank channel, in its
+    // order: for each column tap x the k x 1 sum over y with B, then the 1 x k sum with C
+    const int bg = p.r1p / 4;
+    for (int it = threadIdx.x; it < npos * bg; it += kTyThreads) {
+      const int pp = it / bg, a0 = 4 * (it - pp * bg);
+      const int hl = pp / cols, wl = pp - hl * cols;
+      float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int x = 0; x < p.kw; ++x) {
+        float4 yb = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int y = 0; y < p.kh; ++y) {
+          const float4 tv = *reinterpret_cast<const float4*>(t1 + ((hl * p.sh + y) * p.wc + wl * p.sw + x) * p.r1p + a0);
+          const float4 bv = *reinterpret_cast<const float4*>(gs + y * p.r1p + a0);
+          yb.x = fmaf(bv.x, tv.x, yb.x);
+          yb.y = fmaf(bv.y, tv.y, yb.y);
+          yb.z = fmaf(bv.z, tv.z, yb.z);
+          yb.w = fmaf(bv.w, tv.w, yb.w);
+        }
+        const float4 cv = *reinterpret_cast<const float4*>(gs + (p.kh + x) * p.r1p + a0);
+        out.x = fmaf(cv.x, yb.x, out.x);
+        out.y = fmaf(cv.y, yb.y, out.y);
+        out.z = fmaf(cv.z, yb.z, out.z);
+        out.w = fmaf(cv.w, yb.w, out.w);
+      }
+      *reinterpret_cast<float4*>(t2 + pp * p.r2p + a0) = out;
+    }
+  } else {
     const int bg = p.r2p / 4;
     for (int it = threadIdx.x; it < npos * bg; it += kTyThreads) {
       const int pp = it / bg, b0 = 4 * (it - pp * bg);

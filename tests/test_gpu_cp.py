@@ -96,3 +96,19 @@ def test_cp_equals_tucker_embedding_on_gpu():
                  inp.row_ptr, inp.col_idx, inp.values)
     y_t = lt(torch.from_numpy(inp.x).cuda()).cpu().numpy().astype(np.float64)
     assert np.linalg.norm(y_cp - y_t) / np.linalg.norm(y_t) <= 1e-5
+
+
+@pytest.mark.parametrize("geom", [g for g in GEOMS if g[-1] == "f32"])
+@pytest.mark.parametrize("no_tiny", [False, True])
+def test_cp_fp32_one_kernel_and_chain(geom, no_tiny, monkeypatch):
+    """Small fp32 CP layers run the whole layer in the one-kernel path (the paper's two
+    depthwise stages in its order, lrs_tiny.cuh); LRS_NO_TINY keeps the three-kernel chain.
+    Both meet the fp32 bar against the oracle."""
+    if no_tiny:
+        monkeypatch.setenv("LRS_NO_TINY", "1")
+    n, h, w, cin, cout, k, s, p, r, dens, dt = geom
+    cfg = workloads.LayerConfig("t", n, h, w, cin, cout, k, s, p, r, r, dens, dt, seed=9)
+    inp = workloads.generate_cp(cfg)
+    layer, y = run(inp)
+    assert (layer.sparse_engine[0] == 3) != no_tiny
+    check(y, oracle(inp), dt)
