@@ -544,6 +544,7 @@ lrs_status build_tiny(lrs_conv* h, const lrs_conv_desc* d) {
 // chunks it streams); autotune_core then times the best few plans on the device.
 struct CoreGeom {
   int cin, kh, kw, ho, wo, wc, r1p, r2p, g_kc, taps, n_g;
+  bool cp;
   uint32_t u_bytes, g_bytes, g_slot, avail;
 };
 
@@ -553,9 +554,10 @@ static CoreGeom core_geom(const lrs_conv* h, const lrs_conv_desc* d) {
   G.wc = h->wo + G.kw - 1; G.r1p = h->r1p; G.r2p = h->r2p;
   G.g_kc = G.r1p % 64 == 0 ? 64 : (G.r1p % 32 == 0 ? 32 : 16);
   G.taps = G.kh * G.kw;
-  G.n_g = G.taps * (G.r1p / G.g_kc);
+  G.cp = h->cp_core;
+  G.n_g = G.cp ? 0 : G.taps * (G.r1p / G.g_kc);  // the CP form has no dense core to stream
   G.u_bytes = static_cast<uint32_t>(G.r1p) * 128u;
-  G.g_bytes = static_cast<uint32_t>(G.r2p * G.g_kc * 2);
+  G.g_bytes = G.cp ? 0u : static_cast<uint32_t>(G.r2p * G.g_kc * 2);
   G.g_slot = align1024(G.g_bytes);
   G.avail = static_cast<uint32_t>(kMaxSmem) - 1024u - 2048u;  // alignment slack, barriers
   return G;
@@ -583,8 +585,9 @@ static bool core_layout(const CoreGeom& G, int ipt, int th, CoreParams& q) {
   // all X chunks of a tile if possible, then as much of G as fits (all of it: resident)
   q.ns_x = std::min(kCMaxX, std::max(2, n_ck));
   while (q.ns_x > 2 && q.ns_x * q.x_slot + 2 * G.g_slot > left) --q.ns_x;
-  q.ns_g = static_cast<int>(std::min<uint32_t>(static_cast<uint32_t>(std::min(kCMaxG, G.n_g)),
-                                               (left - q.ns_x * q.x_slot) / G.g_slot));
+  q.ns_g = G.n_g == 0 ? 0
+                      : static_cast<int>(std::min<uint32_t>(static_cast<uint32_t>(std::min(kCMaxG, G.n_g)),
+                                                            (left - q.ns_x * q.x_slot) / G.g_slot));
   if (q.ns_g < G.n_g) {  // prefer a resident G over a full X ring when one X slot less makes room
     const int ns_x2 = std::max(2, q.ns_x - 1);
     if (G.n_g <= kCMaxG && static_cast<uint32_t>(ns_x2) * q.x_slot + G.n_g * G.g_slot <= left) {
@@ -617,7 +620,7 @@ static std::vector<std::tuple<double, int, int>> core_candidates(const lrs_conv*
       const int bands = (G.ho + th - 1) / th;
       const long long tiles = static_cast<long long>((d->batch_max + ipt - 1) / ipt) * bands;
       const double bytes = static_cast<double>(ipt) * p1 * G.cin * 2 + static_cast<double>(G.cin) * G.r1p * 2 +
-                           static_cast<double>(G.taps) * G.r1p * G.r2p * 2 + 8192.0;
+                           (G.cp ? 0.0 : static_cast<double>(G.taps) * G.r1p * G.r2p * 2) + 8192.0;
       v.emplace_back(static_cast<double>((tiles + grid - 1) / grid) * bytes, ipt, th);
     }
   }
@@ -640,11 +643,15 @@ static void apply_core_plan(lrs_conv* h, const lrs_conv_desc* d, int ipt, int th
   c.n = d->batch_max; c.ho = G.ho; c.wo = G.wo; c.kh = G.kh; c.kw = G.kw; c.ph = d->pad_h; c.pw = d->pad_w;
   c.th = th; c.bands = (G.ho + th - 1) / th; c.ipt = ipt; c.wr = th + G.kh - 1; c.wc = G.wc; c.p1 = c.wr * G.wc;
   c.n_ck = G.cin / 64;
-  c.r1p = G.r1p; c.r2p = G.r2p; c.g_kc = G.g_kc; c.n_gk = G.r1p / G.g_kc; c.sw_g = static_cast<uint32_t>(G.g_kc * 2);
+  c.r1p = G.r1p; c.r2p = G.r2p; c.g_kc = G.g_kc; c.n_gk = G.cp ? 0 : G.r1p / G.g_kc;  // CP: no G chunks
+  c.sw_g = static_cast<uint32_t>(G.g_kc * 2);
   c.u_bytes = G.u_bytes;
   c.g_bytes = G.g_bytes;
   c.g_slot = G.g_slot;
   c.t1_sw128 = (G.r1p % 64 == 0 && !getenv("LRS_CORE_T1_NOSWZ")) ? 1 : 0;
+  c.cpb = h->w_cpb;
+  c.cpc = h->w_cpc;
+  if (const char* e = getenv("LRS_CORE_DBG")) c.dbg = atoi(e);
   c.nacc = 2 * c.acc_cols <= 512 ? 2 : 1;
   uint32_t tc = 32;
   while (tc < c.nacc * c.acc_cols) tc <<= 1;
@@ -663,7 +670,7 @@ static void apply_core_plan(lrs_conv* h, const lrs_conv_desc* d, int ipt, int th
 lrs_status build_core(lrs_conv* h, const lrs_conv_desc* d) {
   const int cin = d->c_in, kh = d->kernel_h, kw = d->kernel_w;
   const int r1p = h->r1p, r2p = h->r2p;
-  if (h->f32 || h->svd || h->cp_core || d->stride_h != 1 || d->stride_w != 1 || cin % 64 != 0 || getenv("LRS_NO_CORE"))
+  if (h->f32 || h->svd || d->stride_h != 1 || d->stride_w != 1 || cin % 64 != 0 || getenv("LRS_NO_CORE"))
     return LRS_OK;
   const int wc = h->wo + kw - 1;
   if (wc > 256 || r1p > 256 || r2p > 256) return LRS_OK;
@@ -683,7 +690,7 @@ lrs_status build_core(lrs_conv* h, const lrs_conv_desc* d) {
     if ((st = encode_t(&c.tmU, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, h->w_uin, dims, strides, box, estr, 128)) != LRS_OK)
       return st;
   }
-  {
+  if (!G.cp) {
     uint64_t dims[2] = {static_cast<uint64_t>(kh * kw * r1p), static_cast<uint64_t>(r2p)};
     uint64_t strides[1] = {static_cast<uint64_t>(kh * kw * r1p) * 2};
     uint32_t box[2] = {static_cast<uint32_t>(G.g_kc), static_cast<uint32_t>(r2p)};
@@ -1582,8 +1589,11 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     if (e != cudaSuccess)
       return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
-  for (const void* fn : {reinterpret_cast<const void*>(&lrs_core_kernel<4>), reinterpret_cast<const void*>(&lrs_core_kernel<2>),
-                         reinterpret_cast<const void*>(&lrs_core_kernel<1>), reinterpret_cast<const void*>(&lrs_tiny_kernel)}) {
+  for (const void* fn : {reinterpret_cast<const void*>(&lrs_core_kernel<4, false>),
+                         reinterpret_cast<const void*>(&lrs_core_kernel<2, false>),
+                         reinterpret_cast<const void*>(&lrs_core_kernel<1, false>),
+                         reinterpret_cast<const void*>(&lrs_core_kernel<1, true>),
+                         reinterpret_cast<const void*>(&lrs_tiny_kernel)}) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
@@ -1667,9 +1677,10 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
     const unsigned grid = static_cast<unsigned>(std::min(c.n_tiles, h->core_grid));
     cudaEvent_t e1 = nullptr;
     if ((st = time_begin(h, 0, stream, &e1)) != LRS_OK) return st;
-    const void* kfn = c.g_kc == 64 ? reinterpret_cast<const void*>(&lrs_core_kernel<4>)
-                      : c.g_kc == 32 ? reinterpret_cast<const void*>(&lrs_core_kernel<2>)
-                                     : reinterpret_cast<const void*>(&lrs_core_kernel<1>);
+    const void* kfn = h->cp_core    ? reinterpret_cast<const void*>(&lrs_core_kernel<1, true>)
+                      : c.g_kc == 64 ? reinterpret_cast<const void*>(&lrs_core_kernel<4, false>)
+                      : c.g_kc == 32 ? reinterpret_cast<const void*>(&lrs_core_kernel<2, false>)
+                                     : reinterpret_cast<const void*>(&lrs_core_kernel<1, false>);
     LRS_CUDA(launch_pdl(kfn, dim3(grid), dim3(kCThreads), &c, h->core_smem, stream));
     if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
   }
@@ -1681,7 +1692,7 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
       (st = launch(h, 0, h->a1, dim3(static_cast<unsigned>((pin + kTileM - 1) / kTileM)), stream)) != LRS_OK)
     return st;
   // a2
-  if (h->cp_core && !(h->skip & 2)) {
+  if (h->cp_core && !h->use_core && !(h->skip & 2)) {
     CpDwParams& q = h->cpp;
     q.n = n;
     const long long items = static_cast<long long>(n) * h->ho * h->wo * (q.ld / (f32 ? 4 : 8));
@@ -1874,7 +1885,7 @@ lrs_status lrs_conv_stage_times(lrs_conv* h, float* ms, int64_t* counts, int32_t
 
 const char* lrs_conv_stage_name(const lrs_conv* h, int32_t stage) {
   static const char* names[] = {"a1_proj", "a2_core", "a345_expand_sparse", "a4_sparse_add"};
-  if (stage == 0 && h && h->use_core) return "a12_proj_core";
+  if (stage == 0 && h && h->use_core) return h->cp_core ? "a12_proj_cp" : "a12_proj_core";
   if (stage == 1 && h && h->cp_core) return "a2_cp_depthwise";
   return (stage >= 0 && stage < 4) ? names[stage] : "";
 }

@@ -74,6 +74,9 @@ struct CoreParams {
   int nacc;
   uint32_t tmem_cols;
   uint32_t off_g, off_t1, off_bar;
+  int dbg;           // experiment bits (LRS_CORE_DBG): 1 skip the depthwise loop, 2 skip its T2 stores
+  const float* cpb;  // CP core (CPDW kernels): B [kh][R1p], C [kw][R1p] fp32
+  const float* cpc;
   unsigned long long* trace;  // optional globaltimer stamps (LRS_WCONV_DEBUG builds, tools/ctrace.py)
 };
 
@@ -95,7 +98,10 @@ __device__ __forceinline__ uint32_t t1_piece(const CoreParams& p, uint32_t row, 
 }
 
 // GS = K steps of 16 per G chunk (g_kc / 16: 4, 2 or 1)
-template <int GS>
+// CPDW: the paper's CP form: no G; after the restage the epilogue warps
+// run the two depthwise stages (k x 1 with B, then 1 x k with C, the paper's order) on the
+// T1 window and write T2 -- the computation of lrs_cpdw.cuh, with T1 kept on chip.
+template <int GS, bool CPDW>
 __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_constant__ CoreParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -134,7 +140,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
     fence_mbar_init();
     tma_prefetch_desc(&p.tmX);
     tma_prefetch_desc(&p.tmU);
-    tma_prefetch_desc(&p.tmG);
+    if (n_g > 0) tma_prefetch_desc(&p.tmG);
   }
   if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
   tc_fence_before();
@@ -233,6 +239,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         }
       }
       CTRACE(p, blockIdx.x == 0 && k < 4, 8200 + 10 * k + 3);
+      if constexpr (CPDW) continue;  // the epilogue warps compute T2 from the window
       // ---- wait for the bf16 T1 window in shared memory
       mbar_wait(t1s_full, k & 1);
       tc_fence_after();
@@ -329,7 +336,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       // to four before one wait.
       if (threadIdx.x == 64) {
         mbar_wait(&t1_full[b], use & 1);
-        if (k > 0) mbar_wait(t1w_empty, (k - 1) & 1);
+        if (!CPDW && k > 0) mbar_wait(t1w_empty, (k - 1) & 1);
       }
       named_bar_sync(1, kCThreads - 64);
       tc_fence_after();
@@ -360,6 +367,57 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
             }
           }
         }
+      }
+      if constexpr (CPDW) {
+        // TMEM buffer b is read: the MMA thread may start the tile after next
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[b]);
+        named_bar_sync(1, kCThreads - 64);  // the whole window is restaged
+        CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 5);
+        // ---- depthwise stages: item = (output position of the tile, 8 ranks)
+        const int nv = p.r1p / 8;
+        const int items = (p.dbg & 1) ? 0 : p.ipt * rows * p.wo * nv;
+        for (int it = threadIdx.x - 64; it < items; it += kCThreads - 64) {
+          const int v = it % nv, q = it / nv;
+          const int wl = q % p.wo, q2 = q / p.wo;
+          const int hl = q2 % rows, img = q2 / rows;
+          const int n = g * p.ipt + img;
+          if (n >= p.n) continue;
+          const int a0 = 8 * v;
+          float out[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) out[e] = 0.f;
+          for (int x = 0; x < p.kw; ++x) {
+            float yb[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) yb[e] = 0.f;
+            for (int y = 0; y < p.kh; ++y) {
+              const uint32_t row = static_cast<uint32_t>(img * p.p1 + (hl + y) * p.wc + wl + x);
+              const uint4 tv = lds_v4(t1w + t1_piece(p, row, static_cast<uint32_t>(a0)));
+              const uint32_t tw[4] = {tv.x, tv.y, tv.z, tv.w};
+              const float* bt = p.cpb + y * p.r1p + a0;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                yb[2 * e] = fmaf(__ldg(bt + 2 * e), __uint_as_float(tw[e] << 16), yb[2 * e]);
+                yb[2 * e + 1] = fmaf(__ldg(bt + 2 * e + 1), __uint_as_float(tw[e] & 0xFFFF0000u), yb[2 * e + 1]);
+              }
+            }
+            const float* ct = p.cpc + x * p.r1p + a0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) out[e] = fmaf(__ldg(ct + e), yb[e], out[e]);
+          }
+          uint4 o;
+          o.x = pack_bf16x2(out[0], out[1]);
+          o.y = pack_bf16x2(out[2], out[3]);
+          o.z = pack_bf16x2(out[4], out[5]);
+          o.w = pack_bf16x2(out[6], out[7]);
+          if (!(p.dbg & 2))
+            *reinterpret_cast<uint4*>(p.t2 + ((static_cast<long long>(n) * p.ho + ho0 + hl) * p.wo + wl) * p.r2p + a0) = o;
+        }
+        named_bar_sync(1, kCThreads - 64);  // the window may be overwritten by the next restage
+        CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 9);
+        continue;
       }
       fence_proxy_async_smem();
       tc_fence_before();

@@ -233,6 +233,13 @@ __device__ __forceinline__ void stmatrix_x4_trans(uint32_t saddr, uint32_t a0, u
                "r"(a1), "r"(a2), "r"(a3)
                : "memory");
 }
+// 16-byte shared-memory load (ordered by the surrounding barriers)
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&b);

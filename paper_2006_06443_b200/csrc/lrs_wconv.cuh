@@ -134,12 +134,6 @@ __device__ __forceinline__ TileCoord tile_coord(const WconvParams& p, int tile) 
   return c;
 }
 
-__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
-  uint4 v;
-  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-  return v;
-}
-
 // NU = the layer's exact unit count (1..kWMaxUnits): the MMA issue loops are fully
 // unrolled without predicates -- a generic 8-unit loop measured 17-39 % slower
 // (instruction fetch of the issuing warp dominates small MMAs).

@@ -92,6 +92,9 @@ def layer_work(cfg, n: int, col_idx: np.ndarray, cp: bool = False) -> Dict[str, 
     core_macs = (2 * p * r1 * cfg.k) if cp else (0 if cfg.svd else p * r1 * r2 * cfg.k ** 2)
     if cp:
         st["a2_cp_depthwise"] = {"bytes": t1_b + t2_b + core_w * 4, "flops": 2.0 * core_macs}
+        # a1 + the depthwise pair fused (T1 stays on chip): X in, T2 out, A and B, C read once
+        st["a12_proj_cp"] = {"bytes": x_b + t2_b + cfg.c_in * r1 * esz + core_w * 4,
+                             "flops": 2.0 * p_in * cfg.c_in * r1 + 2.0 * core_macs}
     layer_bytes = x_b + y_b + esz * (cfg.c_in * r1 + core_w + r2 * cfg.c_out) + nnz * 8 + (cfg.c_out + 1) * 4
     chain = 2.0 * (p_in * cfg.c_in * r1 + core_macs + p * r2 * cfg.c_out)
     st["layer"] = {"bytes": layer_bytes, "flops_chain": chain, "flops_sparse": 2.0 * macs_s,

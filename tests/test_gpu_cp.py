@@ -48,7 +48,9 @@ def check(y, ref, dtype):
 def test_cp_configs_vs_oracle(name, batch):
     inp = workloads.generate_cp(workloads.CP_CONFIGS[name], batch=batch)
     layer, y = run(inp)
-    assert not layer.core_fused  # a1, the depthwise pair, then the expansion + sparse kernel(s)
+    c = inp.cfg
+    # bf16, stride 1, Cin % 64 == 0: a1 and the depthwise pair in one kernel (T1 on chip)
+    assert layer.core_fused == (c.dtype == "bf16" and c.stride == 1 and c.c_in % 64 == 0)
     check(y, oracle(inp), inp.cfg.dtype)
 
 
@@ -112,3 +114,25 @@ def test_cp_fp32_one_kernel_and_chain(geom, no_tiny, monkeypatch):
     layer, y = run(inp)
     assert (layer.sparse_engine[0] == 3) != no_tiny
     check(y, oracle(inp), dt)
+
+
+@pytest.mark.parametrize("geom", [
+    (9, 14, 14, 256, 256, 3, 1, 1, 64, 0.02, "bf16"),    # C2 CP shape, ragged batch
+    (4, 9, 11, 64, 64, 3, 1, 0, 32, 0.02, "bf16"),       # pad 0, non-square, R = 32 (SWIZZLE_NONE window)
+    (3, 12, 12, 128, 64, 5, 1, 2, 48, 0.03, "bf16"),     # 5x5, R = 48
+])
+def test_cp_fused_core_bitwise_equal_to_chain(geom, monkeypatch):
+    """a1 + the two depthwise stages fused (lrs_core.cuh CPDW: T1 restaged on chip) compute
+    the same bits as the three-kernel chain (a1 GEMM -> T1 in HBM -> lrs_cpdw.cuh): the same
+    bf16 T1 and the same fp32 FMA order."""
+    from paper_2006_06443_b200 import LrsConv
+    n, h, w, cin, cout, k, s, p, r, dens, dt = geom
+    cfg = workloads.LayerConfig("t", n, h, w, cin, cout, k, s, p, r, r, dens, dt, seed=31)
+    inp = workloads.generate_cp(cfg)
+    fused, yf = run(inp)
+    assert fused.core_fused
+    monkeypatch.setenv("LRS_NO_CORE", "1")
+    chain, yc = run(inp)
+    assert not chain.core_fused
+    assert np.array_equal(yf, yc)
+    check(yf, oracle(inp), dt)
