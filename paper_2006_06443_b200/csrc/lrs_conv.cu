@@ -809,6 +809,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   const int n_ck = cin / 64;
   const int n_mt = (cout + 127) / 128;
   const int rp = h->r2p;  // K of the dense part: R2, or R of the SVD pair
+  const bool ering = getenv("LRS_WCONV_ERING") != nullptr;  // experiment: metadata ring smaller than the A ring
   const int t_kc = rp < 64 ? rp : 64;
   if (rp % t_kc) return LRS_OK;
   if (n_ck * kh * kw > 1024) return LRS_OK;  // residual table staged in shared memory
@@ -889,7 +890,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         if (bpi > bpi_max || ns > ns_max) continue;
         const uint32_t a_slot = static_cast<uint32_t>(bpi) * kSpBlockBytes;  // >= 16 KB dense box
         const uint32_t e_slot = static_cast<uint32_t>(bpi) * kEBlockBytes;
-        if (acc + 4 * bpi * ns > 512) continue;
+        const int es_need = ering ? 1 : ns;  // TMEM metadata slots the plan needs at least
+        if (acc + 4 * bpi * es_need > 512) continue;
         const uint32_t xw = static_cast<uint32_t>(wr) * wcw * 1024u;  // one chunk's box
         const uint32_t tw = static_cast<uint32_t>(th) * tbw * 8u * sw_t;
         // slack: positions read past the end of a window by the last (padded) MMA rows
@@ -907,8 +909,9 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         // the M-tile's block stream: chunk starts + a tap offset per (main or residual) block
         const uint32_t res_bytes = (static_cast<uint32_t>(n_ck + 1 + 2 * n_ck * taps) * 4u + 127u) & ~127u;
         const uint32_t fixed = ns * (a_slot + e_slot) + 8 * kEpiScratch + res_bytes + 1024 + 1024;
-        if (2 * stride + fixed > static_cast<uint32_t>(kMaxSmem)) continue;
-        int nwb = 2;
+        const int nwb_min = getenv("LRS_WCONV_NWB1") ? 1 : 2;  // experiment: a single window buffer
+        if (static_cast<uint32_t>(nwb_min) * stride + fixed > static_cast<uint32_t>(kMaxSmem)) continue;
+        int nwb = nwb_min;
         while (nwb < 4 && (nwb + 1) * stride + fixed <= static_cast<uint32_t>(kMaxSmem)) ++nwb;
         // one buffer per window of a tile when they all fit: windows are then reused by
         // the CTA's next tile of the same images / band (the next M-tile)
@@ -929,7 +932,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         // (~30 cycles per accumulator column, measured with tools/wtrace) unless two
         // accumulators fit in TMEM and it overlaps the next tile's MMAs
         const long long tile_mma = static_cast<long long>(n_tk + n_ck * taps) * item;
-        const bool dbl = 2 * acc + 4 * bpi * ns <= 512;
+        const bool dbl = 2 * acc + 4 * bpi * es_need <= 512;
         const long long cost = waves * (tile_mma + (dbl ? 0LL : 30LL * acc));
         if (cost < best_cost) {
           best_cost = cost;
@@ -1156,8 +1159,9 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   w.a_slot = static_cast<uint32_t>(best_bpi) * kSpBlockBytes;
   w.e_slot = static_cast<uint32_t>(best_bpi) * kEBlockBytes;
   // double-buffered accumulators (epilogue overlaps MMAs) when two fit next to the metadata columns
-  w.nacc = (2 * acc + 4 * best_bpi * best_ns <= 512) ? 2 : 1;
+  w.nacc = (2 * acc + 4 * best_bpi * (ering ? 1 : best_ns) <= 512) ? 2 : 1;
   w.e_col0 = w.nacc * acc;
+  w.e_slots = std::max(1, std::min<int>(best_ns, static_cast<int>((512 - w.nacc * acc) / (4 * best_bpi))));
   w.tmem_cols = 512;  // whole TMEM: base address 0 (lrs_wconv_kernel relies on it)
   w.nwb = best_nwb;
   w.off_a = best_nwb * best_stride;

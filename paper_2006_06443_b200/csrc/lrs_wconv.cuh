@@ -111,6 +111,8 @@ struct WconvParams {
   int nacc;             // accumulator buffers in TMEM (1 or 2)
   uint32_t acc_cols;    // TMEM columns of one accumulator buffer
   uint32_t e_col0, tmem_cols;
+  int e_slots;             // TMEM metadata slots (<= ns): tcgen05.cp and tcgen05.mma of one thread run in
+                           // issue order, so an item's metadata may overwrite that of an item issued before
   uint32_t off_a, off_e, off_epi, off_res, off_bar;
   const float2* epi;    // per output channel (scale, bias) of the fused output epilogue, or NULL
   int relu;
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const uint32_t slot_a16 = p.a_slot >> 4, slot_e16 = p.e_slot >> 4;
     const uint32_t win16 = p.win_stride >> 4;
     const int ksteps = static_cast<int>(p.sw_t / 32);
-    int slot = 0, k = 0, buf = 0;
+    int slot = 0, k = 0, buf = 0, eslot = 0;
     uint32_t ph = 0, wph = 0;
     if (elect_one()) {
     const bool contig = p.nwb == nwin;  // must match the producer's tile order
@@ -375,7 +377,8 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
 #pragma unroll
             for (int q = 0; q < BPI; ++q)
               tapv[q] = (q == 0 ? info0 : ld_shared_u32(slot_info + 4u * (kWMaxBpi * slot + q))) & 0x0FFFFFFFu;
-            const uint32_t et = tmem + p.e_col0 + 4u * static_cast<uint32_t>(p.bpi) * slot;
+            const uint32_t et = tmem + p.e_col0 + 4u * static_cast<uint32_t>(p.bpi) * eslot;
+            if (++eslot == p.e_slots) eslot = 0;
             const uint64_t ab = ad_sp + slot * slot_a16;
             {
               // metadata of block pairs in one tcgen05.cp.128x256b (blocks 2 KB apart = LBO)
