@@ -564,7 +564,9 @@ static CoreGeom core_geom(const lrs_conv* h, const lrs_conv_desc* d) {
 }
 
 // Shared-memory layout of one (ipt, th): X ring (ns_x slots), G ring (ns_g), T1 window.
-static bool core_layout(const CoreGeom& G, int ipt, int th, CoreParams& q) {
+// gmode 0: G resident when it fits (one X slot less if needed); 1: G streamed through a
+// small ring so the X ring is as deep as the tile's chunks (X boxes arrive earlier).
+static bool core_layout(const CoreGeom& G, int ipt, int th, CoreParams& q, int gmode = 0) {
   const int wr = th + G.kh - 1, p1 = wr * G.wc;
   if (wr > 256) return false;
   q.nb1 = (ipt * p1 + 127) / 128;
@@ -588,7 +590,12 @@ static bool core_layout(const CoreGeom& G, int ipt, int th, CoreParams& q) {
   q.ns_g = G.n_g == 0 ? 0
                       : static_cast<int>(std::min<uint32_t>(static_cast<uint32_t>(std::min(kCMaxG, G.n_g)),
                                                             (left - q.ns_x * q.x_slot) / G.g_slot));
-  if (q.ns_g < G.n_g) {  // prefer a resident G over a full X ring when one X slot less makes room
+  if (gmode == 1 && G.n_g > 0) {
+    q.ns_x = std::min(kCMaxX, std::max(2, n_ck));
+    while (q.ns_x > 2 && q.ns_x * q.x_slot + 2 * G.g_slot > left) --q.ns_x;
+    q.ns_g = static_cast<int>(std::min<uint32_t>(std::min<uint32_t>(4u, static_cast<uint32_t>(G.n_g)),
+                                                 (left - q.ns_x * q.x_slot) / G.g_slot));
+  } else if (q.ns_g < G.n_g) {  // prefer a resident G over a full X ring when one X slot less makes room
     const int ns_x2 = std::max(2, q.ns_x - 1);
     if (G.n_g <= kCMaxG && static_cast<uint32_t>(ns_x2) * q.x_slot + G.n_g * G.g_slot <= left) {
       q.ns_x = ns_x2;
@@ -630,7 +637,7 @@ static std::vector<std::tuple<double, int, int>> core_candidates(const lrs_conv*
 }
 
 // Fill h->cp for one plan (the tensor maps of U_in and G are plan-independent and kept).
-static void apply_core_plan(lrs_conv* h, const lrs_conv_desc* d, int ipt, int th, int grid) {
+static void apply_core_plan(lrs_conv* h, const lrs_conv_desc* d, int ipt, int th, int grid, int gmode = 0) {
   const CoreGeom G = core_geom(h, d);
   CoreParams& c = h->cp;
   const CUtensorMap tmU = c.tmU, tmG = c.tmG;
@@ -639,7 +646,7 @@ static void apply_core_plan(lrs_conv* h, const lrs_conv_desc* d, int ipt, int th
   c.tmU = tmU;
   c.tmG = tmG;
   c.trace = trace;
-  core_layout(G, ipt, th, c);
+  core_layout(G, ipt, th, c, gmode);
   c.n = d->batch_max; c.ho = G.ho; c.wo = G.wo; c.kh = G.kh; c.kw = G.kw; c.ph = d->pad_h; c.pw = d->pad_w;
   c.th = th; c.bands = (G.ho + th - 1) / th; c.ipt = ipt; c.wr = th + G.kh - 1; c.wc = G.wc; c.p1 = c.wr * G.wc;
   c.n_ck = G.cin / 64;
@@ -699,7 +706,8 @@ lrs_status build_core(lrs_conv* h, const lrs_conv_desc* d) {
                        static_cast<uint32_t>(G.g_kc * 2))) != LRS_OK)
       return st;
   }
-  apply_core_plan(h, d, std::get<1>(cand[0]), std::get<2>(cand[0]), grid);
+  apply_core_plan(h, d, std::get<1>(cand[0]), std::get<2>(cand[0]), grid,
+                  getenv("LRS_CORE_GSTREAM") ? 1 : 0);  // planner experiments
   h->use_core = true;
   return LRS_OK;
 }
@@ -1194,7 +1202,7 @@ static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d) {
       getenv("LRS_CORE_GRID") || h->skip)
     return LRS_OK;
   const int n = d->batch_max;
-  std::vector<std::tuple<int, int, int>> plans;  // (ipt, th, grid)
+  std::vector<std::tuple<int, int, int, int>> plans;  // (ipt, th, grid, gmode)
   std::vector<int> grids{h->sms};
   if (h->use_w) {
     const WconvParams& w = h->wp;
@@ -1204,7 +1212,16 @@ static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d) {
   }
   for (int g : grids) {
     const auto cand = core_candidates(h, d, g);
-    for (size_t i = 0; i < cand.size() && i < 4; ++i) plans.emplace_back(std::get<1>(cand[i]), std::get<2>(cand[i]), g);
+    const CoreGeom G = core_geom(h, d);
+    for (size_t i = 0; i < cand.size() && i < 4; ++i) {
+      plans.emplace_back(std::get<1>(cand[i]), std::get<2>(cand[i]), g, 0);
+      CoreParams q0, q1;
+      memset(&q0, 0, sizeof(q0));
+      memset(&q1, 0, sizeof(q1));
+      core_layout(G, std::get<1>(cand[i]), std::get<2>(cand[i]), q0, 0);
+      if (core_layout(G, std::get<1>(cand[i]), std::get<2>(cand[i]), q1, 1) && q1.ns_x > q0.ns_x)
+        plans.emplace_back(std::get<1>(cand[i]), std::get<2>(cand[i]), g, 1);  // deeper X ring, G streamed
+    }
   }
   if (plans.size() <= 1) return LRS_OK;
   const size_t xb = static_cast<size_t>(n) * d->in_h * d->in_w * d->c_in * 2;
@@ -1224,7 +1241,7 @@ static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d) {
     st = fail(LRS_ERR_CUDA, "autotune: scratch allocation failed");
   }
   for (size_t i = 0; st == LRS_OK && i < plans.size(); ++i) {
-    apply_core_plan(h, d, std::get<0>(plans[i]), std::get<1>(plans[i]), std::get<2>(plans[i]));
+    apply_core_plan(h, d, std::get<0>(plans[i]), std::get<1>(plans[i]), std::get<2>(plans[i]), std::get<3>(plans[i]));
     for (int r = 0; r < 3 && st == LRS_OK; ++r) st = lrs_conv_forward(h, xs, ys, n, s);
     if (st != LRS_OK) break;
     cudaEventRecord(e0, s);
@@ -1234,15 +1251,15 @@ static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d) {
     float ms = 0.f;
     if (st == LRS_OK) cudaEventElapsedTime(&ms, e0, e1);
     if (getenv("LRS_VERBOSE"))
-      fprintf(stderr, "[lrs] autotune core ipt=%d th=%d grid=%d: %.2f us/forward\n", std::get<0>(plans[i]),
-              std::get<1>(plans[i]), std::get<2>(plans[i]), ms * 100.f);
+      fprintf(stderr, "[lrs] autotune core ipt=%d th=%d grid=%d gmode=%d: %.2f us/forward\n", std::get<0>(plans[i]),
+              std::get<1>(plans[i]), std::get<2>(plans[i]), std::get<3>(plans[i]), ms * 100.f);
     if (st == LRS_OK && ms < best) {
       best = ms;
       bi = static_cast<int>(i);
     }
   }
   if (st == LRS_OK && bi >= 0) {
-    apply_core_plan(h, d, std::get<0>(plans[bi]), std::get<1>(plans[bi]), std::get<2>(plans[bi]));
+    apply_core_plan(h, d, std::get<0>(plans[bi]), std::get<1>(plans[bi]), std::get<2>(plans[bi]), std::get<3>(plans[bi]));
   } else {
     h->cp = keep;
     h->core_smem = keep_smem;

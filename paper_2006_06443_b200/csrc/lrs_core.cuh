@@ -163,27 +163,47 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
+      // Requests follow the MMA thread's consumption order (a1(k+1) before a2(k) when two
+      // TMEM buffers allow the lookahead): a streamed G must never block an X box the
+      // MMA thread needs first.
       int ix = 0, ig = 0;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+      const int m_tiles = static_cast<int>(blockIdx.x) < p.n_tiles
+                              ? (p.n_tiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+                              : 0;
+      auto load_x = [&](int k) {
+        const int tile = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
         const int g = tile / p.bands, ho0 = (tile - g * p.bands) * p.th;
         for (int c = 0; c < p.n_ck; ++c, ++ix) {
           const int s = ix % p.ns_x;
           if (ix >= p.ns_x) mbar_wait(&empty_x[s], ((ix / p.ns_x) - 1) & 1);
-          CTRACE(p, blockIdx.x == 0 && c == 0 && (tile - blockIdx.x) / gridDim.x < 4,
-                 8200 + 10 * ((tile - blockIdx.x) / gridDim.x) + 1);
+          CTRACE(p, blockIdx.x == 0 && c == 0 && k < 4, 8200 + 10 * k + 1);
           uint8_t* dst = smem + s * p.x_slot;
           mbar_arrive_expect_tx(&full_x[s], p.x_bytes + p.u_bytes);
           tma_load_4d(dst, &p.tmX, &full_x[s], c * 64, -p.pw, ho0 - p.ph, g * p.ipt);
           tma_load_2d(dst + p.u_off, &p.tmU, &full_x[s], c * 64, 0);
         }
-        if (!p.g_res)
-          for (int j = 0; j < n_g; ++j, ++ig) {
-            const int s = ig % p.ns_g;
-            if (ig >= p.ns_g) mbar_wait(&empty_g[s], ((ig / p.ns_g) - 1) & 1);
-            const int t = j / p.n_gk, gk = j - t * p.n_gk;
-            mbar_arrive_expect_tx(&full_g[s], p.g_bytes);
-            tma_load_2d(smem + p.off_g + s * p.g_slot, &p.tmG, &full_g[s], t * p.r1p + gk * p.g_kc, 0);
-          }
+      };
+      auto load_g = [&]() {
+        if (p.g_res) return;
+        for (int j = 0; j < n_g; ++j, ++ig) {
+          const int s = ig % p.ns_g;
+          if (ig >= p.ns_g) mbar_wait(&empty_g[s], ((ig / p.ns_g) - 1) & 1);
+          const int t = j / p.n_gk, gk = j - t * p.n_gk;
+          mbar_arrive_expect_tx(&full_g[s], p.g_bytes);
+          tma_load_2d(smem + p.off_g + s * p.g_slot, &p.tmG, &full_g[s], t * p.r1p + gk * p.g_kc, 0);
+        }
+      };
+      if (!CPDW && p.nacc == 2) {
+        if (m_tiles > 0) load_x(0);
+        for (int k = 0; k < m_tiles; ++k) {
+          if (k + 1 < m_tiles) load_x(k + 1);
+          load_g();
+        }
+      } else {
+        for (int k = 0; k < m_tiles; ++k) {
+          load_x(k);
+          load_g();
+        }
       }
     }
   } else if (warp == 1) {
@@ -209,8 +229,12 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
     const uint32_t a_gs = p.t1_sw128 ? p.t1_rows * 8u : static_cast<uint32_t>(p.g_kc / 8) * (lbo >> 4);
     const uint32_t a_ks = p.t1_sw128 ? 2u : 2u * (lbo >> 4);
     const uint32_t x16 = p.x_slot >> 4, g16 = p.g_slot >> 4;
-    int ix = 0, ig = 0, k = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++k) {
+    int ix = 0, ig = 0;
+    const int m_tiles = static_cast<int>(blockIdx.x) < p.n_tiles
+                            ? (p.n_tiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+                            : 0;
+    // a1 of tile k into TMEM buffer b(k)
+    auto phase_a1 = [&](int k) {
       const int b = p.nacc == 2 ? (k & 1) : 0;
       const int use = p.nacc == 2 ? (k >> 1) : k;
       if (use > 0) {
@@ -218,7 +242,6 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         tc_fence_after();
       }
       const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * p.acc_cols;
-      const uint32_t t2c = acc0;  // T2 overwrites T1's columns (restaged already)
       // ---- a1: T1 (window rows) = X window . U_in, K = Cin in 64-channel chunks
       for (int c = 0; c < p.n_ck; ++c, ++ix) {
         const int s = ix % p.ns_x;
@@ -239,7 +262,12 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         }
       }
       CTRACE(p, blockIdx.x == 0 && k < 4, 8200 + 10 * k + 3);
-      if constexpr (CPDW) continue;  // the epilogue warps compute T2 from the window
+    };
+    // a2 of tile k: T2 over T1's columns of buffer b(k), from the restaged window
+    auto phase_a2 = [&](int k) {
+      const int b = p.nacc == 2 ? (k & 1) : 0;
+      const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * p.acc_cols;
+      const uint32_t t2c = acc0;  // T2 overwrites T1's columns (restaged already)
       // ---- wait for the bf16 T1 window in shared memory
       mbar_wait(t1s_full, k & 1);
       tc_fence_after();
@@ -315,6 +343,22 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         mma_commit(t1w_empty);
       }
       CTRACE(p, blockIdx.x == 0 && k < 4, 8200 + 10 * k + 7);
+    };
+    if constexpr (CPDW) {
+      for (int k = 0; k < m_tiles; ++k) phase_a1(k);
+    } else if (p.nacc == 2) {
+      // a1 of tile k+1 is issued before a2 of tile k (two TMEM buffers): the epilogue's T1
+      // restage of tile k then overlaps the projection MMAs of tile k+1
+      if (m_tiles > 0) phase_a1(0);
+      for (int k = 0; k < m_tiles; ++k) {
+        if (k + 1 < m_tiles) phase_a1(k + 1);
+        phase_a2(k);
+      }
+    } else {
+      for (int k = 0; k < m_tiles; ++k) {
+        phase_a1(k);
+        phase_a2(k);
+      }
     }
     }
     __syncwarp();
@@ -323,13 +367,18 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
     const int q4 = warp & 3;            // TMEM lane quarter
     const int ehalf = (warp - 2) >> 2;  // which 16-column half of every 32 columns
     const uint32_t t1w = smem_u32(smem + p.off_t1);
-    int k = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++k) {
+    const int m_tiles = static_cast<int>(blockIdx.x) < p.n_tiles
+                            ? (p.n_tiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+                            : 0;
+    // restage T1 of tile k (TMEM buffer b(k)) into the window
+    auto restage = [&](int k) {
+      const int tile = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
       const int g = tile / p.bands, ho0 = (tile - g * p.bands) * p.th;
       const int rows = min(p.th, p.ho - ho0);
       const int b = p.nacc == 2 ? (k & 1) : 0;
       const int use = p.nacc == 2 ? (k >> 1) : k;
       const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * p.acc_cols + (static_cast<uint32_t>(q4 * 32) << 16);
+      (void)g; (void)ho0; (void)rows; (void)use; (void)acc0;
       // ---- restage T1 (fp32 TMEM) as bf16 into the window (rows >= t1_rows are never read).
       // One thread polls (no sleep: this hand-off is on the tile's critical path), the other
       // epilogue threads block in a named barrier; TMEM loads are issued in groups of up
@@ -368,7 +417,24 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
           }
         }
       }
-      if constexpr (CPDW) {
+      if constexpr (!CPDW) {  // the window is restaged: the MMA thread may run a2(k)
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(t1s_full);
+        CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 5);
+      }
+    };
+    // CP form: the two depthwise stages of tile k from the window, T2 to HBM
+    auto depthwise = [&](int k) {
+      const int tile = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+      const int g = tile / p.bands, ho0 = (tile - g * p.bands) * p.th;
+      const int rows = min(p.th, p.ho - ho0);
+      const int b = p.nacc == 2 ? (k & 1) : 0;
+      const int use = p.nacc == 2 ? (k >> 1) : k;
+      const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * p.acc_cols + (static_cast<uint32_t>(q4 * 32) << 16);
+      (void)g; (void)ho0; (void)rows; (void)use; (void)acc0;
+      {
         // TMEM buffer b is read: the MMA thread may start the tile after next
         tc_fence_before();
         __syncwarp();
@@ -417,13 +483,17 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         }
         named_bar_sync(1, kCThreads - 64);  // the window may be overwritten by the next restage
         CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 9);
-        continue;
       }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(t1s_full);
-      CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 5);
+    };
+    // T2 of tile k: hand the window back to the MMA thread, then TMEM -> HBM
+    auto t2_store = [&](int k) {
+      const int tile = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+      const int g = tile / p.bands, ho0 = (tile - g * p.bands) * p.th;
+      const int rows = min(p.th, p.ho - ho0);
+      const int b = p.nacc == 2 ? (k & 1) : 0;
+      const int use = p.nacc == 2 ? (k >> 1) : k;
+      const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * p.acc_cols + (static_cast<uint32_t>(q4 * 32) << 16);
+      (void)g; (void)ho0; (void)rows; (void)use; (void)acc0;
       // ---- T2 (fp32 TMEM) -> bf16 rows of global T2
       if (threadIdx.x == 64) mbar_wait(&t2_full[b], use & 1);
       named_bar_sync(1, kCThreads - 64);
@@ -460,6 +530,25 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
       CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 9);
+    };
+    if constexpr (CPDW) {
+      for (int k = 0; k < m_tiles; ++k) {
+        restage(k);
+        depthwise(k);
+      }
+    } else if (p.nacc == 2) {
+      // matches the MMA order a1(k+1) before a2(k): restage k+1 as soon as a2(k) has read
+      // the window, then store T2(k) while the MMA thread runs a2(k+1)
+      if (m_tiles > 0) restage(0);
+      for (int k = 0; k < m_tiles; ++k) {
+        if (k + 1 < m_tiles) restage(k + 1);
+        t2_store(k);
+      }
+    } else {
+      for (int k = 0; k < m_tiles; ++k) {
+        restage(k);
+        t2_store(k);
+      }
     }
   }
   CTRACE(p, threadIdx.x == 64 && blockIdx.x < 2048, 9000 + 2 * blockIdx.x + 1);
