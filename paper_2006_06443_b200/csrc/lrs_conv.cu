@@ -166,8 +166,6 @@ struct lrs_conv {
   void* w_uout = nullptr;  // [Cout_p (x2)][R2p or R1p]
   void* t1 = nullptr;
   void* t2 = nullptr;
-  int* sync_buf = nullptr;  // [2 + core tiles]: forward counter, done counter, per-core-tile T2 flags
-  bool use_flags = false;   // the fused kernel waits per tile on the core kernel's flags, not its grid
   int2* ent = nullptr;
   int* ent_ptr = nullptr;
   // stages
@@ -1384,12 +1382,6 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     return cleanup_fail(fail(LRS_ERR_OUT_OF_MEMORY, "T1 scratch allocation failed"));
   if (!h->svd && cudaMalloc(&h->t2, static_cast<size_t>(p_max) * r2p * esz) != cudaSuccess)
     return cleanup_fail(fail(LRS_ERR_OUT_OF_MEMORY, "T2 scratch allocation failed"));
-  {  // core tiles <= batch_max * out_h (ipt >= 1, th >= 1)
-    const size_t nsync = 2 + static_cast<size_t>(d->batch_max) * ho;
-    if (cudaMalloc(&h->sync_buf, nsync * sizeof(int)) != cudaSuccess ||
-        cudaMemset(h->sync_buf, 0, nsync * sizeof(int)) != cudaSuccess)
-      return cleanup_fail(fail(LRS_ERR_OUT_OF_MEMORY, "sync buffer allocation failed"));
-  }
 
   // ---------------------------------------------------------------- a1: T1 = X U_in
   {
@@ -1638,11 +1630,6 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
       if (e != cudaSuccess)
         return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
     }
-  // per-tile T2 hand-off between the two kernels (opt-in LRS_FLAGS=1: the fused kernel waits
-  // on the core tiles covering its rows instead of the core kernel's whole grid).  Correct
-  // (tests/test_gpu_core_fused.py) but measured slower at C2 (27.3 vs 22.7 us), so the
-  // default keeps the grid-wide PDL wait.
-  h->use_flags = h->use_core && h->use_w && !h->skip && getenv("LRS_FLAGS");
   if ((st = autotune_core(h, d)) != LRS_OK) return cleanup_fail(st);
   cudaSetDevice(prev);
   *out = h;
@@ -1708,8 +1695,6 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
     c.n = n;
     c.t2 = static_cast<__nv_bfloat16*>(h->t2);
     c.n_tiles = ((n + c.ipt - 1) / c.ipt) * c.bands;
-    c.flags = h->use_flags ? h->sync_buf + 2 : nullptr;
-    c.epoch = h->sync_buf;
     const unsigned grid = static_cast<unsigned>(std::min(c.n_tiles, h->core_grid));
     cudaEvent_t e1 = nullptr;
     if ((st = time_begin(h, 0, stream, &e1)) != LRS_OK) return st;
@@ -1765,12 +1750,6 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
     w.n = n;
     w.y = y;
     w.n_tiles = ((n + 7) / 8) * w.bands * w.cbands * w.n_mt;
-    w.flags = h->use_flags ? h->sync_buf + 2 : nullptr;
-    w.epoch = h->sync_buf;
-    w.done = h->sync_buf + 1;
-    w.c_ipt = h->cp.ipt;
-    w.c_th = h->cp.th;
-    w.c_bands = h->cp.bands;
     const unsigned grid = static_cast<unsigned>(std::min(w.n_tiles, h->sms));
     cudaEvent_t e1 = nullptr;
     if ((st = time_begin(h, 2, stream, &e1)) != LRS_OK) return st;
@@ -1861,7 +1840,7 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
                   h->w_as, h->w_e, h->w_res, h->w_dense_img, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc,
-                  h->sp_uo, h->epi, h->sync_buf};
+                  h->sp_uo, h->epi};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (void* b : h->tiny_buf)

@@ -75,8 +75,6 @@ struct CoreParams {
   uint32_t tmem_cols;
   uint32_t off_g, off_t1, off_bar;
   int dbg;           // experiment bits (LRS_CORE_DBG): 1 skip the depthwise loop, 2 skip its T2 stores
-  int* flags;        // per-tile readiness for the fused kernel (NULL: it waits for the whole grid)
-  const int* epoch;  // device forward counter (advanced by the fused kernel's last CTA)
   const float* cpb;  // CP core (CPDW kernels): B [kh][R1p], C [kw][R1p] fp32
   const float* cpc;
   unsigned long long* trace;  // optional globaltimer stamps (LRS_WCONV_DEBUG builds, tools/ctrace.py)
@@ -161,9 +159,6 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
   pdl_wait();  // the previous kernel's output is visible from here on
   pdl_launch_dependents();  // only after the wait: every kernel before us is then complete
   CTRACE(p, threadIdx.x == 0 && blockIdx.x == 0, 8190);
-  // this forward's flag value (the previous forward's fused kernel advanced the counter
-  // before it completed; the PDL wait above made that visible)
-  const int flag_val = p.flags ? *p.epoch + 1 : 0;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -487,10 +482,6 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
             *reinterpret_cast<uint4*>(p.t2 + ((static_cast<long long>(n) * p.ho + ho0 + hl) * p.wo + wl) * p.r2p + a0) = o;
         }
         named_bar_sync(1, kCThreads - 64);  // the window may be overwritten by the next restage
-        if (p.flags && threadIdx.x == 64) {  // all T2 stores of the tile precede the barrier
-          __threadfence();
-          st_release_gpu(p.flags + tile, flag_val);
-        }
         CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 9);
       }
     };
@@ -538,13 +529,6 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
-      if (p.flags) {  // every epilogue thread's T2 stores, then the tile's flag (release)
-        named_bar_sync(1, kCThreads - 64);
-        if (threadIdx.x == 64) {
-          __threadfence();
-          st_release_gpu(p.flags + tile, flag_val);
-        }
-      }
       CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 9);
     };
     if constexpr (CPDW) {

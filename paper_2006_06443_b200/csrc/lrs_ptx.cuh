@@ -233,21 +233,6 @@ __device__ __forceinline__ void stmatrix_x4_trans(uint32_t saddr, uint32_t a0, u
                "r"(a1), "r"(a2), "r"(a3)
                : "memory");
 }
-// gpu-scope release store / acquire load of a flag (cross-CTA producer -> consumer hand-off)
-__device__ __forceinline__ void st_release_gpu(int* a, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire_gpu(const int* a) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
-// order this thread's generic-proxy view of global memory before its later async-proxy
-// (TMA) reads of it
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
 // 16-byte shared-memory load (ordered by the surrounding barriers)
 __device__ __forceinline__ uint4 lds_v4(uint32_t a) {
   uint4 v;

@@ -111,10 +111,6 @@ struct WconvParams {
   int nacc;             // accumulator buffers in TMEM (1 or 2)
   uint32_t acc_cols;    // TMEM columns of one accumulator buffer
   uint32_t e_col0, tmem_cols;
-  const int* flags;        // the core kernel's per-tile T2 readiness (NULL: wait for its whole grid)
-  int* epoch;              // device forward counter: the last CTA to finish advances it
-  int* done;               // CTAs finished in this forward (reset by the last one)
-  int c_ipt, c_th, c_bands;  // the core kernel's tiling (images per tile, rows per band, bands)
   int e_slots;             // TMEM metadata slots (<= ns): tcgen05.cp and tcgen05.mma of one thread run in
                            // issue order, so an item's metadata may overwrite that of an item issued before
   uint32_t off_a, off_e, off_epi, off_res, off_bar;
@@ -210,8 +206,6 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       uint32_t* tap_s = reinterpret_cast<uint32_t*>(so_s + p.n_ck + 1);
       int cur_mt = -1, mt0 = 0;
       bool waited = false;
-      // this forward's flag value: the counter advances only when every CTA of this grid is done
-      const int flag_want = p.flags ? ld_acquire_gpu(p.epoch) + 1 : 0;
       // CTAs own contiguous tile ranges, M-tile fastest: consecutive tiles of a CTA share
       // their windows; with one ring buffer per window (nwb == nwin) a window still resident
       // from the previous tile is reused instead of re-loaded
@@ -239,26 +233,8 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           uint8_t* wdst = smem + buf * p.win_stride;
           if (WTRACE(p) && blockIdx.x == 0 && wg < 16) p.trace[3600 + wg] = gtimer();
           const int tk = w - p.n_xw;  // >= 0: dense (T) window, after the tile's sparse ones
-          if (tk == 0 && p.flags && !reuse) {
-            // T2 of this tile's images and rows is ready once the core tiles covering them have
-            // published this forward's flag (the core kernel runs concurrently on other SMs)
-            const int n_last = min(tc.n0 + 7, p.n - 1), r_last = min(tc.ho0 + p.th - 1, p.ho - 1);
-            for (int cg = tc.n0 / p.c_ipt; cg <= n_last / p.c_ipt; ++cg)
-              for (int cb = tc.ho0 / p.c_th; cb <= r_last / p.c_th; ++cb) {
-                const int* f = p.flags + cg * p.c_bands + cb;
-                const long long t0 = clock64();
-                while (ld_acquire_gpu(f) < flag_want) {
-                  __nanosleep(256);  // polling without back-off slowed the co-running core kernel
-                  if (clock64() - t0 > LRS_WAIT_TIMEOUT_CYCLES) {
-                    printf("lrs: core flag wait timeout block %d\n", blockIdx.x);
-                    __trap();
-                  }
-                }
-              }
-            fence_proxy_async_global();  // the T2 rows are read through TMA (async proxy)
-          }
           if (tk >= 0 && !waited) {
-            if (!p.flags) pdl_wait();
+            pdl_wait();
             pdl_launch_dependents();
             waited = true;
           }
@@ -568,14 +544,6 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   tc_fence_before();
   __syncthreads();
   if (WTRACE(p) && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x + 2] = gtimer();
-  if (p.flags && threadIdx.x == 0) {  // the last CTA out advances the forward counter
-    __threadfence();
-    if (atomicAdd(p.done, 1) == static_cast<int>(gridDim.x) - 1) {
-      atomicExch(p.done, 0);
-      __threadfence();
-      atomicAdd(p.epoch, 1);
-    }
-  }
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();

@@ -97,9 +97,6 @@ PLANS = [  # planner overrides (read at create): tile shape, persistent grid, T1
     ("c2", {"LRS_CORE_T1_NOSWZ": "1"}),                                     # SWIZZLE_NONE T1 window
     ("c2", {"LRS_CORE_IPT": "2", "LRS_CORE_TH": "7", "LRS_CORE_GRID": "4", "LRS_CORE_GSTREAM": "1"}),  # G streamed
     ("c3", {"LRS_CORE_GRID": "5", "LRS_CORE_GSTREAM": "1"}),
-    ("c2", {"LRS_FLAGS": "1"}),                                             # per-tile T2 flags
-    ("c2", {"LRS_FLAGS": "1", "LRS_CORE_IPT": "2", "LRS_CORE_TH": "7", "LRS_CORE_GRID": "3"}),
-    ("c3", {"LRS_FLAGS": "1", "LRS_CORE_GRID": "4"}),
     ("c3", {"LRS_CORE_GRID": "7"}),
     ("c3", {"LRS_CORE_IPT": "2", "LRS_CORE_TH": "3", "LRS_CORE_GRID": "4"}),
     ("c3", {"LRS_CORE_IPT": "1", "LRS_CORE_TH": "7", "LRS_CORE_T1_NOSWZ": "1"}),
