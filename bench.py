@@ -413,9 +413,12 @@ def main():
         if with_rem and g_rem is not None:
             g_rem.replay()
 
-    # ---- warm-up
+    # ---- warm-up (every graph the timed region replays is replayed once here: a graph's
+    # first replay uploads it, which must not land in the timed region)
     for _ in range(max(1, math.ceil(W / n_sets))):
         g_full.replay()
+    if g_rem is not None:
+        g_rem.replay()
     torch.cuda.synchronize(dev)
 
     def barrier():
