@@ -74,7 +74,8 @@ struct CoreParams {
   int nacc;
   uint32_t tmem_cols;
   uint32_t off_g, off_t1, off_bar;
-  int dbg;           // experiment bits (LRS_CORE_DBG): 1 skip the depthwise loop, 2 skip its T2 stores
+  int dbg;           // experiment bits (LRS_CORE_DBG): 1 skip the depthwise loop, 2 skip its T2 stores,
+                     // 4 skip the X / U loads (timing only)
   const float* cpb;  // CP core (CPDW kernels): B [kh][R1p], C [kw][R1p] fp32
   const float* cpc;
   unsigned long long* trace;  // optional globaltimer stamps (LRS_WCONV_DEBUG builds, tools/ctrace.py)
@@ -178,6 +179,10 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
           if (ix >= p.ns_x) mbar_wait(&empty_x[s], ((ix / p.ns_x) - 1) & 1);
           CTRACE(p, blockIdx.x == 0 && c == 0 && k < 4, 8200 + 10 * k + 1);
           uint8_t* dst = smem + s * p.x_slot;
+          if (p.dbg & 4) {  // timing experiment: no X / U loads (stale shared memory, wrong T2)
+            mbar_arrive(&full_x[s]);
+            continue;
+          }
           mbar_arrive_expect_tx(&full_x[s], p.x_bytes + p.u_bytes);
           tma_load_4d(dst, &p.tmX, &full_x[s], c * 64, -p.pw, ho0 - p.ph, g * p.ipt);
           tma_load_2d(dst + p.u_off, &p.tmU, &full_x[s], c * 64, 0);
