@@ -102,6 +102,11 @@ typedef struct lrs_conv_desc {
  * the 2:4 sparse tensor cores (lrs_conv_sparse_engine() == 1); S is split at
  * create into exact 2:4 main and residual blocks (PAPER.md:171-191 evaluated
  * exactly).
+ * bf16 stride-1 layers run a1 + a2 (or a1 + the CP depthwise pair) in one
+ * kernel whose tile plan is chosen at create by timing a few candidate plans
+ * on the device (back-to-back forwards on zero-filled scratch of batch_max
+ * images; ~ms; synchronous on a private stream).  Every plan computes the same
+ * bits.  LRS_NO_AUTOTUNE=1 in the environment keeps the cost model's plan.
  * OUT_OF_MEMORY / CUDA: allocation or driver failure (no handle is returned).
  */
 lrs_status lrs_conv_create(const lrs_conv_desc *desc, int device, lrs_conv **out);
