@@ -499,7 +499,7 @@ def main():
     # With the co-resident schedule (the a1+a2 kernel on the SMs the fused kernel leaves
     # free, overlapping under PDL) the per-launch event intervals overlap and each includes
     # the other kernel's time; the fused expansion + sparse kernel is then the dominant one
-    # (serialized ncu launch list, profiles/r01_v15_ncu_launches_c2_bf16.csv: 20.7 vs 17.4 us)
+    # (serialized ncu launch list, profiles/r01_v16_ncu_launches_c2_bf16.csv: 20.7 vs 16.7 us)
     if avg.get("a345_expand_sparse", 0.0) > 0.0 and sum(avg.values()) > 1.2 * ms_per_step:
         dom = "a345_expand_sparse"
     kernel_overlap = sum(avg.values()) > 1.2 * ms_per_step

@@ -5,11 +5,11 @@ import csv, json, os, subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REPS = {  # config -> (report under gpurun_out/, kernel, round tag)
-    "c2_bf16": ("prof_wconv_c2.ncu-rep", "lrs_wconv_kernel", "r01_v15"),
-    "c3": ("prof_wconv_c3.ncu-rep", "lrs_wconv_kernel", "r01_v15"),
-    "c4": ("prof_wconv_c4.ncu-rep", "lrs_wconv_kernel", "r01_v15"),
-    "c2_f32": ("prof_spadd_c2_f32.ncu-rep", "lrs_spadd_kernel", "r01_v15"),
-    "c1": ("prof_tiny_c1.ncu-rep", "lrs_tiny_kernel", "r01_v15"),
+    "c2_bf16": ("prof_wconv_c2.ncu-rep", "lrs_wconv_kernel", "r01_v16"),
+    "c3": ("prof_wconv_c3.ncu-rep", "lrs_wconv_kernel", "r01_v16"),
+    "c4": ("prof_wconv_c4.ncu-rep", "lrs_wconv_kernel", "r01_v16"),
+    "c2_f32": ("prof_spadd_c2_f32.ncu-rep", "lrs_spadd_kernel", "r01_v16"),
+    "c1": ("prof_tiny_c1.ncu-rep", "lrs_tiny_kernel", "r01_v16"),
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
