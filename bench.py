@@ -1,19 +1,27 @@
 #!/usr/bin/env python
 """Benchmark of the B200 compressed convolution W ~ L + S (arXiv 2006.06443).
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_bf16] [--impl lrs|reference]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl lrs|reference]
 (N > 1: launched by torchrun, one process per GPU; RANK/WORLD_SIZE from env.)
 
 A step = one forward of the whole hot path (a1 projection, a2 core, a3
-expansion + a4 sparse + a5 sum/store) over one batch of the workload
-(default BASELINE.json configs[1] = C2, ResNet-50 layer3 3x3 256->256 at
-14x14, batch 64, bf16).  Weak scaling: every rank runs its own batch (its
-own seeded images, same weights); there is no collective on the data path.
+expansion + a4 sparse + a5 sum/store) over one batch of the workload.
+Default workload: BASELINE.json configs[2] = C3, the largest compressed-conv
+layer (ResNet-50 layer4 3x3 512->512 at 7x7, batch 256, Tucker-2 (128,128),
+5 % S, bf16).  Strong scaling at N > 1: the config's global batch is split
+over the ranks (dist.shard_range; --scaling weak gives every rank a full
+batch); weights are replicated, no collective on the data path.
 
 Timing: W untimed warm-up steps, then EXACTLY K steps replayed from a CUDA
 graph, bracketed by barrier + cuda.synchronize; CUDA events on the launching
-stream; max over ranks.  Inputs rotate over enough X/Y buffer sets to cover
-2.1x the L2, so every step reads X from HBM.  Rank 0 prints ONE JSON line.
+stream; max over ranks.  Inputs rotate over enough X/Y buffer sets of
+DISTINCT seeded images to cover 2.1x the L2, so every step reads X from
+HBM; >= 10 further replays are timed one by one (median reported).  After
+timing (untimed): every rotating Y is checked bitwise against an eager
+forward of its X, the shards of set 0 are gathered over NCCL and compared
+bitwise with a 1-GPU forward of the whole batch and, on sampled images, with
+the fp64 oracle.  Refuses to run with LRS_* experiment variables set.
+Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -53,11 +61,16 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c2_bf16", choices=sorted(workloads.CONFIGS) + sorted(workloads.CP_CONFIGS) + ["c5"])
+    ap.add_argument("--config", default="c3", choices=sorted(workloads.CONFIGS) + sorted(workloads.CP_CONFIGS) + ["c5"])
     ap.add_argument("--impl", default="lrs", choices=["lrs", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: strong = the config's global batch split over the ranks (default), "
+                         "weak = a full batch per rank")
+    ap.add_argument("--replays", type=int, default=10, help="separately timed graph replays (median reported)")
+    ap.add_argument("--no-dense", action="store_true", help="skip the cuDNN dense context row")
     return ap.parse_args()
 
 
@@ -76,11 +89,11 @@ def cpu_threads() -> int:
         return 1
 
 
-def oracle_rate(cfg, inp, seconds: float, sample_images: int):
+def oracle_rate(cfg, inp, seconds: float, sample_images: int, x_all):
     """Time the fp64 oracle (forward_factored, as it stands) on a bounded
     sample of the workload: repeated calls on `sample_images` images."""
     from oracle import lrs_oracle as O
-    x = inp.x[:sample_images].astype(np.float64)
+    x = x_all[:sample_images].astype(np.float64)
     calls, t0 = 0, time.perf_counter()
     while True:
         if isinstance(inp, workloads.CpInputs):
@@ -149,7 +162,8 @@ def run_reference(args, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    sample = max(1, min(cfg.batch, 8))
+    # a bounded sample per step: 8 images (2 for C3, whose fp64 oracle takes ~70 ms/image)
+    sample = max(1, min(cfg.batch, 2 if cfg.c_in >= 512 else 8))
     is_cp = args.config in workloads.CP_CONFIGS
     inp = (workloads.generate_cp if is_cp else workloads.generate)(cfg, batch=sample)
     from oracle import lrs_oracle as O
@@ -170,12 +184,12 @@ def run_reference(args, cfg):
     value = args.steps * sample / el
     line = {"metric": METRIC, "value": value, "unit": "images/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, workloads/)",
-            "config": {"workload": CONFIG_TEXT[args.config], "images_per_step": sample},
+            "config": {"workload": CONFIG_TEXT[args.config], "config_id": args.config, "images_per_step": sample},
             "cpu_baseline": {"value": value, "unit": "images/s", "cores": cpu_threads(), "kind": "oracle",
                              "sample": f"{sample} images of {args.config} per step (fp64 numpy oracle, "
-                                       f"{'forward_cp' if is_cp else 'forward_factored'})"},
+                                       f"{'forward_cp' if is_cp else 'forward_factored'})", **host_info()},
             "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -203,6 +217,46 @@ def run_reference_c5(args):
                              "sample": "1 image per step through the fp64 reference network"},
             "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def network_work(model, x1, comp):
+    """Algorithmic bytes and FLOPs of ONE image through the compressed ResNet-50, from
+    forward hooks: every conv / pool / linear / compressed layer reads its input and
+    writes its output once (bf16), every bottleneck reads its identity once for the
+    residual add; BN is folded and ReLU / add fused.  FLOPs: 2 per MAC of
+    the dense convs and FC, and each compressed layer's chain + in-bounds sparse term."""
+    import torch
+    from paper_2006_06443_b200 import roofline as RL
+    lay = {id(c): c for c in comp.values()}
+    acc = {"bytes": 0.0, "flops": 0.0}
+    hooks = []
+
+    def hook(m, inp, out):
+        i, o = inp[0], out
+        acc["bytes"] += 2.0 * (i.numel() + o.numel())
+        if isinstance(m, torch.nn.Conv2d):
+            acc["flops"] += 2.0 * o.numel() * m.in_channels * m.kernel_size[0] * m.kernel_size[1] / m.groups
+        elif isinstance(m, torch.nn.Linear):
+            acc["flops"] += 2.0 * m.in_features * m.out_features * o.shape[0]
+        elif hasattr(m, "c") and id(m.c) in lay:
+            c = m.c
+            acc["flops"] += RL.layer_work(c.cfg, 1, workloads.generate_weights(c.cfg).col_idx)["layer"]["flops"]
+
+    def block_hook(m, inp, out):
+        acc["bytes"] += 2.0 * out.numel()  # the identity read of the residual add
+
+    for name, m in model.named_modules():
+        if isinstance(m, (torch.nn.Conv2d, torch.nn.Linear, torch.nn.MaxPool2d, torch.nn.AdaptiveAvgPool2d)) or (
+                hasattr(m, "c") and id(getattr(m, "c")) in lay):
+            hooks.append(m.register_forward_hook(hook))
+        if type(m).__name__ == "Bottleneck":
+            hooks.append(m.register_forward_hook(block_hook))
+    with torch.no_grad():
+        model(x1)
+    torch.cuda.synchronize()
+    for h in hooks:
+        h.remove()
+    return acc
 
 
 def main_c5(args):
@@ -292,18 +346,39 @@ def main_c5(args):
             model(x)
     torch.cuda.synchronize(dev)
     peaks = RL.measured_peaks()
-    fma = RL.fp32_fma_tflops(peaks["sm_max_mhz"])
     tot = {}
-    sparse_flops = 0.0
+    lay_bytes = lay_flops = lay_roof_s = 0.0
     for idx, c in comp.items():
         st = c.layer.stage_times(reset=True)
         for k, v in st.items():
             if v[1]:
                 tot[k] = tot.get(k, 0.0) + v[0] / v[1]
-        sparse_flops += RL.layer_work(c.cfg, per, workloads.generate_weights(c.cfg).col_idx)["layer"]["flops_sparse"]
+        wk = RL.layer_work(c.cfg, per, workloads.generate_weights(c.cfg).col_idx)
+        lay_bytes += wk["layer"]["bytes"]
+        lay_flops += wk["layer"]["flops"]
+        lay_roof_s += RL.layer_roofs(wk, peaks, "bf16")["t_literal_s"]
         c.layer.set_timing(False)
-    t_a345 = tot["a345_expand_sparse"] / 1e3
-    achieved = sparse_flops / t_a345 / 1e12
+    t_layers = sum(tot.values()) / 1e3
+    # network roof: algorithmic activation traffic of every compute op (input
+    # read + output written once; residual identity read once; BN folded, ReLU / add fused)
+    # and FLOPs (dense convs + FC + the compressed layers' chain + sparse term), per image
+    net = network_work(model, x[:1], comp)
+    t_net_img = max(net["bytes"] / (peaks["hbm_gbs"] * 1e9), net["flops"] / (peaks["bf16_tflops"] * 1e12))
+    ach_gbs = net["bytes"] * value / world / 1e9  # per GPU
+    roof = {"bound": "hbm" if net["bytes"] / peaks["hbm_gbs"] >= net["flops"] / peaks["bf16_tflops"] / 1e3 else
+            "tensor", "unit": "GB/s", "achieved": ach_gbs, "peak": peaks["hbm_gbs"],
+            "frac": ach_gbs / peaks["hbm_gbs"], "traffic": None, "kernel": "whole network (CUDA graph)",
+            "peak_kind": "measured (MEASURED_PEAKS.json)",
+            "network_roof_images_per_s_per_gpu": 1.0 / t_net_img,
+            "frac_of_network_roof": (value / world) * t_net_img,
+            "per_image": {"bytes": net["bytes"], "flops": net["flops"]},
+            "what": "network roof max(bytes / HBM, FLOPs / bf16 peak) per image vs measured images/s per GPU; "
+                    "bytes = every op's input read + output written once + residual reads (BN folded, "
+                    "ReLU / add fused), FLOPs = dense convs + FC + compressed layers (chain + sparse)",
+            "compressed_layers": {"kernel_us_sum": t_layers * 1e6, "literal_roof_us_sum": lay_roof_s * 1e6,
+                                  "frac_literal": lay_roof_s / t_layers if t_layers else None,
+                                  "bytes": lay_bytes, "flops": lay_flops,
+                                  "stage_us_sum_16_layers": {k: round(v * 1e3, 1) for k, v in tot.items()}}}
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -330,13 +405,7 @@ def main_c5(args):
         "clocks": sampler.summary(),
         "e2e": e2e,
         "gpu_launches": sum(c.layer.launches_per_forward for c in comp.values()) * K,
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": fma, "unit": "TFLOP/s", "frac": achieved / fma,
-                     "traffic": None, "kernel": "a345_expand_sparse (16 compressed layers)",
-                     "work": "in-bounds sparse MACs x 2 of the 16 layers / their summed kernel time",
-                     "engine": "2:4 sparse tensor cores (tcgen05.mma.sp) fused with the expansion GEMM",
-                     "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (the sparse term's "
-                                    "CUDA-core roof, SURVEY §8d three-roof)",
-                     "stage_us_sum_16_layers": {k: round(v * 1e3, 1) for k, v in tot.items()}},
+        "roofline": roof,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
@@ -345,8 +414,72 @@ def main_c5(args):
         dist.destroy_process_group()
 
 
+class ShardPlan:
+    """How bench.py splits a layer workload over `world` ranks.
+    strong (default at world > 1): the config's global batch is fixed and rank r takes
+    images [start, end) = dist.shard_range(batch, r, world) of every rotating input set;
+    set i's global X is workloads.generate_x(cfg, batch, seed=i), so the shards of all
+    ranks together are exactly the 1-GPU input.  weak: every rank runs a full batch of
+    its own images (seed 1000 (rank + 1) + i).  Used by the gloo test
+    (tests/test_dist_cpu.py) to run the bench's own partition on CPU."""
+
+    def __init__(self, cfg, rank: int, world: int, scaling: str = "strong"):
+        from paper_2006_06443_b200.dist import shard_range
+        self.cfg, self.rank, self.world = cfg, rank, world
+        self.strong = scaling == "strong" and world > 1
+        self.global_batch = cfg.batch if (self.strong or world == 1) else cfg.batch * world
+        self.start, self.end = shard_range(self.global_batch, rank, world) if self.strong else (0, cfg.batch)
+
+    def seed(self, i: int) -> int:
+        return i if (self.strong or self.world == 1) else 1000 * (self.rank + 1) + i
+
+    def x(self, i: int) -> np.ndarray:
+        """this rank's images of rotating set i (NHWC, storage dtype values as float32)"""
+        full = workloads.generate_x(self.cfg, self.cfg.batch, seed=self.seed(i))
+        return full[self.start:self.end] if self.strong else full
+
+
+def refuse_experiment_env():
+    """Timing with a plan / engine override or (in experiment builds) a work-skipping
+    knob would not measure the product's own path: refuse (include/lrs_conv.h)."""
+    bad = sorted(k for k in os.environ if k.startswith("LRS_") and k != "LRS_VERBOSE")
+    if bad:
+        sys.stderr.write(f"bench.py: refusing to time with experiment variables set: {bad}\n")
+        sys.exit(2)
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "affinity_cores": len(os.sched_getaffinity(0)), "os_cpu_count": os.cpu_count()}
+
+
+def dense_weight(inp, cfg):
+    """W = L + S as a dense [Cout, Cin, k, k] tensor (the cuDNN context row's weight;
+    measurement-side arithmetic, not the product path)."""
+    import torch
+    if cfg.svd:
+        wl = np.einsum("ca,aj->jc", inp.u_in.astype(np.float64), inp.u_out.astype(np.float64))[:, :, None, None]
+    else:
+        wl = np.einsum("ca,abyx,bj->jcyx", inp.u_in.astype(np.float64), inp.core.astype(np.float64),
+                       inp.u_out.astype(np.float64), optimize=True)
+    w = wl.reshape(cfg.c_out, -1).copy()
+    rows = np.repeat(np.arange(cfg.c_out), np.diff(inp.row_ptr))
+    w[rows, inp.col_idx] += inp.values
+    return torch.from_numpy(w.reshape(cfg.c_out, cfg.c_in, cfg.k, cfg.k))
+
+
 def main():
     args = parse()
+    if args.impl != "reference":
+        refuse_experiment_env()
     if args.config == "c5":
         if args.impl == "reference":
             run_reference_c5(args)
@@ -367,13 +500,16 @@ def main():
     dev = torch.device(f"cuda:{local}")
     from paper_2006_06443_b200 import LrsConv
     from paper_2006_06443_b200 import roofline as RL
+    from paper_2006_06443_b200.dist import gather_shards
 
-    # ---- inputs: same weights everywhere, rank-specific images (weak scaling)
+    # ---- inputs.  Strong scaling (default): the config's global batch is fixed and
+    # split over the ranks (shard_range); weak: every rank runs a full batch of its own.
+    # Same weights everywhere; X set i = generate_x(cfg, seed=i) (distinct images per set).
     gen = workloads.generate_cp if is_cp else workloads.generate
-    inp = gen(cfg)
-    if rank > 0:
-        inp.x = gen(cfg, seed=1000 + rank).x
-    n = cfg.batch
+    inp = gen(cfg, batch=1)
+    plan = ShardPlan(cfg, rank, world, args.scaling)
+    strong, gb, s0, s1 = plan.strong, plan.global_batch, plan.start, plan.end
+    n = s1 - s0
     if is_cp:
         layer = LrsConv.from_cp(n, cfg.in_h, cfg.in_w, cfg.k, cfg.stride, cfg.pad, cfg.dtype, inp.a, inp.b, inp.c,
                                 inp.d, inp.row_ptr, inp.col_idx, inp.values, device=local)
@@ -385,8 +521,9 @@ def main():
     y_bytes = n * cfg.out_h * cfg.out_w * cfg.c_out * esz
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     n_sets = max(2, math.ceil(2.1 * l2 / (x_bytes + y_bytes)))
-    x0 = torch.from_numpy(inp.x).to(tdt).to(dev)
-    xs = [x0] + [x0.clone() for _ in range(n_sets - 1)]
+
+    xs_np = [plan.x(i) for i in range(n_sets)]
+    xs = [torch.from_numpy(x).to(tdt).to(dev) for x in xs_np]
     ys = [torch.empty((n, cfg.out_h, cfg.out_w, cfg.c_out), dtype=tdt, device=dev) for _ in range(n_sets)]
     stream = torch.cuda.Stream(device=dev)
 
@@ -443,8 +580,68 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     ms_per_step = ms_max / K
-    value = world * n * K / (ms_max / 1e3)
+    value = gb * K / (ms_max / 1e3)
 
+    # ---- replay statistics: >= 10 separately timed replays of the n_sets-forward graph
+    # (SURVEY §8(d) timing protocol: median of >= 10 replays), max over ranks per replay
+    reps = []
+    for _ in range(max(10, args.replays)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+            g_full.replay()
+            b.record(stream)
+        reps.append((a, b))
+    torch.cuda.synchronize(dev)
+    rep_ms = torch.tensor([a.elapsed_time(b) for a, b in reps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(rep_ms, op=dist.ReduceOp.MAX)
+    rep_us = (rep_ms.cpu().numpy() / n_sets * 1e3)
+    replays = {"n": int(len(rep_us)), "forwards_per_replay": n_sets, "median_us_per_step": float(np.median(rep_us)),
+               "min_us_per_step": float(rep_us.min()), "max_us_per_step": float(rep_us.max()),
+               "median_images_per_s": gb / (float(np.median(rep_us)) * 1e-6)}
+
+    # ---- verification, outside any timed region:
+    #  (1) every rotating set's Y (last written by the graph) is bitwise an eager forward of its X;
+    #  (2) the ranks' shards of set 0 gathered over NCCL: on rank 0, bitwise the 1-GPU Y of the
+    #      whole batch (a second handle) and, on sampled images, the fp64 oracle (bf16 2e-2 /
+    #      fp32 1e-5 relL2, per image).
+    verify = {}
+    ok_rot = True
+    for i in range(n_sets):
+        ye = torch.empty_like(ys[i])
+        layer.forward_into(xs[i], ye)
+        torch.cuda.synchronize(dev)
+        ok_rot &= bool(torch.equal(ye, ys[i]))
+    verify["rotation_bitwise_eager"] = ok_rot
+    if strong or world == 1:
+        y_full = gather_shards(ys[0], gb) if world > 1 else ys[0]
+        if rank == 0:
+            if world > 1:
+                one = LrsConv.from_inputs(inp, batch_max=gb, device=local) if not is_cp else None
+                if one is not None:
+                    x_full = torch.from_numpy(workloads.generate_x(cfg, gb, seed=plan.seed(0))).to(tdt).to(dev)
+                    y_one = torch.empty_like(y_full)
+                    one.forward_into(x_full, y_one)
+                    torch.cuda.synchronize(dev)
+                    verify["gathered_equals_1gpu_bitwise"] = bool(torch.equal(y_one, y_full))
+                    one.close()
+            if not args.no_cpu:
+                from oracle import lrs_oracle as O
+                xg = workloads.generate_x(cfg, gb, seed=plan.seed(0))
+                idx = np.unique(np.linspace(0, gb - 1, min(gb, 8)).astype(int))
+                if is_cp:
+                    ref = O.forward_cp(xg[idx].astype(np.float64), inp.a, inp.b, inp.c, inp.d, inp.row_ptr,
+                                       inp.col_idx, inp.values, cfg.stride, cfg.pad)
+                else:
+                    ref = O.forward_factored(xg[idx].astype(np.float64), inp.u_in, inp.core, inp.u_out, inp.row_ptr,
+                                             inp.col_idx, inp.values, cfg.stride, cfg.pad)
+                yv = y_full[torch.from_numpy(idx).to(dev)].float().cpu().numpy().astype(np.float64)
+                errs = [float(np.linalg.norm(yv[k] - ref[k]) / np.linalg.norm(ref[k])) for k in range(len(idx))]
+                tol = 2e-2 if cfg.dtype == "bf16" else 1e-5
+                verify["oracle_images"] = [int(i) for i in idx]
+                verify["oracle_max_rel_l2"] = max(errs)
+                verify["oracle_ok"] = max(errs) <= tol
     # ---- per-kernel durations: an event pair around every launch.  The
     # launches queue up behind a device-side sleep, so they then run back to
     # back with no host launch gaps inside the event pairs.
@@ -461,7 +658,7 @@ def main():
     # ---- end to end through the C-ABI with host buffers (H2D + forward + D2H per step)
     e2e = None
     if not args.no_e2e:
-        xh = x0.cpu().pin_memory()
+        xh = xs[0].cpu().pin_memory()
         yh = torch.empty(ys[0].shape, dtype=tdt).pin_memory()
         with torch.cuda.stream(stream):
             for _ in range(3):
@@ -480,9 +677,38 @@ def main():
         te = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * n * ke / (float(te.item()) / 1e3), "unit": "images/s",
+        e2e = {"value": gb * ke / (float(te.item()) / 1e3), "unit": "images/s",
                "h2d_bytes_per_step": x_bytes, "d2h_bytes_per_step": y_bytes, "steps": ke,
-               "api": "lrs_conv_forward_host (pinned host buffers)"}
+               "api": "lrs_conv_forward_host (pinned host buffers)",
+               "note": "bytes are per rank (its shard); value is the whole job"}
+        torch.cuda.synchronize(dev)
+        ok_e2e = bool(torch.equal(yh, ys[0].cpu()))
+        verify["e2e_bitwise_device_forward"] = ok_e2e
+
+    # ---- context: cuDNN dense conv of the reconstructed W = L + S, same images, same
+    # rotation (PAPER.md:210-223 -- the paper's "original layer")
+    dense = None
+    if not is_cp and not args.no_dense:
+        wd = dense_weight(inp, cfg).to(tdt).to(dev).contiguous(memory_format=torch.channels_last)
+        xd = [x.permute(0, 3, 1, 2) for x in xs]  # channels_last NCHW views of the NHWC buffers
+        with torch.backends.cudnn.flags(enabled=True, benchmark=True):
+            with torch.cuda.stream(stream):
+                for i in range(n_sets):
+                    torch.nn.functional.conv2d(xd[i], wd, stride=cfg.stride, padding=cfg.pad)
+            torch.cuda.synchronize(dev)
+            ke = max(n_sets, (K // n_sets) * n_sets)
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                d0.record(stream)
+                for i in range(ke):
+                    torch.nn.functional.conv2d(xd[i % n_sets], wd, stride=cfg.stride, padding=cfg.pad)
+                d1.record(stream)
+            torch.cuda.synchronize(dev)
+        us = d0.elapsed_time(d1) / ke * 1e3
+        dense = {"us_per_step": us, "images_per_s": n / (us * 1e-6), "steps": ke,
+                 "what": "torch.nn.functional.conv2d (cuDNN, benchmark mode) of the dense W = L + S, "
+                         f"{cfg.dtype}, channels_last, this rank's {n} images, same X rotation (eager launches)",
+                 "compressed_speedup": us / (ms_per_step * 1e3)}
 
     if rank != 0:
         if world > 1:
@@ -490,7 +716,7 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel + layer roofs
+    # ---- roofline of the dominant kernel + layer roofs (per GPU: this rank's n images)
     peaks = RL.measured_peaks()
     work = RL.layer_work(cfg, n, inp.col_idx, cp=is_cp)
     roofs = RL.layer_roofs(work, peaks, cfg.dtype)
@@ -499,57 +725,21 @@ def main():
     # With the co-resident schedule (the a1+a2 kernel on the SMs the fused kernel leaves
     # free, overlapping under PDL) the per-launch event intervals overlap and each includes
     # the other kernel's time; the fused expansion + sparse kernel is then the dominant one
-    # (serialized ncu launch list, profiles/r01_v16_ncu_launches_c2_bf16.csv: 20.7 vs 16.7 us)
-    if avg.get("a345_expand_sparse", 0.0) > 0.0 and sum(avg.values()) > 1.2 * ms_per_step:
-        dom = "a345_expand_sparse"
+    # (serialized ncu launch list, profiles/)
     kernel_overlap = sum(avg.values()) > 1.2 * ms_per_step
+    if avg.get("a345_expand_sparse", 0.0) > 0.0 and kernel_overlap:
+        dom = "a345_expand_sparse"
     t_dom = avg[dom] / 1e3
-    fma_peak = RL.fp32_fma_tflops(peaks["sm_max_mhz"])
-    tc_peak = peaks["bf16_tflops"] * (1.0 if cfg.dtype == "bf16" else 0.5 / 3.0)  # fp32: 3xTF32 at TF32 = bf16/2
-    eng = layer.sparse_engine[0]
-    wk = work[dom]
-    # the dominant kernel's algorithmic work per pipe: HBM bytes, FP32-pipe flops (the
-    # sparse term -- SURVEY §8d three-roof -- plus whatever the kernel computes on the
-    # CUDA cores), tensor-pipe flops; its roofline bound is the pipe with the largest
-    # roof time, frac = that roof time / the measured kernel time
-    if dom in ("a345_expand_sparse", "a4_sparse_add"):
-        if eng == 3:  # the one-kernel fp32 path: the whole layer on the CUDA cores
-            lay = work["layer"]
-            b_alg, f_fma, f_tc = lay["bytes"], lay["flops_chain"] + lay["flops_sparse"], 0.0
-        elif eng == 2:  # expansion + sparse term on the CUDA cores
-            b_alg, f_fma, f_tc = wk["bytes"], wk["flops_sparse"] + wk["flops_tc"], 0.0
-        else:  # tensor-core expansion (+ 2:4 tensor-core or SIMT sparse term)
-            b_alg, f_fma, f_tc = wk["bytes"], wk["flops_sparse"], wk["flops_tc"]
-    else:
-        b_alg, f_fma, f_tc = wk["bytes"], 0.0, wk["flops"]
-    roofs_k = {"hbm": (b_alg / (peaks["hbm_gbs"] * 1e9), b_alg / t_dom / 1e9, peaks["hbm_gbs"], "GB/s"),
-               "alu": (f_fma / (fma_peak * 1e12), f_fma / t_dom / 1e12, fma_peak, "TFLOP/s"),
-               "tensor": (f_tc / (tc_peak * 1e12), f_tc / t_dom / 1e12, tc_peak, "TFLOP/s")}
-    bound = max(roofs_k, key=lambda k: roofs_k[k][0])
-    t_roof, achieved, peak, unit = roofs_k[bound]
-    roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-            "traffic": None, "kernel": dom,
-            "work": {"bytes": b_alg, "fp32_pipe_flops": f_fma, "tensor_flops": f_tc,
-                     "roof_us": {k: v[0] * 1e6 for k, v in roofs_k.items()}, "kernel_us": t_dom * 1e6},
-            "engine": {0: "SIMT CSR gather fused into the expansion GEMM epilogue",
-                       1: "2:4 sparse tensor cores (tcgen05.mma.sp), fused with the expansion GEMM",
-                       2: "SIMT expansion + CSR gather over 4-image shared-memory windows, Y written once",
-                       3: "the whole fp32 layer in one SIMT kernel"}.get(eng, "?"),
-            "peak_source": {"hbm": "MEASURED_PEAKS.json hbm_gbs",
-                            "alu": "derived: 148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (SURVEY §8d three-roof)",
-                            "tensor": "MEASURED_PEAKS.json bf16_tflops" + (" x 1/6 (3xTF32)" if cfg.dtype != "bf16"
-                                                                          else "")}[bound]}
-    roof["peak_kind"] = peaks["source"]
+    roof = RL.kernel_roofline(dom, work, peaks, cfg.dtype, t_dom, layer.sparse_engine[0])
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
     # (tools/ncu_traffic.py -> profiles/ncu_traffic.json); per launch, cold cache
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f).get(args.config)
-        if tr:
+        if tr and tr.get("kernel_stage", dom) == dom:
             roof["traffic"] = tr["dram_read_bytes"] + tr["dram_write_bytes"]
             roof["traffic_detail"] = {"kernel": tr["kernel"], "dram_read_bytes": tr["dram_read_bytes"],
-                                      "dram_write_bytes": tr["dram_write_bytes"], "source": tr["source"],
-                                      "note": "Y's write-back mostly lands in L2 after the kernel ends"}
+                                      "dram_write_bytes": tr["dram_write_bytes"], "source": tr["source"]}
     except (OSError, ValueError, KeyError):
         pass
     roof["stage_us"] = {k: round(v * 1e3, 3) for k, v in avg.items()}
@@ -560,31 +750,47 @@ def main():
     layer_roof = {"literal_roof_us": roofs["t_literal_s"] * 1e6, "three_roof_us": roofs["t_three_roof_s"] * 1e6,
                   "frac_literal": roofs["t_literal_s"] / step_s, "frac_three_roof": roofs["t_three_roof_s"] / step_s,
                   "t_hbm_us": roofs["t_hbm_s"] * 1e6, "t_chain_tc_us": roofs["t_chain_tc_s"] * 1e6,
-                  "t_sparse_fma_us": roofs["t_sparse_fma_s"] * 1e6}
+                  "t_sparse_tc_us": roofs["t_sparse_tc_s"] * 1e6, "t_sparse_fma_us": roofs["t_sparse_fma_s"] * 1e6,
+                  "fp32_fma_peak_tflops": roofs["fma_tflops"],
+                  "fp32_fma_peak_kind": roofs["fma_kind"],
+                  "what": "whole layer (all kernels) per GPU: literal = max(bytes / HBM, all FLOPs incl. the sparse "
+                          "term / tensor peak) (BASELINE.json north star); three-roof puts the sparse MACs on the "
+                          "FP32 pipe (SURVEY §8d)"}
+    eng, mb, rb = layer.sparse_engine
+    if eng == 1:
+        # the 2:4 engine's own floor: its dense-equivalent MMA work at the 2:4 rate (no
+        # more useful work per block than 128 x 64 logical slots, whatever the density)
+        layer_roof["engine_floor_us"] = RL.sparse24_floor_s(cfg, n, mb, rb, peaks) * 1e6
 
     cpu = None
     if world == 1 and not args.no_cpu:
         sample = max(1, min(n, 8))
-        rate, calls, el = oracle_rate(cfg, inp, args.cpu_seconds, sample)
+        rate, calls, el = oracle_rate(cfg, inp, args.cpu_seconds, sample, xs_np[0])
         cpu = {"value": rate, "unit": "images/s", "cores": cpu_threads(), "kind": "oracle",
                "sample": f"{calls} oracle forwards x {sample} images of {args.config} ({el:.1f} s, fp64 numpy "
-                         "forward_factored; BLAS threads = cores, sparse scatter single-threaded)"}
+                         "forward_factored; BLAS threads = cores, sparse scatter single-threaded)",
+               **host_info()}
 
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if (strong or world == 1) else "weak",
+        "vs_baseline": None,
         "dtype": cfg.dtype, "data": "synthetic (seeded ReLU(N(0,1)) images, N(0,1/fan_in) factors, uniform S)",
-        "config": {"workload": CONFIG_TEXT[args.config], "config_id": args.config, "global_batch": n * world,
+        "config": {"workload": CONFIG_TEXT[args.config], "config_id": args.config, "global_batch": gb,
                    "per_gpu_batch": n, "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
-                   "l2": f"{n_sets} rotating X/Y buffer sets = {n_sets * (x_bytes + y_bytes) / 2**20:.0f} MiB "
-                         f"(2.1x L2 {l2 / 2**20:.0f} MiB)",
+                   "l2": f"{n_sets} rotating X/Y buffer sets of distinct images = "
+                         f"{n_sets * (x_bytes + y_bytes) / 2**20:.0f} MiB (2.1x L2 {l2 / 2**20:.0f} MiB)",
                    "timing": "CUDA graph replay, CUDA events, max over ranks"},
         "clocks": sampler.summary(),
         "e2e": e2e,
         "gpu_launches": layer.launches_per_forward * K,
         "roofline": roof,
         "roofline_layer": layer_roof,
+        "replays": replays,
+        "verify": verify,
+        "dense_context": dense,
         "cpu_baseline": cpu,
+        "host": host_info(),
     }
     print(json.dumps(line), flush=True)
     if world > 1:

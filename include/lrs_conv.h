@@ -24,9 +24,24 @@
  *     strictly increasing within a row (the OIHW flattening).
  * No bias: the paper's layer has none.
  *
- * No function aborts or prints.  Every function returns an lrs_status;
+ * No function aborts.  Every function returns an lrs_status;
  * lrs_conv_last_error() gives the text of the last non-OK status of the
  * calling thread.  There is no CPU fallback: a missing GPU is LRS_ERR_CUDA.
+ * Nothing is printed unless LRS_VERBOSE is set (plan lines on stderr).  A
+ * kernel whose pipeline wait exceeds ~9 s (a protocol bug, never expected)
+ * traps: the launch fails with a CUDA error instead of hanging the device.
+ *
+ * Environment (read at create): LRS_VERBOSE; plan / engine overrides used by
+ * the tests to cover every path -- LRS_NO_AUTOTUNE, LRS_NO_CORE, LRS_NO_TINY,
+ * LRS_F32_FUSED, LRS_CORE_{IPT,TH,GRID,GSTREAM,T1_NOSWZ}, LRS_TINY_CB,
+ * LRS_WCONV_{TH,CB,CPW,NS,BPI,REUSE,NWB1,ERING} -- each selects another plan
+ * that computes the same Y.  Knobs that skip work (timing bisection) exist
+ * only in -DLRS_EXPERIMENTS builds; bench.py refuses to time with any LRS_*
+ * variable set.
+ *
+ * Threads: a handle keeps host-side per-call state (tensor-map caches, launch
+ * parameters), so calls on ONE handle must not run concurrently from several
+ * host threads; use one handle per thread (distinct handles are independent).
  */
 #ifndef LRS_CONV_H_
 #define LRS_CONV_H_
@@ -58,7 +73,7 @@ typedef enum {
                            paper's two depthwise convolutions         */
 } lrs_core_kind;
 
-typedef struct lrs_conv lrs_conv; /* opaque; immutable after create */
+typedef struct lrs_conv lrs_conv; /* opaque; its weights are immutable after create */
 
 typedef struct lrs_conv_desc {
   int32_t batch_max;              /* largest n accepted by forward (> 0)            */
@@ -106,7 +121,9 @@ typedef struct lrs_conv_desc {
  * kernel whose tile plan is chosen at create by timing a few candidate plans
  * on the device (back-to-back forwards on zero-filled scratch of batch_max
  * images; ~ms; synchronous on a private stream).  Every plan computes the same
- * bits.  LRS_NO_AUTOTUNE=1 in the environment keeps the cost model's plan.
+ * bits.  LRS_NO_AUTOTUNE=1 in the environment keeps the cost model's plan, and
+ * so does a scratch allocation that runs out of memory (any other CUDA error
+ * during tuning is LRS_ERR_CUDA).
  * OUT_OF_MEMORY / CUDA: allocation or driver failure (no handle is returned).
  */
 lrs_status lrs_conv_create(const lrs_conv_desc *desc, int device, lrs_conv **out);

@@ -42,7 +42,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     tmp = LIB + ".tmp"
-    extra = ["-DLRS_WCONV_DEBUG"] if os.environ.get("LRS_WCONV_DEBUG") else []  # tools/wtrace.py experiments
+    # experiment builds (tools/ only): work-skipping debug knobs and pipeline trace stamps;
+    # the production library (the default) compiles them out
+    extra = []
+    if os.environ.get("LRS_EXPERIMENTS"):
+        extra += ["-DLRS_EXPERIMENTS", "-DLRS_WCONV_DEBUG"]
+    elif os.environ.get("LRS_WCONV_DEBUG"):
+        extra += ["-DLRS_WCONV_DEBUG"]  # tools/wtrace.py experiments
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", tmp, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = r.stdout + r.stderr

@@ -372,7 +372,11 @@ cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void* param, size_
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
+  #ifdef LRS_EXPERIMENTS
   static const bool no_pdl = getenv("LRS_NO_PDL") != nullptr;  // timing experiments
+#else
+  constexpr bool no_pdl = false;
+#endif
   cfg.numAttrs = no_pdl ? 0 : 1;
   void* args[] = {param};
   return cudaLaunchKernelExC(&cfg, fn, args);
@@ -658,7 +662,9 @@ static void apply_core_plan(lrs_conv* h, const lrs_conv_desc* d, int ipt, int th
   c.t1_sw128 = (G.r1p % 64 == 0 && !getenv("LRS_CORE_T1_NOSWZ")) ? 1 : 0;
   c.cpb = h->w_cpb;
   c.cpc = h->w_cpc;
+  #ifdef LRS_EXPERIMENTS
   if (const char* e = getenv("LRS_CORE_DBG")) c.dbg = atoi(e);
+#endif
   c.nacc = 2 * c.acc_cols <= 512 ? 2 : 1;
   uint32_t tc = 32;
   while (tc < c.nacc * c.acc_cols) tc <<= 1;
@@ -784,7 +790,9 @@ lrs_status build_spadd(lrs_conv* h, const lrs_conv_desc* d) {
   q.th = th; q.bands = bands; q.n_nc = n_nc; q.cc = cc; q.n_cc = n_cc; q.wr = wr; q.wc = wc;
   q.pitch = pitch;
   q.max_ent = max_ent;
+  #ifdef LRS_EXPERIMENTS
   if (const char* e = getenv("LRS_SPADD_DBG")) q.dbg = atoi(e);
+#endif
   q.win_bytes = std::max(static_cast<uint32_t>(cc) * plane * 16, kSpDenseBytes);
   h->sp_smem = q.win_bytes + static_cast<uint32_t>(std::max(max_ent, 1)) * 8;
   if (h->sp_smem > 113 * 1024u) return LRS_OK;  // keep two CTAs per SM
@@ -1103,7 +1111,9 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   }
   WconvParams& w = h->wp;
   memset(&w, 0, sizeof(w));
-  if (const char* e = getenv("LRS_WCONV_DBG")) w.dbg = atoi(e);  // experiment bits (LRS_WCONV_DEBUG builds only)
+#if defined(LRS_EXPERIMENTS) || defined(LRS_WCONV_DEBUG)
+  if (const char* e = getenv("LRS_WCONV_DBG")) w.dbg = atoi(e);  // experiment bits (debug builds only)
+#endif
   w.img_sp = static_cast<const uint8_t*>(h->w_as);
   w.img_e = static_cast<const uint8_t*>(h->w_e);
   w.img_dense = static_cast<const uint8_t*>(h->w_dense_img);
@@ -1236,12 +1246,24 @@ static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d) {
   float best = 1e30f;
   int bi = -1;
   bool ready = true;
-  if (cudaMalloc(&xs, xb) != cudaSuccess || cudaMalloc(&ys, yb) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess || cudaEventCreate(&e0) != cudaSuccess ||
-      cudaEventCreate(&e1) != cudaSuccess || cudaMemsetAsync(xs, 0, xb, s) != cudaSuccess) {
-    // no room for the scratch (huge batch_max): keep the cost model's plan, not an error
-    cudaGetLastError();
-    ready = false;
+  {
+    cudaError_t e = cudaMalloc(&xs, xb);
+    if (e == cudaSuccess) e = cudaMalloc(&ys, yb);
+    if (e == cudaErrorMemoryAllocation) {
+      // no room for the scratch (huge batch_max): keep the cost model's plan, not an error
+      cudaGetLastError();
+      ready = false;
+      if (getenv("LRS_VERBOSE")) fprintf(stderr, "[lrs] autotune skipped: no memory for %zu B of scratch\n", xb + yb);
+    } else {
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreate(&e0);
+      if (e == cudaSuccess) e = cudaEventCreate(&e1);
+      if (e == cudaSuccess) e = cudaMemsetAsync(xs, 0, xb, s);
+      if (e != cudaSuccess) {  // a driver error is an error (only an OOM keeps the model's plan)
+        st = fail(LRS_ERR_CUDA, "autotune setup: %s", cudaGetErrorString(e));
+        ready = false;
+      }
+    }
   }
   for (size_t i = 0; ready && st == LRS_OK && i < plans.size(); ++i) {
     apply_core_plan(h, d, std::get<0>(plans[i]), std::get<1>(plans[i]), std::get<2>(plans[i]), std::get<3>(plans[i]));
@@ -1308,7 +1330,9 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   h->d.values = nullptr;
   h->device = device;
   h->sms = prop.multiProcessorCount;
-  if (const char* e = getenv("LRS_SKIP")) h->skip = atoi(e);
+  #ifdef LRS_EXPERIMENTS
+  if (const char* e = getenv("LRS_SKIP")) h->skip = atoi(e);  // stage skips: timing bisection only (wrong Y)
+#endif
   h->f32 = d->dtype == LRS_DTYPE_F32;
   h->svd = d->core == nullptr;
   h->cp_core = d->core_kind == LRS_CORE_CP;
@@ -1639,18 +1663,29 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   return LRS_OK;
 }
 
-lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t n, void* stream_) {
-  lrs_conv* h = const_cast<lrs_conv*>(hc);
-  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
-  if (n < 0 || n > h->d.batch_max) return fail(LRS_ERR_INVALID_ARGUMENT, "n=%d outside [0, %d]", n, h->d.batch_max);
-  if (n == 0) return LRS_OK;
-  if (!x || !y) return fail(LRS_ERR_INVALID_ARGUMENT, "x / y is NULL");
-  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(y) & 15))
-    return fail(LRS_ERR_INVALID_ARGUMENT, "x / y must be 16-byte aligned");
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  int prev = 0;
-  LRS_CUDA(cudaGetDevice(&prev));
-  if (prev != h->device) LRS_CUDA(cudaSetDevice(h->device));
+}  // extern "C"
+
+namespace {
+// Restores the caller's current device on every exit path of an ABI call.
+struct DeviceGuard {
+  int prev = -1;
+  bool switched = false;
+  cudaError_t enter(int device) {
+    cudaError_t e = cudaGetDevice(&prev);
+    if (e != cudaSuccess) return e;
+    if (prev != device) {
+      e = cudaSetDevice(device);
+      switched = e == cudaSuccess;
+    }
+    return e;
+  }
+  ~DeviceGuard() {
+    if (switched) cudaSetDevice(prev);
+  }
+};
+
+// The launches of one forward on the handle's (current) device; arguments validated.
+lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStream_t stream) {
   const bool f32 = h->f32;
   const int esz = h->esz;
   const lrs_conv_desc& d = h->d;
@@ -1677,7 +1712,6 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
     LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_tiny_kernel), dim3(static_cast<unsigned>(n * q.bands * q.cbands)),
                         dim3(kTyThreads), &q, h->tiny_smem, stream));
     if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
-    if (prev != h->device) cudaSetDevice(prev);
     return LRS_OK;
   }
   if (h->use_core && !(h->skip & 1)) {
@@ -1741,7 +1775,9 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
                           static_cast<uint64_t>(d.in_h)};
       uint64_t strides[3] = {static_cast<uint64_t>(d.in_h) * d.in_w * d.c_in * 2, static_cast<uint64_t>(d.c_in) * 2,
                              static_cast<uint64_t>(d.in_w) * d.c_in * 2};
+#if defined(LRS_EXPERIMENTS) || defined(LRS_WCONV_DEBUG)
       if (w.dbg & 32) strides[0] = 128;  // timing experiment: contiguous 1 KB per position (wrong data)
+#endif
       uint32_t box[4] = {64, 8, static_cast<uint32_t>(w.wc), static_cast<uint32_t>(w.wr)};
       uint32_t estr[4] = {1, 1, 1, 1};
       if ((st = encode_t(&w.tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box,
@@ -1759,7 +1795,6 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
     LRS_CUDA(launch_pdl(wconv_kernel_ptr(w.n_units, w.bpi), dim3(grid), dim3(kWThreads), &w,
                         h->w_smem, stream));
     if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
-    if (prev != h->device) cudaSetDevice(prev);
     return LRS_OK;
   }
   h->a3.p.m_total = static_cast<int>(P);
@@ -1782,8 +1817,26 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
                         h->sp_smem, stream));
     if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
   }
-  if (prev != h->device) cudaSetDevice(prev);
   return LRS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t n, void* stream_) {
+  // host state (tensor-map caches, per-call launch parameters) is updated here: see the
+  // header's note on concurrent host calls
+  lrs_conv* h = const_cast<lrs_conv*>(hc);
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (n < 0 || n > h->d.batch_max) return fail(LRS_ERR_INVALID_ARGUMENT, "n=%d outside [0, %d]", n, h->d.batch_max);
+  if (n == 0) return LRS_OK;
+  if (!x || !y) return fail(LRS_ERR_INVALID_ARGUMENT, "x / y is NULL");
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(y) & 15))
+    return fail(LRS_ERR_INVALID_ARGUMENT, "x / y must be 16-byte aligned");
+  DeviceGuard g;
+  LRS_CUDA(g.enter(h->device));
+  return forward_impl(h, x, y, n, static_cast<cudaStream_t>(stream_));
 }
 
 lrs_status lrs_conv_forward_host(lrs_conv* h, const void* x_host, void* y_host, int32_t n, void* stream_) {
@@ -1791,9 +1844,8 @@ lrs_status lrs_conv_forward_host(lrs_conv* h, const void* x_host, void* y_host, 
   if (n < 0 || n > h->d.batch_max) return fail(LRS_ERR_INVALID_ARGUMENT, "n=%d outside [0, %d]", n, h->d.batch_max);
   if (n == 0) return LRS_OK;
   if (!x_host || !y_host) return fail(LRS_ERR_INVALID_ARGUMENT, "x_host / y_host is NULL");
-  int prev = 0;
-  LRS_CUDA(cudaGetDevice(&prev));
-  if (prev != h->device) LRS_CUDA(cudaSetDevice(h->device));
+  DeviceGuard g;
+  LRS_CUDA(g.enter(h->device));
   const size_t xi = static_cast<size_t>(h->d.in_h) * h->d.in_w * h->d.c_in * h->esz;  // bytes per image
   const size_t yi = static_cast<size_t>(h->ho) * h->wo * h->d.c_out * h->esz;
   if (!h->hx) LRS_CUDA(cudaMalloc(&h->hx, xi * h->d.batch_max));
@@ -1808,7 +1860,9 @@ lrs_status lrs_conv_forward_host(lrs_conv* h, const void* x_host, void* y_host, 
   // chunk i+1 in, the forward of chunk i and the copy of chunk i-1 out overlap (the copy
   // engines run both directions concurrently).  Every stream starts after the caller's
   // prior work on `stream`, and `stream` ends after the last copy out, so the call keeps
-  // single-stream semantics.
+  // single-stream semantics -- also when a step fails midway: the error path still joins
+  // both copy streams into `stream` before returning, so no copy outlives the call's
+  // stream order.
   const int nch = std::max(1, std::min(4, n / 8));
   const uint8_t* xs = static_cast<const uint8_t*>(x_host);
   uint8_t* ys = static_cast<uint8_t*>(y_host);
@@ -1817,23 +1871,34 @@ lrs_status lrs_conv_forward_host(lrs_conv* h, const void* x_host, void* y_host, 
   LRS_CUDA(cudaEventRecord(h->hev[16], stream));
   LRS_CUDA(cudaStreamWaitEvent(h->hs_in, h->hev[16], 0));
   LRS_CUDA(cudaStreamWaitEvent(h->hs_out, h->hev[16], 0));
-  for (int i = 0; i < nch; ++i) {
+  lrs_status st = LRS_OK;
+  auto step = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && st == LRS_OK)
+      st = fail(e == cudaErrorMemoryAllocation ? LRS_ERR_OUT_OF_MEMORY : LRS_ERR_CUDA, "forward_host %s: %s", what,
+                cudaGetErrorString(e));
+    return st == LRS_OK;
+  };
+  for (int i = 0; i < nch && st == LRS_OK; ++i) {
     const int i0 = static_cast<int>(static_cast<long long>(n) * i / nch) / 8 * 8;
     const int i1 = i + 1 == nch ? n : static_cast<int>(static_cast<long long>(n) * (i + 1) / nch) / 8 * 8;
     if (i1 <= i0) continue;
-    LRS_CUDA(cudaMemcpyAsync(dx + i0 * xi, xs + i0 * xi, (i1 - i0) * xi, cudaMemcpyHostToDevice, h->hs_in));
-    LRS_CUDA(cudaEventRecord(h->hev[i], h->hs_in));
-    LRS_CUDA(cudaStreamWaitEvent(stream, h->hev[i], 0));
-    lrs_status st = lrs_conv_forward(h, dx + i0 * xi, dy + i0 * yi, i1 - i0, stream_);
-    if (st != LRS_OK) return st;
-    LRS_CUDA(cudaEventRecord(h->hev[8 + i], stream));
-    LRS_CUDA(cudaStreamWaitEvent(h->hs_out, h->hev[8 + i], 0));
-    LRS_CUDA(cudaMemcpyAsync(ys + i0 * yi, dy + i0 * yi, (i1 - i0) * yi, cudaMemcpyDeviceToHost, h->hs_out));
+    if (!step(cudaMemcpyAsync(dx + i0 * xi, xs + i0 * xi, (i1 - i0) * xi, cudaMemcpyHostToDevice, h->hs_in), "H2D"))
+      break;
+    if (!step(cudaEventRecord(h->hev[i], h->hs_in), "event")) break;
+    if (!step(cudaStreamWaitEvent(stream, h->hev[i], 0), "wait")) break;
+    if ((st = forward_impl(h, dx + i0 * xi, dy + i0 * yi, i1 - i0, stream)) != LRS_OK) break;
+    if (!step(cudaEventRecord(h->hev[8 + i], stream), "event")) break;
+    if (!step(cudaStreamWaitEvent(h->hs_out, h->hev[8 + i], 0), "wait")) break;
+    step(cudaMemcpyAsync(ys + i0 * yi, dy + i0 * yi, (i1 - i0) * yi, cudaMemcpyDeviceToHost, h->hs_out), "D2H");
   }
-  LRS_CUDA(cudaEventRecord(h->hev[17], h->hs_out));
-  LRS_CUDA(cudaStreamWaitEvent(stream, h->hev[17], 0));
-  if (prev != h->device) cudaSetDevice(prev);
-  return LRS_OK;
+  // join: `stream` waits for both copy streams (also on the error path)
+  cudaError_t e1 = cudaEventRecord(h->hev[17], h->hs_out);
+  if (e1 == cudaSuccess) e1 = cudaStreamWaitEvent(stream, h->hev[17], 0);
+  cudaError_t e2 = cudaEventRecord(h->hev[16], h->hs_in);
+  if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(stream, h->hev[16], 0);
+  step(e1, "join");
+  step(e2, "join");
+  return st;
 }
 
 lrs_status lrs_conv_destroy(lrs_conv* h) {
@@ -1980,7 +2045,9 @@ lrs_status lrs_conv_debug_trace(lrs_conv* h, void* dev_buf) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
   h->wp.trace = static_cast<unsigned long long*>(dev_buf);
   h->cp.trace = static_cast<unsigned long long*>(dev_buf);  // core kernel: indices 8190..13095
+#if defined(LRS_EXPERIMENTS) || defined(LRS_WCONV_DEBUG)
   if (const char* e = getenv("LRS_WCONV_DBG")) h->wp.dbg = atoi(e);
+#endif
   return LRS_OK;
 }
 

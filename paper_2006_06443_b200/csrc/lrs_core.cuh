@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
           if (ix >= p.ns_x) mbar_wait(&empty_x[s], ((ix / p.ns_x) - 1) & 1);
           CTRACE(p, blockIdx.x == 0 && c == 0 && k < 4, 8200 + 10 * k + 1);
           uint8_t* dst = smem + s * p.x_slot;
-          if (p.dbg & 4) {  // timing experiment: no X / U loads (stale shared memory, wrong T2)
+          if (LRS_XDBG(p.dbg & 4)) {  // timing experiment: no X / U loads (stale shared memory, wrong T2)
             mbar_arrive(&full_x[s]);
             continue;
           }
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         CTRACE(p, blockIdx.x == 0 && threadIdx.x == 64 && k < 4, 8200 + 10 * k + 5);
         // ---- depthwise stages: item = (output position of the tile, 8 ranks)
         const int nv = p.r1p / 8;
-        const int items = (p.dbg & 1) ? 0 : p.ipt * rows * p.wo * nv;
+        const int items = LRS_XDBG(p.dbg & 1) ? 0 : p.ipt * rows * p.wo * nv;
         for (int it = threadIdx.x - 64; it < items; it += kCThreads - 64) {
           const int v = it % nv, q = it / nv;
           const int wl = q % p.wo, q2 = q / p.wo;
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
           o.y = pack_bf16x2(out[2], out[3]);
           o.z = pack_bf16x2(out[4], out[5]);
           o.w = pack_bf16x2(out[6], out[7]);
-          if (!(p.dbg & 2))
+          if (!LRS_XDBG(p.dbg & 2))
             *reinterpret_cast<uint4*>(p.t2 + ((static_cast<long long>(n) * p.ho + ho0 + hl) * p.wo + wl) * p.r2p + a0) = o;
         }
         named_bar_sync(1, kCThreads - 64);  // the window may be overwritten by the next restage

@@ -56,12 +56,23 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
 #ifndef LRS_WAIT_TIMEOUT_CYCLES
 #define LRS_WAIT_TIMEOUT_CYCLES (1ll << 34)  /* ~9 s at 1.9 GHz: a protocol bug traps, never hangs */
 #endif
+// Experiment builds (-DLRS_EXPERIMENTS, tools/ only) read debug bits that skip work
+// (timing bisection) and print a line before a wait-timeout trap; production builds
+// compile both out: LRS_XDBG(expr) is the constant 0 and a timeout traps silently
+// (the launch fails with cudaErrorLaunchFailure instead of hanging the device).
+#ifdef LRS_EXPERIMENTS
+#define LRS_XDBG(expr) (expr)
+#define LRS_TIMEOUT_MSG() printf("lrs: mbarrier wait timeout block %d thread %d\n", blockIdx.x, threadIdx.x)
+#else
+#define LRS_XDBG(expr) 0
+#define LRS_TIMEOUT_MSG() ((void)0)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
     if (clock64() - t0 > LRS_WAIT_TIMEOUT_CYCLES) {
-      printf("lrs: mbarrier wait timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
+      LRS_TIMEOUT_MSG();
       __trap();
     }
   }
@@ -77,7 +88,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
     __nanosleep(ns);
     if (ns < 512) ns <<= 1;
     if (clock64() - t0 > LRS_WAIT_TIMEOUT_CYCLES) {
-      printf("lrs: mbarrier wait timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
+      LRS_TIMEOUT_MSG();
       __trap();
     }
   }

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_c
     const int e_begin = __ldg(ptr), e_end = __ldg(ptr + 64);
     const int rb = lane <= 8 ? __ldg(ptr + warp * 8 + lane) - e_begin : 0;
     // ---- stage X[n0..n0+3, window rows/cols, c0..c0+cc) as [c][row][pitch][4 images]
-    for (int wi = threadIdx.x; wi < ((p.dbg & 1) ? 0 : items); wi += kSpThreads) {
+    for (int wi = threadIdx.x; wi < (LRS_XDBG(p.dbg & 1) ? 0 : items); wi += kSpThreads) {
       const int c4 = wi / (p.wr * p.wc), pos = wi - c4 * (p.wr * p.wc);
       const int r = pos / p.wc, col = pos - r * p.wc;
       const int hi = ho0 * p.sh - p.ph + r, wi_ = col - p.pw, ch = c0 + 4 * c4;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_c
     // ---- warp-uniform CSR rows of this warp's 8 channels, two nonzeros per step
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
-      const int a = __shfl_sync(0xffffffffu, rb, jj), b = (p.dbg & 2) ? a : __shfl_sync(0xffffffffu, rb, jj + 1);
+      const int a = __shfl_sync(0xffffffffu, rb, jj), b = LRS_XDBG(p.dbg & 2) ? a : __shfl_sync(0xffffffffu, rb, jj + 1);
       int e = a;
       for (; e + 2 <= b; e += 2) {
         const int2 en0 = ents[e], en1 = ents[e + 1];
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_c
     __syncthreads();
   }
   // ---- Y = Y_L + Y_S, written once: each lane owns 8 consecutive channels of its positions
-  if (jw >= p.cout || (p.dbg & 4)) return;
+  if (jw >= p.cout || LRS_XDBG(p.dbg & 4)) return;
   if (p.epi != nullptr || p.relu) {
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {

@@ -183,10 +183,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   // The CTA owns the whole TMEM of its SM (tmem_cols = 512, one CTA per SM), so
   // the allocation starts at lane 0 / column 0.  Using the literal 0 keeps every
   // TMEM address compile-time uniform (uniform registers in the MMA loop).
-  if (threadIdx.x == 32 && *tmem_slot != 0u) {
-    printf("lrs_wconv: unexpected TMEM base %u\n", *tmem_slot);
-    __trap();
-  }
+  if (threadIdx.x == 32 && *tmem_slot != 0u) __trap();
   constexpr uint32_t tmem = 0u;
   // PDL: every kernel of this library triggers its dependents only after its own
   // griddepcontrol.wait, so when this grid starts everything before the previous kernel

@@ -130,18 +130,33 @@ def lrs_conv_last_error() -> str:
     return load_library().lrs_conv_last_error().decode()
 
 
+def bf16_bits_rne(a) -> np.ndarray:
+    """uint16 bf16 bit patterns of float32 values, round-to-nearest-even
+    (ties to the even mantissa); NaN stays a quiet NaN.  Exact for values
+    that are already bf16-representable."""
+    a = np.ascontiguousarray(a, np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    nan = np.isnan(a)
+    if nan.any():
+        r[nan] = 0x7FC0
+    return np.ascontiguousarray(r)
+
+
 def make_desc(batch_max: int, in_h: int, in_w: int, c_in: int, c_out: int, kernel: int,
               stride: int, pad: int, rank_in: int, rank_out: int, dtype: str,
               u_in: np.ndarray, core: Optional[np.ndarray], u_out: np.ndarray,
               row_ptr: np.ndarray, col_idx: np.ndarray, values: np.ndarray, core_kind: int = LRS_CORE_TUCKER2,
               out_scale: Optional[np.ndarray] = None, out_bias: Optional[np.ndarray] = None, out_relu: bool = False):
-    """Build an lrs_conv_desc from host arrays.  Factor arrays are float32
-    holding dtype-representable values; for bf16 their bf16 bits are passed.
+    """Build an lrs_conv_desc from host arrays.  Factor arrays are float32; for
+    bf16 layers they are rounded to bf16 round-to-nearest-even (bf16_bits_rne)
+    and those bits are passed.  S values are passed as fp32 (the ABI's
+    contract; a bf16 layer's engine rounds them itself).
     Returns (desc, keepalive) -- keep `keepalive` until lrs_conv_create returns."""
     def as_dtype(a):
         a = np.ascontiguousarray(a, np.float32)
         if dtype == "bf16":
-            return np.ascontiguousarray((a.view(np.uint32) >> 16).astype(np.uint16))
+            return bf16_bits_rne(a)
         return a
     keep = []
 
@@ -200,7 +215,8 @@ def sparse_from_slices(c_in: int, c_out: int, kernel_h: int, kernel_w: int, vals
 
 class LrsConv:
     """One compressed conv layer on one device: `LrsConv(...)(x) -> y`
-    with x, y NHWC torch tensors (contiguous, or channels_last NCHW views)."""
+    with x, y NHWC torch tensors (contiguous [n, H, W, C], or channels_last
+    NCHW views of NHWC storage; checked by forward_into)."""
 
     def __init__(self, batch_max, in_h, in_w, c_in, c_out, kernel, stride, pad, rank_in, rank_out,
                  dtype, u_in, core, u_out, row_ptr, col_idx, values, device: int = 0,
@@ -257,17 +273,46 @@ class LrsConv:
         """True if a1 + a2 run as one kernel with T1 kept on chip (include/lrs_conv.h)."""
         return load_library().lrs_conv_core_fused(self.handle) == 1
 
-    def forward_into(self, x, y, stream=None) -> None:
+    def _check_act(self, t, name: str, h: int, w: int, c: int) -> None:
+        """t must be this layer's dtype, on its device, with NHWC storage: either a
+        contiguous [n, h, w, c] tensor or a channels_last [n, c, h, w] view."""
         torch = self.torch
+        if t.dtype != self.tdtype:
+            raise ValueError(f"{name}: dtype {t.dtype}, layer expects {self.tdtype}")
+        if not t.is_cuda or t.device.index != self.device:
+            raise ValueError(f"{name}: must live on cuda:{self.device}, got {t.device}")
+        if t.dim() != 4:
+            raise ValueError(f"{name}: expected a 4-D tensor, got shape {tuple(t.shape)}")
+        if tuple(t.shape[1:]) == (h, w, c) and t.is_contiguous():
+            return
+        if tuple(t.shape[1:]) == (c, h, w) and t.is_contiguous(memory_format=torch.channels_last):
+            return
+        raise ValueError(f"{name}: expected contiguous NHWC [n, {h}, {w}, {c}] or channels_last NCHW "
+                         f"[n, {c}, {h}, {w}], got shape {tuple(t.shape)} strides {t.stride()}")
+
+    def forward_into(self, x, y, stream=None) -> None:
+        """y = layer(x) on `stream`; x / y are NHWC [n, H, W, C] contiguous tensors
+        or channels_last NCHW views of the same storage (validated here)."""
+        torch = self.torch
+        self._check_act(x, "x", self.in_h, self.in_w, self.c_in)
+        self._check_act(y, "y", self.out_h, self.out_w, self.c_out)
         n = x.shape[0]
+        if y.shape[0] != n:
+            raise ValueError(f"x has {n} images but y has {y.shape[0]}")
         s = torch.cuda.current_stream(self.device) if stream is None else stream
         lrs_conv_forward(self.handle, x.data_ptr(), y.data_ptr(), n, s.cuda_stream)
 
     def __call__(self, x):
+        """y = layer(x): x NHWC [n, H, W, C] (contiguous) -> new NHWC y; a
+        channels_last NCHW x gives a channels_last NCHW y."""
         torch = self.torch
-        assert x.dtype == self.tdtype and x.is_cuda
-        assert x.shape[1:] == (self.in_h, self.in_w, self.c_in) and x.is_contiguous()
-        y = torch.empty((x.shape[0], self.out_h, self.out_w, self.c_out), dtype=self.tdtype, device=x.device)
+        self._check_act(x, "x", self.in_h, self.in_w, self.c_in)
+        n = x.shape[0]
+        if tuple(x.shape[1:]) == (self.in_h, self.in_w, self.c_in) and x.is_contiguous():
+            y = torch.empty((n, self.out_h, self.out_w, self.c_out), dtype=self.tdtype, device=x.device)
+        else:
+            y = torch.empty((n, self.c_out, self.out_h, self.out_w), dtype=self.tdtype, device=x.device,
+                            memory_format=torch.channels_last)
         self.forward_into(x, y)
         return y
 

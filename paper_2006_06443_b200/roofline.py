@@ -102,14 +102,97 @@ def layer_work(cfg, n: int, col_idx: np.ndarray, cp: bool = False) -> Dict[str, 
     return st
 
 
+def extra_peaks(path: Optional[str] = None) -> Dict[str, float]:
+    """Peaks MEASURED_PEAKS.json lacks, measured on a B200 by tools/measure_extra_peaks.py
+    (profiles/measured_peaks_extra.json): the TF32 tensor peak (torch fp32 matmul with TF32
+    allowed, 8192^3) and the FP32 CUDA-core FMA peak (an FFMA-chain microbenchmark).
+    Empty if the file is absent."""
+    if path is None:
+        path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                            "measured_peaks_extra.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def tensor_peak(peaks: Dict[str, float], dtype: str):
+    """(TFLOP/s, how) of the tensor pipe for a layer's dtype: bf16 = MEASURED_PEAKS.json
+    bf16_tflops (burst); fp32 = 3xTF32 (three TF32 MMAs per fp32 product, the split the
+    fp32 path needs for 1e-5, SURVEY §8c #13) = measured TF32 peak / 3, else bf16 / 2 / 3."""
+    if dtype == "bf16":
+        return peaks["bf16_tflops"], "measured (MEASURED_PEAKS.json bf16_tflops, burst)"
+    ex = extra_peaks()
+    if "tf32_tflops" in ex:
+        return ex["tf32_tflops"] / 3.0, "measured TF32 peak / 3 (3xTF32; profiles/measured_peaks_extra.json)"
+    return peaks["bf16_tflops"] / 2.0 / 3.0, "derived: bf16 peak / 2 (nominal TF32 ratio) / 3 (3xTF32)"
+
+
+def fma_peak(peaks: Dict[str, float]):
+    """(TFLOP/s, how) of the FP32 CUDA-core pipe."""
+    ex = extra_peaks()
+    if "fp32_fma_tflops" in ex:
+        return ex["fp32_fma_tflops"], "measured (FFMA microbenchmark, profiles/measured_peaks_extra.json)"
+    return fp32_fma_tflops(peaks["sm_max_mhz"]), "derived: 148 SM x 128 FMA/clk x 2 x sm_max_mhz"
+
+
 def layer_roofs(work: Dict[str, Dict[str, float]], peaks: Dict[str, float], dtype: str) -> Dict[str, float]:
     """Literal roof (BASELINE: max(bytes/BW, all FLOPs/tensor peak)) and the
     three-roof (sparse MACs on the FP32 pipe), in seconds."""
     lay = work["layer"]
-    tc = peaks["bf16_tflops"] * 1e12 * (1.0 if dtype == "bf16" else 0.5 / 3.0)  # fp32: 3xTF32 at TF32 = bf16/2
+    tc = tensor_peak(peaks, dtype)[0] * 1e12
     bw = peaks["hbm_gbs"] * 1e9
-    fma = fp32_fma_tflops(peaks["sm_max_mhz"]) * 1e12
+    fma, fma_kind = fma_peak(peaks)
+    fma *= 1e12
     t_lit = max(lay["bytes"] / bw, lay["flops"] / tc)
     t_three = max(lay["bytes"] / bw, lay["flops_chain"] / tc, lay["flops_sparse"] / fma)
     return {"t_literal_s": t_lit, "t_three_roof_s": t_three, "t_hbm_s": lay["bytes"] / bw,
-            "t_chain_tc_s": lay["flops_chain"] / tc, "t_sparse_fma_s": lay["flops_sparse"] / fma}
+            "t_chain_tc_s": lay["flops_chain"] / tc, "t_sparse_tc_s": lay["flops_sparse"] / tc,
+            "t_sparse_fma_s": lay["flops_sparse"] / fma, "fma_tflops": fma / 1e12, "fma_kind": fma_kind}
+
+
+def kernel_roofline(stage: str, work: Dict[str, Dict[str, float]], peaks: Dict[str, float], dtype: str,
+                    t_kernel_s: float, engine: int) -> Dict[str, object]:
+    """The bench line's `roofline` object for the dominant kernel, against the LITERAL
+    roof of BASELINE.json's north star: the slower of its algorithmic bytes at the
+    measured HBM bandwidth and its algorithmic FLOPs (the sparse term's included) at the
+    measured tensor peak of the layer's dtype.  achieved = that quantity / the kernel's
+    event-timed launch duration; frac = achieved / peak.  The FP32-pipe (three-roof) view
+    of the same kernel is reported beside it, with its peak's provenance."""
+    if stage in ("a345_expand_sparse", "a4_sparse_add") and engine == 3:
+        wk = dict(work["layer"])  # the one-kernel fp32 path: the whole layer
+    else:
+        wk = dict(work[stage])
+    b = float(wk["bytes"])
+    f = float(wk["flops"])
+    f_sp = float(wk.get("flops_sparse", 0.0))
+    tc, tc_kind = tensor_peak(peaks, dtype)
+    bw = peaks["hbm_gbs"]
+    fma, fma_kind = fma_peak(peaks)
+    t_hbm = b / (bw * 1e9)
+    t_tc = f / (tc * 1e12)
+    if t_hbm >= t_tc:
+        bound, achieved, peak, unit, kind = "hbm", b / t_kernel_s / 1e9, bw, "GB/s", "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        bound, achieved, peak, unit, kind = "tensor", f / t_kernel_s / 1e12, tc, "TFLOP/s", tc_kind
+    return {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+            "traffic": None, "kernel": stage, "peak_kind": kind,
+            "work": {"bytes": b, "flops": f, "flops_sparse": f_sp, "kernel_us": t_kernel_s * 1e6,
+                     "roof_us": {"hbm": t_hbm * 1e6, "tensor": t_tc * 1e6}},
+            "three_roof_view": {"fp32_pipe_us": f_sp / (fma * 1e12) * 1e6, "fp32_peak_tflops": fma,
+                                "fp32_peak_kind": fma_kind,
+                                "frac": max(t_hbm, (f - f_sp) / (tc * 1e12), f_sp / (fma * 1e12)) / t_kernel_s},
+            "what": "literal roof of the dominant kernel: max(algorithmic bytes / HBM, algorithmic FLOPs incl. "
+                    "the sparse term / tensor peak) (BASELINE.json north star)"}
+
+
+def sparse24_floor_s(cfg, n: int, main_blocks: int, res_blocks: int, peaks: Dict[str, float]) -> float:
+    """The 2:4 sparse engine's own floor for n images: every compressed block (128 output
+    channels x 64 logical input-channel slots of one tap) costs a dense 128 x 32 MMA per
+    output position whatever its density, plus the expansion GEMM, at the bf16 tensor
+    peak.  Output positions are counted without the kernel's window padding columns."""
+    p = n * cfg.out_h * cfg.out_w
+    r2 = cfg.rank_in if cfg.svd else cfg.rank_out
+    flops = 2.0 * 128 * 32 * (main_blocks + res_blocks) * p + 2.0 * p * r2 * cfg.c_out
+    return flops / (peaks["bf16_tflops"] * 1e12)

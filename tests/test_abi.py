@@ -134,3 +134,27 @@ def test_cp_core_requires_core_and_equal_ranks():
     assert st == B.LRS_ERR_INVALID_ARGUMENT and "CP" in msg
     st, msg = patched_status(core_kind=1, core=None)
     assert st == B.LRS_ERR_INVALID_ARGUMENT and "CP" in msg
+
+
+def test_binding_rounds_factors_to_nearest_even():
+    """make_desc's fp32 -> bf16 conversion is round-to-nearest-even (ties to even),
+    matching torch's own fp32 -> bf16 cast bit for bit, including ties, subnormals,
+    infinities and values that round up into the next binade; NaN stays NaN."""
+    import torch
+    rng = np.random.default_rng(5)
+    a = (rng.standard_normal(100000) * np.exp(rng.uniform(-60, 60, 100000))).astype(np.float32)
+    ties = (np.arange(0, 65536, dtype=np.uint32) << 16 | 0x8000).view(np.float32)  # exact halfway points
+    special = np.array([0.0, -0.0, 1e-40, -1e-40, np.inf, -np.inf, 3.3895314e38, 1.0 + 2 ** -8, 1.0 + 3 * 2 ** -9],
+                       np.float32)
+    v = np.concatenate([a, ties[np.isfinite(ties)], special])
+    got = B.bf16_bits_rne(v)
+    want = torch.from_numpy(v).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got, want)
+    nan = B.bf16_bits_rne(np.array([np.nan], np.float32))[0]
+    assert (nan & 0x7F80) == 0x7F80 and (nan & 0x7F) != 0
+    # and it is what make_desc hands to the ABI for a bf16 layer
+    args = base_desc_args()
+    args["u_in"] = args["u_in"] + np.float32(1e-3)
+    d, keep = B.make_desc(**args)
+    u = np.ctypeslib.as_array(ctypes.cast(d.u_in, ctypes.POINTER(ctypes.c_uint16)), shape=(16 * 4,))
+    assert np.array_equal(u, B.bf16_bits_rne(args["u_in"]).ravel())

@@ -62,6 +62,51 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
+def _bench_worker(rank, world, port, out_dir):
+    """bench.py's own partition (ShardPlan, strong scaling) + the verification gather."""
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = workloads.CONFIGS["c2_bf16"].replace(batch=7, in_h=5, in_w=5, c_in=16, c_out=24, rank_in=8,
+                                                   rank_out=8, dtype="f32")
+        plan = bench.ShardPlan(cfg, rank, world, "strong")
+        assert plan.global_batch == 7 and plan.strong
+        inp = workloads.generate(cfg, batch=1)
+        outs = []
+        for i in range(2):  # two rotating sets
+            x = plan.x(i)
+            assert x.shape[0] == plan.end - plan.start
+            y = O.forward_factored(x.astype(np.float64), inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx,
+                                   inp.values, cfg.stride, cfg.pad)
+            outs.append(gather_shards(torch.from_numpy(y), plan.global_batch).numpy())
+        if rank == 0:
+            np.save(os.path.join(out_dir, "y_sets.npy"), np.stack(outs))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_strong_shards_gather_to_the_1gpu_problem(tmp_path):
+    """The gathered shards of bench.py's strong-scaling partition are the 1-GPU
+    problem: same images (generate_x of the global batch), same outputs bit for bit."""
+    world, port = 2, _free_port()
+    mp.spawn(_bench_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    import bench
+    cfg = workloads.CONFIGS["c2_bf16"].replace(batch=7, in_h=5, in_w=5, c_in=16, c_out=24, rank_in=8, rank_out=8,
+                                               dtype="f32")
+    inp = workloads.generate(cfg, batch=1)
+    one = bench.ShardPlan(cfg, 0, 1, "strong")
+    got = np.load(tmp_path / "y_sets.npy")
+    for i in range(2):
+        ref = O.forward_factored(one.x(i).astype(np.float64), inp.u_in, inp.core, inp.u_out, inp.row_ptr,
+                                 inp.col_idx, inp.values, cfg.stride, cfg.pad)
+        assert np.array_equal(got[i], ref)
+    assert not np.array_equal(got[0], got[1])  # distinct images per rotating set
+    weak = [bench.ShardPlan(cfg, r, 2, "weak") for r in range(2)]
+    assert weak[0].global_batch == 14 and not np.array_equal(weak[0].x(0), weak[1].x(0))
+
+
 def test_two_rank_sharded_forward_equals_single_process(tmp_path):
     world, port = 2, _free_port()
     mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)

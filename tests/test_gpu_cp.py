@@ -14,6 +14,7 @@ import torch
 
 import workloads
 from oracle import lrs_oracle as O
+import parity
 
 pytestmark = pytest.mark.gpu
 
@@ -37,11 +38,7 @@ def oracle(inp):
 
 
 def check(y, ref, dtype):
-    err = np.linalg.norm(y - ref) / np.linalg.norm(ref)
-    if dtype == "f32":
-        assert err <= 1e-5 and np.abs(y - ref).max() <= 1e-4, err
-    else:
-        assert err <= 2e-2, err
+    parity.check(y, ref, dtype)
 
 
 @pytest.mark.parametrize("name,batch", [("c1_cp", 1), ("c2_cp", 5), ("c2_cp", 64)])

@@ -16,6 +16,7 @@ import torch
 
 import workloads
 from oracle import lrs_oracle as O
+import parity
 
 pytestmark = pytest.mark.gpu
 
@@ -45,9 +46,7 @@ def oracle(inp):
 
 
 def check(y, ref):
-    err = np.linalg.norm(y - ref) / np.linalg.norm(ref)
-    mx = np.abs(y - ref).max()
-    assert err <= 1e-5 and mx <= 1e-4, (err, mx)
+    parity.check(y, ref, "f32")
 
 
 @pytest.mark.parametrize("name", ["c1", "c2_f32"])

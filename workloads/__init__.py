@@ -17,10 +17,11 @@ Recipe (SURVEY.md §8(c) readings #7-#11):
   * S: nnz = round(d * Cout*Cin*k*k) positions drawn uniformly without
     replacement over the OIHW linear index, sorted; values N(0, 0.1)
     (variance 0.1); CSR by output channel with col = (c*k + y)*k + x;
-  * fp64 draws -> fp32 (RNE); bf16 configs additionally round X, the
-    factors and the S values to bf16 (RNE) -- "bf16 with fp32 accumulate"
-    (BASELINE.json configs 2-5) read as every operand in bf16, DESIGN.md
-    reading #12.  The fp32 configs keep fp32 S values.
+  * fp64 draws -> fp32 (RNE); bf16 configs additionally round X and the
+    factors to bf16 (RNE).  S values stay fp32 for every dtype (SURVEY.md
+    §8(c) reading #12: "S values fp32"; the ABI takes fp32 values and a bf16
+    layer's engine rounds them itself -- that rounding is part of what the
+    parity tests check, reading #12).
 
 The arrays returned are exactly what both sides consume: the GPU gets the
 fp32/bf16 bits, the oracle gets the same values widened to fp64.
@@ -36,7 +37,7 @@ __all__ = [
     "LayerConfig", "LayerInputs", "CONFIGS", "generate", "bf16_round",
     "bf16_bits", "resnet50_table2", "RESNET50_COMPRESSED_3X3", "generate_weights",
     "resnet50_compressed_layers", "RESNET50_CONV2_MODULES", "resnet50_images",
-    "CpInputs", "generate_cp", "CP_CONFIGS",
+    "CpInputs", "generate_cp", "CP_CONFIGS", "generate_x",
 ]
 
 
@@ -159,8 +160,18 @@ def generate(cfg: LayerConfig, batch: Optional[int] = None, seed: Optional[int] 
         u_out=_store(u_out, cfg.dtype),
         row_ptr=row_ptr,
         col_idx=cols.astype(np.int32),
-        values=_store(vals, cfg.dtype),
+        values=vals.astype(np.float32),
     )
+
+
+def generate_x(cfg: LayerConfig, batch: Optional[int] = None, seed: int = 0) -> np.ndarray:
+    """Only the input X of `generate(cfg, batch, seed)` (its first draw), so other
+    seeds give other images for the same weights: generate_x(cfg, n, s) ==
+    generate(cfg, n, seed=s).x."""
+    n = cfg.batch if batch is None else batch
+    rng = np.random.Generator(np.random.PCG64(seed))
+    x = np.maximum(rng.standard_normal((n, cfg.in_h, cfg.in_w, cfg.c_in)), 0.0)
+    return _store(x, cfg.dtype)
 
 
 def generate_weights(cfg: LayerConfig, seed: Optional[int] = None) -> LayerInputs:
@@ -185,7 +196,7 @@ def generate_weights(cfg: LayerConfig, seed: Optional[int] = None) -> LayerInput
     np.add.at(row_ptr, rows + 1, 1)
     return LayerInputs(cfg=cfg, x=None, u_in=_store(u_in, cfg.dtype),
                        core=None if core is None else _store(core, cfg.dtype), u_out=_store(u_out, cfg.dtype),
-                       row_ptr=np.cumsum(row_ptr), col_idx=cols.astype(np.int32), values=_store(vals, cfg.dtype))
+                       row_ptr=np.cumsum(row_ptr), col_idx=cols.astype(np.int32), values=vals.astype(np.float32))
 
 
 # the paper's own CP form of L at the C1 / C2 shapes,
@@ -231,7 +242,7 @@ def generate_cp(cfg: LayerConfig, batch: Optional[int] = None, seed: Optional[in
     np.add.at(row_ptr, rows + 1, 1)
     st = lambda t: _store(t, cfg.dtype)  # noqa: E731
     return CpInputs(cfg=cfg, x=st(x), a=st(a), b=st(b), c=st(c), d=st(d), row_ptr=np.cumsum(row_ptr),
-                    col_idx=cols.astype(np.int32), values=st(vals))
+                    col_idx=cols.astype(np.int32), values=vals.astype(np.float32))
 
 
 def resnet50_table2(path: Optional[str] = None):
