@@ -33,7 +33,7 @@
  *
  * Environment (read at create): LRS_VERBOSE; plan / engine overrides used by
  * the tests to cover every path -- LRS_NO_AUTOTUNE, LRS_NO_CORE, LRS_NO_TINY,
- * LRS_F32_FUSED, LRS_CORE_{IPT,TH,GRID,GSTREAM,T1_NOSWZ}, LRS_TINY_CB,
+ * LRS_F32_FUSED, LRS_NO_PW, LRS_PW_{MPC,BP}, LRS_CORE_{IPT,TH,GRID,GSTREAM,T1_NOSWZ}, LRS_TINY_CB,
  * LRS_WCONV_{TH,CB,CPW,NS,BPI,REUSE,NWB1,ERING} -- each selects another plan
  * that computes the same Y.  Knobs that skip work (timing bisection) exist
  * only in -DLRS_EXPERIMENTS builds; bench.py refuses to time with any LRS_*
@@ -227,6 +227,20 @@ int32_t lrs_conv_sparse_engine(const lrs_conv *h, int32_t *main_blocks, int32_t 
 lrs_status lrs_sparse_from_slices(int32_t c_in, int32_t c_out, int32_t kernel_h, int32_t kernel_w,
                                   const int64_t *slice_ptr, const void *packed, int32_t packed_bytes,
                                   const float *values, int64_t *row_ptr, int32_t *col_idx, float *values_out);
+
+/*
+ * Which kernel evaluates the expansion a3 + sparse term a4 + the single store a5
+ * (-1 for NULL):
+ *   0  a GEMM / SIMT kernel (fp32 layers, shapes the tensor-core kernels do not cover);
+ *   1  the windowed fused tensor-core kernel (lrs_wconv.cuh: k x k layers, any stride);
+ *   2  the channel-stationary pointwise kernel (lrs_pw.cuh): 1x1 SVD-pair bf16 layers
+ *      with c_in % 64 == 0 and c_in <= 512 -- each CTA keeps the V^T blocks and the 2:4
+ *      blocks of a fixed group of 128-channel M-tiles resident (metadata in TMEM) and
+ *      streams X and T1 position tiles through it (C4; PAPER.md:168, :171-191 at k = 1).
+ *      LRS_NO_PW=1 at create selects kernel 1 instead; LRS_PW_MPC / LRS_PW_BP override
+ *      the M-tiles per CTA / positions per tile (same Y).
+ */
+int32_t lrs_conv_expand_kernel(const lrs_conv *h);
 
 /*
  * 1 if the projection a1 and the core convolution a2 of this layer run as one

@@ -22,6 +22,7 @@
 #include "lrs_spadd.cuh"
 #include "lrs_tiny.cuh"
 #include "lrs_wconv.cuh"
+#include "lrs_pw.cuh"
 
 using namespace lrs;
 
@@ -135,6 +136,16 @@ const void* wconv_kernel_ptr(int nu, int bpi) {
 #undef LRS_WK
 }
 
+// channel-stationary 1x1 kernel instantiation for mpc M-tiles per CTA
+const void* pw_kernel_ptr(int mpc) {
+  switch (mpc) {
+    case 1: return reinterpret_cast<const void*>(&lrs_pw_kernel<1>);
+    case 2: return reinterpret_cast<const void*>(&lrs_pw_kernel<2>);
+    case 3: return reinterpret_cast<const void*>(&lrs_pw_kernel<3>);
+    default: return reinterpret_cast<const void*>(&lrs_pw_kernel<4>);
+  }
+}
+
 struct Stage {
   const char* name;
   KernelId kid;
@@ -187,6 +198,18 @@ struct lrs_conv {
   TimingRing ring[4];
   // fused a3+a4+a5 on the tensor cores (lrs_wconv.cuh), bf16 layers
   bool use_w = false;
+  // 1x1 SVD-pair layers: channel-stationary fused a3 + a4 + a5 (lrs_pw.cuh)
+  bool use_pw = false;
+  PwParams pp{};
+  uint32_t pw_smem = 0;
+  int pw_grid_per_group = 0;  // CTAs per channel group at most
+  void* pw_w = nullptr;       // per-group weight images
+  void* pw_e = nullptr;       // per-group metadata images
+  void* pw_tab = nullptr;     // per-group block tables
+  const void* px_ptr = nullptr;
+  int px_n = -1;
+  const void* py_ptr = nullptr;
+  int py_n = -1;
   WconvParams wp{};
   uint32_t w_smem = 0;
   void* w_as = nullptr;   // compressed 2:4 blocks of S (SW64 shared-memory images)
@@ -815,6 +838,97 @@ lrs_status build_spadd(lrs_conv* h, const lrs_conv_desc* d) {
   return LRS_OK;
 }
 
+// S -> exact 2:4 main + residual blocks (bf16 values, RNE) with their TMEM metadata:
+// every group of 4 consecutive input channels of a (row j, tap) keeps its first two
+// nonzeros in the main block of (M-tile, 64-channel chunk, tap) and, only where the group
+// holds 3-4 nonzeros, the rest in a residual block (S = S_main + S_res exactly).
+// as: [blocks][128 rows][32] bf16 bits (row-major, unswizzled); ee: [blocks][128 lanes][4]
+// u32 metadata words; main block of key (mt * n_ck + c) * taps + t has index key, its
+// residual block res_tab[key] (-1 if none).
+struct Split24 {
+  std::vector<uint16_t> as;
+  std::vector<uint32_t> ee;
+  std::vector<int> res_tab;
+  int nblk_main = 0, nres = 0;
+};
+
+Split24 split_24(const lrs_conv_desc* d, int n_mt, int n_ck, int taps) {
+  const int cout = d->c_out;
+  Split24 S;
+  const int nblk_main = n_mt * n_ck * taps;
+  S.nblk_main = nblk_main;
+  std::vector<uint16_t>& as = S.as;
+  std::vector<uint32_t>& ee = S.ee;
+  std::vector<int>& res_tab = S.res_tab;
+  as.assign(static_cast<size_t>(nblk_main) * 128 * 32, 0);
+  ee.assign(static_cast<size_t>(nblk_main) * 128 * 4, 0x44444444u);
+  res_tab.assign(nblk_main, -1);
+  int nres = 0;
+  std::vector<float> dense(static_cast<size_t>(n_ck) * taps * 64);
+  auto put = [&](int blk, int m, int grp, int i0, int i1, float v0, float v1) {
+    as[(static_cast<size_t>(blk) * 128 + m) * 32 + 2 * grp] = bf16_bits_rne(v0);
+    as[(static_cast<size_t>(blk) * 128 + m) * 32 + 2 * grp + 1] = bf16_bits_rne(v1);
+    const int st = grp / 8, gs = grp % 8;
+    const int lane = m % 8 + 8 * (gs / 4) + 16 * (m / 16);
+    const int nib = (gs % 4) + 4 * ((m / 8) % 2);
+    uint32_t& w = ee[(static_cast<size_t>(blk) * 128 + lane) * 4 + st];
+    w = (w & ~(0xFu << (4 * nib))) | (static_cast<uint32_t>(i0 | (i1 << 2)) << (4 * nib));
+  };
+  auto put_list = [&](int blk, int m, int grp, const int* idx, const float* val, int cnt) {
+    if (cnt == 0) return;  // block pre-filled with zeros and the (0,1) pattern
+    if (cnt == 1) {
+      if (idx[0] < 3) put(blk, m, grp, idx[0], idx[0] + 1, val[0], 0.f);
+      else put(blk, m, grp, 2, 3, 0.f, val[0]);
+    } else {
+      put(blk, m, grp, idx[0], idx[1], val[0], val[1]);
+    }
+  };
+  for (int j = 0; j < cout; ++j) {
+    const int64_t e0 = d->row_ptr[j], e1 = d->row_ptr[j + 1];
+    if (e0 == e1) continue;
+    std::fill(dense.begin(), dense.end(), 0.f);
+    for (int64_t e = e0; e < e1; ++e) {
+      const int col = d->col_idx[e];
+      const int ch = col / taps, t = col % taps;
+      dense[(static_cast<size_t>(ch / 64) * taps + t) * 64 + ch % 64] = d->values[e];
+    }
+    const int mt = j / 128, m = j % 128;
+    for (int c = 0; c < n_ck; ++c)
+      for (int t = 0; t < taps; ++t) {
+        const float* b = &dense[(static_cast<size_t>(c) * taps + t) * 64];
+        const int key = (mt * n_ck + c) * taps + t;
+        for (int grp = 0; grp < 16; ++grp) {
+          int idx[4];
+          float val[4];
+          int cnt = 0;
+          for (int i = 0; i < 4; ++i)
+            if (b[4 * grp + i] != 0.f) {
+              idx[cnt] = i;
+              val[cnt] = b[4 * grp + i];
+              ++cnt;
+            }
+          put_list(key, m, grp, idx, val, std::min(cnt, 2));
+          if (cnt > 2) {
+            if (res_tab[key] < 0) {
+              res_tab[key] = nblk_main + nres++;
+              as.resize(as.size() + 128 * 32, 0);
+              ee.resize(ee.size() + 128 * 4, 0x44444444u);
+            }
+            put_list(res_tab[key], m, grp, idx + 2, val + 2, cnt - 2);
+          }
+        }
+      }
+  }
+  S.nres = nres;
+  return S;
+}
+
+// K-major operand image with 8-row swizzle atoms: byte offset of (row r, byte `byte`)
+// in a tile of rows of sw bytes (the layout TMA writes with SWIZZLE_<sw>B)
+inline int swz_off(int r, int byte, int sw) {
+  return (r / 8) * (8 * sw) + (r % 8) * sw + ((((byte / 16) ^ ((r % 8) / (128 / sw))) % (sw / 16)) * 16) + byte % 16;
+}
+
 // Fused a3+a4+a5 on the tensor cores (lrs_wconv.cuh): choose the tile geometry,
 // split S into exact 2:4 main + residual blocks with their TMEM metadata, and
 // encode the static tensor maps.  Leaves h->use_w false if the layer does not fit.
@@ -894,7 +1008,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       // (blocks per item, slots): prefer big items, then more slots; but when the layer has
       // several M-tiles, first look for a candidate that keeps ALL of a tile's windows in
       // smem (window reuse across the CTA's consecutive M-tiles)
-      const int cand[][2] = {{4, 3}, {4, 2}, {2, 4}, {2, 3}, {2, 2}};
+      // (one-block items {1, ns} are taken only when bpi_max (LRS_WCONV_BPI) asks for them)
+      const int cand[][2] = {{4, 3}, {4, 2}, {2, 4}, {2, 3}, {2, 2}, {1, 6}, {1, 5}, {1, 4}, {1, 3}};
       // (opt-in: measured slower on C4, 49.4 vs 45.7 us -- the window loads are not its bottleneck)
       int want_all = (n_mt > 1 && n_tk + (d->nnz > 0 ? n_ck / cpw : 0) <= kWMaxWin && getenv("LRS_WCONV_REUSE")) ? 1 : 0;
       for (int pass = 0; pass < 2; ++pass) {
@@ -903,8 +1018,9 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       bool found = false;
       for (const auto& cnd : cand) {
         const int bpi = cnd[0], ns = cnd[1];
-        if (bpi > bpi_max || ns > ns_max) continue;
-        const uint32_t a_slot = static_cast<uint32_t>(bpi) * kSpBlockBytes;  // >= 16 KB dense box
+        if (bpi > bpi_max || ns > ns_max || (bpi == 1 && bpi_max != 1)) continue;
+        // an A slot also holds one dense U_out^T block (128 rows x sw_t B) of the T windows
+        const uint32_t a_slot = std::max<uint32_t>(static_cast<uint32_t>(bpi) * kSpBlockBytes, 128u * sw_t);
         const uint32_t e_slot = static_cast<uint32_t>(bpi) * kEBlockBytes;
         const int es_need = ering ? 1 : ns;  // TMEM metadata slots the plan needs at least
         if (acc + 4 * bpi * es_need > 512) continue;
@@ -981,66 +1097,12 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   const int wc = best_wc, tbox_w = best_tbw, tcols = best_tc;
 
   // ---- S -> exact 2:4 main + residual blocks (bf16 values, RNE), TMEM metadata
-  const int nblk_main = n_mt * n_ck * taps;
-  std::vector<uint16_t> as(static_cast<size_t>(nblk_main) * 128 * 32, 0);
-  std::vector<uint32_t> ee(static_cast<size_t>(nblk_main) * 128 * 4, 0x44444444u);
-  std::vector<int> res_tab(nblk_main, -1);
-  int nres = 0;
-  std::vector<float> dense(static_cast<size_t>(n_ck) * taps * 64);
-  auto put = [&](int blk, int m, int grp, int i0, int i1, float v0, float v1) {
-    as[(static_cast<size_t>(blk) * 128 + m) * 32 + 2 * grp] = bf16_bits_rne(v0);
-    as[(static_cast<size_t>(blk) * 128 + m) * 32 + 2 * grp + 1] = bf16_bits_rne(v1);
-    const int st = grp / 8, gs = grp % 8;
-    const int lane = m % 8 + 8 * (gs / 4) + 16 * (m / 16);
-    const int nib = (gs % 4) + 4 * ((m / 8) % 2);
-    uint32_t& w = ee[(static_cast<size_t>(blk) * 128 + lane) * 4 + st];
-    w = (w & ~(0xFu << (4 * nib))) | (static_cast<uint32_t>(i0 | (i1 << 2)) << (4 * nib));
-  };
-  auto put_list = [&](int blk, int m, int grp, const int* idx, const float* val, int cnt) {
-    if (cnt == 0) return;  // block pre-filled with zeros and the (0,1) pattern
-    if (cnt == 1) {
-      if (idx[0] < 3) put(blk, m, grp, idx[0], idx[0] + 1, val[0], 0.f);
-      else put(blk, m, grp, 2, 3, 0.f, val[0]);
-    } else {
-      put(blk, m, grp, idx[0], idx[1], val[0], val[1]);
-    }
-  };
-  for (int j = 0; j < cout; ++j) {
-    const int64_t e0 = d->row_ptr[j], e1 = d->row_ptr[j + 1];
-    if (e0 == e1) continue;
-    std::fill(dense.begin(), dense.end(), 0.f);
-    for (int64_t e = e0; e < e1; ++e) {
-      const int col = d->col_idx[e];
-      const int ch = col / taps, t = col % taps;
-      dense[(static_cast<size_t>(ch / 64) * taps + t) * 64 + ch % 64] = d->values[e];
-    }
-    const int mt = j / 128, m = j % 128;
-    for (int c = 0; c < n_ck; ++c)
-      for (int t = 0; t < taps; ++t) {
-        const float* b = &dense[(static_cast<size_t>(c) * taps + t) * 64];
-        const int key = (mt * n_ck + c) * taps + t;
-        for (int grp = 0; grp < 16; ++grp) {
-          int idx[4];
-          float val[4];
-          int cnt = 0;
-          for (int i = 0; i < 4; ++i)
-            if (b[4 * grp + i] != 0.f) {
-              idx[cnt] = i;
-              val[cnt] = b[4 * grp + i];
-              ++cnt;
-            }
-          put_list(key, m, grp, idx, val, std::min(cnt, 2));
-          if (cnt > 2) {
-            if (res_tab[key] < 0) {
-              res_tab[key] = nblk_main + nres++;
-              as.resize(as.size() + 128 * 32, 0);
-              ee.resize(ee.size() + 128 * 4, 0x44444444u);
-            }
-            put_list(res_tab[key], m, grp, idx + 2, val + 2, cnt - 2);
-          }
-        }
-      }
-  }
+  Split24 S24 = split_24(d, n_mt, n_ck, taps);
+  const int nblk_main = S24.nblk_main;
+  const int nres = S24.nres;
+  std::vector<uint16_t>& as = S24.as;
+  std::vector<uint32_t>& ee = S24.ee;
+  std::vector<int>& res_tab = S24.res_tab;
   h->w_main_blocks = nblk_main;
   h->w_res_blocks = nres;
   const int nblk = nblk_main + nres;
@@ -1068,10 +1130,6 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   stream_off.back() = static_cast<int>(order.size());
   lrs_status st;
   // shared-memory images of the A operands (swizzle applied here, 1-D bulk copies in the kernel)
-  auto swz_off = [](int r, int byte, int sw) {  // K-major, rows of sw bytes, 8-row atoms
-    return (r / 8) * (8 * sw) + (r % 8) * sw + ((((byte / 16) ^ ((r % 8) / (128 / sw))) % (sw / 16)) * 16) +
-           byte % 16;
-  };
   {
     std::vector<uint8_t> b(static_cast<size_t>(nblk) * kSpBlockBytes, 0);
     std::vector<uint8_t> e(static_cast<size_t>(nblk) * kEBlockBytes);
@@ -1174,7 +1232,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   const uint32_t acc = best_acc;
   w.acc_cols = acc;
   w.bpi = best_bpi;
-  w.a_slot = static_cast<uint32_t>(best_bpi) * kSpBlockBytes;
+  w.a_slot = std::max<uint32_t>(static_cast<uint32_t>(best_bpi) * kSpBlockBytes, 128u * sw_t);
   w.e_slot = static_cast<uint32_t>(best_bpi) * kEBlockBytes;
   // double-buffered accumulators (epilogue overlaps MMAs) when two fit next to the metadata columns
   w.nacc = (2 * acc + 4 * best_bpi * (ering ? 1 : best_ns) <= 512) ? 2 : 1;
@@ -1192,6 +1250,174 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   if (getenv("LRS_VERBOSE"))
     fprintf(stderr, "lrs_wconv plan: th %d tcols %d units %d acc %u nacc %d ns %d bpi %d nwb %d cpw %d win %u B smem %u B tiles/img-group %d\n",
             th, tcols, w.n_units, acc, w.nacc, w.ns, w.bpi, w.nwb, cpw, best_stride, best_total, w.bands * w.cbands * w.n_mt);
+  return LRS_OK;
+}
+
+// 1x1 SVD-pair layers (bf16, stride 1, pad 0, c_in % 64 == 0): plan the channel-stationary
+// fused kernel (lrs_pw.cuh), build the per-group weight images, encode nothing per call
+// yet (X / T1 maps depend on n).  Leaves h->use_pw false if the layer does not fit.
+lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
+  if (h->f32 || !h->svd || d->c_in % 64 != 0 || getenv("LRS_NO_PW")) return LRS_OK;
+  const int cin = d->c_in, cout = d->c_out;
+  const int n_ck = cin / 64;
+  if (n_ck > kPMaxCk) return LRS_OK;
+  const int r1p = h->r1p;
+  const int t_kc = r1p < 64 ? r1p : 64;
+  if (r1p % t_kc) return LRS_OK;
+  const int n_tk = r1p / t_kc;
+  const uint32_t sw_t = static_cast<uint32_t>(t_kc) * 2u;
+  const int n_mt = (cout + 127) / 128;
+  const int n_x = d->nnz > 0 ? n_ck : 0;
+  Split24 S = d->nnz > 0 ? split_24(d, n_mt, n_ck, 1) : Split24{};
+  const long long p_max = static_cast<long long>(d->batch_max) * d->in_h * d->in_w;
+  const int mpc_env = getenv("LRS_PW_MPC") ? atoi(getenv("LRS_PW_MPC")) : 0;  // plan overrides (tests)
+  const int bp_env = getenv("LRS_PW_BP") ? atoi(getenv("LRS_PW_BP")) : 0;
+  struct Plan { int mpc = 0, bp = 0, ns = 0, nblk = 0, gpg = 0; uint32_t smem = 0, w_bytes = 0; double cost = 1e300; };
+  Plan best;
+  for (int mpc = std::min(kPMaxMpc, n_mt); mpc >= 1; --mpc) {
+    if (mpc_env && mpc != mpc_env) continue;
+    const int G = (n_mt + mpc - 1) / mpc;
+    if (G > h->sms) continue;
+    // blocks per group: every (M-tile, chunk) has its main block, plus residual blocks
+    int nblk = 0;
+    if (n_x)
+      for (int g = 0; g < G; ++g) {
+        int nb = 0;
+        for (int m = 0; m < mpc; ++m)
+          for (int c = 0; c < n_ck; ++c) {
+            const int mt = g * mpc + m;
+            nb += 1 + ((mt < n_mt && S.res_tab[mt * n_ck + c] >= 0) ? 1 : 0);
+          }
+        nblk = std::max(nblk, nb);
+      }
+    for (int bp : {128, 96, 64}) {  // multiples of 32: the epilogue stores 32-position TMA boxes
+      if (bp_env && bp != bp_env) continue;
+      const uint32_t acc = static_cast<uint32_t>(mpc * bp);
+      // TMEM: two accumulator sets, the metadata, and the epilogue's 32-column reads past a
+      // set's last column (bp % 32 == 16) must stay inside the 512 columns
+      const uint32_t tail = (bp % 32) ? 16u : 0u;
+      if (2 * acc + std::max<uint32_t>(4u * nblk, tail) > 512) continue;
+      const uint32_t dense = static_cast<uint32_t>(mpc * n_tk) * 128u * sw_t;
+      const uint32_t w_bytes = dense + static_cast<uint32_t>(nblk) * 8192u;
+      const uint32_t e_bytes = static_cast<uint32_t>(nblk) * 2048u;
+      const uint32_t slot = static_cast<uint32_t>(bp) * 128u;
+      const uint32_t fixed = align1024(w_bytes) + align1024(e_bytes) + 8 * kPEpiScratch + 1024 /*tab*/ +
+                             1024 /*bars*/ + 1024 /*align*/;
+      if (fixed >= static_cast<uint32_t>(kMaxSmem)) continue;
+      const int ns = std::min<int>(kPMaxSlots, static_cast<int>((kMaxSmem - fixed) / slot));
+      // slots are released chunk by chunk (tcgen05.commit after each chunk's MMAs); deeper
+      // rings prefetch further ahead (shallow ones cost more below)
+      if (ns < 4) continue;
+      // cost (cycles per CTA): tiles x max(MMA, operand inflow, the group's share of the HBM
+      // write of Y); sparse MMA ~ (A 4 KB + B bp*64 B) / 128 B/clk, dense ~ (4 KB + bp*32 B) / 128
+      const int gpg = h->sms / G;
+      const long long n_pt = (p_max + bp - 1) / bp;
+      const long long tiles = (n_pt + gpg - 1) / gpg;
+      const double sp = std::max(100.0, (4096.0 + 64.0 * bp) / 128.0), dn = std::max(50.0, (4096.0 + 32.0 * bp) / 128.0);
+      const double mma = static_cast<double>(nblk) * 2 * sp + mpc * n_tk * (sw_t / 32.0) * dn;
+      const double in = (static_cast<double>(n_x) * bp * 128 + n_tk * bp * sw_t) / 60.0;
+      const double out = static_cast<double>(bp) * mpc * 128 * 2 * (G * gpg) / 3300.0;  // ~3.3 KB/clk of HBM writes
+      const double shallow = ns < n_x + n_tk + 2 ? 1.25 : 1.0;
+      const double cost = static_cast<double>(tiles) * std::max(mma, std::max(in, out)) * shallow + 400.0 * mpc;
+      if (cost < best.cost) {
+        best.cost = cost; best.mpc = mpc; best.bp = bp; best.ns = ns; best.nblk = nblk; best.gpg = gpg;
+        best.w_bytes = w_bytes;
+        best.smem = fixed + static_cast<uint32_t>(ns) * slot;
+      }
+    }
+  }
+  if (!best.mpc) return LRS_OK;
+  const int mpc = best.mpc, G = (n_mt + mpc - 1) / mpc, nblk = best.nblk;
+  // ---- per-group images: [mpc][n_tk] V^T blocks, then the 2:4 blocks; metadata; tables
+  std::vector<uint8_t> wimg(static_cast<size_t>(G) * best.w_bytes, 0);
+  std::vector<uint8_t> eimg(static_cast<size_t>(G) * std::max(nblk, 1) * 2048u, 0x44);
+  std::vector<uint16_t> tab(static_cast<size_t>(G) * mpc * n_ck, 0);
+  const uint32_t dense = static_cast<uint32_t>(mpc * n_tk) * 128u * sw_t;
+  const int r1 = d->rank_in;
+  for (int g = 0; g < G; ++g) {
+    uint8_t* wg = &wimg[static_cast<size_t>(g) * best.w_bytes];
+    for (int m = 0; m < mpc; ++m)
+      for (int tk = 0; tk < n_tk; ++tk)
+        for (int r = 0; r < 128; ++r) {
+          const int j = (g * mpc + m) * 128 + r;
+          if (j >= cout) continue;
+          for (int e2 = 0; e2 < t_kc; ++e2) {
+            const int bb = tk * t_kc + e2;
+            if (bb >= r1) continue;
+            const uint16_t bits = static_cast<const uint16_t*>(d->u_out)[static_cast<size_t>(bb) * cout + j];
+            memcpy(wg + static_cast<size_t>(m * n_tk + tk) * 128 * sw_t + swz_off(r, 2 * e2, static_cast<int>(sw_t)),
+                   &bits, 2);
+          }
+        }
+    if (!n_x) continue;
+    int nb = 0;
+    for (int m = 0; m < mpc; ++m)
+      for (int c = 0; c < n_ck; ++c) {
+        const int mt = g * mpc + m;
+        const int first = nb;
+        int keys[2] = {-1, -1}, cnt = 1;
+        if (mt < n_mt) {
+          keys[0] = mt * n_ck + c;
+          if (S.res_tab[keys[0]] >= 0) keys[cnt++] = S.res_tab[keys[0]];
+        }
+        for (int q = 0; q < cnt; ++q, ++nb) {
+          uint8_t* blk = wg + dense + static_cast<size_t>(nb) * 8192;
+          uint8_t* eb = &eimg[(static_cast<size_t>(g) * nblk + nb) * 2048];
+          if (keys[q] < 0) continue;  // an M-tile past c_out: zero block (its Y is never stored)
+          for (int r = 0; r < 128; ++r)
+            for (int k = 0; k < 32; ++k)
+              memcpy(blk + swz_off(r, 2 * k, 64), &S.as[(static_cast<size_t>(keys[q]) * 128 + r) * 32 + k], 2);
+          memcpy(eb, &S.ee[static_cast<size_t>(keys[q]) * 128 * 4], 2048);
+        }
+        tab[(static_cast<size_t>(g) * mpc + m) * n_ck + c] = static_cast<uint16_t>(first | (cnt << 12));
+      }
+  }
+  lrs_status st;
+  if ((st = upload(&h->pw_w, wimg)) != LRS_OK) return st;
+  if ((st = upload(&h->pw_e, eimg)) != LRS_OK) return st;
+  {
+    std::vector<uint8_t> tb(tab.size() * 2);
+    memcpy(tb.data(), tab.data(), tb.size());
+    if ((st = upload(&h->pw_tab, tb)) != LRS_OK) return st;
+  }
+  PwParams& q = h->pp;
+  memset(&q, 0, sizeof(q));
+  q.img_w = static_cast<const uint8_t*>(h->pw_w);
+  q.img_e = static_cast<const uint8_t*>(h->pw_e);
+  q.tab = static_cast<const uint16_t*>(h->pw_tab);
+  q.cout = cout;
+  q.n_ck = n_ck;
+  q.n_x = n_x;
+  q.n_tk = n_tk;
+  q.t_kc = t_kc;
+  q.sw_t = sw_t;
+  q.bp = best.bp;
+  q.mpc = mpc;
+  q.n_groups = G;
+  q.w_bytes = best.w_bytes;
+  q.dense_bytes = dense;
+  q.nblk_max = nblk;
+  q.ns = best.ns;
+  q.slot_bytes = static_cast<uint32_t>(best.bp) * 128u;
+  q.acc_cols = static_cast<uint32_t>(mpc * best.bp);
+  q.e_col0 = 2 * q.acc_cols;
+  q.off_e = align1024(best.w_bytes);
+  q.off_ring = q.off_e + align1024(static_cast<uint32_t>(nblk) * 2048u);
+  q.off_epi = q.off_ring + static_cast<uint32_t>(best.ns) * q.slot_bytes;
+  q.off_tab = q.off_epi + 8 * kPEpiScratch;
+  q.off_bar = q.off_tab + 1024;
+  q.relu = 0;
+#ifdef LRS_EXPERIMENTS
+  if (const char* e = getenv("LRS_PW_DBG")) q.dbg = atoi(e);
+#endif
+  h->pw_smem = best.smem;
+  h->pw_grid_per_group = best.gpg;
+  h->w_main_blocks = n_x ? n_mt * n_ck : 0;
+  h->w_res_blocks = S.nres;
+  h->use_pw = true;
+  if (getenv("LRS_VERBOSE"))
+    fprintf(stderr, "[lrs] pw plan: mpc %d groups %d bp %d ns %d blocks/group %d ctas/group %d smem %u B\n", mpc, G,
+            best.bp, best.ns, nblk, best.gpg, best.smem);
   return LRS_OK;
 }
 }  // namespace
@@ -1488,7 +1714,8 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   if ((st = build_core(h, d)) != LRS_OK) return cleanup_fail(st);
   if ((st = build_tiny(h, d)) != LRS_OK) return cleanup_fail(st);
   // ---------------------------------------------------------------- a3+a4+a5
-  if (bf16_w) {
+  if (bf16_w && h->svd && (st = build_pw(h, d)) != LRS_OK) return cleanup_fail(st);
+  if (bf16_w && !h->use_pw) {
     if ((st = build_wconv(h, d, g)) != LRS_OK) return cleanup_fail(st);
   }
   if (!h->use_w && f32 && !getenv("LRS_F32_FUSED")) {
@@ -1509,7 +1736,7 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     q.t_ld = r2p;
     q.r = r2p;
     q.uo = h->sp_uo;
-  } else if (!h->use_w) {
+  } else if (!h->use_w && !h->use_pw) {
     GemmParams& p = h->a3.p;
     memset(&p, 0, sizeof(p));
     const int kdim = r2p;  // K of the expansion (R2, or R for the SVD pair)
@@ -1625,6 +1852,8 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   const int relu = d->out_relu ? 1 : 0;
   h->wp.epi = h->epi;
   h->wp.relu = relu;
+  h->pp.epi = h->epi;
+  h->pp.relu = relu;
   h->spp.epi = h->epi;
   h->spp.relu = relu;
   h->tp.epi = h->epi;
@@ -1645,9 +1874,9 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
-  {
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&lrs_spadd_kernel),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  for (const void* fn : {reinterpret_cast<const void*>(&lrs_spadd_kernel), pw_kernel_ptr(1), pw_kernel_ptr(2),
+                         pw_kernel_ptr(3), pw_kernel_ptr(4)}) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
   for (int u = 1; u <= kWMaxUnits; ++u)
@@ -1749,6 +1978,51 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
   if (!h->use_core && !(h->skip & 1) &&
       (st = launch(h, 0, h->a1, dim3(static_cast<unsigned>((pin + kTileM - 1) / kTileM)), stream)) != LRS_OK)
     return st;
+  if (h->use_pw) {
+    PwParams& q = h->pp;
+    if (h->px_ptr != x || h->px_n != n) {
+      {
+        uint64_t dims[2] = {static_cast<uint64_t>(d.c_in), static_cast<uint64_t>(pin)};
+        uint64_t strides[1] = {static_cast<uint64_t>(d.c_in) * 2};
+        uint32_t box[2] = {64, static_cast<uint32_t>(q.bp)};
+        uint32_t estr[2] = {1, 1};
+        if ((st = encode_t(&q.tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
+                           128)) != LRS_OK)
+          return st;
+      }
+      {
+        uint64_t dims[2] = {static_cast<uint64_t>(h->r1p), static_cast<uint64_t>(pin)};
+        uint64_t strides[1] = {static_cast<uint64_t>(h->r1p) * 2};
+        uint32_t box[2] = {static_cast<uint32_t>(q.t_kc), static_cast<uint32_t>(q.bp)};
+        uint32_t estr[2] = {1, 1};
+        if ((st = encode_t(&q.tmT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, h->t1, dims, strides, box, estr, q.sw_t)) !=
+            LRS_OK)
+          return st;
+      }
+      h->px_ptr = x;
+      h->px_n = n;
+    }
+    if (h->py_ptr != y || h->py_n != n) {
+      uint64_t dims[2] = {static_cast<uint64_t>(d.c_out), static_cast<uint64_t>(pin)};
+      uint64_t strides[1] = {static_cast<uint64_t>(d.c_out) * 2};
+      uint32_t box[2] = {32, 32};
+      uint32_t estr[2] = {1, 1};
+      if ((st = encode_t(&q.tmY, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y, dims, strides, box, estr, 64)) != LRS_OK)
+        return st;
+      h->py_ptr = y;
+      h->py_n = n;
+    }
+    q.y = y;
+    q.P = static_cast<int>(pin);
+    q.n_pt = static_cast<int>((pin + q.bp - 1) / q.bp);
+    const int per_group = std::max(1, std::min(h->pw_grid_per_group, q.n_pt));
+    cudaEvent_t e1 = nullptr;
+    if ((st = time_begin(h, 2, stream, &e1)) != LRS_OK) return st;
+    LRS_CUDA(launch_pdl(pw_kernel_ptr(q.mpc), dim3(static_cast<unsigned>(per_group * q.n_groups)), dim3(kPThreads), &q,
+                        h->pw_smem, stream));
+    if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
+    return LRS_OK;
+  }
   // a2
   if (h->cp_core && !h->use_core && !(h->skip & 2)) {
     CpDwParams& q = h->cpp;
@@ -1908,7 +2182,7 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
                   h->w_as, h->w_e, h->w_res, h->w_dense_img, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc,
-                  h->sp_uo, h->epi};
+                  h->sp_uo, h->epi, h->pw_w, h->pw_e, h->pw_tab};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (void* b : h->tiny_buf)
@@ -1981,9 +2255,15 @@ const char* lrs_conv_stage_name(const lrs_conv* h, int32_t stage) {
 
 int32_t lrs_conv_sparse_engine(const lrs_conv* h, int32_t* main_blocks, int32_t* residual_blocks) {
   if (!h) return -1;
-  if (main_blocks) *main_blocks = h->use_w ? h->w_main_blocks : 0;
-  if (residual_blocks) *residual_blocks = h->use_w ? h->w_res_blocks : 0;
-  return h->use_w ? 1 : (h->use_tiny ? 3 : (h->use_spadd ? 2 : 0));
+  const bool tc = h->use_w || h->use_pw;
+  if (main_blocks) *main_blocks = tc ? h->w_main_blocks : 0;
+  if (residual_blocks) *residual_blocks = tc ? h->w_res_blocks : 0;
+  return tc ? 1 : (h->use_tiny ? 3 : (h->use_spadd ? 2 : 0));
+}
+
+int32_t lrs_conv_expand_kernel(const lrs_conv* h) {
+  if (!h) return -1;
+  return h->use_pw ? 2 : (h->use_w ? 1 : 0);
 }
 
 int32_t lrs_conv_core_fused(const lrs_conv* h) { return h ? (h->use_core ? 1 : 0) : -1; }
@@ -2045,6 +2325,7 @@ lrs_status lrs_conv_debug_trace(lrs_conv* h, void* dev_buf) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
   h->wp.trace = static_cast<unsigned long long*>(dev_buf);
   h->cp.trace = static_cast<unsigned long long*>(dev_buf);  // core kernel: indices 8190..13095
+  h->pp.trace = static_cast<unsigned long long*>(dev_buf);  // pointwise kernel: indices 0..3999
 #if defined(LRS_EXPERIMENTS) || defined(LRS_WCONV_DEBUG)
   if (const char* e = getenv("LRS_WCONV_DBG")) h->wp.dbg = atoi(e);
 #endif

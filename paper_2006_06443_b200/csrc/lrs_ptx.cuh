@@ -106,6 +106,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uin
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// same, destination given as a shared-memory (u32) address
+__device__ __forceinline__ void tma_load_2d_s(uint32_t dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
                                             int c1, int c2, int c3) {
   asm volatile(
@@ -122,6 +130,14 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, const void* s
       "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+// smem -> global 2-D tensor store (bulk group), source given as a shared-memory address
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -372,6 +388,18 @@ __device__ __forceinline__ float2 out_epi_load(const float2* epi, int j) {
 __device__ __forceinline__ float out_epi(float v, float2 sb, int relu) {
   v = fmaf(v, sb.x, sb.y);
   return relu ? fmaxf(v, 0.f) : v;
+}
+
+// Kernel parameters used inside the single-thread issue loops: the compiler treats the
+// constant bank as invariant and re-loads a parameter at every use (LDC / LDCU) instead
+// of keeping it in a register -- inside a loop each reload costs ~100 cycles on the
+// critical path (tools/loop_cost2.cu: an empty loop with two such reloads runs at 217
+// cycles/iteration, 7.6 with the values in registers).  A value loaded from shared
+// memory cannot be re-materialized that way, so the kernels stage the scalars their
+// loops need in shared memory once and read them from there (smem_param()).
+__device__ __forceinline__ int smem_param(const int* s) { return *reinterpret_cast<const volatile int*>(s); }
+__device__ __forceinline__ uint32_t smem_param(const uint32_t* s) {
+  return *reinterpret_cast<const volatile uint32_t*>(s);
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {

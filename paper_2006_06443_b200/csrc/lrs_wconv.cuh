@@ -380,10 +380,17 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             {
               // metadata of block pairs in one tcgen05.cp.128x256b (blocks 2 KB apart = LBO)
 #pragma unroll
+              // (an odd last block copies alone: its neighbour's columns may belong to the
+              // next metadata slot, or lie past the end of TMEM when items are one block)
               for (int bp = 0; bp < BPI; bp += 2)
-                if (bp < nb && !WDBG(p, 5))
-                  tmem_cp_128x256b(et + 4u * static_cast<uint32_t>(bp),
-                                   ed0 + slot * slot_e16 + static_cast<uint32_t>(bp) * (kEBlockBytes >> 4));
+                if (bp < nb && !WDBG(p, 5)) {
+                  if (bp + 1 < nb)
+                    tmem_cp_128x256b(et + 4u * static_cast<uint32_t>(bp),
+                                     ed0 + slot * slot_e16 + static_cast<uint32_t>(bp) * (kEBlockBytes >> 4));
+                  else
+                    tmem_cp_128x128b(et + 4u * static_cast<uint32_t>(bp),
+                                     ed0 + slot * slot_e16 + static_cast<uint32_t>(bp) * (kEBlockBytes >> 4));
+                }
 #pragma unroll
               for (int bi = 0; bi < BPI; ++bi) {
                 if (bi < nb) {

@@ -27,6 +27,7 @@ EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs
             "lrs_conv_last_error", "lrs_conv_output_shape", "lrs_conv_launches_per_forward",
             "lrs_conv_set_timing", "lrs_conv_stage_times", "lrs_conv_stage_name",
             "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine", "lrs_conv_core_fused",
+            "lrs_conv_expand_kernel",
             "lrs_sparse_from_slices")
 
 
@@ -89,6 +90,8 @@ def load_library(path: str = LIB_PATH):
     lib.lrs_conv_sparse_engine.restype = ctypes.c_int32
     lib.lrs_conv_core_fused.argtypes = [P]
     lib.lrs_conv_core_fused.restype = ctypes.c_int32
+    lib.lrs_conv_expand_kernel.argtypes = [P]
+    lib.lrs_conv_expand_kernel.restype = ctypes.c_int32
     lib.lrs_sparse_from_slices.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.POINTER(ctypes.c_int64), P, ctypes.c_int32,
                                            ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64),
@@ -267,6 +270,12 @@ class LrsConv:
         m, r = ctypes.c_int32(), ctypes.c_int32()
         e = load_library().lrs_conv_sparse_engine(self.handle, ctypes.byref(m), ctypes.byref(r))
         return int(e), int(m.value), int(r.value)
+
+    @property
+    def expand_kernel(self) -> int:
+        """0 GEMM / SIMT, 1 windowed tensor-core kernel, 2 channel-stationary 1x1 kernel
+        (lrs_conv_expand_kernel, include/lrs_conv.h)."""
+        return int(load_library().lrs_conv_expand_kernel(self.handle))
 
     @property
     def core_fused(self) -> bool:
