@@ -1305,9 +1305,11 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
                              1024 /*bars*/ + 1024 /*align*/;
       if (fixed >= static_cast<uint32_t>(kMaxSmem)) continue;
       const int ns = std::min<int>(kPMaxSlots, static_cast<int>((kMaxSmem - fixed) / slot));
-      // slots are released chunk by chunk (tcgen05.commit after each chunk's MMAs); deeper
-      // rings prefetch further ahead (shallow ones cost more below)
-      if (ns < 4) continue;
+      // slots are released chunk by chunk (tcgen05.commit after each chunk's MMAs), but the
+      // producer lanes request a tile's chunks in parallel, so the ring must hold a whole
+      // tile: with fewer slots two lanes would wait on two phases of one slot's mbarrier at
+      // once, and a parity wait cannot tell phase r from phase r + 2
+      if (ns < n_x + n_tk) continue;
       // cost (cycles per CTA): tiles x max(MMA, operand inflow, the group's share of the HBM
       // write of Y); sparse MMA ~ (A 4 KB + B bp*64 B) / 128 B/clk, dense ~ (4 KB + bp*32 B) / 128
       const int gpg = h->sms / G;

@@ -121,8 +121,43 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
   uint64_t* t1w_empty = t1s_full + 1;           // MMA -> epilogue: core MMAs done reading the window
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t1w_empty + 1);
   const int n_g = p.kh * p.kw * p.n_gk;         // G chunks per tile
+  // the producer's and MMA issuer's loop scalars, staged in shared memory (a kernel
+  // parameter read inside a loop is re-loaded from the constant bank at every use, ~100
+  // cycles each on the issue path; tools/loop_cost2.cu)
+  int* prm = reinterpret_cast<int*>(smem + p.off_bar + 1024);
 
   if (threadIdx.x == 0) {
+    prm[0] = static_cast<int>(p.acc_cols);
+    prm[1] = static_cast<int>(p.bands);
+    prm[2] = static_cast<int>(p.g_bytes);
+    prm[3] = static_cast<int>(p.g_kc);
+    prm[4] = static_cast<int>(p.g_res);
+    prm[5] = static_cast<int>(p.g_slot);
+    prm[6] = static_cast<int>(p.ipt);
+    prm[7] = static_cast<int>(p.kw);
+    prm[8] = static_cast<int>(p.n_ck);
+    prm[9] = static_cast<int>(p.n_gk);
+    prm[10] = static_cast<int>(p.n_tiles);
+    prm[11] = static_cast<int>(p.nacc);
+    prm[12] = static_cast<int>(p.nb1);
+    prm[13] = static_cast<int>(p.nb2);
+    prm[14] = static_cast<int>(p.ns_g);
+    prm[15] = static_cast<int>(p.ns_x);
+    prm[16] = static_cast<int>(p.off_g);
+    prm[17] = static_cast<int>(p.off_t1);
+    prm[18] = static_cast<int>(p.ph);
+    prm[19] = static_cast<int>(p.pw);
+    prm[20] = static_cast<int>(p.r1p);
+    prm[21] = static_cast<int>(p.r2p);
+    prm[22] = static_cast<int>(p.sw_g);
+    prm[23] = static_cast<int>(p.t1_rows);
+    prm[24] = static_cast<int>(p.t1_sw128);
+    prm[25] = static_cast<int>(p.th);
+    prm[26] = static_cast<int>(p.u_bytes);
+    prm[27] = static_cast<int>(p.u_off);
+    prm[28] = static_cast<int>(p.wc);
+    prm[29] = static_cast<int>(p.x_bytes);
+    prm[30] = static_cast<int>(p.x_slot);
     for (int i = 0; i < p.ns_x; ++i) {
       mbar_init(&full_x[i], 1);
       mbar_init(&empty_x[i], 1);
@@ -162,43 +197,64 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
   CTRACE(p, threadIdx.x == 0 && blockIdx.x == 0, 8190);
 
   if (warp == 0) {
+    const int bands_ = static_cast<int>(smem_param(prm + 1));
+    const uint32_t g_bytes_ = static_cast<uint32_t>(smem_param(prm + 2));
+    const int g_kc_ = static_cast<int>(smem_param(prm + 3));
+    const int g_res_ = static_cast<int>(smem_param(prm + 4));
+    const uint32_t g_slot_ = static_cast<uint32_t>(smem_param(prm + 5));
+    const int ipt_ = static_cast<int>(smem_param(prm + 6));
+    const int n_ck_ = static_cast<int>(smem_param(prm + 8));
+    const int n_gk_ = static_cast<int>(smem_param(prm + 9));
+    const int n_tiles_ = static_cast<int>(smem_param(prm + 10));
+    const int nacc_ = static_cast<int>(smem_param(prm + 11));
+    const int ns_g_ = static_cast<int>(smem_param(prm + 14));
+    const int ns_x_ = static_cast<int>(smem_param(prm + 15));
+    const uint32_t off_g_ = static_cast<uint32_t>(smem_param(prm + 16));
+    const int ph_ = static_cast<int>(smem_param(prm + 18));
+    const int pw_ = static_cast<int>(smem_param(prm + 19));
+    const int r1p_ = static_cast<int>(smem_param(prm + 20));
+    const int th_ = static_cast<int>(smem_param(prm + 25));
+    const uint32_t u_bytes_ = static_cast<uint32_t>(smem_param(prm + 26));
+    const uint32_t u_off_ = static_cast<uint32_t>(smem_param(prm + 27));
+    const uint32_t x_bytes_ = static_cast<uint32_t>(smem_param(prm + 29));
+    const uint32_t x_slot_ = static_cast<uint32_t>(smem_param(prm + 30));
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
       // Requests follow the MMA thread's consumption order (a1(k+1) before a2(k) when two
       // TMEM buffers allow the lookahead): a streamed G must never block an X box the
       // MMA thread needs first.
       int ix = 0, ig = 0;
-      const int m_tiles = static_cast<int>(blockIdx.x) < p.n_tiles
-                              ? (p.n_tiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+      const int m_tiles = static_cast<int>(blockIdx.x) < n_tiles_
+                              ? (n_tiles_ - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
                               : 0;
       auto load_x = [&](int k) {
         const int tile = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
-        const int g = tile / p.bands, ho0 = (tile - g * p.bands) * p.th;
-        for (int c = 0; c < p.n_ck; ++c, ++ix) {
-          const int s = ix % p.ns_x;
-          if (ix >= p.ns_x) mbar_wait(&empty_x[s], ((ix / p.ns_x) - 1) & 1);
+        const int g = tile / bands_, ho0 = (tile - g * bands_) * th_;
+        for (int c = 0; c < n_ck_; ++c, ++ix) {
+          const int s = ix % ns_x_;
+          if (ix >= ns_x_) mbar_wait(&empty_x[s], ((ix / ns_x_) - 1) & 1);
           CTRACE(p, blockIdx.x == 0 && c == 0 && k < 4, 8200 + 10 * k + 1);
-          uint8_t* dst = smem + s * p.x_slot;
+          uint8_t* dst = smem + s * x_slot_;
           if (LRS_XDBG(p.dbg & 4)) {  // timing experiment: no X / U loads (stale shared memory, wrong T2)
             mbar_arrive(&full_x[s]);
             continue;
           }
-          mbar_arrive_expect_tx(&full_x[s], p.x_bytes + p.u_bytes);
-          tma_load_4d(dst, &p.tmX, &full_x[s], c * 64, -p.pw, ho0 - p.ph, g * p.ipt);
-          tma_load_2d(dst + p.u_off, &p.tmU, &full_x[s], c * 64, 0);
+          mbar_arrive_expect_tx(&full_x[s], x_bytes_ + u_bytes_);
+          tma_load_4d(dst, &p.tmX, &full_x[s], c * 64, -pw_, ho0 - ph_, g * ipt_);
+          tma_load_2d(dst + u_off_, &p.tmU, &full_x[s], c * 64, 0);
         }
       };
       auto load_g = [&]() {
-        if (p.g_res) return;
+        if (g_res_) return;
         for (int j = 0; j < n_g; ++j, ++ig) {
-          const int s = ig % p.ns_g;
-          if (ig >= p.ns_g) mbar_wait(&empty_g[s], ((ig / p.ns_g) - 1) & 1);
-          const int t = j / p.n_gk, gk = j - t * p.n_gk;
-          mbar_arrive_expect_tx(&full_g[s], p.g_bytes);
-          tma_load_2d(smem + p.off_g + s * p.g_slot, &p.tmG, &full_g[s], t * p.r1p + gk * p.g_kc, 0);
+          const int s = ig % ns_g_;
+          if (ig >= ns_g_) mbar_wait(&empty_g[s], ((ig / ns_g_) - 1) & 1);
+          const int t = j / n_gk_, gk = j - t * n_gk_;
+          mbar_arrive_expect_tx(&full_g[s], g_bytes_);
+          tma_load_2d(smem + off_g_ + s * g_slot_, &p.tmG, &full_g[s], t * r1p_ + gk * g_kc_, 0);
         }
       };
-      if (!CPDW && p.nacc == 2) {
+      if (!CPDW && nacc_ == 2) {
         if (m_tiles > 0) load_x(0);
         for (int k = 0; k < m_tiles; ++k) {
           if (k + 1 < m_tiles) load_x(k + 1);
@@ -212,6 +268,29 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       }
     }
   } else if (warp == 1) {
+    const uint32_t acc_cols_ = static_cast<uint32_t>(smem_param(prm + 0));
+    const int g_kc_ = static_cast<int>(smem_param(prm + 3));
+    const int g_res_ = static_cast<int>(smem_param(prm + 4));
+    const uint32_t g_slot_ = static_cast<uint32_t>(smem_param(prm + 5));
+    const int kw_ = static_cast<int>(smem_param(prm + 7));
+    const int n_ck_ = static_cast<int>(smem_param(prm + 8));
+    const int n_gk_ = static_cast<int>(smem_param(prm + 9));
+    const int n_tiles_ = static_cast<int>(smem_param(prm + 10));
+    const int nacc_ = static_cast<int>(smem_param(prm + 11));
+    const int nb1_ = static_cast<int>(smem_param(prm + 12));
+    const int nb2_ = static_cast<int>(smem_param(prm + 13));
+    const int ns_g_ = static_cast<int>(smem_param(prm + 14));
+    const int ns_x_ = static_cast<int>(smem_param(prm + 15));
+    const uint32_t off_g_ = static_cast<uint32_t>(smem_param(prm + 16));
+    const uint32_t off_t1_ = static_cast<uint32_t>(smem_param(prm + 17));
+    const int r1p_ = static_cast<int>(smem_param(prm + 20));
+    const int r2p_ = static_cast<int>(smem_param(prm + 21));
+    const uint32_t sw_g_ = static_cast<uint32_t>(smem_param(prm + 22));
+    const uint32_t t1_rows_ = static_cast<uint32_t>(smem_param(prm + 23));
+    const int t1_sw128_ = static_cast<int>(smem_param(prm + 24));
+    const uint32_t u_off_ = static_cast<uint32_t>(smem_param(prm + 27));
+    const int wc_ = static_cast<int>(smem_param(prm + 28));
+    const uint32_t x_slot_ = static_cast<uint32_t>(smem_param(prm + 30));
     // -------------------------------------------------------------- MMA issuer
     // ONE elected thread runs the whole loop (its mbarrier waits included): an elect +
     // reconvergence per item costs ~240 cycles of issue (tools/mma_seq.cu: 108 vs 48
@@ -220,58 +299,58 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
     // Descriptors are linear in the shared-memory address (start >> 4 in the low 14
     // bits), so every operand is a base descriptor plus a precomputed offset: the issue
     // loop is adds and MMAs (address arithmetic per MMA made it issue-bound).
-    const uint32_t idesc1 = umma_idesc(1u, static_cast<uint32_t>(p.r1p), 128u);
-    const uint32_t idesc2 = umma_idesc(1u, static_cast<uint32_t>(p.r2p), 128u);
+    const uint32_t idesc1 = umma_idesc(1u, static_cast<uint32_t>(r1p_), 128u);
+    const uint32_t idesc2 = umma_idesc(1u, static_cast<uint32_t>(r2p_), 128u);
     const uint32_t base = smem_u32(smem);
-    const uint32_t t1w = smem_u32(smem + p.off_t1);
-    const uint32_t lbo = p.t1_rows * 16u;
+    const uint32_t t1w = smem_u32(smem + off_t1_);
+    const uint32_t lbo = t1_rows_ * 16u;
     const uint64_t xd0 = umma_desc(base, 128);
-    const uint64_t ud0 = umma_desc(base + p.u_off, 128);
-    const uint64_t gd0 = umma_desc(base + p.off_g, p.sw_g);
-    const uint64_t t1d0 = p.t1_sw128 ? umma_desc(t1w, 128) : umma_desc_noswz(t1w, lbo, 128u);
+    const uint64_t ud0 = umma_desc(base + u_off_, 128);
+    const uint64_t gd0 = umma_desc(base + off_g_, sw_g_);
+    const uint64_t t1d0 = t1_sw128_ ? umma_desc(t1w, 128) : umma_desc_noswz(t1w, lbo, 128u);
     // T1 window: descriptor units (16 B) per window row, per G chunk of g_kc ranks, per K step of 16
-    const uint32_t a_rs = p.t1_sw128 ? 8u : 1u;
-    const uint32_t a_gs = p.t1_sw128 ? p.t1_rows * 8u : static_cast<uint32_t>(p.g_kc / 8) * (lbo >> 4);
-    const uint32_t a_ks = p.t1_sw128 ? 2u : 2u * (lbo >> 4);
-    const uint32_t x16 = p.x_slot >> 4, g16 = p.g_slot >> 4;
+    const uint32_t a_rs = t1_sw128_ ? 8u : 1u;
+    const uint32_t a_gs = t1_sw128_ ? t1_rows_ * 8u : static_cast<uint32_t>(g_kc_ / 8) * (lbo >> 4);
+    const uint32_t a_ks = t1_sw128_ ? 2u : 2u * (lbo >> 4);
+    const uint32_t x16 = x_slot_ >> 4, g16 = g_slot_ >> 4;
     int ix = 0, ig = 0;
-    const int m_tiles = static_cast<int>(blockIdx.x) < p.n_tiles
-                            ? (p.n_tiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+    const int m_tiles = static_cast<int>(blockIdx.x) < n_tiles_
+                            ? (n_tiles_ - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
                             : 0;
     // a1 of tile k into TMEM buffer b(k)
     auto phase_a1 = [&](int k) {
-      const int b = p.nacc == 2 ? (k & 1) : 0;
-      const int use = p.nacc == 2 ? (k >> 1) : k;
+      const int b = nacc_ == 2 ? (k & 1) : 0;
+      const int use = nacc_ == 2 ? (k >> 1) : k;
       if (use > 0) {
         mbar_wait(&acc_empty[b], (use - 1) & 1);
         tc_fence_after();
       }
-      const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * p.acc_cols;
+      const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * acc_cols_;
       // ---- a1: T1 (window rows) = X window . U_in, K = Cin in 64-channel chunks
-      for (int c = 0; c < p.n_ck; ++c, ++ix) {
-        const int s = ix % p.ns_x;
-        mbar_wait(&full_x[s], (ix / p.ns_x) & 1);
+      for (int c = 0; c < n_ck_; ++c, ++ix) {
+        const int s = ix % ns_x_;
+        mbar_wait(&full_x[s], (ix / ns_x_) & 1);
         tc_fence_after();
         CTRACE(p, blockIdx.x == 0 && k < 4 && c == 0, 8200 + 10 * k + 2);
         const uint64_t xd = xd0 + static_cast<uint32_t>(s) * x16;
         const uint64_t ud = ud0 + static_cast<uint32_t>(s) * x16;
         {
-          for (int b1 = 0; b1 < p.nb1; ++b1) {
-            const uint32_t d = acc0 + static_cast<uint32_t>(b1 * p.r1p);
+          for (int b1 = 0; b1 < nb1_; ++b1) {
+            const uint32_t d = acc0 + static_cast<uint32_t>(b1 * r1p_);
             const uint64_t xb = xd + static_cast<uint32_t>(b1) * 1024u;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) mma_bf16(d, xb + 2 * kk, ud + 2 * kk, idesc1, (c > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&empty_x[s]);
-          if (c == p.n_ck - 1) mma_commit(&t1_full[b]);
+          if (c == n_ck_ - 1) mma_commit(&t1_full[b]);
         }
       }
       CTRACE(p, blockIdx.x == 0 && k < 4, 8200 + 10 * k + 3);
     };
     // a2 of tile k: T2 over T1's columns of buffer b(k), from the restaged window
     auto phase_a2 = [&](int k) {
-      const int b = p.nacc == 2 ? (k & 1) : 0;
-      const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * p.acc_cols;
+      const int b = nacc_ == 2 ? (k & 1) : 0;
+      const uint32_t acc0 = tmem + static_cast<uint32_t>(b) * acc_cols_;
       const uint32_t t2c = acc0;  // T2 overwrites T1's columns (restaged already)
       // ---- wait for the bf16 T1 window in shared memory
       mbar_wait(t1s_full, k & 1);
@@ -280,10 +359,10 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       // ---- a2: T2 = sum over taps of (window shifted by y*wc + x rows) . G[tap]
       // Operand descriptors advance by running offsets: next G chunk of the tap (+a_gs),
       // next tap column (+a_rs), next tap row (+(wc - kw) rows more).
-      const uint32_t a_tap = a_rs - static_cast<uint32_t>(p.n_gk - 1) * a_gs;
-      const uint32_t a_row = static_cast<uint32_t>(p.wc - p.kw) * a_rs;
+      const uint32_t a_tap = a_rs - static_cast<uint32_t>(n_gk_ - 1) * a_gs;
+      const uint32_t a_row = static_cast<uint32_t>(wc_ - kw_) * a_rs;
       const uint32_t a_b2 = 128u * a_rs;
-      if (p.g_res) {
+      if (g_res_) {
         // resident G: one wait per chunk for the CTA's first tile, then one issue block
         if (k == 0)
           for (int j = 0; j < n_g; ++j) mbar_wait(&full_g[j], 0);
@@ -295,16 +374,16 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
           for (int j = 0; j < n_g; ++j) {
             uint64_t ab = t1d0 + aj;
             uint32_t d = t2c;
-            for (int b2 = 0; b2 < p.nb2; ++b2, ab += a_b2, d += static_cast<uint32_t>(p.r2p)) {
+            for (int b2 = 0; b2 < nb2_; ++b2, ab += a_b2, d += static_cast<uint32_t>(r2p_)) {
 #pragma unroll
               for (int kk = 0; kk < GS; ++kk)
                 mma_bf16(d, ab + kk * a_ks, bj + 2 * kk, idesc2, (j > 0 || kk > 0) ? 1u : 0u);
             }
             bj += g16;
-            if (++gk == p.n_gk) {
+            if (++gk == n_gk_) {
               gk = 0;
               aj += a_tap;
-              if (++tx == p.kw) {
+              if (++tx == kw_) {
                 tx = 0;
                 aj += a_row;
               }
@@ -317,24 +396,24 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
         uint32_t aj = 0;
         int gk = 0, tx = 0;
         for (int j = 0; j < n_g; ++j, ++ig) {
-          const int s = ig % p.ns_g;
-          mbar_wait(&full_g[s], static_cast<uint32_t>((ig / p.ns_g) & 1));
+          const int s = ig % ns_g_;
+          mbar_wait(&full_g[s], static_cast<uint32_t>((ig / ns_g_) & 1));
           tc_fence_after();
           const uint64_t bj = gd0 + static_cast<uint32_t>(s) * g16;
           {
             uint64_t ab = t1d0 + aj;
             uint32_t d = t2c;
-            for (int b2 = 0; b2 < p.nb2; ++b2, ab += a_b2, d += static_cast<uint32_t>(p.r2p)) {
+            for (int b2 = 0; b2 < nb2_; ++b2, ab += a_b2, d += static_cast<uint32_t>(r2p_)) {
 #pragma unroll
               for (int kk = 0; kk < GS; ++kk)
                 mma_bf16(d, ab + kk * a_ks, bj + 2 * kk, idesc2, (j > 0 || kk > 0) ? 1u : 0u);
             }
             mma_commit(&empty_g[s]);
           }
-          if (++gk == p.n_gk) {
+          if (++gk == n_gk_) {
             gk = 0;
             aj += a_tap;
-            if (++tx == p.kw) {
+            if (++tx == kw_) {
               tx = 0;
               aj += a_row;
             }
@@ -351,7 +430,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
     };
     if constexpr (CPDW) {
       for (int k = 0; k < m_tiles; ++k) phase_a1(k);
-    } else if (p.nacc == 2) {
+    } else if (nacc_ == 2) {
       // a1 of tile k+1 is issued before a2 of tile k (two TMEM buffers): the epilogue's T1
       // restage of tile k then overlaps the projection MMAs of tile k+1
       if (m_tiles > 0) phase_a1(0);

@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
     // the X chunk l of every tile (item k * nq + l), lane 0 also the T1 chunks
     int xs = lane, xr = 0;       // this lane's X item
     int ts = n_x, tr = 0;        // lane 0's first T1 item of the tile
+    while (xs >= ns) { xs -= ns; ++xr; }  // (a tile may hold more chunks than the ring has slots)
     while (ts >= ns) { ts -= ns; ++tr; }
     for (int pt = li_; pt < n_pt; pt += gct) {
       const int p0 = pt * bp;

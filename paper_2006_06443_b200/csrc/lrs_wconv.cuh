@@ -136,6 +136,21 @@ __device__ __forceinline__ TileCoord tile_coord(const WconvParams& p, int tile) 
   return c;
 }
 
+__device__ __forceinline__ TileCoord tile_coord_v(int tile, int n_mt, int cbands, int bands, int th, int tcols) {
+  TileCoord c;
+  c.mt = tile % n_mt;
+  tile /= n_mt;
+  const int cband = tile % cbands;
+  tile /= cbands;
+  const int band = tile % bands;
+  const int grp = tile / bands;
+  c.n0 = grp * 8;
+  c.ho0 = band * th;
+  c.wo0 = cband * tcols;
+  c.j0 = c.mt * 128;
+  return c;
+}
+
 // NU = the layer's exact unit count (1..kWMaxUnits): the MMA issue loops are fully
 // unrolled without predicates -- a generic 8-unit loop measured 17-39 % slower
 // (instruction fetch of the issuing warp dominates small MMAs).
@@ -158,8 +173,43 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
 
   if (WTRACE(p) && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
   const int nwin = p.n_tk + p.n_xw;
+  // the role loops' scalars, staged in shared memory: a kernel parameter read inside a
+  // loop is re-loaded from the constant bank at every use (~100 cycles each on the issue
+  // path, tools/loop_cost2.cu); a value loaded from shared memory stays in a register
+  int* prm = reinterpret_cast<int*>(smem + p.off_bar + 512);
 
   if (threadIdx.x == 0) {
+    prm[0] = static_cast<int>(p.nwb);
+    prm[1] = static_cast<int>(p.n_tiles);
+    prm[2] = static_cast<int>(p.n_mt);
+    prm[3] = static_cast<int>(p.n_ck);
+    prm[4] = static_cast<int>(p.n_xw);
+    prm[5] = static_cast<int>(p.n_tk);
+    prm[6] = static_cast<int>(p.ns);
+    prm[7] = static_cast<int>(p.bpi);
+    prm[8] = static_cast<int>(p.cpw);
+    prm[9] = static_cast<int>(p.t_kc);
+    prm[10] = static_cast<int>(p.x_win_bytes);
+    prm[11] = static_cast<int>(p.t_win_bytes);
+    prm[12] = static_cast<int>(p.win_stride);
+    prm[13] = static_cast<int>(p.a_slot);
+    prm[14] = static_cast<int>(p.e_slot);
+    prm[15] = static_cast<int>(p.sw);
+    prm[16] = static_cast<int>(p.pw);
+    prm[17] = static_cast<int>(p.sh);
+    prm[18] = static_cast<int>(p.ph);
+    prm[19] = static_cast<int>(p.sw_t);
+    prm[20] = static_cast<int>(p.e_col0);
+    prm[21] = static_cast<int>(p.e_slots);
+    prm[22] = static_cast<int>(p.nacc);
+    prm[23] = static_cast<int>(p.acc_cols);
+    prm[24] = static_cast<int>(p.cbands);
+    prm[25] = static_cast<int>(p.bands);
+    prm[26] = static_cast<int>(p.th);
+    prm[27] = static_cast<int>(p.tcols);
+    prm[28] = static_cast<int>(p.off_a);
+    prm[29] = static_cast<int>(p.off_e);
+    prm[30] = static_cast<int>(p.off_res);
     for (int i = 0; i < p.nwb; ++i) {
       mbar_init(&win_full[i], 1);
       mbar_init(&win_empty[i], 1);
@@ -192,6 +242,33 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   // the producer waits just before the first T window, overlapping the previous kernel.
 
   if (warp == 0) {
+    const int nwb_ = static_cast<int>(smem_param(prm + 0));
+    const int n_tiles_ = static_cast<int>(smem_param(prm + 1));
+    const int n_mt_ = static_cast<int>(smem_param(prm + 2));
+    const int n_ck_ = static_cast<int>(smem_param(prm + 3));
+    const int n_xw_ = static_cast<int>(smem_param(prm + 4));
+    const int n_tk_ = static_cast<int>(smem_param(prm + 5));
+    const int ns_ = static_cast<int>(smem_param(prm + 6));
+    const int bpi_ = static_cast<int>(smem_param(prm + 7));
+    const int cpw_ = static_cast<int>(smem_param(prm + 8));
+    const int t_kc_ = static_cast<int>(smem_param(prm + 9));
+    const uint32_t x_win_bytes_ = static_cast<uint32_t>(smem_param(prm + 10));
+    const uint32_t t_win_bytes_ = static_cast<uint32_t>(smem_param(prm + 11));
+    const uint32_t win_stride_ = static_cast<uint32_t>(smem_param(prm + 12));
+    const uint32_t a_slot_ = static_cast<uint32_t>(smem_param(prm + 13));
+    const uint32_t e_slot_ = static_cast<uint32_t>(smem_param(prm + 14));
+    const int sw_ = static_cast<int>(smem_param(prm + 15));
+    const int pw_ = static_cast<int>(smem_param(prm + 16));
+    const int sh_ = static_cast<int>(smem_param(prm + 17));
+    const int ph_ = static_cast<int>(smem_param(prm + 18));
+    const uint32_t sw_t_ = static_cast<uint32_t>(smem_param(prm + 19));
+    const uint32_t off_a_ = static_cast<uint32_t>(smem_param(prm + 28));
+    const uint32_t off_e_ = static_cast<uint32_t>(smem_param(prm + 29));
+    const uint32_t off_res_ = static_cast<uint32_t>(smem_param(prm + 30));
+    const int cbands_ = static_cast<int>(smem_param(prm + 24));
+    const int bands_ = static_cast<int>(smem_param(prm + 25));
+    const int th_ = static_cast<int>(smem_param(prm + 26));
+    const int tcols_ = static_cast<int>(smem_param(prm + 27));
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
       int it = 0, wg = 0, buf = 0;
@@ -199,37 +276,37 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       // the M-tile's block stream (chunk starts + per-block tap offsets), staged in shared
       // memory by independent (pipelined) loads when the M-tile changes: a global load on
       // the issue path measured ~250 ns each (tools/wtrace.py producer stamps)
-      int* so_s = reinterpret_cast<int*>(smem + p.off_res);   // [n_ck + 1], relative to mt0
-      uint32_t* tap_s = reinterpret_cast<uint32_t*>(so_s + p.n_ck + 1);
+      int* so_s = reinterpret_cast<int*>(smem + off_res_);   // [n_ck + 1], relative to mt0
+      uint32_t* tap_s = reinterpret_cast<uint32_t*>(so_s + n_ck_ + 1);
       int cur_mt = -1, mt0 = 0;
       bool waited = false;
       // CTAs own contiguous tile ranges, M-tile fastest: consecutive tiles of a CTA share
       // their windows; with one ring buffer per window (nwb == nwin) a window still resident
       // from the previous tile is reused instead of re-loaded
-      const bool contig = p.nwb == nwin;
-      const int t_begin = contig ? static_cast<int>(static_cast<long long>(blockIdx.x) * p.n_tiles / gridDim.x)
+      const bool contig = nwb_ == nwin;
+      const int t_begin = contig ? static_cast<int>(static_cast<long long>(blockIdx.x) * n_tiles_ / gridDim.x)
                                  : static_cast<int>(blockIdx.x);
-      const int t_end = contig ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * p.n_tiles / gridDim.x)
-                               : p.n_tiles;
+      const int t_end = contig ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * n_tiles_ / gridDim.x)
+                               : n_tiles_;
       const int t_step = contig ? 1 : static_cast<int>(gridDim.x);
       int prev_win = -1;
       for (int tile = t_begin; tile < t_end; tile += t_step) {
-        const TileCoord tc = tile_coord(p, tile);
-        const int win_key = tile / p.n_mt;
-        const bool reuse = p.nwb == nwin && win_key == prev_win;
+        const TileCoord tc = tile_coord_v(tile, n_mt_, cbands_, bands_, th_, tcols_);
+        const int win_key = tile / n_mt_;
+        const bool reuse = nwb_ == nwin && win_key == prev_win;
         prev_win = win_key;
         if (tc.mt != cur_mt) {
-          mt0 = __ldg(p.stream_off + tc.mt * p.n_ck);
-          for (int i = 0; i <= p.n_ck; ++i) so_s[i] = __ldg(p.stream_off + tc.mt * p.n_ck + i) - mt0;
-          const int len = so_s[p.n_ck];
+          mt0 = __ldg(p.stream_off + tc.mt * n_ck_);
+          for (int i = 0; i <= n_ck_; ++i) so_s[i] = __ldg(p.stream_off + tc.mt * n_ck_ + i) - mt0;
+          const int len = so_s[n_ck_];
           for (int i = 0; i < len; ++i) tap_s[i] = __ldg(p.blk_tap + mt0 + i);
           cur_mt = tc.mt;
         }
         for (int w = 0; w < nwin; ++w, ++wg) {
-          if (wg >= p.nwb) mbar_wait(&win_empty[buf], wph ^ 1u);
-          uint8_t* wdst = smem + buf * p.win_stride;
+          if (wg >= nwb_) mbar_wait(&win_empty[buf], wph ^ 1u);
+          uint8_t* wdst = smem + buf * win_stride_;
           if (WTRACE(p) && blockIdx.x == 0 && wg < 16) p.trace[3600 + wg] = gtimer();
-          const int tk = w - p.n_xw;  // >= 0: dense (T) window, after the tile's sparse ones
+          const int tk = w - n_xw_;  // >= 0: dense (T) window, after the tile's sparse ones
           if (tk >= 0 && !waited) {
             pdl_wait();
             pdl_launch_dependents();
@@ -238,35 +315,35 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           if (WDBG(p, 64) || reuse) {
             mbar_arrive(&win_full[buf]);  // window already resident (or timing experiment)
           } else if (tk >= 0) {
-            mbar_arrive_expect_tx(&win_full[buf], p.t_win_bytes);
-            tma_load_4d(wdst, &p.tmT, &win_full[buf], tk * p.t_kc, tc.n0, tc.wo0, tc.ho0);
+            mbar_arrive_expect_tx(&win_full[buf], t_win_bytes_);
+            tma_load_4d(wdst, &p.tmT, &win_full[buf], tk * t_kc_, tc.n0, tc.wo0, tc.ho0);
           }
           if (tk >= 0) {
-            const int slot = it % p.ns;
-            if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
-            mbar_arrive_expect_tx(&a_full[slot], 128u * p.sw_t);
-            bulk_load(smem + p.off_a + slot * p.a_slot,
-                      p.img_dense + (static_cast<size_t>(tc.mt) * p.n_tk + tk) * (128u * p.sw_t), 128u * p.sw_t,
+            const int slot = it % ns_;
+            if (it >= ns_) mbar_wait(&a_empty[slot], ((it / ns_) - 1) & 1);
+            mbar_arrive_expect_tx(&a_full[slot], 128u * sw_t_);
+            bulk_load(smem + off_a_ + slot * a_slot_,
+                      p.img_dense + (static_cast<size_t>(tc.mt) * n_tk_ + tk) * (128u * sw_t_), 128u * sw_t_,
                       &a_full[slot]);
             ++it;
           } else {
-            const int c = w * p.cpw;  // first chunk of this window
+            const int c = w * cpw_;  // first chunk of this window
             if (!(WDBG(p, 64)) && !reuse) {
-              mbar_arrive_expect_tx(&win_full[buf], static_cast<uint32_t>(p.cpw) * p.x_win_bytes);
-              for (int q = 0; q < p.cpw; ++q)
-                tma_load_4d(wdst + q * p.x_win_bytes, &p.tmX, &win_full[buf], (c + q) * 64, tc.n0,
-                            tc.wo0 * p.sw - p.pw, tc.ho0 * p.sh - p.ph);
+              mbar_arrive_expect_tx(&win_full[buf], static_cast<uint32_t>(cpw_) * x_win_bytes_);
+              for (int q = 0; q < cpw_; ++q)
+                tma_load_4d(wdst + q * x_win_bytes_, &p.tmX, &win_full[buf], (c + q) * 64, tc.n0,
+                            tc.wo0 * sw_ - pw_, tc.ho0 * sh_ - ph_);
             }
             // this window's blocks in stream order, bpi per item: every item costs an
             // mbarrier hand-off and a tcgen05.commit (~450 cycles, tools/mma_rate2.cu), so
             // items are as large as smem allows; each is one bulk copy of A and one of E
-            const int sb = so_s[c], se = so_s[c + p.cpw];
-            for (int b = sb; b < se; b += p.bpi) {
-              const int np = min(p.bpi, se - b);
+            const int sb = so_s[c], se = so_s[c + cpw_];
+            for (int b = sb; b < se; b += bpi_) {
+              const int np = min(bpi_, se - b);
               const bool last = b + np >= se;
-              const int slot = it % p.ns;
+              const int slot = it % ns_;
               if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it] = gtimer();
-              if (it >= p.ns) mbar_wait(&a_empty[slot], ((it / p.ns) - 1) & 1);
+              if (it >= ns_) mbar_wait(&a_empty[slot], ((it / ns_) - 1) & 1);
               if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it + 1] = gtimer();
 #pragma unroll
               for (int q = 0; q < kWMaxBpi; ++q)
@@ -278,20 +355,41 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                 mbar_arrive(&a_full[slot]);
               } else {
                 mbar_arrive_expect_tx(&a_full[slot], static_cast<uint32_t>(np) * (kSpBlockBytes + kEBlockBytes));
-                bulk_load(smem + p.off_a + slot * p.a_slot, p.img_sp + static_cast<size_t>(mt0 + b) * kSpBlockBytes,
+                bulk_load(smem + off_a_ + slot * a_slot_, p.img_sp + static_cast<size_t>(mt0 + b) * kSpBlockBytes,
                           static_cast<uint32_t>(np) * kSpBlockBytes, &a_full[slot]);
-                bulk_load(smem + p.off_e + slot * p.e_slot, p.img_e + static_cast<size_t>(mt0 + b) * kEBlockBytes,
+                bulk_load(smem + off_e_ + slot * e_slot_, p.img_e + static_cast<size_t>(mt0 + b) * kEBlockBytes,
                           static_cast<uint32_t>(np) * kEBlockBytes, &a_full[slot]);
               }
               if (WTRACE(p) && blockIdx.x == 0 && it < 64) p.trace[3000 + 3 * it + 2] = gtimer();
               ++it;
             }
           }
-          if (++buf == p.nwb) { buf = 0; wph ^= 1u; }
+          if (++buf == nwb_) { buf = 0; wph ^= 1u; }
         }
       }
     }
   } else if (warp == 1) {
+    const int nwb_ = static_cast<int>(smem_param(prm + 0));
+    const int n_tiles_ = static_cast<int>(smem_param(prm + 1));
+    const int n_xw_ = static_cast<int>(smem_param(prm + 4));
+    const int ns_ = static_cast<int>(smem_param(prm + 6));
+    const int bpi_ = static_cast<int>(smem_param(prm + 7));
+    const uint32_t win_stride_ = static_cast<uint32_t>(smem_param(prm + 12));
+    const uint32_t a_slot_ = static_cast<uint32_t>(smem_param(prm + 13));
+    const uint32_t e_slot_ = static_cast<uint32_t>(smem_param(prm + 14));
+    const int sw_ = static_cast<int>(smem_param(prm + 15));
+    const uint32_t sw_t_ = static_cast<uint32_t>(smem_param(prm + 19));
+    const uint32_t e_col0_ = static_cast<uint32_t>(smem_param(prm + 20));
+    const int e_slots_ = static_cast<int>(smem_param(prm + 21));
+    const int nacc_ = static_cast<int>(smem_param(prm + 22));
+    const uint32_t acc_cols_ = static_cast<uint32_t>(smem_param(prm + 23));
+    const uint32_t off_a_ = static_cast<uint32_t>(smem_param(prm + 28));
+    const uint32_t off_e_ = static_cast<uint32_t>(smem_param(prm + 29));
+    const int n_mt_ = static_cast<int>(smem_param(prm + 2));
+    const int cbands_ = static_cast<int>(smem_param(prm + 24));
+    const int bands_ = static_cast<int>(smem_param(prm + 25));
+    const int th_ = static_cast<int>(smem_param(prm + 26));
+    const int tcols_ = static_cast<int>(smem_param(prm + 27));
     // -------------------------------------------------------------- MMA issuer
     // ONE elected thread runs the whole loop, its mbarrier waits included: an elect +
     // warp reconvergence around every item cost ~240 cycles of issue each
@@ -300,8 +398,8 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     // so every per-unit descriptor is precomputed once and the inner loop
     // only adds byte offsets >> 4: the single-thread issue loop stays short.
     const uint32_t win0 = smem_u32(smem);
-    const uint32_t t_pos = 8u * p.sw_t;  // bytes per output position in a T window
-    const uint32_t x_sbo = 1024u * static_cast<uint32_t>(p.sw);
+    const uint32_t t_pos = 8u * sw_t_;  // bytes per output position in a T window
+    const uint32_t x_sbo = 1024u * static_cast<uint32_t>(sw_);
     uint32_t dcol[NU], idu[NU];
     uint64_t bxd[NU], btd[NU];
 #pragma unroll
@@ -310,33 +408,33 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         dcol[u] = tmem + static_cast<uint32_t>(p.u_col[u]);
         idu[u] = umma_idesc(1u, static_cast<uint32_t>(p.u_n[u]), 128u);
         bxd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_xpos[u]) * 1024u, 128, x_sbo);
-        btd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_tpos[u]) * t_pos, p.sw_t, t_pos);
+        btd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_tpos[u]) * t_pos, sw_t_, t_pos);
       }
     }
-    const uint64_t ad_dense = umma_desc(smem_u32(smem + p.off_a), p.sw_t);
-    const uint64_t ad_sp = umma_desc(smem_u32(smem + p.off_a), 64);
-    const uint64_t ed0 = umma_desc_rows16(smem_u32(smem + p.off_e));
-    const uint32_t slot_a16 = p.a_slot >> 4, slot_e16 = p.e_slot >> 4;
-    const uint32_t win16 = p.win_stride >> 4;
-    const int ksteps = static_cast<int>(p.sw_t / 32);
+    const uint64_t ad_dense = umma_desc(smem_u32(smem + off_a_), sw_t_);
+    const uint64_t ad_sp = umma_desc(smem_u32(smem + off_a_), 64);
+    const uint64_t ed0 = umma_desc_rows16(smem_u32(smem + off_e_));
+    const uint32_t slot_a16 = a_slot_ >> 4, slot_e16 = e_slot_ >> 4;
+    const uint32_t win16 = win_stride_ >> 4;
+    const int ksteps = static_cast<int>(sw_t_ / 32);
     int slot = 0, k = 0, buf = 0, eslot = 0;
     uint32_t ph = 0, wph = 0;
     if (elect_one()) {
-    const bool contig = p.nwb == nwin;  // must match the producer's tile order
-    const int t_begin = contig ? static_cast<int>(static_cast<long long>(blockIdx.x) * p.n_tiles / gridDim.x)
+    const bool contig = nwb_ == nwin;  // must match the producer's tile order
+    const int t_begin = contig ? static_cast<int>(static_cast<long long>(blockIdx.x) * n_tiles_ / gridDim.x)
                                : static_cast<int>(blockIdx.x);
-    const int t_end = contig ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * p.n_tiles / gridDim.x)
-                             : p.n_tiles;
+    const int t_end = contig ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * n_tiles_ / gridDim.x)
+                             : n_tiles_;
     const int t_step = contig ? 1 : static_cast<int>(gridDim.x);
     for (int tile = t_begin; tile < t_end; tile += t_step, ++k) {
-      const TileCoord tc = tile_coord(p, tile);
-      const int b = p.nacc == 2 ? (k & 1) : 0;
-      const int use = p.nacc == 2 ? (k >> 1) : k;  // previous uses of accumulator b
+      const TileCoord tc = tile_coord_v(tile, n_mt_, cbands_, bands_, th_, tcols_);
+      const int b = nacc_ == 2 ? (k & 1) : 0;
+      const int use = nacc_ == 2 ? (k >> 1) : k;  // previous uses of accumulator b
       if (use > 0) {
         mbar_wait(&acc_empty[b], (use - 1) & 1);
         tc_fence_after();
       }
-      const uint32_t acc0 = static_cast<uint32_t>(b) * p.acc_cols;
+      const uint32_t acc0 = static_cast<uint32_t>(b) * acc_cols_;
       if (WTRACE(p) && blockIdx.x == 0 && k < 16) p.trace[100 + 4 * k] = gtimer();
       for (int w = 0; w < nwin; ++w) {
         if (WTRACE(p) && blockIdx.x == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w] = gtimer();
@@ -344,7 +442,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         tc_fence_after();
         if (WTRACE(p) && blockIdx.x == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w + 1] = gtimer();
         const uint32_t boff = static_cast<uint32_t>(buf) * win16;
-        if (w >= p.n_xw) {  // dense window: the accumulator already holds the sparse term
+        if (w >= n_xw_) {  // dense window: the accumulator already holds the sparse term
           mbar_wait(&a_full[slot], ph);
           tc_fence_after();
           const uint64_t ab = ad_dense + slot * slot_a16;
@@ -354,12 +452,12 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
               {
                 for (int kk = 0; kk < ksteps; ++kk)
                   mma_bf16(dcol[u] + acc0, ab + 2 * kk, btd[u] + boff + 2 * kk, idu[u],
-                           (p.n_xw > 0 || w > 0 || kk > 0) ? 1u : 0u);  // S empty: dense starts the sum
+                           (n_xw_ > 0 || w > 0 || kk > 0) ? 1u : 0u);  // S empty: dense starts the sum
               }
             }
             mma_commit(&a_empty[slot]);
           }
-          if (++slot == p.ns) { slot = 0; ph ^= 1u; }
+          if (++slot == ns_) { slot = 0; ph ^= 1u; }
         } else {
           // sparse items of this window: the producer tags each slot with the
           // tap's window offset and whether it is the window's last item; the tile's
@@ -374,8 +472,8 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
 #pragma unroll
             for (int q = 0; q < BPI; ++q)
               tapv[q] = (q == 0 ? info0 : ld_shared_u32(slot_info + 4u * (kWMaxBpi * slot + q))) & 0x0FFFFFFFu;
-            const uint32_t et = tmem + p.e_col0 + 4u * static_cast<uint32_t>(p.bpi) * eslot;
-            if (++eslot == p.e_slots) eslot = 0;
+            const uint32_t et = tmem + e_col0_ + 4u * static_cast<uint32_t>(bpi_) * eslot;
+            if (++eslot == e_slots_) eslot = 0;
             const uint64_t ab = ad_sp + slot * slot_a16;
             {
               // metadata of block pairs in one tcgen05.cp.128x256b (blocks 2 KB apart = LBO)
@@ -410,12 +508,12 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
               else mma_commit(&a_empty[slot]);
             }
             first = false;
-            if (++slot == p.ns) { slot = 0; ph ^= 1u; }
+            if (++slot == ns_) { slot = 0; ph ^= 1u; }
             if (info0 >> 31) break;
           }
         }
         mma_commit(&win_empty[buf]);
-        if (++buf == p.nwb) { buf = 0; wph ^= 1u; }
+        if (++buf == nwb_) { buf = 0; wph ^= 1u; }
       }
       mma_commit(&acc_full[b]);
       if (WTRACE(p) && blockIdx.x == 0 && k < 16) p.trace[100 + 4 * k + 1] = gtimer();

@@ -67,6 +67,7 @@ GEOMS = [  # (n, h, w, cin, cout, rank, density)
     (1, 5, 5, 64, 64, 256, 0.02),        # rank 256 (4 T chunks), tiny P < one tile
     (2, 8, 8, 128, 256, 48, 0.30),       # dense S: residual blocks, R = 48 -> 64
     (5, 6, 6, 64, 128, 32, 0.0),         # empty S: LR only (no X chunks)
+    (8, 28, 28, 512, 128, 20, 0.01),     # 8 X chunks + T1 per tile: the ring must hold a whole tile
 ]
 
 

@@ -9,10 +9,13 @@ its 3 input channels are below the library's 16-byte TMA rows) at 1x / 2x / 3x i
     the SVD pair), rank R = floor(P(W) / (c * P per rank)), P per rank = Cin + Cout + 2k
     (CP; PAPER.md:138) or Cin + Cout (SVD), capped at the library's 256;
   * low rank (5x) + 1 % sparse: the whole compressed layer; its increment over the 5x
-    low-rank layer is the sparse term's cost (the paper's "sparse component").
+    low-rank layer is the sparse term's cost (the paper's "sparse component");
+  * sparse only, 1 % ("S"): the paper's sparse-component arm, run as
+    the cheapest layer the ABI allows -- L of rank 1 (padded to 16 inside the library)
+    plus the 1 % S -- so its time is the sparse term plus a rank-16 chain.
 Times are CUDA-event means of 20 back-to-back forwards after warm-up, batch 32 (the
 per-GPU batch of C5 at 8 GPUs), synthetic seeded weights (speed does not depend on
-trained values).  Writes profiles/r01_f2_speed_bound.json and prints the paper-style
+trained values).  Writes profiles/r02_f2_speed_bound.json and prints the paper-style
 tables: network-level speedup = sum of dense times / sum of compressed times.
 
 usage: python tools/f2_speed_bound.py [batch]
@@ -110,11 +113,11 @@ def main():
             per_rank = cin + cout + (0 if (k == 1 and s == 1) else 2 * k)
             row = {"scale": scale, "layer": idx, "cin": cin, "cout": cout, "k": k, "stride": s, "h": h, "w": w,
                    "dense_us": t_dense, "lr": {}}
-            for c in COMPRESSIONS + ("5+S",):
+            for c in COMPRESSIONS + ("5+S", "S"):
                 cc = 5 if c == "5+S" else c
-                rank = int(min(256, max(1, p_w // (cc * per_rank))))
+                rank = 1 if c == "S" else int(min(256, max(1, p_w // (cc * per_rank))))
                 try:
-                    layer = lr_layer(n, h, w, cin, cout, k, s, p, rank, 0.01 if c == "5+S" else 0.0, seed=idx)
+                    layer = lr_layer(n, h, w, cin, cout, k, s, p, rank, 0.01 if c in ("5+S", "S") else 0.0, seed=idx)
                 except LrsError as e:  # e.g. output width > 128 at 3x input
                     row["lr"][str(c)] = {"rank": rank, "unsupported": str(e)}
                     continue
@@ -126,14 +129,15 @@ def main():
             rows.append(row)
             sp = lambda c: f"{row['lr'][str(c)]['speedup']:.2f}" if "us" in row["lr"][str(c)] else "n/a"  # noqa: E731
             print(f"x{scale} L{idx:2d} {cin:4d}->{cout:4d} k{k} s{s} {h}x{w}: dense {t_dense:8.1f} us | "
-                  + " ".join(f"{c}x:{sp(c)}" for c in COMPRESSIONS) + f" | 5x+S {sp('5+S')}", flush=True)
+                  + " ".join(f"{c}x:{sp(c)}" for c in COMPRESSIONS) + f" | 5x+S {sp('5+S')} | S-only {sp('S')}",
+                  flush=True)
             del x, wt
     summary = {}
     for scale in SCALES:
         rs = [r for r in rows if r["scale"] == scale and all("us" in v for v in r["lr"].values())]
         dense = sum(r["dense_us"] for r in rs)
         summary[f"x{scale}"] = {str(c): dense / sum(r["lr"][str(c)]["us"] for r in rs)
-                                for c in COMPRESSIONS + ("5+S",)}
+                                for c in COMPRESSIONS + ("5+S", "S")}
     out = {"batch": n, "device": torch.cuda.get_device_name(0), "rows": rows, "network_speedup": summary,
            "layers_in_totals": {f"x{s_}": sum(1 for r in rows if r["scale"] == s_ and
                                               all("us" in v for v in r["lr"].values())) for s_ in SCALES},
@@ -142,7 +146,7 @@ def main():
                    "52 layers (stem excluded); paper_cpu_x1 = PAPER.md:250-266 (i3-8130U CPU), context only"}
     for d in ("profiles", "gpurun_out"):  # gpurun_out/ travels back from the GPU box
         if os.path.isdir(os.path.join(ROOT, d)):
-            with open(os.path.join(ROOT, d, "r01_f2_speed_bound.json"), "w") as f:
+            with open(os.path.join(ROOT, d, "r02_f2_speed_bound.json"), "w") as f:
                 json.dump(out, f, indent=1)
     print("\nnetwork-level speedup of the low-rank layers vs cuDNN dense (paper CPU x1 for context):")
     print("compression | " + " | ".join(f"x{s} input" for s in SCALES) + " | paper CPU x1")
@@ -150,6 +154,7 @@ def main():
         print(f"{c:>5}x      | " + " | ".join(f"{summary[f'x{s}'][str(c)]:.2f}x" for s in SCALES)
               + f" | {out['paper_cpu_x1'][str(c)]}x")
     print("5x + 1% S   | " + " | ".join(f"{summary[f'x{s}']['5+S']:.2f}x" for s in SCALES) + " |")
+    print("S only (1%) | " + " | ".join(f"{summary[f'x{s}']['S']:.2f}x" for s in SCALES) + " | paper CPU: up to 13x")
 
 
 if __name__ == "__main__":

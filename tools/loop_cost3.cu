@@ -25,6 +25,8 @@ __global__ void k(int iters, unsigned long long* out) {
   tc_fence_after();
   if (threadIdx.x == 32) {
     const int n = smem_param(prm);
+    __shared__ __align__(1024) uint8_t ebuf[4096];
+    const uint64_t edesc = umma_desc_rows16(smem_u32(ebuf));
     mbar_arrive(&bar[0]);  // phase 0 of bar 0 complete
     const long long t0 = clock64();
     for (int i = 0; i < n; ++i) {
@@ -34,6 +36,8 @@ __global__ void k(int iters, unsigned long long* out) {
       if (MODE & 8) mbar_arrive(&bar[2]);
       if (MODE & 16) { while (!mbar_test_wait(&bar[0], 0)) {} }
       if (MODE & 32) { while (!mbar_try_wait(&bar[0], 0)) {} }
+      if (MODE & 64) tmem_cp_128x256b(0u, edesc);
+      if (MODE & 128) tmem_cp_128x128b(0u, edesc);
     }
     const long long t1 = clock64();
     out[0] = t1 - t0;
@@ -67,5 +71,8 @@ int main() {
   run<16>("test_wait (complete phase)", d);
   run<32>("bare try_wait loop", d);
   run<18>("test_wait + fence", d);
+  run<64>("tcgen05.cp 128x256b", d);
+  run<128>("tcgen05.cp 128x128b", d);
+  run<64 + 7>("wait+fence+cp256+commit", d);
   return 0;
 }
