@@ -23,6 +23,7 @@
 #include "lrs_tiny.cuh"
 #include "lrs_wconv.cuh"
 #include "lrs_pw.cuh"
+#include "lrs_pwf.cuh"
 
 using namespace lrs;
 
@@ -136,7 +137,15 @@ const void* wconv_kernel_ptr(int nu, int bpi) {
 #undef LRS_WK
 }
 
-// channel-stationary 1x1 kernel instantiation for mpc M-tiles per CTA
+// channel-stationary 1x1 kernel instantiation for mpc M-tiles per CTA (ft: projection fused)
+const void* pwf_kernel_ptr(int mpc) {
+  switch (mpc) {
+    case 1: return reinterpret_cast<const void*>(&lrs_pwf_kernel<1>);
+    case 2: return reinterpret_cast<const void*>(&lrs_pwf_kernel<2>);
+    case 3: return reinterpret_cast<const void*>(&lrs_pwf_kernel<3>);
+    default: return reinterpret_cast<const void*>(&lrs_pwf_kernel<4>);
+  }
+}
 const void* pw_kernel_ptr(int mpc) {
   switch (mpc) {
     case 1: return reinterpret_cast<const void*>(&lrs_pw_kernel<1>);
@@ -200,6 +209,8 @@ struct lrs_conv {
   bool use_w = false;
   // 1x1 SVD-pair layers: channel-stationary fused a3 + a4 + a5 (lrs_pw.cuh)
   bool use_pw = false;
+  bool pw_ft = false;         // ... with the projection a1 fused in (lrs_pwf.cuh): one launch, T1 on chip
+  void* pw_u = nullptr;       // U_in^T image of the fused projection
   PwParams pp{};
   uint32_t pw_smem = 0;
   int pw_grid_per_group = 0;  // CTAs per channel group at most
@@ -949,17 +960,18 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   struct Unit { int col, n, xpos, tpos, r0, wo0, pitch, nw, rows, q0; };
   // MMA units covering a tile of th output rows x tc output columns (see lrs_wconv.cuh);
   // wcw = window width, tbw = T window row pitch
-  auto make_units = [&](int th, int tc, int wcw, int tbw, std::vector<Unit>& us) -> int {
+  auto make_units = [&](int th, int tc, int wcw, int tbw, int ipw, std::vector<Unit>& us) -> int {
     us.clear();
     int col = 0;
     if (s1) {
       // stride 1: the tile's outputs are positions q = r * wcw + c of the window
       // (c >= tc are the window's padding columns, computed and discarded); a unit
-      // is a run of <= 32 consecutive positions, whatever rows it spans
+      // is a run of <= 256 / ipw consecutive positions (N <= 256), whatever rows it spans
       const int npos = (th - 1) * wcw + tc;
-      for (int q0 = 0; q0 < npos; q0 += 32) {
-        const int np = std::min(32, npos - q0);
-        Unit u{col, round_up(8 * np, 16), q0, q0, 0, 0, wcw, tc, th, q0};
+      const int per = 256 / ipw;
+      for (int q0 = 0; q0 < npos; q0 += per) {
+        const int np = std::min(per, npos - q0);
+        Unit u{col, round_up(ipw * np, 16), q0, q0, 0, 0, wcw, tc, th, q0};
         us.push_back(u);
         col += u.n;
       }
@@ -977,7 +989,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     return col;
   };
   std::vector<Unit> units, best_units;
-  int best_th = 0, best_ns = 0, best_tc = 0, best_wc = 0, best_tbw = 0, best_nwb = 2, best_bpi = 2;
+  int best_th = 0, best_ns = 0, best_tc = 0, best_wc = 0, best_tbw = 0, best_nwb = 2, best_bpi = 2, best_ipw = 8;
   long long best_cost = 1LL << 60;
   uint32_t best_stride = 0, best_xw = 0, best_tw = 0, best_total = 0, best_acc = 0;
   // chunks per X window: several 64-channel boxes in one window buffer share one
@@ -987,10 +999,20 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   const int cpw_env = getenv("LRS_WCONV_CPW") ? atoi(getenv("LRS_WCONV_CPW")) : 0;
   // ("largest that fits" shrank the tiles and lost badly at C2/C3, so only 1x1 layers --
   // no halo, small windows -- take cpw > 1; C4: 49.0 -> 47.0 us)
-  for (int cpw = 8; cpw >= 1 && !best_th; cpw /= 2) {
+  // images per window: 8 (one 8-row core matrix = the 8 images of one position), or 4 at
+  // stride 1 (a core matrix = 2 positions x 4 images; a tap then moves the operand start by
+  // 512 B, which SW128 allows): half-size windows leave room for a deeper A/E item ring --
+  // the small-image layers (C3: 9 x 9 windows of 82 KB) are otherwise held to two items in flight
+  // (measured: no config is faster at ipw 4 -- C3 77.5 -> 85.6 us with a 4-deep ring, C2 22 -> 25 us,
+  // profiles/r02_ablate_ipw.log -- so 4 is a plan option for LRS_WCONV_IPW=4 only)
+  const int ipw_env = getenv("LRS_WCONV_IPW") ? atoi(getenv("LRS_WCONV_IPW")) : 8;  // plan override (tests)
+  for (int ipw : {8, 4}) {
+  if (ipw != ipw_env || (ipw == 4 && !s1)) continue;
+  bool found_ipw = false;
+  for (int cpw = 8; cpw >= 1 && !found_ipw; cpw /= 2) {
   if (n_ck % cpw || (cpw_env ? cpw != cpw_env : (taps > 1 && cpw != 1))) continue;
   const int cb_env = getenv("LRS_WCONV_CB") ? atoi(getenv("LRS_WCONV_CB")) : 0;  // planner experiments
-  for (int cb = cb_env ? cb_env : 1; cb <= 16 && !best_th; ++cb) {  // column bands: as few as fit
+  for (int cb = cb_env ? cb_env : 1; cb <= 16 && !found_ipw; ++cb) {  // column bands: as few as fit
     const int tc = (wo + cb - 1) / cb;
     if (cb > 1 && (wo + tc - 1) / tc != cb) continue;
     const int wcw = (tc - 1) * g.sw + kw;
@@ -999,7 +1021,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     const int th_env = getenv("LRS_WCONV_TH") ? atoi(getenv("LRS_WCONV_TH")) : 0;  // planner experiments
     for (int th = std::min(ho, 64); th >= 1; --th) {
       if (th_env && th != th_env) continue;
-      const int acc = make_units(th, tc, wcw, tbw, units);
+      const int acc = make_units(th, tc, wcw, tbw, ipw, units);
       if (static_cast<int>(units.size()) > kWMaxUnits) continue;
       const int wr = (th - 1) * g.sh + kh;
       if (wr > 256) continue;
@@ -1024,18 +1046,19 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         const uint32_t e_slot = static_cast<uint32_t>(bpi) * kEBlockBytes;
         const int es_need = ering ? 1 : ns;  // TMEM metadata slots the plan needs at least
         if (acc + 4 * bpi * es_need > 512) continue;
-        const uint32_t xw = static_cast<uint32_t>(wr) * wcw * 1024u;  // one chunk's box
-        const uint32_t tw = static_cast<uint32_t>(th) * tbw * 8u * sw_t;
+        const uint32_t pos_b = 128u * ipw;  // bytes per window position
+        const uint32_t xw = static_cast<uint32_t>(wr) * wcw * pos_b;  // one chunk's box
+        const uint32_t tw = static_cast<uint32_t>(th) * tbw * ipw * sw_t;
         // slack: positions read past the end of a window by the last (padded) MMA rows
         long long last_x = 0, last_t = 0;
         for (const Unit& u : units) {
           last_x = std::max<long long>(last_x, u.xpos + static_cast<long long>(kh - 1) * wcw + (kw - 1) +
-                                                   static_cast<long long>(u.n / 8 - 1) * g.sw);
-          last_t = std::max<long long>(last_t, u.tpos + u.n / 8 - 1);
+                                                   static_cast<long long>(u.n / ipw - 1) * g.sw);
+          last_t = std::max<long long>(last_t, u.tpos + u.n / ipw - 1);
         }
-        const long long slack_x = std::max(0LL, last_x + 1 - static_cast<long long>(wr) * wcw) * 1024 +
+        const long long slack_x = std::max(0LL, last_x + 1 - static_cast<long long>(wr) * wcw) * pos_b +
                                   static_cast<long long>(cpw - 1) * xw;  // the window's other boxes
-        const long long slack_t = std::max(0LL, last_t + 1 - static_cast<long long>(th) * tbw) * 8 * sw_t;
+        const long long slack_t = std::max(0LL, last_t + 1 - static_cast<long long>(th) * tbw) * ipw * sw_t;
         const uint32_t stride =
             align1024(static_cast<uint32_t>(std::max<long long>(xw + slack_x, tw + slack_t)));
         // the M-tile's block stream: chunk starts + a tap offset per (main or residual) block
@@ -1058,7 +1081,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         // waves of one per SM.
         long long item = 450 / bpi;  // per-block share of the item's hand-off + commit
         for (const Unit& u : units) item += 2 * std::max<long long>(100, (4096 + 64LL * u.n) / 128);
-        const long long ctas = static_cast<long long>((d->batch_max + 7) / 8) * ((ho + th - 1) / th) * cb * n_mt;
+        const long long ctas = static_cast<long long>((d->batch_max + ipw - 1) / ipw) * ((ho + th - 1) / th) * cb * n_mt;
         const long long waves = (ctas + h->sms - 1) / h->sms;
         // waves x per-tile cost: the tile's blocks x per-block cost, plus the epilogue
         // (~30 cycles per accumulator column, measured with tools/wtrace) unless two
@@ -1082,8 +1105,10 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
           best_acc = static_cast<uint32_t>(acc);
           best_units = units;
           best_cpw = cpw;
+          best_ipw = ipw;
         }
         found = true;
+        found_ipw = true;
         break;
       }
       if (found) break;
@@ -1091,8 +1116,10 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     }
   }
   }  // cpw
+  }  // ipw
   if (!best_th) return LRS_OK;
   const int cpw = best_cpw;
+  const int ipw = best_ipw;
   const int th = best_th;
   const int wc = best_wc, tbox_w = best_tbw, tcols = best_tc;
 
@@ -1117,7 +1144,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       stream_off[static_cast<size_t>(mt) * n_ck + c] = static_cast<int>(order.size());
       for (int t = 0; t < taps; ++t) {
         const int key = (mt * n_ck + c) * taps + t;
-        const uint32_t tap16 = static_cast<uint32_t>((t / kw) * wc + (t % kw)) * 64u +  // (pos * 1024) >> 4
+        const uint32_t tap16 = static_cast<uint32_t>((t / kw) * wc + (t % kw)) * (8u * ipw) +  // (pos*128*ipw)>>4
                                static_cast<uint32_t>(c % cpw) * (best_xw >> 4);          // the chunk's box
         order.push_back(key);
         blk_tap.push_back(tap16);
@@ -1181,7 +1208,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     uint64_t dims[4] = {static_cast<uint64_t>(rp), bm, static_cast<uint64_t>(wo), static_cast<uint64_t>(ho)};
     uint64_t strides[3] = {static_cast<uint64_t>(ho) * wo * rp * 2, static_cast<uint64_t>(rp) * 2,
                            static_cast<uint64_t>(wo) * rp * 2};
-    uint32_t box[4] = {static_cast<uint32_t>(t_kc), 8, static_cast<uint32_t>(tbox_w), static_cast<uint32_t>(th)};
+    uint32_t box[4] = {static_cast<uint32_t>(t_kc), static_cast<uint32_t>(ipw), static_cast<uint32_t>(tbox_w),
+                       static_cast<uint32_t>(th)};
     uint32_t estr[4] = {1, 1, 1, 1};
     if ((st = encode_t(&w.tmT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, src, dims, strides, box, estr, sw_t)) != LRS_OK)
       return st;
@@ -1197,6 +1225,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   w.sw = g.sw;
   w.ph = g.ph;
   w.pw = g.pw;
+  w.ipw = ipw;
   w.th = th;
   w.bands = (ho + th - 1) / th;
   w.tcols = tcols;
@@ -1248,8 +1277,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   h->w_smem = best_total;
   h->use_w = true;
   if (getenv("LRS_VERBOSE"))
-    fprintf(stderr, "lrs_wconv plan: th %d tcols %d units %d acc %u nacc %d ns %d bpi %d nwb %d cpw %d win %u B smem %u B tiles/img-group %d\n",
-            th, tcols, w.n_units, acc, w.nacc, w.ns, w.bpi, w.nwb, cpw, best_stride, best_total, w.bands * w.cbands * w.n_mt);
+    fprintf(stderr, "lrs_wconv plan: ipw %d th %d tcols %d units %d acc %u nacc %d ns %d bpi %d nwb %d cpw %d win %u B smem %u B tiles/img-group %d\n",
+            ipw, th, tcols, w.n_units, acc, w.nacc, w.ns, w.bpi, w.nwb, cpw, best_stride, best_total, w.bands * w.cbands * w.n_mt);
   return LRS_OK;
 }
 
@@ -1272,8 +1301,14 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
   const long long p_max = static_cast<long long>(d->batch_max) * d->in_h * d->in_w;
   const int mpc_env = getenv("LRS_PW_MPC") ? atoi(getenv("LRS_PW_MPC")) : 0;  // plan overrides (tests)
   const int bp_env = getenv("LRS_PW_BP") ? atoi(getenv("LRS_PW_BP")) : 0;
-  struct Plan { int mpc = 0, bp = 0, ns = 0, nblk = 0, gpg = 0; uint32_t smem = 0, w_bytes = 0; double cost = 1e300; };
+  // ft: the projection fused in (lrs_pwf.cuh) -- needs 128-position tiles (the M of the T1
+  // MMAs), R1p a multiple of 32 (the restage splits the ranks over two warps in steps of 16)
+  // and the X chunks even without a sparse term; it saves the a1 launch and T1's HBM round
+  // trip, so it is preferred whenever it fits (LRS_PW_FT=0 keeps the two-kernel form)
+  const bool ft_ok = r1p % 32 == 0 && r1p <= 256 && !(getenv("LRS_PW_FT") && atoi(getenv("LRS_PW_FT")) == 0);
+  struct Plan { int mpc = 0, bp = 0, ns = 0, nblk = 0, gpg = 0, ft = 0; uint32_t smem = 0, w_bytes = 0; double cost = 1e300; };
   Plan best;
+  for (int ft = ft_ok ? 1 : 0; ft >= 0 && !best.mpc; --ft) {
   for (int mpc = std::min(kPMaxMpc, n_mt); mpc >= 1; --mpc) {
     if (mpc_env && mpc != mpc_env) continue;
     const int G = (n_mt + mpc - 1) / mpc;
@@ -1291,25 +1326,29 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
         nblk = std::max(nblk, nb);
       }
     for (int bp : {128, 96, 64}) {  // multiples of 32: the epilogue stores 32-position TMA boxes
-      if (bp_env && bp != bp_env) continue;
+      if ((bp_env && bp != bp_env) || (ft && bp != 128)) continue;
       const uint32_t acc = static_cast<uint32_t>(mpc * bp);
-      // TMEM: two accumulator sets, the metadata, and the epilogue's 32-column reads past a
-      // set's last column (bp % 32 == 16) must stay inside the 512 columns
-      const uint32_t tail = (bp % 32) ? 16u : 0u;
-      if (2 * acc + std::max<uint32_t>(4u * nblk, tail) > 512) continue;
+      // TMEM: two accumulator sets (+ two T1 accumulators when fused) and the metadata
+      const uint32_t t1cols = ft ? 2u * static_cast<uint32_t>(r1p) : 0u;
+      if (2 * acc + t1cols + 4u * nblk > 512) continue;
       const uint32_t dense = static_cast<uint32_t>(mpc * n_tk) * 128u * sw_t;
       const uint32_t w_bytes = dense + static_cast<uint32_t>(nblk) * 8192u;
       const uint32_t e_bytes = static_cast<uint32_t>(nblk) * 2048u;
       const uint32_t slot = static_cast<uint32_t>(bp) * 128u;
-      const uint32_t fixed = align1024(w_bytes) + align1024(e_bytes) + 8 * kPEpiScratch + 1024 /*tab*/ +
-                             1024 /*bars*/ + 1024 /*align*/;
+      const uint32_t u_bytes = ft ? static_cast<uint32_t>(n_ck * r1p) * 128u : 0u;
+      const uint32_t t1s = ft ? 2u * 128u * static_cast<uint32_t>(r1p) * 2u : 0u;
+      // (fused: the metadata staging shares the second T1 tile, first written after the copy)
+      const uint32_t e_stage = (ft && e_bytes <= t1s / 2) ? 0u : align1024(e_bytes);
+      const uint32_t fixed = align1024(w_bytes) + align1024(u_bytes) + align1024(t1s) + e_stage + 8 * kPEpiScratch +
+                             1024 /*tab*/ + 1024 /*bars*/ + 1024 /*align*/;
       if (fixed >= static_cast<uint32_t>(kMaxSmem)) continue;
       const int ns = std::min<int>(kPMaxSlots, static_cast<int>((kMaxSmem - fixed) / slot));
       // slots are released chunk by chunk (tcgen05.commit after each chunk's MMAs), but the
       // producer lanes request a tile's chunks in parallel, so the ring must hold a whole
       // tile: with fewer slots two lanes would wait on two phases of one slot's mbarrier at
       // once, and a parity wait cannot tell phase r from phase r + 2
-      if (ns < n_x + n_tk) continue;
+      const int nq = ft ? n_ck : n_x + n_tk;
+      if (ns < nq) continue;
       // cost (cycles per CTA): tiles x max(MMA, operand inflow, the group's share of the HBM
       // write of Y); sparse MMA ~ (A 4 KB + B bp*64 B) / 128 B/clk, dense ~ (4 KB + bp*32 B) / 128
       const int gpg = h->sms / G;
@@ -1319,15 +1358,16 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
       const double mma = static_cast<double>(nblk) * 2 * sp + mpc * n_tk * (sw_t / 32.0) * dn;
       const double in = (static_cast<double>(n_x) * bp * 128 + n_tk * bp * sw_t) / 60.0;
       const double out = static_cast<double>(bp) * mpc * 128 * 2 * (G * gpg) / 3300.0;  // ~3.3 KB/clk of HBM writes
-      const double shallow = ns < n_x + n_tk + 2 ? 1.25 : 1.0;
+      const double shallow = ns < nq + 2 ? 1.25 : 1.0;
       const double cost = static_cast<double>(tiles) * std::max(mma, std::max(in, out)) * shallow + 400.0 * mpc;
       if (cost < best.cost) {
         best.cost = cost; best.mpc = mpc; best.bp = bp; best.ns = ns; best.nblk = nblk; best.gpg = gpg;
-        best.w_bytes = w_bytes;
+        best.w_bytes = w_bytes; best.ft = ft;
         best.smem = fixed + static_cast<uint32_t>(ns) * slot;
       }
     }
   }
+  }  // ft
   if (!best.mpc) return LRS_OK;
   const int mpc = best.mpc, G = (n_mt + mpc - 1) / mpc, nblk = best.nblk;
   // ---- per-group images: [mpc][n_tk] V^T blocks, then the 2:4 blocks; metadata; tables
@@ -1382,6 +1422,16 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
     memcpy(tb.data(), tab.data(), tb.size());
     if ((st = upload(&h->pw_tab, tb)) != LRS_OK) return st;
   }
+  if (best.ft) {  // U_in^T blocks [n_ck][R1p rows x 128 B] (64 channels per row), SW128
+    std::vector<uint8_t> ui(static_cast<size_t>(n_ck) * r1p * 128, 0);
+    for (int c = 0; c < n_ck; ++c)
+      for (int r = 0; r < r1; ++r)
+        for (int k = 0; k < 64; ++k) {
+          const uint16_t bits = static_cast<const uint16_t*>(d->u_in)[static_cast<size_t>(c * 64 + k) * r1 + r];
+          memcpy(&ui[static_cast<size_t>(c) * r1p * 128 + swz_off(r, 2 * k, 128)], &bits, 2);
+        }
+    if ((st = upload(&h->pw_u, ui)) != LRS_OK) return st;
+  }
   PwParams& q = h->pp;
   memset(&q, 0, sizeof(q));
   q.img_w = static_cast<const uint8_t*>(h->pw_w);
@@ -1402,9 +1452,24 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
   q.ns = best.ns;
   q.slot_bytes = static_cast<uint32_t>(best.bp) * 128u;
   q.acc_cols = static_cast<uint32_t>(mpc * best.bp);
-  q.e_col0 = 2 * q.acc_cols;
-  q.off_e = align1024(best.w_bytes);
-  q.off_ring = q.off_e + align1024(static_cast<uint32_t>(nblk) * 2048u);
+  if (best.ft) {
+    q.r1p = r1p;
+    q.u_bytes = static_cast<uint32_t>(n_ck * r1p) * 128u;
+    q.img_u = static_cast<const uint8_t*>(h->pw_u);
+    q.t1s_bytes = 128u * static_cast<uint32_t>(r1p) * 2u;
+    q.t1_col0 = 2 * q.acc_cols;
+    q.e_col0 = q.t1_col0 + 2u * static_cast<uint32_t>(r1p);
+    q.off_u = align1024(best.w_bytes);
+    q.off_t1s = q.off_u + align1024(q.u_bytes);
+    const uint32_t e_bytes = static_cast<uint32_t>(nblk) * 2048u;
+    const bool e_shared = e_bytes <= q.t1s_bytes;
+    q.off_e = e_shared ? q.off_t1s + q.t1s_bytes : q.off_t1s + align1024(2 * q.t1s_bytes);
+    q.off_ring = q.off_t1s + align1024(2 * q.t1s_bytes) + (e_shared ? 0u : align1024(e_bytes));
+  } else {
+    q.e_col0 = 2 * q.acc_cols;
+    q.off_e = align1024(best.w_bytes);
+    q.off_ring = q.off_e + align1024(static_cast<uint32_t>(nblk) * 2048u);
+  }
   q.off_epi = q.off_ring + static_cast<uint32_t>(best.ns) * q.slot_bytes;
   q.off_tab = q.off_epi + 8 * kPEpiScratch;
   q.off_bar = q.off_tab + 1024;
@@ -1417,9 +1482,10 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
   h->w_main_blocks = n_x ? n_mt * n_ck : 0;
   h->w_res_blocks = S.nres;
   h->use_pw = true;
+  h->pw_ft = best.ft != 0;
   if (getenv("LRS_VERBOSE"))
-    fprintf(stderr, "[lrs] pw plan: mpc %d groups %d bp %d ns %d blocks/group %d ctas/group %d smem %u B\n", mpc, G,
-            best.bp, best.ns, nblk, best.gpg, best.smem);
+    fprintf(stderr, "[lrs] pw plan: fused a1 %d mpc %d groups %d bp %d ns %d blocks/group %d ctas/group %d smem %u B\n",
+            best.ft, mpc, G, best.bp, best.ns, nblk, best.gpg, best.smem);
   return LRS_OK;
 }
 }  // namespace
@@ -1444,7 +1510,7 @@ static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d) {
   std::vector<int> grids{h->sms};
   if (h->use_w) {
     const WconvParams& w = h->wp;
-    const long long wt = static_cast<long long>((n + 7) / 8) * w.bands * w.cbands * w.n_mt;
+    const long long wt = static_cast<long long>((n + w.ipw - 1) / w.ipw) * w.bands * w.cbands * w.n_mt;
     const int free_sms = h->sms - static_cast<int>(std::min<long long>(wt, h->sms));
     if (free_sms >= 16) grids.push_back(free_sms);
   }
@@ -1877,7 +1943,8 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
   for (const void* fn : {reinterpret_cast<const void*>(&lrs_spadd_kernel), pw_kernel_ptr(1), pw_kernel_ptr(2),
-                         pw_kernel_ptr(3), pw_kernel_ptr(4)}) {
+                         pw_kernel_ptr(3), pw_kernel_ptr(4), pwf_kernel_ptr(1), pwf_kernel_ptr(2), pwf_kernel_ptr(3),
+                         pwf_kernel_ptr(4)}) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
@@ -1977,7 +2044,7 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
   h->a1.p.tmA = h->xmap;
   h->a1.p.m_total = static_cast<int>(pin);
   h->a1.p.g.n = n;
-  if (!h->use_core && !(h->skip & 1) &&
+  if (!h->use_core && !h->pw_ft && !(h->skip & 1) &&
       (st = launch(h, 0, h->a1, dim3(static_cast<unsigned>((pin + kTileM - 1) / kTileM)), stream)) != LRS_OK)
     return st;
   if (h->use_pw) {
@@ -1992,7 +2059,7 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
                            128)) != LRS_OK)
           return st;
       }
-      {
+      if (!h->pw_ft) {
         uint64_t dims[2] = {static_cast<uint64_t>(h->r1p), static_cast<uint64_t>(pin)};
         uint64_t strides[1] = {static_cast<uint64_t>(h->r1p) * 2};
         uint32_t box[2] = {static_cast<uint32_t>(q.t_kc), static_cast<uint32_t>(q.bp)};
@@ -2020,8 +2087,8 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
     const int per_group = std::max(1, std::min(h->pw_grid_per_group, q.n_pt));
     cudaEvent_t e1 = nullptr;
     if ((st = time_begin(h, 2, stream, &e1)) != LRS_OK) return st;
-    LRS_CUDA(launch_pdl(pw_kernel_ptr(q.mpc), dim3(static_cast<unsigned>(per_group * q.n_groups)), dim3(kPThreads), &q,
-                        h->pw_smem, stream));
+    LRS_CUDA(launch_pdl(h->pw_ft ? pwf_kernel_ptr(q.mpc) : pw_kernel_ptr(q.mpc),
+                        dim3(static_cast<unsigned>(per_group * q.n_groups)), dim3(kPThreads), &q, h->pw_smem, stream));
     if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
     return LRS_OK;
   }
@@ -2054,7 +2121,7 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
 #if defined(LRS_EXPERIMENTS) || defined(LRS_WCONV_DEBUG)
       if (w.dbg & 32) strides[0] = 128;  // timing experiment: contiguous 1 KB per position (wrong data)
 #endif
-      uint32_t box[4] = {64, 8, static_cast<uint32_t>(w.wc), static_cast<uint32_t>(w.wr)};
+      uint32_t box[4] = {64, static_cast<uint32_t>(w.ipw), static_cast<uint32_t>(w.wc), static_cast<uint32_t>(w.wr)};
       uint32_t estr[4] = {1, 1, 1, 1};
       if ((st = encode_t(&w.tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box,
                          estr, 128)) != LRS_OK)
@@ -2064,7 +2131,7 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
     }
     w.n = n;
     w.y = y;
-    w.n_tiles = ((n + 7) / 8) * w.bands * w.cbands * w.n_mt;
+    w.n_tiles = ((n + w.ipw - 1) / w.ipw) * w.bands * w.cbands * w.n_mt;
     const unsigned grid = static_cast<unsigned>(std::min(w.n_tiles, h->sms));
     cudaEvent_t e1 = nullptr;
     if ((st = time_begin(h, 2, stream, &e1)) != LRS_OK) return st;
@@ -2184,7 +2251,7 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
                   h->w_as, h->w_e, h->w_res, h->w_dense_img, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc,
-                  h->sp_uo, h->epi, h->pw_w, h->pw_e, h->pw_tab};
+                  h->sp_uo, h->epi, h->pw_w, h->pw_e, h->pw_tab, h->pw_u};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (void* b : h->tiny_buf)
@@ -2211,7 +2278,7 @@ lrs_status lrs_conv_output_shape(const lrs_conv* h, int32_t* out_h, int32_t* out
 }
 
 int32_t lrs_conv_launches_per_forward(const lrs_conv* h) {
-  if (h && h->use_tiny) return 1;
+  if (h && (h->use_tiny || h->pw_ft)) return 1;
   return h ? (h->svd ? 2 : 3) - (h->use_core ? 1 : 0) : 0;
 }
 

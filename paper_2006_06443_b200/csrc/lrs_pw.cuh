@@ -63,6 +63,14 @@ struct PwParams {
   uint32_t off_e, off_ring, off_epi, off_tab, off_bar;
   unsigned long long* trace;  // debug builds: %globaltimer stamps of CTA 0 (lrs_conv_debug_trace)
   int dbg;                    // experiment builds (LRS_PW_DBG): 1 skip Y stores, 2 skip MMAs, 4 skip X/T loads
+  // projection fused in (lrs_pwf_kernel): T1 = X U computed per position tile from the X
+  // chunks already in the ring, restaged as bf16 into shared memory, never written to HBM
+  const uint8_t* img_u;    // U_in^T blocks [n_ck][R1p rows x 128 B], SW128 (B of the T1 MMAs)
+  uint32_t u_bytes;        // n_ck * R1p * 128
+  int r1p;
+  uint32_t off_u, off_t1s; // resident U^T; two T1 tiles [n_tk][128 rows][sw_t], swizzle sw_t
+  uint32_t t1s_bytes;      // one T1 tile (128 * R1p * 2)
+  uint32_t t1_col0;        // TMEM columns of the two T1 accumulators (R1p each)
 };
 
 #ifdef LRS_WCONV_DEBUG

@@ -66,8 +66,8 @@ constexpr uint32_t kEBlockBytes = 2048;   // its metadata: 128 lanes x 16 B
 constexpr uint32_t kEpiScratch = 2048;   // per epilogue warp: 32 columns x 32 channels bf16
 
 struct WconvParams {
-  CUtensorMap tmX;   // X   4-D (C, N, W, H) bf16, box {64, 8, wc, wr}, SW128
-  CUtensorMap tmT;   // T   4-D (R, N, Wo, Ho) bf16, box {t_kc, 8, tbox_w, th}, swizzle sw_t
+  CUtensorMap tmX;   // X   4-D (C, N, W, H) bf16, box {64, ipw, wc, wr}, SW128
+  CUtensorMap tmT;   // T   4-D (R, N, Wo, Ho) bf16, box {t_kc, ipw, tbox_w, th}, swizzle sw_t
   // A operands as ready-made shared-memory images (host-swizzled), fetched with one
   // 1-D bulk copy each: a 2-D TMA box of 128 short rows costs 128 TMA requests and
   // the TMA request rate measured as the producer's bottleneck (tools/wtrace.py)
@@ -82,6 +82,7 @@ struct WconvParams {
   void* y;
   int n, ho, wo, cout;
   int kh, kw, sh, sw, ph, pw;
+  int ipw;                 // images per window (8, or 4 at stride 1): window rows = (position, image)
   int th, bands, n_mt;
   int tcols, cbands;       // output columns per tile, column bands
   int n_tiles;             // groups * bands * cbands * n_mt (for this forward's n)
@@ -129,14 +130,15 @@ __device__ __forceinline__ TileCoord tile_coord(const WconvParams& p, int tile) 
   tile /= p.cbands;
   const int band = tile % p.bands;
   const int grp = tile / p.bands;
-  c.n0 = grp * 8;
+  c.n0 = grp * p.ipw;
   c.ho0 = band * p.th;
   c.wo0 = cband * p.tcols;
   c.j0 = c.mt * 128;
   return c;
 }
 
-__device__ __forceinline__ TileCoord tile_coord_v(int tile, int n_mt, int cbands, int bands, int th, int tcols) {
+__device__ __forceinline__ TileCoord tile_coord_v(int tile, int n_mt, int cbands, int bands, int th, int tcols,
+                                                  int ipw) {
   TileCoord c;
   c.mt = tile % n_mt;
   tile /= n_mt;
@@ -144,7 +146,7 @@ __device__ __forceinline__ TileCoord tile_coord_v(int tile, int n_mt, int cbands
   tile /= cbands;
   const int band = tile % bands;
   const int grp = tile / bands;
-  c.n0 = grp * 8;
+  c.n0 = grp * ipw;
   c.ho0 = band * th;
   c.wo0 = cband * tcols;
   c.j0 = c.mt * 128;
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     prm[28] = static_cast<int>(p.off_a);
     prm[29] = static_cast<int>(p.off_e);
     prm[30] = static_cast<int>(p.off_res);
+    prm[31] = p.ipw;
     for (int i = 0; i < p.nwb; ++i) {
       mbar_init(&win_full[i], 1);
       mbar_init(&win_empty[i], 1);
@@ -242,6 +245,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   // the producer waits just before the first T window, overlapping the previous kernel.
 
   if (warp == 0) {
+    const int ipw_ = smem_param(prm + 31);
     const int nwb_ = static_cast<int>(smem_param(prm + 0));
     const int n_tiles_ = static_cast<int>(smem_param(prm + 1));
     const int n_mt_ = static_cast<int>(smem_param(prm + 2));
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       const int t_step = contig ? 1 : static_cast<int>(gridDim.x);
       int prev_win = -1;
       for (int tile = t_begin; tile < t_end; tile += t_step) {
-        const TileCoord tc = tile_coord_v(tile, n_mt_, cbands_, bands_, th_, tcols_);
+        const TileCoord tc = tile_coord_v(tile, n_mt_, cbands_, bands_, th_, tcols_, ipw_);
         const int win_key = tile / n_mt_;
         const bool reuse = nwb_ == nwin && win_key == prev_win;
         prev_win = win_key;
@@ -369,6 +373,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       }
     }
   } else if (warp == 1) {
+    const int ipw_ = smem_param(prm + 31);
     const int nwb_ = static_cast<int>(smem_param(prm + 0));
     const int n_tiles_ = static_cast<int>(smem_param(prm + 1));
     const int n_xw_ = static_cast<int>(smem_param(prm + 4));
@@ -398,8 +403,12 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     // so every per-unit descriptor is precomputed once and the inner loop
     // only adds byte offsets >> 4: the single-thread issue loop stays short.
     const uint32_t win0 = smem_u32(smem);
-    const uint32_t t_pos = 8u * sw_t_;  // bytes per output position in a T window
-    const uint32_t x_sbo = 1024u * static_cast<uint32_t>(sw_);
+    const uint32_t t_pos = static_cast<uint32_t>(ipw_) * sw_t_;  // bytes per position in a T window
+    const uint32_t x_pos = 128u * static_cast<uint32_t>(ipw_);     // bytes per position in an X window
+    // stride between 8-row core-matrix groups: one position (x stride) of 8 images, or two
+    // consecutive positions of 4 images (stride 1 only)
+    const uint32_t x_sbo = ipw_ == 8 ? 1024u * static_cast<uint32_t>(sw_) : 1024u;
+    const uint32_t t_sbo = 8u * sw_t_;
     uint32_t dcol[NU], idu[NU];
     uint64_t bxd[NU], btd[NU];
 #pragma unroll
@@ -407,8 +416,8 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       {
         dcol[u] = tmem + static_cast<uint32_t>(p.u_col[u]);
         idu[u] = umma_idesc(1u, static_cast<uint32_t>(p.u_n[u]), 128u);
-        bxd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_xpos[u]) * 1024u, 128, x_sbo);
-        btd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_tpos[u]) * t_pos, sw_t_, t_pos);
+        bxd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_xpos[u]) * x_pos, 128, x_sbo);
+        btd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_tpos[u]) * t_pos, sw_t_, t_sbo);
       }
     }
     const uint64_t ad_dense = umma_desc(smem_u32(smem + off_a_), sw_t_);
@@ -427,7 +436,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                              : n_tiles_;
     const int t_step = contig ? 1 : static_cast<int>(gridDim.x);
     for (int tile = t_begin; tile < t_end; tile += t_step, ++k) {
-      const TileCoord tc = tile_coord_v(tile, n_mt_, cbands_, bands_, th_, tcols_);
+      const TileCoord tc = tile_coord_v(tile, n_mt_, cbands_, bands_, th_, tcols_, ipw_);
       const int b = nacc_ == 2 ? (k & 1) : 0;
       const int use = nacc_ == 2 ? (k >> 1) : k;  // previous uses of accumulator b
       if (use > 0) {
@@ -552,11 +561,15 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       if (WTRACE(p) && blockIdx.x == 0 && threadIdx.x == 64 && k < 16) p.trace[100 + 4 * k + 2] = gtimer();
       const uint32_t acc0 = static_cast<uint32_t>(b) * p.acc_cols;
       const int jw = tc.j0 + q4 * 32;  // first channel of this warp
-      // store side of the transpose: lane = (image lane/4, 8-channel part lane%4)
+      // store side of the transpose: lane = (column lane/4 of every 8, 8-channel part lane%4);
+      // a column is (position, image) with ipw images per position, so the lane's image is
+      // fixed and, at ipw 4, lanes 16..31 take the second position of each 8 columns
       const int part = lane & 3, img8 = lane >> 2;
+      const int ipw = p.ipw;
+      const int img = img8 & (ipw - 1), psub = ipw == 8 ? 0 : (img8 >> 2), ppass = 8 / ipw;
       const int jch = jw + part * 8;
-      const bool lane_ok = tc.n0 + img8 < p.n && jch < p.cout;
-      __nv_bfloat16* ybase = y + (static_cast<long long>(lane_ok ? tc.n0 + img8 : 0) * p.ho * p.wo) * p.cout + jch;
+      const bool lane_ok = tc.n0 + img < p.n && jch < p.cout;
+      __nv_bfloat16* ybase = y + (static_cast<long long>(lane_ok ? tc.n0 + img : 0) * p.ho * p.wo) * p.cout + jch;
       for (int u = 0; u < p.n_units; ++u) {
         const int pitch = p.u_pitch[u], nw = p.u_nw[u], un = p.u_n[u], rows = p.u_rows[u];
         const int r0 = p.u_r0[u], w0 = p.u_wo0[u], ucol = p.u_col[u], q0 = p.u_q0[u];
@@ -614,10 +627,10 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             }
           }
           __syncwarp();
-          // lane l, pass q: column col = q*8 + l/4 = output position q0 + c0/8 + q (warp-uniform,
-          // stepped without divisions) of image l/4, channels 8*(l%4) .. +7
+          // lane l, pass q: column col = q*8 + l/4 = output position q0 + (c0 + col) / ipw
+          // (stepped without per-store divisions) of image `img`, channels 8*(l%4) .. +7
           {
-            const int qv0 = q0 + (c0 >> 3);
+            const int qv0 = q0 + c0 / ipw + psub;
             int rr = qv0 / pitch, cc = qv0 - rr * pitch;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -626,8 +639,9 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
               const int ho = tc.ho0 + r0 + rr, wo = tc.wo0 + w0 + cc;
               if (lane_ok && c0 + col < un && cc < nw && rr < rows && ho < p.ho && wo < p.wo)
                 *reinterpret_cast<uint4*>(ybase + (static_cast<long long>(ho) * p.wo + wo) * p.cout) = val;
-              if (++cc == pitch) {
-                cc = 0;
+              cc += ppass;
+              while (cc >= pitch) {
+                cc -= pitch;
                 ++rr;
               }
             }

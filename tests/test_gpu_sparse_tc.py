@@ -128,3 +128,35 @@ def test_single_nonzero_bitwise_tensor_core():
     ref = np.zeros((n, h, w, cout), np.float32)
     ref[..., j] = workloads.bf16_round(v * xp[:, ty:ty + h, tx:tx + w, c])
     assert np.array_equal(y.astype(np.float32), ref)
+
+
+IPW_CASES = [  # (n, h, w, cin, cout, k, p, r1, r2, density) -- stride 1 (4-image windows need it)
+    (13, 7, 7, 512, 512, 3, 1, 128, 128, 0.05),   # C3 shape, ragged image groups (13 = 3 x 4 + 1)
+    (6, 14, 14, 256, 256, 3, 1, 64, 64, 0.02),    # C2 shape
+    (5, 12, 12, 64, 200, 5, 2, 32, 48, 0.05),     # 5x5, Cout not /128
+    (9, 6, 6, 128, 128, 1, 0, 64, 64, 0.30),      # 1x1 Tucker-2 (G 1x1), dense S: residual blocks
+]
+
+
+@pytest.mark.parametrize("geom", IPW_CASES)
+def test_four_image_windows_bitwise_equal_eight(geom):
+    """The windowed kernel with 4 images per window (a core matrix = 2 positions x 4 images,
+    tap offsets of 512 B) accumulates every output in the same order as with 8: bitwise
+    equal, and against the oracle."""
+    import os
+    n, h, w, cin, cout, k, p, r1, r2, dens = geom
+    cfg = workloads.LayerConfig("ipw", n, h, w, cin, cout, k, 1, p, r1, r2, dens, "bf16", seed=23)
+    inp = workloads.generate(cfg)
+    ys = {}
+    for ipw in ("8", "4"):
+        os.environ["LRS_WCONV_IPW"] = ipw
+        try:
+            layer = layer_of(inp)
+        finally:
+            os.environ.pop("LRS_WCONV_IPW", None)
+        assert layer.expand_kernel == 1
+        y = layer(torch.from_numpy(inp.x).to(torch.bfloat16).cuda())
+        torch.cuda.synchronize()
+        ys[ipw] = y
+    assert torch.equal(ys["8"], ys["4"])
+    parity.check(ys["4"], oracle(inp), "bf16")

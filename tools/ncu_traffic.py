@@ -5,11 +5,11 @@ import csv, json, os, subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REPS = {  # config -> (report under gpurun_out/, kernel, round tag)
-    "c2_bf16": ("prof_wconv_c2.ncu-rep", "lrs_wconv_kernel", "r01_v16"),
-    "c3": ("prof_wconv_c3.ncu-rep", "lrs_wconv_kernel", "r01_v16"),
-    "c4": ("prof_wconv_c4.ncu-rep", "lrs_wconv_kernel", "r01_v16"),
-    "c2_f32": ("prof_spadd_c2_f32.ncu-rep", "lrs_spadd_kernel", "r01_v16"),
-    "c1": ("prof_tiny_c1.ncu-rep", "lrs_tiny_kernel", "r01_v16"),
+    "c2_bf16": ("r02v/prof_wconv_c2_bf16.ncu-rep", "lrs_wconv_kernel", "r02"),
+    "c3": ("r02v/prof_wconv_c3.ncu-rep", "lrs_wconv_kernel", "r02"),
+    "c4": ("r02v/prof_pw_c4.ncu-rep", "lrs_pw_kernel", "r02"),
+    "c2_f32": ("r02v/prof_spadd_c2_f32.ncu-rep", "lrs_spadd_kernel", "r02"),
+    "c1": ("r02v/prof_tiny_c1.ncu-rep", "lrs_tiny_kernel", "r02"),
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
@@ -24,7 +24,7 @@ def main():
         rows = list(csv.reader(txt.splitlines()))
         hdr, units, vals = rows[0], rows[1], rows[2]
         get = lambda m: float(vals[hdr.index(m)]) * UNIT.get(units[hdr.index(m)], 1)  # noqa: E731
-        out[cfg] = {"kernel": kern, "dram_read_bytes": get("dram__bytes_read.sum"),
+        out[cfg] = {"kernel": kern, "kernel_stage": "a345_expand_sparse", "dram_read_bytes": get("dram__bytes_read.sum"),
                     "dram_write_bytes": get("dram__bytes_write.sum"),
                     "duration_us_cold": get("gpu__time_duration.sum"),
                     "source": f"profiles/{tag}_ncu_*_summary.txt (ncu --set full --clock-control none, 1 launch)"}
