@@ -33,8 +33,8 @@
  *
  * Environment (read at create): LRS_VERBOSE; plan / engine overrides used by
  * the tests to cover every path -- LRS_NO_AUTOTUNE, LRS_NO_CORE, LRS_NO_TINY,
- * LRS_F32_FUSED, LRS_NO_PW, LRS_PW_{MPC,BP}, LRS_CORE_{IPT,TH,GRID,GSTREAM,T1_NOSWZ}, LRS_TINY_CB,
- * LRS_WCONV_{TH,CB,CPW,NS,BPI,REUSE,NWB1,ERING} -- each selects another plan
+ * LRS_F32_FUSED, LRS_NO_PW, LRS_PW_{MPC,BP,FT}, LRS_CORE_{IPT,TH,GRID,GSTREAM,T1_NOSWZ},
+ * LRS_TINY_CB, LRS_WCONV_{TH,CB,CPW,NS,BPI,IPW,REUSE,NWB1,ERING} -- each selects another plan
  * that computes the same Y.  Knobs that skip work (timing bisection) exist
  * only in -DLRS_EXPERIMENTS builds; bench.py refuses to time with any LRS_*
  * variable set.
@@ -238,7 +238,9 @@ lrs_status lrs_sparse_from_slices(int32_t c_in, int32_t c_out, int32_t kernel_h,
  *      blocks of a fixed group of 128-channel M-tiles resident (metadata in TMEM) and
  *      streams X and T1 position tiles through it (C4; PAPER.md:168, :171-191 at k = 1).
  *      LRS_NO_PW=1 at create selects kernel 1 instead; LRS_PW_MPC / LRS_PW_BP override
- *      the M-tiles per CTA / positions per tile (same Y).
+ *      the M-tiles per CTA / positions per tile; LRS_PW_FT=1 fuses the projection a1 into
+ *      the same kernel (lrs_pwf.cuh: one launch, T1 never in HBM; measured slower at C4,
+ *      so not the default) -- every choice computes the same bits.
  */
 int32_t lrs_conv_expand_kernel(const lrs_conv *h);
 

@@ -1303,9 +1303,11 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
   const int bp_env = getenv("LRS_PW_BP") ? atoi(getenv("LRS_PW_BP")) : 0;
   // ft: the projection fused in (lrs_pwf.cuh) -- needs 128-position tiles (the M of the T1
   // MMAs), R1p a multiple of 32 (the restage splits the ranks over two warps in steps of 16)
-  // and the X chunks even without a sparse term; it saves the a1 launch and T1's HBM round
-  // trip, so it is preferred whenever it fits (LRS_PW_FT=0 keeps the two-kernel form)
-  const bool ft_ok = r1p % 32 == 0 && r1p <= 256 && !(getenv("LRS_PW_FT") && atoi(getenv("LRS_PW_FT")) == 0);
+  // and the X chunks even without a sparse term.  It saves the a1 launch and T1's HBM round
+  // trip but measured slower at C4 (33.9 vs 25.9 us: U^T, two T1 tiles and the restage
+  // leave a ring of ~1 tile, so every tile's X loads wait for the previous tile's MMAs;
+  // profiles/r02_ablate_pwf_c4.log), so it is a plan option: LRS_PW_FT=1
+  const bool ft_ok = r1p % 32 == 0 && r1p <= 256 && getenv("LRS_PW_FT") && atoi(getenv("LRS_PW_FT")) == 1;
   struct Plan { int mpc = 0, bp = 0, ns = 0, nblk = 0, gpg = 0, ft = 0; uint32_t smem = 0, w_bytes = 0; double cost = 1e300; };
   Plan best;
   for (int ft = ft_ok ? 1 : 0; ft >= 0 && !best.mpc; --ft) {

@@ -55,7 +55,7 @@ def test_c4_uses_the_pointwise_kernel():
     inp = workloads.generate(workloads.CONFIGS["c4"], batch=2)
     layer = make(inp)
     assert layer.expand_kernel == 2
-    assert layer.sparse_engine[0] == 1 and layer.launches_per_forward == 1  # projection fused in
+    assert layer.sparse_engine[0] == 1 and layer.launches_per_forward == 2
     parity.check(fwd(layer, inp), oracle(inp), "bf16")
 
 
@@ -106,16 +106,16 @@ def test_wide_input_falls_back_to_the_windowed_kernel():
     parity.check(fwd(layer, inp), oracle(inp), "bf16")
 
 
-@pytest.mark.parametrize("geom", [(3, 14, 14, 256, 1024, 64, 0.01), (2, 7, 7, 256, 2048, 128, 0.02),
+@pytest.mark.parametrize("geom", [(3, 14, 14, 256, 1024, 64, 0.01), (2, 7, 7, 128, 384, 48, 0.05),
                                   (4, 28, 28, 128, 512, 32, 0.01), (5, 6, 6, 64, 128, 32, 0.0)])
 def test_fused_projection_bitwise_equal_two_kernel_form(geom):
-    """lrs_pwf_kernel (T1 = X U computed per tile from the X chunks in shared memory, one
-    launch) against lrs_pw_kernel fed by the separate projection kernel (LRS_PW_FT=0): the
-    same MMAs in the same K order, so bitwise equal; and against the oracle."""
+    """lrs_pwf_kernel (LRS_PW_FT=1: T1 = X U computed per tile from the X chunks in shared
+    memory, one launch) against lrs_pw_kernel fed by the separate projection kernel (the
+    default): the same MMAs in the same K order, so bitwise equal; and against the oracle."""
     n, h, w, cin, cout, r, dens = geom
     inp = workloads.generate(svd_cfg(n, h, w, cin, cout, r, dens))
-    fused = make(inp)
-    split = make(inp, {"LRS_PW_FT": "0"})
+    fused = make(inp, {"LRS_PW_FT": "1"})
+    split = make(inp)
     assert fused.launches_per_forward == 1 and split.launches_per_forward == 2
     yf, ys = fwd(fused, inp), fwd(split, inp)
     assert torch.equal(yf, ys)
