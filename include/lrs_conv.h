@@ -112,7 +112,10 @@ typedef struct lrs_conv_desc {
  *   unsorted or duplicate columns), core == NULL with a non-1x1 / strided /
  *   padded kernel or rank_in != rank_out, NULL required pointer.
  * UNSUPPORTED: kernel > 7, rank > 256, c_in or c_out not a multiple of 8
- *   (bf16) / 4 (fp32) (16-byte TMA rows), output width > 128.
+ *   (bf16) / 4 (fp32) (16-byte TMA rows), output width > 256; output width > 128
+ *   unless the layer is bf16 with c_in % 64 == 0 and its core runs in the fused core
+ *   kernel (stride 1, window <= 256 columns and fitting shared memory), is the CP form or
+ *   an SVD pair (the GEMM core convolution tiles whole rows of <= 128 outputs).
  * bf16 layers with c_in % 64 == 0 run the fused expansion + sparse term on
  * the 2:4 sparse tensor cores (lrs_conv_sparse_engine() == 1); S is split at
  * create into exact 2:4 main and residual blocks (PAPER.md:171-191 evaluated

@@ -309,7 +309,12 @@ lrs_status validate(const lrs_conv_desc* d) {
   const int vec = d->dtype == LRS_DTYPE_BF16 ? 8 : 4;
   if (d->c_in % vec || d->c_out % vec)
     return fail(LRS_ERR_UNSUPPORTED, "c_in and c_out must be multiples of %d", vec);
-  if (wo > 128) return fail(LRS_ERR_UNSUPPORTED, "output width > 128");
+  // rows wider than 128 outputs: only the bf16 kernels that band the columns (the fused
+  // core, the windowed / pointwise expansion kernels, the CP depthwise kernel) take them;
+  // layers that would need the GEMM core convolution are refused after planning
+  if (wo > 256) return fail(LRS_ERR_UNSUPPORTED, "output width > 256");
+  if (wo > 128 && (d->dtype != LRS_DTYPE_BF16 || d->c_in % 64 != 0))
+    return fail(LRS_ERR_UNSUPPORTED, "output width > 128 needs a bf16 layer with c_in %% 64 == 0");
   if (wo * d->stride_w > 256 || d->stride_h * std::min(ho, 128) > 256)
     return fail(LRS_ERR_UNSUPPORTED, "TMA box too wide");
   return LRS_OK;
@@ -1743,7 +1748,12 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     memset(&p, 0, sizeof(p));
     // K chunks must not straddle taps: the swizzle width has to divide R1p * esz
     const uint32_t sw = (r1p * esz) % 128 == 0 ? 128u : ((r1p * esz) % 64 == 0 ? 64u : 32u);
-    if (ho * wo <= kTileM) {
+    if (wo > kTileM) {
+      // the GEMM core convolution tiles whole output rows (<= 128 outputs): a wider layer
+      // must take the fused core kernel (refused below if it does not)
+      g.th = 1;
+      g.nb = 1;
+    } else if (ho * wo <= kTileM) {
       g.th = ho;
       g.nb = kTileM / (ho * wo);
     } else {
@@ -1782,6 +1792,8 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     h->a2.kid = f32 ? K_STORE_F32 : K_STORE_BF16;
   }
   if ((st = build_core(h, d)) != LRS_OK) return cleanup_fail(st);
+  if (wo > kTileM && !h->svd && !h->cp_core && !h->use_core)
+    return cleanup_fail(fail(LRS_ERR_UNSUPPORTED, "output width > 128 needs the fused core kernel (stride 1)"));
   if ((st = build_tiny(h, d)) != LRS_OK) return cleanup_fail(st);
   // ---------------------------------------------------------------- a3+a4+a5
   if (bf16_w && h->svd && (st = build_pw(h, d)) != LRS_OK) return cleanup_fail(st);

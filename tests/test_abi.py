@@ -158,3 +158,19 @@ def test_binding_rounds_factors_to_nearest_even():
     d, keep = B.make_desc(**args)
     u = np.ctypeslib.as_array(ctypes.cast(d.u_in, ctypes.POINTER(ctypes.c_uint16)), shape=(16 * 4,))
     assert np.array_equal(u, B.bf16_bits_rne(args["u_in"]).ravel())
+
+
+def test_wide_rows_need_a_bf16_tensor_core_layer():
+    """Output rows wider than 128 are refused before any device call for fp32 layers and
+    for c_in % 64 != 0 (their engines tile whole rows of <= 128 outputs); > 256 always."""
+    for over in (dict(dtype="f32", in_w=200), dict(in_w=200), dict(in_w=300, c_in=64)):
+        args = base_desc_args(**{k: v for k, v in over.items() if k in ("dtype", "in_w")})
+        if "c_in" in over:
+            rng = np.random.default_rng(1)
+            args["c_in"] = 64
+            args["u_in"] = rng.standard_normal((64, 4)).astype(np.float32)
+            args["col_idx"] = np.zeros(16, np.int32)
+        d, keep = B.make_desc(**args)
+        h = ctypes.c_void_p()
+        st = P.load_library().lrs_conv_create(ctypes.byref(d), 0, ctypes.byref(h))
+        assert st == B.LRS_ERR_UNSUPPORTED, (over, st)

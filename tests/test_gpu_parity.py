@@ -211,7 +211,9 @@ EDGE = [  # (n, h, w, cin, cout, k, s, p, r1, r2, density, dtype)  -- the ABI's 
     (2, 16, 16, 64, 64, 7, 1, 3, 32, 32, 0.02, "bf16"),     # largest kernel (7x7)
     (2, 9, 9, 64, 64, 7, 2, 3, 16, 16, 0.03, "f32"),        # 7x7, stride 2, fp32
     (3, 7, 7, 256, 256, 3, 1, 1, 256, 256, 0.02, "bf16"),   # largest ranks (256)
-    (2, 5, 128, 64, 64, 3, 1, 1, 16, 16, 0.02, "bf16"),     # widest output row (128)
+    (2, 5, 128, 64, 64, 3, 1, 1, 16, 16, 0.02, "bf16"),     # 128-wide rows (the GEMM core convolution's limit)
+    (2, 4, 168, 64, 64, 3, 1, 1, 16, 16, 0.02, "bf16"),     # 168-wide rows (ResNet-50 layer1 at 3x input): fused core
+    (1, 3, 200, 64, 128, 3, 1, 1, 32, 32, 0.03, "bf16"),    # 200-wide rows: the fused core kernel's X slots near their limit
     (1, 4, 4, 8, 8, 3, 1, 1, 4, 4, 0.5, "bf16"),            # smallest channels (8), dense-ish S
 ]
 
@@ -223,3 +225,27 @@ def test_edge_geometries_vs_oracle(geom):
     inp = workloads.generate(cfg)
     _, _, y = run(inp)
     check(y, oracle(inp), dtype)
+
+
+def test_wide_rows_cp_and_svd_and_refusal():
+    """Output rows wider than 128 (Table 4's 3x input):
+    the paper's CP form (fused projection + depthwise stages) and the 1x1 SVD pair run them;
+    a strided Tucker-2 layer, which needs the GEMM core convolution (whole rows of <= 128
+    outputs), is refused with LRS_ERR_UNSUPPORTED -- never computed wrongly."""
+    from paper_2006_06443_b200 import LrsConv, LrsError
+    cfg = workloads.LayerConfig("cpw", 2, 4, 168, 64, 64, 3, 1, 1, 16, 16, 0.02, "bf16", seed=41)
+    inp = workloads.generate_cp(cfg)
+    layer = LrsConv.from_cp(2, 4, 168, 3, 1, 1, "bf16", inp.a, inp.b, inp.c, inp.d, inp.row_ptr, inp.col_idx,
+                            inp.values)
+    y = layer(torch.from_numpy(inp.x).to(torch.bfloat16).cuda())
+    torch.cuda.synchronize()
+    ref = O.forward_cp(inp.x.astype(np.float64), inp.a, inp.b, inp.c, inp.d, inp.row_ptr, inp.col_idx, inp.values, 1, 1)
+    check(y, ref, "bf16")
+    svd = workloads.generate(workloads.LayerConfig("svdw", 2, 3, 168, 64, 256, 1, 1, 0, 32, 32, 0.02, "bf16",
+                                                   svd=True, seed=42))
+    _, _, y = run(svd)
+    check(y, oracle(svd), "bf16")
+    s2 = workloads.generate(workloads.LayerConfig("s2w", 1, 4, 338, 64, 64, 3, 2, 1, 16, 16, 0.02, "bf16", seed=43))
+    with pytest.raises(LrsError) as e:
+        run(s2)
+    assert e.value.status == 2  # LRS_ERR_UNSUPPORTED
