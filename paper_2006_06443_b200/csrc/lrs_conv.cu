@@ -1313,7 +1313,7 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
   // leave a ring of ~1 tile, so every tile's X loads wait for the previous tile's MMAs;
   // profiles/r02_ablate_pwf_c4.log), so it is a plan option: LRS_PW_FT=1
   const bool ft_ok = r1p % 32 == 0 && r1p <= 256 && getenv("LRS_PW_FT") && atoi(getenv("LRS_PW_FT")) == 1;
-  struct Plan { int mpc = 0, bp = 0, ns = 0, nblk = 0, gpg = 0, ft = 0; uint32_t smem = 0, w_bytes = 0; double cost = 1e300; };
+  struct Plan { int mpc = 0, bp = 0, ns = 0, nblk = 0, gpg = 0, ft = 0, epi_nbuf = 2; uint32_t smem = 0, w_bytes = 0; double cost = 1e300; };
   Plan best;
   for (int ft = ft_ok ? 1 : 0; ft >= 0 && !best.mpc; --ft) {
   for (int mpc = std::min(kPMaxMpc, n_mt); mpc >= 1; --mpc) {
@@ -1346,10 +1346,23 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
       const uint32_t t1s = ft ? 2u * 128u * static_cast<uint32_t>(r1p) * 2u : 0u;
       // (fused: the metadata staging shares the second T1 tile, first written after the copy)
       const uint32_t e_stage = (ft && e_bytes <= t1s / 2) ? 0u : align1024(e_bytes);
-      const uint32_t fixed = align1024(w_bytes) + align1024(u_bytes) + align1024(t1s) + e_stage + 8 * kPEpiScratch +
-                             1024 /*tab*/ + 1024 /*bars*/ + 1024 /*align*/;
-      if (fixed >= static_cast<uint32_t>(kMaxSmem)) continue;
-      const int ns = std::min<int>(kPMaxSlots, static_cast<int>((kMaxSmem - fixed) / slot));
+      // the two-kernel form stages the metadata in the ring's last slots (free once copied to
+      // TMEM) and takes one epilogue scratch buffer per warp when that buys another ring slot
+      const uint32_t e_ring = ft ? e_stage : 0u;
+      const uint32_t base = align1024(w_bytes) + align1024(u_bytes) + align1024(t1s) + e_ring + 1024 /*tab*/ +
+                            1024 /*bars*/ + 1024 /*align*/;
+      const int nbuf_env = getenv("LRS_PW_EPIBUF") ? atoi(getenv("LRS_PW_EPIBUF")) : 0;  // plan override
+      int epi_nbuf = ft ? 2 : (nbuf_env ? nbuf_env : 2);
+      if (base + 8u * 2048u * epi_nbuf >= static_cast<uint32_t>(kMaxSmem)) continue;
+      int ns = static_cast<int>((kMaxSmem - base - 8u * 2048u * epi_nbuf) / slot);
+      if (!ft && !nbuf_env && epi_nbuf == 2 && ns < kPMaxSlots &&
+          static_cast<int>((kMaxSmem - base - 8u * 2048u) / slot) > ns) {
+        epi_nbuf = 1;
+        ns = static_cast<int>((kMaxSmem - base - 8u * 2048u) / slot);
+      }
+      ns = std::min(ns, kPMaxSlots);
+      if (!ft && ns * slot < e_bytes) continue;  // the staging must fit in the ring
+      const uint32_t fixed = base + 8u * 2048u * epi_nbuf;
       // slots are released chunk by chunk (tcgen05.commit after each chunk's MMAs), but the
       // producer lanes request a tile's chunks in parallel, so the ring must hold a whole
       // tile: with fewer slots two lanes would wait on two phases of one slot's mbarrier at
@@ -1369,7 +1382,7 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
       const double cost = static_cast<double>(tiles) * std::max(mma, std::max(in, out)) * shallow + 400.0 * mpc;
       if (cost < best.cost) {
         best.cost = cost; best.mpc = mpc; best.bp = bp; best.ns = ns; best.nblk = nblk; best.gpg = gpg;
-        best.w_bytes = w_bytes; best.ft = ft;
+        best.w_bytes = w_bytes; best.ft = ft; best.epi_nbuf = epi_nbuf;
         best.smem = fixed + static_cast<uint32_t>(ns) * slot;
       }
     }
@@ -1472,13 +1485,20 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
     const bool e_shared = e_bytes <= q.t1s_bytes;
     q.off_e = e_shared ? q.off_t1s + q.t1s_bytes : q.off_t1s + align1024(2 * q.t1s_bytes);
     q.off_ring = q.off_t1s + align1024(2 * q.t1s_bytes) + (e_shared ? 0u : align1024(e_bytes));
+    q.e_slot0 = best.ns;
+    q.epi_nbuf = 2;
   } else {
     q.e_col0 = 2 * q.acc_cols;
-    q.off_e = align1024(best.w_bytes);
-    q.off_ring = q.off_e + align1024(static_cast<uint32_t>(nblk) * 2048u);
+    q.off_ring = align1024(best.w_bytes);
+    // the metadata staging occupies the ring's last slots until its copies to TMEM complete
+    const uint32_t e_bytes = static_cast<uint32_t>(nblk) * 2048u;
+    const int ke = static_cast<int>((e_bytes + q.slot_bytes - 1) / q.slot_bytes);
+    q.e_slot0 = best.ns - ke;
+    q.off_e = q.off_ring + static_cast<uint32_t>(q.e_slot0) * q.slot_bytes;
+    q.epi_nbuf = best.epi_nbuf;
   }
   q.off_epi = q.off_ring + static_cast<uint32_t>(best.ns) * q.slot_bytes;
-  q.off_tab = q.off_epi + 8 * kPEpiScratch;
+  q.off_tab = q.off_epi + 8u * 2048u * static_cast<uint32_t>(q.epi_nbuf);
   q.off_bar = q.off_tab + 1024;
   q.relu = 0;
 #ifdef LRS_EXPERIMENTS
@@ -1491,8 +1511,8 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
   h->use_pw = true;
   h->pw_ft = best.ft != 0;
   if (getenv("LRS_VERBOSE"))
-    fprintf(stderr, "[lrs] pw plan: fused a1 %d mpc %d groups %d bp %d ns %d blocks/group %d ctas/group %d smem %u B\n",
-            best.ft, mpc, G, best.bp, best.ns, nblk, best.gpg, best.smem);
+    fprintf(stderr, "[lrs] pw plan: fused a1 %d mpc %d groups %d bp %d ns %d epi bufs %d blocks/group %d ctas/group %d smem %u B\n",
+            best.ft, mpc, G, best.bp, best.ns, best.epi_nbuf, nblk, best.gpg, best.smem);
   return LRS_OK;
 }
 }  // namespace

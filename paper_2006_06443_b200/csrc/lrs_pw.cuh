@@ -33,7 +33,7 @@ constexpr int kPThreads = 320;
 constexpr int kPMaxMpc = 4;        // M-tiles per CTA
 constexpr int kPMaxCk = 8;         // 64-channel input chunks (Cin <= 512)
 constexpr int kPMaxSlots = 16;
-constexpr uint32_t kPEpiScratch = 4096;  // per epilogue warp: 2 x [32 positions][32 channels] bf16
+constexpr uint32_t kPEpiScratch = 4096;  // per epilogue warp, at most: 2 x [32 positions][32 channels] bf16
 
 struct PwParams {
   CUtensorMap tmX;  // X  2-D [P][Cin] bf16, box {64, bp}, SW128
@@ -61,6 +61,9 @@ struct PwParams {
   uint32_t acc_cols;       // TMEM columns of one accumulator set (mpc * bp)
   uint32_t e_col0;         // first metadata column (2 * acc_cols)
   uint32_t off_e, off_ring, off_epi, off_tab, off_bar;
+  int e_slot0;             // first ring slot the metadata staging shares (ns: none); the producer
+                           // fills slots >= e_slot0 only after the copies to TMEM completed
+  int epi_nbuf;            // epilogue scratch buffers per warp (1 or 2, 2 KB each)
   unsigned long long* trace;  // debug builds: %globaltimer stamps of CTA 0 (lrs_conv_debug_trace)
   int dbg;                    // experiment builds (LRS_PW_DBG): 1 skip Y stores, 2 skip MMAs, 4 skip X/T loads
   // projection fused in (lrs_pwf_kernel): T1 = X U computed per position tile from the X
@@ -95,7 +98,8 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
   uint64_t* acc_full = empty + kPMaxSlots;     // [2]
   uint64_t* acc_empty = acc_full + 2;          // [2]
   uint64_t* w_full = acc_empty + 2;            // weights + metadata staged
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
+  uint64_t* e_done = w_full + 1;               // metadata copied to TMEM: its staging slots are free
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(e_done + 1);
   uint16_t* tab_s = reinterpret_cast<uint16_t*>(smem + p.off_tab);
 
   const int grp = static_cast<int>(blockIdx.x) % p.n_groups;
@@ -112,6 +116,7 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
       mbar_init(&acc_empty[i], 8);
     }
     mbar_init(w_full, 1);
+    mbar_init(e_done, 1);
     fence_mbar_init();
     tma_prefetch_desc(&p.tmX);
     tma_prefetch_desc(&p.tmT);
@@ -128,6 +133,7 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
     prm[5] = static_cast<int>(p.slot_bytes); prm[6] = static_cast<int>(p.sw_t); prm[7] = static_cast<int>(p.acc_cols);
     prm[8] = p.t_kc; prm[9] = static_cast<int>(p.e_col0); prm[10] = p.relu; prm[11] = p.cout; prm[12] = p.P;
     prm[13] = li; prm[14] = gctas; prm[15] = static_cast<int>(p.off_ring); prm[16] = static_cast<int>(p.dense_bytes);
+    prm[17] = p.e_slot0; prm[18] = p.epi_nbuf;
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -156,6 +162,7 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
     }
     bool waited = false;
     const int t_kc = smem_param(prm + 8);
+    const int e_slot0 = smem_param(prm + 17);
     const uint32_t ring = smem_u32(smem) + static_cast<uint32_t>(smem_param(prm + 15));
     // item it = round * ns + slot, tracked incrementally (no divisions): lane l < n_x owns
     // the X chunk l of every tile (item k * nq + l), lane 0 also the T1 chunks
@@ -167,6 +174,7 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
       const int p0 = pt * bp;
       if (lane < n_x) {
         if (xr > 0) mbar_wait(&empty[xs], (xr - 1) & 1);
+        else if (xs >= e_slot0) mbar_wait(e_done, 0);  // the slot still holds metadata staging
         if (LRS_XDBG(p.dbg & 4)) {
           mbar_arrive(&full[xs]);
         } else {
@@ -181,6 +189,7 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
         int s = ts, r = tr;
         for (int tk = 0; tk < n_tk; ++tk) {
           if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
+          else if (s >= e_slot0) mbar_wait(e_done, 0);
           if (!waited) {  // T1 is the previous kernel's output
             pdl_wait();
             pdl_launch_dependents();
@@ -213,6 +222,7 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
       // sparsity metadata of the group's 2:4 blocks -> TMEM, once (block b at e_col0 + 4 b)
       const uint64_t ed = umma_desc_rows16(smem_u32(smem + p.off_e));
       for (int b = 0; b < p.nblk_max; ++b) tmem_cp_128x128b(tmem + p.e_col0 + 4u * b, ed + b * (2048u >> 4));
+      mma_commit(e_done);  // arrives once the copies have read the staging (ring slots >= e_slot0)
       const uint32_t e_col0 = smem_param(prm + 9);
       const uint32_t idn = umma_idesc(1u, static_cast<uint32_t>(bp), 128u);
       const uint32_t ids = idn | (1u << 2);
@@ -290,7 +300,8 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
     // from it two chunks ago has read it (bulk wait_group.read 1).
     const int q4 = warp & 3;            // TMEM lane quarter
     const int ehalf = (warp - 2) >> 2;  // which alternate 32-column chunks
-    const uint32_t scr0 = smem_u32(smem + p.off_epi) + static_cast<uint32_t>(warp - 2) * kPEpiScratch;
+    const int epi_nbuf = smem_param(prm + 18);
+    const uint32_t scr0 = smem_u32(smem + p.off_epi) + static_cast<uint32_t>((warp - 2) * epi_nbuf) * 2048u;
     const int relu = smem_param(prm + 10), cout = smem_param(prm + 11);
     const bool epi = p.epi != nullptr || relu;
     const int t1 = lane >> 2, mi = lane >> 3, mj = lane & 7;
@@ -326,8 +337,11 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
               tmem_ld_16x256b_x2(tmem + (static_cast<uint32_t>(q4 * 32 + 16 * h) << 16) + acc0 +
                                      static_cast<uint32_t>(m * bp + c0 + 16 * cb),
                                  r[h][cb]);
-          const uint32_t scr = scr0 + static_cast<uint32_t>(nchunk & 1) * 2048u;
-          if (lane == 0) bulk_wait_read1();  // the store that last read this buffer is done with it
+          const uint32_t scr = scr0 + static_cast<uint32_t>(nchunk % epi_nbuf) * 2048u;
+          if (lane == 0) {  // the store that last read this buffer is done with it
+            if (epi_nbuf == 2) bulk_wait_read1();
+            else bulk_wait_read0();
+          }
           tmem_ld_wait();
           __syncwarp();
 #pragma unroll
