@@ -248,6 +248,24 @@ lrs_status lrs_sparse_from_slices(int32_t c_in, int32_t c_out, int32_t kernel_h,
 int32_t lrs_conv_expand_kernel(const lrs_conv *h);
 
 /*
+ * How the windowed tensor-core kernel (expand kernel 1) evaluates the entries of S
+ * that an exact 2:4 main block cannot hold (the 3rd / 4th nonzero of a group of 4
+ * input channels, PAPER.md:171-191 evaluated exactly):
+ *   0   residual 2:4 blocks (lrs_conv_sparse_engine's residual_blocks), one per
+ *       (M-tile, 64-channel chunk, tap) that has any such entry -- each costs a
+ *       full sparse MMA pass over the tile's positions;
+ *   g>0 g "overflow gather" chunks per 128-channel M-tile: the M-tile's distinct
+ *       (input channel, tap) pairs of those entries become g * 64 (or g * R2 when
+ *       R2 < 64) extra dense K columns G[pos][slot] = X[pos + tap][channel],
+ *       gathered per tile by the kernel's epilogue warps into a device scratch of
+ *       batch_max * out_h * out_w * n_mt * g * 64 bf16 and multiplied on the dense
+ *       tensor cores by the entries' values (residual_blocks is then 0).
+ * Chosen at create by cost (residual MMA steps vs gather chunks); LRS_WCONV_GATHER=0/1
+ * in the environment at create forces it.  -1 for NULL; 0 for the other kernels.
+ */
+int32_t lrs_conv_overflow_chunks(const lrs_conv *h);
+
+/*
  * 1 if the projection a1 and the core convolution a2 of this layer run as one
  * kernel (bf16 Tucker-2 layers with stride 1 and c_in % 64 == 0: T1 is computed
  * on each tile's input window and kept in shared memory, never written to HBM;

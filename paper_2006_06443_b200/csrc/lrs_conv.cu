@@ -225,6 +225,9 @@ struct lrs_conv {
   uint32_t w_smem = 0;
   void* w_as = nullptr;   // compressed 2:4 blocks of S (SW64 shared-memory images)
   void* w_dense_img = nullptr;  // U_out^T blocks (shared-memory images)
+  void* w_gtab = nullptr;       // overflow-gather slot table (WconvParams::g_tab)
+  void* w_g = nullptr;          // overflow-gather scratch G
+  std::vector<uint8_t> w_ovf;   // build-time: overflow-value blocks
   void* w_e = nullptr;    // their metadata
   int* w_res = nullptr;   // residual block table
   const void* wx_ptr = nullptr;
@@ -861,14 +864,21 @@ lrs_status build_spadd(lrs_conv* h, const lrs_conv_desc* d) {
 // as: [blocks][128 rows][32] bf16 bits (row-major, unswizzled); ee: [blocks][128 lanes][4]
 // u32 metadata words; main block of key (mt * n_ck + c) * taps + t has index key, its
 // residual block res_tab[key] (-1 if none).
+// With `gather`, a group's 3rd/4th nonzero goes to ovf[M-tile] (row, channel, tap, value)
+// instead of a residual block (the overflow-gather form, lrs_wconv.cuh WconvParams::n_gk).
+struct Ovf {
+  int m, ch, t;
+  float v;
+};
 struct Split24 {
   std::vector<uint16_t> as;
   std::vector<uint32_t> ee;
   std::vector<int> res_tab;
+  std::vector<std::vector<Ovf>> ovf;
   int nblk_main = 0, nres = 0;
 };
 
-Split24 split_24(const lrs_conv_desc* d, int n_mt, int n_ck, int taps) {
+Split24 split_24(const lrs_conv_desc* d, int n_mt, int n_ck, int taps, bool gather = false) {
   const int cout = d->c_out;
   Split24 S;
   const int nblk_main = n_mt * n_ck * taps;
@@ -879,6 +889,7 @@ Split24 split_24(const lrs_conv_desc* d, int n_mt, int n_ck, int taps) {
   as.assign(static_cast<size_t>(nblk_main) * 128 * 32, 0);
   ee.assign(static_cast<size_t>(nblk_main) * 128 * 4, 0x44444444u);
   res_tab.assign(nblk_main, -1);
+  if (gather) S.ovf.assign(n_mt, {});
   int nres = 0;
   std::vector<float> dense(static_cast<size_t>(n_ck) * taps * 64);
   auto put = [&](int blk, int m, int grp, int i0, int i1, float v0, float v1) {
@@ -924,7 +935,9 @@ Split24 split_24(const lrs_conv_desc* d, int n_mt, int n_ck, int taps) {
               ++cnt;
             }
           put_list(key, m, grp, idx, val, std::min(cnt, 2));
-          if (cnt > 2) {
+          if (cnt > 2 && gather) {
+            for (int i = 2; i < cnt; ++i) S.ovf[mt].push_back({m, c * 64 + 4 * grp + idx[i], t, val[i]});
+          } else if (cnt > 2) {
             if (res_tab[key] < 0) {
               res_tab[key] = nblk_main + nres++;
               as.resize(as.size() + 128 * 32, 0);
@@ -1130,6 +1143,48 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
 
   // ---- S -> exact 2:4 main + residual blocks (bf16 values, RNE), TMEM metadata
   Split24 S24 = split_24(d, n_mt, n_ck, taps);
+  // overflow gather instead of residual blocks when the residual MMAs cost more than the
+  // G chunks: a residual block is 2 sparse MMA steps (each the time of a dense K = 16 step)
+  // per unit, a G chunk t_kc / 16 dense steps, plus ~8 steps for the gather hand-off
+  int n_gk = 0;
+  std::vector<int> g_tab;
+  {
+    const char* ge = getenv("LRS_WCONV_GATHER");  // plan override: 0 = residual blocks, 1 = gather
+    if (S24.nres > 0 && !(ge && atoi(ge) == 0)) {
+      Split24 G = split_24(d, n_mt, n_ck, taps, true);
+      std::vector<std::vector<std::pair<int, int>>> slots(n_mt);  // distinct (channel, tap) per M-tile
+      size_t mx = 0;
+      for (int mt = 0; mt < n_mt; ++mt) {
+        for (const Ovf& o : G.ovf[mt])
+          if (std::find(slots[mt].begin(), slots[mt].end(), std::make_pair(o.ch, o.t)) == slots[mt].end())
+            slots[mt].emplace_back(o.ch, o.t);
+        mx = std::max(mx, slots[mt].size());
+      }
+      const int gk = static_cast<int>((mx + t_kc - 1) / t_kc);
+      const bool pays = 2.0 * S24.nres / n_mt > gk * (t_kc / 16.0) + 8.0;
+      if (gk * t_kc <= 128 && gk * t_kc <= 0xFFFF && (pays || (ge && atoi(ge) == 1))) {
+        n_gk = gk;
+        const int gs = gk * t_kc;
+        g_tab.assign(static_cast<size_t>(n_mt) * gs, -1);
+        for (int mt = 0; mt < n_mt; ++mt)
+          for (size_t si = 0; si < slots[mt].size(); ++si) {
+            const int t = slots[mt][si].second;
+            g_tab[mt * gs + si] = slots[mt][si].first | ((t / kw) << 16) | ((t % kw) << 24);
+          }
+        // the overflow values as dense U blocks: row m of M-tile mt, column = slot index
+        h->w_ovf.assign(static_cast<size_t>(n_mt) * gk * 128 * sw_t, 0);
+        for (int mt = 0; mt < n_mt; ++mt)
+          for (const Ovf& o : G.ovf[mt]) {
+            const int si = static_cast<int>(std::find(slots[mt].begin(), slots[mt].end(), std::make_pair(o.ch, o.t)) -
+                                            slots[mt].begin());
+            const uint16_t bits = bf16_bits_rne(o.v);
+            memcpy(&h->w_ovf[(static_cast<size_t>(mt) * gk + si / t_kc) * 128 * sw_t + swz_off(o.m, 2 * (si % t_kc), sw_t)],
+                   &bits, 2);
+          }
+        S24 = std::move(G);
+      }
+    }
+  }
   const int nblk_main = S24.nblk_main;
   const int nres = S24.nres;
   std::vector<uint16_t>& as = S24.as;
@@ -1184,8 +1239,10 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     h->w_res = static_cast<int*>(rp_);
     // dense A: U_out^T rows (output channels) x R chunks, the layer's bf16 values
     const int r2 = h->svd ? d->rank_in : d->rank_out;
-    std::vector<uint8_t> dn(static_cast<size_t>(n_mt) * n_tk * 128 * sw_t, 0);
-    for (int mt = 0; mt < n_mt; ++mt)
+    // per M-tile: n_tk U_out^T chunks, then n_gk overflow-value chunks (G mode)
+    const int n_dk = n_tk + n_gk;
+    std::vector<uint8_t> dn(static_cast<size_t>(n_mt) * n_dk * 128 * sw_t, 0);
+    for (int mt = 0; mt < n_mt; ++mt) {
       for (int kc = 0; kc < n_tk; ++kc)
         for (int m = 0; m < 128; ++m) {
           const int j = mt * 128 + m;
@@ -1194,10 +1251,24 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
             const int bb = kc * t_kc + e2;
             if (bb >= r2) continue;
             const uint16_t bits = static_cast<const uint16_t*>(d->u_out)[static_cast<size_t>(bb) * cout + j];
-            memcpy(&dn[(static_cast<size_t>(mt) * n_tk + kc) * 128 * sw_t + swz_off(m, 2 * e2, sw_t)], &bits, 2);
+            memcpy(&dn[(static_cast<size_t>(mt) * n_dk + kc) * 128 * sw_t + swz_off(m, 2 * e2, sw_t)], &bits, 2);
           }
         }
+      if (n_gk)
+        memcpy(&dn[(static_cast<size_t>(mt) * n_dk + n_tk) * 128 * sw_t],
+               &h->w_ovf[static_cast<size_t>(mt) * n_gk * 128 * sw_t], static_cast<size_t>(n_gk) * 128 * sw_t);
+    }
     if ((st = upload(&h->w_dense_img, dn)) != LRS_OK) return st;
+    h->w_ovf.clear();
+    h->w_ovf.shrink_to_fit();
+    if (n_gk) {
+      std::vector<uint8_t> tb(g_tab.size() * 4);
+      memcpy(tb.data(), g_tab.data(), tb.size());
+      if ((st = upload(&h->w_gtab, tb)) != LRS_OK) return st;
+      const size_t gb = static_cast<size_t>(d->batch_max) * ho * wo * n_mt * n_gk * t_kc * 2;
+      LRS_CUDA(cudaMalloc(&h->w_g, gb));
+      LRS_CUDA(cudaMemset(h->w_g, 0, gb));  // empty slots stay 0
+    }
   }
   WconvParams& w = h->wp;
   memset(&w, 0, sizeof(w));
@@ -1218,6 +1289,24 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     uint32_t estr[4] = {1, 1, 1, 1};
     if ((st = encode_t(&w.tmT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, src, dims, strides, box, estr, sw_t)) != LRS_OK)
       return st;
+  }
+  if (n_gk) {
+    const uint64_t bm = static_cast<uint64_t>(d->batch_max);
+    const uint64_t gch = static_cast<uint64_t>(n_mt) * n_gk * t_kc;
+    uint64_t dims[4] = {gch, bm, static_cast<uint64_t>(wo), static_cast<uint64_t>(ho)};
+    uint64_t strides[3] = {static_cast<uint64_t>(ho) * wo * gch * 2, gch * 2, static_cast<uint64_t>(wo) * gch * 2};
+    uint32_t box[4] = {static_cast<uint32_t>(t_kc), static_cast<uint32_t>(ipw), static_cast<uint32_t>(tbox_w),
+                       static_cast<uint32_t>(th)};
+    uint32_t estr[4] = {1, 1, 1, 1};
+    if ((st = encode_t(&w.tmG, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, h->w_g, dims, strides, box, estr, sw_t)) != LRS_OK)
+      return st;
+    w.n_gk = n_gk;
+    w.g_ch = static_cast<int>(gch);
+    w.g_tab = static_cast<const int*>(h->w_gtab);
+    w.g = static_cast<__nv_bfloat16*>(h->w_g);
+    w.in_h = d->in_h;
+    w.in_w = d->in_w;
+    w.c_in = cin;
   }
   w.stream_off = h->w_res;
   w.blk_tap = reinterpret_cast<const uint32_t*>(h->w_res + stream_off.size());
@@ -1282,8 +1371,9 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   h->w_smem = best_total;
   h->use_w = true;
   if (getenv("LRS_VERBOSE"))
-    fprintf(stderr, "lrs_wconv plan: ipw %d th %d tcols %d units %d acc %u nacc %d ns %d bpi %d nwb %d cpw %d win %u B smem %u B tiles/img-group %d\n",
-            ipw, th, tcols, w.n_units, acc, w.nacc, w.ns, w.bpi, w.nwb, cpw, best_stride, best_total, w.bands * w.cbands * w.n_mt);
+    fprintf(stderr, "lrs_wconv plan: ipw %d th %d tcols %d units %d acc %u nacc %d ns %d bpi %d nwb %d cpw %d win %u B smem %u B tiles/img-group %d residual blocks %d gather chunks %d\n",
+            ipw, th, tcols, w.n_units, acc, w.nacc, w.ns, w.bpi, w.nwb, cpw, best_stride, best_total, w.bands * w.cbands * w.n_mt,
+            nres, n_gk);
   return LRS_OK;
 }
 
@@ -2165,6 +2255,7 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
     }
     w.n = n;
     w.y = y;
+    w.x = static_cast<const __nv_bfloat16*>(x);
     w.n_tiles = ((n + w.ipw - 1) / w.ipw) * w.bands * w.cbands * w.n_mt;
     const unsigned grid = static_cast<unsigned>(std::min(w.n_tiles, h->sms));
     cudaEvent_t e1 = nullptr;
@@ -2284,7 +2375,7 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
-                  h->w_as, h->w_e, h->w_res, h->w_dense_img, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc,
+                  h->w_as, h->w_e, h->w_res, h->w_dense_img, h->w_gtab, h->w_g, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc,
                   h->sp_uo, h->epi, h->pw_w, h->pw_e, h->pw_tab, h->pw_u};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -2362,6 +2453,11 @@ int32_t lrs_conv_sparse_engine(const lrs_conv* h, int32_t* main_blocks, int32_t*
   if (main_blocks) *main_blocks = tc ? h->w_main_blocks : 0;
   if (residual_blocks) *residual_blocks = tc ? h->w_res_blocks : 0;
   return tc ? 1 : (h->use_tiny ? 3 : (h->use_spadd ? 2 : 0));
+}
+
+int32_t lrs_conv_overflow_chunks(const lrs_conv* h) {
+  if (!h) return -1;
+  return h->use_w && !h->use_pw ? h->wp.n_gk : 0;
 }
 
 int32_t lrs_conv_expand_kernel(const lrs_conv* h) {

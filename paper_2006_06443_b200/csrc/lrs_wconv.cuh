@@ -117,6 +117,19 @@ struct WconvParams {
   uint32_t off_a, off_e, off_epi, off_res, off_bar;
   const float2* epi;    // per output channel (scale, bias) of the fused output epilogue, or NULL
   int relu;
+  // overflow gather (n_gk > 0): the entries a 2:4 main block cannot hold (3rd/4th nonzero of a
+  // group of 4) are NOT given residual 2:4 blocks -- one per (chunk, tap) with any overflow,
+  // each a full MMA pass for ~1 entry -- but become n_gk extra dense K chunks of the tile:
+  // G[pos][slot] = X[pos shifted by tap_s][c_s] for the M-tile's distinct (c, tap) slots,
+  // gathered by the epilogue warps (idle during the MMAs) into global scratch, TMA-loaded
+  // back like a T window, multiplied by the slots' values (img_dense blocks n_tk..)
+  CUtensorMap tmG;      // G 4-D (n_mt * gs, N, Wo, Ho) bf16, box {t_kc, ipw, tbox_w, th}, swizzle sw_t
+  int n_gk;             // G chunks per M-tile (gs = n_gk * t_kc slots), 0: residual blocks
+  int g_ch;             // channels per position of G (n_mt * gs)
+  const int* g_tab;     // [n_mt][gs] slot -> c | dy << 16 | dx << 24 (dy, dx = tap), -1 = empty slot
+  __nv_bfloat16* g;     // G scratch [N][Ho][Wo][g_ch] (empty slots zeroed once at create)
+  const __nv_bfloat16* x;  // this forward's X (the gather reads it)
+  int in_h, in_w, c_in;
 };
 
 struct TileCoord {
@@ -153,6 +166,40 @@ __device__ __forceinline__ TileCoord tile_coord_v(int tile, int n_mt, int cbands
   return c;
 }
 
+// G rows of one tile: for each valid output position (image, ho, wo) of the tile and each
+// slot s of its M-tile, G[pos][mt * gs + s] = X[n][ho*sh - ph + dy_s][wo*sw - pw + dx_s][c_s]
+// (0 outside the image).  Empty slots are never written (zeroed at create).
+__device__ __forceinline__ void gather_tile(const WconvParams& p, const TileCoord& tc, int we, int lane) {
+  const int gs = p.n_gk * p.t_kc;
+  int tab[4];  // the lane's slots lane, lane + 32, .. (gs <= 128)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tab[i] = (lane + 32 * i < gs) ? __ldg(p.g_tab + tc.mt * gs + lane + 32 * i) : -1;
+  const int npos = p.th * p.tcols * p.ipw;
+  const __nv_bfloat16* __restrict__ x = p.x;
+  __nv_bfloat16* __restrict__ g = p.g + tc.mt * gs;
+  for (int pi = we; pi < npos; pi += 8) {
+    const int img = pi % p.ipw, q = pi / p.ipw;
+    const int r = q / p.tcols, c = q - r * p.tcols;
+    const int n = tc.n0 + img, ho = tc.ho0 + r, wo = tc.wo0 + c;
+    if (n >= p.n || ho >= p.ho || wo >= p.wo) continue;
+    const long long xrow = static_cast<long long>(n) * p.in_h;
+    __nv_bfloat16* grow = g + ((static_cast<long long>(n) * p.ho + ho) * p.wo + wo) * p.g_ch;
+    __nv_bfloat16 v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] = __float2bfloat16_rn(0.f);
+      if (tab[i] >= 0) {
+        const int hi = ho * p.sh - p.ph + ((tab[i] >> 16) & 0xFF), wi = wo * p.sw - p.pw + (tab[i] >> 24);
+        if (hi >= 0 && hi < p.in_h && wi >= 0 && wi < p.in_w)
+          v[i] = x[((xrow + hi) * p.in_w + wi) * p.c_in + (tab[i] & 0xFFFF)];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (tab[i] >= 0) grow[lane + 32 * i] = v[i];
+  }
+}
+
 // NU = the layer's exact unit count (1..kWMaxUnits): the MMA issue loops are fully
 // unrolled without predicates -- a generic 8-unit loop measured 17-39 % slower
 // (instruction fetch of the issuing warp dominates small MMAs).
@@ -172,9 +219,10 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   uint64_t* acc_empty = acc_full + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const uint32_t slot_info = smem_u32(tmem_slot + 4);  // [kWMaxSlots][kWMaxBpi] u32, written by the producer
+  uint64_t* g_ready = bars + 48;  // byte 384: the tile's G chunks are in global memory (8 epilogue warps)
 
   if (WTRACE(p) && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
-  const int nwin = p.n_tk + p.n_xw;
+  const int nwin = p.n_tk + p.n_gk + p.n_xw;
   // the role loops' scalars, staged in shared memory: a kernel parameter read inside a
   // loop is re-loaded from the constant bank at every use (~100 cycles each on the issue
   // path, tools/loop_cost2.cu); a value loaded from shared memory stays in a register
@@ -213,6 +261,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     prm[29] = static_cast<int>(p.off_e);
     prm[30] = static_cast<int>(p.off_res);
     prm[31] = p.ipw;
+    prm[32] = p.n_gk;
     for (int i = 0; i < p.nwb; ++i) {
       mbar_init(&win_full[i], 1);
       mbar_init(&win_empty[i], 1);
@@ -225,9 +274,11 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       mbar_init(&a_full[i], 1);
       mbar_init(&a_empty[i], 1);
     }
+    mbar_init(g_ready, 8);
     fence_mbar_init();
     tma_prefetch_desc(&p.tmX);
     tma_prefetch_desc(&p.tmT);
+    if (p.n_gk > 0) tma_prefetch_desc(&p.tmG);
   }
   if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
   tc_fence_before();
@@ -273,10 +324,12 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const int bands_ = static_cast<int>(smem_param(prm + 25));
     const int th_ = static_cast<int>(smem_param(prm + 26));
     const int tcols_ = static_cast<int>(smem_param(prm + 27));
+    const int n_gk_ = smem_param(prm + 32);
+    const int n_dk_ = n_tk_ + n_gk_;  // dense chunks per M-tile (T, then G)
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
       int it = 0, wg = 0, buf = 0;
-      uint32_t wph = 0;
+      uint32_t wph = 0, gph = 0;
       // the M-tile's block stream (chunk starts + per-block tap offsets), staged in shared
       // memory by independent (pipelined) loads when the M-tile changes: a global load on
       // the issue path measured ~250 ns each (tools/wtrace.py producer stamps)
@@ -316,8 +369,16 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             pdl_launch_dependents();
             waited = true;
           }
-          if (WDBG(p, 64) || reuse) {
+          if (tk == n_tk_) {  // first G chunk: wait until the epilogue warps gathered this tile
+            mbar_wait(g_ready, gph);
+            gph ^= 1u;
+          }
+          if (WDBG(p, 64) || (reuse && tk < n_tk_)) {  // G windows differ per M-tile: never reused
             mbar_arrive(&win_full[buf]);  // window already resident (or timing experiment)
+          } else if (tk >= n_tk_) {
+            mbar_arrive_expect_tx(&win_full[buf], t_win_bytes_);
+            tma_load_4d(wdst, &p.tmG, &win_full[buf], tc.mt * n_gk_ * t_kc_ + (tk - n_tk_) * t_kc_, tc.n0, tc.wo0,
+                        tc.ho0);
           } else if (tk >= 0) {
             mbar_arrive_expect_tx(&win_full[buf], t_win_bytes_);
             tma_load_4d(wdst, &p.tmT, &win_full[buf], tk * t_kc_, tc.n0, tc.wo0, tc.ho0);
@@ -327,7 +388,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             if (it >= ns_) mbar_wait(&a_empty[slot], ((it / ns_) - 1) & 1);
             mbar_arrive_expect_tx(&a_full[slot], 128u * sw_t_);
             bulk_load(smem + off_a_ + slot * a_slot_,
-                      p.img_dense + (static_cast<size_t>(tc.mt) * n_tk_ + tk) * (128u * sw_t_), 128u * sw_t_,
+                      p.img_dense + (static_cast<size_t>(tc.mt) * n_dk_ + tk) * (128u * sw_t_), 128u * sw_t_,
                       &a_full[slot]);
             ++it;
           } else {
@@ -544,6 +605,14 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const int t_step = contig ? 1 : static_cast<int>(gridDim.x);
     for (int tile = t_begin; tile < t_end; tile += t_step, ++k) {
       const TileCoord tc = tile_coord(p, tile);
+      if (p.n_gk > 0) {
+        // overflow gather of this tile (the MMA warp needs it only after the tile's sparse
+        // and T chunks): warp e takes positions e, e + 8, ..; lane = slot (64-byte stores)
+        gather_tile(p, tc, warp - 2, lane);
+        fence_proxy_async_global();  // generic-proxy stores -> the producer's TMA (async proxy) loads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(g_ready);
+      }
       const int b = p.nacc == 2 ? (k & 1) : 0;
       const int use = p.nacc == 2 ? (k >> 1) : k;
       // one thread polls the accumulator barrier, the other epilogue threads block in a

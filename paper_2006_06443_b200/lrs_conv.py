@@ -28,6 +28,7 @@ EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs
             "lrs_conv_set_timing", "lrs_conv_stage_times", "lrs_conv_stage_name",
             "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine", "lrs_conv_core_fused",
             "lrs_conv_expand_kernel",
+            "lrs_conv_overflow_chunks",
             "lrs_sparse_from_slices")
 
 
@@ -92,6 +93,8 @@ def load_library(path: str = LIB_PATH):
     lib.lrs_conv_core_fused.restype = ctypes.c_int32
     lib.lrs_conv_expand_kernel.argtypes = [P]
     lib.lrs_conv_expand_kernel.restype = ctypes.c_int32
+    lib.lrs_conv_overflow_chunks.argtypes = [P]
+    lib.lrs_conv_overflow_chunks.restype = ctypes.c_int32
     lib.lrs_sparse_from_slices.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.POINTER(ctypes.c_int64), P, ctypes.c_int32,
                                            ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64),
@@ -276,6 +279,12 @@ class LrsConv:
         """0 GEMM / SIMT, 1 windowed tensor-core kernel, 2 channel-stationary 1x1 kernel
         (lrs_conv_expand_kernel, include/lrs_conv.h)."""
         return int(load_library().lrs_conv_expand_kernel(self.handle))
+
+    @property
+    def overflow_chunks(self) -> int:
+        """Overflow-gather chunks per M-tile of the windowed kernel, 0 if it uses residual
+        2:4 blocks (lrs_conv_overflow_chunks, include/lrs_conv.h)."""
+        return int(load_library().lrs_conv_overflow_chunks(self.handle))
 
     @property
     def core_fused(self) -> bool:

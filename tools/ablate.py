@@ -3,7 +3,7 @@ LRS_EXPERIMENTS build: `LRS_EXPERIMENTS=1 python -m paper_2006_06443_b200._build
 
 usage: python tools/ablate.py <config> "<ENV=V ENV2=V>" ["<...>" ...]
 Each argument after the config is one setting (space-separated env assignments, or
-"base"); the layer is created under that environment, K forwards over rotating X/Y
+"base"; a CFG_<field>=<value> item changes the layer config, e.g. CFG_density=0.02); the layer is created under that environment, K forwards over rotating X/Y
 sets are captured in a CUDA graph and replayed; prints us per forward (median of 5)."""
 import os
 import sys
@@ -73,11 +73,15 @@ def run(cfg, inp, env):
 
 
 def main():
+    import dataclasses
     name = sys.argv[1]
-    cfg = workloads.CONFIGS[name]
-    inp = workloads.generate(cfg, batch=1)
+    base = workloads.CONFIGS[name]
     for setting in sys.argv[2:]:
         env = [] if setting == "base" else setting.split()
+        over = {kv[4:].split("=")[0]: kv.split("=", 1)[1] for kv in env if kv.startswith("CFG_")}
+        env = [kv for kv in env if not kv.startswith("CFG_")]
+        cfg = dataclasses.replace(base, **{k: type(getattr(base, k))(v) for k, v in over.items()})
+        inp = workloads.generate(cfg, batch=1)
         us, st, eng = run(cfg, inp, env)
         print(f"{name} [{setting}] {us:.2f} us/forward  stages {st}  engine {eng}", flush=True)
 
