@@ -141,6 +141,16 @@ lrs_status lrs_conv_create(const lrs_conv_desc *desc, int device, lrs_conv **out
  * n == 0 is a no-op.  INVALID_ARGUMENT: n < 0, n > batch_max, NULL or
  * misaligned pointer.  CUDA: launch failure (asynchronous faults surface at
  * the caller's next synchronisation).
+ * Kernels are launched with programmatic dependent launch: each waits
+ * (griddepcontrol.wait) before touching what the kernel before it may still
+ * write.  Layers whose projection + core kernel feeds the fused kernel (bf16,
+ * stride 1, not an SVD pair) keep two T2 buffers and let the core kernel start
+ * computing before the previous kernel on the stream has finished, unless x
+ * overlaps the output of the library's previous forward on that stream (then it
+ * waits first, as every other kernel does); the library assumes that kernels the
+ * caller enqueues between forwards do not trigger their dependents early
+ * (griddepcontrol.launch_dependents) before they finish writing.  Same results
+ * either way.  LRS_NO_EARLY=1 in the environment at create disables it.
  */
 lrs_status lrs_conv_forward(const lrs_conv *h, const void *x, void *y, int32_t n, void *stream);
 

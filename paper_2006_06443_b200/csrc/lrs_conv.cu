@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -225,6 +227,13 @@ struct lrs_conv {
   uint32_t w_smem = 0;
   void* w_as = nullptr;   // compressed 2:4 blocks of S (SW64 shared-memory images)
   void* w_dense_img = nullptr;  // U_out^T blocks (shared-memory images)
+  // early-start protocol (core -> fused kernel): T2 and G alternate between two
+  // buffers per forward so the next forward's kernels may start while this one finishes
+  bool dbuf = false;
+  int par = 0;                  // buffer parity of the next forward
+  void* t2b = nullptr;          // second T2
+  void* w_gb = nullptr;         // second overflow-gather scratch
+  CUtensorMap tmT_par[2], tmG_par[2];
   void* w_gtab = nullptr;       // overflow-gather slot table (WconvParams::g_tab)
   void* w_g = nullptr;          // overflow-gather scratch G
   std::vector<uint8_t> w_ovf;   // build-time: overflow-value blocks
@@ -1611,6 +1620,67 @@ extern "C" {
 
 const char* lrs_conv_last_error(void) { return g_err.c_str(); }
 
+// The early-start protocol for core -> fused-kernel layers: a second T2 (and overflow-gather
+// scratch) with the fused kernel's tensor maps for both, so forward f + 1's core kernel can
+// run while forward f's fused kernel still reads its T2 (LRS_NO_EARLY=1: off).
+static lrs_status setup_early(lrs_conv* h, const lrs_conv_desc* d) {
+  if (!h->use_core || !h->use_w || h->svd || getenv("LRS_NO_EARLY")) return LRS_OK;
+  WconvParams& w = h->wp;
+  const size_t t2_bytes = static_cast<size_t>(d->batch_max) * h->ho * h->wo * h->r2p * h->esz;
+  if (cudaMalloc(&h->t2b, t2_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    h->t2b = nullptr;
+    return LRS_OK;  // no room: keep the single-buffer protocol
+  }
+  h->tmT_par[0] = w.tmT;
+  lrs_status st;
+  const uint64_t bm = static_cast<uint64_t>(d->batch_max), rp = static_cast<uint64_t>(h->r2p);
+  const uint64_t ho = static_cast<uint64_t>(h->ho), wo = static_cast<uint64_t>(h->wo);
+  const uint32_t box[4] = {static_cast<uint32_t>(w.t_kc), static_cast<uint32_t>(w.ipw), static_cast<uint32_t>(w.tbox_w),
+                           static_cast<uint32_t>(w.th)};
+  const uint32_t estr[4] = {1, 1, 1, 1};
+  {
+    uint64_t dims[4] = {rp, bm, wo, ho};
+    uint64_t strides[3] = {ho * wo * rp * 2, rp * 2, wo * rp * 2};
+    if ((st = encode_t(&h->tmT_par[1], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, h->t2b, dims, strides,
+                       const_cast<uint32_t*>(box), const_cast<uint32_t*>(estr), w.sw_t)) != LRS_OK)
+      return st;
+  }
+  if (w.n_gk) {
+    const uint64_t gch = static_cast<uint64_t>(w.g_ch);
+    const size_t gb = bm * ho * wo * gch * 2;
+    LRS_CUDA(cudaMalloc(&h->w_gb, gb));
+    LRS_CUDA(cudaMemset(h->w_gb, 0, gb));
+    h->tmG_par[0] = w.tmG;
+    uint64_t dims[4] = {gch, bm, wo, ho};
+    uint64_t strides[3] = {ho * wo * gch * 2, gch * 2, wo * gch * 2};
+    if ((st = encode_t(&h->tmG_par[1], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, h->w_gb, dims, strides,
+                       const_cast<uint32_t*>(box), const_cast<uint32_t*>(estr), w.sw_t)) != LRS_OK)
+      return st;
+  }
+  h->dbuf = true;
+  return LRS_OK;
+}
+
+// Output range of the library's last forward on each (device, stream): a forward whose X
+// overlaps it must not start before that forward's last kernel completes (early = 0).
+std::mutex g_out_mu;
+std::map<std::pair<int, cudaStream_t>, std::pair<uintptr_t, uintptr_t>> g_last_out;
+
+bool x_after_previous_output(int dev, cudaStream_t s, const void* x, size_t xbytes) {
+  std::lock_guard<std::mutex> lk(g_out_mu);
+  auto it = g_last_out.find({dev, s});
+  if (it == g_last_out.end()) return false;
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(x), hi = lo + xbytes;
+  return lo < it->second.second && it->second.first < hi;
+}
+
+void record_output(int dev, cudaStream_t s, const void* y, size_t ybytes) {
+  std::lock_guard<std::mutex> lk(g_out_mu);
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(y);
+  g_last_out[{dev, s}] = {lo, lo + ybytes};
+}
+
 // Time the best few core plans on the device (after every kernel is built): for the
 // full grid and, when the expansion + sparse kernel leaves SMs free, for a grid of
 // exactly those SMs -- the two kernels of consecutive forwards are then co-resident and
@@ -2079,6 +2149,7 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
       if (e != cudaSuccess)
         return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
     }
+  if ((st = setup_early(h, d)) != LRS_OK) return cleanup_fail(st);
   if ((st = autotune_core(h, d)) != LRS_OK) return cleanup_fail(st);
   cudaSetDevice(prev);
   *out = h;
@@ -2153,6 +2224,21 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
     }
     c.n = n;
     c.t2 = static_cast<__nv_bfloat16*>(h->t2);
+    c.early = 0;
+    if (h->dbuf) {
+      // this forward's buffers; early start unless X may still be written by the previous
+      // kernel on the stream (the library's last forward there produced it)
+      const int par = h->par;
+      h->par ^= 1;
+      c.t2 = static_cast<__nv_bfloat16*>(par ? h->t2b : h->t2);
+      h->wp.tmT = h->tmT_par[par];
+      if (h->wp.n_gk) {
+        h->wp.tmG = h->tmG_par[par];
+        h->wp.g = static_cast<__nv_bfloat16*>(par ? h->w_gb : h->w_g);
+      }
+      const size_t xbytes = static_cast<size_t>(n) * d.in_h * d.in_w * d.c_in * esz;
+      c.early = x_after_previous_output(h->device, stream, x, xbytes) ? 0 : 1;
+    }
     c.n_tiles = ((n + c.ipt - 1) / c.ipt) * c.bands;
     const unsigned grid = static_cast<unsigned>(std::min(c.n_tiles, h->core_grid));
     cudaEvent_t e1 = nullptr;
@@ -2304,7 +2390,11 @@ lrs_status lrs_conv_forward(const lrs_conv* hc, const void* x, void* y, int32_t 
     return fail(LRS_ERR_INVALID_ARGUMENT, "x / y must be 16-byte aligned");
   DeviceGuard g;
   LRS_CUDA(g.enter(h->device));
-  return forward_impl(h, x, y, n, static_cast<cudaStream_t>(stream_));
+  const lrs_status st = forward_impl(h, x, y, n, static_cast<cudaStream_t>(stream_));
+  if (st == LRS_OK)
+    record_output(h->device, static_cast<cudaStream_t>(stream_), y,
+                  static_cast<size_t>(n) * h->ho * h->wo * h->d.c_out * h->esz);
+  return st;
 }
 
 lrs_status lrs_conv_forward_host(lrs_conv* h, const void* x_host, void* y_host, int32_t n, void* stream_) {
@@ -2375,7 +2465,7 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
-                  h->w_as, h->w_e, h->w_res, h->w_dense_img, h->w_gtab, h->w_g, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc,
+                  h->w_as, h->w_e, h->w_res, h->w_dense_img, h->w_gtab, h->w_g, h->t2b, h->w_gb, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc,
                   h->sp_uo, h->epi, h->pw_w, h->pw_e, h->pw_tab, h->pw_u};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -2537,7 +2627,7 @@ lrs_status lrs_conv_debug_buffer(const lrs_conv* h, int32_t which, const void** 
     *ptr = h->t1;
     *ld = h->r1p;
   } else if (which == 1) {
-    *ptr = h->t2;
+    *ptr = (h->dbuf && h->par == 0) ? h->t2b : h->t2;  // the buffer the last forward wrote
     *ld = h->r2p;
   } else {
     return fail(LRS_ERR_INVALID_ARGUMENT, "which must be 0 or 1");

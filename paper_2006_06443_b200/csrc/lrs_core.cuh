@@ -79,6 +79,11 @@ struct CoreParams {
   const float* cpb;  // CP core (CPDW kernels): B [kh][R1p], C [kw][R1p] fp32
   const float* cpc;
   unsigned long long* trace;  // optional globaltimer stamps (LRS_WCONV_DEBUG builds, tools/ctrace.py)
+  // 1: start computing at once and wait for the previous kernel only before exiting.  The
+  // host sets it when X is not an output of the library's previous launch on this stream
+  // and T2 alternates between two buffers (lrs_conv.cu forward_impl): the
+  // previous forward's fused kernel may still be reading the other T2.
+  int early;
 };
 
 #ifdef LRS_WCONV_DEBUG
@@ -192,8 +197,11 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       tma_load_2d(smem + p.off_g + j * p.g_slot, &p.tmG, &full_g[j], t * p.r1p + gk * p.g_kc, 0);
     }
   }
-  pdl_wait();  // the previous kernel's output is visible from here on
-  pdl_launch_dependents();  // only after the wait: every kernel before us is then complete
+  // default: wait, then trigger -- when a kernel starts, every kernel before its predecessor
+  // is complete.  early: trigger at once; the wait before exiting keeps the invariant for
+  // whoever waits on this grid (its completion implies the previous kernel's).
+  if (!p.early) pdl_wait();  // the previous kernel's output is visible from here on
+  pdl_launch_dependents();
   CTRACE(p, threadIdx.x == 0 && blockIdx.x == 0, 8190);
 
   if (warp == 0) {
@@ -644,6 +652,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
     tc_fence_after();
     tmem_dealloc(tmem, p.tmem_cols);
   }
+  if (p.early) pdl_wait();
 }
 
 }  // namespace lrs
