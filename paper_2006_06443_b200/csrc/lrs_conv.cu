@@ -658,6 +658,19 @@ static bool core_layout(const CoreGeom& G, int ipt, int th, CoreParams& q, int g
     }
   }
   q.g_res = q.ns_g == G.n_g ? 1 : 0;
+  q.unified = 0;
+  q.gpk = 0;
+  if (!q.g_res && G.n_g > 0 && G.g_slot <= q.x_slot && !getenv("LRS_CORE_SPLIT_RING")) {
+    // streamed G: one ring for X and G items (lrs_core.cuh CoreParams::unified); its slots
+    // are X slots, a G item packs as many chunks as one holds
+    const int ns_u = std::min<int>(kCMaxX, static_cast<int>(left / q.x_slot));
+    if (ns_u >= 2) {
+      q.unified = 1;
+      q.gpk = static_cast<int>(q.x_slot / G.g_slot);
+      q.ns_x = ns_u;
+      q.ns_g = 0;
+    }
+  }
   q.off_g = static_cast<uint32_t>(q.ns_x) * q.x_slot + x_tail;
   q.off_t1 = q.off_g + static_cast<uint32_t>(q.ns_g) * G.g_slot;
   q.off_bar = q.off_t1 + t1_bytes;
@@ -726,9 +739,9 @@ static void apply_core_plan(lrs_conv* h, const lrs_conv_desc* d, int ipt, int th
   if (getenv("LRS_VERBOSE"))
     fprintf(stderr,
             "[lrs] core: th=%d ipt=%d bands=%d wr=%d wc=%d nb1=%d nb2=%d acc=%u nacc=%d ns_x=%d ns_g=%d g_res=%d "
-            "t1_sw128=%d t1_rows=%u smem=%u grid<=%d\n",
-            th, ipt, c.bands, c.wr, G.wc, c.nb1, c.nb2, c.acc_cols, c.nacc, c.ns_x, c.ns_g, c.g_res, c.t1_sw128,
-            c.t1_rows, h->core_smem, h->core_grid);
+            "unified=%d gpk=%d t1_sw128=%d t1_rows=%u smem=%u grid<=%d\n",
+            th, ipt, c.bands, c.wr, G.wc, c.nb1, c.nb2, c.acc_cols, c.nacc, c.ns_x, c.ns_g, c.g_res, c.unified, c.gpk,
+            c.t1_sw128, c.t1_rows, h->core_smem, h->core_grid);
 }
 
 lrs_status build_core(lrs_conv* h, const lrs_conv_desc* d) {

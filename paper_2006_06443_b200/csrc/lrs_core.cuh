@@ -68,6 +68,10 @@ struct CoreParams {
   uint32_t x_slot, g_slot;  // ring slot strides
   int ns_x, ns_g;
   int g_res;             // 1: every G chunk has its own slot, loaded once per CTA
+  int unified;           // 1 (streamed G): ONE ring of ns_x slots of x_slot bytes holds the X items
+                         // (box + U_in chunk) AND the G items (gpk chunks each), in consumption
+                         // order -- a2's G stream gets the X ring's bytes in flight (no G ring)
+  int gpk;               // G chunks per unified-ring item (x_slot / g_slot)
   int t1_sw128;          // 1: T1 window K-major SW128 (R1p % 64 == 0), 0: SWIZZLE_NONE
   uint32_t t1_rows;      // rows of the T1 window (multiple of 8)
   uint32_t acc_cols;     // TMEM columns per buffer: max(nb1 * R1p, nb2 * R2p)
@@ -163,6 +167,8 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
     prm[28] = static_cast<int>(p.wc);
     prm[29] = static_cast<int>(p.x_bytes);
     prm[30] = static_cast<int>(p.x_slot);
+    prm[31] = p.unified;
+    prm[32] = p.gpk;
     for (int i = 0; i < p.ns_x; ++i) {
       mbar_init(&full_x[i], 1);
       mbar_init(&empty_x[i], 1);
@@ -226,6 +232,8 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
     const uint32_t u_off_ = static_cast<uint32_t>(smem_param(prm + 27));
     const uint32_t x_bytes_ = static_cast<uint32_t>(smem_param(prm + 29));
     const uint32_t x_slot_ = static_cast<uint32_t>(smem_param(prm + 30));
+    const int unified_ = smem_param(prm + 31);
+    const int gpk_ = smem_param(prm + 32);
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
       // Requests follow the MMA thread's consumption order (a1(k+1) before a2(k) when two
@@ -254,6 +262,19 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
       };
       auto load_g = [&]() {
         if (g_res_) return;
+        if (unified_) {  // G items of gpk chunks in the unified ring, after the X items
+          for (int j0 = 0; j0 < n_g; j0 += gpk_, ++ix) {
+            const int s = ix % ns_x_;
+            if (ix >= ns_x_) mbar_wait(&empty_x[s], ((ix / ns_x_) - 1) & 1);
+            const int cnt = min(gpk_, n_g - j0);
+            mbar_arrive_expect_tx(&full_x[s], static_cast<uint32_t>(cnt) * g_bytes_);
+            for (int q = 0; q < cnt; ++q) {
+              const int j = j0 + q, t = j / n_gk_, gk = j - t * n_gk_;
+              tma_load_2d(smem + s * x_slot_ + q * g_slot_, &p.tmG, &full_x[s], t * r1p_ + gk * g_kc_, 0);
+            }
+          }
+          return;
+        }
         for (int j = 0; j < n_g; ++j, ++ig) {
           const int s = ig % ns_g_;
           if (ig >= ns_g_) mbar_wait(&empty_g[s], ((ig / ns_g_) - 1) & 1);
@@ -299,6 +320,8 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
     const uint32_t u_off_ = static_cast<uint32_t>(smem_param(prm + 27));
     const int wc_ = static_cast<int>(smem_param(prm + 28));
     const uint32_t x_slot_ = static_cast<uint32_t>(smem_param(prm + 30));
+    const int unified_ = smem_param(prm + 31);
+    const int gpk_ = smem_param(prm + 32);
     // -------------------------------------------------------------- MMA issuer
     // ONE elected thread runs the whole loop (its mbarrier waits included): an elect +
     // reconvergence per item costs ~240 cycles of issue (tools/mma_seq.cu: 108 vs 48
@@ -399,6 +422,39 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
               aj += a_gs;
             }
           }
+        }
+      } else if (unified_) {
+        // streamed G through the unified ring: gpk chunks per item, one commit per item
+        const uint64_t gu0 = umma_desc(base, sw_g_);
+        uint32_t aj = 0;
+        int gk = 0, tx = 0;
+        for (int j0 = 0; j0 < n_g; j0 += gpk_, ++ix) {
+          const int s = ix % ns_x_;
+          mbar_wait(&full_x[s], static_cast<uint32_t>((ix / ns_x_) & 1));
+          tc_fence_after();
+          const int cnt = min(gpk_, n_g - j0);
+          for (int q = 0; q < cnt; ++q) {
+            const int j = j0 + q;
+            const uint64_t bj = gu0 + ((static_cast<uint32_t>(s) * x_slot_ + static_cast<uint32_t>(q) * g_slot_) >> 4);
+            uint64_t ab = t1d0 + aj;
+            uint32_t d = t2c;
+            for (int b2 = 0; b2 < nb2_; ++b2, ab += a_b2, d += static_cast<uint32_t>(r2p_)) {
+#pragma unroll
+              for (int kk = 0; kk < GS; ++kk)
+                mma_bf16(d, ab + kk * a_ks, bj + 2 * kk, idesc2, (j > 0 || kk > 0) ? 1u : 0u);
+            }
+            if (++gk == n_gk_) {
+              gk = 0;
+              aj += a_tap;
+              if (++tx == kw_) {
+                tx = 0;
+                aj += a_row;
+              }
+            } else {
+              aj += a_gs;
+            }
+          }
+          mma_commit(&empty_x[s]);
         }
       } else {
         uint32_t aj = 0;
