@@ -1425,7 +1425,8 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
   // leave a ring of ~1 tile, so every tile's X loads wait for the previous tile's MMAs;
   // profiles/r02_ablate_pwf_c4.log), so it is a plan option: LRS_PW_FT=1
   const bool ft_ok = r1p % 32 == 0 && r1p <= 256 && getenv("LRS_PW_FT") && atoi(getenv("LRS_PW_FT")) == 1;
-  struct Plan { int mpc = 0, bp = 0, ns = 0, nblk = 0, gpg = 0, ft = 0, epi_nbuf = 2; uint32_t smem = 0, w_bytes = 0; double cost = 1e300; };
+  struct Plan { int mpc = 0, bp = 0, ns = 0, nblk = 0, gpg = 0, ft = 0, epi_nbuf = 2, cpi = 1; uint32_t smem = 0, w_bytes = 0; double cost = 1e300; };
+  const int cpi_env = getenv("LRS_PW_CPI") ? atoi(getenv("LRS_PW_CPI")) : 0;  // plan override
   Plan best;
   for (int ft = ft_ok ? 1 : 0; ft >= 0 && !best.mpc; --ft) {
   for (int mpc = std::min(kPMaxMpc, n_mt); mpc >= 1; --mpc) {
@@ -1445,7 +1446,9 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
         nblk = std::max(nblk, nb);
       }
     for (int bp : {128, 96, 64}) {  // multiples of 32: the epilogue stores 32-position TMA boxes
+    for (int cpi : {4, 2, 1}) {     // chunks per ring item (one hand-off each)
       if ((bp_env && bp != bp_env) || (ft && bp != 128)) continue;
+      if ((cpi_env && cpi != cpi_env) || (ft && cpi != 1) || (cpi > 1 && cpi > std::max(n_x, n_tk))) continue;
       const uint32_t acc = static_cast<uint32_t>(mpc * bp);
       // TMEM: two accumulator sets (+ two T1 accumulators when fused) and the metadata
       const uint32_t t1cols = ft ? 2u * static_cast<uint32_t>(r1p) : 0u;
@@ -1453,7 +1456,7 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
       const uint32_t dense = static_cast<uint32_t>(mpc * n_tk) * 128u * sw_t;
       const uint32_t w_bytes = dense + static_cast<uint32_t>(nblk) * 8192u;
       const uint32_t e_bytes = static_cast<uint32_t>(nblk) * 2048u;
-      const uint32_t slot = static_cast<uint32_t>(bp) * 128u;
+      const uint32_t slot = static_cast<uint32_t>(cpi * bp) * 128u;
       const uint32_t u_bytes = ft ? static_cast<uint32_t>(n_ck * r1p) * 128u : 0u;
       const uint32_t t1s = ft ? 2u * 128u * static_cast<uint32_t>(r1p) * 2u : 0u;
       // (fused: the metadata staging shares the second T1 tile, first written after the copy)
@@ -1479,7 +1482,7 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
       // producer lanes request a tile's chunks in parallel, so the ring must hold a whole
       // tile: with fewer slots two lanes would wait on two phases of one slot's mbarrier at
       // once, and a parity wait cannot tell phase r from phase r + 2
-      const int nq = ft ? n_ck : n_x + n_tk;
+      const int nq = ft ? n_ck : (n_x + cpi - 1) / cpi + (n_tk + cpi - 1) / cpi;  // ring items per tile
       if (ns < nq) continue;
       // cost (cycles per CTA): tiles x max(MMA, operand inflow, the group's share of the HBM
       // write of Y); sparse MMA ~ (A 4 KB + B bp*64 B) / 128 B/clk, dense ~ (4 KB + bp*32 B) / 128
@@ -1491,13 +1494,17 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
       const double in = (static_cast<double>(n_x) * bp * 128 + n_tk * bp * sw_t) / 60.0;
       const double out = static_cast<double>(bp) * mpc * 128 * 2 * (G * gpg) / 3300.0;  // ~3.3 KB/clk of HBM writes
       const double shallow = ns < nq + 2 ? 1.25 : 1.0;
-      const double cost = static_cast<double>(tiles) * std::max(mma, std::max(in, out)) * shallow + 400.0 * mpc;
+      // + the MMA thread's serial hand-off per ring item (wait ~160 + commit ~50 + loop:
+      // ~500 cycles measured, tools/loop_cost3.cu, tools/ptrace.py)
+      const double cost =
+          static_cast<double>(tiles) * std::max(mma + 500.0 * nq, std::max(in, out)) * shallow + 400.0 * mpc;
       if (cost < best.cost) {
         best.cost = cost; best.mpc = mpc; best.bp = bp; best.ns = ns; best.nblk = nblk; best.gpg = gpg;
-        best.w_bytes = w_bytes; best.ft = ft; best.epi_nbuf = epi_nbuf;
+        best.w_bytes = w_bytes; best.ft = ft; best.epi_nbuf = epi_nbuf; best.cpi = cpi;
         best.smem = fixed + static_cast<uint32_t>(ns) * slot;
       }
     }
+    }  // cpi
   }
   }  // ft
   if (!best.mpc) return LRS_OK;
@@ -1582,7 +1589,8 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
   q.dense_bytes = dense;
   q.nblk_max = nblk;
   q.ns = best.ns;
-  q.slot_bytes = static_cast<uint32_t>(best.bp) * 128u;
+  q.cpi = best.cpi;
+  q.slot_bytes = static_cast<uint32_t>(best.cpi * best.bp) * 128u;
   q.acc_cols = static_cast<uint32_t>(mpc * best.bp);
   if (best.ft) {
     q.r1p = r1p;
@@ -1623,8 +1631,8 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
   h->use_pw = true;
   h->pw_ft = best.ft != 0;
   if (getenv("LRS_VERBOSE"))
-    fprintf(stderr, "[lrs] pw plan: fused a1 %d mpc %d groups %d bp %d ns %d epi bufs %d blocks/group %d ctas/group %d smem %u B\n",
-            best.ft, mpc, G, best.bp, best.ns, best.epi_nbuf, nblk, best.gpg, best.smem);
+    fprintf(stderr, "[lrs] pw plan: fused a1 %d mpc %d groups %d bp %d ns %d cpi %d epi bufs %d blocks/group %d ctas/group %d smem %u B\n",
+            best.ft, mpc, G, best.bp, best.ns, best.cpi, best.epi_nbuf, nblk, best.gpg, best.smem);
   return LRS_OK;
 }
 }  // namespace

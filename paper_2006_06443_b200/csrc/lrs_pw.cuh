@@ -57,7 +57,10 @@ struct PwParams {
   uint32_t dense_bytes;    // its V^T part (2:4 blocks follow)
   int nblk_max;            // most 2:4 blocks of any group (E staging, TMEM columns)
   int ns;                  // ring slots
-  uint32_t slot_bytes;
+  int cpi;                 // chunks per ring item: a slot holds cpi X (or T1) chunks of bp x 128 B, one
+                           // mbarrier hand-off and one tcgen05.commit per item (~500 cycles of the
+                           // MMA thread's serial loop per hand-off bounded C4's tile rate)
+  uint32_t slot_bytes;     // one item slot (cpi * bp * 128)
   uint32_t acc_cols;       // TMEM columns of one accumulator set (mpc * bp)
   uint32_t e_col0;         // first metadata column (2 * acc_cols)
   uint32_t off_e, off_ring, off_epi, off_tab, off_bar;
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
     prm[5] = static_cast<int>(p.slot_bytes); prm[6] = static_cast<int>(p.sw_t); prm[7] = static_cast<int>(p.acc_cols);
     prm[8] = p.t_kc; prm[9] = static_cast<int>(p.e_col0); prm[10] = p.relu; prm[11] = p.cout; prm[12] = p.P;
     prm[13] = li; prm[14] = gctas; prm[15] = static_cast<int>(p.off_ring); prm[16] = static_cast<int>(p.dense_bytes);
-    prm[17] = p.e_slot0; prm[18] = p.epi_nbuf;
+    prm[17] = p.e_slot0; prm[18] = p.epi_nbuf; prm[19] = p.cpi;
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -143,7 +146,10 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
   constexpr uint32_t tmem = 0u;
   const int n_pt = smem_param(prm + 0), n_x = smem_param(prm + 1), n_tk = smem_param(prm + 2);
   const int ns = smem_param(prm + 3), bp = smem_param(prm + 4);
-  const int nq = n_x + n_tk;
+  const int cpi = smem_param(prm + 19);
+  const int nxi = (n_x + cpi - 1) / cpi, nti = (n_tk + cpi - 1) / cpi;  // X / T1 items per tile
+  const int nq = nxi + nti;                                             // items per tile
+  const uint32_t chunk_bytes = static_cast<uint32_t>(bp) * 128u;        // a chunk's place in its item slot
   const int li_ = smem_param(prm + 13), gct = smem_param(prm + 14);
   const uint32_t slot_bytes = smem_param(prm + 5), sw_t = smem_param(prm + 6), acc_cols = smem_param(prm + 7);
 
@@ -167,19 +173,21 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
     // item it = round * ns + slot, tracked incrementally (no divisions): lane l < n_x owns
     // the X chunk l of every tile (item k * nq + l), lane 0 also the T1 chunks
     int xs = lane, xr = 0;       // this lane's X item
-    int ts = n_x, tr = 0;        // lane 0's first T1 item of the tile
+    int ts = nxi, tr = 0;        // lane 0's first T1 item of the tile
     while (xs >= ns) { xs -= ns; ++xr; }  // (a tile may hold more chunks than the ring has slots)
     while (ts >= ns) { ts -= ns; ++tr; }
     for (int pt = li_; pt < n_pt; pt += gct) {
       const int p0 = pt * bp;
-      if (lane < n_x) {
+      if (lane < nxi) {
         if (xr > 0) mbar_wait(&empty[xs], (xr - 1) & 1);
         else if (xs >= e_slot0) mbar_wait(e_done, 0);  // the slot still holds metadata staging
+        const int c0 = lane * cpi, cn = min(cpi, n_x - c0);
         if (LRS_XDBG(p.dbg & 4)) {
           mbar_arrive(&full[xs]);
         } else {
-          mbar_arrive_expect_tx(&full[xs], static_cast<uint32_t>(bp) * 128u);
-          tma_load_2d_s(ring + xs * slot_bytes, &p.tmX, &full[xs], lane * 64, p0);
+          mbar_arrive_expect_tx(&full[xs], static_cast<uint32_t>(cn * bp) * 128u);
+          for (int j = 0; j < cn; ++j)
+            tma_load_2d_s(ring + xs * slot_bytes + j * chunk_bytes, &p.tmX, &full[xs], (c0 + j) * 64, p0);
         }
         xs += nq;
         while (xs >= ns) { xs -= ns; ++xr; }
@@ -187,7 +195,7 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
       __syncwarp();
       if (lane == 0) {
         int s = ts, r = tr;
-        for (int tk = 0; tk < n_tk; ++tk) {
+        for (int ti = 0; ti < nti; ++ti) {
           if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
           else if (s >= e_slot0) mbar_wait(e_done, 0);
           if (!waited) {  // T1 is the previous kernel's output
@@ -195,11 +203,13 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
             pdl_launch_dependents();
             waited = true;
           }
+          const int t0 = ti * cpi, tn = min(cpi, n_tk - t0);
           if (LRS_XDBG(p.dbg & 4)) {
             mbar_arrive(&full[s]);
           } else {
-            mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(bp) * sw_t);
-            tma_load_2d_s(ring + s * slot_bytes, &p.tmT, &full[s], tk * t_kc, p0);
+            mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(tn * bp) * sw_t);
+            for (int j = 0; j < tn; ++j)
+              tma_load_2d_s(ring + s * slot_bytes + j * chunk_bytes, &p.tmT, &full[s], (t0 + j) * t_kc, p0);
           }
           if (++s == ns) { s = 0; ++r; }
         }
@@ -251,32 +261,38 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
           tc_fence_after();
           PTRACE(p, 2000 + k * nq + q);
           if (LRS_XDBG(p.dbg & 2)) {
-          } else if (q < n_x) {
-            const uint64_t bd = ring0 + slot * slot16;
+          } else if (q < nxi) {
+            const int c0 = q * cpi, cn = min(cpi, n_x - c0);
+            for (int j = 0; j < cn; ++j) {
+              const uint64_t bd = ring0 + slot * slot16 + static_cast<uint32_t>(j) * (chunk_bytes >> 4);
 #pragma unroll
-            for (int m = 0; m < MPC; ++m) {
-              const uint32_t e = tab_s[m * kPMaxCk + q];
-              const int b0 = static_cast<int>(e & 0xFFFu), nb = static_cast<int>(e >> 12);
-              for (int bi = 0; bi < nb; ++bi) {
-                const uint64_t ad = a_sp0 + static_cast<uint32_t>(b0 + bi) * (8192u >> 4);
-                const uint32_t et = tmem + e_col0 + 4u * static_cast<uint32_t>(b0 + bi);
+              for (int m = 0; m < MPC; ++m) {
+                const uint32_t e = tab_s[m * kPMaxCk + c0 + j];
+                const int b0 = static_cast<int>(e & 0xFFFu), nb = static_cast<int>(e >> 12);
+                for (int bi = 0; bi < nb; ++bi) {
+                  const uint64_t ad = a_sp0 + static_cast<uint32_t>(b0 + bi) * (8192u >> 4);
+                  const uint32_t et = tmem + e_col0 + 4u * static_cast<uint32_t>(b0 + bi);
 #pragma unroll
-                for (int s2 = 0; s2 < 2; ++s2) {
-                  mma_sp_bf16(acc0 + static_cast<uint32_t>(m * bp), ad + 2 * s2, bd + 4 * s2,
-                              ids | static_cast<uint32_t>(s2), (started >> m) & 1u, et);
-                  started |= 1u << m;
+                  for (int s2 = 0; s2 < 2; ++s2) {
+                    mma_sp_bf16(acc0 + static_cast<uint32_t>(m * bp), ad + 2 * s2, bd + 4 * s2,
+                                ids | static_cast<uint32_t>(s2), (started >> m) & 1u, et);
+                    started |= 1u << m;
+                  }
                 }
               }
             }
           } else {
-            const int tk = q - n_x;
-            const uint64_t bd = ringt0 + slot * slot16;
+            const int t0 = (q - nxi) * cpi, tn = min(cpi, n_tk - t0);
+            for (int j = 0; j < tn; ++j) {
+              const int tk = t0 + j;
+              const uint64_t bd = ringt0 + slot * slot16 + static_cast<uint32_t>(j) * (chunk_bytes >> 4);
 #pragma unroll
-            for (int m = 0; m < MPC; ++m) {
-              const uint64_t ad = a_dense0 + static_cast<uint32_t>(m * n_tk + tk) * dblk16;
-              for (int kk = 0; kk < ksteps; ++kk) {
-                mma_bf16(acc0 + static_cast<uint32_t>(m * bp), ad + 2 * kk, bd + 2 * kk, idn, (started >> m) & 1u);
-                started |= 1u << m;
+              for (int m = 0; m < MPC; ++m) {
+                const uint64_t ad = a_dense0 + static_cast<uint32_t>(m * n_tk + tk) * dblk16;
+                for (int kk = 0; kk < ksteps; ++kk) {
+                  mma_bf16(acc0 + static_cast<uint32_t>(m * bp), ad + 2 * kk, bd + 2 * kk, idn, (started >> m) & 1u);
+                  started |= 1u << m;
+                }
               }
             }
           }
@@ -314,10 +330,15 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
       if (threadIdx.x == 64) PTRACE(p, 102 + 4 * k);
       const uint32_t acc0 = static_cast<uint32_t>(b) * acc_cols;
       const int p0 = pt * bp;
+      // the quarter's (M-tile, 32-position) chunks alternate between its two warps over the
+      // whole list (a fixed column parity left one warp 4 chunks and the other 2 at bp = 96)
+      int mv = 0;
+      while (mv < MPC && (grp * MPC + mv) * 128 + q4 * 32 < cout) ++mv;
+      const int cpm = bp / 32;
 #pragma unroll 1
-      for (int m = 0; m < MPC; ++m) {
+      for (int i = ehalf; i < mv * cpm; i += 2, ++nchunk) {
+        const int m = i / cpm, c0 = (i - m * cpm) * 32;
         const int jw = (grp * MPC + m) * 128 + q4 * 32;  // first channel of this warp
-        if (jw >= cout) break;
         float2 sb[2][2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -327,8 +348,7 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
             sb[h][1] = out_epi_load(p.epi, min(jw + 16 * h + t1 + 8, cout - 1));
           }
         }
-#pragma unroll 1
-        for (int c0 = ehalf * 32; c0 < bp; c0 += 64, ++nchunk) {
+        {
           uint32_t r[2][2][8];
 #pragma unroll
           for (int h = 0; h < 2; ++h)

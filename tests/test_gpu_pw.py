@@ -84,9 +84,10 @@ def test_geometries_vs_oracle(geom):
 
 @pytest.mark.parametrize("env", [{"LRS_PW_MPC": "1", "LRS_PW_BP": "128"}, {"LRS_PW_MPC": "1", "LRS_PW_BP": "64"},
                                  {"LRS_PW_MPC": "2", "LRS_PW_BP": "64"}, {"LRS_PW_MPC": "2", "LRS_PW_BP": "96"},
-                                 {"LRS_PW_MPC": "1", "LRS_PW_BP": "96"}])
+                                 {"LRS_PW_MPC": "1", "LRS_PW_BP": "96"}, {"LRS_PW_CPI": "1"}, {"LRS_PW_CPI": "2"},
+                                 {"LRS_PW_CPI": "4"}, {"LRS_PW_CPI": "2", "LRS_PW_BP": "96", "LRS_PW_MPC": "2"}])
 def test_plans_bitwise_equal_to_windowed_kernel(env):
-    """Every (M-tiles per CTA, positions per tile) plan, and the windowed fused kernel
+    """Every (M-tiles per CTA, positions per tile, chunks per ring item) plan, and the windowed fused kernel
     (LRS_NO_PW=1), accumulate each output in the same order: bitwise equal."""
     inp = workloads.generate(svd_cfg(3, 14, 14, 256, 1024, 64, 0.01))
     ref = fwd(make(inp, {"LRS_NO_PW": "1", "LRS_WCONV_GATHER": "0"}), inp)
