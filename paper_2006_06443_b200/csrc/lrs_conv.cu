@@ -174,6 +174,13 @@ struct TimingRing {
 
 }  // namespace
 
+// one plan of the channel-stationary 1x1 kernel (build_pw; timed by autotune_pw)
+struct PwPlan {
+  int mpc = 0, bp = 0, ns = 0, nblk = 0, gpg = 0, ft = 0, epi_nbuf = 2, cpi = 1;
+  uint32_t smem = 0, w_bytes = 0;
+  double cost = 1e300;
+};
+
 struct lrs_conv {
   lrs_conv_desc d;
   int device = 0;
@@ -216,6 +223,7 @@ struct lrs_conv {
   PwParams pp{};
   uint32_t pw_smem = 0;
   int pw_grid_per_group = 0;  // CTAs per channel group at most
+  std::vector<PwPlan> pw_cands;  // the cost model's best few plans (autotune_pw times them)
   void* pw_w = nullptr;       // per-group weight images
   void* pw_e = nullptr;       // per-group metadata images
   void* pw_tab = nullptr;     // per-group block tables
@@ -1402,7 +1410,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
 // 1x1 SVD-pair layers (bf16, stride 1, pad 0, c_in % 64 == 0): plan the channel-stationary
 // fused kernel (lrs_pw.cuh), build the per-group weight images, encode nothing per call
 // yet (X / T1 maps depend on n).  Leaves h->use_pw false if the layer does not fit.
-lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
+lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d, const PwPlan* force = nullptr) {
   if (h->f32 || !h->svd || d->c_in % 64 != 0 || getenv("LRS_NO_PW")) return LRS_OK;
   const int cin = d->c_in, cout = d->c_out;
   const int n_ck = cin / 64;
@@ -1425,9 +1433,11 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
   // leave a ring of ~1 tile, so every tile's X loads wait for the previous tile's MMAs;
   // profiles/r02_ablate_pwf_c4.log), so it is a plan option: LRS_PW_FT=1
   const bool ft_ok = r1p % 32 == 0 && r1p <= 256 && getenv("LRS_PW_FT") && atoi(getenv("LRS_PW_FT")) == 1;
-  struct Plan { int mpc = 0, bp = 0, ns = 0, nblk = 0, gpg = 0, ft = 0, epi_nbuf = 2, cpi = 1; uint32_t smem = 0, w_bytes = 0; double cost = 1e300; };
+  using Plan = PwPlan;
   const int cpi_env = getenv("LRS_PW_CPI") ? atoi(getenv("LRS_PW_CPI")) : 0;  // plan override
   Plan best;
+  std::vector<Plan> all;
+  if (force) best = *force;
   for (int ft = ft_ok ? 1 : 0; ft >= 0 && !best.mpc; --ft) {
   for (int mpc = std::min(kPMaxMpc, n_mt); mpc >= 1; --mpc) {
     if (mpc_env && mpc != mpc_env) continue;
@@ -1498,16 +1508,31 @@ lrs_status build_pw(lrs_conv* h, const lrs_conv_desc* d) {
       // ~500 cycles measured, tools/loop_cost3.cu, tools/ptrace.py)
       const double cost =
           static_cast<double>(tiles) * std::max(mma + 500.0 * nq, std::max(in, out)) * shallow + 400.0 * mpc;
-      if (cost < best.cost) {
-        best.cost = cost; best.mpc = mpc; best.bp = bp; best.ns = ns; best.nblk = nblk; best.gpg = gpg;
-        best.w_bytes = w_bytes; best.ft = ft; best.epi_nbuf = epi_nbuf; best.cpi = cpi;
-        best.smem = fixed + static_cast<uint32_t>(ns) * slot;
-      }
+      Plan c;
+      c.cost = cost; c.mpc = mpc; c.bp = bp; c.ns = ns; c.nblk = nblk; c.gpg = gpg;
+      c.w_bytes = w_bytes; c.ft = ft; c.epi_nbuf = epi_nbuf; c.cpi = cpi;
+      c.smem = fixed + static_cast<uint32_t>(ns) * slot;
+      all.push_back(c);
+      if (cost < best.cost) best = c;
     }
     }  // cpi
   }
   }  // ft
   if (!best.mpc) return LRS_OK;
+  if (!force) {  // the best few distinct (mpc, bp, cpi) plans for the create-time timing
+    std::stable_sort(all.begin(), all.end(), [](const Plan& a, const Plan& b) { return a.cost < b.cost; });
+    h->pw_cands.clear();
+    for (const Plan& c : all)
+      if (h->pw_cands.size() < 4) h->pw_cands.push_back(c);
+  }
+  // a re-applied plan (autotune_pw) replaces the previous one's images
+  for (void** b : {&h->pw_w, &h->pw_e, &h->pw_tab, &h->pw_u})
+    if (*b) {
+      cudaFree(*b);
+      *b = nullptr;
+    }
+  h->px_ptr = nullptr;  // tensor-map boxes depend on bp
+  h->py_ptr = nullptr;
   const int mpc = best.mpc, G = (n_mt + mpc - 1) / mpc, nblk = best.nblk;
   // ---- per-group images: [mpc][n_tk] V^T blocks, then the 2:4 blocks; metadata; tables
   std::vector<uint8_t> wimg(static_cast<size_t>(G) * best.w_bytes, 0);
@@ -1804,6 +1829,70 @@ static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d) {
   return st;
 }
 
+// Time the pointwise kernel's best few plans (build_pw's cost-model candidates) on the
+// device like autotune_core and keep the fastest: the model's tile-rate terms were off by
+// up to 15 % between neighbouring plans at C4 (profiles/r02_ablate_pw_cpi_c4.log).  Every
+// plan computes the same bits (tests/test_gpu_pw.py).  Any LRS_PW_* override or
+// LRS_NO_AUTOTUNE keeps the model's plan.
+static lrs_status autotune_pw(lrs_conv* h, const lrs_conv_desc* d) {
+  if (!h->use_pw || h->pw_cands.size() < 2 || getenv("LRS_NO_AUTOTUNE") || getenv("LRS_PW_MPC") ||
+      getenv("LRS_PW_BP") || getenv("LRS_PW_CPI") || getenv("LRS_PW_EPIBUF") || getenv("LRS_PW_FT") || h->skip)
+    return LRS_OK;
+  const int n = d->batch_max;
+  const size_t xb = static_cast<size_t>(n) * d->in_h * d->in_w * d->c_in * 2;
+  const size_t yb = static_cast<size_t>(n) * h->ho * h->wo * d->c_out * 2;
+  void *xs = nullptr, *ys = nullptr;
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  lrs_status st = LRS_OK;
+  cudaError_t e = cudaMalloc(&xs, xb);
+  if (e == cudaSuccess) e = cudaMalloc(&ys, yb);
+  if (e == cudaErrorMemoryAllocation) {  // no room for the scratch: keep the model's plan
+    cudaGetLastError();
+    if (xs) cudaFree(xs);
+    return LRS_OK;
+  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&e0);
+  if (e == cudaSuccess) e = cudaEventCreate(&e1);
+  if (e == cudaSuccess) e = cudaMemsetAsync(xs, 0, xb, s);
+  if (e != cudaSuccess) st = fail(LRS_ERR_CUDA, "autotune setup: %s", cudaGetErrorString(e));
+  const std::vector<PwPlan> cands = h->pw_cands;
+  float best = 1e30f;
+  int bi = -1;
+  for (size_t i = 0; st == LRS_OK && i < cands.size(); ++i) {
+    if ((st = build_pw(h, d, &cands[i])) != LRS_OK) break;
+    h->pp.epi = h->epi;
+    h->pp.relu = d->out_relu ? 1 : 0;
+    for (int r = 0; r < 3 && st == LRS_OK; ++r) st = lrs_conv_forward(h, xs, ys, n, s);
+    if (st != LRS_OK) break;
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < 10 && st == LRS_OK; ++r) st = lrs_conv_forward(h, xs, ys, n, s);
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) != cudaSuccess) st = fail(LRS_ERR_CUDA, "autotune: %s", cudaGetErrorString(cudaGetLastError()));
+    float ms = 0.f;
+    if (st == LRS_OK) cudaEventElapsedTime(&ms, e0, e1);
+    if (getenv("LRS_VERBOSE"))
+      fprintf(stderr, "[lrs] autotune pw mpc=%d bp=%d cpi=%d: %.2f us/forward\n", cands[i].mpc, cands[i].bp,
+              cands[i].cpi, ms * 100.f);
+    if (st == LRS_OK && ms < best) {
+      best = ms;
+      bi = static_cast<int>(i);
+    }
+  }
+  if (st == LRS_OK && bi >= 0 && (st = build_pw(h, d, &cands[bi])) == LRS_OK) {
+    h->pp.epi = h->epi;
+    h->pp.relu = d->out_relu ? 1 : 0;
+  }
+  if (s) cudaStreamSynchronize(s);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (s) cudaStreamDestroy(s);
+  if (xs) cudaFree(xs);
+  if (ys) cudaFree(ys);
+  return st;
+}
+
 lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   if (!out) return fail(LRS_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
@@ -1850,7 +1939,9 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
   // ranks padded to the MMA granularity; a rank consumed as the K of a TMEM-window
   // operand (T2, or T1 of the SVD pair) is padded to 16, 32 or a multiple of 64
   auto t_round = [](int r) { return r <= 16 ? 16 : (r <= 32 ? 32 : round_up(r, 64)); };
-  const bool bf16_w = !f32 && cin % 64 == 0;
+  // LRS_NO_SPTC: no 2:4 sparse tensor-core kernels -- bf16 layers take engine 0 (the a3 GEMM
+  // with the SIMT CSR sparse term in its epilogue), the head-to-head of DESIGN §5
+  const bool bf16_w = !f32 && cin % 64 == 0 && !getenv("LRS_NO_SPTC");
   h->r1p = (bf16_w && h->svd) ? t_round(r1) : round_up(r1, 16);
   h->r2p = h->svd ? h->r1p : (bf16_w ? t_round(r2) : round_up(r2, 16));
   if (h->cp_core) h->r1p = h->r2p = std::max(h->r1p, h->r2p);  // T1 and T2 share one row pitch
@@ -2172,6 +2263,7 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     }
   if ((st = setup_early(h, d)) != LRS_OK) return cleanup_fail(st);
   if ((st = autotune_core(h, d)) != LRS_OK) return cleanup_fail(st);
+  if ((st = autotune_pw(h, d)) != LRS_OK) return cleanup_fail(st);
   cudaSetDevice(prev);
   *out = h;
   return LRS_OK;

@@ -152,3 +152,13 @@ def test_output_epilogue_and_partial_batch():
     ref = O.output_epilogue(oracle(inp), scale, bias, relu=True)
     parity.check(y, ref, "bf16")
     assert (y.float() >= 0).all()
+
+
+def test_autotuned_plan_bitwise_equal_model_plan():
+    """autotune_pw (create-time timing of the cost model's best plans) only picks among plans
+    that accumulate in the same order: bitwise equal to the model's own choice."""
+    inp = workloads.generate(svd_cfg(16, 14, 14, 256, 1024, 64, 0.01, seed=5))
+    tuned = make(inp)
+    model = make(inp, {"LRS_NO_AUTOTUNE": "1"})
+    assert tuned.expand_kernel == 2 and model.expand_kernel == 2
+    assert torch.equal(fwd(tuned, inp), fwd(model, inp))

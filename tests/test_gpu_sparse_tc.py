@@ -224,3 +224,23 @@ def test_c3_takes_the_overflow_gather():
     y = layer(x)
     torch.cuda.synchronize()
     parity.check(y, oracle(inp), "bf16")
+
+
+@pytest.mark.parametrize("name", ["c2_bf16", "c4", "c3"])
+def test_simt_csr_engine_matches_oracle(name):
+    """LRS_NO_SPTC=1: the same bf16 layer on engine 0 (tensor-core a3 GEMM with the SIMT CSR
+    sparse term in its epilogue, no 2:4 blocks) -- the head-to-head arm of DESIGN §5 --
+    against the fp64 oracle, and against the 2:4 engine within the bf16 bar."""
+    import os
+    from paper_2006_06443_b200 import LrsConv
+    inp = workloads.generate(workloads.CONFIGS[name], batch=8)
+    os.environ["LRS_NO_SPTC"] = "1"
+    try:
+        simt = LrsConv.from_inputs(inp, batch_max=8)
+    finally:
+        os.environ.pop("LRS_NO_SPTC", None)
+    assert simt.sparse_engine[0] == 0 and simt.expand_kernel == 0
+    x = torch.from_numpy(inp.x).to(torch.bfloat16).cuda()
+    y = simt(x)
+    torch.cuda.synchronize()
+    parity.check(y, oracle(inp), "bf16")

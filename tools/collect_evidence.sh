@@ -1,0 +1,18 @@
+# Copy one evidence call's outputs (tools/gpu/r02_w*.sh) into profiles/ under the round's names:
+#   bash tools/collect_evidence.sh gpurun_out/r02w2
+set -e
+O=$1
+cp $O/pytest_gpu.log profiles/r02_pytest_gpu.log
+cp $O/smoke.log profiles/r02_smoke.log
+cp $O/launches_c3.csv profiles/r02_ncu_launches_c3.csv
+for f in $O/bench_*.json; do
+  b=$(basename $f .json)
+  [ "$b" = "bench_small" ] && continue
+  cp $f profiles/r02_$b.json
+done
+for r in $O/prof_*.ncu-rep; do
+  b=$(basename $r .ncu-rep); b=${b#prof_}
+  python tools/ncu_sum.py $r > profiles/r02_ncu_${b}_summary.txt
+  python tools/ncu_src.py $r 25 > profiles/r02_ncu_${b}_top_sass.txt
+done
+python tools/ncu_traffic.py $O

@@ -1,7 +1,7 @@
 """Write profiles/ncu_traffic.json: DRAM bytes (read + write) per launch of each config's
 dominant kernel, from the committed `ncu --set full` captures (bench.py reports them as
-roofline.traffic).  usage: python tools/ncu_traffic.py"""
-import csv, json, os, subprocess
+roofline.traffic).  usage: python tools/ncu_traffic.py [evidence dir under gpurun_out/, default r02v]"""
+import csv, json, os, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REPS = {  # config -> (report under gpurun_out/, kernel, round tag)
@@ -16,8 +16,9 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 def main():
     out = {}
+    src = sys.argv[1].rstrip("/").split("/")[-1] if len(sys.argv) > 1 else "r02v"
     for cfg, (rep, kern, tag) in REPS.items():
-        path = os.path.join(ROOT, "gpurun_out", rep)
+        path = os.path.join(ROOT, "gpurun_out", rep.replace("r02v/", src + "/"))
         if not os.path.exists(path):
             continue
         txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
