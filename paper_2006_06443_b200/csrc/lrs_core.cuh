@@ -79,7 +79,8 @@ struct CoreParams {
   uint32_t tmem_cols;
   uint32_t off_g, off_t1, off_bar;
   int dbg;           // experiment bits (LRS_CORE_DBG): 1 skip the depthwise loop, 2 skip its T2 stores,
-                     // 4 skip the X / U loads (timing only)
+                     // 4 skip the X / U loads, 8 skip the T2 stores, 16 skip the T1 restage stores
+                     // (timing only)
   const float* cpb;  // CP core (CPDW kernels): B [kh][R1p], C [kw][R1p] fp32
   const float* cpc;
   unsigned long long* trace;  // optional globaltimer stamps (LRS_WCONV_DEBUG builds, tools/ctrace.py)
@@ -546,7 +547,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
           for (int i = 0; i < 4; ++i)
             if (cg + 32 * i < p.r1p) tmem_ld16_nowait(acc0 + static_cast<uint32_t>(b1 * p.r1p + cg + 32 * i), v[i]);
           tmem_ld_wait();
-          if (row >= p.t1_rows) continue;
+          if (row >= p.t1_rows || LRS_XDBG(p.dbg & 16)) continue;  // experiment: skip the restage stores
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             if (cg + 32 * i >= p.r1p) break;
@@ -661,7 +662,7 @@ __global__ void __launch_bounds__(kCThreads, 1) lrs_core_kernel(const __grid_con
           for (int i = 0; i < 4; ++i)
             if (cg + 32 * i < p.r2p) tmem_ld16_nowait(acc0 + static_cast<uint32_t>(b2 * p.r2p + cg + 32 * i), v[i]);
           tmem_ld_wait();
-          if (!ok) continue;
+          if (!ok || LRS_XDBG(p.dbg & 8)) continue;  // experiment: skip the T2 stores (wrong T2)
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             if (cg + 32 * i >= p.r2p) break;
