@@ -277,6 +277,19 @@ int32_t lrs_conv_expand_kernel(const lrs_conv *h);
 int32_t lrs_conv_overflow_chunks(const lrs_conv *h);
 
 /*
+ * 1 if the windowed tensor-core kernel runs in its CTA-pair form: clusters of two CTAs on
+ * the two SMs of a TPC own two 128-channel M-tiles of the same positions, and one of them
+ * issues tcgen05.mma.cta_group::2 (M = 256) for both, each SM holding half of the activation
+ * window along N -- the 2:4 MMAs then run at the tensor rate instead of the shared-memory
+ * bound of one SM.  Needs an even number of M-tiles, no residual 2:4 blocks
+ * (the overflow gather takes their entries, with the union of the pair's slots) and MMA
+ * units of one width.  Opt-in: LRS_WCONV_PAIR=1 in the environment at create takes it
+ * wherever feasible (exact, tested against the oracle; measured slower than the one-CTA form
+ * at C3).  0 otherwise, -1 for NULL.
+ */
+int32_t lrs_conv_cta_pairs(const lrs_conv *h);
+
+/*
  * 1 if the projection a1 and the core convolution a2 of this layer run as one
  * kernel (bf16 Tucker-2 layers with stride 1 and c_in % 64 == 0: T1 is computed
  * on each tile's input window and kept in shared memory, never written to HBM;

@@ -123,9 +123,16 @@ const void* kernel_ptr(KernelId id) {
 }
 
 // fused TC kernel instantiation for an exact MMA unit count
-const void* wconv_kernel_ptr(int nu, int bpi) {
-#define LRS_WK(U) (bpi == 4 ? reinterpret_cast<const void*>(&lrs_wconv_kernel<U, 4>) \
-                            : reinterpret_cast<const void*>(&lrs_wconv_kernel<U, 2>))
+// (pair: the CTA-pair form, 1 or 2 units)
+const void* wconv_kernel_ptr(int nu, int bpi, bool pair = false) {
+#define LRS_WK(U) (bpi == 4 ? reinterpret_cast<const void*>(&lrs_wconv_kernel<U, 4, false>) \
+                            : reinterpret_cast<const void*>(&lrs_wconv_kernel<U, 2, false>))
+  if (pair) {
+    if (nu == 1) return bpi == 4 ? reinterpret_cast<const void*>(&lrs_wconv_kernel<1, 4, true>)
+                                 : reinterpret_cast<const void*>(&lrs_wconv_kernel<1, 2, true>);
+    return bpi == 4 ? reinterpret_cast<const void*>(&lrs_wconv_kernel<2, 4, true>)
+                    : reinterpret_cast<const void*>(&lrs_wconv_kernel<2, 2, true>);
+  }
   switch (nu) {
     case 1: return LRS_WK(1);
     case 2: return LRS_WK(2);
@@ -437,6 +444,26 @@ cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void* param, size_
   constexpr bool no_pdl = false;
 #endif
   cfg.numAttrs = no_pdl ? 0 : 1;
+  void* args[] = {param};
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+// the same with clusters of 2 CTAs (the windowed kernel's CTA-pair form)
+cudaError_t launch_pdl_pair(const void* fn, dim3 grid, dim3 block, void* param, size_t smem, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
   void* args[] = {param};
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
@@ -1038,6 +1065,42 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   };
   std::vector<Unit> units, best_units;
   int best_th = 0, best_ns = 0, best_tc = 0, best_wc = 0, best_tbw = 0, best_nwb = 2, best_bpi = 2, best_ipw = 8;
+  int best_pair = 0;
+  uint32_t best_margin = 0, best_shift_x = 0, best_shift_t = 0;
+  // ---- S -> exact 2:4 main + residual blocks (bf16 values, RNE), TMEM metadata; the
+  // overflow lists (for the gather form) when any group holds 3+ nonzeros
+  Split24 S24 = split_24(d, n_mt, n_ck, taps);
+  Split24 Gv;
+  if (S24.nres > 0) Gv = split_24(d, n_mt, n_ck, taps, true);
+  // distinct (channel, tap) slots of the overflow entries per group of M-tiles (one M-tile,
+  // or the CTA pair's two: their MMAs share the B operand, so the G slots are the union)
+  auto group_slots = [&](int per) {
+    std::vector<std::vector<std::pair<int, int>>> sl((n_mt + per - 1) / per);
+    if (S24.nres > 0)
+      for (int mt = 0; mt < n_mt; ++mt)
+        for (const Ovf& o : Gv.ovf[mt]) {
+          auto& v = sl[mt / per];
+          if (std::find(v.begin(), v.end(), std::make_pair(o.ch, o.t)) == v.end()) v.emplace_back(o.ch, o.t);
+        }
+    return sl;
+  };
+  const char* gather_env = getenv("LRS_WCONV_GATHER");  // plan override: 0 = residual blocks, 1 = gather
+  const char* pair_env = getenv("LRS_WCONV_PAIR");      // plan override: 0 = never, 1 = whenever feasible
+  const bool pair_force = pair_env && atoi(pair_env) == 1;
+  // the pair form needs identical block streams in both CTAs: no residual blocks (the
+  // overflow gather replaces them, with the union of the pair's slots, <= 256)
+  // (opt-in: exact and at the 2:4 tensor rate in isolation, tools/probe_2cta_rate.cu, but its
+  // item stream measured slower at C3 -- 86.9 vs 55.5 us, profiles/r02_ablate_pair_c3.log -- so
+  // the cost model does not take it unless LRS_WCONV_PAIR=1)
+  bool pair_data = n_mt % 2 == 0 && pair_force && !ering;
+  std::vector<std::vector<std::pair<int, int>>> pair_slots;
+  if (pair_data && S24.nres > 0) {
+    if (gather_env && atoi(gather_env) == 0) pair_data = false;
+    pair_slots = group_slots(2);
+    size_t mx = 0;
+    for (const auto& v : pair_slots) mx = std::max(mx, v.size());
+    if ((mx + t_kc - 1) / t_kc * t_kc > 256) pair_data = false;
+  }
   long long best_cost = 1LL << 60;
   uint32_t best_stride = 0, best_xw = 0, best_tw = 0, best_total = 0, best_acc = 0;
   // chunks per X window: several 64-channel boxes in one window buffer share one
@@ -1055,7 +1118,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   // profiles/r02_ablate_ipw.log -- so 4 is a plan option for LRS_WCONV_IPW=4 only)
   const int ipw_env = getenv("LRS_WCONV_IPW") ? atoi(getenv("LRS_WCONV_IPW")) : 8;  // plan override (tests)
   for (int ipw : {8, 4}) {
-  if (ipw != ipw_env || (ipw == 4 && !s1)) continue;
+  if ((ipw != ipw_env && !pair_data) || (ipw == 4 && !s1)) continue;
   bool found_ipw = false;
   for (int cpw = 8; cpw >= 1 && !found_ipw; cpw /= 2) {
   if (n_ck % cpw || (cpw_env ? cpw != cpw_env : (taps > 1 && cpw != 1))) continue;
@@ -1082,6 +1145,17 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       const int cand[][2] = {{4, 3}, {4, 2}, {2, 4}, {2, 3}, {2, 2}, {1, 6}, {1, 5}, {1, 4}, {1, 3}};
       // (opt-in: measured slower on C4, 49.4 vs 45.7 us -- the window loads are not its bottleneck)
       int want_all = (n_mt > 1 && n_tk + (d->nnz > 0 ? n_ck / cpw : 0) <= kWMaxWin && getenv("LRS_WCONV_REUSE")) ? 1 : 0;
+      // pair: the CTA-pair form (every unit the same N, a multiple of 16, <= 2 units)
+      bool same_n = units.size() <= 2;
+      for (const Unit& u : units) same_n = same_n && u.n == units[0].n && u.n % 16 == 0;
+      for (int pair = 0; pair < 2; ++pair) {
+      if (pair == 0 && ipw != ipw_env) continue;
+      if (pair == 1 && !(pair_data && same_n)) continue;
+      // window margin of the pair's rank 1 (it keeps each window N/2 B rows earlier)
+      const uint32_t x_sbo_b = ipw == 8 ? 1024u * static_cast<uint32_t>(g.sw) : 1024u;
+      const uint32_t p_shift_x = pair ? static_cast<uint32_t>(units[0].n / 16) * x_sbo_b : 0u;
+      const uint32_t p_shift_t = pair ? static_cast<uint32_t>(units[0].n / 2) * sw_t : 0u;
+      const uint32_t margin = align1024(std::max(p_shift_x, p_shift_t));
       for (int pass = 0; pass < 2; ++pass) {
       const bool need_all = pass == 0 && want_all;
       if (pass == 1 && !want_all) break;
@@ -1108,7 +1182,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
                                   static_cast<long long>(cpw - 1) * xw;  // the window's other boxes
         const long long slack_t = std::max(0LL, last_t + 1 - static_cast<long long>(th) * tbw) * ipw * sw_t;
         const uint32_t stride =
-            align1024(static_cast<uint32_t>(std::max<long long>(xw + slack_x, tw + slack_t)));
+            align1024(static_cast<uint32_t>(std::max<long long>(xw + slack_x, tw + slack_t))) + margin;
         // the M-tile's block stream: chunk starts + a tap offset per (main or residual) block
         const uint32_t res_bytes = (static_cast<uint32_t>(n_ck + 1 + 2 * n_ck * taps) * 4u + 127u) & ~127u;
         const uint32_t fixed = ns * (a_slot + e_slot) + 8 * kEpiScratch + res_bytes + 1024 + 1024;
@@ -1128,7 +1202,10 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         // (one tap of a 64-channel chunk: 2 MMA steps per unit) adds ~200; CTAs run in
         // waves of one per SM.
         long long item = 450 / bpi;  // per-block share of the item's hand-off + commit
-        for (const Unit& u : units) item += 2 * std::max<long long>(100, (4096 + 64LL * u.n) / 128);
+        // (pair: ~N/2 cycles per MMA -- the 2:4 tensor rate, B split between the two SMs'
+        // shared memories, tools/probe_2cta_rate.cu)
+        for (const Unit& u : units)
+          item += 2 * (pair ? std::max<long long>(50, u.n / 2) : std::max<long long>(100, (4096 + 64LL * u.n) / 128));
         const long long ctas = static_cast<long long>((d->batch_max + ipw - 1) / ipw) * ((ho + th - 1) / th) * cb * n_mt;
         const long long waves = (ctas + h->sms - 1) / h->sms;
         // waves x per-tile cost: the tile's blocks x per-block cost, plus the epilogue
@@ -1136,8 +1213,13 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         // accumulators fit in TMEM and it overlaps the next tile's MMAs
         const long long tile_mma = static_cast<long long>(n_tk + n_ck * taps) * item;
         const bool dbl = 2 * acc + 4 * bpi * es_need <= 512;
-        const long long cost = waves * (tile_mma + (dbl ? 0LL : 30LL * acc));
+        long long cost = waves * (tile_mma + (dbl ? 0LL : 30LL * acc));
+        if (pair && pair_force) cost /= 1000;
         if (cost < best_cost) {
+          best_pair = pair;
+          best_margin = margin;
+          best_shift_x = p_shift_x;
+          best_shift_t = p_shift_t;
           best_cost = cost;
           best_th = th;
           best_ns = ns;
@@ -1161,6 +1243,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       }
       if (found) break;
       }  // pass
+      }  // pair
     }
   }
   }  // cpw
@@ -1171,50 +1254,43 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   const int th = best_th;
   const int wc = best_wc, tbox_w = best_tbw, tcols = best_tc;
 
-  // ---- S -> exact 2:4 main + residual blocks (bf16 values, RNE), TMEM metadata
-  Split24 S24 = split_24(d, n_mt, n_ck, taps);
   // overflow gather instead of residual blocks when the residual MMAs cost more than the
   // G chunks: a residual block is 2 sparse MMA steps (each the time of a dense K = 16 step)
-  // per unit, a G chunk t_kc / 16 dense steps, plus ~8 steps for the gather hand-off
+  // per unit, a G chunk t_kc / 16 dense steps, plus ~8 steps for the gather hand-off; the
+  // pair form always takes it (its two CTAs' block streams must be identical)
   int n_gk = 0;
+  const int gper = best_pair ? 2 : 1;  // M-tiles per slot group
+  const int n_grp = (n_mt + gper - 1) / gper;
   std::vector<int> g_tab;
-  {
-    const char* ge = getenv("LRS_WCONV_GATHER");  // plan override: 0 = residual blocks, 1 = gather
-    if (S24.nres > 0 && !(ge && atoi(ge) == 0)) {
-      Split24 G = split_24(d, n_mt, n_ck, taps, true);
-      std::vector<std::vector<std::pair<int, int>>> slots(n_mt);  // distinct (channel, tap) per M-tile
-      size_t mx = 0;
-      for (int mt = 0; mt < n_mt; ++mt) {
-        for (const Ovf& o : G.ovf[mt])
-          if (std::find(slots[mt].begin(), slots[mt].end(), std::make_pair(o.ch, o.t)) == slots[mt].end())
-            slots[mt].emplace_back(o.ch, o.t);
-        mx = std::max(mx, slots[mt].size());
-      }
-      const int gk = static_cast<int>((mx + t_kc - 1) / t_kc);
-      const bool pays = 2.0 * S24.nres / n_mt > gk * (t_kc / 16.0) + 8.0;
-      if (gk * t_kc <= 128 && gk * t_kc <= 0xFFFF && (pays || (ge && atoi(ge) == 1))) {
-        n_gk = gk;
-        const int gs = gk * t_kc;
-        g_tab.assign(static_cast<size_t>(n_mt) * gs, -1);
-        for (int mt = 0; mt < n_mt; ++mt)
-          for (size_t si = 0; si < slots[mt].size(); ++si) {
-            const int t = slots[mt][si].second;
-            g_tab[mt * gs + si] = slots[mt][si].first | ((t / kw) << 16) | ((t % kw) << 24);
-          }
-        // the overflow values as dense U blocks: row m of M-tile mt, column = slot index
-        h->w_ovf.assign(static_cast<size_t>(n_mt) * gk * 128 * sw_t, 0);
-        for (int mt = 0; mt < n_mt; ++mt)
-          for (const Ovf& o : G.ovf[mt]) {
-            const int si = static_cast<int>(std::find(slots[mt].begin(), slots[mt].end(), std::make_pair(o.ch, o.t)) -
-                                            slots[mt].begin());
-            const uint16_t bits = bf16_bits_rne(o.v);
-            memcpy(&h->w_ovf[(static_cast<size_t>(mt) * gk + si / t_kc) * 128 * sw_t + swz_off(o.m, 2 * (si % t_kc), sw_t)],
-                   &bits, 2);
-          }
-        S24 = std::move(G);
-      }
+  if (S24.nres > 0 && !(gather_env && atoi(gather_env) == 0)) {
+    const auto slots = best_pair ? pair_slots : group_slots(1);
+    size_t mx = 0;
+    for (const auto& v : slots) mx = std::max(mx, v.size());
+    const int gk = static_cast<int>((mx + t_kc - 1) / t_kc);
+    const bool pays = 2.0 * S24.nres / n_mt > gk * (t_kc / 16.0) + 8.0;
+    if (gk * t_kc <= 256 && (best_pair || pays || (gather_env && atoi(gather_env) == 1))) {
+      n_gk = gk;
+      const int gs = gk * t_kc;
+      g_tab.assign(static_cast<size_t>(n_grp) * gs, -1);
+      for (int gi = 0; gi < n_grp; ++gi)
+        for (size_t si = 0; si < slots[gi].size(); ++si) {
+          const int t = slots[gi][si].second;
+          g_tab[gi * gs + si] = slots[gi][si].first | ((t / kw) << 16) | ((t % kw) << 24);
+        }
+      // the overflow values as dense U blocks: row m of M-tile mt, column = its group's slot index
+      h->w_ovf.assign(static_cast<size_t>(n_mt) * gk * 128 * sw_t, 0);
+      for (int mt = 0; mt < n_mt; ++mt)
+        for (const Ovf& o : Gv.ovf[mt]) {
+          const auto& v = slots[mt / gper];
+          const int si = static_cast<int>(std::find(v.begin(), v.end(), std::make_pair(o.ch, o.t)) - v.begin());
+          const uint16_t bits = bf16_bits_rne(o.v);
+          memcpy(&h->w_ovf[(static_cast<size_t>(mt) * gk + si / t_kc) * 128 * sw_t + swz_off(o.m, 2 * (si % t_kc), sw_t)],
+                 &bits, 2);
+        }
+      S24 = std::move(Gv);
     }
   }
+  if (best_pair && S24.nres > 0) return fail(LRS_ERR_UNSUPPORTED, "CTA-pair plan with residual blocks");
   const int nblk_main = S24.nblk_main;
   const int nres = S24.nres;
   std::vector<uint16_t>& as = S24.as;
@@ -1295,7 +1371,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
       std::vector<uint8_t> tb(g_tab.size() * 4);
       memcpy(tb.data(), g_tab.data(), tb.size());
       if ((st = upload(&h->w_gtab, tb)) != LRS_OK) return st;
-      const size_t gb = static_cast<size_t>(d->batch_max) * ho * wo * n_mt * n_gk * t_kc * 2;
+      const size_t gb = static_cast<size_t>(d->batch_max) * ho * wo * n_grp * n_gk * t_kc * 2;
       LRS_CUDA(cudaMalloc(&h->w_g, gb));
       LRS_CUDA(cudaMemset(h->w_g, 0, gb));  // empty slots stay 0
     }
@@ -1322,7 +1398,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   }
   if (n_gk) {
     const uint64_t bm = static_cast<uint64_t>(d->batch_max);
-    const uint64_t gch = static_cast<uint64_t>(n_mt) * n_gk * t_kc;
+    const uint64_t gch = static_cast<uint64_t>(n_grp) * n_gk * t_kc;
     uint64_t dims[4] = {gch, bm, static_cast<uint64_t>(wo), static_cast<uint64_t>(ho)};
     uint64_t strides[3] = {static_cast<uint64_t>(ho) * wo * gch * 2, gch * 2, static_cast<uint64_t>(wo) * gch * 2};
     uint32_t box[4] = {static_cast<uint32_t>(t_kc), static_cast<uint32_t>(ipw), static_cast<uint32_t>(tbox_w),
@@ -1382,6 +1458,10 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   w.t_win_bytes = best_tw;
   w.win_stride = best_stride;
   w.ns = best_ns;
+  w.pair = best_pair;
+  w.win_margin = best_margin;
+  w.shift_x = best_shift_x;
+  w.shift_t = best_shift_t;
   const uint32_t acc = best_acc;
   w.acc_cols = acc;
   w.bpi = best_bpi;
@@ -1404,6 +1484,9 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     fprintf(stderr, "lrs_wconv plan: ipw %d th %d tcols %d units %d acc %u nacc %d ns %d bpi %d nwb %d cpw %d win %u B smem %u B tiles/img-group %d residual blocks %d gather chunks %d\n",
             ipw, th, tcols, w.n_units, acc, w.nacc, w.ns, w.bpi, w.nwb, cpw, best_stride, best_total, w.bands * w.cbands * w.n_mt,
             nres, n_gk);
+  if (getenv("LRS_VERBOSE") && best_pair)
+    fprintf(stderr, "lrs_wconv plan: CTA pairs (cta_group::2), unit N %d, window margin %u B\n", best_units[0].n,
+            best_margin);
   return LRS_OK;
 }
 
@@ -2255,12 +2338,13 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
     if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
   for (int u = 1; u <= kWMaxUnits; ++u)
-    for (int b = 2; b <= 4; b += 2) {
-      cudaError_t e =
-          cudaFuncSetAttribute(wconv_kernel_ptr(u, b), cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-      if (e != cudaSuccess)
-        return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
-    }
+    for (int b = 2; b <= 4; b += 2)
+      for (int pr = 0; pr < (u <= 2 ? 2 : 1); ++pr) {
+        cudaError_t e = cudaFuncSetAttribute(wconv_kernel_ptr(u, b, pr != 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kMaxSmem);
+        if (e != cudaSuccess)
+          return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
+      }
   if ((st = setup_early(h, d)) != LRS_OK) return cleanup_fail(st);
   if ((st = autotune_core(h, d)) != LRS_OK) return cleanup_fail(st);
   if ((st = autotune_pw(h, d)) != LRS_OK) return cleanup_fail(st);
@@ -2456,11 +2540,15 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
     w.y = y;
     w.x = static_cast<const __nv_bfloat16*>(x);
     w.n_tiles = ((n + w.ipw - 1) / w.ipw) * w.bands * w.cbands * w.n_mt;
-    const unsigned grid = static_cast<unsigned>(std::min(w.n_tiles, h->sms));
+    const unsigned grid = w.pair ? 2u * static_cast<unsigned>(std::min(w.n_tiles / 2, h->sms / 2))
+                                 : static_cast<unsigned>(std::min(w.n_tiles, h->sms));
     cudaEvent_t e1 = nullptr;
     if ((st = time_begin(h, 2, stream, &e1)) != LRS_OK) return st;
-    LRS_CUDA(launch_pdl(wconv_kernel_ptr(w.n_units, w.bpi), dim3(grid), dim3(kWThreads), &w,
-                        h->w_smem, stream));
+    if (w.pair)
+      LRS_CUDA(launch_pdl_pair(wconv_kernel_ptr(w.n_units, w.bpi, true), dim3(grid), dim3(kWThreads), &w, h->w_smem,
+                               stream));
+    else
+      LRS_CUDA(launch_pdl(wconv_kernel_ptr(w.n_units, w.bpi), dim3(grid), dim3(kWThreads), &w, h->w_smem, stream));
     if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
     return LRS_OK;
   }
@@ -2656,6 +2744,11 @@ int32_t lrs_conv_sparse_engine(const lrs_conv* h, int32_t* main_blocks, int32_t*
   if (main_blocks) *main_blocks = tc ? h->w_main_blocks : 0;
   if (residual_blocks) *residual_blocks = tc ? h->w_res_blocks : 0;
   return tc ? 1 : (h->use_tiny ? 3 : (h->use_spadd ? 2 : 0));
+}
+
+int32_t lrs_conv_cta_pairs(const lrs_conv* h) {
+  if (!h) return -1;
+  return h->use_w && !h->use_pw ? h->wp.pair : 0;
 }
 
 int32_t lrs_conv_overflow_chunks(const lrs_conv* h) {

@@ -130,6 +130,13 @@ struct WconvParams {
   __nv_bfloat16* g;     // G scratch [N][Ho][Wo][g_ch] (empty slots zeroed once at create)
   const __nv_bfloat16* x;  // this forward's X (the gather reads it)
   int in_h, in_w, c_in;
+  // CTA pair (lrs_wconv_kernel<.., PAIR = true>, launched as clusters of 2): the pair's two
+  // CTAs own M-tiles 2i and 2i + 1 of the same positions; rank 0 issues cta_group::2 MMAs
+  // (M = 256) for both, B split along N (every unit has the same N, a multiple of 16), so
+  // rank 1 keeps each window shifted by N/2 rows: shift_x (X windows, 128 B rows) and
+  // shift_t (T / G windows, sw_t rows) bytes before its buffer (win_margin bytes reserved)
+  int pair;
+  uint32_t win_margin, shift_x, shift_t;
 };
 
 struct TileCoord {
@@ -171,12 +178,13 @@ __device__ __forceinline__ TileCoord tile_coord_v(int tile, int n_mt, int cbands
 // (0 outside the image).  Empty slots are never written (zeroed at create).
 __device__ __forceinline__ void gather_tile(const WconvParams& p, const TileCoord& tc, int we, int lane) {
   const int gs = p.n_gk * p.t_kc;
-  int tab[4];  // the lane's slots lane, lane + 32, .. (gs <= 128)
+  const int gi = p.pair ? (tc.mt >> 1) : tc.mt;  // slot set: the M-tile's, or the pair's union
+  int tab[8];  // the lane's slots lane, lane + 32, .. (gs <= 256)
 #pragma unroll
-  for (int i = 0; i < 4; ++i) tab[i] = (lane + 32 * i < gs) ? __ldg(p.g_tab + tc.mt * gs + lane + 32 * i) : -1;
+  for (int i = 0; i < 8; ++i) tab[i] = (lane + 32 * i < gs) ? __ldg(p.g_tab + gi * gs + lane + 32 * i) : -1;
   const int npos = p.th * p.tcols * p.ipw;
   const __nv_bfloat16* __restrict__ x = p.x;
-  __nv_bfloat16* __restrict__ g = p.g + tc.mt * gs;
+  __nv_bfloat16* __restrict__ g = p.g + gi * gs;
   for (int pi = we; pi < npos; pi += 8) {
     const int img = pi % p.ipw, q = pi / p.ipw;
     const int r = q / p.tcols, c = q - r * p.tcols;
@@ -184,9 +192,9 @@ __device__ __forceinline__ void gather_tile(const WconvParams& p, const TileCoor
     if (n >= p.n || ho >= p.ho || wo >= p.wo) continue;
     const long long xrow = static_cast<long long>(n) * p.in_h;
     __nv_bfloat16* grow = g + ((static_cast<long long>(n) * p.ho + ho) * p.wo + wo) * p.g_ch;
-    __nv_bfloat16 v[4];
+    __nv_bfloat16 v[8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 8; ++i) {
       v[i] = __float2bfloat16_rn(0.f);
       if (tab[i] >= 0) {
         const int hi = ho * p.sh - p.ph + ((tab[i] >> 16) & 0xFF), wi = wo * p.sw - p.pw + (tab[i] >> 24);
@@ -195,7 +203,7 @@ __device__ __forceinline__ void gather_tile(const WconvParams& p, const TileCoor
       }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 8; ++i)
       if (tab[i] >= 0) grow[lane + 32 * i] = v[i];
   }
 }
@@ -203,7 +211,7 @@ __device__ __forceinline__ void gather_tile(const WconvParams& p, const TileCoor
 // NU = the layer's exact unit count (1..kWMaxUnits): the MMA issue loops are fully
 // unrolled without predicates -- a generic 8-unit loop measured 17-39 % slower
 // (instruction fetch of the issuing warp dominates small MMAs).
-template <int NU, int BPI>
+template <int NU, int BPI, bool PAIR>
 __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_constant__ WconvParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -220,6 +228,12 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const uint32_t slot_info = smem_u32(tmem_slot + 4);  // [kWMaxSlots][kWMaxBpi] u32, written by the producer
   uint64_t* g_ready = bars + 48;  // byte 384: the tile's G chunks are in global memory (8 epilogue warps)
+  // pair: rank 0 = MMA issuer for both CTAs; its full barriers also count the peer's relay
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const bool lead = !PAIR || rank == 0;
+  // work units: tiles, or (pair) tile pairs -- M-tiles 2i, 2i + 1 of the same positions
+  const int g_id = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int g_n = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
 
   if (WTRACE(p) && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x] = gtimer();
   const int nwin = p.n_tk + p.n_gk + p.n_xw;
@@ -262,16 +276,20 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     prm[30] = static_cast<int>(p.off_res);
     prm[31] = p.ipw;
     prm[32] = p.n_gk;
+    prm[33] = static_cast<int>(p.win_margin);
+    prm[34] = static_cast<int>(p.shift_x);
+    prm[35] = static_cast<int>(p.shift_t);
+    const uint32_t nf = (PAIR && rank == 0) ? 2u : 1u;  // + the peer relay's arrival
     for (int i = 0; i < p.nwb; ++i) {
-      mbar_init(&win_full[i], 1);
+      mbar_init(&win_full[i], nf);
       mbar_init(&win_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 8);  // one arrival per epilogue warp
+      mbar_init(&acc_empty[i], 8 * nf);  // one arrival per epilogue warp (of both CTAs)
     }
     for (int i = 0; i < p.ns; ++i) {
-      mbar_init(&a_full[i], 1);
+      mbar_init(&a_full[i], nf);
       mbar_init(&a_empty[i], 1);
     }
     mbar_init(g_ready, 8);
@@ -280,9 +298,13 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     tma_prefetch_desc(&p.tmT);
     if (p.n_gk > 0) tma_prefetch_desc(&p.tmG);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc2(tmem_slot, p.tmem_cols);
+    else tmem_alloc(tmem_slot, p.tmem_cols);
+  }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // the peer's barriers are initialised before any remote arrive
   tc_fence_after();
   // The CTA owns the whole TMEM of its SM (tmem_cols = 512, one CTA per SM), so
   // the allocation starts at lane 0 / column 0.  Using the literal 0 keeps every
@@ -326,6 +348,9 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const int tcols_ = static_cast<int>(smem_param(prm + 27));
     const int n_gk_ = smem_param(prm + 32);
     const int n_dk_ = n_tk_ + n_gk_;  // dense chunks per M-tile (T, then G)
+    const uint32_t win_margin_ = static_cast<uint32_t>(smem_param(prm + 33));
+    const uint32_t shift_x_ = rank ? static_cast<uint32_t>(smem_param(prm + 34)) : 0u;
+    const uint32_t shift_t_ = rank ? static_cast<uint32_t>(smem_param(prm + 35)) : 0u;
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
       int it = 0, wg = 0, buf = 0;
@@ -341,13 +366,14 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       // their windows; with one ring buffer per window (nwb == nwin) a window still resident
       // from the previous tile is reused instead of re-loaded
       const bool contig = nwb_ == nwin;
-      const int t_begin = contig ? static_cast<int>(static_cast<long long>(blockIdx.x) * n_tiles_ / gridDim.x)
-                                 : static_cast<int>(blockIdx.x);
-      const int t_end = contig ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * n_tiles_ / gridDim.x)
-                               : n_tiles_;
-      const int t_step = contig ? 1 : static_cast<int>(gridDim.x);
+      const int n_u = PAIR ? n_tiles_ >> 1 : n_tiles_;
+      const int t_begin = contig ? static_cast<int>(static_cast<long long>(g_id) * n_u / g_n) : g_id;
+      const int t_end = contig ? static_cast<int>(static_cast<long long>(g_id + 1) * n_u / g_n) : n_u;
+      const int t_step = contig ? 1 : g_n;
       int prev_win = -1;
-      for (int tile = t_begin; tile < t_end; tile += t_step) {
+      for (int tu = t_begin; tu < t_end; tu += t_step) {
+        const int hm = n_mt_ >> 1;
+        const int tile = PAIR ? (tu / hm) * n_mt_ + 2 * (tu % hm) + static_cast<int>(rank) : tu;
         const TileCoord tc = tile_coord_v(tile, n_mt_, cbands_, bands_, th_, tcols_, ipw_);
         const int win_key = tile / n_mt_;
         const bool reuse = nwb_ == nwin && win_key == prev_win;
@@ -361,7 +387,10 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         }
         for (int w = 0; w < nwin; ++w, ++wg) {
           if (wg >= nwb_) mbar_wait(&win_empty[buf], wph ^ 1u);
-          uint8_t* wdst = smem + buf * win_stride_;
+          const int tk_ = w - n_xw_;
+          // (pair, rank 1: the window sits N/2 B rows earlier, so the leader's descriptors,
+          // which address both CTAs at the same offset, see the unit's second half here)
+          uint8_t* wdst = smem + win_margin_ + buf * win_stride_ - (tk_ >= 0 ? shift_t_ : shift_x_);
           if (WTRACE(p) && blockIdx.x == 0 && wg < 16) p.trace[3600 + wg] = gtimer();
           const int tk = w - n_xw_;  // >= 0: dense (T) window, after the tile's sparse ones
           if (tk >= 0 && !waited) {
@@ -377,8 +406,8 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             mbar_arrive(&win_full[buf]);  // window already resident (or timing experiment)
           } else if (tk >= n_tk_) {
             mbar_arrive_expect_tx(&win_full[buf], t_win_bytes_);
-            tma_load_4d(wdst, &p.tmG, &win_full[buf], tc.mt * n_gk_ * t_kc_ + (tk - n_tk_) * t_kc_, tc.n0, tc.wo0,
-                        tc.ho0);
+            tma_load_4d(wdst, &p.tmG, &win_full[buf], (PAIR ? tc.mt >> 1 : tc.mt) * n_gk_ * t_kc_ + (tk - n_tk_) * t_kc_,
+                        tc.n0, tc.wo0, tc.ho0);
           } else if (tk >= 0) {
             mbar_arrive_expect_tx(&win_full[buf], t_win_bytes_);
             tma_load_4d(wdst, &p.tmT, &win_full[buf], tk * t_kc_, tc.n0, tc.wo0, tc.ho0);
@@ -463,7 +492,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     // Descriptors are linear in the start address (14-bit field of addr>>4),
     // so every per-unit descriptor is precomputed once and the inner loop
     // only adds byte offsets >> 4: the single-thread issue loop stays short.
-    const uint32_t win0 = smem_u32(smem);
+    const uint32_t win0 = smem_u32(smem) + static_cast<uint32_t>(smem_param(prm + 33));  // + window margin
     const uint32_t t_pos = static_cast<uint32_t>(ipw_) * sw_t_;  // bytes per position in a T window
     const uint32_t x_pos = 128u * static_cast<uint32_t>(ipw_);     // bytes per position in an X window
     // stride between 8-row core-matrix groups: one position (x stride) of 8 images, or two
@@ -476,7 +505,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     for (int u = 0; u < NU; ++u) {
       {
         dcol[u] = tmem + static_cast<uint32_t>(p.u_col[u]);
-        idu[u] = umma_idesc(1u, static_cast<uint32_t>(p.u_n[u]), 128u);
+        idu[u] = umma_idesc(1u, static_cast<uint32_t>(p.u_n[u]), PAIR ? 256u : 128u);
         bxd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_xpos[u]) * x_pos, 128, x_sbo);
         btd[u] = umma_desc_sbo(win0 + static_cast<uint32_t>(p.u_tpos[u]) * t_pos, sw_t_, t_sbo);
       }
@@ -489,43 +518,78 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const int ksteps = static_cast<int>(sw_t_ / 32);
     int slot = 0, k = 0, buf = 0, eslot = 0;
     uint32_t ph = 0, wph = 0;
-    if (elect_one()) {
     const bool contig = nwb_ == nwin;  // must match the producer's tile order
-    const int t_begin = contig ? static_cast<int>(static_cast<long long>(blockIdx.x) * n_tiles_ / gridDim.x)
-                               : static_cast<int>(blockIdx.x);
-    const int t_end = contig ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * n_tiles_ / gridDim.x)
-                             : n_tiles_;
-    const int t_step = contig ? 1 : static_cast<int>(gridDim.x);
-    for (int tile = t_begin; tile < t_end; tile += t_step, ++k) {
-      const TileCoord tc = tile_coord_v(tile, n_mt_, cbands_, bands_, th_, tcols_, ipw_);
+    const int n_u = PAIR ? n_tiles_ >> 1 : n_tiles_;
+    const int t_begin = contig ? static_cast<int>(static_cast<long long>(g_id) * n_u / g_n) : g_id;
+    const int t_end = contig ? static_cast<int>(static_cast<long long>(g_id + 1) * n_u / g_n) : n_u;
+    const int t_step = contig ? 1 : g_n;
+    (void)cbands_; (void)bands_; (void)th_; (void)tcols_; (void)n_mt_;
+    if (PAIR && !lead) {
+      // ---------------------------------------------------------- pair relay (rank 1)
+      // Mirror the leader's consumption order: every window and A/E item this CTA's
+      // producer lands is forwarded to the leader's full barrier (count 2 there), whose
+      // MMAs read this CTA's shared memory at the same offsets.  Releases (empty
+      // barriers) arrive here directly through the leader's multicast commits.
+      if (elect_one()) {
+        for (int tu = t_begin; tu < t_end; tu += t_step) {
+          for (int w = 0; w < nwin; ++w) {
+            mbar_wait(&win_full[buf], wph);
+            mbar_arrive_remote(&win_full[buf], 0);
+            if (w >= n_xw_) {
+              mbar_wait(&a_full[slot], ph);
+              mbar_arrive_remote(&a_full[slot], 0);
+              if (++slot == ns_) { slot = 0; ph ^= 1u; }
+            } else {
+              while (true) {
+                mbar_wait(&a_full[slot], ph);
+                const uint32_t info0 = ld_shared_u32(slot_info + 4u * kWMaxBpi * slot);
+                mbar_arrive_remote(&a_full[slot], 0);
+                if (++slot == ns_) { slot = 0; ph ^= 1u; }
+                if (info0 >> 31) break;
+              }
+            }
+            if (++buf == nwb_) { buf = 0; wph ^= 1u; }
+          }
+        }
+      }
+    } else if (elect_one()) {
+    int mi_ = 0;  // item count (debug trace)
+    (void)mi_;
+    for (int tu = t_begin; tu < t_end; tu += t_step, ++k) {
       const int b = nacc_ == 2 ? (k & 1) : 0;
       const int use = nacc_ == 2 ? (k >> 1) : k;  // previous uses of accumulator b
       if (use > 0) {
-        mbar_wait(&acc_empty[b], (use - 1) & 1);
+        if (PAIR) mbar_wait_cluster(&acc_empty[b], (use - 1) & 1);
+        else mbar_wait(&acc_empty[b], (use - 1) & 1);
         tc_fence_after();
       }
       const uint32_t acc0 = static_cast<uint32_t>(b) * acc_cols_;
       if (WTRACE(p) && blockIdx.x == 0 && k < 16) p.trace[100 + 4 * k] = gtimer();
       for (int w = 0; w < nwin; ++w) {
         if (WTRACE(p) && blockIdx.x == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w] = gtimer();
-        mbar_wait(&win_full[buf], wph);
+        if (PAIR) mbar_wait_cluster(&win_full[buf], wph);
+        else mbar_wait(&win_full[buf], wph);
         tc_fence_after();
         if (WTRACE(p) && blockIdx.x == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w + 1] = gtimer();
         const uint32_t boff = static_cast<uint32_t>(buf) * win16;
         if (w >= n_xw_) {  // dense window: the accumulator already holds the sparse term
-          mbar_wait(&a_full[slot], ph);
+          if (PAIR) mbar_wait_cluster(&a_full[slot], ph);
+          else mbar_wait(&a_full[slot], ph);
           tc_fence_after();
           const uint64_t ab = ad_dense + slot * slot_a16;
           {
 #pragma unroll
             for (int u = 0; u < NU; ++u) {
               {
-                for (int kk = 0; kk < ksteps; ++kk)
-                  mma_bf16(dcol[u] + acc0, ab + 2 * kk, btd[u] + boff + 2 * kk, idu[u],
-                           (n_xw_ > 0 || w > 0 || kk > 0) ? 1u : 0u);  // S empty: dense starts the sum
+                for (int kk = 0; kk < ksteps; ++kk) {
+                  const uint32_t acc1 = (n_xw_ > 0 || w > 0 || kk > 0) ? 1u : 0u;  // S empty: dense starts the sum
+                  if (PAIR) mma_bf16_2(dcol[u] + acc0, ab + 2 * kk, btd[u] + boff + 2 * kk, idu[u], acc1);
+                  else mma_bf16(dcol[u] + acc0, ab + 2 * kk, btd[u] + boff + 2 * kk, idu[u], acc1);
+                }
               }
             }
-            mma_commit(&a_empty[slot]);
+            if (PAIR) mma_commit_pair(&a_empty[slot]);
+            else mma_commit(&a_empty[slot]);
           }
           if (++slot == ns_) { slot = 0; ph ^= 1u; }
         } else {
@@ -534,8 +598,11 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           // very first MMA step of each unit starts the accumulator (accumulate = 0)
           bool first = w == 0;
           while (true) {
-            mbar_wait(&a_full[slot], ph);
+            if (WTRACE(p) && blockIdx.x == 0 && mi_ < 64) p.trace[3300 + 3 * mi_] = gtimer();
+            if (PAIR) mbar_wait_cluster(&a_full[slot], ph);
+            else mbar_wait(&a_full[slot], ph);
             tc_fence_after();
+            if (WTRACE(p) && blockIdx.x == 0 && mi_ < 64) p.trace[3300 + 3 * mi_ + 1] = gtimer();
             const uint32_t info0 = ld_shared_u32(slot_info + 4u * kWMaxBpi * slot);
             const int nb = static_cast<int>((info0 >> 28) & 7u);
             uint32_t tapv[BPI];
@@ -552,12 +619,14 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
               // next metadata slot, or lie past the end of TMEM when items are one block)
               for (int bp = 0; bp < BPI; bp += 2)
                 if (bp < nb && !WDBG(p, 5)) {
-                  if (bp + 1 < nb)
-                    tmem_cp_128x256b(et + 4u * static_cast<uint32_t>(bp),
-                                     ed0 + slot * slot_e16 + static_cast<uint32_t>(bp) * (kEBlockBytes >> 4));
-                  else
-                    tmem_cp_128x128b(et + 4u * static_cast<uint32_t>(bp),
-                                     ed0 + slot * slot_e16 + static_cast<uint32_t>(bp) * (kEBlockBytes >> 4));
+                  const uint64_t esrc = ed0 + slot * slot_e16 + static_cast<uint32_t>(bp) * (kEBlockBytes >> 4);
+                  if (bp + 1 < nb) {
+                    if (PAIR) tmem_cp_128x256b_2(et + 4u * static_cast<uint32_t>(bp), esrc);
+                    else tmem_cp_128x256b(et + 4u * static_cast<uint32_t>(bp), esrc);
+                  } else {
+                    if (PAIR) tmem_cp_128x128b_2(et + 4u * static_cast<uint32_t>(bp), esrc);
+                    else tmem_cp_128x128b(et + 4u * static_cast<uint32_t>(bp), esrc);
+                  }
                 }
 #pragma unroll
               for (int bi = 0; bi < BPI; ++bi) {
@@ -567,25 +636,33 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                   for (int s2 = 0; s2 < (WDBG(p, 8) ? 1 : 2) && !(WDBG(p, 1)); ++s2) {
 #pragma unroll
                     for (int u = 0; u < NU; ++u) {
-                      mma_sp_bf16(dcol[u] + acc0, ab + static_cast<uint32_t>(bi) * (kSpBlockBytes >> 4) + 2 * s2,
-                                  bxd[u] + boff + tapv[bi] + 4 * s2, idu[u] | (1u << 2) | static_cast<uint32_t>(s2),
-                                  (first && bi == 0 && s2 == 0) ? 0u : 1u, ebi);
+                      const uint64_t aa = ab + static_cast<uint32_t>(bi) * (kSpBlockBytes >> 4) + 2 * s2;
+                      const uint64_t bb = bxd[u] + boff + tapv[bi] + 4 * s2;
+                      const uint32_t id = idu[u] | (1u << 2) | static_cast<uint32_t>(s2);
+                      const uint32_t acc1 = (first && bi == 0 && s2 == 0) ? 0u : 1u;
+                      if (PAIR) mma_sp_bf16_2(dcol[u] + acc0, aa, bb, id, acc1, ebi);
+                      else mma_sp_bf16(dcol[u] + acc0, aa, bb, id, acc1, ebi);
                     }
                   }
                 }
               }
               if (WDBG(p, 512)) mbar_arrive(&a_empty[slot]);
+              else if (PAIR) mma_commit_pair(&a_empty[slot]);
               else mma_commit(&a_empty[slot]);
+              if (WTRACE(p) && blockIdx.x == 0 && mi_ < 64) p.trace[3300 + 3 * mi_ + 2] = gtimer();
+              ++mi_;
             }
             first = false;
             if (++slot == ns_) { slot = 0; ph ^= 1u; }
             if (info0 >> 31) break;
           }
         }
-        mma_commit(&win_empty[buf]);
+        if (PAIR) mma_commit_pair(&win_empty[buf]);
+        else mma_commit(&win_empty[buf]);
         if (++buf == nwb_) { buf = 0; wph ^= 1u; }
       }
-      mma_commit(&acc_full[b]);
+      if (PAIR) mma_commit_pair(&acc_full[b]);
+      else mma_commit(&acc_full[b]);
       if (WTRACE(p) && blockIdx.x == 0 && k < 16) p.trace[100 + 4 * k + 1] = gtimer();
     }
     }
@@ -598,12 +675,18 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(p.y);
     int k = 0;
     const bool contig = p.nwb == nwin;  // must match the producer's tile order
-    const int t_begin = contig ? static_cast<int>(static_cast<long long>(blockIdx.x) * p.n_tiles / gridDim.x)
-                               : static_cast<int>(blockIdx.x);
-    const int t_end = contig ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * p.n_tiles / gridDim.x)
-                             : p.n_tiles;
-    const int t_step = contig ? 1 : static_cast<int>(gridDim.x);
-    for (int tile = t_begin; tile < t_end; tile += t_step, ++k) {
+    const int n_u = PAIR ? p.n_tiles >> 1 : p.n_tiles;
+    const int t_begin = contig ? static_cast<int>(static_cast<long long>(g_id) * n_u / g_n) : g_id;
+    const int t_end = contig ? static_cast<int>(static_cast<long long>(g_id + 1) * n_u / g_n) : n_u;
+    const int t_step = contig ? 1 : g_n;
+    // accumulator release: the leader's MMA issuer waits for the epilogues of both CTAs
+    auto release = [&](int b) {
+      if (PAIR && !lead) mbar_arrive_remote(&acc_empty[b], 0);
+      else mbar_arrive(&acc_empty[b]);
+    };
+    for (int tu = t_begin; tu < t_end; tu += t_step, ++k) {
+      const int hm = p.n_mt >> 1;
+      const int tile = PAIR ? (tu / hm) * p.n_mt + 2 * (tu % hm) + static_cast<int>(rank) : tu;
       const TileCoord tc = tile_coord(p, tile);
       if (p.n_gk > 0) {
         // overflow gather of this tile (the MMA warp needs it only after the tile's sparse
@@ -624,7 +707,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       if (WDBG(p, 16)) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[b]);
+        if (lane == 0) release(b);
         continue;
       }
       if (WTRACE(p) && blockIdx.x == 0 && threadIdx.x == 64 && k < 16) p.trace[100 + 4 * k + 2] = gtimer();
@@ -721,18 +804,20 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
       // this warp's TMEM reads of buffer b are complete (wait::ld above)
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[b]);
+      if (lane == 0) release(b);
       if (WTRACE(p) && blockIdx.x == 0 && threadIdx.x == 64 && k < 16) p.trace[100 + 4 * k + 3] = gtimer();
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // neither CTA frees TMEM / leaves while the pair still works
   if (WTRACE(p) && threadIdx.x == 0 && blockIdx.x < 2048) p.trace[2000 + 3 * blockIdx.x + 2] = gtimer();
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem, p.tmem_cols);
+    if (PAIR) tmem_dealloc2(tmem, p.tmem_cols);
+    else tmem_dealloc(tmem, p.tmem_cols);
   }
 }
 

@@ -29,6 +29,7 @@ EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs
             "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine", "lrs_conv_core_fused",
             "lrs_conv_expand_kernel",
             "lrs_conv_overflow_chunks",
+            "lrs_conv_cta_pairs",
             "lrs_sparse_from_slices")
 
 
@@ -95,6 +96,8 @@ def load_library(path: str = LIB_PATH):
     lib.lrs_conv_expand_kernel.restype = ctypes.c_int32
     lib.lrs_conv_overflow_chunks.argtypes = [P]
     lib.lrs_conv_overflow_chunks.restype = ctypes.c_int32
+    lib.lrs_conv_cta_pairs.argtypes = [P]
+    lib.lrs_conv_cta_pairs.restype = ctypes.c_int32
     lib.lrs_sparse_from_slices.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.POINTER(ctypes.c_int64), P, ctypes.c_int32,
                                            ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64),
@@ -279,6 +282,12 @@ class LrsConv:
         """0 GEMM / SIMT, 1 windowed tensor-core kernel, 2 channel-stationary 1x1 kernel
         (lrs_conv_expand_kernel, include/lrs_conv.h)."""
         return int(load_library().lrs_conv_expand_kernel(self.handle))
+
+    @property
+    def cta_pairs(self) -> bool:
+        """True if the windowed kernel runs in its CTA-pair (cta_group::2) form
+        (lrs_conv_cta_pairs, include/lrs_conv.h)."""
+        return load_library().lrs_conv_cta_pairs(self.handle) == 1
 
     @property
     def overflow_chunks(self) -> int:

@@ -244,3 +244,84 @@ def test_simt_csr_engine_matches_oracle(name):
     y = simt(x)
     torch.cuda.synchronize()
     parity.check(y, oracle(inp), "bf16")
+
+
+PAIR_CASES = [  # (n, h, w, cin, cout, k, s, p, r1, r2, density)
+    (13, 7, 7, 512, 512, 3, 1, 1, 128, 128, 0.05),   # C3 shape: pairs of M-tiles + the pair-union gather
+    (9, 14, 14, 256, 256, 3, 1, 1, 64, 64, 0.02),    # C2 shape, ragged image group
+    (6, 12, 12, 128, 256, 5, 1, 2, 32, 48, 0.06),    # 5x5, padding 2, R2 48 -> 64
+    (5, 9, 9, 64, 512, 3, 1, 0, 32, 32, 0.03),       # pad 0, 4 M-tiles (2 pairs)
+]
+
+
+def _make_env(inp, env, batch_max=None, **kw):
+    import os
+    from paper_2006_06443_b200 import LrsConv
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return LrsConv.from_inputs(inp, batch_max=batch_max, **kw)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("geom", PAIR_CASES)
+def test_cta_pair_form_vs_oracle(geom):
+    """The CTA-pair form (LRS_WCONV_PAIR=1: clusters of 2 CTAs, tcgen05.mma.cta_group::2 with
+    M = 256, each SM holding half of every window along N) against the fp64 oracle, with a
+    fused output epilogue, a partial batch and a second forward on other images."""
+    n, h, w, cin, cout, k, s, p, r1, r2, dens = geom
+    cfg = workloads.LayerConfig("pair", n, h, w, cin, cout, k, s, p, r1, r2, dens, "bf16", seed=37)
+    inp = workloads.generate(cfg)
+    rng = np.random.default_rng(8)
+    scale = rng.uniform(0.5, 1.5, cout).astype(np.float32)
+    bias = rng.standard_normal(cout).astype(np.float32) * 0.1
+    layer = _make_env(inp, {"LRS_WCONV_PAIR": "1"}, batch_max=n + 3, out_scale=scale, out_bias=bias, out_relu=True)
+    assert layer.expand_kernel == 1 and layer.cta_pairs
+    assert layer.sparse_engine[2] == 0  # no residual blocks in the pair form
+    c = inp.cfg
+    for seed in (None, 91):
+        x = inp.x if seed is None else workloads.generate_x(cfg, n, seed=seed)
+        y = layer(torch.from_numpy(x).to(torch.bfloat16).cuda())
+        torch.cuda.synchronize()
+        ref = O.output_epilogue(O.forward_factored(x.astype(np.float64), inp.u_in, inp.core, inp.u_out, inp.row_ptr,
+                                                   inp.col_idx, inp.values, c.stride, c.pad), scale, bias, relu=True)
+        parity.check(y, ref, "bf16")
+
+
+def test_cta_pair_bitwise_equal_single_without_overflow():
+    """Without overflow entries (an S with <= 2 nonzeros per group of 4) both forms
+    issue the same MMAs in the same K order -- the pair form only splits B between the two
+    SMs: bitwise equal to the one-CTA form (LRS_WCONV_PAIR=0)."""
+    cfg = workloads.LayerConfig("pair1", 10, 7, 7, 512, 512, 3, 1, 1, 128, 128, 0.02, "bf16", seed=3)
+    g = workloads.generate(cfg)
+    # keep at most 2 nonzeros per (row, group of 4 channels, tap): an exact 2:4 S
+    taps = cfg.k * cfg.k
+    rows, cols, vals = [], [], []
+    for j in range(cfg.c_out):
+        seen = {}
+        for e in range(g.row_ptr[j], g.row_ptr[j + 1]):
+            col = int(g.col_idx[e])
+            key = ((col // taps) // 4, col % taps)
+            if seen.get(key, 0) < 2:
+                seen[key] = seen.get(key, 0) + 1
+                rows.append(j)
+                cols.append(col)
+                vals.append(g.values[e])
+    rp = np.zeros(cfg.c_out + 1, np.int64)
+    np.add.at(rp, np.array(rows) + 1, 1)
+    inp = workloads.LayerInputs(cfg, g.x, g.u_in, g.core, g.u_out, np.cumsum(rp), np.array(cols, np.int32),
+                                np.array(vals, np.float32))
+    a = _make_env(inp, {"LRS_WCONV_PAIR": "1"})
+    b = _make_env(inp, {"LRS_WCONV_PAIR": "0", "LRS_WCONV_IPW": "4"})
+    assert a.cta_pairs and not b.cta_pairs
+    assert a.sparse_engine[2] == 0 and a.overflow_chunks == 0
+    x = torch.from_numpy(inp.x).to(torch.bfloat16).cuda()
+    ya, yb = a(x), b(x)
+    torch.cuda.synchronize()
+    assert torch.equal(ya, yb)
+    parity.check(ya, oracle(inp), "bf16")
