@@ -68,7 +68,8 @@ struct PwParams {
                            // fills slots >= e_slot0 only after the copies to TMEM completed
   int epi_nbuf;            // epilogue scratch buffers per warp (1 or 2, 2 KB each)
   unsigned long long* trace;  // debug builds: %globaltimer stamps of CTA 0 (lrs_conv_debug_trace)
-  int dbg;                    // experiment builds (LRS_PW_DBG): 1 skip Y stores, 2 skip MMAs, 4 skip X/T loads
+  int dbg;                    // experiment builds (LRS_PW_DBG): 1 skip Y stores, 2 skip MMAs, 4 skip X/T loads,
+                              // 8 skip the proxy fence, 16 skip the stmatrix transposes, 32 skip the TMEM loads
   // projection fused in (lrs_pwf_kernel): T1 = X U computed per position tile from the X
   // chunks already in the ring, restaged as bf16 into shared memory, never written to HBM
   const uint8_t* img_u;    // U_in^T blocks [n_ck][R1p rows x 128 B], SW128 (B of the T1 MMAs)
@@ -349,14 +350,16 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
           }
         }
         {
-          uint32_t r[2][2][8];
+          uint32_t r[2][2][8] = {};
+          if (!LRS_XDBG(p.dbg & 32)) {  // experiment: skip the TMEM loads
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int cb = 0; cb < 2; ++cb)
-              tmem_ld_16x256b_x2(tmem + (static_cast<uint32_t>(q4 * 32 + 16 * h) << 16) + acc0 +
-                                     static_cast<uint32_t>(m * bp + c0 + 16 * cb),
-                                 r[h][cb]);
+              for (int cb = 0; cb < 2; ++cb)
+                tmem_ld_16x256b_x2(tmem + (static_cast<uint32_t>(q4 * 32 + 16 * h) << 16) + acc0 +
+                                       static_cast<uint32_t>(m * bp + c0 + 16 * cb),
+                                   r[h][cb]);
+          }
           const uint32_t scr = scr0 + static_cast<uint32_t>(nchunk % epi_nbuf) * 2048u;
           if (lane == 0) {  // the store that last read this buffer is done with it
             if (epi_nbuf == 2) bulk_wait_read1();
@@ -384,11 +387,12 @@ __global__ void __launch_bounds__(kPThreads, 1) lrs_pw_kernel(const __grid_const
               // scratch row (position col, 8-channel part) at col*64 + (part ^ ((col >> 1) & 3))*16
               const int scol = cb * 16 + (mi >> 1) * 8 + mj, spart = 2 * h + (mi & 1);
               const uint32_t addr = scr + static_cast<uint32_t>(scol * 64 + ((spart ^ ((scol >> 1) & 3)) * 16));
+              if (!LRS_XDBG(p.dbg & 16))  // experiment: skip the transposing stores
               stmatrix_x4_trans(addr, pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
                                 pack_bf16x2(f[6], f[7]));
             }
           }
-          fence_proxy_async_smem();  // the generic-proxy stmatrix writes -> visible to the TMA store
+          if (!LRS_XDBG(p.dbg & 8)) fence_proxy_async_smem();  // the generic-proxy stmatrix writes -> visible to the TMA store
           __syncwarp();
           if (lane == 0 && !LRS_XDBG(p.dbg & 1)) {
             tma_store_2d(&p.tmY, scr, jw, p0 + c0);
