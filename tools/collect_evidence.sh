@@ -10,9 +10,15 @@ for f in $O/bench_*.json; do
   [ "$b" = "bench_small" ] && continue
   cp $f profiles/r02_$b.json
 done
-for r in $O/prof_*.ncu-rep; do
+for r in $O/sum_*.txt; do  # summaries written on the box (tools/gpu/r02_w3.sh)
+  b=$(basename $r .txt); b=${b#sum_}
+  cp $r profiles/r02_ncu_${b}_summary.txt
+  cp $O/sass_$b.txt profiles/r02_ncu_${b}_top_sass.txt
+done
+for r in $O/prof_*.ncu-rep; do  # or reports brought back whole
+  [ -e "$r" ] || continue
   b=$(basename $r .ncu-rep); b=${b#prof_}
   python tools/ncu_sum.py $r > profiles/r02_ncu_${b}_summary.txt
   python tools/ncu_src.py $r 25 > profiles/r02_ncu_${b}_top_sass.txt
 done
-python tools/ncu_traffic.py $O
+if [ -e $O/ncu_traffic.json ]; then cp $O/ncu_traffic.json profiles/ncu_traffic.json; else python tools/ncu_traffic.py $O; fi
