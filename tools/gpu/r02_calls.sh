@@ -469,3 +469,35 @@ call_z() {
   cat $O/rc.txt; tail -2 $O/pytest.log; grep "c2_f32 \[" $O/ablate.log
 }
 
+call_q3() {
+  mkdir -p gpurun_out/r02q3; O=gpurun_out/r02q3
+  LRS_EXPERIMENTS=1 python -m paper_2006_06443_b200._build --force > $O/build.log 2>&1
+  E="LRS_SKIP=1 LRS_PW_MPC=2 LRS_PW_BP=96 LRS_PW_CPI=2"
+  timeout 300 python tools/ablate.py c4 "$E" "$E LRS_PW_DBG=1" "$E LRS_PW_DBG=9" "$E LRS_PW_DBG=25" "$E LRS_PW_DBG=57" "$E LRS_PW_DBG=7" "$E LRS_PW_DBG=63" "$E LRS_PW_DBG=6" > $O/ablate.log 2>&1
+  grep "c4 \[" $O/ablate.log
+}
+
+call_q4() {
+  mkdir -p gpurun_out/r02q4; O=gpurun_out/r02q4
+  timeout 900 python -m pytest tests/test_gpu_sparse_tc.py tests/test_gpu_bench_pattern.py tests/test_gpu_overlap.py tests/test_gpu_parity.py -x -q > $O/pytest.log 2>&1; echo "rc=$?" > $O/rc.txt
+  timeout 300 python tools/ablate.py c3 base base > $O/ablate_c3.log 2>&1
+  cat $O/rc.txt; tail -2 $O/pytest.log; grep "c3 \[" $O/ablate_c3.log
+}
+
+call_q5() {
+  mkdir -p gpurun_out/r02q5; O=gpurun_out/r02q5
+  timeout 600 python -m pytest $(grep -ln "forward_host" tests/test_gpu*.py) -x -q > $O/pytest.log 2>&1; echo "rc=$?" > $O/rc.txt
+  timeout 600 python bench.py --steps 100 --warmup 5 --no-cpu --no-dense > $O/bench_c3.json 2> $O/bench_c3.err; echo "bench rc=$?" >> $O/rc.txt
+  timeout 600 python bench.py --config c4 --steps 100 --warmup 5 --no-cpu --no-dense > $O/bench_c4.json 2> $O/bench_c4.err; echo "bench c4 rc=$?" >> $O/rc.txt
+  cat $O/rc.txt; tail -2 $O/pytest.log; python -c "
+  import json
+  for c in ('c3','c4'):
+      d=json.loads(open('$O/bench_'+c+'.json').read().strip().splitlines()[-1]); print(c, round(d['value']), 'e2e', round(d['e2e']['value']), d['verify'].get('e2e_bitwise_device_forward'))"
+}
+
+call_q6() {
+  mkdir -p gpurun_out/r02q6; O=gpurun_out/r02q6
+  LRS_VERBOSE=1 timeout 300 python tools/ablate.py c3 base "LRS_WCONV_TH=4" "LRS_WCONV_TH=3" "LRS_WCONV_TH=4 LRS_WCONV_IPW=4" > $O/ablate_c3.log 2>&1
+  grep "wconv plan\|c3 \[" $O/ablate_c3.log
+}
+
