@@ -231,6 +231,8 @@ struct lrs_conv {
   uint32_t pw_smem = 0;
   int pw_grid_per_group = 0;  // CTAs per channel group at most
   std::vector<PwPlan> pw_cands;  // the cost model's best few plans (autotune_pw times them)
+  int force_wth = 0;             // autotune_w: the band height the windowed kernel's planner must take
+  int wth_max = 0;               // the tallest band height the planner found feasible
   void* pw_w = nullptr;       // per-group weight images
   void* pw_e = nullptr;       // per-group metadata images
   void* pw_tab = nullptr;     // per-group block tables
@@ -1129,7 +1131,8 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
     const int wcw = (tc - 1) * g.sw + kw;
     const int tbw = s1 ? wcw : tc;
     if (wcw > 256) continue;
-    const int th_env = getenv("LRS_WCONV_TH") ? atoi(getenv("LRS_WCONV_TH")) : 0;  // planner experiments
+    const int th_env = h->force_wth ? h->force_wth  // autotune_w's candidate
+                                    : (getenv("LRS_WCONV_TH") ? atoi(getenv("LRS_WCONV_TH")) : 0);  // planner experiments
     for (int th = std::min(ho, 64); th >= 1; --th) {
       if (th_env && th != th_env) continue;
       const int acc = make_units(th, tc, wcw, tbw, ipw, units);
@@ -1239,6 +1242,7 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
         }
         found = true;
         found_ipw = true;
+        h->wth_max = std::max(h->wth_max, th);
         break;
       }
       if (found) break;
@@ -1817,7 +1821,9 @@ void record_output(int dev, cudaStream_t s, const void* y, size_t ybytes) {
 // on the other 112).  Each plan runs back-to-back forwards on zero-filled scratch
 // buffers of batch_max images; the fastest stays.  LRS_NO_AUTOTUNE=1 keeps the model's
 // choice; any LRS_CORE_* override disables the tuning.
-static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d) {
+// best_us (optional): the winning plan's time per forward, or -1 when nothing was timed.
+static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d, float* best_us = nullptr) {
+  if (best_us) *best_us = -1.f;
   if (!h->use_core || getenv("LRS_NO_AUTOTUNE") || getenv("LRS_CORE_IPT") || getenv("LRS_CORE_TH") ||
       getenv("LRS_CORE_GRID") || h->skip)
     return LRS_OK;
@@ -1895,6 +1901,7 @@ static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d) {
   }
   if (ready && st == LRS_OK && bi >= 0) {
     apply_core_plan(h, d, std::get<0>(plans[bi]), std::get<1>(plans[bi]), std::get<2>(plans[bi]), std::get<3>(plans[bi]));
+    if (best_us) *best_us = best * 100.f;  // 10 forwards per timing
   } else {
     h->cp = keep;
     h->core_smem = keep_smem;
@@ -1909,6 +1916,116 @@ static lrs_status autotune_core(lrs_conv* h, const lrs_conv_desc* d) {
   if (s) cudaStreamDestroy(s);
   if (xs) cudaFree(xs);
   if (ys) cudaFree(ys);
+  return st;
+}
+
+// The windowed kernel's buffers and plan state, freed before autotune_w rebuilds it
+static void free_wconv(lrs_conv* h) {
+  for (void** b : {&h->w_as, &h->w_e, &h->w_dense_img, &h->w_gtab, &h->w_g, &h->t2b, &h->w_gb})
+    if (*b) {
+      cudaFree(*b);
+      *b = nullptr;
+    }
+  if (h->w_res) {
+    cudaFree(h->w_res);
+    h->w_res = nullptr;
+  }
+  h->use_w = false;
+  h->dbuf = false;
+  h->par = 0;
+  h->wx_ptr = nullptr;  // the X map's box depends on the band height
+}
+
+// Time the windowed kernel's band height: the cost model's choice against the tallest band
+// that fits (one tile per image group per M-tile), each with the core kernel's plan tuned
+// for it (autotune_core: the co-resident grid depends on the windowed kernel's tile count).
+// The model prices MMA issue and item hand-offs per block; at C3 with 128 images per GPU (the
+// 2-GPU shard) it picked 2-row bands (45.6 us) where 7-row bands with a co-resident core run
+// 42.7 us (profiles/r02_ablate_wconv_th_small_batch.log).  Every band height computes the same
+// products in the same order per output (tests/test_gpu_sparse_tc.py).  Any LRS_WCONV_* plan
+// override or LRS_NO_AUTOTUNE keeps the model's plan.  *core_tuned: autotune_core has run.
+static lrs_status autotune_w(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g, bool* core_tuned) {
+  *core_tuned = false;
+  if (!h->use_w || getenv("LRS_NO_AUTOTUNE") || getenv("LRS_WCONV_TH") || getenv("LRS_WCONV_IPW") ||
+      getenv("LRS_WCONV_PAIR") || getenv("LRS_WCONV_BPI") || getenv("LRS_WCONV_NS") || getenv("LRS_WCONV_CB") || h->skip)
+    return LRS_OK;
+  const int th0 = h->wp.th, thx = h->wth_max;
+  if (thx <= th0) return LRS_OK;
+  const int n = d->batch_max;
+  const size_t xb = static_cast<size_t>(n) * d->in_h * d->in_w * d->c_in * 2;
+  const size_t yb = static_cast<size_t>(n) * h->ho * h->wo * d->c_out * 2;
+  void *xs = nullptr, *ys = nullptr;
+  cudaError_t e = cudaMalloc(&xs, xb);
+  if (e == cudaSuccess) e = cudaMalloc(&ys, yb);
+  if (e == cudaErrorMemoryAllocation) {  // no room for the scratch: keep the model's plan
+    cudaGetLastError();
+    if (xs) cudaFree(xs);
+    return LRS_OK;
+  }
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  lrs_status st = LRS_OK;
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&e0);
+  if (e == cudaSuccess) e = cudaEventCreate(&e1);
+  if (e == cudaSuccess) e = cudaMemsetAsync(xs, 0, xb, s);
+  if (e != cudaSuccess) st = fail(LRS_ERR_CUDA, "autotune setup: %s", cudaGetErrorString(e));
+  const int cand[2] = {th0, thx};
+  float best = 1e30f;
+  int bi = -1, built = th0;
+  for (int i = 0; i < 2 && st == LRS_OK; ++i) {
+    if (cand[i] != built) {
+      free_wconv(h);
+      h->force_wth = cand[i];
+      st = build_wconv(h, d, g);
+      h->force_wth = 0;
+      built = cand[i];
+      if (st != LRS_OK) break;
+      if (!h->use_w) continue;  // not feasible after all
+      h->wp.epi = h->epi;
+      h->wp.relu = d->out_relu ? 1 : 0;
+      if ((st = setup_early(h, d)) != LRS_OK) break;
+    }
+    float us = -1.f;
+    if ((st = autotune_core(h, d, &us)) != LRS_OK) break;  // the core plan for this band height
+    if (us < 0.f) {  // no core plan to time: time the forward as it is
+      for (int r = 0; r < 3 && st == LRS_OK; ++r) st = lrs_conv_forward(h, xs, ys, n, s);
+      if (st != LRS_OK) break;
+      cudaEventRecord(e0, s);
+      for (int r = 0; r < 10 && st == LRS_OK; ++r) st = lrs_conv_forward(h, xs, ys, n, s);
+      cudaEventRecord(e1, s);
+      if (cudaEventSynchronize(e1) != cudaSuccess)
+        st = fail(LRS_ERR_CUDA, "autotune: %s", cudaGetErrorString(cudaGetLastError()));
+      float ms = 0.f;
+      if (st == LRS_OK) cudaEventElapsedTime(&ms, e0, e1);
+      us = ms * 100.f;
+    }
+    if (getenv("LRS_VERBOSE")) fprintf(stderr, "[lrs] autotune wconv th=%d: %.2f us/forward\n", cand[i], us);
+    if (st == LRS_OK && us < best) {
+      best = us;
+      bi = i;
+    }
+  }
+  if (st == LRS_OK && bi >= 0 && cand[bi] != built) {
+    free_wconv(h);
+    h->force_wth = cand[bi];
+    st = build_wconv(h, d, g);
+    h->force_wth = 0;
+    if (st == LRS_OK) {
+      h->wp.epi = h->epi;
+      h->wp.relu = d->out_relu ? 1 : 0;
+      st = setup_early(h, d);
+    }
+    if (st == LRS_OK) st = autotune_core(h, d);
+  }
+  *core_tuned = st == LRS_OK;
+  if (s) cudaStreamSynchronize(s);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (s) cudaStreamDestroy(s);
+  if (xs) cudaFree(xs);
+  if (ys) cudaFree(ys);
+  if (st == LRS_OK && !h->use_w) st = fail(LRS_ERR_UNSUPPORTED, "autotune: the windowed kernel's plan vanished");
   return st;
 }
 
@@ -2346,7 +2463,9 @@ lrs_status lrs_conv_create(const lrs_conv_desc* d, int device, lrs_conv** out) {
           return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
       }
   if ((st = setup_early(h, d)) != LRS_OK) return cleanup_fail(st);
-  if ((st = autotune_core(h, d)) != LRS_OK) return cleanup_fail(st);
+  bool core_tuned = false;
+  if ((st = autotune_w(h, d, g, &core_tuned)) != LRS_OK) return cleanup_fail(st);
+  if (!core_tuned && (st = autotune_core(h, d)) != LRS_OK) return cleanup_fail(st);
   if ((st = autotune_pw(h, d)) != LRS_OK) return cleanup_fail(st);
   cudaSetDevice(prev);
   *out = h;

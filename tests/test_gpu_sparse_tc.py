@@ -325,3 +325,37 @@ def test_cta_pair_bitwise_equal_single_without_overflow():
     torch.cuda.synchronize()
     assert torch.equal(ya, yb)
     parity.check(ya, oracle(inp), "bf16")
+
+
+@pytest.mark.parametrize("th", ["1", "2", "4"])
+def test_band_heights_bitwise_equal(th):
+    """autotune_w picks the windowed kernel's band height by timing; every height accumulates
+    each output in the same K order (sparse blocks by chunk and tap, then T, then the overflow
+    gather): bitwise equal to the tallest band (one tile per image group), and to the oracle."""
+    cfg = workloads.LayerConfig("th", 16, 7, 7, 512, 512, 3, 1, 1, 128, 128, 0.05, "bf16", seed=43)
+    inp = workloads.generate(cfg)
+    a = _make_env(inp, {"LRS_WCONV_TH": th})
+    b = _make_env(inp, {"LRS_WCONV_TH": "7"})
+    assert a.expand_kernel == 1 and b.expand_kernel == 1
+    x = torch.from_numpy(inp.x).to(torch.bfloat16).cuda()
+    ya, yb = a(x), b(x)
+    torch.cuda.synchronize()
+    assert torch.equal(ya, yb)
+    parity.check(ya, oracle(inp), "bf16")
+
+
+def test_autotuned_band_height_at_the_two_gpu_shard():
+    """C3 with 128 images (its 2-GPU shard): the cost model's band height and the tallest one
+    are both timed at create; whichever wins, Y matches the fp64 oracle on sampled images."""
+    cfg = workloads.CONFIGS["c3"]
+    inp = workloads.generate(cfg, batch=1)
+    from paper_2006_06443_b200 import LrsConv
+    layer = LrsConv.from_inputs(inp, batch_max=128)
+    x_np = workloads.generate_x(cfg, 128, seed=5)
+    y = layer(torch.from_numpy(x_np).to(torch.bfloat16).cuda())
+    torch.cuda.synchronize()
+    idx = np.array([0, 63, 127])
+    c = inp.cfg
+    ref = O.forward_factored(x_np[idx].astype(np.float64), inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx,
+                             inp.values, c.stride, c.pad)
+    parity.check(y[idx], ref, "bf16")

@@ -501,3 +501,25 @@ call_q6() {
   grep "wconv plan\|c3 \[" $O/ablate_c3.log
 }
 
+call_q7() {
+  mkdir -p gpurun_out/r02q7; O=gpurun_out/r02q7
+  LRS_VERBOSE=1 timeout 300 python tools/ablate.py c3 "CFG_batch=32" "CFG_batch=32 LRS_WCONV_IPW=4" "CFG_batch=32 LRS_WCONV_TH=4" "CFG_batch=32 LRS_WCONV_IPW=4 LRS_WCONV_TH=4" "CFG_batch=64" "CFG_batch=128" > $O/ablate_c3.log 2>&1
+  LRS_VERBOSE=1 timeout 300 python tools/ablate.py c2_bf16 "CFG_batch=8" "CFG_batch=16" "CFG_batch=32" > $O/ablate_c2.log 2>&1
+  LRS_VERBOSE=1 timeout 300 python tools/ablate.py c4 "CFG_batch=16" "CFG_batch=32" "CFG_batch=64" > $O/ablate_c4.log 2>&1
+  grep "wconv plan\|pw plan\|\]" $O/ablate_c3.log $O/ablate_c2.log $O/ablate_c4.log | grep -v autotune
+}
+
+call_q8() {
+  mkdir -p gpurun_out/r02q8; O=gpurun_out/r02q8
+  LRS_VERBOSE=1 timeout 300 python tools/ablate.py c3 base "LRS_WCONV_TH=2" "LRS_WCONV_TH=1" "CFG_batch=128 LRS_WCONV_TH=7" > $O/ablate_c3.log 2>&1
+  grep "wconv plan\|c3 \[" $O/ablate_c3.log
+}
+
+call_q9() {
+  mkdir -p gpurun_out/r02q9; O=gpurun_out/r02q9
+  timeout 900 python -m pytest tests/test_gpu_sparse_tc.py tests/test_gpu_bench_pattern.py tests/test_gpu_overlap.py -x -q > $O/pytest.log 2>&1; echo "rc=$?" > $O/rc.txt
+  LRS_VERBOSE=1 timeout 300 python tools/ablate.py c3 base "CFG_batch=128" "CFG_batch=64" "CFG_batch=32" > $O/ablate_c3.log 2>&1
+  LRS_VERBOSE=1 timeout 300 python tools/ablate.py c2_bf16 base "CFG_batch=32" "CFG_batch=16" "CFG_batch=8" > $O/ablate_c2.log 2>&1
+  cat $O/rc.txt; tail -2 $O/pytest.log; grep "autotune wconv\|c3 \[\|c2_bf16 \[" $O/ablate_c3.log $O/ablate_c2.log
+}
+
