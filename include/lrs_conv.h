@@ -124,8 +124,9 @@ typedef struct lrs_conv_desc {
  * bf16 stride-1 layers run a1 + a2 (or a1 + the CP depthwise pair) in one
  * kernel whose tile plan is chosen at create by timing a few candidate plans
  * on the device (back-to-back forwards on zero-filled scratch of batch_max
- * images; ~ms; synchronous on a private stream).  Every plan computes the same
- * bits.  LRS_NO_AUTOTUNE=1 in the environment keeps the cost model's plan, and
+ * images; ~ms; synchronous on a private stream); so are the windowed fused
+ * kernel's band height (jointly with that core plan) and the 1x1 pointwise
+ * kernel's plan.  Every plan computes the same bits.  LRS_NO_AUTOTUNE=1 in the environment keeps the cost model's plan, and
  * so does a scratch allocation that runs out of memory (any other CUDA error
  * during tuning is LRS_ERR_CUDA).
  * OUT_OF_MEMORY / CUDA: allocation or driver failure (no handle is returned).
