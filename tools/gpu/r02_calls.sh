@@ -523,3 +523,17 @@ call_q9() {
   cat $O/rc.txt; tail -2 $O/pytest.log; grep "autotune wconv\|c3 \[\|c2_bf16 \[" $O/ablate_c3.log $O/ablate_c2.log
 }
 
+call_r1() {
+  mkdir -p gpurun_out/r02r1; O=gpurun_out/r02r1
+  LRS_VERBOSE=1 timeout 300 python tools/ablate.py c3 base "LRS_CORE_IPT=1 LRS_CORE_TH=7" "LRS_CORE_IPT=2 LRS_CORE_TH=7" "LRS_CORE_IPT=1 LRS_CORE_TH=4" "LRS_CORE_IPT=1 LRS_CORE_TH=7 LRS_CORE_GRID=148" > $O/ablate_c3.log 2>&1
+  grep "core:\|c3 \[" $O/ablate_c3.log | grep -v autotune | tail -12
+}
+
+call_r2() {
+  mkdir -p gpurun_out/r02r2; O=gpurun_out/r02r2
+  timeout 300 python tools/ablate.py c3 base base > $O/ablate_c3.log 2>&1
+  timeout 300 python tools/ablate.py c2_bf16 base base > $O/ablate_c2.log 2>&1
+  timeout 900 python -m pytest tests/test_gpu_overlap.py tests/test_gpu_bench_pattern.py -x -q > $O/pytest.log 2>&1; echo "rc=$?" > $O/rc.txt
+  cat $O/rc.txt; tail -2 $O/pytest.log; grep "\[" $O/ablate_c3.log $O/ablate_c2.log
+}
+
