@@ -537,3 +537,18 @@ call_r2() {
   cat $O/rc.txt; tail -2 $O/pytest.log; grep "\[" $O/ablate_c3.log $O/ablate_c2.log
 }
 
+call_s1() {
+  mkdir -p gpurun_out/r02s1; O=gpurun_out/r02s1
+  LRS_EXPERIMENTS=1 python -m paper_2006_06443_b200._build --force > $O/build.log 2>&1
+  timeout 300 python tools/ctrace.py c3 > $O/ctrace_c3.log 2>&1
+  cat $O/ctrace_c3.log
+}
+
+call_s2() {
+  mkdir -p gpurun_out/r02s2; O=gpurun_out/r02s2
+  timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" > $O/rc.txt
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/rc.txt
+  timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench rc=$?" >> $O/rc.txt
+  cat $O/rc.txt; tail -1 $O/pytest_gpu.log
+}
+
