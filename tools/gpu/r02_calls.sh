@@ -552,3 +552,11 @@ call_s2() {
   cat $O/rc.txt; tail -1 $O/pytest_gpu.log
 }
 
+call_t1() {
+  mkdir -p gpurun_out/r02t1; O=gpurun_out/r02t1
+  timeout 600 python -m pytest tests/test_gpu_sparse_tc.py -x -q -k "tma_store" > $O/pytest.log 2>&1; echo "rc=$?" > $O/rc.txt
+  timeout 300 python tools/ablate.py c3 base "LRS_WCONV_EPI_TMA=1" > $O/ablate_c3.log 2>&1
+  timeout 300 python tools/ablate.py c2_bf16 base "LRS_WCONV_EPI_TMA=1" > $O/ablate_c2.log 2>&1
+  cat $O/rc.txt; tail -3 $O/pytest.log; grep "\[" $O/ablate_c3.log $O/ablate_c2.log
+}
+
