@@ -351,29 +351,53 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const uint32_t win_margin_ = static_cast<uint32_t>(smem_param(prm + 33));
     const uint32_t shift_x_ = rank ? static_cast<uint32_t>(smem_param(prm + 34)) : 0u;
     const uint32_t shift_t_ = rank ? static_cast<uint32_t>(smem_param(prm + 35)) : 0u;
+    // the M-tile's block stream (chunk starts + per-block tap offsets), staged in shared
+    // memory: a global load on the issue path measured ~250 ns each (tools/wtrace.py)
+    int* so_s = reinterpret_cast<int*>(smem + off_res_);   // [n_ck + 1], relative to mt0
+    uint32_t* tap_s = reinterpret_cast<uint32_t*>(so_s + n_ck_ + 1);
+    // CTAs own contiguous tile ranges, M-tile fastest: consecutive tiles of a CTA share
+    // their windows; with one ring buffer per window (nwb == nwin) a window still resident
+    // from the previous tile is reused instead of re-loaded
+    const bool contig = nwb_ == nwin;
+    const int n_u = PAIR ? n_tiles_ >> 1 : n_tiles_;
+    const int t_begin = contig ? static_cast<int>(static_cast<long long>(g_id) * n_u / g_n) : g_id;
+    const int t_end = contig ? static_cast<int>(static_cast<long long>(g_id + 1) * n_u / g_n) : n_u;
+    const int t_step = contig ? 1 : g_n;
+    auto tile_of = [&](int tu) {
+      const int hm = n_mt_ >> 1;
+      return PAIR ? (tu / hm) * n_mt_ + 2 * (tu % hm) + static_cast<int>(rank) : tu;
+    };
+    // CTA start: the first window's TMA goes out at once (it needs no table), and the whole
+    // warp stages the first M-tile's block stream -- one thread's ~80 loads had delayed the
+    // first window by ~2 us (profiles/r02_wtrace_c3_early.log: issued at 3.3 us)
+    int first_mt = -1, first_mt0 = 0;
+    bool first_issued = false;
+    if (t_begin < t_end) {
+      const TileCoord tc0 = tile_coord_v(tile_of(t_begin), n_mt_, cbands_, bands_, th_, tcols_, ipw_);
+      if (lane == 0 && n_xw_ > 0 && !WDBG(p, 64)) {
+        mbar_arrive_expect_tx(&win_full[0], static_cast<uint32_t>(cpw_) * x_win_bytes_);
+        for (int q = 0; q < cpw_; ++q)
+          tma_load_4d(smem + win_margin_ - shift_x_ + q * x_win_bytes_, &p.tmX, &win_full[0], q * 64, tc0.n0,
+                      tc0.wo0 * sw_ - pw_, tc0.ho0 * sh_ - ph_);
+        first_issued = true;
+      }
+      first_mt = tc0.mt;
+      first_mt0 = __ldg(p.stream_off + first_mt * n_ck_);
+      for (int i = lane; i <= n_ck_; i += 32) so_s[i] = __ldg(p.stream_off + first_mt * n_ck_ + i) - first_mt0;
+      __syncwarp();
+      const int len = so_s[n_ck_];
+      for (int i = lane; i < len; i += 32) tap_s[i] = __ldg(p.blk_tap + first_mt0 + i);
+      __syncwarp();
+    }
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
       int it = 0, wg = 0, buf = 0;
       uint32_t wph = 0, gph = 0;
-      // the M-tile's block stream (chunk starts + per-block tap offsets), staged in shared
-      // memory by independent (pipelined) loads when the M-tile changes: a global load on
-      // the issue path measured ~250 ns each (tools/wtrace.py producer stamps)
-      int* so_s = reinterpret_cast<int*>(smem + off_res_);   // [n_ck + 1], relative to mt0
-      uint32_t* tap_s = reinterpret_cast<uint32_t*>(so_s + n_ck_ + 1);
-      int cur_mt = -1, mt0 = 0;
+      int cur_mt = first_mt, mt0 = first_mt0;
       bool waited = false;
-      // CTAs own contiguous tile ranges, M-tile fastest: consecutive tiles of a CTA share
-      // their windows; with one ring buffer per window (nwb == nwin) a window still resident
-      // from the previous tile is reused instead of re-loaded
-      const bool contig = nwb_ == nwin;
-      const int n_u = PAIR ? n_tiles_ >> 1 : n_tiles_;
-      const int t_begin = contig ? static_cast<int>(static_cast<long long>(g_id) * n_u / g_n) : g_id;
-      const int t_end = contig ? static_cast<int>(static_cast<long long>(g_id + 1) * n_u / g_n) : n_u;
-      const int t_step = contig ? 1 : g_n;
       int prev_win = -1;
       for (int tu = t_begin; tu < t_end; tu += t_step) {
-        const int hm = n_mt_ >> 1;
-        const int tile = PAIR ? (tu / hm) * n_mt_ + 2 * (tu % hm) + static_cast<int>(rank) : tu;
+        const int tile = tile_of(tu);
         const TileCoord tc = tile_coord_v(tile, n_mt_, cbands_, bands_, th_, tcols_, ipw_);
         const int win_key = tile / n_mt_;
         const bool reuse = nwb_ == nwin && win_key == prev_win;
@@ -422,7 +446,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
             ++it;
           } else {
             const int c = w * cpw_;  // first chunk of this window
-            if (!(WDBG(p, 64)) && !reuse) {
+            if (!(WDBG(p, 64)) && !reuse && !(first_issued && wg == 0)) {
               mbar_arrive_expect_tx(&win_full[buf], static_cast<uint32_t>(cpw_) * x_win_bytes_);
               for (int q = 0; q < cpw_; ++q)
                 tma_load_4d(wdst + q * x_win_bytes_, &p.tmX, &win_full[buf], (c + q) * 64, tc.n0,
