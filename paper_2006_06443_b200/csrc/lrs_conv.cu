@@ -1453,6 +1453,10 @@ lrs_status build_wconv(lrs_conv* h, const lrs_conv_desc* d, const ConvGeom& g) {
   w.n_ck = n_ck;
   w.cpw = cpw;
   w.n_xw = d->nnz > 0 ? n_ck / cpw : 0;  // an empty S needs no X windows at all (LR-only layers)
+  // k x k layers interleave the dense windows with the last X windows (1 x 1 layers keep
+  // them at the end: one tap per X window hides nothing, and the pointwise kernel's
+  // summation order stays the windowed kernel's)
+  w.ilv = (taps > 1 && w.n_xw >= n_tk + n_gk && !getenv("LRS_WCONV_DENSE_LAST")) ? w.n_xw - (n_tk + n_gk) : -1;
   w.n_tk = n_tk;
   w.t_kc = t_kc;
   w.sw_t = sw_t;

@@ -137,7 +137,20 @@ struct WconvParams {
   // shift_t (T / G windows, sw_t rows) bytes before its buffer (win_margin bytes reserved)
   int pair;
   uint32_t win_margin, shift_x, shift_t;
+  // window order of a tile: -1 = all X windows, then the dense (T, G) ones; >= 0 = that many
+  // X windows first, then X and dense windows alternate, so each dense window's load hides
+  // behind an X window's k*k taps of MMAs instead of queueing behind another short window
+  int ilv;
 };
+
+// window p of a tile -> its dense chunk (>= 0: T chunks, then G chunks), or -(1 + its X
+// window index)
+__device__ __forceinline__ int win_map(int p, int n_xw, int ilv) {
+  if (ilv < 0) return p >= n_xw ? p - n_xw : -(1 + p);
+  if (p < ilv) return -(1 + p);
+  const int q = p - ilv;
+  return (q & 1) ? (q >> 1) : -(1 + ilv + (q >> 1));
+}
 
 struct TileCoord {
   int mt, n0, ho0, wo0, j0;
@@ -279,6 +292,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     prm[33] = static_cast<int>(p.win_margin);
     prm[34] = static_cast<int>(p.shift_x);
     prm[35] = static_cast<int>(p.shift_t);
+    prm[36] = p.ilv;
     const uint32_t nf = (PAIR && rank == 0) ? 2u : 1u;  // + the peer relay's arrival
     for (int i = 0; i < p.nwb; ++i) {
       mbar_init(&win_full[i], nf);
@@ -348,6 +362,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const int tcols_ = static_cast<int>(smem_param(prm + 27));
     const int n_gk_ = smem_param(prm + 32);
     const int n_dk_ = n_tk_ + n_gk_;  // dense chunks per M-tile (T, then G)
+    const int ilv_ = smem_param(prm + 36);
     const uint32_t win_margin_ = static_cast<uint32_t>(smem_param(prm + 33));
     const uint32_t shift_x_ = rank ? static_cast<uint32_t>(smem_param(prm + 34)) : 0u;
     const uint32_t shift_t_ = rank ? static_cast<uint32_t>(smem_param(prm + 35)) : 0u;
@@ -411,12 +426,11 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         }
         for (int w = 0; w < nwin; ++w, ++wg) {
           if (wg >= nwb_) mbar_wait(&win_empty[buf], wph ^ 1u);
-          const int tk_ = w - n_xw_;
+          const int tk = win_map(w, n_xw_, ilv_);  // >= 0: dense (T, then G) chunk; < 0: X window
           // (pair, rank 1: the window sits N/2 B rows earlier, so the leader's descriptors,
           // which address both CTAs at the same offset, see the unit's second half here)
-          uint8_t* wdst = smem + win_margin_ + buf * win_stride_ - (tk_ >= 0 ? shift_t_ : shift_x_);
+          uint8_t* wdst = smem + win_margin_ + buf * win_stride_ - (tk >= 0 ? shift_t_ : shift_x_);
           if (WTRACE(p) && blockIdx.x == 0 && wg < 16) p.trace[3600 + wg] = gtimer();
-          const int tk = w - n_xw_;  // >= 0: dense (T) window, after the tile's sparse ones
           if (tk >= 0 && !waited) {
             pdl_wait();
             pdl_launch_dependents();
@@ -445,7 +459,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
                       &a_full[slot]);
             ++it;
           } else {
-            const int c = w * cpw_;  // first chunk of this window
+            const int c = (-tk - 1) * cpw_;  // first chunk of this X window
             if (!(WDBG(p, 64)) && !reuse && !(first_issued && wg == 0)) {
               mbar_arrive_expect_tx(&win_full[buf], static_cast<uint32_t>(cpw_) * x_win_bytes_);
               for (int q = 0; q < cpw_; ++q)
@@ -548,6 +562,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
     const int t_end = contig ? static_cast<int>(static_cast<long long>(g_id + 1) * n_u / g_n) : n_u;
     const int t_step = contig ? 1 : g_n;
     (void)cbands_; (void)bands_; (void)th_; (void)tcols_; (void)n_mt_;
+    const int ilv_m = smem_param(prm + 36);
     if (PAIR && !lead) {
       // ---------------------------------------------------------- pair relay (rank 1)
       // Mirror the leader's consumption order: every window and A/E item this CTA's
@@ -559,7 +574,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
           for (int w = 0; w < nwin; ++w) {
             mbar_wait(&win_full[buf], wph);
             mbar_arrive_remote(&win_full[buf], 0);
-            if (w >= n_xw_) {
+            if (win_map(w, n_xw_, ilv_m) >= 0) {
               mbar_wait(&a_full[slot], ph);
               mbar_arrive_remote(&a_full[slot], 0);
               if (++slot == ns_) { slot = 0; ph ^= 1u; }
@@ -596,7 +611,7 @@ __global__ void __launch_bounds__(kWThreads, 1) lrs_wconv_kernel(const __grid_co
         tc_fence_after();
         if (WTRACE(p) && blockIdx.x == 0 && k < 16 && w < 8) p.trace[200 + 16 * k + 2 * w + 1] = gtimer();
         const uint32_t boff = static_cast<uint32_t>(buf) * win16;
-        if (w >= n_xw_) {  // dense window: the accumulator already holds the sparse term
+        if (win_map(w, n_xw_, ilv_m) >= 0) {  // dense window: the accumulator already holds a sparse part
           if (PAIR) mbar_wait_cluster(&a_full[slot], ph);
           else mbar_wait(&a_full[slot], ph);
           tc_fence_after();

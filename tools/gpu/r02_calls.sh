@@ -568,3 +568,11 @@ call_u1() {
   cat $O/rc.txt; tail -2 $O/pytest.log; grep "\[" $O/ablate_c3.log $O/ablate_c2.log
 }
 
+call_u2() {
+  mkdir -p gpurun_out/r02u2; O=gpurun_out/r02u2
+  timeout 300 python tools/ablate.py c3 base "LRS_WCONV_DENSE_LAST=1" base > $O/ablate_c3.log 2>&1
+  timeout 300 python tools/ablate.py c2_bf16 base "LRS_WCONV_DENSE_LAST=1" > $O/ablate_c2.log 2>&1
+  timeout 900 python -m pytest tests/test_gpu_sparse_tc.py tests/test_gpu_parity.py tests/test_gpu_bench_pattern.py tests/test_gpu_overlap.py tests/test_gpu_pw.py -x -q > $O/pytest.log 2>&1; echo "rc=$?" > $O/rc.txt
+  cat $O/rc.txt; tail -2 $O/pytest.log; grep "\[" $O/ablate_c3.log $O/ablate_c2.log
+}
+
