@@ -146,8 +146,9 @@ lrs_status lrs_conv_create(const lrs_conv_desc *desc, int device, lrs_conv **out
  * Kernels are launched with programmatic dependent launch: each waits
  * (griddepcontrol.wait) before touching what the kernel before it may still
  * write.  Layers whose projection + core kernel feeds the fused kernel (bf16,
- * stride 1, not an SVD pair) keep two T2 buffers and let the core kernel start
- * computing before the previous kernel on the stream has finished, unless x
+ * stride 1, not an SVD pair) keep two T2 buffers, and 1x1 SVD pairs on the pointwise
+ * kernel two T1 buffers, and let that first kernel start computing before the
+ * previous kernel on the stream has finished, unless x
  * overlaps the output of the library's previous forward on that stream (then it
  * waits first, as every other kernel does); the library assumes that kernels the
  * caller enqueues between forwards do not trigger their dependents early

@@ -249,6 +249,9 @@ struct lrs_conv {
   bool dbuf = false;
   int par = 0;                  // buffer parity of the next forward
   void* t2b = nullptr;          // second T2
+  void* t1b = nullptr;          // second T1 (projection -> pointwise kernel)
+  bool dbuf_pw = false;         // the early-start protocol on the projection -> pointwise chain
+  CUtensorMap tmT_pw_par[2];    // the pointwise kernel's T1 maps, per buffer
   void* w_gb = nullptr;         // second overflow-gather scratch
   CUtensorMap tmT_par[2], tmG_par[2];
   void* w_gtab = nullptr;       // overflow-gather slot table (WconvParams::g_tab)
@@ -1761,6 +1764,17 @@ const char* lrs_conv_last_error(void) { return g_err.c_str(); }
 // scratch) with the fused kernel's tensor maps for both, so forward f + 1's core kernel can
 // run while forward f's fused kernel still reads its T2 (LRS_NO_EARLY=1: off).
 static lrs_status setup_early(lrs_conv* h, const lrs_conv_desc* d) {
+  if (h->use_pw && !h->pw_ft && !getenv("LRS_NO_EARLY")) {
+    // the projection GEMM -> pointwise kernel chain: T1 alternates between two buffers
+    const size_t t1_bytes = static_cast<size_t>(d->batch_max) * d->in_h * d->in_w * h->r1p * h->esz;
+    if (!h->t1b && cudaMalloc(&h->t1b, t1_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      h->t1b = nullptr;
+      return LRS_OK;  // no room: keep the single-buffer protocol
+    }
+    h->dbuf_pw = true;
+    return LRS_OK;
+  }
   if (!h->use_core || !h->use_w || h->svd || getenv("LRS_NO_EARLY")) return LRS_OK;
   WconvParams& w = h->wp;
   const size_t t2_bytes = static_cast<size_t>(d->batch_max) * h->ho * h->wo * h->r2p * h->esz;
@@ -2574,6 +2588,18 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
   h->a1.p.tmA = h->xmap;
   h->a1.p.m_total = static_cast<int>(pin);
   h->a1.p.g.n = n;
+  int pw_par = 0;
+  h->a1.p.early = 0;
+  h->a1.p.out = h->t1;
+  if (h->dbuf_pw) {
+    // the projection of forward f+1 may run while the pointwise kernel of f still reads the
+    // other T1 (same protocol as the core kernel's T2 above)
+    pw_par = h->par;
+    h->par ^= 1;
+    h->a1.p.out = pw_par ? h->t1b : h->t1;
+    const size_t xbytes = static_cast<size_t>(pin) * d.c_in * esz;
+    h->a1.p.early = x_after_previous_output(h->device, stream, x, xbytes) ? 0 : 1;
+  }
   if (!h->use_core && !h->pw_ft && !(h->skip & 1) &&
       (st = launch(h, 0, h->a1, dim3(static_cast<unsigned>((pin + kTileM - 1) / kTileM)), stream)) != LRS_OK)
     return st;
@@ -2594,9 +2620,10 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
         uint64_t strides[1] = {static_cast<uint64_t>(h->r1p) * 2};
         uint32_t box[2] = {static_cast<uint32_t>(q.t_kc), static_cast<uint32_t>(q.bp)};
         uint32_t estr[2] = {1, 1};
-        if ((st = encode_t(&q.tmT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, h->t1, dims, strides, box, estr, q.sw_t)) !=
-            LRS_OK)
-          return st;
+        for (int b = 0; b < (h->dbuf_pw ? 2 : 1); ++b)
+          if ((st = encode_t(&h->tmT_pw_par[b], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, b ? h->t1b : h->t1, dims, strides,
+                             box, estr, q.sw_t)) != LRS_OK)
+            return st;
       }
       h->px_ptr = x;
       h->px_n = n;
@@ -2611,6 +2638,7 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
       h->py_ptr = y;
       h->py_n = n;
     }
+    if (!h->pw_ft) q.tmT = h->tmT_pw_par[pw_par];
     q.y = y;
     q.P = static_cast<int>(pin);
     q.n_pt = static_cast<int>((pin + q.bp - 1) / q.bp);
@@ -2789,7 +2817,7 @@ lrs_status lrs_conv_destroy(lrs_conv* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->t1, h->t2, h->ent, h->ent_ptr, h->hx, h->hy,
-                  h->w_as, h->w_e, h->w_res, h->w_dense_img, h->w_gtab, h->w_g, h->t2b, h->w_gb, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc,
+                  h->w_as, h->w_e, h->w_res, h->w_dense_img, h->w_gtab, h->w_g, h->t2b, h->w_gb, h->t1b, h->sp_ent, h->sp_ptr, h->w_cpb, h->w_cpc,
                   h->sp_uo, h->epi, h->pw_w, h->pw_e, h->pw_tab, h->pw_u};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -2953,7 +2981,7 @@ lrs_status lrs_conv_debug_trace(lrs_conv* h, void* dev_buf) {
 lrs_status lrs_conv_debug_buffer(const lrs_conv* h, int32_t which, const void** ptr, int32_t* ld) {
   if (!h || !ptr || !ld) return fail(LRS_ERR_INVALID_ARGUMENT, "NULL argument");
   if (which == 0) {
-    *ptr = h->t1;
+    *ptr = (h->dbuf_pw && h->par == 0) ? h->t1b : h->t1;  // the buffer the last forward wrote
     *ld = h->r1p;
   } else if (which == 1) {
     *ptr = (h->dbuf && h->par == 0) ? h->t2b : h->t2;  // the buffer the last forward wrote

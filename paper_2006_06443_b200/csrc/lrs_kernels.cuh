@@ -76,6 +76,9 @@ struct GemmParams {
   int out_cols;           // EPI_STORE: valid destination columns (0: all); N chunk c writes columns c*bn..
   uint32_t smem_sparse_off;
   uint32_t smem_bar_off;
+  // 1: compute at once, wait for the previous kernel only before exiting (the projection of
+  // a 1x1 SVD pair whose T1 alternates between two buffers; lrs_conv.cu forward_impl)
+  int early;
   SparseParams sp;
 };
 
@@ -199,8 +202,8 @@ __global__ void __launch_bounds__(kThreads, 1) lrs_gemm_kernel(const __grid_cons
   const uint32_t tmem = *tmem_slot;
   // PDL: the prologue above overlapped the previous kernel's tail; from here on
   // we read its outputs (and overwrite buffers it may read)
-  pdl_wait();  // the previous kernel's output is visible from here on
-  pdl_launch_dependents();  // only after the wait: every kernel before us is then complete
+  if (!p.early) pdl_wait();  // the previous kernel's output is visible from here on
+  pdl_launch_dependents();  // (default: only after the wait, so every kernel before us is complete)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -464,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) lrs_gemm_kernel(const __grid_cons
     tc_fence_after();
     tmem_dealloc(tmem, p.tmem_cols);
   }
+  if (p.early) pdl_wait();  // completion of this grid still implies the previous kernel's
 }
 
 }  // namespace lrs

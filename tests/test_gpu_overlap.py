@@ -153,3 +153,36 @@ def test_early_start_bitwise_equal_to_waiting(name):
         outs[mode] = ys
     for a, b in zip(outs["early"], outs["wait"]):
         assert torch.equal(a, b)
+
+
+def test_pointwise_chain_early_start():
+    """The same protocol on the 1x1 SVD-pair chain (projection GEMM -> pointwise kernel, T1
+    double-buffered): rotating inputs into one output buffer, and a layer fed its own output,
+    enqueued without syncs -- bitwise equal to one forward at a time."""
+    cfg = workloads.LayerConfig("pw_chain", 32, 14, 14, 256, 256, 1, 1, 0, 64, 64, 0.01, "bf16", svd=True, seed=51)
+    inp = workloads.generate(cfg)
+    layer = make(inp, cfg.batch)
+    assert layer.expand_kernel == 2
+    xs = [torch.from_numpy(workloads.generate_x(cfg, cfg.batch, seed=400 + i)).to(torch.bfloat16).cuda()
+          for i in range(5)]
+    ref = one_at_a_time([layer] * 5, xs)
+    y = torch.empty_like(ref[0])
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for x in xs:
+            layer.forward_into(x, y, stream=s)
+    s.synchronize()
+    assert torch.equal(y, ref[-1])
+    # self-feeding: x -> p -> q -> p
+    r = xs[0]
+    for _ in range(3):
+        torch.cuda.synchronize()
+        r = layer(r).clone()
+    torch.cuda.synchronize()
+    p, q = torch.empty_like(xs[0]), torch.empty_like(xs[0])
+    with torch.cuda.stream(s):
+        layer.forward_into(xs[0], p, stream=s)
+        layer.forward_into(p, q, stream=s)
+        layer.forward_into(q, p, stream=s)
+    s.synchronize()
+    assert torch.equal(p, r)

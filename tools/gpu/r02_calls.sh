@@ -576,3 +576,10 @@ call_u2() {
   cat $O/rc.txt; tail -2 $O/pytest.log; grep "\[" $O/ablate_c3.log $O/ablate_c2.log
 }
 
+call_v1() {
+  mkdir -p gpurun_out/r02v1; O=gpurun_out/r02v1
+  timeout 900 python -m pytest tests/test_gpu_overlap.py tests/test_gpu_pw.py tests/test_gpu_bench_pattern.py tests/test_gpu_parity.py -x -q > $O/pytest.log 2>&1; echo "rc=$?" > $O/rc.txt
+  timeout 300 python tools/ablate.py c4 base "LRS_NO_EARLY=1" base > $O/ablate_c4.log 2>&1
+  cat $O/rc.txt; tail -3 $O/pytest.log; grep "c4 \[" $O/ablate_c4.log
+}
+
