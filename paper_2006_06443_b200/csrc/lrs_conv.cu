@@ -251,6 +251,7 @@ struct lrs_conv {
   void* t2b = nullptr;          // second T2
   void* t1b = nullptr;          // second T1 (projection -> pointwise kernel)
   bool dbuf_pw = false;         // the early-start protocol on the projection -> pointwise chain
+  bool no_early = false;        // LRS_NO_EARLY at create
   CUtensorMap tmT_pw_par[2];    // the pointwise kernel's T1 maps, per buffer
   void* w_gb = nullptr;         // second overflow-gather scratch
   CUtensorMap tmT_par[2], tmG_par[2];
@@ -1764,6 +1765,7 @@ const char* lrs_conv_last_error(void) { return g_err.c_str(); }
 // scratch) with the fused kernel's tensor maps for both, so forward f + 1's core kernel can
 // run while forward f's fused kernel still reads its T2 (LRS_NO_EARLY=1: off).
 static lrs_status setup_early(lrs_conv* h, const lrs_conv_desc* d) {
+  h->no_early = getenv("LRS_NO_EARLY") != nullptr;
   if (h->use_pw && !h->pw_ft && !getenv("LRS_NO_EARLY")) {
     // the projection GEMM -> pointwise kernel chain: T1 alternates between two buffers
     const size_t t1_bytes = static_cast<size_t>(d->batch_max) * d->in_h * d->in_w * h->r1p * h->esz;
@@ -2534,6 +2536,11 @@ lrs_status forward_impl(lrs_conv* h, const void* x, void* y, int32_t n, cudaStre
     q.x = static_cast<const float*>(x);
     q.y = static_cast<float*>(y);
     q.n = n;
+    // early start unless X may be the previous kernel's output (the registry of the
+    // library's last output on this stream); LRS_NO_EARLY=1 at create disables it
+    q.early = (!h->no_early &&
+               !x_after_previous_output(h->device, stream, x, static_cast<size_t>(n) * d.in_h * d.in_w * d.c_in * esz))
+                  ? 1 : 0;
     cudaEvent_t e1 = nullptr;
     if ((st = time_begin(h, 2, stream, &e1)) != LRS_OK) return st;
     LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_tiny_kernel), dim3(static_cast<unsigned>(n * q.bands * q.cbands)),

@@ -40,6 +40,10 @@ struct TinyParams {
   uint32_t off_t1, off_t2, off_u, off_g, off_uo, off_rp, off_ec, off_ev;  // shared-memory carve-up (bytes)
   const float2* epi;  // per output channel (scale, bias) of the fused output epilogue, or NULL
   int relu;
+  // 1: X is not the previous kernel's output (lrs_conv.cu forward_impl): compute at once and
+  // wait for the previous kernel only before the first store of Y (the one buffer a previous
+  // forward may still be writing)
+  int early;
 };
 
 __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_constant__ TinyParams p) {
@@ -73,8 +77,8 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
     ecs[i] = __ldg(p.ent_c + i);
     evs[i] = __ldg(p.ent_v + i);
   }
-  pdl_wait();  // the previous kernel's output is visible from here on
-  pdl_launch_dependents();  // only after the wait: every kernel before us is then complete
+  if (!p.early) pdl_wait();  // the previous kernel's output is visible from here on
+  pdl_launch_dependents();
   // ---- X window [c][row][col] (zero padding), 4 channels per load, 4 loads in flight
   {
     const int nit = wrc * (p.cin / 4);
@@ -186,6 +190,7 @@ __global__ void __launch_bounds__(kTyThreads, 1) lrs_tiny_kernel(const __grid_co
   }
   __syncthreads();
   // ---- a3 + a4 + a5: thread = (output channel j, group of positions); Y written once
+  if (p.early) pdl_wait();  // before touching Y
   const int pgroups = max(1, kTyThreads / p.cout);
   const int per = (npos + pgroups - 1) / pgroups;
   for (int it = threadIdx.x; it < p.cout * pgroups; it += kTyThreads) {

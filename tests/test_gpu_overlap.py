@@ -186,3 +186,35 @@ def test_pointwise_chain_early_start():
         layer.forward_into(q, p, stream=s)
     s.synchronize()
     assert torch.equal(p, r)
+
+
+def test_tiny_kernel_early_start():
+    """The one-kernel fp32 path (lrs_tiny.cuh) computes a forward before the previous one has
+    finished and waits only before storing Y: rotating inputs into one output buffer and a
+    layer fed its own output, enqueued without syncs -- bitwise equal to one at a time."""
+    from paper_2006_06443_b200 import LrsConv
+    cfg = workloads.LayerConfig("tiny_chain", 1, 14, 14, 64, 64, 3, 1, 1, 16, 16, 0.02, "f32", seed=53)
+    inp = workloads.generate(cfg)
+    layer = LrsConv.from_inputs(inp, batch_max=1)
+    assert layer.sparse_engine[0] == 3  # the tiny kernel
+    xs = [torch.from_numpy(workloads.generate_x(cfg, 1, seed=500 + i)).cuda() for i in range(6)]
+    ref = one_at_a_time([layer] * 6, xs)
+    y = torch.empty_like(ref[0])
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for x in xs:
+            layer.forward_into(x, y, stream=s)
+    s.synchronize()
+    assert torch.equal(y, ref[-1])
+    r = xs[0]
+    for _ in range(3):
+        torch.cuda.synchronize()
+        r = layer(r).clone()
+    torch.cuda.synchronize()
+    p, q = torch.empty_like(xs[0]), torch.empty_like(xs[0])
+    with torch.cuda.stream(s):
+        layer.forward_into(xs[0], p, stream=s)
+        layer.forward_into(p, q, stream=s)
+        layer.forward_into(q, p, stream=s)
+    s.synchronize()
+    assert torch.equal(p, r)

@@ -583,3 +583,10 @@ call_v1() {
   cat $O/rc.txt; tail -3 $O/pytest.log; grep "c4 \[" $O/ablate_c4.log
 }
 
+call_v2() {
+  mkdir -p gpurun_out/r02v2; O=gpurun_out/r02v2
+  timeout 600 python -m pytest tests/test_gpu_overlap.py tests/test_gpu_parity.py tests/test_gpu_cp.py -x -q > $O/pytest.log 2>&1; echo "rc=$?" > $O/rc.txt
+  timeout 300 python tools/ablate.py c1 base "LRS_NO_EARLY=1" base > $O/ablate_c1.log 2>&1
+  cat $O/rc.txt; tail -3 $O/pytest.log; grep "c1 \[" $O/ablate_c1.log
+}
+
