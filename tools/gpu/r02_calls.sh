@@ -590,3 +590,19 @@ call_v2() {
   cat $O/rc.txt; tail -3 $O/pytest.log; grep "c1 \[" $O/ablate_c1.log
 }
 
+call_v3() {
+  mkdir -p gpurun_out/r02v3; O=gpurun_out/r02v3
+  LRS_EXPERIMENTS=1 python -m paper_2006_06443_b200._build --force > $O/build.log 2>&1
+  timeout 300 python tools/wtrace.py c2_bf16 > $O/wtrace_c2.log 2>&1
+  timeout 300 python tools/ctrace.py c2_bf16 > $O/ctrace_c2.log 2>&1
+  grep -v "^\[lrs\]\|plan" $O/wtrace_c2.log | cut -c1-600 | head -5; cat $O/ctrace_c2.log
+}
+
+call_v4() {
+  mkdir -p gpurun_out/r02v4; O=gpurun_out/r02v4
+  timeout 300 python tools/ablate.py c3 base base > $O/ablate_c3.log 2>&1
+  timeout 300 python tools/ablate.py c2_bf16 base base > $O/ablate_c2.log 2>&1
+  timeout 900 python -m pytest tests/test_gpu_sparse_tc.py tests/test_gpu_parity.py tests/test_gpu_bench_pattern.py -x -q > $O/pytest.log 2>&1; echo "rc=$?" > $O/rc.txt
+  cat $O/rc.txt; tail -2 $O/pytest.log; grep "\[" $O/ablate_c3.log $O/ablate_c2.log
+}
+
