@@ -307,6 +307,75 @@ int32_t lrs_conv_core_fused(const lrs_conv *h);
  */
 lrs_status lrs_conv_debug_trace(lrs_conv *h, void *dev_buf);
 
+/* ------------------------------------------------------------------------------------------
+ * Backward pass: the gradients that fine-tuning the decomposed layer by
+ * "ordinary back-propagation with respect to the original loss" needs (PAPER.md:194-195
+ * §3.5; §5.5 fine-tunes each decomposed layer with SGD).  The trainable
+ * parameters are the factors of L and the VALUES of S at its fixed support (the support is
+ * chosen by the projection P_c).  Given dY = dLoss/dY:
+ *
+ *   dX                      the adjoint convolution of dY with W = L + S
+ *                           (dX[n, ho*s+y-p, wo*s+x-p, c] += sum_j dY[n,ho,wo,j] W[c,j,y,x])
+ *   dU_in [c_in][rank_in]   = X^T dT1          dT1 = adjoint of conv(., G) at dT2
+ *   dG [rank_in][rank_out][kernel_h][kernel_w] = weight gradient of conv(T1, G) at dT2
+ *   dU_out [rank_out][c_out] = T2^T dY         dT2 = dY U_out^T
+ *   dvalues [nnz]           dvalues[e] = sum over output positions of dY[., j_e] X[shift_e(.), c_e]
+ *   (SVD pair: dU = X^T (dY V^T), dV = (X U)^T dY.)
+ * oracle/lrs_backward.py writes both formulations out.
+ *
+ * Engines:
+ *   - dX is the FORWARD of the transposed layer (u_in' = U_out^T, core'[b][a][y][x] =
+ *     G[a][b][kh-1-y][kw-1-x], u_out' = U_in^T, S' = S by input channel with flipped
+ *     taps, pad' = kernel-1-pad, stride 1), created inside the backward handle through
+ *     lrs_conv_create: the same fused tensor-core kernels (2:4 sparse term included).
+ *   - T1, T2 (recomputed from X), dT2 and dT1 run on the library's tcgen05 GEMM engine.
+ *   - the four weight-gradient reductions over positions run as ONE grouped tcgen05
+ *     launch with MN-major operands (lrs_wgrad.cuh); S's value gradient is the dense
+ *     weight gradient of the taps at S's support (every 128 x 256 output tile holds
+ *     nonzeros at 1-5 % uniform density, so skipping tiles saves nothing), summed over
+ *     the K splits in a fixed order (deterministic: the same inputs give the same bits).
+ *   Intermediates T1, T2, dT2, dT1 are bf16 (like the forward's); accumulation is fp32.
+ *
+ * Requirements: dtype BF16, Tucker-2 core or SVD pair (not the CP kind), stride 1, no
+ * fused output epilogue (out_scale / out_bias / out_relu: back-propagate through them in
+ * the caller), every forward requirement of the layer and of its transposed layer, and
+ * output rows of at most 128 positions (in_w <= 128); else LRS_ERR_UNSUPPORTED.
+ */
+typedef struct lrs_conv_bwd lrs_conv_bwd; /* opaque */
+
+/* Parameter gradients, device fp32, overwritten (not accumulated).  Any pointer may be
+   NULL to skip that output (its reduction is still computed when another needs it).    */
+typedef struct lrs_conv_grads {
+  float *d_u_in;   /* [c_in][rank_in]                                      */
+  float *d_core;   /* [rank_in][rank_out][kernel_h][kernel_w] (NULL for an SVD pair) */
+  float *d_u_out;  /* [rank_out][c_out]                                    */
+  float *d_values; /* [nnz], in the order of the descriptor's CSR entries  */
+} lrs_conv_grads;
+
+/* Create the backward state of a layer from the SAME descriptor as its forward (host
+   arrays, deep-copied).  Owns the transposed layer, the recompute scratch (T1, T2, dT2,
+   dT1 for batch_max images) and the K-split partial-sum slabs.  Errors as lrs_conv_create. */
+lrs_status lrs_conv_bwd_create(const lrs_conv_desc *desc, int device, lrs_conv_bwd **out);
+
+/* dX for n images: dy device [n][out_h][out_w][c_out] bf16 -> dx device
+   [n][in_h][in_w][c_in] bf16 (overwritten).  Enqueued on `stream`; graph-capturable;
+   no host sync.  n == 0: no-op.  n > batch_max, NULL or misaligned pointers:
+   INVALID_ARGUMENT. */
+lrs_status lrs_conv_backward_data(lrs_conv_bwd *h, const void *dy, void *dx, int32_t n, void *stream);
+
+/* Parameter gradients for n images: x device [n][in_h][in_w][c_in] (the forward's input),
+   dy as above, g->* device fp32 (overwritten).  Enqueued on `stream`; graph-capturable.
+   The handle's scratch holds one call at a time: calls on one handle are stream-ordered. */
+lrs_status lrs_conv_backward_weights(lrs_conv_bwd *h, const void *x, const void *dy, int32_t n,
+                                     const lrs_conv_grads *g, void *stream);
+
+/* Kernel launches of one backward_weights call (the recompute GEMMs, the grouped weight
+   gradient, the split reduction); of backward_data: lrs_conv_launches_per_forward of the
+   transposed layer. */
+int32_t lrs_conv_bwd_launches(const lrs_conv_bwd *h, int32_t *data_launches);
+
+lrs_status lrs_conv_bwd_destroy(lrs_conv_bwd *h); /* NULL-safe; no call may be in flight */
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,6 +26,7 @@
 #include "lrs_wconv.cuh"
 #include "lrs_pw.cuh"
 #include "lrs_pwf.cuh"
+#include "lrs_wgrad.cuh"
 
 using namespace lrs;
 
@@ -3000,3 +3001,6 @@ lrs_status lrs_conv_debug_buffer(const lrs_conv* h, int32_t which, const void** 
 }
 
 }  // extern "C"
+
+// the backward pass (include/lrs_conv.h "Backward pass"); shares this unit's helpers
+#include "lrs_backward.cuh"

@@ -1,0 +1,230 @@
+// lrs_wgrad.cuh -- the weight-gradient contractions of the backward pass (
+// PAPER.md:194-195 §3.5 "ordinary back-propagation"; oracle/lrs_backward.py).
+//
+// Every parameter gradient of W = U_in G U_out + S is a reduction over output (or input)
+// positions q of a product of two position-major activations:
+//
+//   dU_out[b][j]     = sum_q T2[q][b]             dY[q][j]     (taps 1)
+//   dG[a][b][tap]    = sum_q T1[shift_tap(q)][a]  dT2[q][b]    (taps k*k)
+//   dU_in[c][a]      = sum_q X[q][c]              dT1[q][a]    (taps 1, input grid)
+//   dW_S[tap][c][j]  = sum_q X[shift_tap(q)][c]   dY[q][j]     (taps k*k; gathered at S's support)
+//
+// i.e. C[tap][m][n] = sum_q A_tap[q][m] B[q][n] with BOTH operands M/N-contiguous
+// ("MN-major" for tcgen05: the reduction index q is the strided one).  One grouped launch
+// serves up to four such problems:
+//
+//   * CTA = 6 warps: warp 0 lane 0 TMA producer, warp 1 TMEM allocator + lane 0 MMA issuer,
+//     warps 2-5 epilogue (one TMEM lane quarter each).  One CTA per (problem, tap, M tile
+//     of 128, N tile of BN, K split); the K split is a contiguous range of position steps.
+//   * A position step is one 4-D TMA box (64 channels x bw x bh x bi images) of each operand:
+//     bw = the full row, bh x bi chosen so bw*bh*bi (the MMA K extent of the step, `kst`)
+//     is a multiple of 16.  A's box is displaced by the tap (x - pad_w, y - pad_h); the
+//     zero fill of out-of-bounds boxes is the convolution's zero padding, and B's boxes
+//     past the last image / row are zero, so ragged tails contribute nothing.
+//   * Each 64-channel box lands as kst rows of 128 bytes in the SWIZZLE_128B layout, which
+//     is exactly the MN-major SW128 canonical layout of tcgen05 (8 K rows x 64 M/N elements
+//     per atom): SBO = 1024 B between 8-row K groups, LBO = kst*128 B between the 64-wide
+//     M/N atoms; instruction descriptor bits 15/16 select MN-major A / B.
+//   * Accumulator fp32 [128 lanes][BN columns] in TMEM; the epilogue stores the split's
+//     partial tile into a per-split slab (fp32); lrs_wgrad_reduce_kernel sums the splits in
+//     a fixed order (deterministic) and scatters each gradient entry to its destination
+//     (factor layouts, or S's value order for dW_S).
+#pragma once
+#include "lrs_ptx.cuh"
+
+namespace lrs {
+
+constexpr int kGThreads = 192;
+constexpr int kGMaxProblems = 4;
+
+struct WgradProblem {
+  CUtensorMap tmA;     // 4-D (C_A, W, H, N) bf16, box (64, bw, bh, bi), SWIZZLE_128B
+  CUtensorMap tmB;     // 4-D (C_B, W, H, N) bf16, same box
+  float* slab;         // [splits][taps][m_tiles*128][n_tiles*bn] fp32 partial sums
+  long long split_stride;  // floats per split
+  int cta_base;        // first CTA of this problem in the grouped grid
+  int taps, kw, pad_h, pad_w;
+  int m_tiles, n_tiles, bn;  // bn in {64, 128, 192, 256}
+  int splits;
+  int kst;             // positions per step (MMA K of one stage), multiple of 16
+  int hsteps;          // row steps per image group: ceil(rows / bh)
+  int bh, bi;          // rows / images per step
+  int k_steps;         // position steps in total = image groups * hsteps
+  uint32_t stage_bytes;  // (2 + bn/64) * kst * 128, 1024-aligned
+  int stages;
+};
+
+struct WgradParams {
+  WgradProblem pr[kGMaxProblems];
+  int n_problems;
+};
+
+// MN-major SWIZZLE_128B descriptor: atoms of 8 K rows x 128 B; lbo = bytes between
+// 64-element M/N atoms, sbo = bytes between 8-row K groups
+__device__ __forceinline__ uint64_t umma_desc_mn128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_constant__ WgradParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // ---- which problem / tile / split this CTA owns
+  int pi = 0;
+  for (int i = 1; i < P.n_problems; ++i)
+    if (static_cast<int>(blockIdx.x) >= P.pr[i].cta_base) pi = i;
+  const WgradProblem& p = P.pr[pi];
+  const int local = static_cast<int>(blockIdx.x) - p.cta_base;
+  const int split = local % p.splits;
+  int tile = local / p.splits;
+  const int nt = tile % p.n_tiles;
+  tile /= p.n_tiles;
+  const int mt = tile % p.m_tiles;
+  const int tap = tile / p.m_tiles;
+  const int ty = tap / p.kw, tx = tap - ty * p.kw;
+  const int k_begin = static_cast<int>((static_cast<long long>(p.k_steps) * split) / p.splits);
+  const int k_end = static_cast<int>((static_cast<long long>(p.k_steps) * (split + 1)) / p.splits);
+  const int S = p.stages;
+  const uint32_t atom = static_cast<uint32_t>(p.kst) * 128u;  // bytes of one 64-wide box
+  const int nb_atoms = p.bn >> 6;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * p.stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tmem_full = bars + 2 * S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 1);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&p.tmA);
+    tma_prefetch_desc(&p.tmB);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the recompute kernels before us wrote T1 / T2 / dT2 / dT1
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      const uint32_t tx_bytes = static_cast<uint32_t>(2 + nb_atoms) * atom;
+      const int m0 = mt * 128, n0 = nt * p.bn;
+      for (int it = k_begin; it < k_end; ++it) {
+        const int i = it - k_begin;
+        const int s = i % S;
+        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+        uint8_t* st = smem + s * p.stage_bytes;
+        const int ig = it / p.hsteps;
+        const int h0 = (it - ig * p.hsteps) * p.bh;
+        const int img0 = ig * p.bi;
+        mbar_arrive_expect_tx(&full[s], tx_bytes);
+        tma_load_4d(st, &p.tmA, &full[s], m0, tx - p.pad_w, h0 + ty - p.pad_h, img0);
+        tma_load_4d(st + atom, &p.tmA, &full[s], m0 + 64, tx - p.pad_w, h0 + ty - p.pad_h, img0);
+        for (int b = 0; b < nb_atoms; ++b)
+          tma_load_4d(st + (2 + b) * atom, &p.tmB, &full[s], n0 + 64 * b, 0, h0, img0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      // kind::f16, bf16 A/B, fp32 D, M = 128, N = bn, A and B MN-major (bits 15, 16)
+      const uint32_t idesc = umma_idesc(1u, static_cast<uint32_t>(p.bn), 128u) | (1u << 15) | (1u << 16);
+      const int ksub = p.kst >> 4;
+      for (int it = k_begin; it < k_end; ++it) {
+        const int i = it - k_begin;
+        const int s = i % S;
+        mbar_wait(&full[s], (i / S) & 1);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(smem + s * p.stage_bytes);
+        const uint32_t b_addr = a_addr + 2u * atom;
+        for (int kk = 0; kk < ksub; ++kk) {
+          const uint64_t ad = umma_desc_mn128(a_addr + kk * 2048u, atom, 1024u);
+          const uint64_t bd = umma_desc_mn128(b_addr + kk * 2048u, atom, 1024u);
+          mma_bf16(tmem, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(tmem_full);
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter of this warp
+    const int row = q * 32 + lane;
+    const bool any = k_end > k_begin;
+    if (any) {
+      mbar_wait(tmem_full, 0);
+      tc_fence_after();
+    }
+    const int ld = p.n_tiles * p.bn;
+    float* out = p.slab + split * p.split_stride +
+                 (static_cast<long long>(tap) * p.m_tiles * 128 + mt * 128 + row) * ld + nt * p.bn;
+    for (int cb = 0; cb < p.bn; cb += 16) {
+      float v[16];
+      if (any) {
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + cb, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      }
+      float4* o = reinterpret_cast<float4*>(out + cb);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 256);
+}
+
+// dst[i] = sum_{s < splits} slab[s * split_stride + idx[i]] (fixed order: deterministic);
+// one launch covers every gradient of the backward (concatenated index tables).
+struct WgradReduceParams {
+  const float* slab;
+  long long split_stride;
+  int splits;
+  const long long* idx;
+  float* dst;
+  int count;
+};
+
+constexpr int kGRThreads = 256;
+
+struct WgradReduceSet {
+  WgradReduceParams r[kGMaxProblems];
+  int n;
+  int block_base[kGMaxProblems + 1];
+};
+
+__global__ void __launch_bounds__(kGRThreads) lrs_wgrad_reduce_kernel(const __grid_constant__ WgradReduceSet R) {
+  int pi = 0;
+  for (int i = 1; i < R.n; ++i)
+    if (static_cast<int>(blockIdx.x) >= R.block_base[i]) pi = i;
+  const WgradReduceParams& r = R.r[pi];
+  pdl_wait();
+  pdl_launch_dependents();
+  const int i = (static_cast<int>(blockIdx.x) - R.block_base[pi]) * kGRThreads + threadIdx.x;
+  if (i >= r.count) return;
+  const long long off = r.idx[i];
+  float acc = 0.f;
+  for (int s = 0; s < r.splits; ++s) acc += __ldg(r.slab + s * r.split_stride + off);
+  r.dst[i] = acc;
+}
+
+}  // namespace lrs

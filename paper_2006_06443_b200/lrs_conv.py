@@ -30,7 +30,9 @@ EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs
             "lrs_conv_expand_kernel",
             "lrs_conv_overflow_chunks",
             "lrs_conv_cta_pairs",
-            "lrs_sparse_from_slices")
+            "lrs_sparse_from_slices",
+            "lrs_conv_bwd_create", "lrs_conv_backward_data", "lrs_conv_backward_weights",
+            "lrs_conv_bwd_launches", "lrs_conv_bwd_destroy")
 
 
 class LrsError(RuntimeError):
@@ -58,6 +60,11 @@ class lrs_conv_desc(ctypes.Structure):
         ("out_bias", ctypes.POINTER(ctypes.c_float)),
         ("out_relu", ctypes.c_int32),
     ]
+
+
+class lrs_conv_grads(ctypes.Structure):
+    _fields_ = [("d_u_in", ctypes.c_void_p), ("d_core", ctypes.c_void_p), ("d_u_out", ctypes.c_void_p),
+                ("d_values", ctypes.c_void_p)]
 
 
 _lib = None
@@ -103,6 +110,15 @@ def load_library(path: str = LIB_PATH):
                                            ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64),
                                            ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_float)]
     lib.lrs_sparse_from_slices.restype = ctypes.c_int
+    lib.lrs_conv_bwd_create.argtypes = [ctypes.POINTER(lrs_conv_desc), ctypes.c_int, ctypes.POINTER(P)]
+    lib.lrs_conv_backward_data.argtypes = [P, P, P, ctypes.c_int32, P]
+    lib.lrs_conv_backward_weights.argtypes = [P, P, P, ctypes.c_int32, ctypes.POINTER(lrs_conv_grads), P]
+    lib.lrs_conv_bwd_launches.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
+    lib.lrs_conv_bwd_launches.restype = ctypes.c_int32
+    lib.lrs_conv_bwd_destroy.argtypes = [P]
+    for name in ("lrs_conv_bwd_create", "lrs_conv_backward_data", "lrs_conv_backward_weights",
+                 "lrs_conv_bwd_destroy"):
+        getattr(lib, name).restype = ctypes.c_int
     for name in ("lrs_conv_debug_trace", "lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
                  "lrs_conv_output_shape", "lrs_conv_set_timing", "lrs_conv_stage_times",
                  "lrs_conv_debug_buffer", "lrs_conv_debug_trace", "lrs_conv_sparse_engine"):
@@ -377,6 +393,130 @@ class LrsConv:
     def close(self) -> None:
         if getattr(self, "handle", None):
             lrs_conv_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def lrs_conv_bwd_create(desc: lrs_conv_desc, device: int = 0) -> int:
+    h = ctypes.c_void_p()
+    _check(load_library().lrs_conv_bwd_create(ctypes.byref(desc), device, ctypes.byref(h)))
+    return h.value
+
+
+def lrs_conv_backward_data(handle: int, dy_ptr: int, dx_ptr: int, n: int, stream: int = 0) -> None:
+    _check(load_library().lrs_conv_backward_data(handle, dy_ptr, dx_ptr, n, stream))
+
+
+def lrs_conv_backward_weights(handle: int, x_ptr: int, dy_ptr: int, n: int, grads: lrs_conv_grads,
+                              stream: int = 0) -> None:
+    _check(load_library().lrs_conv_backward_weights(handle, x_ptr, dy_ptr, n, ctypes.byref(grads), stream))
+
+
+def lrs_conv_bwd_destroy(handle: int) -> None:
+    _check(load_library().lrs_conv_bwd_destroy(handle))
+
+
+class LrsConvBackward:
+    """The backward pass of one compressed layer (include/lrs_conv.h "Backward pass";
+    PAPER.md:194-195 fine-tuning by back-propagation): built from the same arguments as
+    LrsConv.  `backward_data(dy) -> dx` and `backward_weights(x, dy) -> dict` of fp32
+    gradients {d_u_in, d_core, d_u_out, d_values}; tensors NHWC bf16 on the device."""
+
+    def __init__(self, batch_max, in_h, in_w, c_in, c_out, kernel, stride, pad, rank_in, rank_out,
+                 dtype, u_in, core, u_out, row_ptr, col_idx, values, device: int = 0):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.svd = core is None
+        self.in_h, self.in_w, self.c_in, self.c_out = in_h, in_w, c_in, c_out
+        self.out_h = (in_h + 2 * pad - kernel) // stride + 1
+        self.out_w = (in_w + 2 * pad - kernel) // stride + 1
+        self.kernel, self.rank_in = kernel, rank_in
+        self.rank_out = rank_in if core is None else rank_out
+        self.nnz = len(values)
+        desc, keep = make_desc(batch_max, in_h, in_w, c_in, c_out, kernel, stride, pad, rank_in, rank_out,
+                               dtype, u_in, core, u_out, row_ptr, col_idx, values)
+        self.handle = lrs_conv_bwd_create(desc, device)
+        del keep
+
+    @classmethod
+    def from_inputs(cls, inp, batch_max: Optional[int] = None, device: int = 0) -> "LrsConvBackward":
+        c = inp.cfg
+        return cls(batch_max or c.batch, c.in_h, c.in_w, c.c_in, c.c_out, c.k, c.stride, c.pad, c.rank_in,
+                   c.rank_out, c.dtype, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx, inp.values,
+                   device)
+
+    def _check(self, t, name, h, w, c):
+        if t.dtype != self.torch.bfloat16 or not t.is_cuda or t.device.index != self.device:
+            raise ValueError(f"{name}: expected a bf16 tensor on cuda:{self.device}")
+        if t.dim() != 4 or tuple(t.shape[1:]) != (h, w, c) or not t.is_contiguous():
+            raise ValueError(f"{name}: expected contiguous NHWC [n, {h}, {w}, {c}], got {tuple(t.shape)}")
+
+    def alloc_grads(self):
+        torch = self.torch
+        dev = f"cuda:{self.device}"
+        g = {"d_u_in": torch.empty((self.c_in, self.rank_in), dtype=torch.float32, device=dev),
+             "d_core": None if self.svd else torch.empty((self.rank_in, self.rank_out, self.kernel, self.kernel),
+                                                         dtype=torch.float32, device=dev),
+             "d_u_out": torch.empty((self.rank_out, self.c_out), dtype=torch.float32, device=dev),
+             "d_values": torch.empty((max(self.nnz, 1),), dtype=torch.float32, device=dev)[:self.nnz]}
+        return g
+
+    def backward_data_into(self, dy, dx, stream=None) -> None:
+        self._check(dy, "dy", self.out_h, self.out_w, self.c_out)
+        self._check(dx, "dx", self.in_h, self.in_w, self.c_in)
+        if dx.shape[0] != dy.shape[0]:
+            raise ValueError("dx / dy image counts differ")
+        s = self.torch.cuda.current_stream(self.device) if stream is None else stream
+        lrs_conv_backward_data(self.handle, dy.data_ptr(), dx.data_ptr(), dy.shape[0], s.cuda_stream)
+
+    def backward_data(self, dy):
+        dx = self.torch.empty((dy.shape[0], self.in_h, self.in_w, self.c_in), dtype=self.torch.bfloat16,
+                              device=dy.device)
+        self.backward_data_into(dy, dx)
+        return dx
+
+    def backward_weights_into(self, x, dy, grads: dict, stream=None) -> None:
+        self._check(x, "x", self.in_h, self.in_w, self.c_in)
+        self._check(dy, "dy", self.out_h, self.out_w, self.c_out)
+        if x.shape[0] != dy.shape[0]:
+            raise ValueError("x / dy image counts differ")
+        sizes = {"d_u_in": self.c_in * self.rank_in, "d_u_out": self.rank_out * self.c_out,
+                 "d_core": 0 if self.svd else self.rank_in * self.rank_out * self.kernel ** 2,
+                 "d_values": self.nnz}
+        ptrs = {}
+        for k, numel in sizes.items():
+            t = grads.get(k)
+            if t is None or numel == 0:
+                ptrs[k] = None
+                continue
+            if t.dtype != self.torch.float32 or not t.is_contiguous() or t.numel() != numel or not t.is_cuda:
+                raise ValueError(f"{k}: expected a contiguous fp32 CUDA tensor of {numel} elements")
+            ptrs[k] = t.data_ptr()
+        g = lrs_conv_grads(**ptrs)
+        s = self.torch.cuda.current_stream(self.device) if stream is None else stream
+        lrs_conv_backward_weights(self.handle, x.data_ptr(), dy.data_ptr(), x.shape[0], g, s.cuda_stream)
+
+    def backward_weights(self, x, dy) -> dict:
+        g = self.alloc_grads()
+        self.backward_weights_into(x, dy, g)
+        return g
+
+    @property
+    def launches(self):
+        """(backward_weights launches, backward_data launches)"""
+        d = ctypes.c_int32()
+        w = load_library().lrs_conv_bwd_launches(self.handle, ctypes.byref(d))
+        return int(w), int(d.value)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            lrs_conv_bwd_destroy(self.handle)
             self.handle = None
 
     def __del__(self):

@@ -1,0 +1,167 @@
+"""GPU parity of the backward pass (§3.5 fine-tuning by
+back-propagation) against the fp64 oracle (oracle/lrs_backward.py, pinned in
+tests/test_backward_oracle.py), through the C-ABI (lrs_conv_bwd_create /
+lrs_conv_backward_data / lrs_conv_backward_weights).
+
+bf16 path, tolerance relL2 <= 2e-2 (BASELINE.json north star) on dX (whole tensor, per
+image, per 128-channel block, border rows / columns: tests/parity.py) and on every
+parameter gradient (dU_in, dG, dU_out, and S's value gradient); shapes span several
+tiles, ragged image groups, padding 0 (the transposed layer then pads 2), an SVD pair,
+an empty S, and the full-size C2 / C3 / C4 layers.
+"""
+import numpy as np
+import pytest
+import torch
+
+import parity
+import workloads
+from oracle import lrs_backward as B
+
+pytestmark = pytest.mark.gpu
+
+CFG = workloads.LayerConfig
+CASES = {
+    "small_3x3": CFG("small_3x3", 6, 14, 14, 128, 192, 3, 1, 1, 64, 32, 0.02, "bf16"),
+    "pad0": CFG("pad0", 3, 9, 9, 64, 128, 3, 1, 0, 32, 48, 0.03, "bf16"),
+    "c2_b8": workloads.CONFIGS["c2_bf16"].replace(batch=8),
+    "c3_b20": workloads.CONFIGS["c3"].replace(batch=20),
+    "c4_b5": workloads.CONFIGS["c4"].replace(batch=5),
+    "no_s": CFG("no_s", 4, 14, 14, 128, 128, 3, 1, 1, 32, 32, 0.0, "bf16"),
+    "k5": CFG("k5", 2, 12, 12, 64, 64, 5, 1, 2, 32, 32, 0.02, "bf16"),
+}
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def run_gpu(inp, dy_np, batch_max=None):
+    from paper_2006_06443_b200 import LrsConvBackward
+    n = inp.x.shape[0]
+    bw = LrsConvBackward.from_inputs(inp, batch_max=batch_max or n)
+    x = torch.from_numpy(inp.x).to(torch.bfloat16).cuda()
+    dy = torch.from_numpy(dy_np).to(torch.bfloat16).cuda()
+    dx = bw.backward_data(dy)
+    g = bw.backward_weights(x, dy)
+    torch.cuda.synchronize()
+    return bw, x, dy, dx, g
+
+
+def check_grads(g, ref, svd):
+    errs = {}
+    for key in ("d_u_in", "d_u_out", "d_values") + (() if svd else ("d_core",)):
+        got = g[key].cpu().numpy().astype(np.float64)
+        want = ref[key]
+        assert got.shape == want.shape, (key, got.shape, want.shape)
+        assert np.isfinite(got).all(), key
+        if want.size == 0:
+            continue
+        errs[key] = rel(got, want)
+        assert errs[key] <= 2e-2, f"{key}: relL2 {errs[key]:.3e}"
+    return errs
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_backward_matches_oracle(name):
+    cfg = CASES[name]
+    inp = workloads.generate(cfg)
+    dy_np = workloads.generate_dy(cfg, seed=11)
+    bw, x, dy, dx, g = run_gpu(inp, dy_np)
+    ref = B.backward_factored(inp.x, dy_np, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx,
+                              inp.values, cfg.stride, cfg.pad)
+    parity.check(dx, ref["dx"], "bf16")
+    check_grads(g, ref, cfg.svd)
+
+
+@pytest.mark.parametrize("name", ["c3_b20", "small_3x3"])
+def test_backward_deterministic_and_graph_capturable(name):
+    """Same inputs -> the same bits (fixed split-sum order), eagerly and replayed from a
+    CUDA graph; a smaller n than batch_max on the same handle (ragged split ranges)."""
+    cfg = CASES[name]
+    inp = workloads.generate(cfg)
+    dy_np = workloads.generate_dy(cfg, seed=12)
+    bw, x, dy, dx, g = run_gpu(inp, dy_np, batch_max=cfg.batch + 5)
+    g2 = bw.alloc_grads()
+    dx2 = torch.empty_like(dx)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        bw.backward_data_into(dy, dx2, stream=s)
+        bw.backward_weights_into(x, dy, g2, stream=s)
+    s.synchronize()
+    assert torch.equal(dx, dx2)
+    for k in g:
+        if g[k] is not None:
+            assert torch.equal(g[k], g2[k]), k
+    graph = torch.cuda.CUDAGraph()
+    g3 = bw.alloc_grads()
+    dx3 = torch.full_like(dx, float("nan"))
+    with torch.cuda.graph(graph, stream=s):
+        bw.backward_data_into(dy, dx3, stream=s)
+        bw.backward_weights_into(x, dy, g3, stream=s)
+    for _ in range(2):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(dx, dx3)
+    for k in g:
+        if g[k] is not None:
+            assert torch.equal(g[k], g3[k]), k
+
+
+def test_backward_linearity_in_the_batch():
+    """Weight gradients are sums over images: g(X, dY) = g(first half) + g(second half)
+    (a property at any size; here through two calls of the same handle)."""
+    cfg = workloads.CONFIGS["c2_bf16"].replace(batch=16)
+    inp = workloads.generate(cfg)
+    dy_np = workloads.generate_dy(cfg, seed=13)
+    bw, x, dy, dx, g = run_gpu(inp, dy_np)
+    ga = bw.backward_weights(x[:7].contiguous(), dy[:7].contiguous())
+    gb = bw.backward_weights(x[7:].contiguous(), dy[7:].contiguous())
+    torch.cuda.synchronize()
+    for k in ("d_u_in", "d_core", "d_u_out", "d_values"):
+        s = (ga[k] + gb[k]).cpu().double().numpy()
+        assert rel(s, g[k].cpu().double().numpy()) < 1e-5, k
+
+
+@pytest.mark.parametrize("name", ["c3", "c2_bf16", "c4"])
+def test_backward_full_size(name):
+    """The BASELINE layer at its full batch (the bench's configuration): dX on sampled
+    images (each image's dX depends only on its own dY), every parameter gradient whole."""
+    cfg = workloads.CONFIGS[name]
+    inp = workloads.generate(cfg)
+    dy_np = workloads.generate_dy(cfg, seed=14)
+    bw, x, dy, dx, g = run_gpu(inp, dy_np)
+    ref = B.backward_factored(inp.x, dy_np, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx,
+                              inp.values, cfg.stride, cfg.pad)
+    check_grads(g, ref, cfg.svd)
+    idx = np.unique(np.r_[0:4, cfg.batch // 2, cfg.batch - 3:cfg.batch])
+    parity.check(dx[idx], ref["dx"][idx], "bf16")
+
+
+def test_backward_n0_and_errors():
+    from paper_2006_06443_b200 import LrsConvBackward, LrsError
+    cfg = CASES["small_3x3"]
+    inp = workloads.generate(cfg)
+    bw = LrsConvBackward.from_inputs(inp, batch_max=cfg.batch)
+    g = bw.alloc_grads()
+    for t in g.values():
+        if t is not None:
+            t.fill_(float("nan"))
+    x = torch.zeros((0, cfg.in_h, cfg.in_w, cfg.c_in), dtype=torch.bfloat16, device="cuda")
+    dy = torch.zeros((0, cfg.out_h, cfg.out_w, cfg.c_out), dtype=torch.bfloat16, device="cuda")
+    bw.backward_weights_into(x, dy, g)
+    torch.cuda.synchronize()
+    for t in g.values():
+        if t is not None:
+            assert torch.count_nonzero(t).item() == 0
+    with pytest.raises(LrsError):
+        big = torch.zeros((cfg.batch + 1, cfg.in_h, cfg.in_w, cfg.c_in), dtype=torch.bfloat16, device="cuda")
+        bdy = torch.zeros((cfg.batch + 1, cfg.out_h, cfg.out_w, cfg.c_out), dtype=torch.bfloat16, device="cuda")
+        bw.backward_weights_into(big, bdy, g)
+    # stride 2 and fp32 are refused (UNSUPPORTED), not silently wrong
+    for bad in (cfg.replace(stride=2), cfg.replace(dtype="f32")):
+        binp = workloads.generate(bad.replace(batch=1))
+        with pytest.raises(LrsError, match="UNSUPPORTED"):
+            LrsConvBackward.from_inputs(binp, batch_max=1)

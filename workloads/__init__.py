@@ -304,3 +304,12 @@ def resnet50_images(n: int, seed: int = 0) -> np.ndarray:
     normalised ImageNet pixels; float32 holding bf16 values."""
     rng = np.random.Generator(np.random.PCG64(seed))
     return bf16_round(rng.standard_normal((n, 3, 224, 224)).astype(np.float32))
+
+
+def generate_dy(cfg: LayerConfig, batch: Optional[int] = None, seed: int = 1) -> np.ndarray:
+    """An upstream gradient dY = dLoss/dY of the layer's output shape for the backward
+    pass: N(0, 1) entries from PCG64(seed), rounded like X to the
+    layer's dtype.  A loss gradient has no sign structure, so unlike X it is not ReLU'd."""
+    n = cfg.batch if batch is None else batch
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return _store(rng.standard_normal((n, cfg.out_h, cfg.out_w, cfg.c_out)), cfg.dtype)
