@@ -71,6 +71,8 @@ def parse():
                          "weak = a full batch per rank")
     ap.add_argument("--replays", type=int, default=10, help="separately timed graph replays (median reported)")
     ap.add_argument("--no-dense", action="store_true", help="skip the cuDNN dense context row")
+    ap.add_argument("--backward", action="store_true",
+                    help="time the layer's backward pass (dX + parameter gradients, SURVEY 8f f3) instead")
     return ap.parse_args()
 
 
@@ -488,6 +490,9 @@ def main():
         return
     is_cp = args.config in workloads.CP_CONFIGS
     cfg = workloads.CP_CONFIGS[args.config] if is_cp else workloads.CONFIGS[args.config]
+    if args.backward:
+        main_bwd(args, cfg)
+        return
     if args.impl == "reference":
         run_reference(args, cfg)
         return
@@ -796,6 +801,354 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bwd_work(cfg, n: int, inp) -> dict:
+    """Algorithmic work of one backward step on n images (per GPU).  FLOPs: dX as the
+    transposed layer's forward (chain 2P(R2 Cout + R1 R2 k^2 + R1 Cin) + 2 x sparse MACs);
+    the weight-gradient reductions dU_out 2 P R2 Cout, dG 2 P R1 R2 k^2, dU_in 2 Pin Cin R1,
+    dvalues 2 x sparse MACs; the recompute T1, T2, dT2, dT1 (2 Pin Cin R1, 2 P R1 R2 k^2,
+    2 P Cout R2, 2 Pin R1 R2 k^2).  Bytes: X, dY read, dX written (bf16) -- each once --
+    plus the factors and S (read) and the gradients (fp32, written)."""
+    from paper_2006_06443_b200 import roofline as RL
+    k2 = cfg.k * cfg.k
+    pin = n * cfg.in_h * cfg.in_w
+    P = n * cfg.out_h * cfg.out_w
+    r1, r2 = cfg.rank_in, (cfg.rank_in if cfg.svd else cfg.rank_out)
+    kc = 1 if cfg.svd else k2
+    sp = RL.sparse_macs(n, cfg.in_h, cfg.in_w, cfg.k, cfg.stride, cfg.pad, inp.col_idx)
+    wg = {"d_u_out": 2 * P * r2 * cfg.c_out, "d_core": 0 if cfg.svd else 2 * P * r1 * r2 * k2,
+          "d_u_in": 2 * pin * cfg.c_in * r1, "d_values": 2 * sp}
+    # executed by the grouped kernel: dvalues as the dense tap weight gradient
+    wg_exec = dict(wg, d_values=2 * P * cfg.c_in * cfg.c_out * k2 if len(inp.col_idx) else 0)
+    recompute = 2 * pin * cfg.c_in * r1 + 2 * P * cfg.c_out * r2 + (0 if cfg.svd else 2 * P * r1 * r2 * k2 * 2)
+    dx = 2 * P * (r2 * cfg.c_out + (0 if cfg.svd else r1 * r2 * k2)) + 2 * pin * r1 * cfg.c_in + 2 * sp
+    nparam = cfg.c_in * r1 + cfg.c_out * r2 + (0 if cfg.svd else r1 * r2 * k2)
+    act = 2 * (2 * pin * cfg.c_in + P * cfg.c_out)
+    byts = act + 2 * nparam + 8 * len(inp.col_idx) + 4 * (nparam + len(inp.col_idx))
+    return {"flops_wgrad": sum(wg.values()), "flops_wgrad_executed": sum(wg_exec.values()),
+            "flops_recompute": recompute, "flops_dx": dx, "flops": sum(wg.values()) + recompute + dx,
+            "bytes": byts, "wgrad_split": wg}
+
+
+def main_bwd(args, cfg):
+    """--backward: one step = the layer's backward for one batch -- dX (lrs_conv_backward_data)
+    and every parameter gradient (lrs_conv_backward_weights) -- and, at N > 1, the
+    data-parallel exchange fine-tuning needs: an NCCL all-reduce of the parameter gradients
+    (the one real collective of the path).  Same timing protocol as the forward: CUDA graph of
+    the rotating sets (X, dY, dX of distinct seeded images, > 2.1x L2), K timed steps, max over
+    ranks, median of >= 10 replays; verification after timing (bitwise vs eager, fp64 oracle)."""
+    import torch
+    import torch.distributed as dist
+    if cfg.dtype != "bf16" or cfg.stride != 1:
+        raise SystemExit("--backward: bf16 stride-1 layers (c2_bf16, c3, c4)")
+    if args.impl == "reference":
+        return run_reference_bwd(args, cfg)
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    from paper_2006_06443_b200 import LrsConvBackward
+    from paper_2006_06443_b200 import roofline as RL
+    inp = workloads.generate(cfg, batch=1)
+    plan = ShardPlan(cfg, rank, world, args.scaling)
+    gb, s0, s1 = plan.global_batch, plan.start, plan.end
+    n = s1 - s0
+    bw = LrsConvBackward.from_inputs(inp, batch_max=n, device=local)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    set_bytes = 2 * n * (2 * cfg.in_h * cfg.in_w * cfg.c_in + cfg.out_h * cfg.out_w * cfg.c_out)
+    n_sets = max(2, math.ceil(2.1 * l2 / set_bytes))
+    xs_np = [plan.x(i) for i in range(n_sets)]
+    dys_np = [workloads.generate_dy(cfg, cfg.batch, seed=10_000 + plan.seed(i))[s0:s1] if plan.strong or world == 1
+              else workloads.generate_dy(cfg, cfg.batch, seed=10_000 + plan.seed(i)) for i in range(n_sets)]
+    xs = [torch.from_numpy(x).to(torch.bfloat16).to(dev) for x in xs_np]
+    dys = [torch.from_numpy(d).to(torch.bfloat16).to(dev) for d in dys_np]
+    dxs = [torch.empty_like(x) for x in xs]
+    grads = bw.alloc_grads()
+    gl = [t for t in grads.values() if t is not None and t.numel()]
+    stream = torch.cuda.Stream(device=dev)
+
+    def step(i):
+        bw.backward_data_into(dys[i], dxs[i], stream=stream)
+        bw.backward_weights_into(xs[i], dys[i], grads, stream=stream)
+        if world > 1:
+            for t in gl:
+                dist.all_reduce(t)
+
+    with torch.cuda.stream(stream):
+        for i in range(n_sets):
+            step(i)
+    torch.cuda.synchronize(dev)
+    K, W = args.steps, args.warmup
+
+    def capture(count):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(count):
+                    step(i % n_sets)
+        return g
+
+    g_full = capture(n_sets)
+    rem = K % n_sets
+    g_rem = capture(rem) if rem else None
+    for _ in range(max(1, math.ceil(W / n_sets))):
+        g_full.replay()
+    if g_rem is not None:
+        g_rem.replay()
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+    barrier()
+    with sampler:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for _ in range(K // n_sets):
+                g_full.replay()
+            if g_rem is not None:
+                g_rem.replay()
+            ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    t = torch.tensor([ev0.elapsed_time(ev1)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / K
+    value = gb * K / (ms_max / 1e3)
+    reps = []
+    for _ in range(max(10, args.replays)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+            g_full.replay()
+            b.record(stream)
+        reps.append((a, b))
+    torch.cuda.synchronize(dev)
+    rep_ms = torch.tensor([a.elapsed_time(b) for a, b in reps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(rep_ms, op=dist.ReduceOp.MAX)
+    rep_us = rep_ms.cpu().numpy() / n_sets * 1e3
+    replays = {"n": int(len(rep_us)), "steps_per_replay": n_sets, "median_us_per_step": float(np.median(rep_us)),
+               "median_images_per_s": gb / (float(np.median(rep_us)) * 1e-6)}
+
+    # ---- verification (untimed): the graph's last gradients and every dX bitwise = eager
+    verify = {}
+    last = n_sets - 1  # the replays above ran the full rotation last: grads hold set n_sets - 1
+    ge = bw.alloc_grads()
+    ok = True
+    for i in range(n_sets):
+        dxe = torch.empty_like(dxs[i])
+        bw.backward_data_into(dys[i], dxe)
+        torch.cuda.synchronize(dev)
+        ok &= bool(torch.equal(dxe, dxs[i]))
+    bw.backward_weights_into(xs[last], dys[last], ge)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        for k_ in ge:
+            if ge[k_] is not None and ge[k_].numel():
+                dist.all_reduce(ge[k_])
+    verify["dx_rotation_bitwise_eager"] = ok
+    verify["grads_bitwise_eager"] = all(torch.equal(ge[k_], grads[k_]) for k_ in ge if ge[k_] is not None)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import lrs_backward as B
+        ref = B.backward_factored(xs_np[last].astype(np.float64), dys_np[last].astype(np.float64), inp.u_in,
+                                  inp.core, inp.u_out, inp.row_ptr, inp.col_idx, inp.values, cfg.stride, cfg.pad)
+        errs = {}
+        for k_ in ("d_u_in", "d_core", "d_u_out", "d_values"):
+            if ref[k_] is None or ref[k_].size == 0:
+                continue
+            gpu = grads[k_].double().cpu().numpy()
+            errs[k_] = float(np.linalg.norm(gpu - ref[k_]) / np.linalg.norm(ref[k_]))
+        dxl = dxs[last].double().cpu().numpy()
+        errs["dx"] = float(np.linalg.norm(dxl - ref["dx"]) / np.linalg.norm(ref["dx"]))
+        verify["oracle_rel_l2"] = errs
+        verify["oracle_ok"] = max(errs.values()) <= 2e-2
+
+    # ---- per-kernel durations (event pairs around every launch, queued behind a sleep)
+    bw.set_timing(True)
+    bw.stage_times(reset=True)
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(2e7))
+        for i in range(n_sets):
+            bw.backward_data_into(dys[i], dxs[i], stream=stream)
+            bw.backward_weights_into(xs[i], dys[i], grads, stream=stream)
+    torch.cuda.synchronize(dev)
+    stages = bw.stage_times(reset=True)
+    bw.set_timing(False)
+
+    # ---- end to end with host buffers: X, dY in (pinned) -> dX and the gradients out
+    e2e = None
+    if not args.no_e2e:
+        xh = xs[0].cpu().pin_memory()
+        dyh = dys[0].cpu().pin_memory()
+        dxh = torch.empty(dxs[0].shape, dtype=torch.bfloat16).pin_memory()
+        gh = {k_: torch.empty(v.shape, dtype=torch.float32).pin_memory() for k_, v in grads.items()
+              if v is not None and v.numel()}
+        xd, dyd, dxd = torch.empty_like(xs[0]), torch.empty_like(dys[0]), torch.empty_like(dxs[0])
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            dyd.copy_(dyh, non_blocking=True)
+            bw.backward_data_into(dyd, dxd, stream=stream)
+            bw.backward_weights_into(xd, dyd, grads, stream=stream)
+            if world > 1:
+                for t_ in gl:
+                    dist.all_reduce(t_)
+            dxh.copy_(dxd, non_blocking=True)
+            for k_, v in gh.items():
+                v.copy_(grads[k_], non_blocking=True)
+
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                e2e_step()
+        torch.cuda.synchronize(dev)
+        ke = max(3, min(K, 50))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(ke):
+                e2e_step()
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": gb * ke / (float(te.item()) / 1e3), "unit": "images/s",
+               "h2d_bytes_per_step": xh.numel() * 2 + dyh.numel() * 2,
+               "d2h_bytes_per_step": dxh.numel() * 2 + sum(v.numel() * 4 for v in gh.values()), "steps": ke,
+               "api": "LrsConvBackward.backward_data_into + backward_weights_into with pinned-host copies in and out"}
+
+    # ---- context: cuDNN's backward of the dense layer (dgrad + wgrad of conv2d, W = L + S)
+    dense = None
+    if not args.no_dense:
+        wd = dense_weight(inp, cfg).to(torch.bfloat16).to(dev).contiguous(memory_format=torch.channels_last)
+        xd_ = [x.permute(0, 3, 1, 2) for x in xs]
+        dyd_ = [d.permute(0, 3, 1, 2) for d in dys]
+        gi = torch.nn.grad.conv2d_input
+        gw = torch.nn.grad.conv2d_weight
+        with torch.backends.cudnn.flags(enabled=True, benchmark=True):
+            def dstep(i):
+                gi(xd_[i].shape, wd, dyd_[i], stride=cfg.stride, padding=cfg.pad)
+                gw(xd_[i], wd.shape, dyd_[i], stride=cfg.stride, padding=cfg.pad)
+            with torch.cuda.stream(stream):
+                for i in range(n_sets):
+                    dstep(i)
+            torch.cuda.synchronize(dev)
+            ke = max(n_sets, (K // n_sets) * n_sets)
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                d0.record(stream)
+                for i in range(ke):
+                    dstep(i % n_sets)
+                d1.record(stream)
+            torch.cuda.synchronize(dev)
+        us = d0.elapsed_time(d1) / ke * 1e3
+        dense = {"us_per_step": us, "images_per_s": n / (us * 1e-6), "steps": ke,
+                 "what": "torch.nn.grad.conv2d_input + conv2d_weight (cuDNN, benchmark mode) of the dense "
+                         "W = L + S, bf16, channels_last, this rank's images (eager launches)",
+                 "compressed_speedup": us / (ms_per_step * 1e3)}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    peaks = RL.measured_peaks()
+    work = bwd_work(cfg, n, inp)
+    avg = {k_: v[0] / v[1] for k_, v in stages.items() if v[1]}
+    t_w = avg["wgrad"] / 1e3
+    peak = peaks["bf16_tflops_sustained"]
+    roof = {"bound": "tensor", "kernel": "lrs_wgrad_kernel (grouped weight-gradient reductions)",
+            "achieved": work["flops_wgrad"] / t_w / 1e12, "peak": peak, "unit": "TFLOP/s",
+            "frac": work["flops_wgrad"] / t_w / 1e12 / peak, "traffic": None,
+            "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json bf16_tflops_sustained): the kernel runs "
+                         "inside a long step",
+            "executed_tflops": work["flops_wgrad_executed"] / t_w / 1e12,
+            "executed_frac": work["flops_wgrad_executed"] / t_w / 1e12 / peak,
+            "what": "achieved = ALGORITHMIC FLOPs of the four reductions (dU_out, dG, dU_in, and dvalues as the "
+                    "sparse MACs only) / the kernel's event-timed launch; executed counts dvalues as the dense "
+                    "tap weight gradient the kernel computes before gathering S's support",
+            "kernel_us": t_w * 1e6, "work": work,
+            "stage_us": {k_: round(v * 1e3, 3) for k_, v in avg.items()}}
+    step_s = ms_per_step / 1e3
+    layer_roof = {"t_tensor_us": work["flops"] / (peak * 1e12) * 1e6,
+                  "t_hbm_us": work["bytes"] / (peaks["hbm_gbs"] * 1e9) * 1e6}
+    layer_roof["frac_literal"] = max(layer_roof["t_tensor_us"], layer_roof["t_hbm_us"]) / (step_s * 1e6)
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu = bwd_oracle_rate(cfg, inp, args.cpu_seconds, xs_np[0], dys_np[0])
+    wl, dl = bw.launches
+    line = {
+        "metric": METRIC + " (backward pass: dX + parameter gradients)", "value": value, "unit": "images/s",
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if (plan.strong or world == 1) else "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded ReLU(N(0,1)) images, N(0,1) dY, N(0,1/fan_in) factors, uniform S)",
+        "config": {"workload": CONFIG_TEXT[args.config] + " -- BACKWARD (SURVEY 8f f3)", "config_id": args.config + "_bwd",
+                   "global_batch": gb, "per_gpu_batch": n,
+                   "parallelism": f"dp{world} (batch-sharded; NCCL all-reduce of the parameter gradients)",
+                   "l2": f"{n_sets} rotating X/dY/dX sets of distinct images ({n_sets * set_bytes / 2**20:.0f} MiB, "
+                         f"2.1x L2)", "timing": "CUDA graph replay, CUDA events, max over ranks"},
+        "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": (wl + dl) * K, "roofline": roof,
+        "roofline_layer": layer_roof, "replays": replays, "verify": verify, "dense_context": dense,
+        "cpu_baseline": cpu, "host": host_info(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def bwd_oracle_rate(cfg, inp, seconds, x_all, dy_all, sample=2):
+    """The fp64 backward oracle (oracle/lrs_backward.backward_factored, as it stands) on a
+    bounded sample: repeated calls on `sample` images."""
+    from oracle import lrs_backward as B
+    x = x_all[:sample].astype(np.float64)
+    dy = dy_all[:sample].astype(np.float64)
+    calls, t0 = 0, time.perf_counter()
+    while True:
+        B.backward_factored(x, dy, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx, inp.values,
+                            cfg.stride, cfg.pad)
+        calls += 1
+        el = time.perf_counter() - t0
+        if el >= seconds and calls >= 2:
+            break
+    return {"value": calls * sample / el, "unit": "images/s", "cores": cpu_threads(), "kind": "oracle",
+            "sample": f"{calls} oracle backward calls x {sample} images ({el:.1f} s, fp64 numpy backward_factored)",
+            **host_info()}
+
+
+def run_reference_bwd(args, cfg):
+    """--impl reference --backward: the fp64 backward oracle as it stands, on rank 0."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    inp = workloads.generate(cfg, batch=1)
+    x = workloads.generate_x(cfg, 2, seed=0)
+    dy = workloads.generate_dy(cfg, 2, seed=10_000)
+    for _ in range(args.warmup):
+        bwd_oracle_rate(cfg, inp, 0.0, x, dy)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        bwd_oracle_rate(cfg, inp, 0.0, x, dy)
+    el = time.perf_counter() - t0
+    v = 2 * 2 * args.steps / el
+    cpu = {"value": v, "unit": "images/s", "cores": cpu_threads(), "kind": "oracle",
+           "sample": f"{args.steps} steps x 2 calls x 2 images of {args.config} backward"}
+    print(json.dumps({"impl": "reference", "metric": METRIC + " (backward pass: dX + parameter gradients)",
+                      "value": v, "unit": "images/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                      "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "dtype": "f64",
+                      "config": {"workload": CONFIG_TEXT[args.config] + " -- BACKWARD", "config_id": args.config + "_bwd"},
+                      "cpu_baseline": cpu, "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0,
+                                                   "d2h_bytes_per_step": 0}}), flush=True)
 
 
 if __name__ == "__main__":

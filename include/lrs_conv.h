@@ -374,6 +374,14 @@ lrs_status lrs_conv_backward_weights(lrs_conv_bwd *h, const void *x, const void 
    transposed layer. */
 int32_t lrs_conv_bwd_launches(const lrs_conv_bwd *h, int32_t *data_launches);
 
+/* Stage timing of the backward (as lrs_conv_set_timing / lrs_conv_stage_times): stages
+   0-5 bwd_t1, bwd_t2, bwd_dt2, bwd_dt1, wgrad, wgrad_reduce (backward_weights), 6-9 the
+   transposed layer's forward stages (backward_data, names prefixed "dx_"). */
+lrs_status lrs_conv_bwd_set_timing(lrs_conv_bwd *h, int32_t enable);
+lrs_status lrs_conv_bwd_stage_times(lrs_conv_bwd *h, float *ms, int64_t *counts, int32_t max_stages,
+                                    int32_t *n_stages, int32_t reset);
+const char *lrs_conv_bwd_stage_name(const lrs_conv_bwd *h, int32_t stage);
+
 lrs_status lrs_conv_bwd_destroy(lrs_conv_bwd *h); /* NULL-safe; no call may be in flight */
 
 #ifdef __cplusplus

@@ -49,6 +49,9 @@ struct lrs_conv_bwd {
   int dst_of[kGMaxProblems];  // 0 d_u_out, 1 d_core, 2 d_u_in, 3 d_values
   WgradReduceSet rs{};
   int rs_blocks = 0;
+  // stage timing (lrs_conv_bwd_set_timing): bwd_t1, bwd_t2, bwd_dt2, bwd_dt1, wgrad, wgrad_reduce
+  bool timing = false;
+  TimingRing ring[6];
   // per-call map caches
   const void* cx = nullptr;
   const void* cdy = nullptr;
@@ -235,6 +238,8 @@ lrs_status lrs_conv_bwd_destroy(lrs_conv_bwd* h) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->tr) lrs_conv_destroy(h->tr);
+  for (auto& r : h->ring)
+    for (auto e : r.ev) cudaEventDestroy(e);
   cudaSetDevice(prev);
   delete h;
   return LRS_OK;
@@ -586,9 +591,27 @@ lrs_status lrs_conv_backward_weights(lrs_conv_bwd* h, const void* x, const void*
   if (st != LRS_OK) return st;
   const long long pin = static_cast<long long>(n) * h->H * h->W;
   const long long P = static_cast<long long>(n) * h->ho * h->wo;
-  auto launch_stage = [&](Stage& s, dim3 grid) -> lrs_status {
-    LRS_CUDA(launch_pdl(kernel_ptr(s.kid), grid, dim3(kThreads), &s.p, s.smem, stream));
+  // an event pair around a launch of stage si when timing is on
+  auto timed = [&](int si, auto&& fn) -> lrs_status {
+    cudaEvent_t e1 = nullptr;
+    if (h->timing) {
+      TimingRing& r = h->ring[si];
+      if (r.used + 2 > static_cast<int>(r.ev.size())) {
+        const size_t old = r.ev.size();
+        r.ev.resize(old + 256);
+        for (size_t i = old; i < r.ev.size(); ++i) LRS_CUDA(cudaEventCreate(&r.ev[i]));
+      }
+      e1 = r.ev[r.used + 1];
+      LRS_CUDA(cudaEventRecord(r.ev[r.used], stream));
+      r.used += 2;
+    }
+    LRS_CUDA(fn());
+    if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
     return LRS_OK;
+  };
+  auto launch_stage = [&](Stage& s, dim3 grid) -> lrs_status {
+    const int si = &s == &h->g_t1 ? 0 : (&s == &h->g_t2 ? 1 : (&s == &h->g_dt2 ? 2 : 3));
+    return timed(si, [&] { return launch_pdl(kernel_ptr(s.kid), grid, dim3(kThreads), &s.p, s.smem, stream); });
   };
   // recompute the chain's activations and back-propagate through it
   if ((st = launch_stage(h->g_t1, dim3(static_cast<unsigned>((pin + kTileM - 1) / kTileM)))) != LRS_OK) return st;
@@ -605,8 +628,11 @@ lrs_status lrs_conv_backward_weights(lrs_conv_bwd* h, const void* x, const void*
   }
   // the grouped weight-gradient launch; split counts were sized at batch_max (a smaller n
   // keeps them: a split may then own no position step and stores zeros)
-  LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_wgrad_kernel), dim3(static_cast<unsigned>(h->wg_ctas)),
-                      dim3(kGThreads), &h->wp, h->wg_smem, stream));
+  if ((st = timed(4, [&] {
+         return launch_pdl(reinterpret_cast<const void*>(&lrs_wgrad_kernel), dim3(static_cast<unsigned>(h->wg_ctas)),
+                           dim3(kGThreads), &h->wp, h->wg_smem, stream);
+       })) != LRS_OK)
+    return st;
   // split sums -> gradients (problems whose output the caller skipped are not gathered)
   WgradReduceSet rs = h->rs;
   int blocks = 0, k = 0;
@@ -621,10 +647,62 @@ lrs_status lrs_conv_backward_weights(lrs_conv_bwd* h, const void* x, const void*
   }
   rs.n = k;
   rs.block_base[k] = blocks;
-  if (blocks > 0)
-    LRS_CUDA(launch_pdl(reinterpret_cast<const void*>(&lrs_wgrad_reduce_kernel), dim3(static_cast<unsigned>(blocks)),
-                        dim3(kGRThreads), &rs, 0, stream));
+  if (blocks > 0 && (st = timed(5, [&] {
+                       return launch_pdl(reinterpret_cast<const void*>(&lrs_wgrad_reduce_kernel),
+                                         dim3(static_cast<unsigned>(blocks)), dim3(kGRThreads), &rs, 0, stream);
+                     })) != LRS_OK)
+    return st;
   return LRS_OK;
+}
+
+lrs_status lrs_conv_bwd_set_timing(lrs_conv_bwd* h, int32_t enable) {
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  h->timing = enable != 0;
+  return lrs_conv_set_timing(h->tr, enable);
+}
+
+lrs_status lrs_conv_bwd_stage_times(lrs_conv_bwd* h, float* ms, int64_t* counts, int32_t max_stages,
+                                    int32_t* n_stages, int32_t reset) {
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  float tms[4];
+  int64_t tcnt[4];
+  int32_t tn = 0;
+  lrs_status st = lrs_conv_stage_times(h->tr, tms, tcnt, 4, &tn, reset);
+  if (st != LRS_OK) return st;
+  for (int s = 0; s < 6; ++s) {
+    TimingRing& r = h->ring[s];
+    for (int i = 0; i + 1 < r.used; i += 2) {
+      LRS_CUDA(cudaEventSynchronize(r.ev[i + 1]));
+      float t = 0.f;
+      LRS_CUDA(cudaEventElapsedTime(&t, r.ev[i], r.ev[i + 1]));
+      r.ms += t;
+      r.count += 1;
+    }
+    r.used = 0;
+  }
+  if (n_stages) *n_stages = 10;
+  for (int s = 0; s < 10 && s < max_stages; ++s) {
+    if (ms) ms[s] = s < 6 ? static_cast<float>(h->ring[s].ms) : tms[s - 6];
+    if (counts) counts[s] = s < 6 ? h->ring[s].count : tcnt[s - 6];
+  }
+  if (reset)
+    for (auto& r : h->ring) {
+      r.ms = 0.0;
+      r.count = 0;
+    }
+  return LRS_OK;
+}
+
+const char* lrs_conv_bwd_stage_name(const lrs_conv_bwd* h, int32_t stage) {
+  static const char* names[] = {"bwd_t1", "bwd_t2", "bwd_dt2", "bwd_dt1", "wgrad", "wgrad_reduce"};
+  static const char* dx_names[] = {"dx_a1_proj", "dx_a2_core", "dx_a345_expand_sparse", "dx_a4_sparse_add",
+                                   "dx_a12_proj_core"};
+  if (stage >= 0 && stage < 6) return names[stage];
+  if (stage >= 6 && stage < 10) {
+    if (stage == 6 && h && h->tr && h->tr->use_core) return dx_names[4];
+    return dx_names[stage - 6];
+  }
+  return "";
 }
 
 int32_t lrs_conv_bwd_launches(const lrs_conv_bwd* h, int32_t* data_launches) {

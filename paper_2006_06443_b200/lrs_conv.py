@@ -32,7 +32,8 @@ EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs
             "lrs_conv_cta_pairs",
             "lrs_sparse_from_slices",
             "lrs_conv_bwd_create", "lrs_conv_backward_data", "lrs_conv_backward_weights",
-            "lrs_conv_bwd_launches", "lrs_conv_bwd_destroy")
+            "lrs_conv_bwd_launches", "lrs_conv_bwd_destroy", "lrs_conv_bwd_set_timing",
+            "lrs_conv_bwd_stage_times", "lrs_conv_bwd_stage_name")
 
 
 class LrsError(RuntimeError):
@@ -116,8 +117,13 @@ def load_library(path: str = LIB_PATH):
     lib.lrs_conv_bwd_launches.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
     lib.lrs_conv_bwd_launches.restype = ctypes.c_int32
     lib.lrs_conv_bwd_destroy.argtypes = [P]
+    lib.lrs_conv_bwd_set_timing.argtypes = [P, ctypes.c_int32]
+    lib.lrs_conv_bwd_stage_times.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64),
+                                             ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]
+    lib.lrs_conv_bwd_stage_name.argtypes = [P, ctypes.c_int32]
+    lib.lrs_conv_bwd_stage_name.restype = ctypes.c_char_p
     for name in ("lrs_conv_bwd_create", "lrs_conv_backward_data", "lrs_conv_backward_weights",
-                 "lrs_conv_bwd_destroy"):
+                 "lrs_conv_bwd_destroy", "lrs_conv_bwd_set_timing", "lrs_conv_bwd_stage_times"):
         getattr(lib, name).restype = ctypes.c_int
     for name in ("lrs_conv_debug_trace", "lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
                  "lrs_conv_output_shape", "lrs_conv_set_timing", "lrs_conv_stage_times",
@@ -506,6 +512,19 @@ class LrsConvBackward:
         g = self.alloc_grads()
         self.backward_weights_into(x, dy, g)
         return g
+
+    def set_timing(self, on: bool) -> None:
+        _check(load_library().lrs_conv_bwd_set_timing(self.handle, 1 if on else 0))
+
+    def stage_times(self, reset: bool = True):
+        """{stage name: (total ms, launches)} of event-timed backward kernels since the last reset."""
+        ms = (ctypes.c_float * 10)()
+        cnt = (ctypes.c_int64 * 10)()
+        ns = ctypes.c_int32()
+        lib = load_library()
+        _check(lib.lrs_conv_bwd_stage_times(self.handle, ms, cnt, 10, ctypes.byref(ns), 1 if reset else 0))
+        return {lib.lrs_conv_bwd_stage_name(self.handle, i).decode(): (ms[i], cnt[i]) for i in range(ns.value)
+                if cnt[i]}
 
     @property
     def launches(self):
