@@ -832,8 +832,8 @@ def bwd_work(cfg, n: int, inp) -> dict:
 
 
 def main_bwd(args, cfg):
-    """--backward: one step = the layer's backward for one batch -- dX (lrs_conv_backward_data)
-    and every parameter gradient (lrs_conv_backward_weights) -- and, at N > 1, the
+    """--backward: one step = the layer's backward for one batch -- dX and every parameter
+    gradient (one lrs_conv_backward call) -- and, at N > 1, the
     data-parallel exchange fine-tuning needs: an NCCL all-reduce of the parameter gradients
     (the one real collective of the path).  Same timing protocol as the forward: CUDA graph of
     the rotating sets (X, dY, dX of distinct seeded images, > 2.1x L2), K timed steps, max over
@@ -870,8 +870,7 @@ def main_bwd(args, cfg):
     stream = torch.cuda.Stream(device=dev)
 
     def step(i):
-        bw.backward_data_into(dys[i], dxs[i], stream=stream)
-        bw.backward_weights_into(xs[i], dys[i], grads, stream=stream)
+        bw.backward_into(xs[i], dys[i], dxs[i], grads, stream=stream)
         if world > 1:
             for t in gl:
                 dist.all_reduce(t)
@@ -946,10 +945,10 @@ def main_bwd(args, cfg):
     ok = True
     for i in range(n_sets):
         dxe = torch.empty_like(dxs[i])
-        bw.backward_data_into(dys[i], dxe)
+        bw.backward_into(xs[i], dys[i], dxe, ge)
         torch.cuda.synchronize(dev)
         ok &= bool(torch.equal(dxe, dxs[i]))
-    bw.backward_weights_into(xs[last], dys[last], ge)
+    bw.backward_into(xs[last], dys[last], torch.empty_like(dxs[last]), ge)
     torch.cuda.synchronize(dev)
     if world > 1:
         for k_ in ge:
@@ -978,8 +977,7 @@ def main_bwd(args, cfg):
     with torch.cuda.stream(stream):
         torch.cuda._sleep(int(2e7))
         for i in range(n_sets):
-            bw.backward_data_into(dys[i], dxs[i], stream=stream)
-            bw.backward_weights_into(xs[i], dys[i], grads, stream=stream)
+            bw.backward_into(xs[i], dys[i], dxs[i], grads, stream=stream)
     torch.cuda.synchronize(dev)
     stages = bw.stage_times(reset=True)
     bw.set_timing(False)
@@ -997,8 +995,7 @@ def main_bwd(args, cfg):
         def e2e_step():
             xd.copy_(xh, non_blocking=True)
             dyd.copy_(dyh, non_blocking=True)
-            bw.backward_data_into(dyd, dxd, stream=stream)
-            bw.backward_weights_into(xd, dyd, grads, stream=stream)
+            bw.backward_into(xd, dyd, dxd, grads, stream=stream)
             if world > 1:
                 for t_ in gl:
                     dist.all_reduce(t_)
@@ -1026,7 +1023,7 @@ def main_bwd(args, cfg):
         e2e = {"value": gb * ke / (float(te.item()) / 1e3), "unit": "images/s",
                "h2d_bytes_per_step": xh.numel() * 2 + dyh.numel() * 2,
                "d2h_bytes_per_step": dxh.numel() * 2 + sum(v.numel() * 4 for v in gh.values()), "steps": ke,
-               "api": "LrsConvBackward.backward_data_into + backward_weights_into with pinned-host copies in and out"}
+               "api": "LrsConvBackward.backward_into (lrs_conv_backward) with pinned-host copies in and out"}
 
     # ---- context: cuDNN's backward of the dense layer (dgrad + wgrad of conv2d, W = L + S)
     dense = None
@@ -1087,7 +1084,7 @@ def main_bwd(args, cfg):
     cpu = None
     if world == 1 and not args.no_cpu:
         cpu = bwd_oracle_rate(cfg, inp, args.cpu_seconds, xs_np[0], dys_np[0])
-    wl, dl = bw.launches
+    _, _, cl = bw.launches
     line = {
         "metric": METRIC + " (backward pass: dX + parameter gradients)", "value": value, "unit": "images/s",
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -1098,7 +1095,7 @@ def main_bwd(args, cfg):
                    "parallelism": f"dp{world} (batch-sharded; NCCL all-reduce of the parameter gradients)",
                    "l2": f"{n_sets} rotating X/dY/dX sets of distinct images ({n_sets * set_bytes / 2**20:.0f} MiB, "
                          f"2.1x L2)", "timing": "CUDA graph replay, CUDA events, max over ranks"},
-        "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": (wl + dl) * K, "roofline": roof,
+        "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": cl * K, "roofline": roof,
         "roofline_layer": layer_roof, "replays": replays, "verify": verify, "dense_context": dense,
         "cpu_baseline": cpu, "host": host_info(),
     }

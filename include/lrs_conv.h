@@ -369,10 +369,17 @@ lrs_status lrs_conv_backward_data(lrs_conv_bwd *h, const void *dy, void *dx, int
 lrs_status lrs_conv_backward_weights(lrs_conv_bwd *h, const void *x, const void *dy, int32_t n,
                                      const lrs_conv_grads *g, void *stream);
 
+/* Both at once: dX, then the parameter gradients with dT1 taken from the transposed layer's
+   forward (its intermediate) instead of recomputed -- one GEMM launch fewer than the two
+   calls above (an SVD pair: when that forward keeps T1 in device memory); dX is identical,
+   the gradients equal up to the fp32 summation order of dT1. */
+lrs_status lrs_conv_backward(lrs_conv_bwd *h, const void *x, const void *dy, void *dx, int32_t n,
+                             const lrs_conv_grads *g, void *stream);
+
 /* Kernel launches of one backward_weights call (the recompute GEMMs, the grouped weight
-   gradient, the split reduction); of backward_data: lrs_conv_launches_per_forward of the
-   transposed layer. */
-int32_t lrs_conv_bwd_launches(const lrs_conv_bwd *h, int32_t *data_launches);
+   gradient, the split reduction); of backward_data (lrs_conv_launches_per_forward of the
+   transposed layer) and of one lrs_conv_backward call, if the pointers are non-NULL. */
+int32_t lrs_conv_bwd_launches(const lrs_conv_bwd *h, int32_t *data_launches, int32_t *combined_launches);
 
 /* Stage timing of the backward (as lrs_conv_set_timing / lrs_conv_stage_times): stages
    0-5 bwd_t1, bwd_t2, bwd_dt2, bwd_dt1, wgrad, wgrad_reduce (backward_weights), 6-9 the

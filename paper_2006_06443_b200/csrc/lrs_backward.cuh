@@ -38,6 +38,9 @@ struct lrs_conv_bwd {
   WgradParams wp{};
   int wg_ctas = 0;
   uint32_t wg_smem = 0;
+  void* wg_items = nullptr;  // WgradItem lists of the persistent CTAs
+  void* wg_ptr = nullptr;    // [wg_ctas + 1]
+  double wg_max_load = 0;    // the most loaded CTA's work / the mean (LPT balance)
   // which operand of each problem is which (rebuilt per call: pointer / n dependent maps)
   struct Opnd {
     int kind;      // 0 X, 1 dY, 2 T1, 3 T2, 4 dT2, 5 dT1
@@ -52,6 +55,10 @@ struct lrs_conv_bwd {
   // stage timing (lrs_conv_bwd_set_timing): bwd_t1, bwd_t2, bwd_dt2, bwd_dt1, wgrad, wgrad_reduce
   bool timing = false;
   TimingRing ring[6];
+  // lrs_conv_backward: dT1 taken from the transposed layer's forward (its T2, or T1 for an
+  // SVD pair) instead of recomputed; nullptr = the handle's own dT1
+  const void* dt1_ext = nullptr;
+  const void* cdt1 = nullptr;
   // per-call map caches
   const void* cx = nullptr;
   const void* cdy = nullptr;
@@ -158,7 +165,9 @@ bool pick_wgrad_step(int rows, int w, int n_img, int bn, int* bh_out, int* bi_ou
       if (stages < 2) continue;
       const double waste = (static_cast<double>((rows + bh - 1) / bh) * bh / rows) *
                            (static_cast<double>((n_img + bi - 1) / bi) * bi / n_img);
-      const double cost = waste * (1.0 + 32.0 / kst);  // per-step overheads favour longer steps
+      // per-step overheads favour longer steps; slots over 96 KB leave a 2-deep ring for
+      // every problem of the grouped launch (one slot size), so they pay a penalty
+      const double cost = waste * (1.0 + 32.0 / kst) * (stage > 96u * 1024u ? 1.25 : 1.0);
       if (cost < best) {
         best = cost;
         *bh_out = bh;
@@ -183,13 +192,13 @@ const void* bwd_operand_ptr(const lrs_conv_bwd* h, int kind, const void* x, cons
     case 2: return h->t1;
     case 3: return h->t2;
     case 4: return h->dt2;
-    default: return h->dt1;
+    default: return h->dt1_ext ? h->dt1_ext : h->dt1;
   }
 }
 
 // per-call: the pointer- and n-dependent tensor maps
 lrs_status bwd_encode_call(lrs_conv_bwd* h, const void* x, const void* dy, int n) {
-  if (h->cx == x && h->cdy == dy && h->cn == n) return LRS_OK;
+  if (h->cx == x && h->cdy == dy && h->cn == n && h->cdt1 == h->dt1_ext) return LRS_OK;
   lrs_status st;
   const long long pin = static_cast<long long>(n) * h->H * h->W;
   const long long P = static_cast<long long>(n) * h->ho * h->wo;
@@ -222,9 +231,15 @@ lrs_status bwd_encode_call(lrs_conv_bwd* h, const void* x, const void* dy, int n
   h->cx = x;
   h->cdy = dy;
   h->cn = n;
+  h->cdt1 = h->dt1_ext;
   return LRS_OK;
 }
 
+}  // namespace
+
+namespace {
+lrs_status bwd_weights_impl(lrs_conv_bwd* h, const void* x, const void* dy, int32_t n, const lrs_conv_grads* gr,
+                            void* stream_);
 }  // namespace
 
 extern "C" {
@@ -234,7 +249,8 @@ lrs_status lrs_conv_bwd_destroy(lrs_conv_bwd* h) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
-  void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->w_coret, h->t1, h->t2, h->dt2, h->dt1, h->slab, h->idx};
+  void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->w_coret, h->t1, h->t2, h->dt2, h->dt1, h->slab, h->idx,
+                  h->wg_items, h->wg_ptr};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->tr) lrs_conv_destroy(h->tr);
@@ -428,8 +444,7 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
   const int np = static_cast<int>(probs.size());
   h->wp.n_problems = np;
   std::vector<double> work(np);
-  std::vector<int> tiles(np), ksteps_max(np);
-  uint32_t smem_need = 0;
+  std::vector<int> tiles(np), ksteps_max(np), stage_count(np);
   for (int i = 0; i < np; ++i) {
     const Prob& pr = probs[i];
     WgradProblem& q = h->wp.pr[i];
@@ -449,7 +464,7 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
     q.bi = bi;
     q.kst = gw * bh * bi;
     q.stage_bytes = static_cast<uint32_t>(2 + bn / 64) * q.kst * 128u;
-    q.stages = stages;
+    stage_count[i] = stages;
     q.hsteps = (gh + bh - 1) / bh;
     q.k_steps = ((d->batch_max + bi - 1) / bi) * q.hsteps;
     h->box_bw[i] = gw;
@@ -462,29 +477,74 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
     tiles[i] = pr.taps * q.m_tiles * q.n_tiles;
     ksteps_max[i] = q.k_steps;
     work[i] = static_cast<double>(tiles[i]) * q.k_steps * q.kst * (2 + bn / 64);
-    smem_need = std::max(smem_need, static_cast<uint32_t>(q.stages) * q.stage_bytes +
-                                        8u * (2u * q.stages + 1u) + 16u + 1024u);
   }
-  // K splits: about one wave of equal-work CTAs over all problems (at batch_max)
+  // K splits and the persistent schedule: items (problem, tile, split) of about equal work,
+  // ~3 per SM, assigned longest-first to the least-loaded of the SMs' CTAs (LPT)
   double total = 0;
   for (double w : work) total += w;
-  const double per_cta = total / h->sms;
-  int base = 0;
+  const double item_work = total / (3.0 * h->sms);
   size_t slab_off = 0;
   std::vector<size_t> slab_at(np);
+  std::vector<std::pair<double, WgradItem>> items;
+  uint32_t slot = 0;
+  int max_stages = 4;
   for (int i = 0; i < np; ++i) {
     WgradProblem& q = h->wp.pr[i];
-    int splits = static_cast<int>(std::lround(work[i] / (tiles[i] * per_cta)));
+    int splits = static_cast<int>(std::lround(work[i] / (tiles[i] * item_work)));
     splits = std::max(1, std::min(splits, ksteps_max[i]));
     q.splits = splits;
-    q.cta_base = base;
-    base += tiles[i] * splits;
     q.split_stride = static_cast<long long>(q.taps) * q.m_tiles * 128 * q.n_tiles * q.bn;
     slab_at[i] = slab_off;
     slab_off += static_cast<size_t>(splits) * q.split_stride;
+    for (int t = 0; t < tiles[i]; ++t)
+      for (int sp = 0; sp < splits; ++sp) {
+        WgradItem it;
+        it.problem = static_cast<uint16_t>(i);
+        it.split = static_cast<uint16_t>(sp);
+        it.tile = t;
+        const long long kb = static_cast<long long>(q.k_steps) * sp / splits;
+        const long long ke = static_cast<long long>(q.k_steps) * (sp + 1) / splits;
+        items.push_back({static_cast<double>(ke - kb) * q.kst * (2 + q.bn / 64), it});
+      }
+    slot = std::max(slot, q.stage_bytes);
+    max_stages = std::min(max_stages, stage_count[i]);
   }
-  h->wg_ctas = base;
-  h->wg_smem = smem_need;
+  std::stable_sort(items.begin(), items.end(),
+                   [](const std::pair<double, WgradItem>& a, const std::pair<double, WgradItem>& b) {
+                     return a.first > b.first;
+                   });
+  const int grid = std::min<int>(h->sms, static_cast<int>(items.size()));
+  std::vector<std::vector<WgradItem>> lists(grid);
+  std::vector<double> load(grid, 0.0);
+  for (auto& it : items) {
+    const int c = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+    load[c] += it.first;
+    lists[c].push_back(it.second);
+  }
+  std::vector<WgradItem> flat;
+  std::vector<int> ptr(grid + 1, 0);
+  for (int c = 0; c < grid; ++c) {
+    for (auto& it : lists[c]) flat.push_back(it);
+    ptr[c + 1] = static_cast<int>(flat.size());
+  }
+  {
+    std::vector<uint8_t> b(flat.size() * sizeof(WgradItem)), pb(ptr.size() * 4);
+    memcpy(b.data(), flat.data(), b.size());
+    memcpy(pb.data(), ptr.data(), pb.size());
+    void* p1 = nullptr;
+    void* p2 = nullptr;
+    if ((st = upload(&p1, b)) != LRS_OK) return cleanup_fail(st);
+    h->wg_items = p1;
+    if ((st = upload(&p2, pb)) != LRS_OK) return cleanup_fail(st);
+    h->wg_ptr = p2;
+  }
+  h->wp.items = static_cast<const WgradItem*>(h->wg_items);
+  h->wp.item_ptr = static_cast<const int*>(h->wg_ptr);
+  h->wp.slot_bytes = slot;
+  h->wp.stages = max_stages;
+  h->wg_ctas = grid;
+  h->wg_smem = static_cast<uint32_t>(max_stages) * slot + 8u * (2u * max_stages + 4u) + 16u + 1024u;
+  h->wg_max_load = *std::max_element(load.begin(), load.end()) / (total / grid);
   h->slab_floats = slab_off;
   if ((st = bwd_alloc(reinterpret_cast<void**>(&h->slab), slab_off * 4, "weight-gradient slabs")) != LRS_OK)
     return cleanup_fail(st);
@@ -551,11 +611,12 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
     for (int i = 0; i < np; ++i) {
       const WgradProblem& q = h->wp.pr[i];
       fprintf(stderr, "lrs bwd: problem %d dst %d taps %d m_tiles %d n_tiles %d bn %d kst %d (bh %d bi %d) "
-              "stages %d splits %d k_steps %d\n", i, probs[i].dst, q.taps, q.m_tiles, q.n_tiles, q.bn, q.kst, q.bh,
-              q.bi, q.stages, q.splits, q.k_steps);
+              "splits %d k_steps %d\n", i, probs[i].dst, q.taps, q.m_tiles, q.n_tiles, q.bn, q.kst, q.bh,
+              q.bi, q.splits, q.k_steps);
     }
-    fprintf(stderr, "lrs bwd: %d weight-gradient CTAs, %u B smem, slabs %.1f MB, reduce %d blocks\n", h->wg_ctas,
-            h->wg_smem, h->slab_floats * 4.0 / 1e6, h->rs_blocks);
+    fprintf(stderr, "lrs bwd: %d persistent weight-gradient CTAs (max load %.3f x mean), %d stages x %u B, "
+            "slabs %.1f MB, reduce %d blocks\n", h->wg_ctas, h->wg_max_load, h->wp.stages, h->wp.slot_bytes,
+            h->slab_floats * 4.0 / 1e6, h->rs_blocks);
   }
   *out = h;
   return LRS_OK;
@@ -569,6 +630,35 @@ lrs_status lrs_conv_backward_data(lrs_conv_bwd* h, const void* dy, void* dx, int
 lrs_status lrs_conv_backward_weights(lrs_conv_bwd* h, const void* x, const void* dy, int32_t n,
                                      const lrs_conv_grads* gr, void* stream_) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  h->dt1_ext = nullptr;
+  return bwd_weights_impl(h, x, dy, n, gr, stream_);
+}
+
+lrs_status lrs_conv_backward(lrs_conv_bwd* h, const void* x, const void* dy, void* dx, int32_t n,
+                             const lrs_conv_grads* gr, void* stream_) {
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  lrs_status st = lrs_conv_forward(h->tr, dy, dx, n, stream_);
+  if (st != LRS_OK || n == 0) {
+    if (st == LRS_OK) st = bwd_weights_impl(h, x, dy, n, gr, stream_);
+    return st;
+  }
+  // the transposed layer's forward just computed dT1 (its T2; T1 for an SVD pair) in the
+  // scratch buffer of this forward's parity; it stays intact until its forward after next
+  const void* buf = nullptr;
+  int32_t ld = 0;
+  const bool have = h->svd ? !h->tr->pw_ft : true;
+  h->dt1_ext = nullptr;
+  if (have && lrs_conv_debug_buffer(h->tr, h->svd ? 0 : 1, &buf, &ld) == LRS_OK && ld == h->r1p) h->dt1_ext = buf;
+  st = bwd_weights_impl(h, x, dy, n, gr, stream_);
+  h->dt1_ext = nullptr;
+  return st;
+}
+
+}  // extern "C"
+
+namespace {
+lrs_status bwd_weights_impl(lrs_conv_bwd* h, const void* x, const void* dy, int32_t n, const lrs_conv_grads* gr,
+                            void* stream_) {
   if (n < 0 || n > h->batch_max) return fail(LRS_ERR_INVALID_ARGUMENT, "n=%d outside [0, %d]", n, h->batch_max);
   if (!gr) return fail(LRS_ERR_INVALID_ARGUMENT, "grads is NULL");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
@@ -620,8 +710,10 @@ lrs_status lrs_conv_backward_weights(lrs_conv_bwd* h, const void* x, const void*
     if ((st = launch_stage(h->g_t2, dim3(static_cast<unsigned>(((n + g.nb - 1) / g.nb) * g.tiles_h)))) != LRS_OK)
       return st;
   }
-  if ((st = launch_stage(h->g_dt2, dim3(static_cast<unsigned>((P + kTileM - 1) / kTileM)))) != LRS_OK) return st;
-  if (!h->svd) {
+  if ((!h->svd || !h->dt1_ext) &&
+      (st = launch_stage(h->g_dt2, dim3(static_cast<unsigned>((P + kTileM - 1) / kTileM)))) != LRS_OK)
+    return st;
+  if (!h->svd && !h->dt1_ext) {
     const ConvGeom& g = h->g_dt1.p.g;
     if ((st = launch_stage(h->g_dt1, dim3(static_cast<unsigned>(((n + g.nb - 1) / g.nb) * g.tiles_h)))) != LRS_OK)
       return st;
@@ -654,6 +746,10 @@ lrs_status lrs_conv_backward_weights(lrs_conv_bwd* h, const void* x, const void*
     return st;
   return LRS_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 lrs_status lrs_conv_bwd_set_timing(lrs_conv_bwd* h, int32_t enable) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
@@ -705,10 +801,14 @@ const char* lrs_conv_bwd_stage_name(const lrs_conv_bwd* h, int32_t stage) {
   return "";
 }
 
-int32_t lrs_conv_bwd_launches(const lrs_conv_bwd* h, int32_t* data_launches) {
+int32_t lrs_conv_bwd_launches(const lrs_conv_bwd* h, int32_t* data_launches, int32_t* combined_launches) {
   if (!h) return 0;
-  if (data_launches) *data_launches = lrs_conv_launches_per_forward(h->tr);
-  return (h->svd ? 2 : 4) + 2;
+  const int32_t d = lrs_conv_launches_per_forward(h->tr);
+  const int32_t w = (h->svd ? 2 : 4) + 2;
+  const bool reuse = h->svd ? (!h->tr->pw_ft && h->tr->r1p == h->r1p) : (h->tr->r2p == h->r1p);
+  if (data_launches) *data_launches = d;
+  if (combined_launches) *combined_launches = d + w - (reuse ? 1 : 0);
+  return w;
 }
 
 }  // extern "C"

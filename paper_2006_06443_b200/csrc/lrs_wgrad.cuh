@@ -14,8 +14,9 @@
 // serves up to four such problems:
 //
 //   * CTA = 6 warps: warp 0 lane 0 TMA producer, warp 1 TMEM allocator + lane 0 MMA issuer,
-//     warps 2-5 epilogue (one TMEM lane quarter each).  One CTA per (problem, tap, M tile
-//     of 128, N tile of BN, K split); the K split is a contiguous range of position steps.
+//     warps 2-5 epilogue (one TMEM lane quarter each).  Persistent: one CTA per SM runs a
+//     list of work items (problem, tap, M tile of 128, N tile of BN, K split -- a contiguous
+//     range of position steps), the lists balanced at create (longest processing time first).
 //   * A position step is one 4-D TMA box (64 channels x bw x bh x bi images) of each operand:
 //     bw = the full row, bh x bi chosen so bw*bh*bi (the MMA K extent of the step, `kst`)
 //     is a multiple of 16.  A's box is displaced by the tap (x - pad_w, y - pad_h); the
@@ -42,7 +43,6 @@ struct WgradProblem {
   CUtensorMap tmB;     // 4-D (C_B, W, H, N) bf16, same box
   float* slab;         // [splits][taps][m_tiles*128][n_tiles*bn] fp32 partial sums
   long long split_stride;  // floats per split
-  int cta_base;        // first CTA of this problem in the grouped grid
   int taps, kw, pad_h, pad_w;
   int m_tiles, n_tiles, bn;  // bn in {64, 128, 192, 256}
   int splits;
@@ -51,12 +51,25 @@ struct WgradProblem {
   int bh, bi;          // rows / images per step
   int k_steps;         // position steps in total = image groups * hsteps
   uint32_t stage_bytes;  // (2 + bn/64) * kst * 128, 1024-aligned
-  int stages;
+};
+
+// One work item = (problem, tile, K split); a persistent CTA runs the items of its list
+// (items[item_ptr[cta] .. item_ptr[cta + 1]), balanced at create by longest-processing-time
+// assignment) back to back: one continuous smem ring over all of its position steps, two
+// TMEM accumulators (item i+1's MMAs overlap item i's epilogue).
+struct WgradItem {
+  uint16_t problem;
+  uint16_t split;
+  int tile;
 };
 
 struct WgradParams {
   WgradProblem pr[kGMaxProblems];
   int n_problems;
+  int stages;              // ring depth (max stage_bytes over the problems per slot)
+  uint32_t slot_bytes;
+  const WgradItem* items;
+  const int* item_ptr;     // [grid + 1]
 };
 
 // MN-major SWIZZLE_128B descriptor: atoms of 8 K rows x 128 B; lbo = bytes between
@@ -71,49 +84,59 @@ __device__ __forceinline__ uint64_t umma_desc_mn128(uint32_t saddr, uint32_t lbo
   return d;
 }
 
+struct WgradItemGeom {
+  int pi, split, nt, mt, tap, ty, tx, k_begin, k_end;
+};
+
+__device__ __forceinline__ WgradItemGeom wgrad_item(const WgradParams& P, const WgradItem& it) {
+  WgradItemGeom g;
+  g.pi = it.problem;
+  g.split = it.split;
+  const WgradProblem& p = P.pr[g.pi];
+  int tile = it.tile;
+  g.nt = tile % p.n_tiles;
+  tile /= p.n_tiles;
+  g.mt = tile % p.m_tiles;
+  g.tap = tile / p.m_tiles;
+  g.ty = g.tap / p.kw;
+  g.tx = g.tap - g.ty * p.kw;
+  g.k_begin = static_cast<int>((static_cast<long long>(p.k_steps) * g.split) / p.splits);
+  g.k_end = static_cast<int>((static_cast<long long>(p.k_steps) * (g.split + 1)) / p.splits);
+  return g;
+}
+
 __global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_constant__ WgradParams P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int S = P.stages;
+  const int i_begin = P.item_ptr[blockIdx.x], i_end = P.item_ptr[blockIdx.x + 1];
 
-  // ---- which problem / tile / split this CTA owns
-  int pi = 0;
-  for (int i = 1; i < P.n_problems; ++i)
-    if (static_cast<int>(blockIdx.x) >= P.pr[i].cta_base) pi = i;
-  const WgradProblem& p = P.pr[pi];
-  const int local = static_cast<int>(blockIdx.x) - p.cta_base;
-  const int split = local % p.splits;
-  int tile = local / p.splits;
-  const int nt = tile % p.n_tiles;
-  tile /= p.n_tiles;
-  const int mt = tile % p.m_tiles;
-  const int tap = tile / p.m_tiles;
-  const int ty = tap / p.kw, tx = tap - ty * p.kw;
-  const int k_begin = static_cast<int>((static_cast<long long>(p.k_steps) * split) / p.splits);
-  const int k_end = static_cast<int>((static_cast<long long>(p.k_steps) * (split + 1)) / p.splits);
-  const int S = p.stages;
-  const uint32_t atom = static_cast<uint32_t>(p.kst) * 128u;  // bytes of one 64-wide box
-  const int nb_atoms = p.bn >> 6;
-
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * p.stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * P.slot_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
-  uint64_t* tmem_full = bars + 2 * S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 1);
+  uint64_t* tmem_full = bars + 2 * S;       // [2]
+  uint64_t* tmem_empty = bars + 2 * S + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 4);  // one arrival per epilogue warp
+    }
     fence_mbar_init();
-    tma_prefetch_desc(&p.tmA);
-    tma_prefetch_desc(&p.tmB);
+    for (int i = 0; i < P.n_problems; ++i) {
+      tma_prefetch_desc(&P.pr[i].tmA);
+      tma_prefetch_desc(&P.pr[i].tmB);
+    }
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 256);
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -124,73 +147,97 @@ __global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_co
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
-      const uint32_t tx_bytes = static_cast<uint32_t>(2 + nb_atoms) * atom;
-      const int m0 = mt * 128, n0 = nt * p.bn;
-      for (int it = k_begin; it < k_end; ++it) {
-        const int i = it - k_begin;
-        const int s = i % S;
-        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
-        uint8_t* st = smem + s * p.stage_bytes;
-        const int ig = it / p.hsteps;
-        const int h0 = (it - ig * p.hsteps) * p.bh;
-        const int img0 = ig * p.bi;
-        mbar_arrive_expect_tx(&full[s], tx_bytes);
-        tma_load_4d(st, &p.tmA, &full[s], m0, tx - p.pad_w, h0 + ty - p.pad_h, img0);
-        tma_load_4d(st + atom, &p.tmA, &full[s], m0 + 64, tx - p.pad_w, h0 + ty - p.pad_h, img0);
-        for (int b = 0; b < nb_atoms; ++b)
-          tma_load_4d(st + (2 + b) * atom, &p.tmB, &full[s], n0 + 64 * b, 0, h0, img0);
+      int q = 0;  // ring position over all of this CTA's position steps
+      for (int ii = i_begin; ii < i_end; ++ii) {
+        const WgradItemGeom g = wgrad_item(P, P.items[ii]);
+        const WgradProblem& p = P.pr[g.pi];
+        const uint32_t atom = static_cast<uint32_t>(p.kst) * 128u;
+        const int nb_atoms = p.bn >> 6;
+        const uint32_t tx_bytes = static_cast<uint32_t>(2 + nb_atoms) * atom;
+        const int m0 = g.mt * 128, n0 = g.nt * p.bn;
+        for (int it = g.k_begin; it < g.k_end; ++it, ++q) {
+          const int s = q % S;
+          if (q >= S) mbar_wait(&empty[s], ((q / S) - 1) & 1);
+          uint8_t* st = smem + s * P.slot_bytes;
+          const int ig = it / p.hsteps;
+          const int h0 = (it - ig * p.hsteps) * p.bh;
+          const int img0 = ig * p.bi;
+          mbar_arrive_expect_tx(&full[s], tx_bytes);
+          tma_load_4d(st, &p.tmA, &full[s], m0, g.tx - p.pad_w, h0 + g.ty - p.pad_h, img0);
+          tma_load_4d(st + atom, &p.tmA, &full[s], m0 + 64, g.tx - p.pad_w, h0 + g.ty - p.pad_h, img0);
+          for (int b = 0; b < nb_atoms; ++b)
+            tma_load_4d(st + (2 + b) * atom, &p.tmB, &full[s], n0 + 64 * b, 0, h0, img0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ------------------------------------------------------------ MMA issuer
-      // kind::f16, bf16 A/B, fp32 D, M = 128, N = bn, A and B MN-major (bits 15, 16)
-      const uint32_t idesc = umma_idesc(1u, static_cast<uint32_t>(p.bn), 128u) | (1u << 15) | (1u << 16);
-      const int ksub = p.kst >> 4;
-      for (int it = k_begin; it < k_end; ++it) {
-        const int i = it - k_begin;
-        const int s = i % S;
-        mbar_wait(&full[s], (i / S) & 1);
+      int q = 0;
+      for (int ii = i_begin; ii < i_end; ++ii) {
+        const int li = ii - i_begin;
+        const int buf = li & 1;
+        const WgradItemGeom g = wgrad_item(P, P.items[ii]);
+        const WgradProblem& p = P.pr[g.pi];
+        const uint32_t atom = static_cast<uint32_t>(p.kst) * 128u;
+        // kind::f16, bf16 A/B, fp32 D, M = 128, N = bn, A and B MN-major (bits 15, 16)
+        const uint32_t idesc = umma_idesc(1u, static_cast<uint32_t>(p.bn), 128u) | (1u << 15) | (1u << 16);
+        const int ksub = p.kst >> 4;
+        const uint32_t acc_t = tmem + static_cast<uint32_t>(buf * 256);
+        if (li >= 2) mbar_wait(&tmem_empty[buf], ((li >> 1) - 1) & 1);  // the epilogue drained it
         tc_fence_after();
-        const uint32_t a_addr = smem_u32(smem + s * p.stage_bytes);
-        const uint32_t b_addr = a_addr + 2u * atom;
-        for (int kk = 0; kk < ksub; ++kk) {
-          const uint64_t ad = umma_desc_mn128(a_addr + kk * 2048u, atom, 1024u);
-          const uint64_t bd = umma_desc_mn128(b_addr + kk * 2048u, atom, 1024u);
-          mma_bf16(tmem, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+        for (int it = g.k_begin; it < g.k_end; ++it, ++q) {
+          const int s = q % S;
+          mbar_wait(&full[s], (q / S) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * P.slot_bytes);
+          const uint32_t b_addr = a_addr + 2u * atom;
+          for (int kk = 0; kk < ksub; ++kk) {
+            const uint64_t ad = umma_desc_mn128(a_addr + kk * 2048u, atom, 1024u);
+            const uint64_t bd = umma_desc_mn128(b_addr + kk * 2048u, atom, 1024u);
+            mma_bf16(acc_t, ad, bd, idesc, (it > g.k_begin || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&tmem_full[buf]);  // (an item without steps: arrives at once; stores zeros)
       }
-      mma_commit(tmem_full);
     }
   } else {
     // -------------------------------------------------------------- epilogue
-    const int q = warp & 3;  // TMEM lane quarter of this warp
-    const int row = q * 32 + lane;
-    const bool any = k_end > k_begin;
-    if (any) {
-      mbar_wait(tmem_full, 0);
+    const int qd = warp & 3;  // TMEM lane quarter of this warp
+    const int row = qd * 32 + lane;
+    for (int ii = i_begin; ii < i_end; ++ii) {
+      const int li = ii - i_begin;
+      const int buf = li & 1;
+      const WgradItemGeom g = wgrad_item(P, P.items[ii]);
+      const WgradProblem& p = P.pr[g.pi];
+      const bool any = g.k_end > g.k_begin;
+      mbar_wait(&tmem_full[buf], (li >> 1) & 1);
       tc_fence_after();
-    }
-    const int ld = p.n_tiles * p.bn;
-    float* out = p.slab + split * p.split_stride +
-                 (static_cast<long long>(tap) * p.m_tiles * 128 + mt * 128 + row) * ld + nt * p.bn;
-    for (int cb = 0; cb < p.bn; cb += 16) {
-      float v[16];
-      if (any) {
-        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + cb, v);
-      } else {
+      const int ld = p.n_tiles * p.bn;
+      float* out = p.slab + g.split * p.split_stride +
+                   (static_cast<long long>(g.tap) * p.m_tiles * 128 + g.mt * 128 + row) * ld + g.nt * p.bn;
+      const uint32_t acc_t = tmem + static_cast<uint32_t>(buf * 256) + (static_cast<uint32_t>(qd * 32) << 16);
+      for (int cb = 0; cb < p.bn; cb += 16) {
+        float v[16];
+        if (any) {
+          tmem_ld16(acc_t + cb, v);
+        } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        float4* o = reinterpret_cast<float4*>(out + cb);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
       }
-      float4* o = reinterpret_cast<float4*>(out + cb);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[buf]);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 256);
+  if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
 // dst[i] = sum_{s < splits} slab[s * split_stride + idx[i]] (fixed order: deterministic);

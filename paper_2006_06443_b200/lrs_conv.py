@@ -31,7 +31,7 @@ EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs
             "lrs_conv_overflow_chunks",
             "lrs_conv_cta_pairs",
             "lrs_sparse_from_slices",
-            "lrs_conv_bwd_create", "lrs_conv_backward_data", "lrs_conv_backward_weights",
+            "lrs_conv_bwd_create", "lrs_conv_backward_data", "lrs_conv_backward_weights", "lrs_conv_backward",
             "lrs_conv_bwd_launches", "lrs_conv_bwd_destroy", "lrs_conv_bwd_set_timing",
             "lrs_conv_bwd_stage_times", "lrs_conv_bwd_stage_name")
 
@@ -114,7 +114,8 @@ def load_library(path: str = LIB_PATH):
     lib.lrs_conv_bwd_create.argtypes = [ctypes.POINTER(lrs_conv_desc), ctypes.c_int, ctypes.POINTER(P)]
     lib.lrs_conv_backward_data.argtypes = [P, P, P, ctypes.c_int32, P]
     lib.lrs_conv_backward_weights.argtypes = [P, P, P, ctypes.c_int32, ctypes.POINTER(lrs_conv_grads), P]
-    lib.lrs_conv_bwd_launches.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
+    lib.lrs_conv_backward.argtypes = [P, P, P, P, ctypes.c_int32, ctypes.POINTER(lrs_conv_grads), P]
+    lib.lrs_conv_bwd_launches.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
     lib.lrs_conv_bwd_launches.restype = ctypes.c_int32
     lib.lrs_conv_bwd_destroy.argtypes = [P]
     lib.lrs_conv_bwd_set_timing.argtypes = [P, ctypes.c_int32]
@@ -122,7 +123,7 @@ def load_library(path: str = LIB_PATH):
                                              ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]
     lib.lrs_conv_bwd_stage_name.argtypes = [P, ctypes.c_int32]
     lib.lrs_conv_bwd_stage_name.restype = ctypes.c_char_p
-    for name in ("lrs_conv_bwd_create", "lrs_conv_backward_data", "lrs_conv_backward_weights",
+    for name in ("lrs_conv_bwd_create", "lrs_conv_backward_data", "lrs_conv_backward_weights", "lrs_conv_backward",
                  "lrs_conv_bwd_destroy", "lrs_conv_bwd_set_timing", "lrs_conv_bwd_stage_times"):
         getattr(lib, name).restype = ctypes.c_int
     for name in ("lrs_conv_debug_trace", "lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
@@ -423,6 +424,11 @@ def lrs_conv_backward_weights(handle: int, x_ptr: int, dy_ptr: int, n: int, grad
     _check(load_library().lrs_conv_backward_weights(handle, x_ptr, dy_ptr, n, ctypes.byref(grads), stream))
 
 
+def lrs_conv_backward(handle: int, x_ptr: int, dy_ptr: int, dx_ptr: int, n: int, grads: lrs_conv_grads,
+                      stream: int = 0) -> None:
+    _check(load_library().lrs_conv_backward(handle, x_ptr, dy_ptr, dx_ptr, n, ctypes.byref(grads), stream))
+
+
 def lrs_conv_bwd_destroy(handle: int) -> None:
     _check(load_library().lrs_conv_bwd_destroy(handle))
 
@@ -487,11 +493,7 @@ class LrsConvBackward:
         self.backward_data_into(dy, dx)
         return dx
 
-    def backward_weights_into(self, x, dy, grads: dict, stream=None) -> None:
-        self._check(x, "x", self.in_h, self.in_w, self.c_in)
-        self._check(dy, "dy", self.out_h, self.out_w, self.c_out)
-        if x.shape[0] != dy.shape[0]:
-            raise ValueError("x / dy image counts differ")
+    def _grads_struct(self, grads: dict):
         sizes = {"d_u_in": self.c_in * self.rank_in, "d_u_out": self.rank_out * self.c_out,
                  "d_core": 0 if self.svd else self.rank_in * self.rank_out * self.kernel ** 2,
                  "d_values": self.nnz}
@@ -504,9 +506,35 @@ class LrsConvBackward:
             if t.dtype != self.torch.float32 or not t.is_contiguous() or t.numel() != numel or not t.is_cuda:
                 raise ValueError(f"{k}: expected a contiguous fp32 CUDA tensor of {numel} elements")
             ptrs[k] = t.data_ptr()
-        g = lrs_conv_grads(**ptrs)
+        return lrs_conv_grads(**ptrs)
+
+    def backward_weights_into(self, x, dy, grads: dict, stream=None) -> None:
+        self._check(x, "x", self.in_h, self.in_w, self.c_in)
+        self._check(dy, "dy", self.out_h, self.out_w, self.c_out)
+        if x.shape[0] != dy.shape[0]:
+            raise ValueError("x / dy image counts differ")
+        g = self._grads_struct(grads)
         s = self.torch.cuda.current_stream(self.device) if stream is None else stream
         lrs_conv_backward_weights(self.handle, x.data_ptr(), dy.data_ptr(), x.shape[0], g, s.cuda_stream)
+
+    def backward_into(self, x, dy, dx, grads: dict, stream=None) -> None:
+        """dX and the parameter gradients in one call (lrs_conv_backward: dT1 reused from
+        the transposed layer's forward)."""
+        self._check(x, "x", self.in_h, self.in_w, self.c_in)
+        self._check(dy, "dy", self.out_h, self.out_w, self.c_out)
+        self._check(dx, "dx", self.in_h, self.in_w, self.c_in)
+        if not (x.shape[0] == dy.shape[0] == dx.shape[0]):
+            raise ValueError("x / dy / dx image counts differ")
+        g = self._grads_struct(grads)
+        s = self.torch.cuda.current_stream(self.device) if stream is None else stream
+        lrs_conv_backward(self.handle, x.data_ptr(), dy.data_ptr(), dx.data_ptr(), x.shape[0], g, s.cuda_stream)
+
+    def backward(self, x, dy):
+        """(dx, gradients) of one batch."""
+        dx = self.torch.empty_like(x)
+        g = self.alloc_grads()
+        self.backward_into(x, dy, dx, g)
+        return dx, g
 
     def backward_weights(self, x, dy) -> dict:
         g = self.alloc_grads()
@@ -528,10 +556,10 @@ class LrsConvBackward:
 
     @property
     def launches(self):
-        """(backward_weights launches, backward_data launches)"""
-        d = ctypes.c_int32()
-        w = load_library().lrs_conv_bwd_launches(self.handle, ctypes.byref(d))
-        return int(w), int(d.value)
+        """(backward_weights launches, backward_data launches, backward (combined) launches)"""
+        d, c = ctypes.c_int32(), ctypes.c_int32()
+        w = load_library().lrs_conv_bwd_launches(self.handle, ctypes.byref(d), ctypes.byref(c))
+        return int(w), int(d.value), int(c.value)
 
     def close(self) -> None:
         if getattr(self, "handle", None):

@@ -110,6 +110,26 @@ def test_backward_deterministic_and_graph_capturable(name):
             assert torch.equal(g[k], g3[k]), k
 
 
+@pytest.mark.parametrize("name", ["c3_b20", "c4_b5", "small_3x3"])
+def test_combined_backward_matches_oracle_and_split_calls(name):
+    """lrs_conv_backward (dT1 reused from the transposed layer's forward): the oracle's
+    tolerance on every output, dX bitwise the backward_data result, the gradients within
+    fp32-summation-order distance (1e-3) of the two-call form."""
+    cfg = CASES[name]
+    inp = workloads.generate(cfg)
+    dy_np = workloads.generate_dy(cfg, seed=15)
+    bw, x, dy, dx, g = run_gpu(inp, dy_np)
+    dx2, g2 = bw.backward(x, dy)
+    torch.cuda.synchronize()
+    assert torch.equal(dx, dx2)
+    ref = B.backward_factored(inp.x, dy_np, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx,
+                              inp.values, cfg.stride, cfg.pad)
+    check_grads(g2, ref, cfg.svd)
+    for k in g:
+        if g[k] is not None and g[k].numel():
+            assert rel(g2[k].cpu().double().numpy(), g[k].cpu().double().numpy()) < 1e-3, k
+
+
 def test_backward_linearity_in_the_batch():
     """Weight gradients are sums over images: g(X, dY) = g(first half) + g(second half)
     (a property at any size; here through two calls of the same handle)."""

@@ -20,7 +20,6 @@ dys = [torch.from_numpy(workloads.generate_dy(cfg, cfg.batch, seed=10 + i)).to(t
 dx = torch.empty_like(xs[0])
 g = bw.alloc_grads()
 for i in range(reps):
-    bw.backward_data_into(dys[i % 2], dx)
-    bw.backward_weights_into(xs[i % 2], dys[i % 2], g)
+    bw.backward_into(xs[i % 2], dys[i % 2], dx, g)
 torch.cuda.synchronize()
 print(f"{name}: {reps} backward passes ok, launches {bw.launches}")
