@@ -479,48 +479,73 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
     work[i] = static_cast<double>(tiles[i]) * q.k_steps * q.kst * (2 + bn / 64);
   }
   // K splits and the persistent schedule: items (problem, tile, split) of about equal work,
-  // ~3 per SM, assigned longest-first to the least-loaded of the SMs' CTAs (LPT)
+  // assigned longest-first to the least-loaded of the SMs' CTAs (LPT).  The granularity g
+  // (items per SM) trades balance against the split slabs the reduction reads back: the
+  // model time = the most loaded CTA's operand bytes at ~60 B/clk per SM (TMA inbound,
+  // profiles/r02_tma_bw.log) + the slab bytes written and read at ~5 TB/s
   double total = 0;
   for (double w : work) total += w;
-  const double item_work = total / (3.0 * h->sms);
+  struct Sched {
+    std::vector<int> splits;
+    std::vector<std::vector<WgradItem>> lists;
+    std::vector<double> load;
+    size_t slab = 0;
+    double t = 1e300;
+  };
+  Sched best;
+  for (double g : {1.0, 1.5, 2.0, 3.0, 4.0}) {
+    Sched sc;
+    const double item_work = total / (g * h->sms);
+    std::vector<std::pair<double, WgradItem>> items;
+    for (int i = 0; i < np; ++i) {
+      const WgradProblem& q = h->wp.pr[i];
+      int splits = static_cast<int>(std::lround(work[i] / (tiles[i] * item_work)));
+      splits = std::max(1, std::min(splits, ksteps_max[i]));
+      sc.splits.push_back(splits);
+      sc.slab += static_cast<size_t>(splits) * q.taps * q.m_tiles * 128 * q.n_tiles * q.bn;
+      for (int t = 0; t < tiles[i]; ++t)
+        for (int sp = 0; sp < splits; ++sp) {
+          WgradItem it;
+          it.problem = static_cast<uint16_t>(i);
+          it.split = static_cast<uint16_t>(sp);
+          it.tile = t;
+          const long long kb = static_cast<long long>(q.k_steps) * sp / splits;
+          const long long ke = static_cast<long long>(q.k_steps) * (sp + 1) / splits;
+          items.push_back({static_cast<double>(ke - kb) * q.kst * (2 + q.bn / 64), it});
+        }
+    }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const std::pair<double, WgradItem>& x, const std::pair<double, WgradItem>& y) {
+                       return x.first > y.first;
+                     });
+    const int grid = std::min<int>(h->sms, static_cast<int>(items.size()));
+    sc.lists.assign(grid, {});
+    sc.load.assign(grid, 0.0);
+    for (auto& it : items) {
+      const int c = static_cast<int>(std::min_element(sc.load.begin(), sc.load.end()) - sc.load.begin());
+      sc.load[c] += it.first;
+      sc.lists[c].push_back(it.second);
+    }
+    const double mk = *std::max_element(sc.load.begin(), sc.load.end()) * 128.0 / (60.0 * 1.965e9);
+    sc.t = mk + 2.0 * sc.slab * 4.0 / 5e12;
+    if (sc.t < best.t) best = std::move(sc);
+  }
   size_t slab_off = 0;
   std::vector<size_t> slab_at(np);
-  std::vector<std::pair<double, WgradItem>> items;
   uint32_t slot = 0;
   int max_stages = 4;
   for (int i = 0; i < np; ++i) {
     WgradProblem& q = h->wp.pr[i];
-    int splits = static_cast<int>(std::lround(work[i] / (tiles[i] * item_work)));
-    splits = std::max(1, std::min(splits, ksteps_max[i]));
-    q.splits = splits;
+    q.splits = best.splits[i];
     q.split_stride = static_cast<long long>(q.taps) * q.m_tiles * 128 * q.n_tiles * q.bn;
     slab_at[i] = slab_off;
-    slab_off += static_cast<size_t>(splits) * q.split_stride;
-    for (int t = 0; t < tiles[i]; ++t)
-      for (int sp = 0; sp < splits; ++sp) {
-        WgradItem it;
-        it.problem = static_cast<uint16_t>(i);
-        it.split = static_cast<uint16_t>(sp);
-        it.tile = t;
-        const long long kb = static_cast<long long>(q.k_steps) * sp / splits;
-        const long long ke = static_cast<long long>(q.k_steps) * (sp + 1) / splits;
-        items.push_back({static_cast<double>(ke - kb) * q.kst * (2 + q.bn / 64), it});
-      }
+    slab_off += static_cast<size_t>(q.splits) * q.split_stride;
     slot = std::max(slot, q.stage_bytes);
     max_stages = std::min(max_stages, stage_count[i]);
   }
-  std::stable_sort(items.begin(), items.end(),
-                   [](const std::pair<double, WgradItem>& a, const std::pair<double, WgradItem>& b) {
-                     return a.first > b.first;
-                   });
-  const int grid = std::min<int>(h->sms, static_cast<int>(items.size()));
-  std::vector<std::vector<WgradItem>> lists(grid);
-  std::vector<double> load(grid, 0.0);
-  for (auto& it : items) {
-    const int c = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-    load[c] += it.first;
-    lists[c].push_back(it.second);
-  }
+  const int grid = static_cast<int>(best.lists.size());
+  std::vector<std::vector<WgradItem>>& lists = best.lists;
+  std::vector<double>& load = best.load;
   std::vector<WgradItem> flat;
   std::vector<int> ptr(grid + 1, 0);
   for (int c = 0; c < grid; ++c) {

@@ -1,5 +1,5 @@
-# backward pass combined call: tests, bench C3 / C2 / C4, launch list
-mkdir -p gpurun_out/bwd5; O=gpurun_out/bwd5; rm -f $O/rc.txt
+# backward pass split granularity chooser: tests, bench C3 / C2 / C4, launch list
+mkdir -p gpurun_out/bwd6; O=gpurun_out/bwd6; rm -f $O/rc.txt
 timeout 1200 python -m pytest tests/test_gpu_backward.py -q -x > $O/pytest_bwd.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
 for c in c3 c2_bf16 c4; do
   LRS_VERBOSE= timeout 900 python bench.py --backward --config $c --steps 50 --warmup 5 --no-cpu > $O/bench_bwd_$c.json 2> $O/bench_bwd_$c.err; echo "bench $c rc=$?" >> $O/rc.txt
