@@ -391,6 +391,57 @@ const char *lrs_conv_bwd_stage_name(const lrs_conv_bwd *h, int32_t stage);
 
 lrs_status lrs_conv_bwd_destroy(lrs_conv_bwd *h); /* NULL-safe; no call may be in flight */
 
+/* ------------------------------------------------------------------------------------------
+ * Decomposition: the offline side of the method, W ~ L + S with L of CP rank
+ * r (L_ijkt = A_ir B_jr C_kr D_tr) and S of fixed cardinality c, by the paper's
+ * two-step iteration:  L_i = update(L_{i-1}, W - S_{i-1});  S_i = P_c(W - L_i)
+ * with update = one alternating-least-squares sweep over the four factors (SPEC.md:151-158:
+ * F_n = mttkrp(W - S, F, n) (*_{m != n} F_m^T F_m)^+, pseudo-inverse with a relative eigenvalue
+ * cutoff rcond) and P_c = the n = round(c * numel) entries of largest |value|, ties to the
+ * smaller linear index.  eps_i = ||W - L_i - S_i||_F / ||W||_F; the run stops
+ * when eps improves by less than tol (after the first iteration) or after max_iters.
+ * oracle/lrs_decomp.py writes the same algorithm out step by step.
+ *
+ * W: device fp64 [dims[0]][dims[1]][dims[2]][dims[3]] row-major (a conv weight (in, out, kh, kw):
+ * F0 = u_in, F1 = u_out^T, F2 / F3 = the CP core kind's B / C, see LRS_CORE_CP).  Every step
+ * runs in fp64 CUDA kernels (lrs_decomp.cuh): MTTKRP as split reductions added in a fixed order,
+ * the R x R pseudo-inverse by a one-CTA parallel-ordering Jacobi eigensolver, the projection
+ * by an exact radix select over the fp64 bit patterns of |W - L| plus an index-ordered
+ * compaction -- deterministic: the same inputs give the same bits.
+ * Requirements: dims > 0, dims[2], dims[3] <= 8, numel < 2^31, 1 <= rank <= 256,
+ * 0 <= cardinality < 1, max_iters >= 1, rcond >= 0.
+ */
+typedef struct lrs_decomp_params {
+  int32_t dims[4];     /* I0..I3 of W                                            */
+  int32_t rank;        /* CP rank r                                              */
+  double cardinality;  /* c: S keeps round(c * numel) entries (half to even)     */
+  int32_t max_iters;   /* >= 1                                                   */
+  double tol;          /* stop when eps_{i-1} - eps_i < tol (i >= 1)             */
+  double rcond;        /* pseudo-inverse cutoff relative to the largest eigenvalue (SPEC: 1e-10) */
+} lrs_decomp_params;
+
+typedef struct lrs_decomp lrs_decomp; /* opaque: fp64 workspace for one W shape */
+
+lrs_status lrs_decomp_create(const lrs_decomp_params *p, int device, lrs_decomp **out);
+
+/* Run the iteration from the initial factors f0..f3 (device fp64 [dims[m]][rank], e.g. the
+   leading singular vectors of the mode unfoldings, or random), which are
+   overwritten with the result.  S: s_idx (device int64, linear indices ascending) and
+   s_val (device fp64), capacity round(c * numel) (lrs_decomp_nnz); *s_count = entries
+   written.  eps_hist: host [max_iters]; *iters_done = iterations run.  Enqueued on `stream`
+   and synchronised once per iteration (the stopping rule runs on the host): NOT
+   graph-capturable.  A zero W gives zero factors, an empty S and eps 0. */
+lrs_status lrs_decomp_run(lrs_decomp *h, const double *w, double *f0, double *f1, double *f2, double *f3,
+                          int64_t *s_idx, double *s_val, int64_t *s_count, double *eps_hist,
+                          int32_t *iters_done, void *stream);
+int64_t lrs_decomp_nnz(const lrs_decomp *h); /* round(c * numel) */
+/* stage timing: 0 MTTKRP (+ partial sums), 1 pseudo-inverse + factor update + Gram,
+   2 residual W - L, 3 projection P_c + T = W - S + eps */
+lrs_status lrs_decomp_set_timing(lrs_decomp *h, int32_t enable);
+lrs_status lrs_decomp_stage_times(lrs_decomp *h, float *ms, int64_t *counts, int32_t max_stages,
+                                  int32_t *n_stages, int32_t reset);
+lrs_status lrs_decomp_destroy(lrs_decomp *h); /* NULL-safe */
+
 #ifdef __cplusplus
 }
 #endif

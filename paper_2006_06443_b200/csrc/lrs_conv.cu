@@ -27,6 +27,7 @@
 #include "lrs_pw.cuh"
 #include "lrs_pwf.cuh"
 #include "lrs_wgrad.cuh"
+#include "lrs_decomp.cuh"
 
 using namespace lrs;
 
@@ -3004,3 +3005,5 @@ lrs_status lrs_conv_debug_buffer(const lrs_conv* h, int32_t which, const void** 
 
 // the backward pass (include/lrs_conv.h "Backward pass"); shares this unit's helpers
 #include "lrs_backward.cuh"
+// the low-rank + sparse decomposition (include/lrs_conv.h "Decomposition")
+#include "lrs_decomp_host.cuh"

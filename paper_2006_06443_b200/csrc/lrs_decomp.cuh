@@ -1,0 +1,462 @@
+// lrs_decomp.cuh -- the low-rank + sparse DECOMPOSITION W ~ L + S on the GPU (
+// PAPER.md:124-146 §3.2; oracle/lrs_decomp.py).  fp64 throughout (the ALS normal equations
+// are solved by a pseudo-inverse with a 1e-10 relative cutoff).
+//
+// W is an order-4 tensor [I0][I1][I2][I3] (a conv weight: in, out, kh, kw) with I2*I3 <= 64;
+// L is CP rank r: L = sum_r F0[:,r] o F1[:,r] o F2[:,r] o F3[:,r].  One iteration
+// of the paper's two-step scheme:
+//   1. ALS sweep on T = W - S (modes 0..3 in order):   M = MTTKRP(T, F, m)   lrs_mttkrp*_kernel
+//                                                       V = *_{o != m} F_o^T F_o, P = V^+
+//                                                                              lrs_sym_pinv_kernel
+//                                                       F_m = M P             lrs_cp_update_kernel
+//   2. Rsd = W - L  (L reconstructed on the fly)                              lrs_cp_residual_kernel
+//   3. S = P_c(Rsd): the n = round(c numel) largest |Rsd| (ties: smaller index) by an exact
+//      8-bit-digit radix select over the fp64 bit patterns of |Rsd| and an ordered compaction
+//                                                       lrs_radix_hist_kernel / lrs_radix_pick_kernel /
+//                                                       lrs_select_flags_kernel / scan / compact
+//   4. T = W - S, eps = ||Rsd - S|| / ||W||                                    lrs_decomp_finish_kernel
+// MTTKRP is a reduction over the other three modes; it is split over blocks and the partial
+// sums are added in a fixed order (deterministic results: the same inputs give the same bits).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lrs {
+
+constexpr int kDThreads = 256;
+
+// ---------------------------------------------------------------- MTTKRP, modes 0 and 1
+// M[i][r] = sum_j F_other[j][r] * sum_q T[i, j, q] KR23[q][r] where (i, j) = (i0, i1) for mode
+// 0 and (i1, i0) for mode 1, q over the I2*I3 inner entries, KR23[q][r] = F2[q / I3][r] F3[q % I3][r].
+// Block (i, chunk): threads over r, a chunk of j; partial sums part[chunk][i][r].
+struct MttkrpParams {
+  const double* t;         // [I0][I1][Q]
+  const double* f[4];
+  double* part;            // [nchunk][I_m][R]
+  int dims[4];
+  int q;                   // I2 * I3
+  int r;                   // rank
+  int mode;
+  int nchunk, chunk;       // chunks of the reduced outer index
+};
+
+__global__ void __launch_bounds__(kDThreads) lrs_mttkrp01_kernel(const __grid_constant__ MttkrpParams p) {
+  __shared__ double kr[64 * 256 / 4];  // KR23 for this block's r slice (<= 64 x 64) -- see below
+  const int i = blockIdx.x;
+  const int c = blockIdx.y;
+  const int r0 = blockIdx.z * 64;       // r slice of 64 (4 warps x 2 ... threads = 256: 4 j-lanes x 64 r)
+  const int rr = threadIdx.x & 63;
+  const int jl = threadIdx.x >> 6;      // 0..3
+  const int r = r0 + rr;
+  const int I2 = p.dims[2], I3 = p.dims[3], Q = p.q;
+  for (int e = threadIdx.x; e < Q * 64; e += kDThreads) {
+    const int qq = e / 64, x = e % 64;
+    const int rx = r0 + x;
+    kr[e] = rx < p.r ? p.f[2][(qq / I3) * p.r + rx] * p.f[3][(qq % I3) * p.r + rx] : 0.0;
+  }
+  __syncthreads();
+  (void)I2;
+  const int n_other = p.mode == 0 ? p.dims[1] : p.dims[0];
+  const double* fo = p.mode == 0 ? p.f[1] : p.f[0];
+  const long long s_i = p.mode == 0 ? static_cast<long long>(p.dims[1]) * Q : Q;
+  const long long s_j = p.mode == 0 ? Q : static_cast<long long>(p.dims[1]) * Q;
+  const int j_begin = c * p.chunk, j_end = min(n_other, j_begin + p.chunk);
+  double acc = 0.0;
+  if (r < p.r) {
+    for (int j = j_begin + jl; j < j_end; j += 4) {
+      const double* tp = p.t + i * s_i + j * s_j;
+      double inner = 0.0;
+      for (int qq = 0; qq < Q; ++qq) inner = fma(__ldg(tp + qq), kr[qq * 64 + rr], inner);
+      acc = fma(__ldg(fo + static_cast<long long>(j) * p.r + r), inner, acc);
+    }
+  }
+  // the 4 j-lanes of one r: fixed-order sum through shared memory
+  __syncthreads();
+  double* red = kr;
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (jl == 0 && r < p.r) {
+    const double s = ((red[rr] + red[64 + rr]) + red[128 + rr]) + red[192 + rr];
+    p.part[(static_cast<long long>(c) * p.dims[p.mode] + i) * p.r + r] = s;
+  }
+}
+
+// ---------------------------------------------------------------- MTTKRP, modes 2 and 3
+// M[k][r] (mode 2) = sum_{i0,i1} F0[i0][r] F1[i1][r] sum_t T[i0,i1,k,t] F3[t][r]; mode 3 alike
+// with (k, t) swapped.  Block (chunk of (i0, i1) pairs, r slice): per-thread registers for the
+// <= 8 outputs, fixed-order combination of the 4 pair-lanes; partials part[chunk][I_m][R].
+__global__ void __launch_bounds__(kDThreads) lrs_mttkrp23_kernel(const __grid_constant__ MttkrpParams p) {
+  __shared__ double red[kDThreads * 8];
+  const int c = blockIdx.x;
+  const int r0 = blockIdx.z * 64;
+  const int rr = threadIdx.x & 63;
+  const int pl = threadIdx.x >> 6;
+  const int r = r0 + rr;
+  const int I2 = p.dims[2], I3 = p.dims[3], Q = p.q;
+  const int nout = p.mode == 2 ? I2 : I3;
+  const int nin = p.mode == 2 ? I3 : I2;
+  const double* fin = p.mode == 2 ? p.f[3] : p.f[2];
+  double acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+  const long long npairs = static_cast<long long>(p.dims[0]) * p.dims[1];
+  const long long b = static_cast<long long>(c) * p.chunk;
+  const long long e_end = min(npairs, b + p.chunk);
+  if (r < p.r) {
+    double fi[8];
+    for (int t = 0; t < nin; ++t) fi[t] = __ldg(fin + t * p.r + r);
+    for (long long pr = b + pl; pr < e_end; pr += 4) {
+      const int i0 = static_cast<int>(pr / p.dims[1]), i1 = static_cast<int>(pr % p.dims[1]);
+      const double g = __ldg(p.f[0] + static_cast<long long>(i0) * p.r + r) * __ldg(p.f[1] + static_cast<long long>(i1) * p.r + r);
+      const double* tp = p.t + pr * Q;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k < nout) {
+          double s = 0.0;
+          for (int t = 0; t < nin; ++t) {
+            const int qq = p.mode == 2 ? k * I3 + t : t * I3 + k;
+            s = fma(__ldg(tp + qq), fi[t], s);
+          }
+          acc[k] = fma(g, s, acc[k]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) red[k * kDThreads + threadIdx.x] = acc[k];
+  __syncthreads();
+  if (pl == 0 && r < p.r) {
+    for (int k = 0; k < nout; ++k) {
+      const double* q = red + k * kDThreads;
+      const double s = ((q[rr] + q[64 + rr]) + q[128 + rr]) + q[192 + rr];
+      p.part[(static_cast<long long>(c) * nout + k) * p.r + r] = s;
+    }
+  }
+}
+
+// part[nchunk][rows][R] -> m[rows][R], chunks added in order
+__global__ void lrs_part_sum_kernel(const double* part, int nchunk, long long count, double* m) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunk; ++c) s += part[c * count + i];
+  m[i] = s;
+}
+
+// G[a][b] = sum_i F[i][a] F[i][b]  (one Gram matrix)
+__global__ void lrs_gram_kernel(const double* f, int rows, int r, double* g) {
+  const int a = blockIdx.x, b = threadIdx.x;
+  if (b >= r) return;
+  double s = 0.0;
+  for (int i = 0; i < rows; ++i) s = fma(f[static_cast<long long>(i) * r + a], f[static_cast<long long>(i) * r + b], s);
+  g[a * r + b] = s;
+}
+
+// ---------------------------------------------------------------- pseudo-inverse (one CTA)
+// V = Hadamard product of the three Gram matrices of the other modes (SPD, R x R); cyclic
+// Jacobi with the parallel (round-robin) ordering: each round rotates R/2 disjoint (p, q)
+// pairs at once (rows, then columns, then the eigenvector columns); sweeps until the
+// off-diagonal mass is below 1e-30 of the total.  P = Q diag(1/lambda, lambda > rcond max) Q^T.
+struct PinvParams {
+  const double* g[4];
+  int mode;
+  int r;       // rank
+  int rp;      // rank rounded up to even (a dummy index pads odd ranks)
+  double rcond;
+  double* a;   // workspace [rp][rp]
+  double* v;   // workspace [rp][rp]
+  double* p;   // out [r][r]
+  int* sweeps; // out (diagnostic)
+};
+
+constexpr int kJThreads = 512;
+
+__global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_constant__ PinvParams q) {
+  __shared__ double cs[256][2];
+  __shared__ int pairs[256][2];
+  __shared__ double offn, totn;
+  __shared__ double wsum[kJThreads / 32][2];
+  const int n = q.rp, r = q.r;
+  double* A = q.a;
+  double* V = q.v;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    double val = 0.0;
+    if (i < r && j < r) {
+      val = 1.0;
+      for (int o = 0; o < 4; ++o)
+        if (o != q.mode) val *= q.g[o][i * r + j];
+    } else if (i == j) {
+      val = 0.0;  // dummy index: a zero eigenvalue, dropped by the cutoff
+    }
+    A[e] = val;
+    V[e] = i == j ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    // convergence test
+    double lo = 0.0, lt = 0.0;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const double x = A[e] * A[e];
+      lt += x;
+      if (e / n != e % n) lo += x;
+    }
+    for (int o = 16; o; o >>= 1) {
+      lo += __shfl_xor_sync(0xffffffffu, lo, o);
+      lt += __shfl_xor_sync(0xffffffffu, lt, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      wsum[threadIdx.x >> 5][0] = lo;
+      wsum[threadIdx.x >> 5][1] = lt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // fixed order: the sweep count is deterministic
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+        a += wsum[w][0];
+        b += wsum[w][1];
+      }
+      offn = a;
+      totn = b;
+    }
+    __syncthreads();
+    if (!(offn > 1e-30 * totn)) break;
+    __syncthreads();
+    for (int round = 0; round < n - 1; ++round) {
+      // pairs of this round (circle method: 0 fixed, the rest rotated by `round`)
+      for (int k = threadIdx.x; k < n / 2; k += blockDim.x) {
+        auto pos = [&](int i) { return i == 0 ? 0 : 1 + ((i - 1 + round) % (n - 1)); };
+        int pp = pos(k), qq = pos(n - 1 - k);
+        if (pp > qq) {
+          const int t = pp;
+          pp = qq;
+          qq = t;
+        }
+        pairs[k][0] = pp;
+        pairs[k][1] = qq;
+        const double apq = A[pp * n + qq];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0) {
+          const double theta = (A[qq * n + qq] - A[pp * n + pp]) / (2.0 * apq);
+          const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+          c = 1.0 / sqrt(t * t + 1.0);
+          s = t * c;
+        }
+        cs[k][0] = c;
+        cs[k][1] = s;
+      }
+      __syncthreads();
+      // rows:  A <- P^T A
+      for (int e = threadIdx.x; e < (n / 2) * n; e += blockDim.x) {
+        const int k = e / n, j = e % n;
+        const int pp = pairs[k][0], qq = pairs[k][1];
+        const double c = cs[k][0], s = cs[k][1];
+        const double ap = A[pp * n + j], aq = A[qq * n + j];
+        A[pp * n + j] = c * ap - s * aq;
+        A[qq * n + j] = s * ap + c * aq;
+      }
+      __syncthreads();
+      // columns: A <- A P, V <- V P
+      for (int e = threadIdx.x; e < (n / 2) * n; e += blockDim.x) {
+        const int k = e / n, i = e % n;
+        const int pp = pairs[k][0], qq = pairs[k][1];
+        const double c = cs[k][0], s = cs[k][1];
+        const double ap = A[i * n + pp], aq = A[i * n + qq];
+        A[i * n + pp] = c * ap - s * aq;
+        A[i * n + qq] = s * ap + c * aq;
+        const double vp = V[i * n + pp], vq = V[i * n + qq];
+        V[i * n + pp] = c * vp - s * vq;
+        V[i * n + qq] = s * vp + c * vq;
+      }
+      __syncthreads();
+    }
+  }
+  // P = sum_k [lambda_k > rcond * max] V[:, k] V[:, k]^T / lambda_k
+  __shared__ double lmax;
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int k = 0; k < n; ++k) m = fmax(m, fabs(A[k * n + k]));
+    lmax = m;
+    if (q.sweeps) *q.sweeps = sweep;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const int i = e / r, j = e % r;
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) {
+      const double lam = A[k * n + k];
+      if (fabs(lam) > q.rcond * lmax) s += V[i * n + k] * V[j * n + k] / lam;
+    }
+    q.p[e] = s;
+  }
+}
+
+// F[i][c] = sum_k M[i][k] P[k][c]
+__global__ void lrs_cp_update_kernel(const double* m, const double* pm, int rows, int r, double* f) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<long long>(rows) * r) return;
+  const int i = static_cast<int>(e / r), c = static_cast<int>(e % r);
+  double s = 0.0;
+  for (int k = 0; k < r; ++k) s = fma(m[static_cast<long long>(i) * r + k], pm[k * r + c], s);
+  f[e] = s;
+}
+
+// ---------------------------------------------------------------- residual Rsd = W - L
+// block (i0, chunk of i1): the block's F0 row and the KR23 table in shared memory; thread per
+// (i1, q) entry; L = sum_r F0[i0][r] F1[i1][r] KR23[q][r]
+__global__ void __launch_bounds__(kDThreads) lrs_cp_residual_kernel(const double* w, const double* f0,
+                                                                     const double* f1, const double* f2,
+                                                                     const double* f3, int i1n, int i3n, int q,
+                                                                     int r, double* rsd) {
+  extern __shared__ double dsm[];
+  double* f0r = dsm;         // [r]
+  double* kr = dsm + r;      // [q][r]
+  const int i0 = blockIdx.x;
+  for (int e = threadIdx.x; e < r; e += blockDim.x) f0r[e] = f0[static_cast<long long>(i0) * r + e];
+  for (int e = threadIdx.x; e < q * r; e += blockDim.x) {
+    const int qq = e / r, x = e % r;
+    kr[e] = f2[(qq / i3n) * r + x] * f3[(qq % i3n) * r + x] * f0r[x];
+  }
+  __syncthreads();
+  const long long row = static_cast<long long>(i1n) * q;
+  for (long long e = static_cast<long long>(blockIdx.y) * blockDim.x + threadIdx.x; e < row;
+       e += static_cast<long long>(gridDim.y) * blockDim.x) {
+    const int i1 = static_cast<int>(e / q), qq = static_cast<int>(e % q);
+    const double* fr = f1 + static_cast<long long>(i1) * r;
+    const double* kq = kr + qq * r;
+    double s = 0.0;
+    for (int x = 0; x < r; ++x) s = fma(__ldg(fr + x), kq[x], s);
+    const long long gi = static_cast<long long>(i0) * row + e;
+    rsd[gi] = w[gi] - s;
+  }
+}
+
+// ---------------------------------------------------------------- P_c: exact radix select
+// keys = bit patterns of |Rsd| (non-negative doubles order like their uint64 bits).  State:
+// st[0] = key prefix found so far, st[1] = its mask, st[2] = entries still needed among keys
+// matching the prefix; st[3] = entries strictly above the final key (set by the last pick).
+__global__ void lrs_radix_hist_kernel(const double* rsd, long long n, const unsigned long long* st, int shift,
+                                      unsigned int* hist) {
+  __shared__ unsigned int h[256];
+  for (int e = threadIdx.x; e < 256; e += blockDim.x) h[e] = 0;
+  __syncthreads();
+  const unsigned long long pre = st[0], mask = st[1];
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const unsigned long long k = static_cast<unsigned long long>(__double_as_longlong(fabs(rsd[i])));
+    if ((k & mask) == pre) atomicAdd(&h[(k >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 256; e += blockDim.x)
+    if (h[e]) atomicAdd(&hist[e], h[e]);
+}
+
+// one thread: the digit (from the top) at which the count of larger keys reaches `need`
+__global__ void lrs_radix_pick_kernel(unsigned long long* st, int shift, unsigned int* hist) {
+  unsigned long long need = st[2];
+  int d = 255;
+  for (; d > 0; --d) {
+    if (hist[d] >= need) break;
+    need -= hist[d];
+  }
+  st[0] |= static_cast<unsigned long long>(d) << shift;
+  st[1] |= 255ull << shift;
+  st[2] = need;  // entries to take among keys equal to the final prefix
+  for (int e = 0; e < 256; ++e) hist[e] = 0;
+}
+
+// flag[i] = 1 if |Rsd[i]| > K*, or == K* (the selected key) -- the latter count toward the
+// ordered tie-break below; eq[i] = 1 for the ties
+__global__ void lrs_select_flags_kernel(const double* rsd, long long n, const unsigned long long* st,
+                                        unsigned int* gt, unsigned int* eq) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long k = static_cast<unsigned long long>(__double_as_longlong(fabs(rsd[i])));
+  gt[i] = k > st[0] ? 1u : 0u;
+  eq[i] = k == st[0] ? 1u : 0u;
+}
+
+// exclusive scan helpers (two levels; block = 1024 elements)
+constexpr int kScanBlock = 1024;
+__global__ void lrs_scan_block_kernel(const unsigned int* in, long long n, unsigned int* out, unsigned int* sums) {
+  __shared__ unsigned int s[kScanBlock];
+  const long long base = static_cast<long long>(blockIdx.x) * kScanBlock;
+  for (int e = threadIdx.x; e < kScanBlock; e += blockDim.x) s[e] = base + e < n ? in[base + e] : 0u;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int acc = 0;
+    for (int e = 0; e < kScanBlock; ++e) {
+      const unsigned int v = s[e];
+      s[e] = acc;
+      acc += v;
+    }
+    sums[blockIdx.x] = acc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kScanBlock; e += blockDim.x)
+    if (base + e < n) out[base + e] = s[e];
+}
+__global__ void lrs_scan_sums_kernel(unsigned int* sums, int nb) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned int acc = 0;
+    for (int b = 0; b < nb; ++b) {
+      const unsigned int v = sums[b];
+      sums[b] = acc;
+      acc += v;
+    }
+  }
+}
+
+// selection + compaction in index order, T = W - S, and the residual mass of the entries
+// S does not take (per-block partials, added in order by lrs_decomp_eps_kernel)
+__global__ void lrs_decomp_finish_kernel(const double* w, const double* rsd, long long n,
+                                         const unsigned long long* st, const unsigned int* gt,
+                                         const unsigned int* eq, const unsigned int* eq_pre,
+                                         const unsigned int* eq_sums, unsigned int* sel, double* t,
+                                         double* eps_part) {
+  __shared__ double red[kDThreads];
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double rem = 0.0;
+  if (i < n) {
+    const unsigned long long take_eq = st[2];
+    const unsigned int rank_eq = eq_pre[i] + eq_sums[i / kScanBlock];
+    const bool s = gt[i] || (eq[i] && rank_eq < take_eq);
+    sel[i] = s ? 1u : 0u;
+    t[i] = s ? w[i] - rsd[i] : w[i];
+    if (!s) rem = rsd[i] * rsd[i];
+  }
+  red[threadIdx.x] = rem;
+  __syncthreads();
+  for (int o = kDThreads / 2; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) eps_part[blockIdx.x] = red[0];
+}
+
+__global__ void lrs_decomp_compact_kernel(const double* rsd, long long n, const unsigned int* sel,
+                                          const unsigned int* pre, const unsigned int* sums, long long* idx,
+                                          double* val) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n || !sel[i]) return;
+  const unsigned int o = pre[i] + sums[i / kScanBlock];
+  idx[o] = i;
+  val[o] = rsd[i];
+}
+
+__global__ void lrs_decomp_eps_kernel(const double* part, int nb, double* out) {
+  __shared__ double red[kDThreads];
+  double s = 0.0;
+  // fixed-order: thread t sums blocks t, t + 256, ... in order; then a fixed tree
+  for (int b = threadIdx.x; b < nb; b += kDThreads) s += part[b];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = kDThreads / 2; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+}  // namespace lrs

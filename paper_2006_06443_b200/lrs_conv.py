@@ -33,7 +33,9 @@ EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs
             "lrs_sparse_from_slices",
             "lrs_conv_bwd_create", "lrs_conv_backward_data", "lrs_conv_backward_weights", "lrs_conv_backward",
             "lrs_conv_bwd_launches", "lrs_conv_bwd_destroy", "lrs_conv_bwd_set_timing",
-            "lrs_conv_bwd_stage_times", "lrs_conv_bwd_stage_name")
+            "lrs_conv_bwd_stage_times", "lrs_conv_bwd_stage_name",
+            "lrs_decomp_create", "lrs_decomp_run", "lrs_decomp_nnz", "lrs_decomp_set_timing",
+            "lrs_decomp_stage_times", "lrs_decomp_destroy")
 
 
 class LrsError(RuntimeError):
@@ -61,6 +63,11 @@ class lrs_conv_desc(ctypes.Structure):
         ("out_bias", ctypes.POINTER(ctypes.c_float)),
         ("out_relu", ctypes.c_int32),
     ]
+
+
+class lrs_decomp_params(ctypes.Structure):
+    _fields_ = [("dims", ctypes.c_int32 * 4), ("rank", ctypes.c_int32), ("cardinality", ctypes.c_double),
+                ("max_iters", ctypes.c_int32), ("tol", ctypes.c_double), ("rcond", ctypes.c_double)]
 
 
 class lrs_conv_grads(ctypes.Structure):
@@ -125,6 +132,18 @@ def load_library(path: str = LIB_PATH):
     lib.lrs_conv_bwd_stage_name.restype = ctypes.c_char_p
     for name in ("lrs_conv_bwd_create", "lrs_conv_backward_data", "lrs_conv_backward_weights", "lrs_conv_backward",
                  "lrs_conv_bwd_destroy", "lrs_conv_bwd_set_timing", "lrs_conv_bwd_stage_times"):
+        getattr(lib, name).restype = ctypes.c_int
+    lib.lrs_decomp_create.argtypes = [ctypes.POINTER(lrs_decomp_params), ctypes.c_int, ctypes.POINTER(P)]
+    lib.lrs_decomp_run.argtypes = [P, P, P, P, P, P, P, P, ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32), P]
+    lib.lrs_decomp_nnz.argtypes = [P]
+    lib.lrs_decomp_nnz.restype = ctypes.c_int64
+    lib.lrs_decomp_set_timing.argtypes = [P, ctypes.c_int32]
+    lib.lrs_decomp_stage_times.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64),
+                                           ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]
+    lib.lrs_decomp_destroy.argtypes = [P]
+    for name in ("lrs_decomp_create", "lrs_decomp_run", "lrs_decomp_set_timing", "lrs_decomp_stage_times",
+                 "lrs_decomp_destroy"):
         getattr(lib, name).restype = ctypes.c_int
     for name in ("lrs_conv_debug_trace", "lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
                  "lrs_conv_output_shape", "lrs_conv_set_timing", "lrs_conv_stage_times",
@@ -564,6 +583,70 @@ class LrsConvBackward:
     def close(self) -> None:
         if getattr(self, "handle", None):
             lrs_conv_bwd_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LrsDecomp:
+    """The low-rank + sparse decomposition W ~ L + S on the GPU (include/lrs_conv.h
+    "Decomposition"): CP rank `rank`, S of cardinality c, by the paper's
+    two-step iteration.  run(w, factors) takes W as a device fp64 tensor [I0, I1, I2, I3] and
+    the initial factors (device fp64 [I_m, rank]; overwritten with the result) and returns
+    (s_idx int64, s_val fp64 device tensors, eps history list)."""
+
+    STAGES = ("mttkrp", "pinv_update", "residual", "project")
+
+    def __init__(self, dims, rank: int, cardinality: float, max_iters: int = 100, tol: float = 1e-6,
+                 rcond: float = 1e-10, device: int = 0):
+        import torch
+        self.torch = torch
+        self.dims = tuple(int(d) for d in dims)
+        self.rank, self.max_iters, self.device = int(rank), int(max_iters), device
+        prm = lrs_decomp_params(dims=(ctypes.c_int32 * 4)(*self.dims), rank=self.rank, cardinality=float(cardinality),
+                                max_iters=self.max_iters, tol=float(tol), rcond=float(rcond))
+        h = ctypes.c_void_p()
+        _check(load_library().lrs_decomp_create(ctypes.byref(prm), device, ctypes.byref(h)))
+        self.handle = h.value
+        self.nnz = int(load_library().lrs_decomp_nnz(self.handle))
+
+    def run(self, w, factors, stream=None):
+        torch = self.torch
+        if w.dtype != torch.float64 or not w.is_cuda or tuple(w.shape) != self.dims or not w.is_contiguous():
+            raise ValueError(f"w: expected a contiguous fp64 CUDA tensor of shape {self.dims}")
+        for m, f in enumerate(factors):
+            if f.dtype != torch.float64 or not f.is_cuda or tuple(f.shape) != (self.dims[m], self.rank) or \
+                    not f.is_contiguous():
+                raise ValueError(f"factor {m}: expected a contiguous fp64 CUDA tensor [{self.dims[m]}, {self.rank}]")
+        dev = w.device
+        idx = torch.empty(max(self.nnz, 1), dtype=torch.int64, device=dev)
+        val = torch.empty(max(self.nnz, 1), dtype=torch.float64, device=dev)
+        eps = (ctypes.c_double * self.max_iters)()
+        cnt = ctypes.c_int64()
+        its = ctypes.c_int32()
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        _check(load_library().lrs_decomp_run(self.handle, w.data_ptr(), *(f.data_ptr() for f in factors),
+                                             idx.data_ptr(), val.data_ptr(), ctypes.byref(cnt), eps, ctypes.byref(its),
+                                             s.cuda_stream))
+        return idx[:cnt.value], val[:cnt.value], [eps[i] for i in range(its.value)]
+
+    def set_timing(self, on: bool) -> None:
+        _check(load_library().lrs_decomp_set_timing(self.handle, 1 if on else 0))
+
+    def stage_times(self, reset: bool = True):
+        ms = (ctypes.c_float * 4)()
+        cnt = (ctypes.c_int64 * 4)()
+        ns = ctypes.c_int32()
+        _check(load_library().lrs_decomp_stage_times(self.handle, ms, cnt, 4, ctypes.byref(ns), 1 if reset else 0))
+        return {self.STAGES[i]: (ms[i], cnt[i]) for i in range(ns.value)}
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _check(load_library().lrs_decomp_destroy(self.handle))
             self.handle = None
 
     def __del__(self):

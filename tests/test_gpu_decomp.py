@@ -1,0 +1,119 @@
+"""GPU parity of the low-rank + sparse decomposition
+against the fp64 oracle (oracle/lrs_decomp.py, pinned in tests/test_decomp_oracle.py),
+through the C-ABI (lrs_decomp_create / lrs_decomp_run).
+
+Both sides compute in fp64; the projection P_c is integer / index work and must select
+exactly the oracle's entries (ties to the smaller index) -- bit-exact when both sides see
+the same tensor (zero initial factors make L = 0, so P_c acts on W itself), and identical
+supports along short runs where the residuals agree to ~1e-13.  Factors and eps histories
+within 1e-8 relative (fp64, different summation orders).
+"""
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from oracle import lrs_decomp as D
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def run_gpu(w, f0, card, iters, tol=0.0, rcond=1e-10):
+    from paper_2006_06443_b200 import LrsDecomp
+    dc = LrsDecomp(w.shape, f0[0].shape[1], card, max_iters=iters, tol=tol, rcond=rcond)
+    wd = torch.from_numpy(np.ascontiguousarray(w, np.float64)).cuda()
+    fs = [torch.from_numpy(np.ascontiguousarray(f, np.float64)).cuda() for f in f0]
+    idx, val, eps = dc.run(wd, fs)
+    torch.cuda.synchronize()
+    return [f.cpu().numpy() for f in fs], idx.cpu().numpy(), val.cpu().numpy(), eps
+
+
+def test_projection_exact_with_ties():
+    """Zero initial factors keep L = 0 (V = 0 has an empty pseudo-inverse), so S = P_c(W):
+    the GPU's radix select + ordered compaction must pick exactly the oracle's entries,
+    including runs of equal |value| decided by the index."""
+    rng = np.random.default_rng(0)
+    dims = (64, 48, 3, 3)
+    w = np.round(rng.standard_normal(dims) * 4) / 4  # many exact ties in |w|
+    f0 = [np.zeros((d, 4)) for d in dims]
+    for card in (0.0, 0.001, 0.01, 0.05, 0.3):
+        f, idx, val, eps = run_gpu(w, f0, card, 1)
+        ridx, rval = D.project_sparse(w, card)
+        assert np.array_equal(idx, ridx), card
+        assert np.array_equal(val, rval), card
+        assert all(not np.any(x) for x in f)
+
+
+@pytest.mark.parametrize("rank", [8, 33])
+def test_one_iteration_matches_oracle(rank):
+    rng = np.random.default_rng(1)
+    dims = (40, 36, 3, 3)
+    w = rng.standard_normal(dims)
+    f0 = [rng.standard_normal((d, rank)) for d in dims]
+    f, idx, val, eps = run_gpu(w, f0, 0.02, 1)
+    rf, (ridx, rval), reps = D.decompose_lrs(w, f0, 0.02, max_iters=1, tol=0.0)
+    for m in range(4):
+        assert rel(f[m], rf[m]) < 1e-8, m
+    assert np.array_equal(idx, ridx)
+    assert rel(val, rval) < 1e-8
+    assert abs(eps[0] - reps[0]) < 1e-9
+
+
+def test_iterations_match_oracle_on_a_planted_tensor():
+    cfg = workloads.DecompConfig("t", (48, 40, 3, 3), 6, 8, 0.01)
+    w, f0 = workloads.generate_decomp(cfg)
+    f, idx, val, eps = run_gpu(w, f0, cfg.cardinality, 12)
+    rf, (ridx, rval), reps = D.decompose_lrs(w, f0, cfg.cardinality, max_iters=12, tol=0.0)
+    assert len(eps) == len(reps) == 12
+    assert np.allclose(eps, reps, rtol=1e-7, atol=1e-12)
+    assert np.array_equal(idx, ridx)
+    l_gpu = D.cp_reconstruct(f)
+    assert rel(l_gpu, D.cp_reconstruct(rf)) < 1e-7
+
+
+def test_planted_spikes_recovered_on_gpu():
+    """SPEC.md:167 (as in tests/test_decomp_oracle.py): rank 2 + 1 % spikes of magnitude 10."""
+    rng = np.random.default_rng(7)
+    dims = (10, 10, 3, 3)
+    low = D.cp_reconstruct([rng.standard_normal((d, 2)) for d in dims])
+    n = int(round(0.01 * low.size))
+    spikes = np.sort(rng.choice(low.size, n, replace=False))
+    w = low.copy()
+    w.flat[spikes] += 10.0 * np.sign(rng.standard_normal(n))
+    f, idx, val, eps = run_gpu(w, D.svd_init(w, 2), 0.01, 300, tol=0.0)
+    assert eps[-1] < 1e-3
+    assert np.array_equal(idx, spikes)
+
+
+def test_stopping_rule_determinism_and_zero_w():
+    cfg = workloads.DecompConfig("t", (32, 24, 3, 3), 4, 6, 0.02, seed=3)
+    w, f0 = workloads.generate_decomp(cfg)
+    a = run_gpu(w, f0, cfg.cardinality, 200, tol=1e-4)
+    b = run_gpu(w, f0, cfg.cardinality, 200, tol=1e-4)
+    _, _, reps = D.decompose_lrs(w, f0, cfg.cardinality, max_iters=200, tol=1e-4)
+    assert len(a[3]) == len(reps) < 200  # the same stopping iteration as the oracle
+    for x, y in zip(a[0], b[0]):
+        assert np.array_equal(x, y)  # bitwise reproducible
+    assert np.array_equal(a[1], b[1]) and a[3] == b[3]
+    z = np.zeros((8, 8, 3, 3))
+    f, idx, val, eps = run_gpu(z, [np.ones((d, 3)) for d in z.shape], 0.05, 10)
+    assert idx.size == 0 and eps == [0.0] and all(not np.any(x) for x in f)
+
+
+def test_full_size_c3_weight():
+    """The C3 layer's weight shape (512 x 512 x 3 x 3), rank 128, c = 1 %: three iterations
+    against the oracle (eps history, factors, S support)."""
+    cfg = workloads.DECOMP_CONFIGS["c3_decomp"]
+    w, f0 = workloads.generate_decomp(cfg)
+    f, idx, val, eps = run_gpu(w, f0, cfg.cardinality, 3)
+    rf, (ridx, rval), reps = D.decompose_lrs(w, f0, cfg.cardinality, max_iters=3, tol=0.0)
+    assert np.allclose(eps, reps, rtol=1e-7)
+    assert np.array_equal(idx, ridx)
+    for m in range(4):
+        assert rel(f[m], rf[m]) < 1e-6, m

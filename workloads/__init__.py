@@ -313,3 +313,45 @@ def generate_dy(cfg: LayerConfig, batch: Optional[int] = None, seed: int = 1) ->
     n = cfg.batch if batch is None else batch
     rng = np.random.Generator(np.random.PCG64(seed))
     return _store(rng.standard_normal((n, cfg.out_h, cfg.out_w, cfg.c_out)), cfg.dtype)
+
+
+# ---------------------------------------------------------------- decomposition inputs (f4)
+@dataclasses.dataclass(frozen=True)
+class DecompConfig:
+    """A weight tensor to decompose: dims (in, out, kh, kw), a planted CP
+    rank, the decomposition's rank and cardinality, and the seed."""
+    name: str
+    dims: tuple
+    planted_rank: int
+    rank: int
+    cardinality: float
+    noise: float = 0.05
+    spike: float = 10.0
+    seed: int = 0
+
+
+DECOMP_CONFIGS = {
+    # the C3 layer's weight shape (ResNet-50 layer4 3x3 512 -> 512), CP rank 128, c = 1 % (PAPER.md:244)
+    "c3_decomp": DecompConfig("c3_decomp", (512, 512, 3, 3), 96, 128, 0.01),
+    # the C2 layer's weight shape (layer3 3x3 256 -> 256), CP rank 64
+    "c2_decomp": DecompConfig("c2_decomp", (256, 256, 3, 3), 48, 64, 0.01),
+}
+
+
+def generate_decomp(cfg: DecompConfig):
+    """(W, initial factors) for a decomposition run, from PCG64(seed), draw order: the planted
+    factors (N(0,1) each, [dims[m], planted_rank]), the noise (N(0, noise^2)), the spike
+    positions (uniform without replacement, round(cardinality * numel) of them), the spike signs,
+    then the initial factors (N(0,1) [dims[m], rank]).  W = (planted CP tensor) / sqrt(planted_rank)
+    + noise + spike * sign at the spike positions: a weight with a low-rank body and a few large
+    entries -- the structure the paper's W ~ L + S targets (pretrained weights are unavailable)."""
+    rng = np.random.Generator(np.random.PCG64(cfg.seed))
+    pf = [rng.standard_normal((d, cfg.planted_rank)) for d in cfg.dims]
+    w = np.einsum("ar,br,cr,dr->abcd", *pf, optimize=True) / np.sqrt(cfg.planted_rank)
+    w += cfg.noise * rng.standard_normal(cfg.dims)
+    numel = int(np.prod(cfg.dims))
+    n = int(round(cfg.cardinality * numel))
+    pos = rng.choice(numel, size=n, replace=False)
+    w.flat[pos] += cfg.spike * np.sign(rng.standard_normal(n))
+    f0 = [rng.standard_normal((d, cfg.rank)) for d in cfg.dims]
+    return w, f0
