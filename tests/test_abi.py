@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_functions():
     src = open(os.path.join(ROOT, "include", "lrs_conv.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:lrs_status|const char \*|int32_t)\s*\**\s*(lrs_(?:conv|sparse)_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:lrs_status|const char \*|int32_t|int64_t)\s*\**\s*(lrs_(?:conv|sparse|decomp)_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_header_symbol():
@@ -174,3 +174,43 @@ def test_wide_rows_need_a_bf16_tensor_core_layer():
         h = ctypes.c_void_p()
         st = P.load_library().lrs_conv_create(ctypes.byref(d), 0, ctypes.byref(h))
         assert st == B.LRS_ERR_UNSUPPORTED, (over, st)
+
+
+def bwd_status(**over):
+    d, keep = B.make_desc(**base_desc_args(**over))
+    lib = P.load_library()
+    h = ctypes.c_void_p()
+    st = lib.lrs_conv_bwd_create(ctypes.byref(d), 0, ctypes.byref(h))
+    if st == 0:
+        lib.lrs_conv_bwd_destroy(h)
+    return st, lib.lrs_conv_last_error().decode()
+
+
+def test_backward_create_validation_before_any_device_call():
+    """The backward's documented refusals (include/lrs_conv.h "Backward pass") come before
+    any device call; a well-formed layer on this GPU-less host is LRS_ERR_CUDA."""
+    assert bwd_status(stride=2)[0] == B.LRS_ERR_UNSUPPORTED
+    assert bwd_status(dtype="f32", u_in=base_desc_args()["u_in"])[0] == B.LRS_ERR_UNSUPPORTED
+    assert bwd_status(batch_max=0)[0] == B.LRS_ERR_INVALID_ARGUMENT
+    st, msg = bwd_status()
+    assert st == B.LRS_ERR_CUDA and "no CPU fallback" in msg
+
+
+def test_decomp_create_validation_before_any_device_call():
+    lib = P.load_library()
+
+    def status(**kw):
+        a = dict(dims=(8, 8, 3, 3), rank=4, cardinality=0.01, max_iters=5, tol=1e-6, rcond=1e-10)
+        a.update(kw)
+        prm = B.lrs_decomp_params(dims=(ctypes.c_int32 * 4)(*a["dims"]), rank=a["rank"], cardinality=a["cardinality"],
+                                  max_iters=a["max_iters"], tol=a["tol"], rcond=a["rcond"])
+        h = ctypes.c_void_p()
+        return lib.lrs_decomp_create(ctypes.byref(prm), 0, ctypes.byref(h))
+
+    assert status(rank=0) == B.LRS_ERR_INVALID_ARGUMENT
+    assert status(dims=(8, 0, 3, 3)) == B.LRS_ERR_INVALID_ARGUMENT
+    assert status(cardinality=1.0) == B.LRS_ERR_INVALID_ARGUMENT
+    assert status(max_iters=0) == B.LRS_ERR_INVALID_ARGUMENT
+    assert status(rank=257) == B.LRS_ERR_UNSUPPORTED
+    assert status(dims=(8, 8, 9, 3)) == B.LRS_ERR_UNSUPPORTED
+    assert status() == B.LRS_ERR_CUDA
