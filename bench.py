@@ -71,6 +71,8 @@ def parse():
                          "weak = a full batch per rank")
     ap.add_argument("--replays", type=int, default=10, help="separately timed graph replays (median reported)")
     ap.add_argument("--no-dense", action="store_true", help="skip the cuDNN dense context row")
+    ap.add_argument("--decompose", action="store_true",
+                    help="time the GPU low-rank + sparse decomposition of the layer's weight shape (SURVEY 8f f4)")
     ap.add_argument("--backward", action="store_true",
                     help="time the layer's backward pass (dX + parameter gradients, SURVEY 8f f3) instead")
     return ap.parse_args()
@@ -492,6 +494,9 @@ def main():
     cfg = workloads.CP_CONFIGS[args.config] if is_cp else workloads.CONFIGS[args.config]
     if args.backward:
         main_bwd(args, cfg)
+        return
+    if args.decompose:
+        main_decomp(args)
         return
     if args.impl == "reference":
         run_reference(args, cfg)
@@ -1103,6 +1108,177 @@ def main_bwd(args, cfg):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+DECOMP_OF = {"c3": "c3_decomp", "c2_bf16": "c2_decomp", "c2_f32": "c2_decomp"}
+
+
+def fp64_peak():
+    """(TFLOP/s, kind): the measured DFMA peak (tools/dfma_peak.cu) if profiles/ holds it,
+    else 148 SMs x 64 DFMA/clk x 2 at the max SM clock (derived)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "measured_peaks_extra.json")) as f:
+            v = json.load(f).get("fp64_fma_tflops")
+        if v:
+            return float(v), "measured (tools/dfma_peak.cu, profiles/measured_peaks_extra.json)"
+    except (OSError, ValueError):
+        pass
+    return 148 * 64 * 2 * 1.965e9 / 1e12, "derived (148 SMs x 64 DFMA/clk x 2 x 1965 MHz)"
+
+
+def main_decomp(args):
+    """--decompose: one step = one iteration of the paper's two-step scheme (ALS sweep on
+    W - S, then S = P_c(W - L)) on the GPU (lrs_decomp_run), for the weight
+    shape of --config (c3 -> 512 x 512 x 3 x 3, CP rank 128, c = 1 %).  A run synchronises
+    once per iteration (host stopping rule), so it is timed eagerly (no CUDA graph): CUDA
+    events around one run of K iterations after a W-iteration warm-up run.  Replicas only at
+    N > 1 (one decomposition per GPU, no collective)."""
+    import torch
+    if args.impl == "reference":
+        return run_reference_decomp(args)
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    from paper_2006_06443_b200 import LrsDecomp
+    cfg = workloads.DECOMP_CONFIGS[DECOMP_OF.get(args.config, "c3_decomp")]
+    w, f0 = workloads.generate_decomp(cfg)
+    wd = torch.from_numpy(w).to(dev)
+    K, W = args.steps, args.warmup
+    never = -float("inf")
+    warm = LrsDecomp(cfg.dims, cfg.rank, cfg.cardinality, max_iters=max(1, W), tol=never, device=local)
+    fs = [torch.from_numpy(f).to(dev) for f in f0]
+    warm.run(wd, fs)
+    torch.cuda.synchronize(dev)
+    dc = LrsDecomp(cfg.dims, cfg.rank, cfg.cardinality, max_iters=K, tol=never, device=local)
+    fs = [torch.from_numpy(f).to(dev) for f in f0]
+    stream = torch.cuda.current_stream(dev)
+    sampler = ClockSampler(torch.cuda.current_device())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    with sampler:
+        e0.record(stream)
+        idx, val, eps = dc.run(wd, fs)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    value = K / (ms / 1e3)
+    # verification (untimed): the first iterations against the fp64 oracle, and determinism
+    verify = {}
+    n_chk = min(3, K)
+    chk = LrsDecomp(cfg.dims, cfg.rank, cfg.cardinality, max_iters=n_chk, tol=never, device=local)
+    fc = [torch.from_numpy(f).to(dev) for f in f0]
+    ci, cv, ce = chk.run(wd, fc)
+    verify["first_iterations_bitwise_timed_run"] = bool(ce == eps[:n_chk])
+    if not args.no_cpu:
+        from oracle import lrs_decomp as D
+        rf, (ridx, rval), reps = D.decompose_lrs(w, f0, cfg.cardinality, max_iters=n_chk, tol=never)
+        verify["oracle_eps"] = reps
+        verify["gpu_eps"] = ce
+        verify["eps_max_rel_diff"] = float(max(abs(a - b) / b for a, b in zip(ce, reps)))
+        verify["s_support_equal"] = bool(np.array_equal(ci.cpu().numpy(), ridx))
+        verify["oracle_ok"] = verify["eps_max_rel_diff"] < 1e-7 and verify["s_support_equal"]
+    # stage timing over a short run
+    st_run = LrsDecomp(cfg.dims, cfg.rank, cfg.cardinality, max_iters=min(K, 10), tol=never, device=local)
+    fsr = [torch.from_numpy(f).to(dev) for f in f0]
+    st_run.set_timing(True)
+    st_run.run(wd, fsr)
+    torch.cuda.synchronize(dev)
+    stages = st_run.stage_times()
+    iters_t = min(K, 10)
+    avg_iter = {k_: v[0] / iters_t for k_, v in stages.items()}  # ms per iteration per stage
+    # e2e: W and the initial factors in from pinned host memory, K iterations, factors + S out
+    e2e = None
+    if not args.no_e2e:
+        wh = torch.from_numpy(w).pin_memory()
+        fh = [torch.from_numpy(f).pin_memory() for f in f0]
+        oh = [torch.empty(f.shape, dtype=torch.float64).pin_memory() for f in f0]
+        e2 = LrsDecomp(cfg.dims, cfg.rank, cfg.cardinality, max_iters=K, tol=never, device=local)
+        wd2 = torch.empty_like(wd)
+        fd2 = [torch.empty_like(f) for f in fs]
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        a.record(stream)
+        wd2.copy_(wh, non_blocking=True)
+        for x, y in zip(fd2, fh):
+            x.copy_(y, non_blocking=True)
+        i2, v2, _ = e2.run(wd2, fd2)
+        for x, y in zip(oh, fd2):
+            x.copy_(y, non_blocking=True)
+        ih = i2.cpu()
+        vh = v2.cpu()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e = {"value": K / (a.elapsed_time(b) / 1e3), "unit": "iterations/s",
+               "h2d_bytes_per_step": (wh.numel() + sum(f.numel() for f in fh)) * 8 / K,
+               "d2h_bytes_per_step": (sum(f.numel() for f in oh) * 8 + ih.numel() * 8 + vh.numel() * 8) / K,
+               "api": "LrsDecomp.run (lrs_decomp_run) with pinned-host copies of W, the factors and S",
+               "note": "one job = copy in, K iterations, copy out; bytes amortised per iteration"}
+    numel = int(np.prod(cfg.dims))
+    r = cfg.rank
+    flops_mttkrp = 4 * 2 * numel * r  # per iteration: the contraction of T with the rank-r Khatri-Rao, per mode
+    flops_res = 2 * numel * r
+    peak, kind = fp64_peak()
+    t_m = avg_iter["mttkrp"] / 1e3
+    roof = {"bound": "alu", "kernel": "lrs_mttkrp01_kernel / lrs_mttkrp23_kernel (+ partial sums), 4 per iteration",
+            "achieved": flops_mttkrp / t_m / 1e12, "peak": peak, "unit": "TFLOP/s (fp64)",
+            "frac": flops_mttkrp / t_m / 1e12 / peak, "traffic": None, "peak_kind": kind,
+            "what": "ALGORITHMIC fp64 FLOPs of the four MTTKRPs of one iteration (2 numel r each: T contracted "
+                    "with the rank-r Khatri-Rao of the other factors) / their event-timed duration per iteration",
+            "stage_ms_per_iteration": {k_: round(v, 4) for k_, v in avg_iter.items()},
+            "residual_tflops": flops_res / (avg_iter["residual"] / 1e3) / 1e12}
+    cpu = None
+    if not args.no_cpu:
+        from oracle import lrs_decomp as D
+        t0 = time.perf_counter()
+        calls = 0
+        while True:
+            D.decompose_lrs(w, f0, cfg.cardinality, max_iters=1, tol=never)
+            calls += 1
+            el = time.perf_counter() - t0
+            if el >= args.cpu_seconds and calls >= 2:
+                break
+        cpu = {"value": calls / el, "unit": "iterations/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": f"{calls} oracle iterations (decompose_lrs max_iters=1) of {cfg.name} ({el:.1f} s, fp64 numpy)",
+               **host_info()}
+    if rank != 0:
+        return
+    line = {
+        "metric": "GPU low-rank + sparse decomposition iterations/s (SURVEY 8f f4)", "value": value,
+        "unit": "iterations/s", "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms / K,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (planted CP rank + N(0, 0.05^2) noise + 1% spikes of magnitude 10; N(0,1) initial factors)",
+        "config": {"workload": f"{cfg.name}: W {cfg.dims} (the {args.config} layer's weight shape), CP rank {cfg.rank}, "
+                               f"cardinality {cfg.cardinality}, planted rank {cfg.planted_rank}",
+                   "config_id": cfg.name, "parallelism": "replicas (one decomposition per GPU)",
+                   "timing": "CUDA events around one run of K iterations (host stopping rule: one sync per iteration)",
+                   "l2": "W is 2.36M fp64 (18.9 MB): L2-resident by design"},
+        "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": dc.launches_per_iteration * K, "roofline": roof,
+        "verify": verify,
+        "eps_last": eps[-1] if eps else None, "cpu_baseline": cpu, "host": host_info(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_reference_decomp(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    from oracle import lrs_decomp as D
+    cfg = workloads.DECOMP_CONFIGS[DECOMP_OF.get(args.config, "c3_decomp")]
+    w, f0 = workloads.generate_decomp(cfg)
+    never = -float("inf")
+    D.decompose_lrs(w, f0, cfg.cardinality, max_iters=max(1, args.warmup), tol=never)
+    t0 = time.perf_counter()
+    D.decompose_lrs(w, f0, cfg.cardinality, max_iters=args.steps, tol=never)
+    el = time.perf_counter() - t0
+    v = args.steps / el
+    print(json.dumps({"impl": "reference", "metric": "GPU low-rank + sparse decomposition iterations/s (SURVEY 8f f4)",
+                      "value": v, "unit": "iterations/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                      "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "dtype": "f64",
+                      "config": {"workload": cfg.name, "config_id": cfg.name},
+                      "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": cpu_threads(), "kind": "oracle",
+                                       "sample": f"{args.steps} iterations of {cfg.name}"},
+                      "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+          flush=True)
 
 
 def bwd_oracle_rate(cfg, inp, seconds, x_all, dy_all, sample=2):

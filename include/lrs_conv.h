@@ -435,6 +435,7 @@ lrs_status lrs_decomp_run(lrs_decomp *h, const double *w, double *f0, double *f1
                           int64_t *s_idx, double *s_val, int64_t *s_count, double *eps_hist,
                           int32_t *iters_done, void *stream);
 int64_t lrs_decomp_nnz(const lrs_decomp *h); /* round(c * numel) */
+int32_t lrs_decomp_launches_per_iteration(const lrs_decomp *h); /* kernel launches per iteration */
 /* stage timing: 0 MTTKRP (+ partial sums), 1 pseudo-inverse + factor update + Gram,
    2 residual W - L, 3 projection P_c + T = W - S + eps */
 lrs_status lrs_decomp_set_timing(lrs_decomp *h, int32_t enable);

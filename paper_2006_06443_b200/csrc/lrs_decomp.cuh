@@ -81,6 +81,60 @@ __global__ void __launch_bounds__(kDThreads) lrs_mttkrp01_kernel(const __grid_co
   }
 }
 
+// Register-blocked form for Q = QC in {1, 9} (1x1 and 3x3 kernels): a thread owns 4 ranks
+// (rr, rr + 64, rr + 128, rr + 192) and keeps their KR23 columns in registers, so each
+// broadcast load of T feeds 4 fp64 FMAs; one block covers every rank (R <= 256).  Same
+// partial-sum layout and the same fixed-order lane combination as lrs_mttkrp01_kernel.
+template <int QC>
+__global__ void __launch_bounds__(kDThreads) lrs_mttkrp01q_kernel(const __grid_constant__ MttkrpParams p) {
+  __shared__ double red[4][kDThreads];
+  const int i = blockIdx.x;
+  const int c = blockIdx.y;
+  const int rr = threadIdx.x & 63;
+  const int jl = threadIdx.x >> 6;
+  const int I3 = p.dims[3];
+  double kr[QC][4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = rr + 64 * k;
+#pragma unroll
+    for (int qq = 0; qq < QC; ++qq)
+      kr[qq][k] = r < p.r ? __ldg(p.f[2] + (qq / I3) * p.r + r) * __ldg(p.f[3] + (qq % I3) * p.r + r) : 0.0;
+  }
+  const int n_other = p.mode == 0 ? p.dims[1] : p.dims[0];
+  const double* fo = p.mode == 0 ? p.f[1] : p.f[0];
+  const long long s_i = p.mode == 0 ? static_cast<long long>(p.dims[1]) * QC : QC;
+  const long long s_j = p.mode == 0 ? QC : static_cast<long long>(p.dims[1]) * QC;
+  const int j_begin = c * p.chunk, j_end = min(n_other, j_begin + p.chunk);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int j = j_begin + jl; j < j_end; j += 4) {
+    const double* tp = p.t + i * s_i + j * s_j;
+    double tv[QC];
+#pragma unroll
+    for (int qq = 0; qq < QC; ++qq) tv[qq] = __ldg(tp + qq);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = rr + 64 * k;
+      double inner = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < QC; ++qq) inner = fma(tv[qq], kr[qq][k], inner);
+      if (r < p.r) acc[k] = fma(__ldg(fo + static_cast<long long>(j) * p.r + r), inner, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) red[k][threadIdx.x] = acc[k];
+  __syncthreads();
+  if (jl == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = rr + 64 * k;
+      if (r >= p.r) continue;
+      const double sum = ((red[k][rr] + red[k][64 + rr]) + red[k][128 + rr]) + red[k][192 + rr];
+      p.part[(static_cast<long long>(c) * p.dims[p.mode] + i) * p.r + r] = sum;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- MTTKRP, modes 2 and 3
 // M[k][r] (mode 2) = sum_{i0,i1} F0[i0][r] F1[i1][r] sum_t T[i0,i1,k,t] F3[t][r]; mode 3 alike
 // with (k, t) swapped.  Block (chunk of (i0, i1) pairs, r slice): per-thread registers for the
@@ -155,15 +209,20 @@ __global__ void lrs_gram_kernel(const double* f, int rows, int r, double* g) {
 // ---------------------------------------------------------------- pseudo-inverse (one CTA)
 // V = Hadamard product of the three Gram matrices of the other modes (SPD, R x R); cyclic
 // Jacobi with the parallel (round-robin) ordering: each round rotates R/2 disjoint (p, q)
-// pairs at once (rows, then columns, then the eigenvector columns); sweeps until the
-// off-diagonal mass is below 1e-30 of the total.  P = Q diag(1/lambda, lambda > rcond max) Q^T.
+// pairs at once (one pass: every 2 x 2 block of a pair of pairs maps to itself, plus the
+// eigenvector columns); sweeps until the
+// off-diagonal mass is below (1e-13)^2 of the total (at most 40; sums in a fixed order, so the
+// sweep count and the bits are deterministic).  A lives in shared memory when it fits
+// (R <= 160), the (transposed) eigenvectors in the global workspace.
+// P = Q diag(1/lambda for lambda > rcond * max |lambda|) Q^T.
 struct PinvParams {
   const double* g[4];
   int mode;
   int r;       // rank
   int rp;      // rank rounded up to even (a dummy index pads odd ranks)
+  int a_smem;  // 1: A in dynamic shared memory
   double rcond;
-  double* a;   // workspace [rp][rp]
+  double* a;   // workspace [rp][rp] (when A is not in shared memory)
   double* v;   // workspace [rp][rp]
   double* p;   // out [r][r]
   int* sweeps; // out (diagnostic)
@@ -172,13 +231,17 @@ struct PinvParams {
 constexpr int kJThreads = 512;
 
 __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_constant__ PinvParams q) {
-  __shared__ double cs[256][2];
-  __shared__ int pairs[256][2];
-  __shared__ double offn, totn;
+  extern __shared__ double jsm[];
+  __shared__ double cs[128][2];
+  __shared__ int pairs[128][2];
   __shared__ double wsum[kJThreads / 32][2];
+  __shared__ double offn, totn;
   const int n = q.rp, r = q.r;
-  double* A = q.a;
-  double* V = q.v;
+  // A: the full matrix (shared memory when it fits, else the global workspace); the
+  // eigenvectors are kept TRANSPOSED (Vt[k][i] = V[i][k]) so a rotation of columns p, q of V
+  // touches two contiguous rows of Vt (coalesced / conflict-free)
+  double* A = q.a_smem ? jsm : q.a;
+  double* Vt = q.v;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e / n, j = e % n;
     double val = 0.0;
@@ -186,16 +249,15 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
       val = 1.0;
       for (int o = 0; o < 4; ++o)
         if (o != q.mode) val *= q.g[o][i * r + j];
-    } else if (i == j) {
-      val = 0.0;  // dummy index: a zero eigenvalue, dropped by the cutoff
     }
-    A[e] = val;
-    V[e] = i == j ? 1.0 : 0.0;
+    A[e] = val;  // the dummy index of an odd rank: a zero row / column (eigenvalue 0, dropped)
+    Vt[e] = i == j ? 1.0 : 0.0;
   }
   __syncthreads();
   int sweep = 0;
-  for (; sweep < 60; ++sweep) {
-    // convergence test
+  for (; sweep < 40; ++sweep) {
+    // convergence: off-diagonal mass below (1e-13)^2 of the total (the round-off floor of an
+    // n = 256 matrix is ~ (n 1e-16)^2; fixed-order sums)
     double lo = 0.0, lt = 0.0;
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
       const double x = A[e] * A[e];
@@ -211,18 +273,17 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
       wsum[threadIdx.x >> 5][1] = lt;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {  // fixed order: the sweep count is deterministic
-      double a = 0.0, b = 0.0;
+    if (threadIdx.x == 0) {
+      double sa = 0.0, sb = 0.0;
       for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
-        a += wsum[w][0];
-        b += wsum[w][1];
+        sa += wsum[w][0];
+        sb += wsum[w][1];
       }
-      offn = a;
-      totn = b;
+      offn = sa;
+      totn = sb;
     }
     __syncthreads();
-    if (!(offn > 1e-30 * totn)) break;
-    __syncthreads();
+    if (!(offn > 1e-26 * totn)) break;
     for (int round = 0; round < n - 1; ++round) {
       // pairs of this round (circle method: 0 fixed, the rest rotated by `round`)
       for (int k = threadIdx.x; k < n / 2; k += blockDim.x) {
@@ -247,27 +308,31 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
         cs[k][1] = s;
       }
       __syncthreads();
-      // rows:  A <- P^T A
-      for (int e = threadIdx.x; e < (n / 2) * n; e += blockDim.x) {
-        const int k = e / n, j = e % n;
-        const int pp = pairs[k][0], qq = pairs[k][1];
-        const double c = cs[k][0], s = cs[k][1];
-        const double ap = A[pp * n + j], aq = A[qq * n + j];
-        A[pp * n + j] = c * ap - s * aq;
-        A[qq * n + j] = s * ap + c * aq;
+      // A <- P^T A P in ONE pass: the pairs are disjoint, so each 2 x 2 block (rows of pair a,
+      // columns of pair b) maps to itself -- a' = J_a^T a J_b; and Vt <- P^T Vt (rows p, q)
+      const int nh = n / 2;
+      for (int e = threadIdx.x; e < nh * nh; e += blockDim.x) {
+        const int ka = e / nh, kb = e % nh;
+        const double ca = cs[ka][0], sa = cs[ka][1], cb = cs[kb][0], sb = cs[kb][1];
+        if (sa == 0.0 && sb == 0.0) continue;
+        const int pa = pairs[ka][0], qa = pairs[ka][1], pb = pairs[kb][0], qb = pairs[kb][1];
+        const double x00 = A[pa * n + pb], x01 = A[pa * n + qb], x10 = A[qa * n + pb], x11 = A[qa * n + qb];
+        const double r00 = ca * x00 - sa * x10, r01 = ca * x01 - sa * x11;
+        const double r10 = sa * x00 + ca * x10, r11 = sa * x01 + ca * x11;
+        A[pa * n + pb] = cb * r00 - sb * r01;
+        A[pa * n + qb] = sb * r00 + cb * r01;
+        A[qa * n + pb] = cb * r10 - sb * r11;
+        A[qa * n + qb] = sb * r10 + cb * r11;
       }
-      __syncthreads();
-      // columns: A <- A P, V <- V P
-      for (int e = threadIdx.x; e < (n / 2) * n; e += blockDim.x) {
+      for (int e = threadIdx.x; e < nh * n; e += blockDim.x) {
         const int k = e / n, i = e % n;
+        const double s = cs[k][1];
+        if (s == 0.0) continue;
+        const double c = cs[k][0];
         const int pp = pairs[k][0], qq = pairs[k][1];
-        const double c = cs[k][0], s = cs[k][1];
-        const double ap = A[i * n + pp], aq = A[i * n + qq];
-        A[i * n + pp] = c * ap - s * aq;
-        A[i * n + qq] = s * ap + c * aq;
-        const double vp = V[i * n + pp], vq = V[i * n + qq];
-        V[i * n + pp] = c * vp - s * vq;
-        V[i * n + qq] = s * vp + c * vq;
+        const double vp = Vt[pp * n + i], vq = Vt[qq * n + i];
+        Vt[pp * n + i] = c * vp - s * vq;
+        Vt[qq * n + i] = s * vp + c * vq;
       }
       __syncthreads();
     }
@@ -281,13 +346,16 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
     if (q.sweeps) *q.sweeps = sweep;
   }
   __syncthreads();
+  __shared__ double inv[256];
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const double lam = A[k * n + k];
+    inv[k] = fabs(lam) > q.rcond * lmax ? 1.0 / lam : 0.0;
+  }
+  __syncthreads();
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
     const int i = e / r, j = e % r;
     double s = 0.0;
-    for (int k = 0; k < n; ++k) {
-      const double lam = A[k * n + k];
-      if (fabs(lam) > q.rcond * lmax) s += V[i * n + k] * V[j * n + k] / lam;
-    }
+    for (int k = 0; k < n; ++k) s += Vt[k * n + i] * Vt[k * n + j] * inv[k];
     q.p[e] = s;
   }
 }
@@ -314,6 +382,7 @@ __global__ void __launch_bounds__(kDThreads) lrs_cp_residual_kernel(const double
   double* kr = dsm + r;      // [q][r]
   const int i0 = blockIdx.x;
   for (int e = threadIdx.x; e < r; e += blockDim.x) f0r[e] = f0[static_cast<long long>(i0) * r + e];
+  __syncthreads();  // kr below reads f0r
   for (int e = threadIdx.x; e < q * r; e += blockDim.x) {
     const int qq = e / r, x = e % r;
     kr[e] = f2[(qq / i3n) * r + x] * f3[(qq % i3n) * r + x] * f0r[x];

@@ -29,6 +29,7 @@ struct lrs_decomp {
   int chunks01[2] = {1, 1}; // MTTKRP chunking per mode (0, 1)
   int chunks23 = 1;
   long long chunk23 = 1;
+  size_t pinv_smem = 0;     // dynamic shared memory of the pseudo-inverse (A resident), 0 = global
   // stage timing
   bool timing = false;
   TimingRing ring[4];       // mttkrp, pinv, residual, select
@@ -124,9 +125,10 @@ lrs_status lrs_decomp_create(const lrs_decomp_params* p, int device, lrs_decomp*
   const int r = p->rank;
   // MTTKRP chunking: ~4 blocks per SM over the output rows x chunks x r slices
   const int rs = (r + 63) / 64;
+  const int rs01 = (h->q == 9 || h->q == 1) ? 1 : rs;  // the register-blocked forms cover every rank
   for (int m = 0; m < 2; ++m) {
     const int rows = p->dims[m], other = p->dims[1 - m];
-    int nc = std::max(1, (4 * h->sms) / std::max(1, rows * rs));
+    int nc = std::max(1, (4 * h->sms) / std::max(1, rows * rs01));
     nc = std::min(nc, other);
     h->chunks01[m] = nc;
   }
@@ -168,6 +170,14 @@ lrs_status lrs_decomp_create(const lrs_decomp_params* p, int device, lrs_decomp*
   DC_ALLOC(h->eps_part, nb_fin * 8);
   DC_ALLOC(h->scal, 4 * 8);
 #undef DC_ALLOC
+  // the Jacobi matrix A in dynamic shared memory when it fits
+  const size_t a_bytes = static_cast<size_t>(h->rp) * h->rp * 8;
+  h->pinv_smem = a_bytes <= 200 * 1024 ? a_bytes : 0;
+  if (h->pinv_smem) {
+    cudaError_t e2 = cudaFuncSetAttribute(reinterpret_cast<const void*>(&lrs_sym_pinv_kernel),
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->pinv_smem));
+    if (e2 != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e2)));
+  }
   const size_t res_smem = static_cast<size_t>(r + h->q * r) * 8;
   cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&lrs_cp_residual_kernel),
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(res_smem));
@@ -243,8 +253,15 @@ lrs_status lrs_decomp_run(lrs_decomp* h, const double* w, double* f0, double* f1
         const int other = p.dims[1 - mode];
         mp.nchunk = nchunk;
         mp.chunk = (other + nchunk - 1) / nchunk;
-        lrs_mttkrp01_kernel<<<dim3(static_cast<unsigned>(p.dims[mode]), static_cast<unsigned>(nchunk), rs), kDThreads,
-                              0, s>>>(mp);
+        if (h->q == 9)
+          lrs_mttkrp01q_kernel<9><<<dim3(static_cast<unsigned>(p.dims[mode]), static_cast<unsigned>(nchunk)), kDThreads, 0,
+                                    s>>>(mp);
+        else if (h->q == 1)
+          lrs_mttkrp01q_kernel<1><<<dim3(static_cast<unsigned>(p.dims[mode]), static_cast<unsigned>(nchunk)), kDThreads, 0,
+                                    s>>>(mp);
+        else
+          lrs_mttkrp01_kernel<<<dim3(static_cast<unsigned>(p.dims[mode]), static_cast<unsigned>(nchunk), rs), kDThreads,
+                                0, s>>>(mp);
       } else {
         nchunk = h->chunks23;
         mp.nchunk = nchunk;
@@ -266,7 +283,8 @@ lrs_status lrs_decomp_run(lrs_decomp* h, const double* w, double* f0, double* f1
       pp.v = h->jv;
       pp.p = h->pinv;
       pp.sweeps = h->sweeps;
-      lrs_sym_pinv_kernel<<<1, kJThreads, 0, s>>>(pp);
+      pp.a_smem = h->pinv_smem ? 1 : 0;
+      lrs_sym_pinv_kernel<<<1, kJThreads, h->pinv_smem, s>>>(pp);
       lrs_cp_update_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, s>>>(h->m, h->pinv, p.dims[mode], r,
                                                                                      f[mode]);
       lrs_gram_kernel<<<r, 256, 0, s>>>(f[mode], p.dims[mode], r, h->gram[mode]);
@@ -329,6 +347,13 @@ lrs_status lrs_decomp_run(lrs_decomp* h, const double* w, double* f0, double* f1
 }
 
 int64_t lrs_decomp_nnz(const lrs_decomp* h) { return h ? h->nnz : -1; }
+
+int32_t lrs_decomp_launches_per_iteration(const lrs_decomp* h) {
+  // 4 modes x (MTTKRP, partial sums, pseudo-inverse, update, Gram) + residual + flags, scan x 2,
+  // finish, eps; with S: 8 radix passes x (histogram, pick) + scan x 2 + compaction
+  if (!h) return 0;
+  return 4 * 5 + 1 + 5 + (h->nnz > 0 ? 16 + 3 : 0);
+}
 
 lrs_status lrs_decomp_set_timing(lrs_decomp* h, int32_t enable) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");

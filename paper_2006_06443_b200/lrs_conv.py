@@ -34,7 +34,7 @@ EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs
             "lrs_conv_bwd_create", "lrs_conv_backward_data", "lrs_conv_backward_weights", "lrs_conv_backward",
             "lrs_conv_bwd_launches", "lrs_conv_bwd_destroy", "lrs_conv_bwd_set_timing",
             "lrs_conv_bwd_stage_times", "lrs_conv_bwd_stage_name",
-            "lrs_decomp_create", "lrs_decomp_run", "lrs_decomp_nnz", "lrs_decomp_set_timing",
+            "lrs_decomp_create", "lrs_decomp_run", "lrs_decomp_nnz", "lrs_decomp_launches_per_iteration", "lrs_decomp_set_timing",
             "lrs_decomp_stage_times", "lrs_decomp_destroy")
 
 
@@ -138,6 +138,8 @@ def load_library(path: str = LIB_PATH):
                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32), P]
     lib.lrs_decomp_nnz.argtypes = [P]
     lib.lrs_decomp_nnz.restype = ctypes.c_int64
+    lib.lrs_decomp_launches_per_iteration.argtypes = [P]
+    lib.lrs_decomp_launches_per_iteration.restype = ctypes.c_int32
     lib.lrs_decomp_set_timing.argtypes = [P, ctypes.c_int32]
     lib.lrs_decomp_stage_times.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64),
                                            ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]
@@ -613,6 +615,7 @@ class LrsDecomp:
         _check(load_library().lrs_decomp_create(ctypes.byref(prm), device, ctypes.byref(h)))
         self.handle = h.value
         self.nnz = int(load_library().lrs_decomp_nnz(self.handle))
+        self.launches_per_iteration = int(load_library().lrs_decomp_launches_per_iteration(self.handle))
 
     def run(self, w, factors, stream=None):
         torch = self.torch

@@ -1,0 +1,7 @@
+# decomposition (f4): tests + bench Jacobi off-norm criterion, register-blocked MTTKRP
+mkdir -p gpurun_out/dec7; O=gpurun_out/dec7; rm -f $O/rc.txt
+timeout 900 python -m pytest tests/test_gpu_decomp.py -q -x > $O/pytest_dec.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+for c in c3 c2_bf16; do
+  timeout 900 python bench.py --decompose --config $c --steps 30 --warmup 3 > $O/bench_dec_$c.json 2> $O/bench_dec_$c.err; echo "bench $c rc=$?" >> $O/rc.txt
+done
+cat $O/rc.txt

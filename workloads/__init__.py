@@ -347,7 +347,7 @@ def generate_decomp(cfg: DecompConfig):
     entries -- the structure the paper's W ~ L + S targets (pretrained weights are unavailable)."""
     rng = np.random.Generator(np.random.PCG64(cfg.seed))
     pf = [rng.standard_normal((d, cfg.planted_rank)) for d in cfg.dims]
-    w = np.einsum("ar,br,cr,dr->abcd", *pf, optimize=True) / np.sqrt(cfg.planted_rank)
+    w = np.ascontiguousarray(np.einsum("ar,br,cr,dr->abcd", *pf, optimize=True)) / np.sqrt(cfg.planted_rank)
     w += cfg.noise * rng.standard_normal(cfg.dims)
     numel = int(np.prod(cfg.dims))
     n = int(round(cfg.cardinality * numel))
