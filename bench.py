@@ -856,6 +856,7 @@ def main_bwd(args, cfg):
     dev = torch.device(f"cuda:{local}")
     from paper_2006_06443_b200 import LrsConvBackward
     from paper_2006_06443_b200 import roofline as RL
+    from paper_2006_06443_b200.dist import allreduce_grads
     inp = workloads.generate(cfg, batch=1)
     plan = ShardPlan(cfg, rank, world, args.scaling)
     gb, s0, s1 = plan.global_batch, plan.start, plan.end
@@ -876,9 +877,7 @@ def main_bwd(args, cfg):
 
     def step(i):
         bw.backward_into(xs[i], dys[i], dxs[i], grads, stream=stream)
-        if world > 1:
-            for t in gl:
-                dist.all_reduce(t)
+        allreduce_grads(gl)
 
     with torch.cuda.stream(stream):
         for i in range(n_sets):
@@ -955,10 +954,7 @@ def main_bwd(args, cfg):
         ok &= bool(torch.equal(dxe, dxs[i]))
     bw.backward_into(xs[last], dys[last], torch.empty_like(dxs[last]), ge)
     torch.cuda.synchronize(dev)
-    if world > 1:
-        for k_ in ge:
-            if ge[k_] is not None and ge[k_].numel():
-                dist.all_reduce(ge[k_])
+    allreduce_grads(list(ge.values()))
     verify["dx_rotation_bitwise_eager"] = ok
     verify["grads_bitwise_eager"] = all(torch.equal(ge[k_], grads[k_]) for k_ in ge if ge[k_] is not None)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -1001,9 +997,7 @@ def main_bwd(args, cfg):
             xd.copy_(xh, non_blocking=True)
             dyd.copy_(dyh, non_blocking=True)
             bw.backward_into(xd, dyd, dxd, grads, stream=stream)
-            if world > 1:
-                for t_ in gl:
-                    dist.all_reduce(t_)
+            allreduce_grads(gl)
             dxh.copy_(dxd, non_blocking=True)
             for k_, v in gh.items():
                 v.copy_(grads[k_], non_blocking=True)

@@ -50,3 +50,15 @@ def gather_shards(y_local, global_batch: int, group=None):
     out = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(out, pad, group=group)
     return torch.cat([o[: e - s] for o, (s, e) in zip(out, sizes)], dim=0)
+
+
+def allreduce_grads(tensors, group=None) -> None:
+    """The one exchange of the backward pass: data-parallel fine-tuning
+    sums each parameter gradient over the ranks' image shards (weight gradients are sums over
+    images).  In place, SUM, one all-reduce per tensor (NCCL on the GPUs, gloo in the tests)."""
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    for t in tensors:
+        if t is not None and t.numel():
+            dist.all_reduce(t, group=group)

@@ -117,3 +117,45 @@ def test_two_rank_sharded_forward_equals_single_process(tmp_path):
     got = np.load(tmp_path / "y.npy")
     assert np.array_equal(got, ref)
     assert float(np.load(tmp_path / "t.npy")[0]) == 2.0
+
+
+def _bwd_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import lrs_backward as B
+        from paper_2006_06443_b200.dist import allreduce_grads
+        cfg = workloads.CONFIGS["c2_bf16"].replace(batch=5, in_h=6, in_w=6, c_in=16, c_out=24, rank_in=8, rank_out=8)
+        inp = workloads.generate(cfg)
+        dy = workloads.generate_dy(cfg, seed=4)
+        s, e = shard_range(cfg.batch, rank, world)
+        g = B.backward_factored(inp.x[s:e], dy[s:e], inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx,
+                                inp.values, cfg.stride, cfg.pad)
+        ts = [torch.from_numpy(np.ascontiguousarray(g[k])) for k in ("d_u_in", "d_core", "d_u_out", "d_values")]
+        allreduce_grads(ts)
+        dx = gather_shards(torch.from_numpy(g["dx"]), cfg.batch)
+        if rank == 0:
+            for k, t in zip(("d_u_in", "d_core", "d_u_out", "d_values"), ts):
+                np.save(os.path.join(out_dir, f"{k}.npy"), t.numpy())
+            np.save(os.path.join(out_dir, "dx.npy"), dx.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_backward_gradients_allreduced_over_shards_equal_the_full_batch(tmp_path):
+    """The backward's exchange (bench.py --backward at N > 1): each rank back-propagates its
+    image shard, the parameter gradients are summed with allreduce_grads (gloo here, NCCL on
+    the GPUs) and equal the 1-process full-batch gradients; dX gathers bitwise."""
+    from oracle import lrs_backward as B
+    port = _free_port()
+    mp.spawn(_bwd_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    cfg = workloads.CONFIGS["c2_bf16"].replace(batch=5, in_h=6, in_w=6, c_in=16, c_out=24, rank_in=8, rank_out=8)
+    inp = workloads.generate(cfg)
+    dy = workloads.generate_dy(cfg, seed=4)
+    ref = B.backward_factored(inp.x, dy, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx, inp.values,
+                              cfg.stride, cfg.pad)
+    for k in ("d_u_in", "d_core", "d_u_out", "d_values"):
+        got = np.load(tmp_path / f"{k}.npy")
+        assert np.allclose(got, ref[k], rtol=1e-12, atol=1e-12), k
+    assert np.array_equal(np.load(tmp_path / "dx.npy"), ref["dx"])
