@@ -484,6 +484,9 @@ def main():
     args = parse()
     if args.impl != "reference":
         refuse_experiment_env()
+    if args.decompose and args.config == "c5":
+        main_decomp(args)  # the 16 ResNet-50 3x3 weights, decomposed concurrently
+        return
     if args.config == "c5":
         if args.impl == "reference":
             run_reference_c5(args)
@@ -1076,6 +1079,14 @@ def main_bwd(args, cfg):
                     "tap weight gradient the kernel computes before gathering S's support",
             "kernel_us": t_w * 1e6, "work": work,
             "stage_us": {k_: round(v * 1e3, 3) for k_, v in avg.items()}}
+    try:  # DRAM bytes per launch of the weight-gradient kernel (committed ncu capture)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(args.config + "_bwd")
+        if tr:
+            roof["traffic"] = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+            roof["traffic_detail"] = tr
+    except (OSError, ValueError, KeyError):
+        pass
     step_s = ms_per_step / 1e3
     layer_roof = {"t_tensor_us": work["flops"] / (peak * 1e12) * 1e6,
                   "t_hbm_us": work["bytes"] / (peaks["hbm_gbs"] * 1e9) * 1e6}
@@ -1134,6 +1145,8 @@ def main_decomp(args):
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     from paper_2006_06443_b200 import LrsDecomp
+    if args.config == "c5":
+        return main_decomp_network(args, dev, local, rank, world)
     cfg = workloads.DECOMP_CONFIGS[DECOMP_OF.get(args.config, "c3_decomp")]
     w, f0 = workloads.generate_decomp(cfg)
     wd = torch.from_numpy(w).to(dev)
@@ -1213,13 +1226,32 @@ def main_decomp(args):
     flops_res = 2 * numel * r
     peak, kind = fp64_peak()
     t_m = avg_iter["mttkrp"] / 1e3
-    roof = {"bound": "alu", "kernel": "lrs_mttkrp01_kernel / lrs_mttkrp23_kernel (+ partial sums), 4 per iteration",
-            "achieved": flops_mttkrp / t_m / 1e12, "peak": peak, "unit": "TFLOP/s (fp64)",
-            "frac": flops_mttkrp / t_m / 1e12 / peak, "traffic": None, "peak_kind": kind,
-            "what": "ALGORITHMIC fp64 FLOPs of the four MTTKRPs of one iteration (2 numel r each: T contracted "
-                    "with the rank-r Khatri-Rao of the other factors) / their event-timed duration per iteration",
+    t_p = avg_iter["pinv_update"] / 1e3
+    # the pseudo-inverse stage: 4 symmetric eigendecompositions (~9 r^3 flops each, the dense
+    # tridiagonal-QR count) + P = Q diag Q^T (2 r^3) + the factor update F = M P (2 I_m r^2) + Gram
+    flops_pinv = 4 * (11 * r ** 3) + sum(4 * d * r * r for d in cfg.dims)
+    mttkrp = {"kernel": "lrs_mttkrp01q_kernel / lrs_mttkrp23_kernel (+ partial sums), 4 per iteration",
+              "achieved": flops_mttkrp / t_m / 1e12, "frac": flops_mttkrp / t_m / 1e12 / peak,
+              "what": "ALGORITHMIC fp64 FLOPs of the four MTTKRPs (2 numel r each) / their time per iteration"}
+    pinv = {"kernel": "lrs_sym_pinv_kernel (one CTA) + lrs_cp_update_kernel + lrs_gram_kernel, 4 per iteration",
+            "achieved": flops_pinv / t_p / 1e12, "frac": flops_pinv / t_p / 1e12 / peak,
+            "what": "ALGORITHMIC fp64 FLOPs (4 x (9 r^3 eigendecomposition + 2 r^3 pseudo-inverse) + the factor "
+                    "updates and Grams) / the stage's time per iteration; a one-CTA kernel can reach at most "
+                    "1/148 of the chip's peak"}
+    dom = pinv if t_p >= t_m else mttkrp
+    roof = {"bound": "alu", "kernel": dom["kernel"], "achieved": dom["achieved"], "peak": peak,
+            "unit": "TFLOP/s (fp64)", "frac": dom["frac"], "traffic": None, "peak_kind": kind, "what": dom["what"],
             "stage_ms_per_iteration": {k_: round(v, 4) for k_, v in avg_iter.items()},
+            "mttkrp": mttkrp, "pseudo_inverse": pinv,
             "residual_tflops": flops_res / (avg_iter["residual"] / 1e3) / 1e12}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(cfg.name)
+        if tr and dom is pinv:
+            roof["traffic"] = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+            roof["traffic_detail"] = tr
+    except (OSError, ValueError, KeyError):
+        pass
     cpu = None
     if not args.no_cpu:
         from oracle import lrs_decomp as D
@@ -1249,6 +1281,86 @@ def main_decomp(args):
         "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": dc.launches_per_iteration * K, "roofline": roof,
         "verify": verify,
         "eps_last": eps[-1] if eps else None, "cpu_baseline": cpu, "host": host_info(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main_decomp_network(args, dev, local, rank, world):
+    """--decompose --config c5: the 16 ResNet-50 3x3 weights decomposed CONCURRENTLY (f4
+    "batched over layers"): one handle + CUDA stream + host thread per layer (calls on
+    distinct handles are independent; ctypes releases the GIL), K iterations each; device time
+    from an event before every stream starts to one after every stream ends."""
+    import threading
+    import torch
+    from paper_2006_06443_b200 import LrsDecomp
+    cfgs = workloads.resnet50_decomp_configs()
+    K, W = args.steps, args.warmup
+    never = -float("inf")
+    data = []
+    for c in cfgs:
+        w, f0 = workloads.generate_decomp(c)
+        data.append((c, torch.from_numpy(w).to(dev), f0))
+    streams = [torch.cuda.Stream(device=dev) for _ in cfgs]
+
+    def run_all(iters, out):
+        hs = [LrsDecomp(c.dims, c.rank, c.cardinality, max_iters=iters, tol=never, device=local) for c, _, _ in data]
+        fss = [[torch.from_numpy(f).to(dev) for f in f0] for _, _, f0 in data]
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        base = torch.cuda.current_stream(dev)
+        e0.record(base)
+        for s_ in streams:
+            s_.wait_event(e0)
+
+        def one(i):
+            torch.cuda.set_device(dev)
+            out[i] = hs[i].run(data[i][1], fss[i], stream=streams[i])
+
+        ths = [threading.Thread(target=one, args=(i,)) for i in range(len(data))]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        for s_ in streams:
+            base.wait_stream(s_)
+        e1.record(base)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1), fss, sum(h_.launches_per_iteration for h_ in hs)
+
+    run_all(max(1, W), [None] * len(data))
+    sampler = ClockSampler(torch.cuda.current_device())
+    res = [None] * len(data)
+    with sampler:
+        ms, fss, launches = run_all(K, res)
+    value = len(data) * K / (ms / 1e3)
+    verify = {}
+    if not args.no_cpu:  # the first iteration of every layer against the fp64 oracle
+        from oracle import lrs_decomp as D
+        chk = [None] * len(data)
+        run_all(1, chk)
+        errs, supp = [], []
+        for (c, _, f0), (ci, _, ce) in zip(data, chk):
+            w = workloads.generate_decomp(c)[0]
+            _, (ridx, _), reps = D.decompose_lrs(w, f0, c.cardinality, max_iters=1, tol=never)
+            errs.append(abs(ce[0] - reps[0]) / reps[0])
+            supp.append(bool(np.array_equal(ci.cpu().numpy(), ridx)))
+        verify = {"eps1_max_rel_diff": float(max(errs)), "s_support_equal_all": all(supp),
+                  "oracle_ok": max(errs) < 1e-7 and all(supp)}
+    if rank != 0:
+        return
+    numel = sum(int(np.prod(c.dims)) for c in cfgs)
+    line = {
+        "metric": "GPU low-rank + sparse decomposition iterations/s (SURVEY 8f f4), 16 layers concurrently",
+        "value": value, "unit": "layer-iterations/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (planted CP rank + noise + 1% spikes per layer, N(0,1) initial factors)",
+        "config": {"workload": "the 16 ResNet-50 3x3 conv weights (PAPER.md Table 2 shapes), CP rank min(Cin,Cout)/4, "
+                               "c = 1 %, one handle + stream + host thread per layer", "config_id": "c5_decomp",
+                   "layers": [{"name": c.name, "dims": c.dims, "rank": c.rank} for c in cfgs], "weights_numel": numel,
+                   "parallelism": "16 concurrent decompositions on one GPU", "timing": "CUDA events around all streams"},
+        "clocks": sampler.summary(), "e2e": None, "gpu_launches": launches * K,
+        "roofline": None, "verify": verify, "eps_last": [r_[2][-1] for r_ in res], "cpu_baseline": None,
+        "host": host_info(),
     }
     print(json.dumps(line), flush=True)
 

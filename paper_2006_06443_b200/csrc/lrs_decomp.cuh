@@ -226,6 +226,8 @@ struct PinvParams {
   double* v;   // workspace [rp][rp]
   double* p;   // out [r][r]
   int* sweeps; // out (diagnostic)
+  double* qt;  // [rp][rp] this mode's eigenvectors (transposed) from its previous call: in if warm, out always
+  int warm;    // 1: start from A = Q^T V Q (the normal matrix changes little between sweeps)
 };
 
 constexpr int kJThreads = 512;
@@ -254,6 +256,34 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
     Vt[e] = i == j ? 1.0 : 0.0;
   }
   __syncthreads();
+  if (q.warm) {
+    // warm start: A <- Q^T A Q with Q the previous eigenvectors of this mode (Vt <- Q^T), so
+    // the rotations only have to remove the change since the last sweep
+    const double* Qt = q.qt;
+    double* T = q.a;  // the global workspace (A itself is in shared memory on this path)
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {  // T = A Q
+      const int i = e / n, b = e % n;
+      double acc = 0.0;
+      for (int j = 0; j < n; ++j) acc = fma(A[i * n + j], Qt[b * n + j], acc);
+      T[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {  // A = Q^T T
+      const int a = e / n, b = e % n;
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) acc = fma(Qt[a * n + i], T[i * n + b], acc);
+      Vt[e] = acc;  // staged (A is still read above by no one; T done)
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int a = e / n, b = e % n;
+      // symmetrise (the two triangles of Q^T A Q differ in rounding)
+      A[e] = 0.5 * (Vt[e] + Vt[b * n + a]);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) Vt[e] = Qt[e];
+    __syncthreads();
+  }
   int sweep = 0;
   for (; sweep < 40; ++sweep) {
     // convergence: off-diagonal mass below (1e-13)^2 of the total (the round-off floor of an
@@ -324,15 +354,36 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
         A[qa * n + pb] = cb * r10 - sb * r11;
         A[qa * n + qb] = sb * r10 + cb * r11;
       }
-      for (int e = threadIdx.x; e < nh * n; e += blockDim.x) {
-        const int k = e / n, i = e % n;
-        const double s = cs[k][1];
-        if (s == 0.0) continue;
-        const double c = cs[k][0];
-        const int pp = pairs[k][0], qq = pairs[k][1];
-        const double vp = Vt[pp * n + i], vq = Vt[qq * n + i];
-        Vt[pp * n + i] = c * vp - s * vq;
-        Vt[qq * n + i] = s * vp + c * vq;
+      // Vt rows in global memory: all loads of a batch are issued before its stores (the
+      // compiler cannot reorder them past possibly aliasing stores), so the L2 latency is paid
+      // once per batch rather than once per element
+      for (int e0 = threadIdx.x; e0 < nh * n; e0 += 8 * blockDim.x) {
+        double vp[8], vq[8];
+        int off_p[8], off_q[8];
+        double cc[8], ss[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * blockDim.x;
+          ss[u] = 0.0;
+          if (e < nh * n) {
+            const int k = e / n, i = e % n;
+            ss[u] = cs[k][1];
+            cc[u] = cs[k][0];
+            off_p[u] = pairs[k][0] * n + i;
+            off_q[u] = pairs[k][1] * n + i;
+            if (ss[u] != 0.0) {
+              vp[u] = Vt[off_p[u]];
+              vq[u] = Vt[off_q[u]];
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (ss[u] != 0.0) {
+            Vt[off_p[u]] = cc[u] * vp[u] - ss[u] * vq[u];
+            Vt[off_q[u]] = ss[u] * vp[u] + cc[u] * vq[u];
+          }
+        }
       }
       __syncthreads();
     }
@@ -358,6 +409,8 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
     for (int k = 0; k < n; ++k) s += Vt[k * n + i] * Vt[k * n + j] * inv[k];
     q.p[e] = s;
   }
+  if (q.qt)
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) q.qt[e] = Vt[e];
 }
 
 // F[i][c] = sum_k M[i][k] P[k][c]

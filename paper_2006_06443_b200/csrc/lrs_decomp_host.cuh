@@ -19,6 +19,7 @@ struct lrs_decomp {
   double* ja = nullptr;     // Jacobi workspaces [rp][rp]
   double* jv = nullptr;
   double* pinv = nullptr;   // [R][R]
+  double* qt[4] = {nullptr, nullptr, nullptr, nullptr};  // per mode: last eigenvectors (warm start)
   int* sweeps = nullptr;
   unsigned long long* st = nullptr;  // radix-select state [4]
   unsigned int* hist = nullptr;      // [256]
@@ -77,6 +78,7 @@ lrs_status lrs_decomp_destroy(lrs_decomp* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   void* bufs[] = {h->t, h->rsd, h->part, h->m, h->gram[0], h->gram[1], h->gram[2], h->gram[3], h->ja, h->jv,
+                  h->qt[0], h->qt[1], h->qt[2], h->qt[3],
                   h->pinv, h->sweeps, h->st, h->hist, h->gt, h->eq, h->eq_pre, h->sel, h->sel_pre, h->sums_a,
                   h->sums_b, h->eps_part, h->scal};
   for (void* b : bufs)
@@ -157,6 +159,7 @@ lrs_status lrs_decomp_create(const lrs_decomp_params* p, int device, lrs_decomp*
   DC_ALLOC(h->ja, static_cast<size_t>(h->rp) * h->rp * 8);
   DC_ALLOC(h->jv, static_cast<size_t>(h->rp) * h->rp * 8);
   DC_ALLOC(h->pinv, static_cast<size_t>(r) * r * 8);
+  for (int i = 0; i < 4; ++i) DC_ALLOC(h->qt[i], static_cast<size_t>(h->rp) * h->rp * 8);
   DC_ALLOC(h->sweeps, 16);
   DC_ALLOC(h->st, 4 * 8);
   DC_ALLOC(h->hist, 256 * 4);
@@ -284,6 +287,8 @@ lrs_status lrs_decomp_run(lrs_decomp* h, const double* w, double* f0, double* f1
       pp.p = h->pinv;
       pp.sweeps = h->sweeps;
       pp.a_smem = h->pinv_smem ? 1 : 0;
+      pp.qt = h->qt[mode];
+      pp.warm = (it > 0 && h->pinv_smem) ? 1 : 0;  // from the second sweep on (needs A in shared memory)
       lrs_sym_pinv_kernel<<<1, kJThreads, h->pinv_smem, s>>>(pp);
       lrs_cp_update_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, s>>>(h->m, h->pinv, p.dims[mode], r,
                                                                                      f[mode]);

@@ -5,6 +5,7 @@ O=$1
 cp $O/pytest_gpu.log profiles/r02_pytest_gpu.log
 cp $O/smoke.log profiles/r02_smoke.log
 cp $O/launches_c3.csv profiles/r02_ncu_launches_c3.csv
+[ -e $O/launches_bwd_c3.csv ] && cp $O/launches_bwd_c3.csv profiles/r02_ncu_launches_bwd_c3.csv
 for f in $O/bench_*.json; do
   b=$(basename $f .json)
   [ "$b" = "bench_small" ] && continue

@@ -10,7 +10,11 @@ REPS = {  # config -> (report under gpurun_out/, kernel, round tag)
     "c4": ("r02v/prof_pw_c4.ncu-rep", "lrs_pw_kernel", "r02"),
     "c2_f32": ("r02v/prof_spadd_c2_f32.ncu-rep", "lrs_spadd_kernel", "r02"),
     "c1": ("r02v/prof_tiny_c1.ncu-rep", "lrs_tiny_kernel", "r02"),
+    # backward (f3): the weight-gradient kernel; decomposition (f4): the pseudo-inverse kernel
+    "c3_bwd": ("r02v/prof_wgrad_c3.ncu-rep", "lrs_wgrad_kernel", "r02"),
+    "c3_decomp": ("r02v/prof_pinv_c3.ncu-rep", "lrs_sym_pinv_kernel", "r02"),
 }
+STAGE = {"c3_bwd": "wgrad", "c3_decomp": "pinv_update"}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -25,7 +29,7 @@ def main():
         rows = list(csv.reader(txt.splitlines()))
         hdr, units, vals = rows[0], rows[1], rows[2]
         get = lambda m: float(vals[hdr.index(m)]) * UNIT.get(units[hdr.index(m)], 1)  # noqa: E731
-        out[cfg] = {"kernel": kern, "kernel_stage": "a345_expand_sparse", "dram_read_bytes": get("dram__bytes_read.sum"),
+        out[cfg] = {"kernel": kern, "kernel_stage": STAGE.get(cfg, "a345_expand_sparse"), "dram_read_bytes": get("dram__bytes_read.sum"),
                     "dram_write_bytes": get("dram__bytes_write.sum"),
                     "duration_us_cold": get("gpu__time_duration.sum"),
                     "source": f"profiles/{tag}_ncu_*_summary.txt (ncu --set full --clock-control none, 1 launch)"}

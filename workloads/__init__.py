@@ -355,3 +355,14 @@ def generate_decomp(cfg: DecompConfig):
     w.flat[pos] += cfg.spike * np.sign(rng.standard_normal(n))
     f0 = [rng.standard_normal((d, cfg.rank)) for d in cfg.dims]
     return w, f0
+
+
+def resnet50_decomp_configs(cardinality: float = 0.01):
+    """The 16 ResNet-50 3x3 weights of C5 as decomposition inputs (f4 "batched over layers"):
+    dims (Cin, Cout, 3, 3), CP rank min(Cin, Cout) / 4, a planted rank of 3/4 of it,
+    cardinality 1 %, seed 1000 + the Table-2 index."""
+    out = []
+    for idx, _, cfg in resnet50_compressed_layers():
+        r = min(cfg.c_in, cfg.c_out) // 4
+        out.append(DecompConfig(f"l{idx}", (cfg.c_in, cfg.c_out, 3, 3), (3 * r) // 4, r, cardinality, seed=1000 + idx))
+    return out
