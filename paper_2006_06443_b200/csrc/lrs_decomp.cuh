@@ -207,7 +207,9 @@ __global__ void lrs_gram_kernel(const double* f, int rows, int r, double* g) {
 }
 
 // ---------------------------------------------------------------- pseudo-inverse (one CTA)
-// V = Hadamard product of the three Gram matrices of the other modes (SPD, R x R); cyclic
+// V = Hadamard product of the three Gram matrices of the other modes (SPD, R x R).  First a
+// CERTIFIED Cholesky path (the inverse, when a norm bound proves no eigenvalue falls under the
+// cutoff -- the usual case, ~20x cheaper); else the eigen path: cyclic
 // Jacobi with the parallel (round-robin) ordering: each round rotates R/2 disjoint (p, q)
 // pairs at once (one pass: every 2 x 2 block of a pair of pairs maps to itself, plus the
 // eigenvector columns); sweeps until the
@@ -228,6 +230,7 @@ struct PinvParams {
   int* sweeps; // out (diagnostic)
   double* qt;  // [rp][rp] this mode's eigenvectors (transposed) from its previous call: in if warm, out always
   int warm;    // 1: start from A = Q^T V Q (the normal matrix changes little between sweeps)
+  int force_eigen;  // 1: skip the certified Cholesky path (LRS_DECOMP_EIGEN; tests of the eigen path)
 };
 
 constexpr int kJThreads = 512;
@@ -244,6 +247,100 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
   // touches two contiguous rows of Vt (coalesced / conflict-free)
   double* A = q.a_smem ? jsm : q.a;
   double* Vt = q.v;
+  // ---- certified Cholesky path: when every eigenvalue of V exceeds rcond * lambda_max, the
+  // pseudo-inverse IS the inverse.  V = L L^T (in place, lower triangle), X = L^-1, P = X^T X.
+  // Certificate: lambda_min >= 1 / ||P||_F and lambda_max <= ||V||_F, so
+  // 1 / ||P||_F > rcond ||V||_F proves the cutoff drops nothing; otherwise (or if the
+  // factorisation meets a non-positive pivot) the Jacobi eigensolver below decides.
+  if (!q.force_eigen) {
+    __shared__ int fail;
+    __shared__ double vn2, pn2;
+    double* L = A;
+    double* X = q.a_smem ? q.a : q.v;  // a global workspace other than A
+    if (threadIdx.x == 0) {
+      fail = 0;
+      vn2 = 0.0;
+      pn2 = 0.0;
+    }
+    double lv = 0.0;
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+      const int i = e / r, j = e % r;
+      double val = 1.0;
+      for (int o = 0; o < 4; ++o)
+        if (o != q.mode) val *= q.g[o][i * r + j];
+      L[e] = val;
+      lv += val * val;
+    }
+    for (int o = 16; o; o >>= 1) lv += __shfl_xor_sync(0xffffffffu, lv, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5][0] = lv;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += wsum[w][0];
+      vn2 = t;
+    }
+    for (int k = 0; k < r; ++k) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const double d = L[k * r + k];
+        if (!(d > 0.0)) fail = 1;
+        L[k * r + k] = sqrt(fmax(d, 0.0));
+      }
+      __syncthreads();
+      if (fail) break;
+      const double dk = L[k * r + k];
+      for (int i = k + 1 + threadIdx.x; i < r; i += blockDim.x) L[i * r + k] /= dk;
+      __syncthreads();
+      const int m = r - k - 1;  // trailing lower triangle, row-major over (i, j), k < j <= i
+      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+        const int i = k + 1 + e / m, j = k + 1 + e % m;
+        if (j <= i) L[i * r + j] -= L[i * r + k] * L[j * r + k];
+      }
+    }
+    __syncthreads();
+    if (!fail) {
+      // X = L^-1 (lower triangular), one column per thread, forward substitution
+      for (int j = threadIdx.x; j < r; j += blockDim.x) {
+        for (int i = 0; i < r; ++i) {
+          if (i < j) {
+            X[i * r + j] = 0.0;
+            continue;
+          }
+          double acc = i == j ? 1.0 : 0.0;
+          for (int k = j; k < i; ++k) acc -= L[i * r + k] * X[k * r + j];
+          X[i * r + j] = acc / L[i * r + i];
+        }
+      }
+      __syncthreads();
+      double lp = 0.0;
+      for (int e = threadIdx.x; e < r * r; e += blockDim.x) {  // P = X^T X
+        const int a = e / r, b = e % r;
+        double acc = 0.0;
+        for (int k = a > b ? a : b; k < r; ++k) acc = fma(X[k * r + a], X[k * r + b], acc);
+        q.p[e] = acc;
+        lp += acc * acc;
+      }
+      for (int o = 16; o; o >>= 1) lp += __shfl_xor_sync(0xffffffffu, lp, o);
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5][1] = lp;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += wsum[w][1];
+        pn2 = t;
+        if (!(1.0 / sqrt(t) > q.rcond * sqrt(vn2))) fail = 1;
+      }
+      __syncthreads();
+      if (!fail) {
+        // the mode's warm-start basis restarts from the identity (any orthogonal start is valid)
+        if (q.qt)
+          for (int e = threadIdx.x; e < n * n; e += blockDim.x) q.qt[e] = (e / n == e % n) ? 1.0 : 0.0;
+        if (q.sweeps && threadIdx.x == 0) *q.sweeps = -1;  // diagnostic: the Cholesky path
+        return;
+      }
+    }
+    __syncthreads();
+  }
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e / n, j = e % n;
     double val = 0.0;

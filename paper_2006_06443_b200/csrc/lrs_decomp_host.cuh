@@ -31,6 +31,7 @@ struct lrs_decomp {
   int chunks23 = 1;
   long long chunk23 = 1;
   size_t pinv_smem = 0;     // dynamic shared memory of the pseudo-inverse (A resident), 0 = global
+  bool force_eigen = false; // LRS_DECOMP_EIGEN at create: always the Jacobi eigen path
   // stage timing
   bool timing = false;
   TimingRing ring[4];       // mttkrp, pinv, residual, select
@@ -124,6 +125,7 @@ lrs_status lrs_decomp_create(const lrs_decomp_params* p, int device, lrs_decomp*
   h->q = p->dims[2] * p->dims[3];
   h->rp = (p->rank + 1) & ~1;
   h->nnz = static_cast<long long>(std::nearbyint(p->cardinality * static_cast<double>(numel)));  // half to even
+  h->force_eigen = getenv("LRS_DECOMP_EIGEN") != nullptr;
   const int r = p->rank;
   // MTTKRP chunking: ~4 blocks per SM over the output rows x chunks x r slices
   const int rs = (r + 63) / 64;
@@ -289,6 +291,7 @@ lrs_status lrs_decomp_run(lrs_decomp* h, const double* w, double* f0, double* f1
       pp.a_smem = h->pinv_smem ? 1 : 0;
       pp.qt = h->qt[mode];
       pp.warm = (it > 0 && h->pinv_smem) ? 1 : 0;  // from the second sweep on (needs A in shared memory)
+      pp.force_eigen = h->force_eigen ? 1 : 0;
       lrs_sym_pinv_kernel<<<1, kJThreads, h->pinv_smem, s>>>(pp);
       lrs_cp_update_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, s>>>(h->m, h->pinv, p.dims[mode], r,
                                                                                      f[mode]);

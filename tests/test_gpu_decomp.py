@@ -117,3 +117,19 @@ def test_full_size_c3_weight():
     assert np.array_equal(idx, ridx)
     for m in range(4):
         assert rel(f[m], rf[m]) < 1e-6, m
+
+
+def test_eigen_path_equals_cholesky_path(monkeypatch):
+    """The pseudo-inverse's two paths (include/lrs_conv.h: the certified Cholesky inverse, and
+    the Jacobi eigensolver with the rcond cutoff, forced by LRS_DECOMP_EIGEN) give the same
+    iterations up to fp64 rounding, both against the oracle."""
+    cfg = workloads.DecompConfig("t", (64, 56, 3, 3), 8, 12, 0.01, seed=5)
+    w, f0 = workloads.generate_decomp(cfg)
+    a = run_gpu(w, f0, cfg.cardinality, 6)
+    monkeypatch.setenv("LRS_DECOMP_EIGEN", "1")
+    b = run_gpu(w, f0, cfg.cardinality, 6)
+    _, (ridx, _), reps = D.decompose_lrs(w, f0, cfg.cardinality, max_iters=6, tol=0.0)
+    assert np.allclose(a[3], b[3], rtol=1e-9) and np.allclose(a[3], reps, rtol=1e-8)
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[1], ridx)
+    for x, y in zip(a[0], b[0]):
+        assert rel(x, y) < 1e-8

@@ -42,6 +42,7 @@ int main(int argc, char** argv) {
       PinvParams q{};
       for (int i = 0; i < 4; ++i) q.g[i] = dg[i];
       q.mode = 0; q.r = r; q.rp = rp; q.a_smem = vsm; q.rcond = 1e-10; q.a = a; q.v = v; q.p = p; q.sweeps = sw;
+      q.force_eigen = argc > 2 ? atoi(argv[2]) : 0;
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       cudaEventRecord(e0);
       lrs_sym_pinv_kernel<<<1, kJThreads, smem>>>(q);
