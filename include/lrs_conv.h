@@ -370,8 +370,9 @@ lrs_status lrs_conv_backward_weights(lrs_conv_bwd *h, const void *x, const void 
                                      const lrs_conv_grads *g, void *stream);
 
 /* Both at once: dX, then the parameter gradients with dT1 taken from the transposed layer's
-   forward (its intermediate) instead of recomputed -- one GEMM launch fewer than the two
-   calls above (an SVD pair: when that forward keeps T1 in device memory); dX is identical,
+   forward (its intermediate) instead of recomputed, and the recompute GEMMs (T1, T2, dT2) on
+   the handle's internal side stream concurrently with that forward (fork / join events on
+   `stream`: graph-capturable) -- one GEMM launch fewer than the two calls above (an SVD pair: when that forward keeps T1 in device memory); dX is identical,
    the gradients equal up to the fp32 summation order of dT1. */
 lrs_status lrs_conv_backward(lrs_conv_bwd *h, const void *x, const void *dy, void *dx, int32_t n,
                              const lrs_conv_grads *g, void *stream);

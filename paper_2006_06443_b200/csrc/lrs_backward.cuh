@@ -52,6 +52,11 @@ struct lrs_conv_bwd {
   int dst_of[kGMaxProblems];  // 0 d_u_out, 1 d_core, 2 d_u_in, 3 d_values
   WgradReduceSet rs{};
   int rs_blocks = 0;
+  // lrs_conv_backward: the recompute GEMMs (T1, T2, dT2) run on a side stream concurrently
+  // with the transposed layer's forward (fork / join events; graph-capturable)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool use_side = false;
   // stage timing (lrs_conv_bwd_set_timing): bwd_t1, bwd_t2, bwd_dt2, bwd_dt1, wgrad, wgrad_reduce
   bool timing = false;
   TimingRing ring[6];
@@ -254,6 +259,9 @@ lrs_status lrs_conv_bwd_destroy(lrs_conv_bwd* h) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->tr) lrs_conv_destroy(h->tr);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   for (auto& r : h->ring)
     for (auto e : r.ev) cudaEventDestroy(e);
   cudaSetDevice(prev);
@@ -628,6 +636,10 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
   }
   h->rs.block_base[np] = blocks;
   h->rs_blocks = blocks;
+  if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)
+    return cleanup_fail(fail(LRS_ERR_CUDA, "backward: side stream / event creation failed"));
   for (const void* fn : {reinterpret_cast<const void*>(&lrs_wgrad_kernel), kernel_ptr(K_STORE_BF16)}) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
@@ -662,6 +674,11 @@ lrs_status lrs_conv_backward_weights(lrs_conv_bwd* h, const void* x, const void*
 lrs_status lrs_conv_backward(lrs_conv_bwd* h, const void* x, const void* dy, void* dx, int32_t n,
                              const lrs_conv_grads* gr, void* stream_) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (n > 0 && n <= h->batch_max) {
+    DeviceGuard dg;
+    LRS_CUDA(dg.enter(h->device));
+    LRS_CUDA(cudaEventRecord(h->ev_fork, static_cast<cudaStream_t>(stream_)));  // before the transposed forward
+  }
   lrs_status st = lrs_conv_forward(h->tr, dy, dx, n, stream_);
   if (st != LRS_OK || n == 0) {
     if (st == LRS_OK) st = bwd_weights_impl(h, x, dy, n, gr, stream_);
@@ -674,7 +691,9 @@ lrs_status lrs_conv_backward(lrs_conv_bwd* h, const void* x, const void* dy, voi
   const bool have = h->svd ? !h->tr->pw_ft : true;
   h->dt1_ext = nullptr;
   if (have && lrs_conv_debug_buffer(h->tr, h->svd ? 0 : 1, &buf, &ld) == LRS_OK && ld == h->r1p) h->dt1_ext = buf;
+  h->use_side = true;
   st = bwd_weights_impl(h, x, dy, n, gr, stream_);
+  h->use_side = false;
   h->dt1_ext = nullptr;
   return st;
 }
@@ -706,8 +725,12 @@ lrs_status bwd_weights_impl(lrs_conv_bwd* h, const void* x, const void* dy, int3
   if (st != LRS_OK) return st;
   const long long pin = static_cast<long long>(n) * h->H * h->W;
   const long long P = static_cast<long long>(n) * h->ho * h->wo;
+  // the recompute GEMMs: on the side stream when lrs_conv_backward forked it (they do not
+  // read dT1, so they overlap the transposed layer's forward), else in order on `stream`
+  const cudaStream_t rstream = h->use_side ? h->side : stream;
+  if (h->use_side) LRS_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
   // an event pair around a launch of stage si when timing is on
-  auto timed = [&](int si, auto&& fn) -> lrs_status {
+  auto timed = [&](int si, auto&& fn, cudaStream_t ts) -> lrs_status {
     cudaEvent_t e1 = nullptr;
     if (h->timing) {
       TimingRing& r = h->ring[si];
@@ -717,16 +740,17 @@ lrs_status bwd_weights_impl(lrs_conv_bwd* h, const void* x, const void* dy, int3
         for (size_t i = old; i < r.ev.size(); ++i) LRS_CUDA(cudaEventCreate(&r.ev[i]));
       }
       e1 = r.ev[r.used + 1];
-      LRS_CUDA(cudaEventRecord(r.ev[r.used], stream));
+      LRS_CUDA(cudaEventRecord(r.ev[r.used], ts));
       r.used += 2;
     }
     LRS_CUDA(fn());
-    if (e1) LRS_CUDA(cudaEventRecord(e1, stream));
+    if (e1) LRS_CUDA(cudaEventRecord(e1, ts));
     return LRS_OK;
   };
   auto launch_stage = [&](Stage& s, dim3 grid) -> lrs_status {
     const int si = &s == &h->g_t1 ? 0 : (&s == &h->g_t2 ? 1 : (&s == &h->g_dt2 ? 2 : 3));
-    return timed(si, [&] { return launch_pdl(kernel_ptr(s.kid), grid, dim3(kThreads), &s.p, s.smem, stream); });
+    return timed(si, [&] { return launch_pdl(kernel_ptr(s.kid), grid, dim3(kThreads), &s.p, s.smem, rstream); },
+                 rstream);
   };
   // recompute the chain's activations and back-propagate through it
   if ((st = launch_stage(h->g_t1, dim3(static_cast<unsigned>((pin + kTileM - 1) / kTileM)))) != LRS_OK) return st;
@@ -743,12 +767,16 @@ lrs_status bwd_weights_impl(lrs_conv_bwd* h, const void* x, const void* dy, int3
     if ((st = launch_stage(h->g_dt1, dim3(static_cast<unsigned>(((n + g.nb - 1) / g.nb) * g.tiles_h)))) != LRS_OK)
       return st;
   }
+  if (h->use_side) {  // join: the weight gradients need the recompute AND the transposed forward
+    LRS_CUDA(cudaEventRecord(h->ev_join, h->side));
+    LRS_CUDA(cudaStreamWaitEvent(stream, h->ev_join, 0));
+  }
   // the grouped weight-gradient launch; split counts were sized at batch_max (a smaller n
   // keeps them: a split may then own no position step and stores zeros)
   if ((st = timed(4, [&] {
          return launch_pdl(reinterpret_cast<const void*>(&lrs_wgrad_kernel), dim3(static_cast<unsigned>(h->wg_ctas)),
                            dim3(kGThreads), &h->wp, h->wg_smem, stream);
-       })) != LRS_OK)
+       }, stream)) != LRS_OK)
     return st;
   // split sums -> gradients (problems whose output the caller skipped are not gathered)
   WgradReduceSet rs = h->rs;
@@ -767,7 +795,7 @@ lrs_status bwd_weights_impl(lrs_conv_bwd* h, const void* x, const void* dy, int3
   if (blocks > 0 && (st = timed(5, [&] {
                        return launch_pdl(reinterpret_cast<const void*>(&lrs_wgrad_reduce_kernel),
                                          dim3(static_cast<unsigned>(blocks)), dim3(kGRThreads), &rs, 0, stream);
-                     })) != LRS_OK)
+                     }, stream)) != LRS_OK)
     return st;
   return LRS_OK;
 }
