@@ -106,12 +106,23 @@ __global__ void __launch_bounds__(kDThreads) lrs_mttkrp01q_kernel(const __grid_c
   const long long s_i = p.mode == 0 ? static_cast<long long>(p.dims[1]) * QC : QC;
   const long long s_j = p.mode == 0 ? QC : static_cast<long long>(p.dims[1]) * QC;
   const int j_begin = c * p.chunk, j_end = min(n_other, j_begin + p.chunk);
+  // stage this block's rows of T (the chunk's j x QC entries) in shared memory with all
+  // threads (coalesced for mode 0; QC-element runs for mode 1): the per-j loads in the loop
+  // below are then shared-memory broadcasts instead of a dependent global-load chain
+  extern __shared__ double tsm[];
+  const int nj = j_end - j_begin;
+  for (int e = threadIdx.x; e < nj * QC; e += kDThreads) {
+    const int jj = e / QC, qq = e - jj * QC;
+    tsm[e] = __ldg(p.t + i * s_i + static_cast<long long>(j_begin + jj) * s_j + qq);
+  }
+  __syncthreads();
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
   for (int j = j_begin + jl; j < j_end; j += 4) {
-    const double* tp = p.t + i * s_i + j * s_j;
+    const double* tp = tsm + (j - j_begin) * QC;
     double tv[QC];
 #pragma unroll
-    for (int qq = 0; qq < QC; ++qq) tv[qq] = __ldg(tp + qq);
+    for (int qq = 0; qq < QC; ++qq) tv[qq] = tp[qq];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int r = rr + 64 * k;
@@ -156,20 +167,25 @@ __global__ void __launch_bounds__(kDThreads) lrs_mttkrp23_kernel(const __grid_co
   const long long npairs = static_cast<long long>(p.dims[0]) * p.dims[1];
   const long long b = static_cast<long long>(c) * p.chunk;
   const long long e_end = min(npairs, b + p.chunk);
+  // the chunk's rows of T (contiguous: pairs b .. e_end, Q entries each) staged in shared memory
+  extern __shared__ double tsm2[];
+  const long long nst = (e_end > b ? e_end - b : 0) * Q;
+  for (long long e = threadIdx.x; e < nst; e += kDThreads) tsm2[e] = __ldg(p.t + b * Q + e);
+  __syncthreads();
   if (r < p.r) {
     double fi[8];
     for (int t = 0; t < nin; ++t) fi[t] = __ldg(fin + t * p.r + r);
     for (long long pr = b + pl; pr < e_end; pr += 4) {
       const int i0 = static_cast<int>(pr / p.dims[1]), i1 = static_cast<int>(pr % p.dims[1]);
       const double g = __ldg(p.f[0] + static_cast<long long>(i0) * p.r + r) * __ldg(p.f[1] + static_cast<long long>(i1) * p.r + r);
-      const double* tp = p.t + pr * Q;
+      const double* tp = tsm2 + (pr - b) * Q;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (k < nout) {
           double s = 0.0;
           for (int t = 0; t < nin; ++t) {
             const int qq = p.mode == 2 ? k * I3 + t : t * I3 + k;
-            s = fma(__ldg(tp + qq), fi[t], s);
+            s = fma(tp[qq], fi[t], s);
           }
           acc[k] = fma(g, s, acc[k]);
         }
@@ -248,20 +264,17 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
   double* A = q.a_smem ? jsm : q.a;
   double* Vt = q.v;
   // ---- certified Cholesky path: when every eigenvalue of V exceeds rcond * lambda_max, the
-  // pseudo-inverse IS the inverse.  V = L L^T (in place, lower triangle), X = L^-1, P = X^T X.
-  // Certificate: lambda_min >= 1 / ||P||_F and lambda_max <= ||V||_F, so
-  // 1 / ||P||_F > rcond ||V||_F proves the cutoff drops nothing; otherwise (or if the
-  // factorisation meets a non-positive pivot) the Jacobi eigensolver below decides.
+  // pseudo-inverse IS the inverse.  V = L L^T (blocked, in place: lower triangle), X = L^-1
+  // (strictly lower part kept TRANSPOSED in the free upper triangle, diagonal 1 / L_ii),
+  // P = X^T X -- all in shared memory when A is.  Certificate: lambda_min >= 1 / ||P||_F and
+  // lambda_max <= ||V||_F, so 1 / ||P||_F > rcond ||V||_F proves the cutoff drops nothing;
+  // otherwise (or at a non-positive pivot) the Jacobi eigensolver below decides.
   if (!q.force_eigen) {
     __shared__ int fail;
-    __shared__ double vn2, pn2;
+    __shared__ double vn2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* L = A;
-    double* X = q.a_smem ? q.a : q.v;  // a global workspace other than A
-    if (threadIdx.x == 0) {
-      fail = 0;
-      vn2 = 0.0;
-      pn2 = 0.0;
-    }
+    if (threadIdx.x == 0) fail = 0;
     double lv = 0.0;
     for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
       const int i = e / r, j = e % r;
@@ -272,62 +285,86 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
       lv += val * val;
     }
     for (int o = 16; o; o >>= 1) lv += __shfl_xor_sync(0xffffffffu, lv, o);
-    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5][0] = lv;
+    if (lane == 0) wsum[warp][0] = lv;
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += wsum[w][0];
       vn2 = t;
     }
-    for (int k = 0; k < r; ++k) {
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const double d = L[k * r + k];
-        if (!(d > 0.0)) fail = 1;
-        L[k * r + k] = sqrt(fmax(d, 0.0));
-      }
-      __syncthreads();
-      if (fail) break;
-      const double dk = L[k * r + k];
-      for (int i = k + 1 + threadIdx.x; i < r; i += blockDim.x) L[i * r + k] /= dk;
-      __syncthreads();
-      const int m = r - k - 1;  // trailing lower triangle, row-major over (i, j), k < j <= i
-      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-        const int i = k + 1 + e / m, j = k + 1 + e % m;
-        if (j <= i) L[i * r + j] -= L[i * r + k] * L[j * r + k];
-      }
-    }
-    __syncthreads();
-    if (!fail) {
-      // X = L^-1 (lower triangular), one column per thread, forward substitution
-      for (int j = threadIdx.x; j < r; j += blockDim.x) {
-        for (int i = 0; i < r; ++i) {
-          if (i < j) {
-            X[i * r + j] = 0.0;
-            continue;
+    constexpr int NB = 32;
+    for (int kb = 0; kb < r; kb += NB) {
+      const int nb = min(NB, r - kb);
+      // (1) the diagonal block, by warp 0 (lane = row)
+      if (warp == 0) {
+        for (int k = 0; k < nb; ++k) {
+          const int kk = kb + k;
+          double d = L[kk * r + kk];
+          const bool bad = !(d > 0.0);
+          d = sqrt(fmax(d, 0.0));
+          __syncwarp();
+          if (lane == 0) {
+            L[kk * r + kk] = d;
+            if (bad) fail = 1;
           }
-          double acc = i == j ? 1.0 : 0.0;
-          for (int k = j; k < i; ++k) acc -= L[i * r + k] * X[k * r + j];
-          X[i * r + j] = acc / L[i * r + i];
+          if (lane > k && lane < nb) L[(kb + lane) * r + kk] /= d;
+          __syncwarp();
+          if (lane > k && lane < nb)
+            for (int j = k + 1; j <= lane; ++j) L[(kb + lane) * r + kb + j] -= L[(kb + lane) * r + kk] * L[(kb + j) * r + kk];
+          __syncwarp();
         }
       }
       __syncthreads();
-      double lp = 0.0;
-      for (int e = threadIdx.x; e < r * r; e += blockDim.x) {  // P = X^T X
-        const int a = e / r, b = e % r;
+      if (fail) break;
+      // (2) the panel below: rows i >= kb + nb, L[i][kb:kb+nb] <- L[i][kb:kb+nb] L_kk^-T
+      for (int i = kb + nb + threadIdx.x; i < r; i += blockDim.x) {
+        for (int k = 0; k < nb; ++k) {
+          double acc = L[i * r + kb + k];
+          for (int m = 0; m < k; ++m) acc -= L[i * r + kb + m] * L[(kb + k) * r + kb + m];
+          L[i * r + kb + k] = acc / L[(kb + k) * r + kb + k];
+        }
+      }
+      __syncthreads();
+      // (3) the trailing lower triangle: L[i][j] -= sum_m L[i][kb+m] L[j][kb+m]
+      const int t0 = kb + nb, m = r - t0;
+      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+        const int i = t0 + e / m, j = t0 + e % m;
+        if (j > i) continue;
         double acc = 0.0;
-        for (int k = a > b ? a : b; k < r; ++k) acc = fma(X[k * r + a], X[k * r + b], acc);
-        q.p[e] = acc;
-        lp += acc * acc;
+        for (int mm = 0; mm < nb; ++mm) acc = fma(L[i * r + kb + mm], L[j * r + kb + mm], acc);
+        L[i * r + j] -= acc;
+      }
+      __syncthreads();
+    }
+    if (!fail) {
+      // X = L^-1: thread j computes column j; X[i][j] (i > j) is stored at L[j][i]
+      for (int j = threadIdx.x; j < r; j += blockDim.x) {
+        const double xjj = 1.0 / L[j * r + j];
+        for (int i = j + 1; i < r; ++i) {
+          double acc = L[i * r + j] * xjj;  // k = j term
+          for (int k = j + 1; k < i; ++k) acc = fma(L[i * r + k], L[j * r + k], acc);
+          L[j * r + i] = -acc / L[i * r + i];
+        }
+      }
+      __syncthreads();
+      // P = X^T X: P[a][b] = sum_{k >= max(a, b)} X[k][a] X[k][b]
+      double lp = 0.0;
+      for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+        const int a = e / r, bb = e % r;
+        if (bb < a) continue;
+        auto xk = [&](int k, int c) { return k == c ? 1.0 / L[c * r + c] : L[c * r + k]; };  // X[k][c], k >= c
+        double acc = 0.0;
+        for (int k = bb; k < r; ++k) acc = fma(xk(k, a), xk(k, bb), acc);
+        q.p[a * r + bb] = acc;
+        q.p[bb * r + a] = acc;
+        lp += (a == bb ? 1.0 : 2.0) * acc * acc;
       }
       for (int o = 16; o; o >>= 1) lp += __shfl_xor_sync(0xffffffffu, lp, o);
-      __syncthreads();
-      if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5][1] = lp;
+      if (lane == 0) wsum[warp][1] = lp;
       __syncthreads();
       if (threadIdx.x == 0) {
         double t = 0.0;
         for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += wsum[w][1];
-        pn2 = t;
         if (!(1.0 / sqrt(t) > q.rcond * sqrt(vn2))) fail = 1;
       }
       __syncthreads();

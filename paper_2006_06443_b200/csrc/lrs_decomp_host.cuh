@@ -133,12 +133,14 @@ lrs_status lrs_decomp_create(const lrs_decomp_params* p, int device, lrs_decomp*
   for (int m = 0; m < 2; ++m) {
     const int rows = p->dims[m], other = p->dims[1 - m];
     int nc = std::max(1, (4 * h->sms) / std::max(1, rows * rs01));
+    if (rs01 == 1) nc = std::max(nc, (other * h->q * 8 + 96 * 1024 - 1) / (96 * 1024));  // staged rows <= 96 KB
     nc = std::min(nc, other);
     h->chunks01[m] = nc;
   }
   {
     const long long pairs = static_cast<long long>(p->dims[0]) * p->dims[1];
     long long nc = std::max<long long>(1, (4LL * h->sms) / rs);
+    nc = std::max<long long>(nc, (pairs * h->q * 8 + 48 * 1024 - 1) / (48 * 1024));  // staged rows <= 48 KB
     nc = std::min<long long>(nc, pairs);
     h->chunk23 = (pairs + nc - 1) / nc;
     h->chunks23 = static_cast<int>((pairs + h->chunk23 - 1) / h->chunk23);
@@ -182,6 +184,12 @@ lrs_status lrs_decomp_create(const lrs_decomp_params* p, int device, lrs_decomp*
     cudaError_t e2 = cudaFuncSetAttribute(reinterpret_cast<const void*>(&lrs_sym_pinv_kernel),
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->pinv_smem));
     if (e2 != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e2)));
+  }
+  for (const void* fn : {reinterpret_cast<const void*>(&lrs_mttkrp01q_kernel<9>),
+                         reinterpret_cast<const void*>(&lrs_mttkrp01q_kernel<1>),
+                         reinterpret_cast<const void*>(&lrs_mttkrp23_kernel)}) {
+    cudaError_t e3 = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024 + 1024);
+    if (e3 != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e3)));
   }
   const size_t res_smem = static_cast<size_t>(r + h->q * r) * 8;
   cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&lrs_cp_residual_kernel),
@@ -258,12 +266,13 @@ lrs_status lrs_decomp_run(lrs_decomp* h, const double* w, double* f0, double* f1
         const int other = p.dims[1 - mode];
         mp.nchunk = nchunk;
         mp.chunk = (other + nchunk - 1) / nchunk;
+        const size_t tsm = static_cast<size_t>(mp.chunk) * h->q * 8;  // the staged rows of T
         if (h->q == 9)
-          lrs_mttkrp01q_kernel<9><<<dim3(static_cast<unsigned>(p.dims[mode]), static_cast<unsigned>(nchunk)), kDThreads, 0,
-                                    s>>>(mp);
+          lrs_mttkrp01q_kernel<9><<<dim3(static_cast<unsigned>(p.dims[mode]), static_cast<unsigned>(nchunk)), kDThreads,
+                                    tsm, s>>>(mp);
         else if (h->q == 1)
-          lrs_mttkrp01q_kernel<1><<<dim3(static_cast<unsigned>(p.dims[mode]), static_cast<unsigned>(nchunk)), kDThreads, 0,
-                                    s>>>(mp);
+          lrs_mttkrp01q_kernel<1><<<dim3(static_cast<unsigned>(p.dims[mode]), static_cast<unsigned>(nchunk)), kDThreads,
+                                    tsm, s>>>(mp);
         else
           lrs_mttkrp01_kernel<<<dim3(static_cast<unsigned>(p.dims[mode]), static_cast<unsigned>(nchunk), rs), kDThreads,
                                 0, s>>>(mp);
@@ -271,7 +280,8 @@ lrs_status lrs_decomp_run(lrs_decomp* h, const double* w, double* f0, double* f1
         nchunk = h->chunks23;
         mp.nchunk = nchunk;
         mp.chunk = static_cast<int>(h->chunk23);
-        lrs_mttkrp23_kernel<<<dim3(static_cast<unsigned>(nchunk), 1, rs), kDThreads, 0, s>>>(mp);
+        lrs_mttkrp23_kernel<<<dim3(static_cast<unsigned>(nchunk), 1, rs), kDThreads,
+                              static_cast<size_t>(mp.chunk) * h->q * 8, s>>>(mp);
       }
       const long long cnt = static_cast<long long>(p.dims[mode]) * r;
       lrs_part_sum_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, s>>>(h->part, nchunk, cnt, h->m);
