@@ -216,3 +216,28 @@ dec12() {
   python tools/decomp_det.py c2_decomp > $O/decomp_det.log 2>&1
   cat $O/rc.txt
 }
+refresh() {
+  # final refresh after the side-stream backward and the decomposition changes: GPU suite, smoke,
+  # default bench, backward and decomposition lines, the wgrad / MTTKRP / pseudo-inverse captures
+  mkdir -p gpurun_out/r02g; O=gpurun_out/r02g; rm -f $O/rc.txt
+  timeout 1800 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/rc.txt
+  timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench default rc=$?" >> $O/rc.txt
+  for c in c3 c2_bf16 c4; do
+    timeout 900 python bench.py --backward --config $c --steps 100 --warmup 10 > $O/bench_bwd_$c.json 2> $O/bench_bwd_$c.err; echo "bench bwd $c rc=$?" >> $O/rc.txt
+  done
+  for c in c3 c2_bf16 c5; do
+    timeout 900 python bench.py --decompose --config $c --steps 30 --warmup 3 > $O/bench_dec_$c.json 2> $O/bench_dec_$c.err; echo "bench dec $c rc=$?" >> $O/rc.txt
+  done
+  timeout 120 python tools/run_bwd.py c3 3 > $O/plain_bwd.log 2>&1 && \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_bwd_c3.csv python tools/run_bwd.py c3 3 > $O/ncu_lb.log 2>&1; echo "ncu launches bwd rc=$?" >> $O/rc.txt
+  summ() { python tools/ncu_sum.py $O/prof_$1.ncu-rep > $O/sum_$1.txt 2>&1; python tools/ncu_src.py $O/prof_$1.ncu-rep 25 > $O/sass_$1.txt 2>&1; }
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:wgrad_kernel -s 1 -c 1 -o $O/prof_wgrad_c3 -f python tools/run_bwd.py c3 3 > $O/ncu_wgrad.log 2>&1; echo "ncu wgrad rc=$?" >> $O/rc.txt
+  summ wgrad_c3
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:mttkrp01q -s 4 -c 1 -o $O/prof_mttkrp_c3 -f python bench.py --decompose --config c3 --steps 2 --warmup 1 --no-cpu --no-e2e > $O/ncu_mttkrp.log 2>&1; echo "ncu mttkrp rc=$?" >> $O/rc.txt
+  summ mttkrp_c3
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:sym_pinv -s 5 -c 1 -o $O/prof_pinv_c3 -f python bench.py --decompose --config c3 --steps 2 --warmup 1 --no-cpu --no-e2e > $O/ncu_pinv.log 2>&1; echo "ncu pinv rc=$?" >> $O/rc.txt
+  summ pinv_c3
+  rm -f $O/*.ncu-rep
+  cat $O/rc.txt
+}
