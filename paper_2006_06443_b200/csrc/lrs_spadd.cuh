@@ -147,11 +147,8 @@ __global__ void __launch_bounds__(kSpThreads, 2) lrs_spadd_kernel(const __grid_c
     const int e_begin = __ldg(ptr), e_end = __ldg(ptr + 64);
     const int rb = lane <= 8 ? __ldg(ptr + warp * 8 + lane) - e_begin : 0;
     // ---- stage X[n0..n0+3, window rows/cols, c0..c0+cc) as [c][row][pitch][4 images]
-    // channel groups vary fastest across the threads: a warp reads 32 consecutive 16-byte
-    // vectors of one position (coalesced NHWC rows) instead of one vector per position
-    const int ncq = p.cc / 4;
     for (int wi = threadIdx.x; wi < (LRS_XDBG(p.dbg & 1) ? 0 : items); wi += kSpThreads) {
-      const int pos = wi / ncq, c4 = wi - pos * ncq;
+      const int c4 = wi / (p.wr * p.wc), pos = wi - c4 * (p.wr * p.wc);
       const int r = pos / p.wc, col = pos - r * p.wc;
       const int hi = ho0 * p.sh - p.ph + r, wi_ = col - p.pw, ch = c0 + 4 * c4;
       const bool inb = hi >= 0 && hi < p.h && wi_ >= 0 && wi_ < p.w && ch < p.cin;

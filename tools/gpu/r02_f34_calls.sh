@@ -241,3 +241,10 @@ refresh() {
   rm -f $O/*.ncu-rep
   cat $O/rc.txt
 }
+f32stage() {
+  # fp32 kernel: coalesced X window staging -- fp32 parity tests and the C2-fp32 bench line
+  mkdir -p gpurun_out/f32; O=gpurun_out/f32; rm -f $O/rc.txt
+  timeout 900 python -m pytest tests/test_gpu_spadd_f32.py tests/test_gpu_parity.py tests/test_gpu_bounds.py -q -x > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  timeout 600 python bench.py --config c2_f32 --steps 200 --warmup 10 > $O/bench_c2_f32.json 2> $O/bench_c2_f32.err; echo "bench rc=$?" >> $O/rc.txt
+  cat $O/rc.txt
+}
