@@ -35,7 +35,7 @@
  * the tests to cover every path -- LRS_NO_AUTOTUNE, LRS_NO_CORE, LRS_NO_TINY,
  * LRS_F32_FUSED, LRS_NO_PW, LRS_NO_SPTC, LRS_NO_EARLY, LRS_PW_{MPC,BP,FT,CPI,EPIBUF},
  * LRS_CORE_{IPT,TH,GRID,GSTREAM,T1_NOSWZ,SPLIT_RING}, LRS_TINY_CB,
- * LRS_WCONV_{TH,CB,CPW,NS,BPI,IPW,REUSE,NWB1,ERING,GATHER,PAIR,DENSE_LAST}, LRS_DECOMP_EIGEN -- each selects another plan
+ * LRS_WCONV_{TH,CB,CPW,NS,BPI,IPW,REUSE,NWB1,ERING,GATHER,PAIR,DENSE_LAST}, LRS_DECOMP_EIGEN, LRS_WGRAD_PAIR -- each selects another plan
  * that computes the same Y (up to the fp32 summation order where an engine changes).  Knobs that skip work (timing bisection) exist
  * only in -DLRS_EXPERIMENTS builds; bench.py refuses to time with any LRS_*
  * variable set.

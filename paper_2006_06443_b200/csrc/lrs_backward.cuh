@@ -36,10 +36,11 @@ struct lrs_conv_bwd {
   uint32_t sw_x = 0, sw_dy = 0;
   // grouped weight-gradient launch
   WgradParams wp{};
-  int wg_ctas = 0;
-  uint32_t wg_smem = 0;
-  void* wg_items = nullptr;  // WgradItem lists of the persistent CTAs
-  void* wg_ptr = nullptr;    // [wg_ctas + 1]
+  WgradParams wpp{};        // the CTA-pair launch (lrs_wgrad_kernel<true>)
+  int wg_ctas_l[2] = {0, 0};   // per launch: CTAs (solo) / clusters (pair)
+  uint32_t wg_smem_l[2] = {0, 0};
+  void* wg_items_l[2] = {nullptr, nullptr};  // WgradItem lists of the persistent CTAs / pairs
+  void* wg_ptr_l[2] = {nullptr, nullptr};
   double wg_max_load = 0;    // the most loaded CTA's work / the mean (LPT balance)
   // which operand of each problem is which (rebuilt per call: pointer / n dependent maps)
   struct Opnd {
@@ -255,7 +256,7 @@ lrs_status lrs_conv_bwd_destroy(lrs_conv_bwd* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->w_coret, h->t1, h->t2, h->dt2, h->dt1, h->slab, h->idx,
-                  h->wg_items, h->wg_ptr};
+                  h->wg_items_l[0], h->wg_ptr_l[0], h->wg_items_l[1], h->wg_ptr_l[1]};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->tr) lrs_conv_destroy(h->tr);
@@ -450,16 +451,23 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
   }
   if (d->nnz > 0) probs.push_back({0, cin, 1, cout, cin, cout, kk, 0, 3});  // dW_S at S's support
   const int np = static_cast<int>(probs.size());
+  // LRS_WGRAD_PAIR=1: the CTA-pair form (exact, measured SLOWER -- C3 95.7 vs 84.8 us, C2 43.7 vs
+  // 29.6 us -- so opt-in)
+  const bool pair_on = getenv("LRS_WGRAD_PAIR") != nullptr;
   h->wp.n_problems = np;
   std::vector<double> work(np);
   std::vector<int> tiles(np), ksteps_max(np), stage_count(np);
   for (int i = 0; i < np; ++i) {
     const Prob& pr = probs[i];
     WgradProblem& q = h->wp.pr[i];
-    const int bn = std::min(256, round_up(pr.n, 64));
+    // the CTA-pair form (opt-in) needs an even number of 128-row M tiles and N tiles of 128
+    // or 256 (each CTA loads half of B in 64-wide boxes): small problems are padded (the
+    // out-of-range rows / columns load as zeros and are never gathered) so that ONE balanced
+    // pair launch covers every problem
+    const int bn = pair_on ? std::min(256, round_up(pr.n, 128)) : std::min(256, round_up(pr.n, 64));  // pair: 2 x 64k
     q.bn = bn;
     q.n_tiles = (pr.n + bn - 1) / bn;
-    q.m_tiles = (pr.m + 127) / 128;
+    q.m_tiles = pair_on ? round_up((pr.m + 127) / 128, 2) : (pr.m + 127) / 128;
     q.taps = pr.taps;
     q.kw = pr.taps == 1 ? 1 : kw;
     q.pad_h = pr.taps == 1 ? 0 : d->pad_h;
@@ -487,12 +495,13 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
     work[i] = static_cast<double>(tiles[i]) * q.k_steps * q.kst * (2 + bn / 64);
   }
   // K splits and the persistent schedule: items (problem, tile, split) of about equal work,
-  // assigned longest-first to the least-loaded of the SMs' CTAs (LPT).  The granularity g
-  // (items per SM) trades balance against the split slabs the reduction reads back: the
-  // model time = the most loaded CTA's operand bytes at ~60 B/clk per SM (TMA inbound,
-  // profiles/r02_tma_bw.log) + the slab bytes written and read at ~5 TB/s
-  double total = 0;
-  for (double w : work) total += w;
+  // assigned longest-first to the least-loaded unit (LPT): one CTA per item
+  // (lrs_wgrad_kernel<false>), or with LRS_WGRAD_PAIR every problem in ONE launch of CTA PAIRS
+  // (cta_group::2: an item covers 2 M tiles, each CTA loads half of B; lrs_wgrad_kernel<true>;
+  // the problems were padded to fit above).  Per launch, the granularity g (items per unit) trades balance against the split
+  // slabs the reduction reads back: the model time = the most loaded unit's operand bytes at
+  // ~60 B/clk per SM (TMA inbound, profiles/r02_tma_bw.log) + the slab bytes written and read
+  // at ~5 TB/s.
   struct Sched {
     std::vector<int> splits;
     std::vector<std::vector<WgradItem>> lists;
@@ -500,84 +509,112 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
     size_t slab = 0;
     double t = 1e300;
   };
-  Sched best;
-  for (double g : {1.0, 1.5, 2.0, 3.0, 4.0}) {
-    Sched sc;
-    const double item_work = total / (g * h->sms);
-    std::vector<std::pair<double, WgradItem>> items;
-    for (int i = 0; i < np; ++i) {
-      const WgradProblem& q = h->wp.pr[i];
-      int splits = static_cast<int>(std::lround(work[i] / (tiles[i] * item_work)));
-      splits = std::max(1, std::min(splits, ksteps_max[i]));
-      sc.splits.push_back(splits);
-      sc.slab += static_cast<size_t>(splits) * q.taps * q.m_tiles * 128 * q.n_tiles * q.bn;
-      for (int t = 0; t < tiles[i]; ++t)
-        for (int sp = 0; sp < splits; ++sp) {
-          WgradItem it;
-          it.problem = static_cast<uint16_t>(i);
-          it.split = static_cast<uint16_t>(sp);
-          it.tile = t;
-          const long long kb = static_cast<long long>(q.k_steps) * sp / splits;
-          const long long ke = static_cast<long long>(q.k_steps) * (sp + 1) / splits;
-          items.push_back({static_cast<double>(ke - kb) * q.kst * (2 + q.bn / 64), it});
-        }
-    }
-    std::stable_sort(items.begin(), items.end(),
-                     [](const std::pair<double, WgradItem>& x, const std::pair<double, WgradItem>& y) {
-                       return x.first > y.first;
-                     });
-    const int grid = std::min<int>(h->sms, static_cast<int>(items.size()));
-    sc.lists.assign(grid, {});
-    sc.load.assign(grid, 0.0);
-    for (auto& it : items) {
-      const int c = static_cast<int>(std::min_element(sc.load.begin(), sc.load.end()) - sc.load.begin());
-      sc.load[c] += it.first;
-      sc.lists[c].push_back(it.second);
-    }
-    const double mk = *std::max_element(sc.load.begin(), sc.load.end()) * 128.0 / (60.0 * 1.965e9);
-    sc.t = mk + 2.0 * sc.slab * 4.0 / 5e12;
-    if (sc.t < best.t) best = std::move(sc);
+  std::vector<int> pairp(np);
+  for (int i = 0; i < np; ++i) {
+    const WgradProblem& q = h->wp.pr[i];
+    pairp[i] = (pair_on && q.m_tiles % 2 == 0 && q.bn >= 128) ? 1 : 0;
   }
+  std::vector<int> splits_of(np, 1);
+  auto schedule = [&](int pair, Sched& best) {
+    const int units = pair ? h->sms / 2 : h->sms;
+    double total = 0;
+    for (int i = 0; i < np; ++i)
+      if (pairp[i] == pair) total += work[i] * (pair ? (2.0 + h->wp.pr[i].bn / 128) / (2.0 + h->wp.pr[i].bn / 64) : 1.0);
+    if (total <= 0) return;
+    for (double g : {1.0, 1.5, 2.0, 3.0, 4.0}) {
+      Sched sc;
+      sc.splits.assign(np, 1);
+      const double item_work = total / (g * units);
+      std::vector<std::pair<double, WgradItem>> items;
+      for (int i = 0; i < np; ++i) {
+        if (pairp[i] != pair) continue;
+        const WgradProblem& q = h->wp.pr[i];
+        const int ut = pair ? tiles[i] / 2 : tiles[i];  // items per split
+        const double per_step = static_cast<double>(q.kst) * (2 + q.bn / (pair ? 128 : 64));  // per CTA
+        int splits = static_cast<int>(std::lround(per_step * q.k_steps * ut / (ut * item_work)));
+        splits = std::max(1, std::min(splits, ksteps_max[i]));
+        sc.splits[i] = splits;
+        sc.slab += static_cast<size_t>(splits) * q.taps * q.m_tiles * 128 * q.n_tiles * q.bn;
+        for (int t = 0; t < ut; ++t)
+          for (int sp = 0; sp < splits; ++sp) {
+            WgradItem it;
+            it.problem = static_cast<uint16_t>(i);
+            it.split = static_cast<uint16_t>(sp);
+            it.tile = t;
+            const long long kb = static_cast<long long>(q.k_steps) * sp / splits;
+            const long long ke = static_cast<long long>(q.k_steps) * (sp + 1) / splits;
+            items.push_back({static_cast<double>(ke - kb) * per_step, it});
+          }
+      }
+      std::stable_sort(items.begin(), items.end(),
+                       [](const std::pair<double, WgradItem>& x, const std::pair<double, WgradItem>& y) {
+                         return x.first > y.first;
+                       });
+      const int grid = std::min<int>(units, static_cast<int>(items.size()));
+      sc.lists.assign(grid, {});
+      sc.load.assign(grid, 0.0);
+      for (auto& it : items) {
+        const int c = static_cast<int>(std::min_element(sc.load.begin(), sc.load.end()) - sc.load.begin());
+        sc.load[c] += it.first;
+        sc.lists[c].push_back(it.second);
+      }
+      const double mk = *std::max_element(sc.load.begin(), sc.load.end()) * 128.0 / (60.0 * 1.965e9);
+      sc.t = mk + 2.0 * sc.slab * 4.0 / 5e12;
+      if (sc.t < best.t) best = std::move(sc);
+    }
+  };
+  Sched sch[2];
+  schedule(0, sch[0]);
+  schedule(1, sch[1]);
+  for (int i = 0; i < np; ++i) splits_of[i] = sch[pairp[i]].splits.empty() ? 1 : sch[pairp[i]].splits[i];
   size_t slab_off = 0;
   std::vector<size_t> slab_at(np);
-  uint32_t slot = 0;
-  int max_stages = 4;
   for (int i = 0; i < np; ++i) {
     WgradProblem& q = h->wp.pr[i];
-    q.splits = best.splits[i];
+    q.splits = splits_of[i];
     q.split_stride = static_cast<long long>(q.taps) * q.m_tiles * 128 * q.n_tiles * q.bn;
     slab_at[i] = slab_off;
     slab_off += static_cast<size_t>(q.splits) * q.split_stride;
-    slot = std::max(slot, q.stage_bytes);
-    max_stages = std::min(max_stages, stage_count[i]);
   }
-  const int grid = static_cast<int>(best.lists.size());
-  std::vector<std::vector<WgradItem>>& lists = best.lists;
-  std::vector<double>& load = best.load;
-  std::vector<WgradItem> flat;
-  std::vector<int> ptr(grid + 1, 0);
-  for (int c = 0; c < grid; ++c) {
-    for (auto& it : lists[c]) flat.push_back(it);
-    ptr[c + 1] = static_cast<int>(flat.size());
-  }
-  {
+  h->wg_max_load = 0;
+  for (int L = 0; L < 2; ++L) {
+    WgradParams& wpL = L ? h->wpp : h->wp;
+    if (L) wpL = h->wp;  // the same problems (maps refreshed per call), its own items
+    const int grid = static_cast<int>(sch[L].lists.size());
+    h->wg_ctas_l[L] = grid;
+    if (grid == 0) continue;
+    uint32_t slot = 0;
+    for (int i = 0; i < np; ++i)
+      if (pairp[i] == L) {
+        const WgradProblem& q = h->wp.pr[i];
+        slot = std::max(slot, static_cast<uint32_t>(2 + q.bn / (L ? 128 : 64)) * q.kst * 128u);
+      }
+    const int stages = std::min<int>(4, static_cast<int>((static_cast<uint32_t>(kMaxSmem) - 2048u) / slot));
+    if (stages < 2) return cleanup_fail(fail(LRS_ERR_UNSUPPORTED, "backward: weight-gradient stages do not fit"));
+    std::vector<WgradItem> flat;
+    std::vector<int> ptr(grid + 1, 0);
+    for (int c = 0; c < grid; ++c) {
+      for (auto& it : sch[L].lists[c]) flat.push_back(it);
+      ptr[c + 1] = static_cast<int>(flat.size());
+    }
     std::vector<uint8_t> b(flat.size() * sizeof(WgradItem)), pb(ptr.size() * 4);
     memcpy(b.data(), flat.data(), b.size());
     memcpy(pb.data(), ptr.data(), pb.size());
     void* p1 = nullptr;
     void* p2 = nullptr;
     if ((st = upload(&p1, b)) != LRS_OK) return cleanup_fail(st);
-    h->wg_items = p1;
+    h->wg_items_l[L] = p1;
     if ((st = upload(&p2, pb)) != LRS_OK) return cleanup_fail(st);
-    h->wg_ptr = p2;
+    h->wg_ptr_l[L] = p2;
+    wpL.items = static_cast<const WgradItem*>(p1);
+    wpL.item_ptr = static_cast<const int*>(p2);
+    wpL.slot_bytes = slot;
+    wpL.stages = stages;
+    h->wg_smem_l[L] = static_cast<uint32_t>(stages) * slot + 8u * (2u * stages + 4u) + 16u + 1024u;
+    double tot = 0;
+    for (double v : sch[L].load) tot += v;
+    h->wg_max_load = std::max(h->wg_max_load, *std::max_element(sch[L].load.begin(), sch[L].load.end()) / (tot / grid));
   }
-  h->wp.items = static_cast<const WgradItem*>(h->wg_items);
-  h->wp.item_ptr = static_cast<const int*>(h->wg_ptr);
-  h->wp.slot_bytes = slot;
-  h->wp.stages = max_stages;
-  h->wg_ctas = grid;
-  h->wg_smem = static_cast<uint32_t>(max_stages) * slot + 8u * (2u * max_stages + 4u) + 16u + 1024u;
-  h->wg_max_load = *std::max_element(load.begin(), load.end()) / (total / grid);
   h->slab_floats = slab_off;
   if ((st = bwd_alloc(reinterpret_cast<void**>(&h->slab), slab_off * 4, "weight-gradient slabs")) != LRS_OK)
     return cleanup_fail(st);
@@ -640,7 +677,8 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)
     return cleanup_fail(fail(LRS_ERR_CUDA, "backward: side stream / event creation failed"));
-  for (const void* fn : {reinterpret_cast<const void*>(&lrs_wgrad_kernel), kernel_ptr(K_STORE_BF16)}) {
+  for (const void* fn : {reinterpret_cast<const void*>(&lrs_wgrad_kernel<false>),
+                         reinterpret_cast<const void*>(&lrs_wgrad_kernel<true>), kernel_ptr(K_STORE_BF16)}) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     if (e != cudaSuccess) return cleanup_fail(fail(LRS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)));
   }
@@ -651,9 +689,9 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
               "splits %d k_steps %d\n", i, probs[i].dst, q.taps, q.m_tiles, q.n_tiles, q.bn, q.kst, q.bh,
               q.bi, q.splits, q.k_steps);
     }
-    fprintf(stderr, "lrs bwd: %d persistent weight-gradient CTAs (max load %.3f x mean), %d stages x %u B, "
-            "slabs %.1f MB, reduce %d blocks\n", h->wg_ctas, h->wg_max_load, h->wp.stages, h->wp.slot_bytes,
-            h->slab_floats * 4.0 / 1e6, h->rs_blocks);
+    fprintf(stderr, "lrs bwd: weight gradients: %d solo CTAs (%d stages x %u B) + %d CTA pairs (%d stages x %u B), "
+            "max load %.3f x mean, slabs %.1f MB, reduce %d blocks\n", h->wg_ctas_l[0], h->wp.stages, h->wp.slot_bytes,
+            h->wg_ctas_l[1], h->wpp.stages, h->wpp.slot_bytes, h->wg_max_load, h->slab_floats * 4.0 / 1e6, h->rs_blocks);
   }
   *out = h;
   return LRS_OK;
@@ -774,8 +812,17 @@ lrs_status bwd_weights_impl(lrs_conv_bwd* h, const void* x, const void* dy, int3
   // the grouped weight-gradient launch; split counts were sized at batch_max (a smaller n
   // keeps them: a split may then own no position step and stores zeros)
   if ((st = timed(4, [&] {
-         return launch_pdl(reinterpret_cast<const void*>(&lrs_wgrad_kernel), dim3(static_cast<unsigned>(h->wg_ctas)),
-                           dim3(kGThreads), &h->wp, h->wg_smem, stream);
+         cudaError_t e = cudaSuccess;
+         if (h->wg_ctas_l[0] > 0)
+           e = launch_pdl(reinterpret_cast<const void*>(&lrs_wgrad_kernel<false>),
+                          dim3(static_cast<unsigned>(h->wg_ctas_l[0])), dim3(kGThreads), &h->wp, h->wg_smem_l[0], stream);
+         if (e == cudaSuccess && h->wg_ctas_l[1] > 0) {
+           for (int i = 0; i < h->wp.n_problems; ++i) h->wpp.pr[i] = h->wp.pr[i];  // this call's maps
+           e = launch_pdl_pair(reinterpret_cast<const void*>(&lrs_wgrad_kernel<true>),
+                               dim3(static_cast<unsigned>(2 * h->wg_ctas_l[1])), dim3(kGThreads), &h->wpp,
+                               h->wg_smem_l[1], stream);
+         }
+         return e;
        }, stream)) != LRS_OK)
     return st;
   // split sums -> gradients (problems whose output the caller skipped are not gathered)
@@ -857,7 +904,8 @@ const char* lrs_conv_bwd_stage_name(const lrs_conv_bwd* h, int32_t stage) {
 int32_t lrs_conv_bwd_launches(const lrs_conv_bwd* h, int32_t* data_launches, int32_t* combined_launches) {
   if (!h) return 0;
   const int32_t d = lrs_conv_launches_per_forward(h->tr);
-  const int32_t w = (h->svd ? 2 : 4) + 2;
+  // recompute GEMMs + the weight-gradient launch(es) (solo, CTA pairs) + the reduction
+  const int32_t w = (h->svd ? 2 : 4) + (h->wg_ctas_l[0] > 0 ? 1 : 0) + (h->wg_ctas_l[1] > 0 ? 1 : 0) + 1;
   const bool reuse = h->svd ? (!h->tr->pw_ft && h->tr->r1p == h->r1p) : (h->tr->r2p == h->r1p);
   if (data_launches) *data_launches = d;
   if (combined_launches) *combined_launches = d + w - (reuse ? 1 : 0);

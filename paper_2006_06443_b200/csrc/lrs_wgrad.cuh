@@ -105,6 +105,14 @@ __device__ __forceinline__ WgradItemGeom wgrad_item(const WgradParams& P, const 
   return g;
 }
 
+// PAIR = true: launched as clusters of 2 CTAs (cta_group::2).  A work item then covers TWO
+// M tiles (256 rows): CTA rank r loads its own 128 rows of A and HALF of B's N columns
+// (n0 + r * bn/2; tcgen05's pair form splits B along N), so per SM a stage moves (2 + bn/128)
+// boxes instead of (2 + bn/64) for the same MACs; the leader (rank 0) issues the M = 256
+// MMAs over both CTAs' shared memory, its full barriers count the peer's relayed arrival, its
+// multicast commits release both rings and both accumulators; each CTA drains its own 128
+// accumulator rows.  (Item tile index: ((tap * m_pairs + pair) * n_tiles + nt).)
+template <bool PAIR>
 __global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_constant__ WgradParams P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -112,7 +120,10 @@ __global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_co
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int S = P.stages;
-  const int i_begin = P.item_ptr[blockIdx.x], i_end = P.item_ptr[blockIdx.x + 1];
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const bool lead = rank == 0;
+  const int gid = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int i_begin = P.item_ptr[gid], i_end = P.item_ptr[gid + 1];
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * P.slot_bytes);
   uint64_t* full = bars;
@@ -122,13 +133,14 @@ __global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_co
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
 
   if (threadIdx.x == 0) {
+    const uint32_t nf = (PAIR && lead) ? 2u : 1u;  // + the peer relay's arrival
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], nf);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tmem_full[b], 1);
-      mbar_init(&tmem_empty[b], 4);  // one arrival per epilogue warp
+      mbar_init(&tmem_empty[b], 4 * nf);  // one arrival per epilogue warp (of both CTAs)
     }
     fence_mbar_init();
     for (int i = 0; i < P.n_problems; ++i) {
@@ -136,25 +148,46 @@ __global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_co
       tma_prefetch_desc(&P.pr[i].tmB);
     }
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc2(tmem_slot, 512);
+    else tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // the peer's barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // the recompute kernels before us wrote T1 / T2 / dT2 / dT1
   pdl_launch_dependents();
+
+  auto geom = [&](const WgradItem& it) {
+    WgradItemGeom g = wgrad_item(P, it);
+    if (PAIR) {  // mt counted the M-tile PAIR: this CTA's tile is 2 mt + rank
+      const WgradProblem& p = P.pr[g.pi];
+      int tile = it.tile;
+      g.nt = tile % p.n_tiles;
+      tile /= p.n_tiles;
+      const int m_pairs = p.m_tiles >> 1;
+      g.mt = 2 * (tile % m_pairs) + static_cast<int>(rank);
+      g.tap = tile / m_pairs;
+      g.ty = g.tap / p.kw;
+      g.tx = g.tap - g.ty * p.kw;
+    }
+    return g;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
       int q = 0;  // ring position over all of this CTA's position steps
       for (int ii = i_begin; ii < i_end; ++ii) {
-        const WgradItemGeom g = wgrad_item(P, P.items[ii]);
+        const WgradItemGeom g = geom(P.items[ii]);
         const WgradProblem& p = P.pr[g.pi];
         const uint32_t atom = static_cast<uint32_t>(p.kst) * 128u;
-        const int nb_atoms = p.bn >> 6;
+        const int nb_atoms = PAIR ? (p.bn >> 7) : (p.bn >> 6);  // B boxes this CTA loads
         const uint32_t tx_bytes = static_cast<uint32_t>(2 + nb_atoms) * atom;
-        const int m0 = g.mt * 128, n0 = g.nt * p.bn;
+        const int m0 = g.mt * 128;
+        const int n0 = g.nt * p.bn + (PAIR ? static_cast<int>(rank) * (p.bn >> 1) : 0);
         for (int it = g.k_begin; it < g.k_end; ++it, ++q) {
           const int s = q % S;
           if (q >= S) mbar_wait(&empty[s], ((q / S) - 1) & 1);
@@ -172,34 +205,57 @@ __global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_co
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      int q = 0;
-      for (int ii = i_begin; ii < i_end; ++ii) {
-        const int li = ii - i_begin;
-        const int buf = li & 1;
-        const WgradItemGeom g = wgrad_item(P, P.items[ii]);
-        const WgradProblem& p = P.pr[g.pi];
-        const uint32_t atom = static_cast<uint32_t>(p.kst) * 128u;
-        // kind::f16, bf16 A/B, fp32 D, M = 128, N = bn, A and B MN-major (bits 15, 16)
-        const uint32_t idesc = umma_idesc(1u, static_cast<uint32_t>(p.bn), 128u) | (1u << 15) | (1u << 16);
-        const int ksub = p.kst >> 4;
-        const uint32_t acc_t = tmem + static_cast<uint32_t>(buf * 256);
-        if (li >= 2) mbar_wait(&tmem_empty[buf], ((li >> 1) - 1) & 1);  // the epilogue drained it
-        tc_fence_after();
-        for (int it = g.k_begin; it < g.k_end; ++it, ++q) {
-          const int s = q % S;
-          mbar_wait(&full[s], (q / S) & 1);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + s * P.slot_bytes);
-          const uint32_t b_addr = a_addr + 2u * atom;
-          for (int kk = 0; kk < ksub; ++kk) {
-            const uint64_t ad = umma_desc_mn128(a_addr + kk * 2048u, atom, 1024u);
-            const uint64_t bd = umma_desc_mn128(b_addr + kk * 2048u, atom, 1024u);
-            mma_bf16(acc_t, ad, bd, idesc, (it > g.k_begin || kk > 0) ? 1u : 0u);
+      if (PAIR && !lead) {
+        // ---------------------------------------------------------- pair relay (rank 1)
+        // every stage this CTA's producer lands is forwarded to the leader's full barrier
+        int q = 0;
+        for (int ii = i_begin; ii < i_end; ++ii) {
+          const WgradItemGeom g = geom(P.items[ii]);
+          for (int it = g.k_begin; it < g.k_end; ++it, ++q) {
+            const int s = q % S;
+            mbar_wait(&full[s], (q / S) & 1);
+            mbar_arrive_remote(&full[s], 0);
           }
-          mma_commit(&empty[s]);
         }
-        mma_commit(&tmem_full[buf]);  // (an item without steps: arrives at once; stores zeros)
+      } else {
+        // ---------------------------------------------------------- MMA issuer
+        int q = 0;
+        for (int ii = i_begin; ii < i_end; ++ii) {
+          const int li = ii - i_begin;
+          const int buf = li & 1;
+          const WgradItemGeom g = geom(P.items[ii]);
+          const WgradProblem& p = P.pr[g.pi];
+          const uint32_t atom = static_cast<uint32_t>(p.kst) * 128u;
+          // kind::f16, bf16 A/B, fp32 D, M = 128 (256 for the pair), N = bn, A and B MN-major
+          const uint32_t idesc =
+              umma_idesc(1u, static_cast<uint32_t>(p.bn), PAIR ? 256u : 128u) | (1u << 15) | (1u << 16);
+          const int ksub = p.kst >> 4;
+          const uint32_t acc_t = tmem + static_cast<uint32_t>(buf * 256);
+          if (li >= 2) {  // the epilogue(s) drained this accumulator
+            if (PAIR) mbar_wait_cluster(&tmem_empty[buf], ((li >> 1) - 1) & 1);
+            else mbar_wait(&tmem_empty[buf], ((li >> 1) - 1) & 1);
+          }
+          tc_fence_after();
+          for (int it = g.k_begin; it < g.k_end; ++it, ++q) {
+            const int s = q % S;
+            if (PAIR) mbar_wait_cluster(&full[s], (q / S) & 1);
+            else mbar_wait(&full[s], (q / S) & 1);
+            tc_fence_after();
+            const uint32_t a_addr = smem_u32(smem + s * P.slot_bytes);
+            const uint32_t b_addr = a_addr + 2u * atom;
+            for (int kk = 0; kk < ksub; ++kk) {
+              const uint64_t ad = umma_desc_mn128(a_addr + kk * 2048u, atom, 1024u);
+              const uint64_t bd = umma_desc_mn128(b_addr + kk * 2048u, atom, 1024u);
+              const uint32_t accf = (it > g.k_begin || kk > 0) ? 1u : 0u;
+              if (PAIR) mma_bf16_2(acc_t, ad, bd, idesc, accf);
+              else mma_bf16(acc_t, ad, bd, idesc, accf);
+            }
+            if (PAIR) mma_commit_pair(&empty[s]);
+            else mma_commit(&empty[s]);
+          }
+          if (PAIR) mma_commit_pair(&tmem_full[buf]);  // (an item without steps: arrives at once)
+          else mma_commit(&tmem_full[buf]);
+        }
       }
     }
   } else {
@@ -209,7 +265,7 @@ __global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_co
     for (int ii = i_begin; ii < i_end; ++ii) {
       const int li = ii - i_begin;
       const int buf = li & 1;
-      const WgradItemGeom g = wgrad_item(P, P.items[ii]);
+      const WgradItemGeom g = geom(P.items[ii]);
       const WgradProblem& p = P.pr[g.pi];
       const bool any = g.k_end > g.k_begin;
       mbar_wait(&tmem_full[buf], (li >> 1) & 1);
@@ -232,12 +288,21 @@ __global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_co
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+      if (lane == 0) {
+        if (PAIR && !lead) mbar_arrive_remote(&tmem_empty[buf], 0);
+        else mbar_arrive(&tmem_empty[buf]);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (PAIR) cluster_sync();  // neither CTA frees TMEM / leaves while the pair still works
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    if (PAIR) tmem_dealloc2(tmem, 512);
+    else tmem_dealloc(tmem, 512);
+  }
 }
 
 // dst[i] = sum_{s < splits} slab[s * split_stride + idx[i]] (fixed order: deterministic);

@@ -185,3 +185,24 @@ def test_backward_n0_and_errors():
         binp = workloads.generate(bad.replace(batch=1))
         with pytest.raises(LrsError, match="UNSUPPORTED"):
             LrsConvBackward.from_inputs(binp, batch_max=1)
+
+
+@pytest.mark.parametrize("name", ["c3_b20", "c4_b5", "small_3x3"])
+def test_pair_and_solo_weight_gradient_forms_agree(name, monkeypatch):
+    """The weight-gradient kernel's one-CTA form (default) and its CTA-pair form
+    (LRS_WGRAD_PAIR=1: cta_group::2, M = 256 items, B split across the pair, small problems
+    padded) compute the same sums (up to the fp32 order of the K splits), both at the oracle's
+    bar."""
+    cfg = CASES[name]
+    inp = workloads.generate(cfg)
+    dy_np = workloads.generate_dy(cfg, seed=16)
+    _, _, _, _, g_solo = run_gpu(inp, dy_np)
+    monkeypatch.setenv("LRS_WGRAD_PAIR", "1")
+    _, _, _, _, g_pair = run_gpu(inp, dy_np)
+    ref = B.backward_factored(inp.x, dy_np, inp.u_in, inp.core, inp.u_out, inp.row_ptr, inp.col_idx,
+                              inp.values, cfg.stride, cfg.pad)
+    check_grads(g_pair, ref, cfg.svd)
+    check_grads(g_solo, ref, cfg.svd)
+    for k in g_pair:
+        if g_pair[k] is not None and g_pair[k].numel():
+            assert rel(g_pair[k].cpu().double().numpy(), g_solo[k].cpu().double().numpy()) < 1e-5, k

@@ -248,3 +248,24 @@ f32stage() {
   timeout 600 python bench.py --config c2_f32 --steps 200 --warmup 10 > $O/bench_c2_f32.json 2> $O/bench_c2_f32.err; echo "bench rc=$?" >> $O/rc.txt
   cat $O/rc.txt
 }
+wpair() {
+  # backward: the weight-gradient kernel's CTA-pair form -- backward tests, bench C3/C2/C4 (pair and LRS_WGRAD_NO_PAIR in a tool)
+  mkdir -p gpurun_out/wpair; O=gpurun_out/wpair; rm -f $O/rc.txt
+  LRS_VERBOSE=1 timeout 300 python tools/run_bwd.py c3 3 > $O/plain.log 2>&1; echo "plain rc=$?" >> $O/rc.txt
+  timeout 1200 python -m pytest tests/test_gpu_backward.py -q -x > $O/pytest_bwd.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  for c in c3 c2_bf16 c4; do
+    timeout 900 python bench.py --backward --config $c --steps 50 --warmup 5 --no-cpu > $O/bench_bwd_$c.json 2> $O/bench_bwd_$c.err; echo "bench $c rc=$?" >> $O/rc.txt
+  done
+  cat $O/rc.txt
+}
+
+wpair2() {
+  # backward: ONE padded CTA-pair weight-gradient launch -- backward tests, bench C3/C2/C4 (pair and LRS_WGRAD_NO_PAIR in a tool)
+  mkdir -p gpurun_out/wpair2; O=gpurun_out/wpair2; rm -f $O/rc.txt
+  LRS_VERBOSE=1 timeout 300 python tools/run_bwd.py c3 3 > $O/plain.log 2>&1; echo "plain rc=$?" >> $O/rc.txt
+  timeout 1200 python -m pytest tests/test_gpu_backward.py -q -x > $O/pytest_bwd.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  for c in c3 c2_bf16 c4; do
+    timeout 900 python bench.py --backward --config $c --steps 50 --warmup 5 --no-cpu > $O/bench_bwd_$c.json 2> $O/bench_bwd_$c.err; echo "bench $c rc=$?" >> $O/rc.txt
+  done
+  cat $O/rc.txt
+}
