@@ -269,3 +269,14 @@ wpair2() {
   done
   cat $O/rc.txt
 }
+
+wsolo() {
+  # backward: the default one-CTA weight-gradient form after the pair refactor -- backward tests, bench C3/C2/C4 (pair and LRS_WGRAD_NO_PAIR in a tool)
+  mkdir -p gpurun_out/wsolo; O=gpurun_out/wsolo; rm -f $O/rc.txt
+  LRS_VERBOSE=1 timeout 300 python tools/run_bwd.py c3 3 > $O/plain.log 2>&1; echo "plain rc=$?" >> $O/rc.txt
+  timeout 1200 python -m pytest tests/test_gpu_backward.py -q -x > $O/pytest_bwd.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  for c in c3 c2_bf16 c4; do
+    timeout 900 python bench.py --backward --config $c --steps 50 --warmup 5 --no-cpu > $O/bench_bwd_$c.json 2> $O/bench_bwd_$c.err; echo "bench $c rc=$?" >> $O/rc.txt
+  done
+  cat $O/rc.txt
+}
