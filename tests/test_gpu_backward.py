@@ -28,6 +28,9 @@ CASES = {
     "c4_b5": workloads.CONFIGS["c4"].replace(batch=5),
     "no_s": CFG("no_s", 4, 14, 14, 128, 128, 3, 1, 1, 32, 32, 0.0, "bf16"),
     "k5": CFG("k5", 2, 12, 12, 64, 64, 5, 1, 2, 32, 32, 0.02, "bf16"),
+    # channel counts and ranks off the 64 / 16 grids (padded boxes, odd R2 pitch), 7x7 kernel
+    "odd": CFG("odd", 3, 10, 11, 32, 96, 3, 1, 1, 24, 40, 0.03, "bf16"),
+    "k7": CFG("k7", 2, 9, 9, 64, 128, 7, 1, 3, 16, 48, 0.02, "bf16"),
 }
 
 

@@ -280,3 +280,9 @@ wsolo() {
   done
   cat $O/rc.txt
 }
+bwdedge() {
+  # backward: off-grid channel counts / ranks and a 7x7 kernel
+  mkdir -p gpurun_out/bwdedge; O=gpurun_out/bwdedge; rm -f $O/rc.txt
+  timeout 900 python -m pytest tests/test_gpu_backward.py -q -k "odd or k7" > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  cat $O/rc.txt
+}
