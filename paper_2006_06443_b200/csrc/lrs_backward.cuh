@@ -464,7 +464,8 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
     // or 256 (each CTA loads half of B in 64-wide boxes): small problems are padded (the
     // out-of-range rows / columns load as zeros and are never gathered) so that ONE balanced
     // pair launch covers every problem
-    const int bn = pair_on ? std::min(256, round_up(pr.n, 128)) : std::min(256, round_up(pr.n, 64));  // pair: 2 x 64k
+    const int bn_cap = getenv("LRS_WGRAD_BN") ? std::max(64, atoi(getenv("LRS_WGRAD_BN")) / 64 * 64) : 256;  // plan override
+    const int bn = pair_on ? std::min(256, round_up(pr.n, 128)) : std::min(bn_cap, round_up(pr.n, 64));  // pair: 2 x 64k
     q.bn = bn;
     q.n_tiles = (pr.n + bn - 1) / bn;
     q.m_tiles = pair_on ? round_up((pr.m + 127) / 128, 2) : (pr.m + 127) / 128;

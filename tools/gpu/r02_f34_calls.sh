@@ -286,3 +286,12 @@ bwdedge() {
   timeout 900 python -m pytest tests/test_gpu_backward.py -q -k "odd or k7" > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
   cat $O/rc.txt
 }
+wbn() {
+  # backward: weight-gradient N-tile cap (LRS_WGRAD_BN) vs the default
+  mkdir -p gpurun_out/wbn; O=gpurun_out/wbn
+  for c in c3 c2_bf16 c4; do
+    python tools/bwd_time.py $c >> $O/log.txt 2>&1
+    LRS_WGRAD_BN=128 python tools/bwd_time.py $c >> $O/log.txt 2>&1
+    LRS_WGRAD_BN=192 python tools/bwd_time.py $c >> $O/log.txt 2>&1
+  done
+}
