@@ -326,7 +326,7 @@ lrs_status lrs_conv_debug_trace(lrs_conv *h, void *dev_buf);
  * Engines:
  *   - dX is the FORWARD of the transposed layer (u_in' = U_out^T, core'[b][a][y][x] =
  *     G[a][b][kh-1-y][kw-1-x], u_out' = U_in^T, S' = S by input channel with flipped
- *     taps, pad' = kernel-1-pad, stride 1), created inside the backward handle through
+ *     taps, pad' = kernel-1-pad, stride 1; on the zero-inserted dY at stride > 1), created inside the backward handle through
  *     lrs_conv_create: the same fused tensor-core kernels (2:4 sparse term included).
  *   - T1, T2 (recomputed from X), dT2 and dT1 run on the library's tcgen05 GEMM engine.
  *   - the four weight-gradient reductions over positions run as ONE grouped tcgen05
@@ -336,10 +336,14 @@ lrs_status lrs_conv_debug_trace(lrs_conv *h, void *dev_buf);
  *     the K splits in a fixed order (deterministic: the same inputs give the same bits).
  *   Intermediates T1, T2, dT2, dT1 are bf16 (like the forward's); accumulation is fp32.
  *
- * Requirements: dtype BF16, Tucker-2 core or SVD pair (not the CP kind), stride 1, no
+ * Stride s > 1: the two adjoint convolutions (dX, dT1) run on zero-inserted gradients
+ * (dY_up[n][ho*s][wo*s] = dY[n][ho][wo], extent (out-1) s + 1 + ((in + 2p - k) mod s)) through
+ * the same stride-1 transposed layer; the shifted weight-gradient operands are TMA boxes
+ * sampled every s positions.
+ * Requirements: dtype BF16, Tucker-2 core or SVD pair (not the CP kind), stride <= 4, no
  * fused output epilogue (out_scale / out_bias / out_relu: back-propagate through them in
  * the caller), every forward requirement of the layer and of its transposed layer, and
- * output rows of at most 128 positions (in_w <= 128); else LRS_ERR_UNSUPPORTED.
+ * rows of at most 128 positions (in_w <= 128); else LRS_ERR_UNSUPPORTED.
  */
 typedef struct lrs_conv_bwd lrs_conv_bwd; /* opaque */
 

@@ -15,6 +15,10 @@ struct lrs_conv_bwd {
   lrs_conv_desc d{};
   bool svd = false;
   int kh = 1, kw = 1, H = 0, W = 0, ho = 0, wo = 0, cin = 0, cout = 0, r1 = 0, r2 = 0, r1p = 0, r2p = 0;
+  int sh = 1, sw = 1;   // stride
+  int hu = 0, wu = 0;   // extent of the zero-inserted gradient grid (= ho, wo at stride 1)
+  void* dy_up = nullptr;   // zero-inserted dY  [batch_max][hu][wu][Cout] (stride > 1)
+  void* dt2_up = nullptr;  // zero-inserted dT2 [batch_max][hu][wu][R2p]  (stride > 1)
   int batch_max = 0;
   long long nnz = 0;
   lrs_conv* tr = nullptr;  // the transposed layer (dX = its forward of dY)
@@ -108,9 +112,9 @@ lrs_status plan_conv_stage(Stage& s, ConvGeom g, int k_p, int n_p, void* in, voi
                         static_cast<uint64_t>(batch_max)};
     uint64_t strides[3] = {static_cast<uint64_t>(k_p) * 2, static_cast<uint64_t>(g.w) * k_p * 2,
                            static_cast<uint64_t>(g.h) * g.w * k_p * 2};
-    uint32_t box[4] = {static_cast<uint32_t>(p.kc), static_cast<uint32_t>(g.wo), static_cast<uint32_t>(g.th),
-                       static_cast<uint32_t>(g.nb)};
-    uint32_t estr[4] = {1, 1, 1, 1};
+    uint32_t box[4] = {static_cast<uint32_t>(p.kc), static_cast<uint32_t>(g.wo * g.sw),
+                       static_cast<uint32_t>(g.th * g.sh), static_cast<uint32_t>(g.nb)};
+    uint32_t estr[4] = {1, static_cast<uint32_t>(g.sw), static_cast<uint32_t>(g.sh), 1};  // stride: traversal
     if ((st = encode(&p.tmA, false, 4, in, dims, strides, box, estr, sw)) != LRS_OK) return st;
   }
   {
@@ -223,9 +227,11 @@ lrs_status bwd_encode_call(lrs_conv_bwd* h, const void* x, const void* dy, int n
                           static_cast<uint64_t>(n)};
       uint64_t strides[3] = {static_cast<uint64_t>(o.ch) * 2, static_cast<uint64_t>(o.w) * o.ch * 2,
                              static_cast<uint64_t>(o.h) * o.w * o.ch * 2};
-      uint32_t box[4] = {64, static_cast<uint32_t>(h->box_bw[i]), static_cast<uint32_t>(h->box_bh[i]),
+      // the shifted operand of a strided layer is sampled every s positions (TMA traversal stride)
+      const uint32_t ssw = ab ? 1u : static_cast<uint32_t>(q.sw), ssh = ab ? 1u : static_cast<uint32_t>(q.sh);
+      uint32_t box[4] = {64, static_cast<uint32_t>(h->box_bw[i]) * ssw, static_cast<uint32_t>(h->box_bh[i]) * ssh,
                          static_cast<uint32_t>(h->box_bi[i])};
-      uint32_t estr[4] = {1, 1, 1, 1};
+      uint32_t estr[4] = {1, ssw, ssh, 1};
       if ((st = encode_t(ab ? &q.tmB : &q.tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims,
                          strides, box, estr, 128)) != LRS_OK)
         return st;
@@ -246,6 +252,18 @@ lrs_status bwd_encode_call(lrs_conv_bwd* h, const void* x, const void* dy, int n
 namespace {
 lrs_status bwd_weights_impl(lrs_conv_bwd* h, const void* x, const void* dy, int32_t n, const lrs_conv_grads* gr,
                             void* stream_);
+// dY (or dT2) -> its zero-inserted grid for the stride-s adjoint (a plain launch: the next
+// kernel, PDL or not, starts after it completes)
+lrs_status bwd_zero_insert(const lrs_conv_bwd* h, const void* src, void* up, int n, int c, cudaStream_t s) {
+  const int cv = c / 8;
+  const long long total = static_cast<long long>(n) * h->hu * h->wu * cv;
+  const unsigned grid = static_cast<unsigned>(std::min<long long>((total + 255) / 256, 8LL * h->sms));
+  lrs_zero_insert_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint4*>(up), n, h->ho,
+                                              h->wo, h->hu, h->wu, h->sh, h->sw, cv);
+  LRS_CUDA(cudaGetLastError());
+  return LRS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -256,6 +274,7 @@ lrs_status lrs_conv_bwd_destroy(lrs_conv_bwd* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->w_coret, h->t1, h->t2, h->dt2, h->dt1, h->slab, h->idx,
+                  h->dy_up, h->dt2_up,
                   h->wg_items_l[0], h->wg_ptr_l[0], h->wg_items_l[1], h->wg_ptr_l[1]};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -277,7 +296,7 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
   if (st != LRS_OK) return st;
   if (d->dtype != LRS_DTYPE_BF16) return fail(LRS_ERR_UNSUPPORTED, "backward: bf16 layers only");
   if (d->core && d->core_kind == LRS_CORE_CP) return fail(LRS_ERR_UNSUPPORTED, "backward: the CP core kind is not supported");
-  if (d->stride_h != 1 || d->stride_w != 1) return fail(LRS_ERR_UNSUPPORTED, "backward: stride 1 only");
+  if (d->stride_h > 4 || d->stride_w > 4) return fail(LRS_ERR_UNSUPPORTED, "backward: stride > 4");
   if (d->out_scale || d->out_bias || d->out_relu)
     return fail(LRS_ERR_UNSUPPORTED, "backward: no fused output epilogue (back-propagate through it in the caller)");
   if (d->in_w > kTileM) return fail(LRS_ERR_UNSUPPORTED, "backward: in_w > 128");
@@ -304,8 +323,15 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
   h->kw = d->kernel_w;
   h->H = d->in_h;
   h->W = d->in_w;
-  h->ho = d->in_h + 2 * d->pad_h - d->kernel_h + 1;
-  h->wo = d->in_w + 2 * d->pad_w - d->kernel_w + 1;
+  h->sh = d->stride_h;
+  h->sw = d->stride_w;
+  h->ho = (d->in_h + 2 * d->pad_h - d->kernel_h) / h->sh + 1;
+  h->wo = (d->in_w + 2 * d->pad_w - d->kernel_w) / h->sw + 1;
+  // at stride s the adjoint convolutions run on zero-inserted gradients: dY_up[n][ho*s][wo*s]
+  // = dY[n][ho][wo], extent (out - 1) s + 1 + r with r = (in + 2p - k) mod s, so that the
+  // stride-1 transposed convolution (pad k-1-p) returns exactly the input extent
+  h->hu = (h->ho - 1) * h->sh + 1 + (d->in_h + 2 * d->pad_h - d->kernel_h) % h->sh;
+  h->wu = (h->wo - 1) * h->sw + 1 + (d->in_w + 2 * d->pad_w - d->kernel_w) % h->sw;
   h->cin = d->c_in;
   h->cout = d->c_out;
   h->r1 = d->rank_in;
@@ -359,8 +385,10 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
       rp[c + 1] = static_cast<int64_t>(ci.size());
     }
     lrs_conv_desc t = *d;
-    t.in_h = h->ho;
-    t.in_w = h->wo;
+    t.in_h = h->hu;
+    t.in_w = h->wu;
+    t.stride_h = 1;
+    t.stride_w = 1;
     t.c_in = cout;
     t.c_out = cin;
     t.pad_h = kh - 1 - d->pad_h;
@@ -414,6 +442,11 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
     if ((st = bwd_alloc(&h->t2, static_cast<size_t>(p_max) * r2p * 2, "T2")) != LRS_OK) return cleanup_fail(st);
     if ((st = bwd_alloc(&h->dt2, static_cast<size_t>(p_max) * r2p * 2, "dT2")) != LRS_OK) return cleanup_fail(st);
   }
+  if (h->sh > 1 || h->sw > 1) {
+    const size_t pu = static_cast<size_t>(d->batch_max) * h->hu * h->wu;
+    if ((st = bwd_alloc(&h->dy_up, pu * cout * 2, "dY_up")) != LRS_OK) return cleanup_fail(st);
+    if (!h->svd && (st = bwd_alloc(&h->dt2_up, pu * r2p * 2, "dT2_up")) != LRS_OK) return cleanup_fail(st);
+  }
   // ------------------------------------------------ recompute GEMM stages
   if ((st = plan_proj_stage(h->g_t1, cin, r1p, h->w_uin, h->t1, &h->sw_x, &h->kc_x)) != LRS_OK) return cleanup_fail(st);
   h->g_t1.name = "bwd_t1";
@@ -423,13 +456,14 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
   if (!h->svd) {
     ConvGeom g{};
     g.h = h->H; g.w = h->W; g.ho = h->ho; g.wo = h->wo; g.kh = kh; g.kw = kw;
-    g.sh = 1; g.sw = 1; g.ph = d->pad_h; g.pw = d->pad_w;
+    g.sh = h->sh; g.sw = h->sw; g.ph = d->pad_h; g.pw = d->pad_w;
     if ((st = plan_conv_stage(h->g_t2, g, r1p, r2p, h->t1, h->w_core, h->t2, d->batch_max)) != LRS_OK) return cleanup_fail(st);
     h->g_t2.name = "bwd_t2";
     ConvGeom gt{};
-    gt.h = h->ho; gt.w = h->wo; gt.ho = h->H; gt.wo = h->W; gt.kh = kh; gt.kw = kw;
+    gt.h = h->hu; gt.w = h->wu; gt.ho = h->H; gt.wo = h->W; gt.kh = kh; gt.kw = kw;
     gt.sh = 1; gt.sw = 1; gt.ph = kh - 1 - d->pad_h; gt.pw = kw - 1 - d->pad_w;
-    if ((st = plan_conv_stage(h->g_dt1, gt, r2p, r1p, h->dt2, h->w_coret, h->dt1, d->batch_max)) != LRS_OK)
+    void* dt1_in = (h->sh > 1 || h->sw > 1) ? h->dt2_up : h->dt2;
+    if ((st = plan_conv_stage(h->g_dt1, gt, r2p, r1p, dt1_in, h->w_coret, h->dt1, d->batch_max)) != LRS_OK)
       return cleanup_fail(st);
     h->g_dt1.name = "bwd_dt1";
   }
@@ -473,6 +507,8 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
     q.kw = pr.taps == 1 ? 1 : kw;
     q.pad_h = pr.taps == 1 ? 0 : d->pad_h;
     q.pad_w = pr.taps == 1 ? 0 : d->pad_w;
+    q.sh = pr.taps == 1 ? 1 : h->sh;  // the shifted operand (T1 / X) is sampled at the stride
+    q.sw = pr.taps == 1 ? 1 : h->sw;
     const int gh = pr.grid_in ? h->H : h->ho, gw = pr.grid_in ? h->W : h->wo;
     int bh = 0, bi = 0, stages = 0;
     if (!pick_wgrad_step(gh, gw, d->batch_max, bn, &bh, &bi, &stages))
@@ -700,6 +736,14 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
 
 lrs_status lrs_conv_backward_data(lrs_conv_bwd* h, const void* dy, void* dx, int32_t n, void* stream) {
   if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (h->dy_up && n > 0 && n <= h->batch_max) {
+    if (!dy || !dx) return fail(LRS_ERR_INVALID_ARGUMENT, "dy / dx is NULL");
+    DeviceGuard dg;
+    LRS_CUDA(dg.enter(h->device));
+    lrs_status st = bwd_zero_insert(h, dy, h->dy_up, n, h->cout, static_cast<cudaStream_t>(stream));
+    if (st != LRS_OK) return st;
+    return lrs_conv_forward(h->tr, h->dy_up, dx, n, stream);
+  }
   return lrs_conv_forward(h->tr, dy, dx, n, stream);
 }
 
@@ -718,7 +762,7 @@ lrs_status lrs_conv_backward(lrs_conv_bwd* h, const void* x, const void* dy, voi
     LRS_CUDA(dg.enter(h->device));
     LRS_CUDA(cudaEventRecord(h->ev_fork, static_cast<cudaStream_t>(stream_)));  // before the transposed forward
   }
-  lrs_status st = lrs_conv_forward(h->tr, dy, dx, n, stream_);
+  lrs_status st = lrs_conv_backward_data(h, dy, dx, n, stream_);
   if (st != LRS_OK || n == 0) {
     if (st == LRS_OK) st = bwd_weights_impl(h, x, dy, n, gr, stream_);
     return st;
@@ -802,6 +846,7 @@ lrs_status bwd_weights_impl(lrs_conv_bwd* h, const void* x, const void* dy, int3
       (st = launch_stage(h->g_dt2, dim3(static_cast<unsigned>((P + kTileM - 1) / kTileM)))) != LRS_OK)
     return st;
   if (!h->svd && !h->dt1_ext) {
+    if (h->dt2_up && (st = bwd_zero_insert(h, h->dt2, h->dt2_up, n, h->r2p, rstream)) != LRS_OK) return st;
     const ConvGeom& g = h->g_dt1.p.g;
     if ((st = launch_stage(h->g_dt1, dim3(static_cast<unsigned>(((n + g.nb - 1) / g.nb) * g.tiles_h)))) != LRS_OK)
       return st;

@@ -44,6 +44,7 @@ struct WgradProblem {
   float* slab;         // [splits][taps][m_tiles*128][n_tiles*bn] fp32 partial sums
   long long split_stride;  // floats per split
   int taps, kw, pad_h, pad_w;
+  int sh, sw;          // stride of the shifted operand A (its box samples every s positions)
   int m_tiles, n_tiles, bn;  // bn in {64, 128, 192, 256}
   int splits;
   int kst;             // positions per step (MMA K of one stage), multiple of 16
@@ -196,8 +197,8 @@ __global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_co
           const int h0 = (it - ig * p.hsteps) * p.bh;
           const int img0 = ig * p.bi;
           mbar_arrive_expect_tx(&full[s], tx_bytes);
-          tma_load_4d(st, &p.tmA, &full[s], m0, g.tx - p.pad_w, h0 + g.ty - p.pad_h, img0);
-          tma_load_4d(st + atom, &p.tmA, &full[s], m0 + 64, g.tx - p.pad_w, h0 + g.ty - p.pad_h, img0);
+          tma_load_4d(st, &p.tmA, &full[s], m0, g.tx - p.pad_w, h0 * p.sh + g.ty - p.pad_h, img0);
+          tma_load_4d(st + atom, &p.tmA, &full[s], m0 + 64, g.tx - p.pad_w, h0 * p.sh + g.ty - p.pad_h, img0);
           for (int b = 0; b < nb_atoms; ++b)
             tma_load_4d(st + (2 + b) * atom, &p.tmB, &full[s], n0 + 64 * b, 0, h0, img0);
         }
@@ -302,6 +303,26 @@ __global__ void __launch_bounds__(kGThreads, 1) lrs_wgrad_kernel(const __grid_co
     tc_fence_after();
     if (PAIR) tmem_dealloc2(tmem, 512);
     else tmem_dealloc(tmem, 512);
+  }
+}
+
+// Zero insertion for the adjoint of a strided convolution: up[n][h][w][:] = src[n][h/s][w/s][:]
+// when s divides h and w (and the source position exists), else 0.  16-byte vectors.
+__global__ void lrs_zero_insert_kernel(const uint4* src, uint4* up, int n, int hs, int ws, int hu, int wu, int sh,
+                                       int sw, int cv /* 16-byte vectors per position */) {
+  const long long total = static_cast<long long>(n) * hu * wu * cv;
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(e % cv);
+    long long r = e / cv;
+    const int w = static_cast<int>(r % wu);
+    r /= wu;
+    const int hh = static_cast<int>(r % hu);
+    const long long img = r / hu;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (hh % sh == 0 && w % sw == 0 && hh / sh < hs && w / sw < ws)
+      v = src[((img * hs + hh / sh) * ws + w / sw) * cv + c];
+    up[e] = v;
   }
 }
 

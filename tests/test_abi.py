@@ -189,7 +189,7 @@ def bwd_status(**over):
 def test_backward_create_validation_before_any_device_call():
     """The backward's documented refusals (include/lrs_conv.h "Backward pass") come before
     any device call; a well-formed layer on this GPU-less host is LRS_ERR_CUDA."""
-    assert bwd_status(stride=2)[0] == B.LRS_ERR_UNSUPPORTED
+    assert bwd_status(stride=5)[0] == B.LRS_ERR_UNSUPPORTED
     assert bwd_status(dtype="f32", u_in=base_desc_args()["u_in"])[0] == B.LRS_ERR_UNSUPPORTED
     assert bwd_status(batch_max=0)[0] == B.LRS_ERR_INVALID_ARGUMENT
     st, msg = bwd_status()

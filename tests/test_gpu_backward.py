@@ -6,8 +6,9 @@ lrs_conv_backward_data / lrs_conv_backward_weights).
 bf16 path, tolerance relL2 <= 2e-2 (BASELINE.json north star) on dX (whole tensor, per
 image, per 128-channel block, border rows / columns: tests/parity.py) and on every
 parameter gradient (dU_in, dG, dU_out, and S's value gradient); shapes span several
-tiles, ragged image groups, padding 0 (the transposed layer then pads 2), an SVD pair,
-an empty S, and the full-size C2 / C3 / C4 layers.
+tiles, ragged image groups, padding 0 (the transposed layer then pads 2), stride 2 (even /
+odd extents, a C5-like 28x28 layer), an SVD pair, an empty S, and the full-size C2 / C3 / C4
+layers.
 """
 import numpy as np
 import pytest
@@ -28,6 +29,12 @@ CASES = {
     "c4_b5": workloads.CONFIGS["c4"].replace(batch=5),
     "no_s": CFG("no_s", 4, 14, 14, 128, 128, 3, 1, 1, 32, 32, 0.0, "bf16"),
     "k5": CFG("k5", 2, 12, 12, 64, 64, 5, 1, 2, 32, 32, 0.02, "bf16"),
+    # stride 2 (the adjoints run on zero-inserted gradients; the shifted weight-gradient
+    # operands are TMA boxes sampled every 2 positions): even and odd input extents (r = 0 / 1)
+    "s2_even": CFG("s2_even", 4, 14, 14, 64, 128, 3, 2, 1, 32, 32, 0.02, "bf16"),
+    "s2_odd": CFG("s2_odd", 3, 15, 13, 128, 64, 3, 2, 1, 48, 16, 0.03, "bf16"),
+    "s2_c5": workloads.CONFIGS["c2_bf16"].replace(name="s2_c5", batch=6, in_h=28, in_w=28, c_in=128, c_out=128,
+                                                  stride=2, rank_in=32, rank_out=32),
     # channel counts and ranks off the 64 / 16 grids (padded boxes, odd R2 pitch), 7x7 kernel
     "odd": CFG("odd", 3, 10, 11, 32, 96, 3, 1, 1, 24, 40, 0.03, "bf16"),
     "k7": CFG("k7", 2, 9, 9, 64, 128, 7, 1, 3, 16, 48, 0.02, "bf16"),
@@ -78,7 +85,7 @@ def test_backward_matches_oracle(name):
     check_grads(g, ref, cfg.svd)
 
 
-@pytest.mark.parametrize("name", ["c3_b20", "small_3x3"])
+@pytest.mark.parametrize("name", ["c3_b20", "small_3x3", "s2_odd"])
 def test_backward_deterministic_and_graph_capturable(name):
     """Same inputs -> the same bits (fixed split-sum order), eagerly and replayed from a
     CUDA graph; a smaller n than batch_max on the same handle (ragged split ranges)."""
@@ -113,7 +120,7 @@ def test_backward_deterministic_and_graph_capturable(name):
             assert torch.equal(g[k], g3[k]), k
 
 
-@pytest.mark.parametrize("name", ["c3_b20", "c4_b5", "small_3x3"])
+@pytest.mark.parametrize("name", ["c3_b20", "c4_b5", "small_3x3", "s2_even", "s2_odd"])
 def test_combined_backward_matches_oracle_and_split_calls(name):
     """lrs_conv_backward (dT1 reused from the transposed layer's forward): the oracle's
     tolerance on every output, dX bitwise the backward_data result, the gradients within
@@ -183,8 +190,8 @@ def test_backward_n0_and_errors():
         big = torch.zeros((cfg.batch + 1, cfg.in_h, cfg.in_w, cfg.c_in), dtype=torch.bfloat16, device="cuda")
         bdy = torch.zeros((cfg.batch + 1, cfg.out_h, cfg.out_w, cfg.c_out), dtype=torch.bfloat16, device="cuda")
         bw.backward_weights_into(big, bdy, g)
-    # stride 2 and fp32 are refused (UNSUPPORTED), not silently wrong
-    for bad in (cfg.replace(stride=2), cfg.replace(dtype="f32")):
+    # fp32 and strides > 4 are refused (UNSUPPORTED), not silently wrong
+    for bad in (cfg.replace(stride=5), cfg.replace(dtype="f32")):
         binp = workloads.generate(bad.replace(batch=1))
         with pytest.raises(LrsError, match="UNSUPPORTED"):
             LrsConvBackward.from_inputs(binp, batch_max=1)

@@ -295,3 +295,9 @@ wbn() {
     LRS_WGRAD_BN=192 python tools/bwd_time.py $c >> $O/log.txt 2>&1
   done
 }
+bwds2() {
+  # backward at stride 2 (zero insertion + strided TMA boxes): the backward suite
+  mkdir -p gpurun_out/bwds2; O=gpurun_out/bwds2; rm -f $O/rc.txt
+  timeout 1200 python -m pytest tests/test_gpu_backward.py -q > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  cat $O/rc.txt
+}
