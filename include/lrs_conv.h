@@ -340,7 +340,10 @@ lrs_status lrs_conv_debug_trace(lrs_conv *h, void *dev_buf);
  * (dY_up[n][ho*s][wo*s] = dY[n][ho][wo], extent (out-1) s + 1 + ((in + 2p - k) mod s)) through
  * the same stride-1 transposed layer; the shifted weight-gradient operands are TMA boxes
  * sampled every s positions.
- * Requirements: dtype BF16, Tucker-2 core or SVD pair (not the CP kind), stride <= 4, no
+ * The paper's CP core kind runs as its Tucker-2 embedding (diagonal core G[a][a][y][x] =
+ * B[y][a] C[x][a], bf16) and folds dG into the CP factor gradients: d_core = [dB (kernel_h x R);
+ * dC (kernel_w x R)] (the core array's layout), d_u_in = dA, d_u_out = dD^T.
+ * Requirements: dtype BF16, stride <= 4, no
  * fused output epilogue (out_scale / out_bias / out_relu: back-propagate through them in
  * the caller), every forward requirement of the layer and of its transposed layer, and
  * rows of at most 128 positions (in_w <= 128); else LRS_ERR_UNSUPPORTED.
@@ -351,7 +354,8 @@ typedef struct lrs_conv_bwd lrs_conv_bwd; /* opaque */
    NULL to skip that output (its reduction is still computed when another needs it).    */
 typedef struct lrs_conv_grads {
   float *d_u_in;   /* [c_in][rank_in]                                      */
-  float *d_core;   /* [rank_in][rank_out][kernel_h][kernel_w] (NULL for an SVD pair) */
+  float *d_core;   /* [rank_in][rank_out][kernel_h][kernel_w] (CP kind: [kernel_h + kernel_w][R];
+                      NULL for an SVD pair)                                                    */
   float *d_u_out;  /* [rank_out][c_out]                                    */
   float *d_values; /* [nnz], in the order of the descriptor's CSR entries  */
 } lrs_conv_grads;

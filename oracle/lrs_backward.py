@@ -37,10 +37,10 @@ from typing import Optional
 
 import numpy as np
 
-from .lrs_oracle import (conv_1x1, conv_direct, densify_sparse, out_size, reconstruct_tucker2)
+from .lrs_oracle import (conv_1x1, conv_direct, densify_sparse, out_size, reconstruct_cp, reconstruct_tucker2)
 
 __all__ = ["conv_adjoint_input", "weight_grad_dense", "backward_dense", "backward_factored",
-           "sparse_values_grad", "transposed_layer"]
+           "sparse_values_grad", "transposed_layer", "backward_cp"]
 
 
 def conv_adjoint_input(dy: np.ndarray, w: np.ndarray, in_h: int, in_w: int, stride: int = 1,
@@ -208,3 +208,26 @@ def transposed_layer(u_in, core, u_out, row_ptr, col_idx, values, c_in: int, pad
         rp.append(len(ci))
     return (u_out.T.copy(), core_t, u_in.T.copy(), np.asarray(rp, np.int64), np.asarray(ci, np.int32),
             np.asarray(va, np.float64), k - 1 - pad)
+
+
+def backward_cp(x, dy, a, b, c, d, row_ptr, col_idx, values, stride=1, pad=0) -> dict:
+    """The gradients of a layer whose L is in the paper's CP form, L_ijkp = A_ir B_kr C_pr D_jr
+    (A [Cin][R], B [k][R] (taps along H), C [k][R] (along W), D [Cout][R]),
+    the paper's own decomposed layer that §3.5 fine-tunes: dX as the adjoint
+    convolution with W = L + S, dW the full weight gradient, and the chain rule through the
+    four factors
+      dA[i,r] = sum dW[i,j,k,p] B[k,r] C[p,r] D[j,r]      dB[k,r] = sum dW A[i,r] C[p,r] D[j,r]
+      dC[p,r] = sum dW A[i,r] B[k,r] D[j,r]               dD[j,r] = sum dW A[i,r] B[k,r] C[p,r]
+    and dvalues = dW at S's support."""
+    x = np.asarray(x, np.float64)
+    a, b, c, d = (np.asarray(t, np.float64) for t in (a, b, c, d))
+    k = b.shape[0]
+    w = reconstruct_cp(a, b, c, d) + densify_sparse(a.shape[0], d.shape[0], k, row_ptr, col_idx, values)
+    dx = conv_adjoint_input(dy, w, x.shape[1], x.shape[2], stride, pad)
+    dw = weight_grad_dense(x, dy, k, stride, pad)
+    return {"dx": dx,
+            "d_a": np.einsum("ijkp,kr,pr,jr->ir", dw, b, c, d, optimize=True),
+            "d_b": np.einsum("ijkp,ir,pr,jr->kr", dw, a, c, d, optimize=True),
+            "d_c": np.einsum("ijkp,ir,kr,jr->pr", dw, a, b, d, optimize=True),
+            "d_d": np.einsum("ijkp,ir,kr,pr->jr", dw, a, b, c, optimize=True),
+            "d_values": sparse_values_grad(dw, row_ptr, col_idx), "dw": dw}

@@ -16,6 +16,12 @@ struct lrs_conv_bwd {
   bool svd = false;
   int kh = 1, kw = 1, H = 0, W = 0, ho = 0, wo = 0, cin = 0, cout = 0, r1 = 0, r2 = 0, r1p = 0, r2p = 0;
   int sh = 1, sw = 1;   // stride
+  // the paper's CP core kind: run as its Tucker-2 embedding (diagonal core G[a][a][y][x] =
+  // B[y][a] C[x][a]); dG goes to dg_int and lrs_cp_core_grad_kernel folds it into dB, dC
+  bool cp = false;
+  float* cp_b = nullptr;   // B [kh][R] fp32
+  float* cp_c = nullptr;   // C [kw][R] fp32
+  float* dg_int = nullptr; // dG [R][R][kh][kw] fp32
   int hu = 0, wu = 0;   // extent of the zero-inserted gradient grid (= ho, wo at stride 1)
   void* dy_up = nullptr;   // zero-inserted dY  [batch_max][hu][wu][Cout] (stride > 1)
   void* dt2_up = nullptr;  // zero-inserted dT2 [batch_max][hu][wu][R2p]  (stride > 1)
@@ -274,7 +280,7 @@ lrs_status lrs_conv_bwd_destroy(lrs_conv_bwd* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   void* bufs[] = {h->w_uin, h->w_core, h->w_uout, h->w_coret, h->t1, h->t2, h->dt2, h->dt1, h->slab, h->idx,
-                  h->dy_up, h->dt2_up,
+                  h->dy_up, h->dt2_up, h->cp_b, h->cp_c, h->dg_int,
                   h->wg_items_l[0], h->wg_ptr_l[0], h->wg_items_l[1], h->wg_ptr_l[1]};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -295,7 +301,32 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
   lrs_status st = validate(d);
   if (st != LRS_OK) return st;
   if (d->dtype != LRS_DTYPE_BF16) return fail(LRS_ERR_UNSUPPORTED, "backward: bf16 layers only");
-  if (d->core && d->core_kind == LRS_CORE_CP) return fail(LRS_ERR_UNSUPPORTED, "backward: the CP core kind is not supported");
+  // the CP core kind (the paper's own decomposition): its Tucker-2 embedding, a
+  // diagonal core G[a][b][y][x] = [a == b] B[y][a] C[x][a] (bf16, RNE of the fp32 product)
+  std::vector<uint16_t> cp_emb;
+  std::vector<float> cp_bf, cp_cf;
+  lrs_conv_desc d_emb;
+  const bool is_cp = d->core && d->core_kind == LRS_CORE_CP;
+  if (is_cp) {
+    const int R = d->rank_in, kh_ = d->kernel_h, kw_ = d->kernel_w;
+    cp_bf.resize(static_cast<size_t>(kh_) * R);
+    cp_cf.resize(static_cast<size_t>(kw_) * R);
+    for (int y = 0; y < kh_; ++y)
+      for (int a = 0; a < R; ++a) cp_bf[static_cast<size_t>(y) * R + a] = host_val(d->core, static_cast<size_t>(y) * R + a, false);
+    for (int x = 0; x < kw_; ++x)
+      for (int a = 0; a < R; ++a)
+        cp_cf[static_cast<size_t>(x) * R + a] = host_val(d->core, static_cast<size_t>(kh_ + x) * R + a, false);
+    cp_emb.assign(static_cast<size_t>(R) * R * kh_ * kw_, 0);
+    for (int a = 0; a < R; ++a)
+      for (int y = 0; y < kh_; ++y)
+        for (int x = 0; x < kw_; ++x)
+          cp_emb[((static_cast<size_t>(a) * R + a) * kh_ + y) * kw_ + x] =
+              bf16_bits_rne(cp_bf[static_cast<size_t>(y) * R + a] * cp_cf[static_cast<size_t>(x) * R + a]);
+    d_emb = *d;
+    d_emb.core = cp_emb.data();
+    d_emb.core_kind = LRS_CORE_TUCKER2;
+    d = &d_emb;
+  }
   if (d->stride_h > 4 || d->stride_w > 4) return fail(LRS_ERR_UNSUPPORTED, "backward: stride > 4");
   if (d->out_scale || d->out_bias || d->out_relu)
     return fail(LRS_ERR_UNSUPPORTED, "backward: no fused output epilogue (back-propagate through it in the caller)");
@@ -311,6 +342,7 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
   if (prop.major != 10) return fail(LRS_ERR_UNSUPPORTED, "device %d is not sm_100", device);
 
   lrs_conv_bwd* h = new lrs_conv_bwd();
+  h->cp = is_cp;
   auto cleanup_fail = [&](lrs_status s) {
     lrs_conv_bwd_destroy(h);
     return s;
@@ -441,6 +473,19 @@ lrs_status lrs_conv_bwd_create(const lrs_conv_desc* d, int device, lrs_conv_bwd*
   if (!h->svd) {
     if ((st = bwd_alloc(&h->t2, static_cast<size_t>(p_max) * r2p * 2, "T2")) != LRS_OK) return cleanup_fail(st);
     if ((st = bwd_alloc(&h->dt2, static_cast<size_t>(p_max) * r2p * 2, "dT2")) != LRS_OK) return cleanup_fail(st);
+  }
+  if (h->cp) {
+    std::vector<uint8_t> bb(cp_bf.size() * 4), cb(cp_cf.size() * 4);
+    memcpy(bb.data(), cp_bf.data(), bb.size());
+    memcpy(cb.data(), cp_cf.data(), cb.size());
+    void* p1 = nullptr;
+    void* p2 = nullptr;
+    if ((st = upload(&p1, bb)) != LRS_OK) return cleanup_fail(st);
+    h->cp_b = static_cast<float*>(p1);
+    if ((st = upload(&p2, cb)) != LRS_OK) return cleanup_fail(st);
+    h->cp_c = static_cast<float*>(p2);
+    if ((st = bwd_alloc(reinterpret_cast<void**>(&h->dg_int), static_cast<size_t>(r1) * r2 * kk * 4, "dG")) != LRS_OK)
+      return cleanup_fail(st);
   }
   if (h->sh > 1 || h->sw > 1) {
     const size_t pu = static_cast<size_t>(d->batch_max) * h->hu * h->wu;
@@ -791,17 +836,21 @@ lrs_status bwd_weights_impl(lrs_conv_bwd* h, const void* x, const void* dy, int3
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   DeviceGuard dg;
   LRS_CUDA(dg.enter(h->device));
-  const float* dsts[4] = {gr->d_u_out, gr->d_core, gr->d_u_in, gr->d_values};
+  // CP: dG is reduced into the internal buffer and folded into dB, dC afterwards
+  const float* dsts[4] = {gr->d_u_out, (h->cp && gr->d_core) ? h->dg_int : gr->d_core, gr->d_u_in, gr->d_values};
   if (n > 0 && (!x || !dy)) return fail(LRS_ERR_INVALID_ARGUMENT, "x / dy is NULL");
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(dy) & 15))
     return fail(LRS_ERR_INVALID_ARGUMENT, "x / dy must be 16-byte aligned");
   if (n == 0) {
     // no positions: every gradient is zero
-    const size_t sizes[4] = {static_cast<size_t>(h->r2) * h->cout, static_cast<size_t>(h->r1) * h->r2 * h->kh * h->kw,
+    const size_t sizes[4] = {static_cast<size_t>(h->r2) * h->cout,
+                             h->cp ? static_cast<size_t>(h->kh + h->kw) * h->r1
+                                   : static_cast<size_t>(h->r1) * h->r2 * h->kh * h->kw,
                              static_cast<size_t>(h->cin) * h->r1, static_cast<size_t>(h->nnz)};
+    const float* user[4] = {gr->d_u_out, gr->d_core, gr->d_u_in, gr->d_values};
     for (int i = 0; i < 4; ++i)
-      if (dsts[i] && sizes[i] && !(i == 1 && h->svd))
-        LRS_CUDA(cudaMemsetAsync(const_cast<float*>(dsts[i]), 0, sizes[i] * 4, stream));
+      if (user[i] && sizes[i] && !(i == 1 && h->svd))
+        LRS_CUDA(cudaMemsetAsync(const_cast<float*>(user[i]), 0, sizes[i] * 4, stream));
     return LRS_OK;
   }
   lrs_status st = bwd_encode_call(h, x, dy, n);
@@ -890,6 +939,10 @@ lrs_status bwd_weights_impl(lrs_conv_bwd* h, const void* x, const void* dy, int3
                                          dim3(static_cast<unsigned>(blocks)), dim3(kGRThreads), &rs, 0, stream);
                      }, stream)) != LRS_OK)
     return st;
+  if (h->cp && gr->d_core) {
+    lrs_cp_core_grad_kernel<<<1, 256, 0, stream>>>(h->dg_int, h->cp_b, h->cp_c, h->r1, h->kh, h->kw, gr->d_core);
+    LRS_CUDA(cudaGetLastError());
+  }
   return LRS_OK;
 }
 
@@ -951,7 +1004,8 @@ int32_t lrs_conv_bwd_launches(const lrs_conv_bwd* h, int32_t* data_launches, int
   if (!h) return 0;
   const int32_t d = lrs_conv_launches_per_forward(h->tr);
   // recompute GEMMs + the weight-gradient launch(es) (solo, CTA pairs) + the reduction
-  const int32_t w = (h->svd ? 2 : 4) + (h->wg_ctas_l[0] > 0 ? 1 : 0) + (h->wg_ctas_l[1] > 0 ? 1 : 0) + 1;
+  const int32_t w = (h->svd ? 2 : 4) + (h->wg_ctas_l[0] > 0 ? 1 : 0) + (h->wg_ctas_l[1] > 0 ? 1 : 0) + 1 +
+                    (h->cp ? 1 : 0);
   const bool reuse = h->svd ? (!h->tr->pw_ft && h->tr->r1p == h->r1p) : (h->tr->r2p == h->r1p);
   if (data_launches) *data_launches = d;
   if (combined_launches) *combined_launches = d + w - (reuse ? 1 : 0);

@@ -326,6 +326,26 @@ __global__ void lrs_zero_insert_kernel(const uint4* src, uint4* up, int n, int h
   }
 }
 
+// The CP core kind's factor gradients from the embedded dense core's gradient (PAPER.md:158:
+// G[a][b][y][x] = [a == b] B[y][a] C[x][a]):  dB[y][r] = sum_x dG[r][r][y][x] C[x][r],
+// dC[x][r] = sum_y dG[r][r][y][x] B[y][r].  out = [dB (kh x R) ; dC (kw x R)], the core
+// array's layout.  Fixed-order sums.
+__global__ void lrs_cp_core_grad_kernel(const float* dg, const float* b, const float* c, int r, int kh, int kw,
+                                        float* out) {
+  for (int e = threadIdx.x; e < (kh + kw) * r; e += blockDim.x) {
+    const int t = e / r, q = e - (e / r) * r;
+    const float* dq = dg + (static_cast<long long>(q) * r + q) * kh * kw;  // dG[q][q][.][.]
+    float acc = 0.f;
+    if (t < kh) {
+      for (int x = 0; x < kw; ++x) acc = fmaf(dq[t * kw + x], c[x * r + q], acc);
+    } else {
+      const int x = t - kh;
+      for (int y = 0; y < kh; ++y) acc = fmaf(dq[y * kw + x], b[y * r + q], acc);
+    }
+    out[e] = acc;
+  }
+}
+
 // dst[i] = sum_{s < splits} slab[s * split_stride + idx[i]] (fixed order: deterministic);
 // one launch covers every gradient of the backward (concatenated index tables).
 struct WgradReduceParams {

@@ -461,11 +461,13 @@ class LrsConvBackward:
     gradients {d_u_in, d_core, d_u_out, d_values}; tensors NHWC bf16 on the device."""
 
     def __init__(self, batch_max, in_h, in_w, c_in, c_out, kernel, stride, pad, rank_in, rank_out,
-                 dtype, u_in, core, u_out, row_ptr, col_idx, values, device: int = 0):
+                 dtype, u_in, core, u_out, row_ptr, col_idx, values, device: int = 0,
+                 core_kind: int = LRS_CORE_TUCKER2):
         import torch
         self.torch = torch
         self.device = device
         self.svd = core is None
+        self.cp = core is not None and core_kind == LRS_CORE_CP
         self.in_h, self.in_w, self.c_in, self.c_out = in_h, in_w, c_in, c_out
         self.out_h = (in_h + 2 * pad - kernel) // stride + 1
         self.out_w = (in_w + 2 * pad - kernel) // stride + 1
@@ -473,9 +475,20 @@ class LrsConvBackward:
         self.rank_out = rank_in if core is None else rank_out
         self.nnz = len(values)
         desc, keep = make_desc(batch_max, in_h, in_w, c_in, c_out, kernel, stride, pad, rank_in, rank_out,
-                               dtype, u_in, core, u_out, row_ptr, col_idx, values)
+                               dtype, u_in, core, u_out, row_ptr, col_idx, values, core_kind)
         self.handle = lrs_conv_bwd_create(desc, device)
         del keep
+
+    @classmethod
+    def from_cp(cls, batch_max: int, in_h: int, in_w: int, kernel: int, stride: int, pad: int, dtype: str,
+                a, b, c, d, row_ptr, col_idx, values, device: int = 0) -> "LrsConvBackward":
+        """The backward of the paper's CP layer (LrsConv.from_cp's arguments):
+        d_u_in = dA [c_in][R], d_u_out = dD^T [R][c_out], d_core = [dB (k x R); dC (k x R)]."""
+        a, b, c, d = (np.asarray(t, np.float32) for t in (a, b, c, d))
+        r = a.shape[1]
+        core = np.concatenate([b, c], axis=0)
+        return cls(batch_max, in_h, in_w, a.shape[0], d.shape[0], kernel, stride, pad, r, r, dtype,
+                   a, core, np.ascontiguousarray(d.T), row_ptr, col_idx, values, device, core_kind=LRS_CORE_CP)
 
     @classmethod
     def from_inputs(cls, inp, batch_max: Optional[int] = None, device: int = 0) -> "LrsConvBackward":
@@ -494,8 +507,9 @@ class LrsConvBackward:
         torch = self.torch
         dev = f"cuda:{self.device}"
         g = {"d_u_in": torch.empty((self.c_in, self.rank_in), dtype=torch.float32, device=dev),
-             "d_core": None if self.svd else torch.empty((self.rank_in, self.rank_out, self.kernel, self.kernel),
-                                                         dtype=torch.float32, device=dev),
+             "d_core": None if self.svd else (
+                 torch.empty((2 * self.kernel, self.rank_in), dtype=torch.float32, device=dev) if self.cp else
+                 torch.empty((self.rank_in, self.rank_out, self.kernel, self.kernel), dtype=torch.float32, device=dev)),
              "d_u_out": torch.empty((self.rank_out, self.c_out), dtype=torch.float32, device=dev),
              "d_values": torch.empty((max(self.nnz, 1),), dtype=torch.float32, device=dev)[:self.nnz]}
         return g
@@ -516,7 +530,8 @@ class LrsConvBackward:
 
     def _grads_struct(self, grads: dict):
         sizes = {"d_u_in": self.c_in * self.rank_in, "d_u_out": self.rank_out * self.c_out,
-                 "d_core": 0 if self.svd else self.rank_in * self.rank_out * self.kernel ** 2,
+                 "d_core": 0 if self.svd else (2 * self.kernel * self.rank_in if self.cp else
+                                               self.rank_in * self.rank_out * self.kernel ** 2),
                  "d_values": self.nnz}
         ptrs = {}
         for k, numel in sizes.items():

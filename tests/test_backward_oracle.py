@@ -134,3 +134,29 @@ def test_transposed_layer_forward_is_dx(case):
     y = O.forward_factored(dy, ui, g, uo, rp2, ci2, va2, 1, p2)
     assert y.shape == dx.shape
     assert rel_l2(y, dx) < 1e-12
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c[5] > 1])
+def test_cp_backward_matches_torch_autograd(case):
+    """The CP layer's gradients (PAPER.md:137 L = A o B o C o D, fine-tuned per §3.5) against
+    torch reverse mode in fp64 through the CP reconstruction and conv2d."""
+    n, h, w, cin, cout, k, s, p, r1, r2, nnz, svd = case
+    rng = np.random.default_rng(11)
+    x, _, _, _, row_ptr, col_idx, vals = rand_layer(rng, n, h, w, cin, cout, k, r1, r2, nnz)
+    r = 3
+    a, b, c, d = (rng.standard_normal(sh) for sh in ((cin, r), (k, r), (k, r), (cout, r)))
+    ho, wo = O.out_size(h, k, s, p), O.out_size(w, k, s, p)
+    dy = rng.standard_normal((n, ho, wo, cout))
+    got = B.backward_cp(x, dy, a, b, c, d, row_ptr, col_idx, vals, s, p)
+    t = lambda v: torch.tensor(v, requires_grad=True)
+    xt, at, bt, ct, dt, vt = t(x), t(a), t(b), t(c), t(d), t(vals)
+    wl = torch.einsum("ir,kr,pr,jr->ijkp", at, bt, ct, dt)
+    rows = np.repeat(np.arange(cout), np.diff(row_ptr))
+    cc, rem = np.divmod(col_idx.astype(np.int64), k * k)
+    yy, xx = np.divmod(rem, k)
+    ws = torch.zeros((cin, cout, k, k), dtype=torch.float64).index_put(
+        (torch.from_numpy(cc), torch.from_numpy(rows), torch.from_numpy(yy), torch.from_numpy(xx)), vt, accumulate=True)
+    y = torch.nn.functional.conv2d(xt.permute(0, 3, 1, 2), (wl + ws).permute(1, 0, 2, 3), stride=s, padding=p)
+    y.permute(0, 2, 3, 1).backward(torch.from_numpy(dy))
+    for key, tt in (("dx", xt), ("d_a", at), ("d_b", bt), ("d_c", ct), ("d_d", dt), ("d_values", vt)):
+        assert rel_l2(got[key], tt.grad.numpy()) < 1e-12, key

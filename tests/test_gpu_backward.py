@@ -216,3 +216,33 @@ def test_pair_and_solo_weight_gradient_forms_agree(name, monkeypatch):
     for k in g_pair:
         if g_pair[k] is not None and g_pair[k].numel():
             assert rel(g_pair[k].cpu().double().numpy(), g_solo[k].cpu().double().numpy()) < 1e-5, k
+
+
+@pytest.mark.parametrize("name,batch", [("c2_cp", 6), ("c1_cp", 1)])
+def test_cp_layer_backward_matches_oracle(name, batch):
+    """The paper's own decomposed layer (CP) fine-tuned by back-propagation
+    (§3.5): dX, dA, dB, dC, dD and the S value gradients against oracle/lrs_backward.backward_cp
+    (pinned to torch autograd).  The GPU runs the CP layer's Tucker-2 embedding (diagonal core,
+    bf16-rounded products) and folds dG into dB, dC."""
+    from paper_2006_06443_b200 import LrsConvBackward
+    cfg = workloads.CP_CONFIGS[name]
+    if cfg.dtype != "bf16":
+        cfg = cfg.replace(dtype="bf16")
+    inp = workloads.generate_cp(cfg, batch=batch)
+    dy_np = workloads.generate_dy(cfg, batch, seed=17)
+    bw = LrsConvBackward.from_cp(batch, cfg.in_h, cfg.in_w, cfg.k, cfg.stride, cfg.pad, "bf16", inp.a, inp.b, inp.c,
+                                 inp.d, inp.row_ptr, inp.col_idx, inp.values)
+    x = torch.from_numpy(inp.x).to(torch.bfloat16).cuda()
+    dy = torch.from_numpy(dy_np).to(torch.bfloat16).cuda()
+    dx, g = bw.backward(x, dy)
+    torch.cuda.synchronize()
+    xr = x.float().cpu().numpy().astype(np.float64)
+    ref = B.backward_cp(xr, dy_np, inp.a, inp.b, inp.c, inp.d, inp.row_ptr, inp.col_idx, inp.values, cfg.stride,
+                        cfg.pad)
+    parity.check(dx, ref["dx"], "bf16")
+    k = cfg.k
+    got = {"d_a": g["d_u_in"], "d_d": g["d_u_out"].T, "d_b": g["d_core"][:k], "d_c": g["d_core"][k:],
+           "d_values": g["d_values"]}
+    for key, t in got.items():
+        e = rel(t.cpu().double().numpy(), ref[key])
+        assert e <= 2e-2, f"{key}: relL2 {e:.3e}"

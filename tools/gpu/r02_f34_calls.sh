@@ -301,3 +301,9 @@ bwds2() {
   timeout 1200 python -m pytest tests/test_gpu_backward.py -q > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
   cat $O/rc.txt
 }
+bwdcp() {
+  # backward of the paper's CP layer (Tucker-2 embedding + dB / dC fold) and the whole backward suite
+  mkdir -p gpurun_out/bwdcp; O=gpurun_out/bwdcp; rm -f $O/rc.txt
+  timeout 1500 python -m pytest tests/test_gpu_backward.py -q > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  cat $O/rc.txt
+}
