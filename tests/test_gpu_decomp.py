@@ -133,3 +133,41 @@ def test_eigen_path_equals_cholesky_path(monkeypatch):
     assert np.array_equal(a[1], b[1]) and np.array_equal(a[1], ridx)
     for x, y in zip(a[0], b[0]):
         assert rel(x, y) < 1e-8
+
+
+def test_decomposed_weight_runs_as_a_cp_layer():
+    """The paper's pipeline end to end on the GPU: decompose a conv weight W[c][j][y][x] into
+    CP factors + S (f4), load them as a CP layer (F0 = A = u_in, F1 = D,
+    F2 = B, F3 = C; S's linear indices -> CSR by output channel) and run
+    its forward: Y = conv(X, L + S) of the decomposed weight (the fp64 oracle on the same
+    factors), and ||W - L - S|| / ||W|| equal to the decomposition's last eps."""
+    from paper_2006_06443_b200 import LrsConv
+    from oracle import lrs_oracle as O
+    cin, cout, k, r = 64, 128, 3, 16
+    cfg = workloads.DecompConfig("pipe", (cin, cout, k, k), 12, r, 0.02, seed=9)
+    w, f0 = workloads.generate_decomp(cfg)
+    f, idx, val, eps = run_gpu(w, f0, cfg.cardinality, 20)
+    a, d, b, c = f  # mode order (in, out, ky, kx)
+    l = D.cp_reconstruct(f)
+    s_dense = D.sparse_dense(w.shape, idx, val)
+    assert abs(np.linalg.norm(w - l - s_dense) / np.linalg.norm(w) - eps[-1]) < 1e-9
+    # S -> CSR by output channel j, col (c*k + y)*k + x, columns increasing
+    cc, rem = np.divmod(idx, cout * k * k)
+    j, rem = np.divmod(rem, k * k)
+    y, xx = np.divmod(rem, k)
+    col = (cc * k + y) * k + xx
+    order = np.lexsort((col, j))
+    row_ptr = np.zeros(cout + 1, np.int64)
+    np.add.at(row_ptr, j + 1, 1)
+    row_ptr = np.cumsum(row_ptr)
+    col_idx = col[order].astype(np.int32)
+    values = val[order].astype(np.float32)
+    # the layer in fp32 (the decomposition's fp64 factors rounded to fp32 only)
+    n, hh = 2, 10
+    layer = LrsConv.from_cp(n, hh, hh, k, 1, 1, "f32", a, b, c, d, row_ptr, col_idx, values)
+    x = np.maximum(np.random.default_rng(3).standard_normal((n, hh, hh, cin)), 0).astype(np.float32)
+    yg = layer(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    ref = O.conv_direct(x.astype(np.float64), l + s_dense, 1, 1)
+    e = rel(yg.cpu().numpy(), ref)
+    assert e < 1e-5, e
