@@ -452,6 +452,52 @@ lrs_status lrs_decomp_stage_times(lrs_decomp *h, float *ms, int64_t *counts, int
                                   int32_t *n_stages, int32_t reset);
 lrs_status lrs_decomp_destroy(lrs_decomp *h); /* NULL-safe */
 
+/* ------------------------------------------------------------------------------------------
+ * Tucker-2 decomposition (SURVEY §8(f) f4 "Alternating Tucker-2/CP-ALS on W - S"): the same
+ * two-step iteration with L in the forward's primary form, Tucker-2 over the
+ * channel modes -- L[c][j][y][x] = sum_{a,b} U_in[c][a] G[a][b][y][x] U_out[j][b] (PAPER.md:409,
+ * §7: Tucker decomposition "might be extended to low rank and sparse form"; the north star's L is
+ * this Tucker-2 form, SURVEY.md §1 note 2).  update = one higher-order orthogonal
+ * iteration (HOOI) sweep on T = W - S: U_in <- `inner` subspace-iteration steps
+ * orth(Z1 Z1^T U_in) on Z1 = T x_out U_out^T unfolded [Cin][R2 kh kw], then U_out likewise on
+ * Z2 = T x_in U_in^T, then G = T x_in U_in^T x_out U_out^T; orth(Y) = Y (Y^T Y)^-1/2 (Loewdin,
+ * eigenvalues under rcond * the largest dropped).  P_c, eps and the stopping rule as
+ * lrs_decomp_run.  oracle/lrs_decomp.py decompose_lrs_tucker2 writes the algorithm out; every step
+ * runs in fp64 CUDA kernels (a strided batched fp64 GEMM for the mode products, the one-CTA Jacobi
+ * for (Y^T Y)^-1/2, the radix-select projection), deterministic.
+ * Requirements: as lrs_decomp_params with rank = max(r1, r2); 1 <= r1 <= dims[0], 1 <= r2 <= dims[1],
+ * inner >= 1.
+ */
+typedef struct lrs_tucker2_params {
+  int32_t dims[4];     /* Cin, Cout, kh, kw of W[c][j][y][x]                     */
+  int32_t r1, r2;      /* channel ranks (U_in [Cin][r1], U_out [Cout][r2])       */
+  double cardinality;  /* c: S keeps round(c * numel) entries (half to even)     */
+  int32_t max_iters;   /* >= 1                                                   */
+  double tol;          /* stop when eps_{i-1} - eps_i < tol (i >= 1)             */
+  double rcond;        /* Loewdin cutoff relative to the largest eigenvalue      */
+  int32_t inner;       /* subspace-iteration steps per factor per sweep (>= 1)   */
+} lrs_tucker2_params;
+
+typedef struct lrs_tucker2 lrs_tucker2; /* opaque: fp64 workspace for one W shape */
+
+lrs_status lrs_tucker2_create(const lrs_tucker2_params *p, int device, lrs_tucker2 **out);
+
+/* Run from the initial factors u_in (device fp64 [Cin][r1]) and u_out (device fp64 [Cout][r2]:
+   COLUMNS are the basis, i.e. the layer's u_out transposed), overwritten with the orthonormal
+   result; core: device fp64 [r1][r2][kh][kw] (out).  S, eps_hist, iters_done, stream: as
+   lrs_decomp_run (synchronised once per iteration, not graph-capturable).  A zero W gives zero
+   factors and core, an empty S and eps 0. */
+lrs_status lrs_tucker2_run(lrs_tucker2 *h, const double *w, double *u_in, double *u_out, double *core,
+                           int64_t *s_idx, double *s_val, int64_t *s_count, double *eps_hist,
+                           int32_t *iters_done, void *stream);
+int64_t lrs_tucker2_nnz(const lrs_tucker2 *h); /* round(c * numel) */
+/* stage timing: 0 mode products (Z1, Z2, G), 1 subspace steps + Loewdin, 2 residual W - L,
+   3 projection P_c + T = W - S + eps */
+lrs_status lrs_tucker2_set_timing(lrs_tucker2 *h, int32_t enable);
+lrs_status lrs_tucker2_stage_times(lrs_tucker2 *h, float *ms, int64_t *counts, int32_t max_stages,
+                                   int32_t *n_stages, int32_t reset);
+lrs_status lrs_tucker2_destroy(lrs_tucker2 *h); /* NULL-safe */
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,7 +34,8 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 __all__ = ["cp_reconstruct", "mttkrp", "gram_hadamard", "sym_pinv", "cp_als_step", "project_sparse",
-           "sparse_dense", "decompose_lrs", "rel_residual"]
+           "sparse_dense", "decompose_lrs", "rel_residual", "orth_lowdin", "tucker2_reconstruct",
+           "tucker2_hooi_step", "decompose_lrs_tucker2"]
 
 
 def cp_reconstruct(f: Sequence[np.ndarray]) -> np.ndarray:
@@ -155,3 +156,75 @@ def svd_init(w: np.ndarray, rank: int, seed: int = 0) -> List[np.ndarray]:
         sgn[sgn == 0] = 1.0
         out.append(u * sgn)
     return out
+
+
+# --------------------------------------------------------------------------
+# Tucker-2 form (BASELINE's primary L; SURVEY §8(f) f4 "Alternating Tucker-2/CP-ALS"
+# §7 names Tucker decomposition "extended to low rank and sparse form" as the next step)
+# --------------------------------------------------------------------------
+# W[c][j][y][x] ~ L = sum_{a,b} U_in[c,a] G[a,b,y,x] U_out[j,b] with orthonormal U_in [Cin][R1],
+# U_out [Cout][R2] (the layer's u_out = U_out^T), the kernel modes uncompressed.  `update`
+# = one higher-order orthogonal iteration (HOOI) sweep on T = W - S: each channel
+# factor becomes the dominant R-dimensional left singular subspace of T contracted with the
+# other factor, computed by `inner` steps of subspace iteration U <- orth(Z Z^T U) with the
+# symmetric (Loewdin) orthonormalisation orth(Y) = Y (Y^T Y)^(-1/2); then G = T x U_in^T x U_out^T.
+
+def orth_lowdin(y: np.ndarray, rcond: float = 1e-10) -> np.ndarray:
+    """Y (Y^T Y)^(-1/2) through the eigendecomposition of the Gram matrix (eigenvalues under
+    rcond * the largest dropped): the orthonormal basis of span(Y) closest to Y."""
+    y = np.asarray(y, np.float64)
+    lam, q = np.linalg.eigh(y.T @ y)
+    lmax = float(np.max(np.abs(lam))) if lam.size else 0.0
+    keep = np.abs(lam) > rcond * lmax
+    inv = np.zeros_like(lam)
+    inv[keep] = 1.0 / np.sqrt(np.abs(lam[keep]))
+    return y @ ((q * inv) @ q.T)
+
+
+def tucker2_reconstruct(u_in, g, u_out) -> np.ndarray:
+    """L[c,j,y,x] = sum_{a,b} U_in[c,a] G[a,b,y,x] U_out[j,b]."""
+    return np.einsum("ca,abyx,jb->cjyx", np.asarray(u_in, np.float64), np.asarray(g, np.float64),
+                     np.asarray(u_out, np.float64), optimize=True)
+
+
+def tucker2_hooi_step(u_in, u_out, target, inner: int = 1, rcond: float = 1e-10):
+    """One HOOI sweep on `target` [Cin][Cout][kh][kw] (see the section comment)."""
+    t = np.asarray(target, np.float64)
+    cin, cout = t.shape[0], t.shape[1]
+    u_in = np.array(u_in, np.float64)
+    u_out = np.array(u_out, np.float64)
+    z1 = np.einsum("cjyx,jb->cbyx", t, u_out, optimize=True).reshape(cin, -1)  # T x_out U_out^T
+    for _ in range(inner):
+        u_in = orth_lowdin(z1 @ (z1.T @ u_in), rcond)
+    z2 = np.einsum("cjyx,ca->jayx", t, u_in, optimize=True).reshape(cout, -1)  # T x_in U_in^T
+    for _ in range(inner):
+        u_out = orth_lowdin(z2 @ (z2.T @ u_out), rcond)
+    g = np.einsum("cjyx,ca,jb->abyx", t, u_in, u_out, optimize=True)
+    return u_in, u_out, g
+
+
+def decompose_lrs_tucker2(w, u_in0, u_out0, cardinality: float, max_iters: int = 100, tol: float = 1e-6,
+                          inner: int = 1, rcond: float = 1e-10):
+    """PAPER.md:142-144 with the Tucker-2 update: from S_0 = 0,
+      (U_in, U_out, G)_i = tucker2_hooi_step(.., W - S_{i-1});  S_i = P_c(W - L_i);
+      eps_i = ||W - L_i - S_i|| / ||W||, stopping as decompose_lrs.  Returns
+    ((U_in, U_out, G), (S indices, values), eps history)."""
+    w = np.asarray(w, np.float64)
+    if not np.any(w):  # as decompose_lrs: zero factors and core, empty S, eps 0
+        r1, r2 = np.asarray(u_in0).shape[1], np.asarray(u_out0).shape[1]
+        return ((np.zeros((w.shape[0], r1)), np.zeros((w.shape[1], r2)), np.zeros((r1, r2) + w.shape[2:])),
+                (np.zeros(0, np.int64), np.zeros(0)), [0.0])
+    u_in, u_out = np.array(u_in0, np.float64), np.array(u_out0, np.float64)
+    s_dense = np.zeros_like(w)
+    idx, vals = np.zeros(0, np.int64), np.zeros(0)
+    hist: List[float] = []
+    g = None
+    for it in range(max_iters):
+        u_in, u_out, g = tucker2_hooi_step(u_in, u_out, w - s_dense, inner, rcond)
+        l = tucker2_reconstruct(u_in, g, u_out)
+        idx, vals = project_sparse(w - l, cardinality)
+        s_dense = sparse_dense(w.shape, idx, vals)
+        hist.append(rel_residual(w, l, s_dense))
+        if it > 0 and (hist[-2] - hist[-1]) < tol:
+            break
+    return (u_in, u_out, g), (idx, vals), hist

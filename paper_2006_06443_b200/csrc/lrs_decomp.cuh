@@ -247,6 +247,8 @@ struct PinvParams {
   double* qt;  // [rp][rp] this mode's eigenvectors (transposed) from its previous call: in if warm, out always
   int warm;    // 1: start from A = Q^T V Q (the normal matrix changes little between sweeps)
   int force_eigen;  // 1: skip the certified Cholesky path (LRS_DECOMP_EIGEN; tests of the eigen path)
+  const double* single;  // non-NULL: V = this matrix itself (g / mode unused) -- the Tucker-2 Gram Y^T Y
+  int inv_sqrt;          // 1: P = Q diag(lambda^-1/2) Q^T (the Loewdin orthonormaliser; eigen path only)
 };
 
 constexpr int kJThreads = 512;
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
   // P = X^T X -- all in shared memory when A is.  Certificate: lambda_min >= 1 / ||P||_F and
   // lambda_max <= ||V||_F, so 1 / ||P||_F > rcond ||V||_F proves the cutoff drops nothing;
   // otherwise (or at a non-positive pivot) the Jacobi eigensolver below decides.
-  if (!q.force_eigen) {
+  if (!q.force_eigen && !q.inv_sqrt) {
     __shared__ int fail;
     __shared__ double vn2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -279,8 +281,11 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
     for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
       const int i = e / r, j = e % r;
       double val = 1.0;
-      for (int o = 0; o < 4; ++o)
-        if (o != q.mode) val *= q.g[o][i * r + j];
+      if (q.single)
+        val = q.single[i * r + j];
+      else
+        for (int o = 0; o < 4; ++o)
+          if (o != q.mode) val *= q.g[o][i * r + j];
       L[e] = val;
       lv += val * val;
     }
@@ -383,8 +388,11 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
     double val = 0.0;
     if (i < r && j < r) {
       val = 1.0;
-      for (int o = 0; o < 4; ++o)
-        if (o != q.mode) val *= q.g[o][i * r + j];
+      if (q.single)
+        val = q.single[i * r + j];
+      else
+        for (int o = 0; o < 4; ++o)
+          if (o != q.mode) val *= q.g[o][i * r + j];
     }
     A[e] = val;  // the dummy index of an odd rank: a zero row / column (eigenvalue 0, dropped)
     Vt[e] = i == j ? 1.0 : 0.0;
@@ -534,7 +542,7 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
   __shared__ double inv[256];
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const double lam = A[k * n + k];
-    inv[k] = fabs(lam) > q.rcond * lmax ? 1.0 / lam : 0.0;
+    inv[k] = fabs(lam) > q.rcond * lmax ? (q.inv_sqrt ? 1.0 / sqrt(fabs(lam)) : 1.0 / lam) : 0.0;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
@@ -545,6 +553,72 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
   }
   if (q.qt)
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) q.qt[e] = Vt[e];
+}
+
+// ---------------------------------------------------------------- strided batched fp64 GEMM
+// C(b, m, n) = sum_k A(b, m, k) B(b, k, n) with arbitrary element strides (the Tucker-2 mode
+// products and subspace steps: every operand is a view of a row-major tensor); C = sub - acc when
+// `sub` is set (indexed like C: the residual W - L).  64 x 64 tiles, 256 threads x 4 x 4
+// outputs (rows ty + 16 i, columns tx + 16 j), K-tiles of 16 through shared memory; each output
+// sums its k in order (deterministic).
+struct DgemmParams {
+  const double* a;
+  const double* b;
+  double* c;
+  const double* sub;
+  int m, n, k;
+  long long sam, sak, sab, sbk, sbn, sbb, scm, scn, scb;
+};
+
+__global__ void __launch_bounds__(256) lrs_dgemm_kernel(const __grid_constant__ DgemmParams p) {
+  __shared__ double as[16][65], bs[16][65];
+  const long long bz = blockIdx.z;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const double* A = p.a + bz * p.sab;
+  const double* B = p.b + bz * p.sbb;
+  const bool a_mfast = p.sam <= p.sak, b_nfast = p.sbn <= p.sbk;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int k0 = 0; k0 < p.k; k0 += 16) {
+    for (int e = threadIdx.x; e < 1024; e += 256) {
+      const int kk = a_mfast ? e >> 6 : e & 15, mm = a_mfast ? e & 63 : e >> 4;
+      const int gm = m0 + mm, gk = k0 + kk;
+      as[kk][mm] = (gm < p.m && gk < p.k) ? A[gm * p.sam + gk * p.sak] : 0.0;
+      const int kb = b_nfast ? e >> 6 : e & 15, nn = b_nfast ? e & 63 : e >> 4;
+      const int gn = n0 + nn, gkb = k0 + kb;
+      bs[kb][nn] = (gn < p.n && gkb < p.k) ? B[gkb * p.sbk + gn * p.sbn] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double ar[4], br[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ar[i] = as[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) br[j] = bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(ar[i], br[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty + 16 * i;
+    if (gm >= p.m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tx + 16 * j;
+      if (gn >= p.n) continue;
+      const long long o = bz * p.scb + gm * p.scm + gn * p.scn;
+      p.c[o] = p.sub ? p.sub[o] - acc[i][j] : acc[i][j];
+    }
+  }
 }
 
 // F[i][c] = sum_k M[i][k] P[k][c]

@@ -69,6 +69,66 @@ struct DcTimer {
   }
 };
 
+// T = W (S_0 = 0) and *wn2 = ||W||^2 (synchronises the stream)
+lrs_status dc_begin(lrs_decomp* h, const double* w, cudaStream_t s, double* wn2_out) {
+  const long long numel = h->numel;
+  // ||W||^2 (T = W on entry: S_0 = 0)
+  LRS_CUDA(cudaMemcpyAsync(h->t, w, numel * 8, cudaMemcpyDeviceToDevice, s));
+  const unsigned nb_fin = static_cast<unsigned>((numel + kDThreads - 1) / kDThreads);
+  {
+    // residual mass of "no selection" on W itself: sum W^2 through the finish kernel's
+    // reduction with an all-false selection (st = max key, nothing taken)
+    const unsigned long long init[4] = {~0ull, ~0ull, 0ull, 0ull};
+    LRS_CUDA(cudaMemcpyAsync(h->st, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    lrs_select_flags_kernel<<<nb_fin, kDThreads, 0, s>>>(w, numel, h->st, h->gt, h->eq);
+    lrs_decomp_finish_kernel<<<nb_fin, kDThreads, 0, s>>>(w, w, numel, h->st, h->gt, h->eq, h->eq_pre, h->sums_a,
+                                                           h->sel, h->rsd, h->eps_part);
+    // (rsd scratch receives W here; overwritten by the first residual)
+    LRS_CUDA(cudaGetLastError());
+    lrs_decomp_eps_kernel<<<1, kDThreads, 0, s>>>(h->eps_part, static_cast<int>(nb_fin), h->scal);
+  }
+  double wn2 = 0.0;
+  LRS_CUDA(cudaMemcpyAsync(&wn2, h->scal, 8, cudaMemcpyDeviceToHost, s));
+  LRS_CUDA(cudaStreamSynchronize(s));
+  *wn2_out = wn2;
+  return LRS_OK;
+}
+
+// S = P_c(Rsd) (exact radix select + ordered compaction into s_idx / s_val), T = W - S, and the
+// residual mass sum (W - L - S)^2 into scal[1] -- PAPER.md:144-146 (h->rsd holds W - L)
+lrs_status dc_project(lrs_decomp* h, const double* w, long long nnz, int64_t* s_idx, double* s_val, cudaStream_t s) {
+  const long long numel = h->numel;
+  const unsigned nb_fin = static_cast<unsigned>((numel + kDThreads - 1) / kDThreads);
+  const unsigned nb_scan = static_cast<unsigned>((numel + kScanBlock - 1) / kScanBlock);
+  {
+    unsigned long long init[4] = {0ull, 0ull, static_cast<unsigned long long>(nnz), 0ull};
+    if (nnz == 0) init[0] = init[1] = ~0ull;  // nothing above the maximal key, no ties taken
+    LRS_CUDA(cudaMemcpyAsync(h->st, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    if (nnz > 0) {
+      LRS_CUDA(cudaMemsetAsync(h->hist, 0, 256 * 4, s));
+      const unsigned gb = static_cast<unsigned>(std::min<long long>((numel + kDThreads - 1) / kDThreads, 8LL * h->sms));
+      for (int shift = 56; shift >= 0; shift -= 8) {
+        lrs_radix_hist_kernel<<<gb, kDThreads, 0, s>>>(h->rsd, numel, h->st, shift, h->hist);
+        lrs_radix_pick_kernel<<<1, 1, 0, s>>>(h->st, shift, h->hist);
+      }
+    }
+    lrs_select_flags_kernel<<<nb_fin, kDThreads, 0, s>>>(h->rsd, numel, h->st, h->gt, h->eq);
+    lrs_scan_block_kernel<<<nb_scan, 256, 0, s>>>(h->eq, numel, h->eq_pre, h->sums_a);
+    lrs_scan_sums_kernel<<<1, 32, 0, s>>>(h->sums_a, static_cast<int>(nb_scan));
+    lrs_decomp_finish_kernel<<<nb_fin, kDThreads, 0, s>>>(w, h->rsd, numel, h->st, h->gt, h->eq, h->eq_pre,
+                                                           h->sums_a, h->sel, h->t, h->eps_part);
+    lrs_decomp_eps_kernel<<<1, kDThreads, 0, s>>>(h->eps_part, static_cast<int>(nb_fin), h->scal + 1);
+    if (nnz > 0) {
+      lrs_scan_block_kernel<<<nb_scan, 256, 0, s>>>(h->sel, numel, h->sel_pre, h->sums_b);
+      lrs_scan_sums_kernel<<<1, 32, 0, s>>>(h->sums_b, static_cast<int>(nb_scan));
+      lrs_decomp_compact_kernel<<<nb_fin, kDThreads, 0, s>>>(h->rsd, numel, h->sel, h->sel_pre, h->sums_b,
+                                                              reinterpret_cast<long long*>(s_idx), s_val);
+    }
+    LRS_CUDA(cudaGetLastError());
+  }
+  return LRS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -215,25 +275,8 @@ lrs_status lrs_decomp_run(lrs_decomp* h, const double* w, double* f0, double* f1
   double* f[4] = {f0, f1, f2, f3};
   DcTimer tm{h, s};
   lrs_status st;
-  // ||W||^2 (T = W on entry: S_0 = 0)
-  LRS_CUDA(cudaMemcpyAsync(h->t, w, numel * 8, cudaMemcpyDeviceToDevice, s));
-  const unsigned nb_fin = static_cast<unsigned>((numel + kDThreads - 1) / kDThreads);
-  const unsigned nb_scan = static_cast<unsigned>((numel + kScanBlock - 1) / kScanBlock);
-  {
-    // residual mass of "no selection" on W itself: sum W^2 through the finish kernel's
-    // reduction with an all-false selection (st = max key, nothing taken)
-    const unsigned long long init[4] = {~0ull, ~0ull, 0ull, 0ull};
-    LRS_CUDA(cudaMemcpyAsync(h->st, init, sizeof(init), cudaMemcpyHostToDevice, s));
-    lrs_select_flags_kernel<<<nb_fin, kDThreads, 0, s>>>(w, numel, h->st, h->gt, h->eq);
-    lrs_decomp_finish_kernel<<<nb_fin, kDThreads, 0, s>>>(w, w, numel, h->st, h->gt, h->eq, h->eq_pre, h->sums_a,
-                                                           h->sel, h->rsd, h->eps_part);
-    // (rsd scratch receives W here; overwritten by the first residual)
-    LRS_CUDA(cudaGetLastError());
-    lrs_decomp_eps_kernel<<<1, kDThreads, 0, s>>>(h->eps_part, static_cast<int>(nb_fin), h->scal);
-  }
   double wn2 = 0.0;
-  LRS_CUDA(cudaMemcpyAsync(&wn2, h->scal, 8, cudaMemcpyDeviceToHost, s));
-  LRS_CUDA(cudaStreamSynchronize(s));
+  if ((st = dc_begin(h, w, s, &wn2)) != LRS_OK) return st;
   if (wn2 == 0.0) {
     // a zero W gives zero factors, an empty S and eps 0
     for (int m = 0; m < 4; ++m) LRS_CUDA(cudaMemsetAsync(f[m], 0, static_cast<size_t>(p.dims[m]) * r * 8, s));
@@ -323,32 +366,7 @@ lrs_status lrs_decomp_run(lrs_decomp* h, const double* w, double* f0, double* f1
     if ((st = tm.end()) != LRS_OK) return st;
     // ---------------------------------------------------------- 3. S = P_c(Rsd), 4. T, eps
     if ((st = tm.begin(3)) != LRS_OK) return st;
-    {
-      unsigned long long init[4] = {0ull, 0ull, static_cast<unsigned long long>(nnz), 0ull};
-      if (nnz == 0) init[0] = init[1] = ~0ull;  // nothing above the maximal key, no ties taken
-      LRS_CUDA(cudaMemcpyAsync(h->st, init, sizeof(init), cudaMemcpyHostToDevice, s));
-      if (nnz > 0) {
-        LRS_CUDA(cudaMemsetAsync(h->hist, 0, 256 * 4, s));
-        const unsigned gb = static_cast<unsigned>(std::min<long long>((numel + kDThreads - 1) / kDThreads, 8LL * h->sms));
-        for (int shift = 56; shift >= 0; shift -= 8) {
-          lrs_radix_hist_kernel<<<gb, kDThreads, 0, s>>>(h->rsd, numel, h->st, shift, h->hist);
-          lrs_radix_pick_kernel<<<1, 1, 0, s>>>(h->st, shift, h->hist);
-        }
-      }
-      lrs_select_flags_kernel<<<nb_fin, kDThreads, 0, s>>>(h->rsd, numel, h->st, h->gt, h->eq);
-      lrs_scan_block_kernel<<<nb_scan, 256, 0, s>>>(h->eq, numel, h->eq_pre, h->sums_a);
-      lrs_scan_sums_kernel<<<1, 32, 0, s>>>(h->sums_a, static_cast<int>(nb_scan));
-      lrs_decomp_finish_kernel<<<nb_fin, kDThreads, 0, s>>>(w, h->rsd, numel, h->st, h->gt, h->eq, h->eq_pre,
-                                                             h->sums_a, h->sel, h->t, h->eps_part);
-      lrs_decomp_eps_kernel<<<1, kDThreads, 0, s>>>(h->eps_part, static_cast<int>(nb_fin), h->scal + 1);
-      if (nnz > 0) {
-        lrs_scan_block_kernel<<<nb_scan, 256, 0, s>>>(h->sel, numel, h->sel_pre, h->sums_b);
-        lrs_scan_sums_kernel<<<1, 32, 0, s>>>(h->sums_b, static_cast<int>(nb_scan));
-        lrs_decomp_compact_kernel<<<nb_fin, kDThreads, 0, s>>>(h->rsd, numel, h->sel, h->sel_pre, h->sums_b,
-                                                                reinterpret_cast<long long*>(s_idx), s_val);
-      }
-      LRS_CUDA(cudaGetLastError());
-    }
+    if ((st = dc_project(h, w, nnz, s_idx, s_val, s)) != LRS_OK) return st;
     if ((st = tm.end()) != LRS_OK) return st;
     double rem = 0.0;
     LRS_CUDA(cudaMemcpyAsync(&rem, h->scal + 1, 8, cudaMemcpyDeviceToHost, s));
@@ -404,6 +422,204 @@ lrs_status lrs_decomp_stage_times(lrs_decomp* h, float* ms, int64_t* counts, int
       r.count = 0;
     }
   return LRS_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------ Tucker-2
+// include/lrs_conv.h "Tucker-2 decomposition"; oracle/lrs_decomp.py decompose_lrs_tucker2.
+struct lrs_tucker2 {
+  lrs_decomp* d = nullptr;  // W's shape: T, Rsd, the projection and the Jacobi workspaces
+  lrs_tucker2_params prm{};
+  double *z1 = nullptr, *z2 = nullptr, *x = nullptr, *y = nullptr, *c = nullptr, *p = nullptr, *hh = nullptr;
+};
+
+namespace {
+
+void t2_gemm(const double* a, const double* b, double* c, const double* sub, int m, int n, int k, int batch,
+             long long sam, long long sak, long long sab, long long sbk, long long sbn, long long sbb, long long scm,
+             long long scn, long long scb, cudaStream_t s) {
+  DgemmParams g{a, b, c, sub, m, n, k, sam, sak, sab, sbk, sbn, sbb, scm, scn, scb};
+  lrs_dgemm_kernel<<<dim3(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((m + 63) / 64),
+                          static_cast<unsigned>(batch)),
+                     256, 0, s>>>(g);
+}
+
+// U <- orth(Z Z^T U) `inner` times: Z [rows][cols] row-major, U [rows][r] (in place);
+// orth(Y) = Y (Y^T Y)^-1/2 by the eigen path of the one-CTA pseudo-inverse kernel
+lrs_status t2_subspace(lrs_tucker2* h, const double* z, int rows, int cols, double* u, int r, double* qt, bool warm,
+                       cudaStream_t s) {
+  lrs_decomp* d = h->d;
+  for (int i = 0; i < h->prm.inner; ++i) {
+    // X = Z^T U [cols][r];  Y = Z X [rows][r]
+    t2_gemm(z, u, h->x, nullptr, cols, r, rows, 1, 1, cols, 0, r, 1, 0, r, 1, 0, s);
+    t2_gemm(z, h->x, h->y, nullptr, rows, r, cols, 1, cols, 1, 0, r, 1, 0, r, 1, 0, s);
+    lrs_gram_kernel<<<r, 256, 0, s>>>(h->y, rows, r, h->c);
+    PinvParams pp{};
+    pp.single = h->c;
+    pp.inv_sqrt = 1;
+    pp.r = r;
+    pp.rp = (r + 1) & ~1;
+    pp.rcond = h->prm.rcond;
+    pp.a = d->ja;
+    pp.v = d->jv;
+    pp.p = h->p;
+    pp.sweeps = d->sweeps;
+    pp.a_smem = d->pinv_smem ? 1 : 0;
+    pp.qt = qt;
+    pp.warm = (warm || i > 0) && d->pinv_smem ? 1 : 0;
+    lrs_sym_pinv_kernel<<<1, kJThreads, d->pinv_smem, s>>>(pp);
+    lrs_cp_update_kernel<<<static_cast<unsigned>((static_cast<long long>(rows) * r + 255) / 256), 256, 0, s>>>(
+        h->y, h->p, rows, r, u);
+    LRS_CUDA(cudaGetLastError());
+  }
+  return LRS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lrs_status lrs_tucker2_destroy(lrs_tucker2* h) {
+  if (!h) return LRS_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (h->d) cudaSetDevice(h->d->device);
+  for (double* b : {h->z1, h->z2, h->x, h->y, h->c, h->p, h->hh})
+    if (b) cudaFree(b);
+  lrs_decomp_destroy(h->d);
+  cudaSetDevice(prev);
+  delete h;
+  return LRS_OK;
+}
+
+lrs_status lrs_tucker2_create(const lrs_tucker2_params* p, int device, lrs_tucker2** out) {
+  if (!out || !p) return fail(LRS_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  if (p->r1 < 1 || p->r2 < 1) return fail(LRS_ERR_INVALID_ARGUMENT, "r1, r2 must be >= 1");
+  if (p->inner < 1) return fail(LRS_ERR_INVALID_ARGUMENT, "inner < 1");
+  for (int i = 0; i < 4; ++i)
+    if (p->dims[i] <= 0) return fail(LRS_ERR_INVALID_ARGUMENT, "dims must be > 0");
+  if (p->r1 > p->dims[0] || p->r2 > p->dims[1]) return fail(LRS_ERR_INVALID_ARGUMENT, "r1 > dims[0] or r2 > dims[1]");
+  lrs_decomp_params dp{};
+  for (int i = 0; i < 4; ++i) dp.dims[i] = p->dims[i];
+  dp.rank = std::max(p->r1, p->r2);
+  dp.cardinality = p->cardinality;
+  dp.max_iters = p->max_iters;
+  dp.tol = p->tol;
+  dp.rcond = p->rcond;
+  lrs_decomp* d = nullptr;
+  lrs_status st = lrs_decomp_create(&dp, device, &d);  // validates the rest (rank <= 256, sizes, device)
+  if (st != LRS_OK) return st;
+  DeviceGuard dg;
+  LRS_CUDA(dg.enter(device));
+  lrs_tucker2* h = new lrs_tucker2();
+  h->d = d;
+  h->prm = *p;
+  const long long q = d->q, cin = p->dims[0], cout = p->dims[1], rm = dp.rank;
+  const long long zc = std::max(p->r2 * q, p->r1 * q);
+  const size_t sizes[7] = {static_cast<size_t>(cin * p->r2 * q), static_cast<size_t>(cout * p->r1 * q),
+                           static_cast<size_t>(zc * rm), static_cast<size_t>(std::max(cin, cout) * rm),
+                           static_cast<size_t>(rm * rm), static_cast<size_t>(rm * rm),
+                           static_cast<size_t>(p->r1 * cout * q)};
+  double** bufs[7] = {&h->z1, &h->z2, &h->x, &h->y, &h->c, &h->p, &h->hh};
+  for (int i = 0; i < 7; ++i)
+    if ((st = dc_alloc(reinterpret_cast<void**>(bufs[i]), sizes[i] * 8)) != LRS_OK) {
+      lrs_tucker2_destroy(h);
+      return st;
+    }
+  *out = h;
+  return LRS_OK;
+}
+
+lrs_status lrs_tucker2_run(lrs_tucker2* h, const double* w, double* u_in, double* u_out, double* core,
+                           int64_t* s_idx, double* s_val, int64_t* s_count, double* eps_hist, int32_t* iters_done,
+                           void* stream_) {
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (!w || !u_in || !u_out || !core || !eps_hist || !iters_done || !s_count)
+    return fail(LRS_ERR_INVALID_ARGUMENT, "NULL argument");
+  lrs_decomp* d = h->d;
+  if (d->nnz > 0 && (!s_idx || !s_val)) return fail(LRS_ERR_INVALID_ARGUMENT, "s_idx / s_val is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream_);
+  DeviceGuard dg;
+  LRS_CUDA(dg.enter(d->device));
+  const lrs_tucker2_params& p = h->prm;
+  const int cin = p.dims[0], cout = p.dims[1], r1 = p.r1, r2 = p.r2, q = d->q;
+  const long long nnz = d->nnz;
+  DcTimer tm{d, s};
+  lrs_status st;
+  double wn2 = 0.0;
+  if ((st = dc_begin(d, w, s, &wn2)) != LRS_OK) return st;
+  if (wn2 == 0.0) {
+    LRS_CUDA(cudaMemsetAsync(u_in, 0, static_cast<size_t>(cin) * r1 * 8, s));
+    LRS_CUDA(cudaMemsetAsync(u_out, 0, static_cast<size_t>(cout) * r2 * 8, s));
+    LRS_CUDA(cudaMemsetAsync(core, 0, static_cast<size_t>(r1) * r2 * q * 8, s));
+    eps_hist[0] = 0.0;
+    *iters_done = 1;
+    *s_count = 0;
+    LRS_CUDA(cudaStreamSynchronize(s));
+    return LRS_OK;
+  }
+  const long long jq = static_cast<long long>(cout) * q;  // T's row stride (input channel)
+  int it = 0;
+  for (; it < p.max_iters; ++it) {
+    // ------------------------------------------------ 1. HOOI sweep on T = W - S (stage 0: products, 1: orth)
+    if ((st = tm.begin(0)) != LRS_OK) return st;
+    // Z1[c][b][t] = sum_j T[c][j][t] U_out[j][b]   (batch t)
+    t2_gemm(d->t, u_out, h->z1, nullptr, cin, r2, cout, q, jq, q, 1, r2, 1, 0, static_cast<long long>(r2) * q, q, 1, s);
+    if ((st = tm.end()) != LRS_OK) return st;
+    if ((st = tm.begin(1)) != LRS_OK) return st;
+    if ((st = t2_subspace(h, h->z1, cin, r2 * q, u_in, r1, d->qt[0], it > 0, s)) != LRS_OK) return st;
+    if ((st = tm.end()) != LRS_OK) return st;
+    if ((st = tm.begin(0)) != LRS_OK) return st;
+    // Z2[j][a][t] = sum_c T[c][j][t] U_in[c][a]   (batch t)
+    t2_gemm(d->t, u_in, h->z2, nullptr, cout, r1, cin, q, q, jq, 1, r1, 1, 0, static_cast<long long>(r1) * q, q, 1, s);
+    if ((st = tm.end()) != LRS_OK) return st;
+    if ((st = tm.begin(1)) != LRS_OK) return st;
+    if ((st = t2_subspace(h, h->z2, cout, r1 * q, u_out, r2, d->qt[1], it > 0, s)) != LRS_OK) return st;
+    if ((st = tm.end()) != LRS_OK) return st;
+    if ((st = tm.begin(0)) != LRS_OK) return st;
+    // G[a][b][t] = sum_j Z2[j][a][t] U_out[j][b]   (batch t)
+    t2_gemm(h->z2, u_out, core, nullptr, r1, r2, cout, q, q, static_cast<long long>(r1) * q, 1, r2, 1, 0,
+            static_cast<long long>(r2) * q, q, 1, s);
+    if ((st = tm.end()) != LRS_OK) return st;
+    // ------------------------------------------------ 2. Rsd = W - L,  L = U_in (G x_out U_out)
+    if ((st = tm.begin(2)) != LRS_OK) return st;
+    // H[a][j][t] = sum_b G[a][b][t] U_out[j][b]   (batch t)
+    t2_gemm(core, u_out, h->hh, nullptr, r1, cout, r2, q, static_cast<long long>(r2) * q, q, 1, 1, r2, 0, jq, q, 1, s);
+    // Rsd[c][(j, t)] = W[c][(j, t)] - sum_a U_in[c][a] H[a][(j, t)]
+    t2_gemm(u_in, h->hh, d->rsd, w, cin, static_cast<int>(jq), r1, 1, r1, 1, 0, jq, 1, 0, jq, 1, 0, s);
+    LRS_CUDA(cudaGetLastError());
+    if ((st = tm.end()) != LRS_OK) return st;
+    // ------------------------------------------------ 3. S = P_c(Rsd), T = W - S, eps
+    if ((st = tm.begin(3)) != LRS_OK) return st;
+    if ((st = dc_project(d, w, nnz, s_idx, s_val, s)) != LRS_OK) return st;
+    if ((st = tm.end()) != LRS_OK) return st;
+    double rem = 0.0;
+    LRS_CUDA(cudaMemcpyAsync(&rem, d->scal + 1, 8, cudaMemcpyDeviceToHost, s));
+    LRS_CUDA(cudaStreamSynchronize(s));
+    eps_hist[it] = std::sqrt(rem / wn2);
+    if (it > 0 && (eps_hist[it - 1] - eps_hist[it]) < p.tol) {
+      ++it;
+      break;
+    }
+  }
+  *iters_done = it;
+  *s_count = nnz;
+  return LRS_OK;
+}
+
+int64_t lrs_tucker2_nnz(const lrs_tucker2* h) { return h ? h->d->nnz : -1; }
+
+lrs_status lrs_tucker2_set_timing(lrs_tucker2* h, int32_t enable) {
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  return lrs_decomp_set_timing(h->d, enable);
+}
+
+lrs_status lrs_tucker2_stage_times(lrs_tucker2* h, float* ms, int64_t* counts, int32_t max_stages, int32_t* n_stages,
+                                   int32_t reset) {
+  if (!h) return fail(LRS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  return lrs_decomp_stage_times(h->d, ms, counts, max_stages, n_stages, reset);
 }
 
 }  // extern "C"

@@ -35,7 +35,9 @@ EXPORTED = ("lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs
             "lrs_conv_bwd_launches", "lrs_conv_bwd_destroy", "lrs_conv_bwd_set_timing",
             "lrs_conv_bwd_stage_times", "lrs_conv_bwd_stage_name",
             "lrs_decomp_create", "lrs_decomp_run", "lrs_decomp_nnz", "lrs_decomp_launches_per_iteration", "lrs_decomp_set_timing",
-            "lrs_decomp_stage_times", "lrs_decomp_destroy")
+            "lrs_decomp_stage_times", "lrs_decomp_destroy",
+            "lrs_tucker2_create", "lrs_tucker2_run", "lrs_tucker2_nnz", "lrs_tucker2_set_timing",
+            "lrs_tucker2_stage_times", "lrs_tucker2_destroy")
 
 
 class LrsError(RuntimeError):
@@ -68,6 +70,12 @@ class lrs_conv_desc(ctypes.Structure):
 class lrs_decomp_params(ctypes.Structure):
     _fields_ = [("dims", ctypes.c_int32 * 4), ("rank", ctypes.c_int32), ("cardinality", ctypes.c_double),
                 ("max_iters", ctypes.c_int32), ("tol", ctypes.c_double), ("rcond", ctypes.c_double)]
+
+
+class lrs_tucker2_params(ctypes.Structure):
+    _fields_ = [("dims", ctypes.c_int32 * 4), ("r1", ctypes.c_int32), ("r2", ctypes.c_int32),
+                ("cardinality", ctypes.c_double), ("max_iters", ctypes.c_int32), ("tol", ctypes.c_double),
+                ("rcond", ctypes.c_double), ("inner", ctypes.c_int32)]
 
 
 class lrs_conv_grads(ctypes.Structure):
@@ -146,6 +154,18 @@ def load_library(path: str = LIB_PATH):
     lib.lrs_decomp_destroy.argtypes = [P]
     for name in ("lrs_decomp_create", "lrs_decomp_run", "lrs_decomp_set_timing", "lrs_decomp_stage_times",
                  "lrs_decomp_destroy"):
+        getattr(lib, name).restype = ctypes.c_int
+    lib.lrs_tucker2_create.argtypes = [ctypes.POINTER(lrs_tucker2_params), ctypes.c_int, ctypes.POINTER(P)]
+    lib.lrs_tucker2_run.argtypes = [P, P, P, P, P, P, P, ctypes.POINTER(ctypes.c_int64),
+                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32), P]
+    lib.lrs_tucker2_nnz.argtypes = [P]
+    lib.lrs_tucker2_nnz.restype = ctypes.c_int64
+    lib.lrs_tucker2_set_timing.argtypes = [P, ctypes.c_int32]
+    lib.lrs_tucker2_stage_times.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64),
+                                            ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]
+    lib.lrs_tucker2_destroy.argtypes = [P]
+    for name in ("lrs_tucker2_create", "lrs_tucker2_run", "lrs_tucker2_set_timing", "lrs_tucker2_stage_times",
+                 "lrs_tucker2_destroy"):
         getattr(lib, name).restype = ctypes.c_int
     for name in ("lrs_conv_debug_trace", "lrs_conv_create", "lrs_conv_forward", "lrs_conv_forward_host", "lrs_conv_destroy",
                  "lrs_conv_output_shape", "lrs_conv_set_timing", "lrs_conv_stage_times",
@@ -665,6 +685,73 @@ class LrsDecomp:
     def close(self) -> None:
         if getattr(self, "handle", None):
             _check(load_library().lrs_decomp_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LrsTucker2Decomp:
+    """The low-rank + sparse decomposition with L in Tucker-2 form on the GPU (include/lrs_conv.h
+    "Tucker-2 decomposition"): run(w, u_in, u_out) takes W (device fp64 [Cin, Cout, kh, kw]) and
+    the initial channel bases (device fp64 [Cin, r1] / [Cout, r2]; overwritten with the
+    orthonormal result) and returns (core [r1, r2, kh, kw], s_idx, s_val, eps history).  The
+    layer's u_out is the returned u_out transposed."""
+
+    STAGES = ("mode_products", "subspace_orth", "residual", "project")
+
+    def __init__(self, dims, r1: int, r2: int, cardinality: float, max_iters: int = 100, tol: float = 1e-6,
+                 rcond: float = 1e-10, inner: int = 1, device: int = 0):
+        import torch
+        self.torch = torch
+        self.dims = tuple(int(d) for d in dims)
+        self.r1, self.r2, self.max_iters, self.device = int(r1), int(r2), int(max_iters), device
+        prm = lrs_tucker2_params(dims=(ctypes.c_int32 * 4)(*self.dims), r1=self.r1, r2=self.r2,
+                                 cardinality=float(cardinality), max_iters=self.max_iters, tol=float(tol),
+                                 rcond=float(rcond), inner=int(inner))
+        h = ctypes.c_void_p()
+        _check(load_library().lrs_tucker2_create(ctypes.byref(prm), device, ctypes.byref(h)))
+        self.handle = h.value
+        self.nnz = int(load_library().lrs_tucker2_nnz(self.handle))
+
+    def run(self, w, u_in, u_out, stream=None):
+        torch = self.torch
+
+        def check(t, shape, name):
+            if t.dtype != torch.float64 or not t.is_cuda or tuple(t.shape) != shape or not t.is_contiguous():
+                raise ValueError(f"{name}: expected a contiguous fp64 CUDA tensor of shape {shape}")
+        check(w, self.dims, "w")
+        check(u_in, (self.dims[0], self.r1), "u_in")
+        check(u_out, (self.dims[1], self.r2), "u_out")
+        dev = w.device
+        core = torch.empty((self.r1, self.r2) + self.dims[2:], dtype=torch.float64, device=dev)
+        idx = torch.empty(max(self.nnz, 1), dtype=torch.int64, device=dev)
+        val = torch.empty(max(self.nnz, 1), dtype=torch.float64, device=dev)
+        eps = (ctypes.c_double * self.max_iters)()
+        cnt = ctypes.c_int64()
+        its = ctypes.c_int32()
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        _check(load_library().lrs_tucker2_run(self.handle, w.data_ptr(), u_in.data_ptr(), u_out.data_ptr(),
+                                              core.data_ptr(), idx.data_ptr(), val.data_ptr(), ctypes.byref(cnt), eps,
+                                              ctypes.byref(its), s.cuda_stream))
+        return core, idx[:cnt.value], val[:cnt.value], [eps[i] for i in range(its.value)]
+
+    def set_timing(self, on: bool) -> None:
+        _check(load_library().lrs_tucker2_set_timing(self.handle, 1 if on else 0))
+
+    def stage_times(self, reset: bool = True):
+        ms = (ctypes.c_float * 4)()
+        cnt = (ctypes.c_int64 * 4)()
+        ns = ctypes.c_int32()
+        _check(load_library().lrs_tucker2_stage_times(self.handle, ms, cnt, 4, ctypes.byref(ns), 1 if reset else 0))
+        return {self.STAGES[i]: (ms[i], cnt[i]) for i in range(ns.value)}
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _check(load_library().lrs_tucker2_destroy(self.handle))
             self.handle = None
 
     def __del__(self):

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_functions():
     src = open(os.path.join(ROOT, "include", "lrs_conv.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:lrs_status|const char \*|int32_t|int64_t)\s*\**\s*(lrs_(?:conv|sparse|decomp)_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:lrs_status|const char \*|int32_t|int64_t)\s*\**\s*(lrs_(?:conv|sparse|decomp|tucker2)_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_header_symbol():
@@ -214,3 +214,24 @@ def test_decomp_create_validation_before_any_device_call():
     assert status(rank=257) == B.LRS_ERR_UNSUPPORTED
     assert status(dims=(8, 8, 9, 3)) == B.LRS_ERR_UNSUPPORTED
     assert status() == B.LRS_ERR_CUDA
+
+
+def test_tucker2_create_validation_before_any_device_call():
+    lib = P.load_library()
+
+    def status(**kw):
+        a = dict(dims=(8, 8, 3, 3), r1=4, r2=3, cardinality=0.01, max_iters=5, tol=1e-6, rcond=1e-10, inner=1)
+        a.update(kw)
+        prm = B.lrs_tucker2_params(dims=(ctypes.c_int32 * 4)(*a["dims"]), r1=a["r1"], r2=a["r2"],
+                                   cardinality=a["cardinality"], max_iters=a["max_iters"], tol=a["tol"],
+                                   rcond=a["rcond"], inner=a["inner"])
+        h = ctypes.c_void_p()
+        return lib.lrs_tucker2_create(ctypes.byref(prm), 0, ctypes.byref(h))
+
+    assert status(r1=0) == B.LRS_ERR_INVALID_ARGUMENT
+    assert status(r2=9) == B.LRS_ERR_INVALID_ARGUMENT  # r2 > Cout
+    assert status(inner=0) == B.LRS_ERR_INVALID_ARGUMENT
+    assert status(cardinality=-0.1) == B.LRS_ERR_INVALID_ARGUMENT
+    assert status(dims=(300, 300, 3, 3), r1=257, r2=4) == B.LRS_ERR_UNSUPPORTED
+    assert status() == B.LRS_ERR_CUDA
+    assert lib.lrs_tucker2_destroy(None) == B.LRS_OK

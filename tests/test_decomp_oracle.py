@@ -131,3 +131,53 @@ def test_decompose_degenerate_cases():
     z = np.zeros(dims)
     f, (idx, _), hist = D.decompose_lrs(z, D.svd_init(z + 1.0, 2), 0.01)  # SPEC.md:163 zero W
     assert idx.size == 0 and hist == [0.0] and all(not np.any(x) for x in f)
+
+
+def rand_tucker2(rng, dims, r1, r2):
+    u = np.linalg.qr(rng.standard_normal((dims[0], r1)))[0]
+    v = np.linalg.qr(rng.standard_normal((dims[1], r2)))[0]
+    g = rng.standard_normal((r1, r2) + dims[2:])
+    return u, v, g
+
+
+def test_lowdin_is_the_closest_orthonormal_basis():
+    """orth_lowdin(Y) = U V^T of the SVD Y = U s V^T (numpy's SVD: the polar factor)."""
+    y = np.random.default_rng(20).standard_normal((9, 4))
+    u, _, vt = np.linalg.svd(y, full_matrices=False)
+    q = D.orth_lowdin(y)
+    assert np.allclose(q, u @ vt, atol=1e-12)
+    assert np.allclose(q.T @ q, np.eye(4), atol=1e-12)
+
+
+def test_hooi_recovers_a_planted_tucker2_tensor():
+    """An exact Tucker-2 tensor of ranks (3, 2) is reproduced to round-off (cardinality 0),
+    and the factors span the same subspaces as numpy's SVD of the unfoldings (library pin)."""
+    rng = np.random.default_rng(21)
+    dims = (12, 10, 3, 3)
+    u, v, g = rand_tucker2(rng, dims, 3, 2)
+    w = D.tucker2_reconstruct(u, g, v)
+    (ui, uo, gg), (idx, _), hist = D.decompose_lrs_tucker2(w, rng.standard_normal((12, 3)),
+                                                          rng.standard_normal((10, 2)), 0.0, max_iters=30, tol=-1)
+    assert hist[-1] < 1e-10 and idx.size == 0
+    su = np.linalg.svd(w.reshape(12, -1), full_matrices=False)[0][:, :3]
+    sv = np.linalg.svd(np.moveaxis(w, 1, 0).reshape(10, -1), full_matrices=False)[0][:, :2]
+    assert np.allclose(ui @ ui.T, su @ su.T, atol=1e-8)
+    assert np.allclose(uo @ uo.T, sv @ sv.T, atol=1e-8)
+
+
+def test_tucker2_decompose_monotone_and_spikes():
+    """W = Tucker-2 (4, 4) + 1 % spikes of magnitude 10: eps non-increasing and the spikes
+    recovered as S's support."""
+    rng = np.random.default_rng(22)
+    dims = (16, 14, 3, 3)
+    u, v, g = rand_tucker2(rng, dims, 4, 4)
+    low = D.tucker2_reconstruct(u, g * 3.0, v)
+    n = int(round(0.01 * low.size))
+    spikes = np.sort(rng.choice(low.size, n, replace=False))
+    w = low.copy()
+    w.flat[spikes] += 10.0 * np.sign(rng.standard_normal(n))
+    (ui, uo, gg), (idx, _), hist = D.decompose_lrs_tucker2(w, rng.standard_normal((16, 4)),
+                                                          rng.standard_normal((14, 4)), 0.01, max_iters=60, tol=-1)
+    assert all(b <= a + 1e-9 for a, b in zip(hist, hist[1:]))
+    assert hist[-1] < 1e-6
+    assert np.array_equal(idx, spikes)

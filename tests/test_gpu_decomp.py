@@ -171,3 +171,105 @@ def test_decomposed_weight_runs_as_a_cp_layer():
     ref = O.conv_direct(x.astype(np.float64), l + s_dense, 1, 1)
     e = rel(yg.cpu().numpy(), ref)
     assert e < 1e-5, e
+
+
+# ------------------------------------------------------------------ Tucker-2 form (lrs_tucker2_*)
+
+def run_t2(w, u_in0, u_out0, card, iters, tol=0.0, inner=1):
+    from paper_2006_06443_b200 import LrsTucker2Decomp
+    dc = LrsTucker2Decomp(w.shape, u_in0.shape[1], u_out0.shape[1], card, max_iters=iters, tol=tol, inner=inner)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float64)).cuda()
+    wd, ui, uo = dev(w), dev(u_in0), dev(u_out0)
+    core, idx, val, eps = dc.run(wd, ui, uo)
+    torch.cuda.synchronize()
+    return ui.cpu().numpy(), uo.cpu().numpy(), core.cpu().numpy(), idx.cpu().numpy(), val.cpu().numpy(), eps
+
+
+@pytest.mark.parametrize("inner", [1, 2])
+@pytest.mark.parametrize("planted,r1,r2", [(8, 8, 8), (6, 8, 10)])
+def test_tucker2_iterations_match_oracle(inner, planted, r1, r2):
+    """At the planted ranks (a wide spectral gap) the factors themselves match; over-ranked, the
+    extra directions lie in the noise spectrum (tiny gaps amplify rounding), so the unique
+    quantities are compared: eps, S and L = U_in G U_out^T."""
+    cfg = workloads.DecompConfig("t2", (48, 40, 3, 3), planted, 0, 0.01, seed=4)
+    w, ui0, uo0 = workloads.generate_decomp_tucker2(cfg, r1, r2)
+    ui, uo, g, idx, val, eps = run_t2(w, ui0, uo0, cfg.cardinality, 6, inner=inner)
+    (rui, ruo, rg), (ridx, rval), reps = D.decompose_lrs_tucker2(w, ui0, uo0, cfg.cardinality, max_iters=6, tol=0.0,
+                                                                inner=inner)
+    assert len(eps) == len(reps) == 6
+    assert np.allclose(eps, reps, rtol=1e-8, atol=1e-13)
+    assert np.array_equal(idx, ridx)
+    assert rel(val, rval) < 1e-9
+    assert rel(D.tucker2_reconstruct(ui, g, uo), D.tucker2_reconstruct(rui, rg, ruo)) < 1e-8
+    if planted == r1 == r2:
+        assert rel(ui, rui) < 1e-8 and rel(uo, ruo) < 1e-8 and rel(g, rg) < 1e-8
+    # orthonormal bases (Loewdin through the Gram: the error grows with its condition number; the
+    # over-ranked noise directions leave ~1e-8, the oracle's own level)
+    assert np.allclose(ui.T @ ui, np.eye(r1), atol=1e-6) and np.allclose(uo.T @ uo, np.eye(r2), atol=1e-6)
+
+
+def test_tucker2_ragged_shapes_and_1x1():
+    """Shapes off every GEMM tile (Cin 70, Cout 33, ranks 5 / 17, a 1 x 1 and a 5 x 5 kernel)."""
+    for dims, r1, r2 in (((70, 33, 1, 1), 5, 17), ((21, 19, 5, 5), 7, 3)):
+        cfg = workloads.DecompConfig("t2r", dims, 4, 0, 0.02, seed=6)
+        w, ui0, uo0 = workloads.generate_decomp_tucker2(cfg, r1, r2)
+        ui, uo, g, idx, val, eps = run_t2(w, ui0, uo0, cfg.cardinality, 4)
+        (rui, ruo, rg), (ridx, _), reps = D.decompose_lrs_tucker2(w, ui0, uo0, cfg.cardinality, max_iters=4, tol=0.0)
+        assert np.allclose(eps, reps, rtol=1e-8, atol=1e-13), dims
+        assert np.array_equal(idx, ridx), dims
+        assert rel(D.tucker2_reconstruct(ui, g, uo), D.tucker2_reconstruct(rui, rg, ruo)) < 1e-8, dims
+
+
+def test_tucker2_full_size_c3_weight():
+    """The C3 weight shape (512 x 512 x 3 x 3) at the north star's Tucker ranks 128 / 128, c = 1 %:
+    three sweeps against the oracle."""
+    cfg = workloads.DECOMP_CONFIGS["c3_decomp"]
+    w, ui0, uo0 = workloads.generate_decomp_tucker2(cfg, 128, 128)
+    ui, uo, g, idx, val, eps = run_t2(w, ui0, uo0, cfg.cardinality, 3)
+    (rui, ruo, rg), (ridx, _), reps = D.decompose_lrs_tucker2(w, ui0, uo0, cfg.cardinality, max_iters=3, tol=0.0)
+    assert np.allclose(eps, reps, rtol=1e-8)
+    assert np.array_equal(idx, ridx)
+    assert rel(D.tucker2_reconstruct(ui, g, uo), D.tucker2_reconstruct(rui, rg, ruo)) < 1e-8
+
+
+def test_tucker2_determinism_stopping_and_zero_w():
+    cfg = workloads.DecompConfig("t2d", (32, 24, 3, 3), 4, 0, 0.02, seed=3)
+    w, ui0, uo0 = workloads.generate_decomp_tucker2(cfg, 6, 6)
+    a = run_t2(w, ui0, uo0, cfg.cardinality, 100, tol=1e-6)
+    b = run_t2(w, ui0, uo0, cfg.cardinality, 100, tol=1e-6)
+    _, _, reps = D.decompose_lrs_tucker2(w, ui0, uo0, cfg.cardinality, max_iters=100, tol=1e-6)
+    assert len(a[5]) == len(reps) < 100
+    for x, y in zip(a[:5], b[:5]):
+        assert np.array_equal(x, y)  # bitwise reproducible
+    z = np.zeros((8, 8, 3, 3))
+    ui, uo, g, idx, val, eps = run_t2(z, np.ones((8, 2)), np.ones((8, 3)), 0.05, 10)
+    assert idx.size == 0 and eps == [0.0] and not np.any(ui) and not np.any(uo) and not np.any(g)
+
+
+def test_tucker2_decomposed_weight_runs_as_the_layer():
+    """Decompose W into Tucker-2 + S on the GPU and run it as the forward's Tucker-2 layer
+    (u_in, core, u_out = U_out^T; S -> CSR by output channel): Y = conv(X, L + S)."""
+    from paper_2006_06443_b200 import LrsConv
+    from oracle import lrs_oracle as O
+    cin, cout, k, r1, r2 = 64, 96, 3, 16, 24
+    cfg = workloads.DecompConfig("t2pipe", (cin, cout, k, k), 10, 0, 0.02, seed=8)
+    w, ui0, uo0 = workloads.generate_decomp_tucker2(cfg, r1, r2)
+    ui, uo, g, idx, val, eps = run_t2(w, ui0, uo0, cfg.cardinality, 15)
+    l = D.tucker2_reconstruct(ui, g, uo)
+    s_dense = D.sparse_dense(w.shape, idx, val)
+    assert abs(np.linalg.norm(w - l - s_dense) / np.linalg.norm(w) - eps[-1]) < 1e-9
+    cc, rem = np.divmod(idx, cout * k * k)
+    j, rem = np.divmod(rem, k * k)
+    y, xx = np.divmod(rem, k)
+    col = (cc * k + y) * k + xx
+    order = np.lexsort((col, j))
+    row_ptr = np.cumsum(np.concatenate([[0], np.bincount(j, minlength=cout)])).astype(np.int64)
+    n, hh = 2, 10
+    layer = LrsConv(n, hh, hh, cin, cout, k, 1, 1, r1, r2, "f32", ui.astype(np.float32), g.astype(np.float32),
+                    np.ascontiguousarray(uo.T).astype(np.float32), row_ptr, col[order].astype(np.int32),
+                    val[order].astype(np.float32))
+    x = np.maximum(np.random.default_rng(3).standard_normal((n, hh, hh, cin)), 0).astype(np.float32)
+    yg = layer(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    ref = O.conv_direct(x.astype(np.float64), l + s_dense, 1, 1)
+    assert rel(yg.cpu().numpy(), ref) < 1e-5

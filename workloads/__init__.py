@@ -366,3 +366,12 @@ def resnet50_decomp_configs(cardinality: float = 0.01):
         r = min(cfg.c_in, cfg.c_out) // 4
         out.append(DecompConfig(f"l{idx}", (cfg.c_in, cfg.c_out, 3, 3), (3 * r) // 4, r, cardinality, seed=1000 + idx))
     return out
+
+
+def generate_decomp_tucker2(cfg: DecompConfig, r1: int, r2: int):
+    """(W, U_in0, U_out0) for a Tucker-2 decomposition run: W of generate_decomp(cfg) (a planted
+    CP tensor is a Tucker-2 tensor of channel ranks <= planted_rank, plus noise and spikes); the
+    initial channel bases N(0,1) [dims[0], r1] and [dims[1], r2] from PCG64(seed + 1000)."""
+    w, _ = generate_decomp(cfg)
+    rng = np.random.Generator(np.random.PCG64(cfg.seed + 1000))
+    return w, rng.standard_normal((cfg.dims[0], r1)), rng.standard_normal((cfg.dims[1], r2))
