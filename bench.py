@@ -71,6 +71,8 @@ def parse():
                          "weak = a full batch per rank")
     ap.add_argument("--replays", type=int, default=10, help="separately timed graph replays (median reported)")
     ap.add_argument("--no-dense", action="store_true", help="skip the cuDNN dense context row")
+    ap.add_argument("--tucker2", action="store_true",
+                    help="with --decompose: L in Tucker-2 form (lrs_tucker2_run, HOOI sweeps) at ranks 128 / 128")
     ap.add_argument("--decompose", action="store_true",
                     help="time the GPU low-rank + sparse decomposition of the layer's weight shape (SURVEY 8f f4)")
     ap.add_argument("--backward", action="store_true",
@@ -1139,6 +1141,8 @@ def main_decomp(args):
     events around one run of K iterations after a W-iteration warm-up run.  Replicas only at
     N > 1 (one decomposition per GPU, no collective)."""
     import torch
+    if args.tucker2:
+        return main_decomp_t2(args)
     if args.impl == "reference":
         return run_reference_decomp(args)
     rank, world, local = dist_env()
@@ -1363,6 +1367,148 @@ def main_decomp_network(args, dev, local, rank, world):
         "host": host_info(),
     }
     print(json.dumps(line), flush=True)
+
+
+T2_RANKS = (128, 128)  # the north star's Tucker ranks at the C3 shape (BASELINE.json configs[1])
+
+
+def main_decomp_t2(args):
+    """--decompose --tucker2: one step = one Tucker-2 iteration (a HOOI sweep on W - S, then
+    S = P_c(W - L); include/lrs_conv.h "Tucker-2 decomposition") at the c3 weight shape and the
+    north star's ranks 128 / 128, timed like main_decomp.  --impl reference: the fp64 oracle."""
+    import torch
+    cfg = workloads.DECOMP_CONFIGS[DECOMP_OF.get(args.config, "c3_decomp")]
+    r1, r2 = T2_RANKS
+    w, ui0, uo0 = workloads.generate_decomp_tucker2(cfg, r1, r2)
+    K, W = args.steps, args.warmup
+    never = -float("inf")
+    metric = "GPU low-rank + sparse Tucker-2 decomposition iterations/s (SURVEY 8f f4)"
+    workload = f"{cfg.name}_tucker2: W {cfg.dims}, Tucker ranks {r1}/{r2}, cardinality {cfg.cardinality}"
+
+    def oracle_rate(steps):
+        from oracle import lrs_decomp as D
+        t0 = time.perf_counter()
+        D.decompose_lrs_tucker2(w, ui0, uo0, cfg.cardinality, max_iters=steps, tol=never)
+        el = time.perf_counter() - t0
+        return steps / el, el
+
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        oracle_rate(max(1, W))
+        v, el = oracle_rate(K)
+        print(json.dumps({"impl": "reference", "metric": metric, "value": v, "unit": "iterations/s", "n_gpus": 1,
+                          "steps": K, "warmup": W, "ms_per_step": el / K * 1e3, "higher_is_better": True,
+                          "dtype": "f64", "config": {"workload": workload, "config_id": cfg.name + "_tucker2"},
+                          "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": cpu_threads(), "kind": "oracle",
+                                           "sample": f"{K} iterations of {cfg.name}_tucker2"},
+                          "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    from paper_2006_06443_b200 import LrsTucker2Decomp
+    wd = torch.from_numpy(w).to(dev)
+    fresh = lambda: (torch.from_numpy(ui0).to(dev), torch.from_numpy(uo0).to(dev))
+
+    def handle(iters):
+        return LrsTucker2Decomp(cfg.dims, r1, r2, cfg.cardinality, max_iters=iters, tol=never, device=local)
+    handle(max(1, W)).run(wd, *fresh())
+    torch.cuda.synchronize(dev)
+    dc = handle(K)
+    ui, uo = fresh()
+    stream = torch.cuda.current_stream(dev)
+    sampler = ClockSampler(torch.cuda.current_device())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    with sampler:
+        e0.record(stream)
+        core, idx, val, eps = dc.run(wd, ui, uo)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    value = K / (ms / 1e3)
+    verify = {}
+    n_chk = min(3, K)
+    ci, cv_, ce = None, None, None
+    _, ci, _, ce = handle(n_chk).run(wd, *fresh())
+    verify["first_iterations_bitwise_timed_run"] = bool(ce == eps[:n_chk])
+    if not args.no_cpu:
+        from oracle import lrs_decomp as D
+        _, (ridx, _), reps = D.decompose_lrs_tucker2(w, ui0, uo0, cfg.cardinality, max_iters=n_chk, tol=never)
+        verify["oracle_eps"] = reps
+        verify["gpu_eps"] = ce
+        verify["eps_max_rel_diff"] = float(max(abs(a - b) / b for a, b in zip(ce, reps)))
+        verify["s_support_equal"] = bool(np.array_equal(ci.cpu().numpy(), ridx))
+        verify["oracle_ok"] = verify["eps_max_rel_diff"] < 1e-7 and verify["s_support_equal"]
+    n_t = min(K, 10)
+    st_run = handle(n_t)
+    st_run.set_timing(True)
+    st_run.run(wd, *fresh())
+    torch.cuda.synchronize(dev)
+    avg_iter = {k_: v[0] / n_t for k_, v in st_run.stage_times().items()}
+    e2e = None
+    if not args.no_e2e:
+        wh = torch.from_numpy(w).pin_memory()
+        uih, uoh = torch.from_numpy(ui0).pin_memory(), torch.from_numpy(uo0).pin_memory()
+        e2 = handle(K)
+        wd2, ui2, uo2 = torch.empty_like(wd), torch.empty(ui0.shape, dtype=torch.float64, device=dev), \
+            torch.empty(uo0.shape, dtype=torch.float64, device=dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        a.record(stream)
+        wd2.copy_(wh, non_blocking=True)
+        ui2.copy_(uih, non_blocking=True)
+        uo2.copy_(uoh, non_blocking=True)
+        c2, i2, v2, _ = e2.run(wd2, ui2, uo2)
+        outs = [t.cpu() for t in (ui2, uo2, c2, i2, v2)]
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e = {"value": K / (a.elapsed_time(b) / 1e3), "unit": "iterations/s",
+               "h2d_bytes_per_step": (w.size + ui0.size + uo0.size) * 8 / K,
+               "d2h_bytes_per_step": sum(t.numel() for t in outs) * 8 / K,
+               "api": "LrsTucker2Decomp.run (lrs_tucker2_run) with pinned-host copies in, factors + core + S out",
+               "note": "one job = copy in, K iterations, copy out; bytes amortised per iteration"}
+    cin, cout = cfg.dims[0], cfg.dims[1]
+    q = cfg.dims[2] * cfg.dims[3]
+    # ALGORITHMIC fp64 FLOPs per sweep of the mode products (Z1, Z2: 2 Cin Cout q R each; G: 2 R1 R2 Cout q;
+    # the two subspace steps: 4 rows (R q) R each) -- the stage timed as "mode_products" + "subspace_orth"
+    flops_prod = 2 * cin * cout * q * r2 + 2 * cin * cout * q * r1 + 2 * r1 * r2 * cout * q
+    flops_sub = 4 * cin * r2 * q * r1 + 4 * cout * r1 * q * r2
+    flops_res = 2 * r1 * r2 * cout * q + 2 * cin * cout * q * r1
+    peak, kind = fp64_peak()
+    t_prod = avg_iter["mode_products"] / 1e3
+    roof = {"bound": "alu", "kernel": "lrs_dgemm_kernel (Z1, Z2, G mode products)",
+            "achieved": flops_prod / t_prod / 1e12, "peak": peak, "unit": "TFLOP/s (fp64)",
+            "frac": flops_prod / t_prod / 1e12 / peak, "traffic": None, "peak_kind": kind,
+            "what": "ALGORITHMIC fp64 FLOPs of the three mode products per sweep / their time per iteration",
+            "stage_ms_per_iteration": {k_: round(v, 4) for k_, v in avg_iter.items()},
+            "subspace_tflops_incl_jacobi": flops_sub / (avg_iter["subspace_orth"] / 1e3) / 1e12,
+            "residual_tflops": flops_res / (avg_iter["residual"] / 1e3) / 1e12}
+    cpu = None
+    if not args.no_cpu:
+        v1, el1 = oracle_rate(1)
+        calls = max(1, int(args.cpu_seconds / max(el1, 1e-3)))
+        v, el = oracle_rate(calls)
+        cpu = {"value": v, "unit": "iterations/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": f"{calls} oracle iterations (decompose_lrs_tucker2) of {cfg.name} ({el:.1f} s, fp64 numpy)",
+               **host_info()}
+    if rank != 0:
+        return
+    print(json.dumps({
+        "metric": metric, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (planted CP rank 96 + N(0, 0.05^2) noise + 1% spikes of magnitude 10; N(0,1) initial bases)",
+        "config": {"workload": workload, "config_id": cfg.name + "_tucker2",
+                   "parallelism": "replicas (one decomposition per GPU)",
+                   "timing": "CUDA events around one run of K iterations (host stopping rule: one sync per iteration)",
+                   "l2": "W is 2.36M fp64 (18.9 MB): L2-resident by design"},
+        "clocks": sampler.summary(), "e2e": e2e, "roofline": roof, "verify": verify,
+        # per sweep: 3 mode products + 2 x (2 GEMMs, Gram, Loewdin, update) + 2 residual GEMMs + the
+        # projection (flags, 2 scans, finish, eps; with S: 8 x (histogram, pick) + 2 scans + compaction)
+        "gpu_launches": (3 + 10 + 2 + 5 + (19 if dc.nnz > 0 else 0)) * K,
+        "eps_last": eps[-1] if eps else None, "cpu_baseline": cpu, "host": host_info()}), flush=True)
 
 
 def run_reference_decomp(args):

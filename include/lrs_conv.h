@@ -460,11 +460,12 @@ lrs_status lrs_decomp_destroy(lrs_decomp *h); /* NULL-safe */
  * this Tucker-2 form, SURVEY.md §1 note 2).  update = one higher-order orthogonal
  * iteration (HOOI) sweep on T = W - S: U_in <- `inner` subspace-iteration steps
  * orth(Z1 Z1^T U_in) on Z1 = T x_out U_out^T unfolded [Cin][R2 kh kw], then U_out likewise on
- * Z2 = T x_in U_in^T, then G = T x_in U_in^T x_out U_out^T; orth(Y) = Y (Y^T Y)^-1/2 (Loewdin,
+ * Z2 = T x_in U_in^T, then G = T x_in U_in^T x_out U_out^T; orth(Y) = Cholesky-QR Y L^-T
+ * (Y^T Y = L L^T) while every pivot exceeds rcond * max_i (Y^T Y)_ii, else Y (Y^T Y)^-1/2 (Loewdin,
  * eigenvalues under rcond * the largest dropped).  P_c, eps and the stopping rule as
  * lrs_decomp_run.  oracle/lrs_decomp.py decompose_lrs_tucker2 writes the algorithm out; every step
- * runs in fp64 CUDA kernels (a strided batched fp64 GEMM for the mode products, the one-CTA Jacobi
- * for (Y^T Y)^-1/2, the radix-select projection), deterministic.
+ * runs in fp64 CUDA kernels (a strided batched fp64 GEMM for the mode products, the one-CTA
+ * blocked Cholesky (Jacobi for the fallback), the radix-select projection), deterministic.
  * Requirements: as lrs_decomp_params with rank = max(r1, r2); 1 <= r1 <= dims[0], 1 <= r2 <= dims[1],
  * inner >= 1.
  */
@@ -474,7 +475,7 @@ typedef struct lrs_tucker2_params {
   double cardinality;  /* c: S keeps round(c * numel) entries (half to even)     */
   int32_t max_iters;   /* >= 1                                                   */
   double tol;          /* stop when eps_{i-1} - eps_i < tol (i >= 1)             */
-  double rcond;        /* Loewdin cutoff relative to the largest eigenvalue      */
+  double rcond;        /* orth: Cholesky pivot floor / Loewdin eigenvalue cutoff (relative) */
   int32_t inner;       /* subspace-iteration steps per factor per sweep (>= 1)   */
 } lrs_tucker2_params;
 
@@ -491,7 +492,7 @@ lrs_status lrs_tucker2_run(lrs_tucker2 *h, const double *w, double *u_in, double
                            int64_t *s_idx, double *s_val, int64_t *s_count, double *eps_hist,
                            int32_t *iters_done, void *stream);
 int64_t lrs_tucker2_nnz(const lrs_tucker2 *h); /* round(c * numel) */
-/* stage timing: 0 mode products (Z1, Z2, G), 1 subspace steps + Loewdin, 2 residual W - L,
+/* stage timing: 0 mode products (Z1, Z2, G), 1 subspace steps + orth, 2 residual W - L,
    3 projection P_c + T = W - S + eps */
 lrs_status lrs_tucker2_set_timing(lrs_tucker2 *h, int32_t enable);
 lrs_status lrs_tucker2_stage_times(lrs_tucker2 *h, float *ms, int64_t *counts, int32_t max_stages,

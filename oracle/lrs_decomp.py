@@ -34,7 +34,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 __all__ = ["cp_reconstruct", "mttkrp", "gram_hadamard", "sym_pinv", "cp_als_step", "project_sparse",
-           "sparse_dense", "decompose_lrs", "rel_residual", "orth_lowdin", "tucker2_reconstruct",
+           "sparse_dense", "decompose_lrs", "rel_residual", "orth_lowdin", "orth_cholqr", "tucker2_reconstruct",
            "tucker2_hooi_step", "decompose_lrs_tucker2"]
 
 
@@ -166,8 +166,12 @@ def svd_init(w: np.ndarray, rank: int, seed: int = 0) -> List[np.ndarray]:
 # U_out [Cout][R2] (the layer's u_out = U_out^T), the kernel modes uncompressed.  `update`
 # = one higher-order orthogonal iteration (HOOI) sweep on T = W - S: each channel
 # factor becomes the dominant R-dimensional left singular subspace of T contracted with the
-# other factor, computed by `inner` steps of subspace iteration U <- orth(Z Z^T U) with the
-# symmetric (Loewdin) orthonormalisation orth(Y) = Y (Y^T Y)^(-1/2); then G = T x U_in^T x U_out^T.
+# other factor, computed by `inner` steps of subspace iteration U <- orth(Z Z^T U), then
+# G = T x U_in^T x U_out^T.  orth = Cholesky-QR (Y = Q R, R upper triangular with a positive
+# diagonal: the Gram-Schmidt basis) while the Gram Y^T Y has every Cholesky pivot above
+# rcond * its largest diagonal entry, else the symmetric (Loewdin) Y (Y^T Y)^(-1/2) with the rcond
+# eigenvalue cutoff (a rank-deficient Y; reading #22).  L = U_in G U_out^T depends on the
+# subspaces only, so the choice of basis changes U and G, not eps or S.
 
 def orth_lowdin(y: np.ndarray, rcond: float = 1e-10) -> np.ndarray:
     """Y (Y^T Y)^(-1/2) through the eigendecomposition of the Gram matrix (eigenvalues under
@@ -179,6 +183,24 @@ def orth_lowdin(y: np.ndarray, rcond: float = 1e-10) -> np.ndarray:
     inv = np.zeros_like(lam)
     inv[keep] = 1.0 / np.sqrt(np.abs(lam[keep]))
     return y @ ((q * inv) @ q.T)
+
+
+def orth_cholqr(y: np.ndarray, rcond: float = 1e-10) -> np.ndarray:
+    """Q = Y L^-T with C = Y^T Y = L L^T (the textbook Cholesky loop, written out); a pivot at or
+    under rcond * max_i C_ii -> orth_lowdin(Y) instead."""
+    y = np.asarray(y, np.float64)
+    c = y.T @ y
+    r = c.shape[0]
+    thr = rcond * (float(np.max(np.diag(c))) if r else 0.0)
+    l = np.zeros_like(c)
+    for k in range(r):
+        d = c[k, k] - float(np.dot(l[k, :k], l[k, :k]))
+        if not d > thr:
+            return orth_lowdin(y, rcond)
+        l[k, k] = np.sqrt(d)
+        for i in range(k + 1, r):
+            l[i, k] = (c[i, k] - float(np.dot(l[i, :k], l[k, :k]))) / l[k, k]
+    return np.linalg.solve(l, y.T).T  # Y L^-T
 
 
 def tucker2_reconstruct(u_in, g, u_out) -> np.ndarray:
@@ -195,10 +217,10 @@ def tucker2_hooi_step(u_in, u_out, target, inner: int = 1, rcond: float = 1e-10)
     u_out = np.array(u_out, np.float64)
     z1 = np.einsum("cjyx,jb->cbyx", t, u_out, optimize=True).reshape(cin, -1)  # T x_out U_out^T
     for _ in range(inner):
-        u_in = orth_lowdin(z1 @ (z1.T @ u_in), rcond)
+        u_in = orth_cholqr(z1 @ (z1.T @ u_in), rcond)
     z2 = np.einsum("cjyx,ca->jayx", t, u_in, optimize=True).reshape(cout, -1)  # T x_in U_in^T
     for _ in range(inner):
-        u_out = orth_lowdin(z2 @ (z2.T @ u_out), rcond)
+        u_out = orth_cholqr(z2 @ (z2.T @ u_out), rcond)
     g = np.einsum("cjyx,ca,jb->abyx", t, u_in, u_out, optimize=True)
     return u_in, u_out, g
 

@@ -249,6 +249,8 @@ struct PinvParams {
   int force_eigen;  // 1: skip the certified Cholesky path (LRS_DECOMP_EIGEN; tests of the eigen path)
   const double* single;  // non-NULL: V = this matrix itself (g / mode unused) -- the Tucker-2 Gram Y^T Y
   int inv_sqrt;          // 1: P = Q diag(lambda^-1/2) Q^T (the Loewdin orthonormaliser; eigen path only)
+  int chol_qr;           // 1 (with inv_sqrt): P = L^-T of V = L L^T (Cholesky-QR: Y P orthonormal) when every
+                         // pivot exceeds rcond * max_i V_ii, else the Loewdin eigen path
 };
 
 constexpr int kJThreads = 512;
@@ -271,13 +273,13 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
   // P = X^T X -- all in shared memory when A is.  Certificate: lambda_min >= 1 / ||P||_F and
   // lambda_max <= ||V||_F, so 1 / ||P||_F > rcond ||V||_F proves the cutoff drops nothing;
   // otherwise (or at a non-positive pivot) the Jacobi eigensolver below decides.
-  if (!q.force_eigen && !q.inv_sqrt) {
+  if (!q.force_eigen && (!q.inv_sqrt || q.chol_qr)) {
     __shared__ int fail;
-    __shared__ double vn2;
+    __shared__ double vn2, piv_min;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* L = A;
     if (threadIdx.x == 0) fail = 0;
-    double lv = 0.0;
+    double lv = 0.0, ld = 0.0;
     for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
       const int i = e / r, j = e % r;
       double val = 1.0;
@@ -288,15 +290,27 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
           if (o != q.mode) val *= q.g[o][i * r + j];
       L[e] = val;
       lv += val * val;
+      if (i == j) ld = fmax(ld, val);
     }
-    for (int o = 16; o; o >>= 1) lv += __shfl_xor_sync(0xffffffffu, lv, o);
-    if (lane == 0) wsum[warp][0] = lv;
+    for (int o = 16; o; o >>= 1) {
+      lv += __shfl_xor_sync(0xffffffffu, lv, o);
+      ld = fmax(ld, __shfl_xor_sync(0xffffffffu, ld, o));
+    }
+    if (lane == 0) {
+      wsum[warp][0] = lv;
+      wsum[warp][1] = ld;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += wsum[w][0];
+      double t = 0.0, dm = 0.0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+        t += wsum[w][0];
+        dm = fmax(dm, wsum[w][1]);
+      }
       vn2 = t;
+      piv_min = q.chol_qr ? q.rcond * dm : 0.0;  // Cholesky-QR: a relative pivot floor (oracle orth_cholqr)
     }
+    __syncthreads();
     constexpr int NB = 32;
     for (int kb = 0; kb < r; kb += NB) {
       const int nb = min(NB, r - kb);
@@ -305,7 +319,7 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
         for (int k = 0; k < nb; ++k) {
           const int kk = kb + k;
           double d = L[kk * r + kk];
-          const bool bad = !(d > 0.0);
+          const bool bad = !(d > piv_min);
           d = sqrt(fmax(d, 0.0));
           __syncwarp();
           if (lane == 0) {
@@ -352,6 +366,17 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
         }
       }
       __syncthreads();
+      if (q.chol_qr) {
+        // P = X^T = L^-T (upper triangular): P[k][c] = X[c][k] for c >= k
+        for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+          const int k = e / r, c = e % r;
+          q.p[e] = c < k ? 0.0 : (c == k ? 1.0 / L[k * r + k] : L[k * r + c]);
+        }
+        if (q.qt)
+          for (int e = threadIdx.x; e < n * n; e += blockDim.x) q.qt[e] = (e / n == e % n) ? 1.0 : 0.0;
+        if (q.sweeps && threadIdx.x == 0) *q.sweeps = -2;  // diagnostic: Cholesky-QR
+        return;
+      }
       // P = X^T X: P[a][b] = sum_{k >= max(a, b)} X[k][a] X[k][b]
       double lp = 0.0;
       for (int e = threadIdx.x; e < r * r; e += blockDim.x) {

@@ -446,7 +446,8 @@ void t2_gemm(const double* a, const double* b, double* c, const double* sub, int
 }
 
 // U <- orth(Z Z^T U) `inner` times: Z [rows][cols] row-major, U [rows][r] (in place);
-// orth(Y) = Y (Y^T Y)^-1/2 by the eigen path of the one-CTA pseudo-inverse kernel
+// orth(Y) = Y L^-T (Cholesky-QR) or, for a rank-deficient Y, Y (Y^T Y)^-1/2 (the eigen path)
+// -- both in the one-CTA pseudo-inverse kernel
 lrs_status t2_subspace(lrs_tucker2* h, const double* z, int rows, int cols, double* u, int r, double* qt, bool warm,
                        cudaStream_t s) {
   lrs_decomp* d = h->d;
@@ -458,6 +459,7 @@ lrs_status t2_subspace(lrs_tucker2* h, const double* z, int rows, int cols, doub
     PinvParams pp{};
     pp.single = h->c;
     pp.inv_sqrt = 1;
+    pp.chol_qr = 1;
     pp.r = r;
     pp.rp = (r + 1) & ~1;
     pp.rcond = h->prm.rcond;

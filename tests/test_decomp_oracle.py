@@ -149,6 +149,21 @@ def test_lowdin_is_the_closest_orthonormal_basis():
     assert np.allclose(q.T @ q, np.eye(4), atol=1e-12)
 
 
+def test_cholqr_is_numpy_qr_with_a_positive_r_diagonal():
+    """orth_cholqr(Y) = the Q of numpy's thin QR with column signs making diag(R) > 0 (library
+    pin); a rank-deficient Y (a repeated column) takes the Loewdin fallback: an orthonormal basis
+    of span(Y) of dimension rank(Y), the dropped direction a zero column."""
+    y = np.random.default_rng(23).standard_normal((11, 5))
+    q, r = np.linalg.qr(y)
+    sg = np.sign(np.diag(r))
+    assert np.allclose(D.orth_cholqr(y), q * sg, atol=1e-12)
+    yd = np.concatenate([y[:, :3], y[:, :1]], axis=1)
+    qd = D.orth_cholqr(yd)
+    assert np.allclose(qd, D.orth_lowdin(yd))
+    assert np.linalg.matrix_rank(qd, tol=1e-8) == 3
+    assert np.allclose(qd @ qd.T @ yd, yd, atol=1e-10)  # spans span(Y)
+
+
 def test_hooi_recovers_a_planted_tucker2_tensor():
     """An exact Tucker-2 tensor of ranks (3, 2) is reproduced to round-off (cardinality 0),
     and the factors span the same subspaces as numpy's SVD of the unfoldings (library pin)."""
