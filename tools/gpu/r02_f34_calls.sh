@@ -307,3 +307,16 @@ bwdcp() {
   timeout 1500 python -m pytest tests/test_gpu_backward.py -q > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
   cat $O/rc.txt
 }
+final() {
+  # last validation of the round: the whole GPU suite, smoke, the default bench line, the
+  # Tucker-2 decomposition line and a full capture of its mode-product GEMM
+  mkdir -p gpurun_out/fin; O=gpurun_out/fin; rm -f $O/rc.txt
+  timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/rc.txt
+  timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench default rc=$?" >> $O/rc.txt
+  timeout 600 python bench.py --decompose --tucker2 --steps 30 --warmup 3 > $O/bench_dec_t2.json 2> $O/bench_dec_t2.err; echo "bench dec t2 rc=$?" >> $O/rc.txt
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:dgemm -s 3 -c 1 -o $O/prof_dgemm_t2 -f python bench.py --decompose --tucker2 --steps 2 --warmup 1 --no-cpu --no-e2e > $O/ncu_dgemm.log 2>&1; echo "ncu dgemm rc=$?" >> $O/rc.txt
+  python tools/ncu_sum.py $O/prof_dgemm_t2.ncu-rep > $O/sum_dgemm_t2.txt 2>&1
+  rm -f $O/*.ncu-rep
+  cat $O/rc.txt
+}
