@@ -255,8 +255,10 @@ struct PinvParams {
 
 constexpr int kJThreads = 512;
 
-__global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_constant__ PinvParams q) {
-  extern __shared__ double jsm[];
+// the body, instantiated once with A in shared memory (so every access to it compiles to LDS /
+// STS, not generic loads) and once with A in the global workspace
+template <bool A_SMEM>
+__device__ __forceinline__ void sym_pinv_body(const PinvParams& q, double* A) {
   __shared__ double cs[128][2];
   __shared__ int pairs[128][2];
   __shared__ double wsum[kJThreads / 32][2];
@@ -265,7 +267,6 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
   // A: the full matrix (shared memory when it fits, else the global workspace); the
   // eigenvectors are kept TRANSPOSED (Vt[k][i] = V[i][k]) so a rotation of columns p, q of V
   // touches two contiguous rows of Vt (coalesced / conflict-free)
-  double* A = q.a_smem ? jsm : q.a;
   double* Vt = q.v;
   // ---- certified Cholesky path: when every eigenvalue of V exceeds rcond * lambda_max, the
   // pseudo-inverse IS the inverse.  V = L L^T (blocked, in place: lower triangle), X = L^-1
@@ -578,6 +579,14 @@ __global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_co
   }
   if (q.qt)
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) q.qt[e] = Vt[e];
+}
+
+__global__ void __launch_bounds__(kJThreads) lrs_sym_pinv_kernel(const __grid_constant__ PinvParams q) {
+  extern __shared__ double jsm[];
+  if (q.a_smem)
+    sym_pinv_body<true>(q, jsm);
+  else
+    sym_pinv_body<false>(q, q.a);
 }
 
 // ---------------------------------------------------------------- strided batched fp64 GEMM
