@@ -1,0 +1,15 @@
+#!/bin/bash
+# round 2, last session: validate HEAD (after the pseudo-inverse LDS/STS change) on a B200
+val() {
+  mkdir -p gpurun_out/s3; O=gpurun_out/s3; rm -f $O/rc.txt
+  timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/rc.txt
+  timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench default rc=$?" >> $O/rc.txt
+  timeout 600 python bench.py --decompose --steps 30 --warmup 3 > $O/bench_dec_c3.json 2> $O/bench_dec_c3.err; echo "bench dec c3 rc=$?" >> $O/rc.txt
+  timeout 600 python bench.py --decompose --tucker2 --steps 30 --warmup 3 > $O/bench_dec_t2.json 2> $O/bench_dec_t2.err; echo "bench dec t2 rc=$?" >> $O/rc.txt
+  for c in c4 c2_f32; do
+    timeout 600 python bench.py --config $c --steps 200 --warmup 10 > $O/bench_$c.json 2> $O/bench_$c.err; echo "bench $c rc=$?" >> $O/rc.txt
+  done
+  cat $O/rc.txt
+}
+"$@"
