@@ -12,4 +12,12 @@ val() {
   done
   cat $O/rc.txt
 }
+
+db() {
+  # the double-buffered fp32 sparse/expansion kernel: whole GPU suite, then the C2-fp32 line
+  mkdir -p gpurun_out/db; O=gpurun_out/db; rm -f $O/rc.txt
+  LRS_VERBOSE=1 timeout 300 python bench.py --config c2_f32 --steps 200 --warmup 10 > $O/bench_c2_f32.json 2> $O/bench_c2_f32.err; echo "bench c2_f32 rc=$?" >> $O/rc.txt
+  timeout 2400 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  cat $O/rc.txt
+}
 "$@"
