@@ -20,4 +20,11 @@ db() {
   timeout 2400 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
   cat $O/rc.txt
 }
+unr() {
+  # staging loops unrolled by 2 (two items' loads in flight per thread): C2-fp32 line + fp32 tests
+  mkdir -p gpurun_out/unr; O=gpurun_out/unr; rm -f $O/rc.txt
+  for i in 1 2; do timeout 300 python bench.py --config c2_f32 --steps 200 --warmup 10 --no-cpu > $O/bench_c2_f32_$i.json 2> $O/bench_c2_f32_$i.err; echo "bench c2_f32 rc=$?" >> $O/rc.txt; done
+  timeout 900 python -m pytest tests/test_gpu_spadd_f32.py tests/test_gpu_parity.py tests/test_gpu_epilogue.py -m gpu -q -x > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+  cat $O/rc.txt
+}
 "$@"
